@@ -1,0 +1,1 @@
+"""Test oracles (TEST INFRASTRUCTURE ONLY) -- see oracle/oracle.py."""
