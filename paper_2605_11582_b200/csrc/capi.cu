@@ -1,0 +1,507 @@
+// C-ABI entry points (include/egt_b200.h): upload + validation, row slicing,
+// launch planning, per-stream split-K workspaces, error mapping.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "egt_b200.h"
+#include "handle.h"
+
+using namespace egt_impl;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local bool g_pdl = true;
+
+egt_status fail(egt_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+
+#define CUDA_TRY(expr)                                                                    \
+  do {                                                                                    \
+    cudaError_t e_ = (expr);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(EGT_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));        \
+  } while (0)
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+// Bump allocator over one cudaMalloc.
+struct Carve {
+  std::vector<std::pair<size_t*, size_t>> req;
+  size_t total = 0;
+  size_t add(size_t bytes) {
+    size_t off = total;
+    total = align_up(total + std::max<size_t>(bytes, 16), 256);
+    return off;
+  }
+};
+
+int num_sms() {
+  static int n = [] {
+    int dev = 0, v = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess)
+      cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v;
+  }();
+  return n;
+}
+
+// Per (device, stream) split-K workspace; grows, never shrinks.
+struct Workspace {
+  float* partial = nullptr;
+  size_t partial_floats = 0;
+  uint32_t* counters = nullptr;
+  size_t n_counters = 0;
+};
+std::mutex g_ws_mu;
+std::map<std::pair<int, cudaStream_t>, Workspace> g_ws;
+
+egt_status get_workspace(cudaStream_t s, size_t floats, size_t counters, Workspace** out) {
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  Workspace& w = g_ws[{dev, s}];
+  if (w.partial_floats < floats) {
+    if (w.partial) CUDA_TRY(cudaFree(w.partial));
+    w.partial = nullptr;
+    size_t n = std::max(floats, static_cast<size_t>(1) << 20);
+    CUDA_TRY(cudaMalloc(&w.partial, n * sizeof(float)));
+    w.partial_floats = n;
+  }
+  if (w.n_counters < counters) {
+    if (w.counters) CUDA_TRY(cudaFree(w.counters));
+    w.counters = nullptr;
+    size_t n = std::max(counters, static_cast<size_t>(4096));
+    CUDA_TRY(cudaMalloc(&w.counters, n * sizeof(uint32_t)));
+    CUDA_TRY(cudaMemset(w.counters, 0, n * sizeof(uint32_t)));
+    w.n_counters = n;
+  }
+  *out = &w;
+  return EGT_OK;
+}
+
+// check_packed (packed.cpp:145-166) on the host view, same messages.
+egt_status check_view(const egt_packed_view* v) {
+  if (!v) return fail(EGT_EINVAL, "packed matrix: null view");
+  if (v->m != 4) return fail(EGT_EFORMAT, "packed matrix: group width must be 4");
+  if (v->n < 1 || v->n >= v->m) return fail(EGT_EFORMAT, "packed matrix: bad keep count");
+  if (v->cols % v->m != 0)
+    return fail(EGT_EFORMAT, "packed matrix: columns not a multiple of the group width");
+  const uint64_t nnz = static_cast<uint64_t>(v->rows) * v->cols * v->n / v->m;
+  if (v->n_index_words != (nnz + 7) / 8)
+    return fail(EGT_EFORMAT, "packed matrix: index word count mismatch");
+  if (v->kind == EGT_KIND_INT4) {
+    if (v->n_value_bytes != (nnz + 1) / 2)
+      return fail(EGT_EFORMAT, "packed matrix: value byte count mismatch");
+    if (v->n_group_sizes != v->rows || v->n_group_offsets != static_cast<size_t>(v->rows) + 1)
+      return fail(EGT_EFORMAT, "packed matrix: group table size mismatch");
+    if (v->n_scales != v->group_offsets[v->rows] || v->n_zero_points != v->n_scales)
+      return fail(EGT_EFORMAT, "packed matrix: scale table size mismatch");
+  } else if (v->kind == EGT_KIND_F32) {
+    if (v->n_values != nnz) return fail(EGT_EFORMAT, "packed matrix: value count mismatch");
+  } else {
+    return fail(EGT_EFORMAT, "packed matrix: unknown value kind");
+  }
+  if (nnz > 0 && !v->index_words) return fail(EGT_EINVAL, "packed matrix: null index stream");
+  return EGT_OK;
+}
+
+// Whether every row's quant groups start on 32-column (k-tile) boundaries.
+bool groups_k_aligned(uint32_t rows, uint32_t cols, const uint32_t* gs, int* ss_out) {
+  int ss = 4;
+  for (uint32_t r = 0; r < rows; ++r) {
+    const uint32_t g = gs[r];
+    if (g >= cols) continue;  // one group per row
+    if (g % 32 != 0) return false;
+    const uint32_t kt = g / 32;
+    while (kt % ss != 0) ss >>= 1;
+  }
+  *ss_out = ss;
+  return true;
+}
+
+egt_status finish_error_flag(uint32_t* d_err, cudaStream_t s) {
+  uint32_t h_err = 0;
+  CUDA_TRY(cudaMemcpyAsync(&h_err, d_err, sizeof h_err, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  if (h_err & 1u) return fail(EGT_EFORMAT, "packed matrix: in-group offsets not increasing");
+  if (h_err & 2u) return fail(EGT_EFORMAT, "packed matrix: zero group size");
+  if (h_err & 4u) return fail(EGT_EFORMAT, "packed matrix: group table does not cover the row");
+  return EGT_OK;
+}
+
+struct Upload {
+  // device pointers into one temporary allocation
+  void* base = nullptr;
+  uint16_t* words = nullptr;
+  uint8_t* codes = nullptr;
+  uint8_t* dense = nullptr;
+  float* f32 = nullptr;
+  __half* f16 = nullptr;
+  uint32_t* gs = nullptr;
+  uint32_t* goff = nullptr;
+  float* scales = nullptr;
+  uint8_t* zps = nullptr;
+  uint32_t* err = nullptr;
+  ~Upload() {
+    if (base) cudaFree(base);
+  }
+};
+
+// Shared tail of create(): decide the path, re-tile if possible, fill info.
+egt_status build_handle(int format, uint8_t n, uint8_t kind, uint32_t rows, uint32_t cols,
+                        uint64_t nnz, const uint32_t* host_gs, uint64_t n_scales, Upload& up,
+                        size_t up_bytes, cudaStream_t s, egt_dev_packed** out) {
+  using namespace egt_fmt;
+  auto h = std::make_unique<egt_dev_packed>();
+  h->rows = rows;
+  h->cols = cols;
+  h->n = n;
+  h->m = 4;
+  h->kind = kind;
+  h->format = static_cast<uint8_t>(format);
+  h->nnz = nnz;
+  // weight-side bytes a product must read (footprint, packed.cpp:222-240;
+  // FP16 values on the device)
+  const uint64_t idx_b = format == I4_DENSE ? 0 : 2 * ((nnz + 7) / 8);
+  const uint64_t val_b = kind == EGT_KIND_INT4 ? (nnz + 1) / 2 : 2 * nnz;
+  h->algorithmic_bytes = idx_b + val_b + (kind == EGT_KIND_INT4 ? 5 * n_scales : 0);
+
+  int ss = 4;
+  const bool tiled = rows > 0 && cols > 0 && cols % 32 == 0 &&
+                     (kind == EGT_KIND_F32 || groups_k_aligned(rows, cols, host_gs, &ss));
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  auto store = std::make_shared<DevStorage>();
+  store->device = dev;
+  if (tiled) {
+    TiledStream ts;
+    ts.KQ = static_cast<int>((cols + 127) / 128);
+    ts.RT = static_cast<int>((rows + 15) / 16);
+    ts.SS = kind == EGT_KIND_INT4 ? ss : 4;
+    ts.E = 4 / ts.SS;
+    const size_t blocks = static_cast<size_t>(ts.RT) * ts.KQ;
+    Carve c;
+    const size_t o_vals = c.add(blocks * 32 * val_lane_bytes(format));
+    const size_t o_meta = c.add(blocks * 32 * meta_lane_bytes(format));
+    const size_t o_sc = has_scales(format) ? c.add(blocks * ts.E * 16 * sizeof(float)) : 0;
+    const size_t o_zp = has_scales(format) ? c.add(blocks * ts.E * 16) : 0;
+    CUDA_TRY(cudaMalloc(&store->base, c.total));
+    store->bytes = c.total;
+    uint8_t* b = static_cast<uint8_t*>(store->base);
+    CUDA_TRY(cudaMemsetAsync(b, 0, c.total, s));
+    ts.vals = b + o_vals;
+    ts.meta = b + o_meta;
+    ts.scales = has_scales(format) ? reinterpret_cast<float*>(b + o_sc) : nullptr;
+    ts.zps = has_scales(format) ? b + o_zp : nullptr;
+    RawStream raw;
+    raw.words = up.words;
+    raw.codes = up.codes;
+    raw.dense_codes = up.dense;
+    raw.values = up.f16;
+    raw.group_sizes = up.gs;
+    raw.group_offsets = up.goff;
+    raw.scales = up.scales;
+    raw.zps = up.zps;
+    raw.n_scales = n_scales;
+    CUDA_TRY(launch_relayout(raw, format, rows, cols, ts, const_cast<uint8_t*>(ts.vals),
+                             const_cast<uint8_t*>(ts.meta), const_cast<float*>(ts.scales),
+                             const_cast<uint8_t*>(ts.zps), s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    h->path = EGT_PATH_TILED;
+    h->tiled = ts;
+    h->device_bytes = c.total;
+  } else {
+    // keep the reference-order upload as the device copy
+    store->base = up.base;
+    store->bytes = up_bytes;
+    up.base = nullptr;  // ownership moves to the handle
+    h->path = EGT_PATH_GENERAL;
+    h->raw.words = up.words;
+    h->raw.codes = up.codes;
+    h->raw.dense_codes = up.dense;
+    h->raw.values = up.f16;
+    h->raw.group_sizes = up.gs;
+    h->raw.group_offsets = up.goff;
+    h->raw.scales = up.scales;
+    h->raw.zps = up.zps;
+    h->raw.n_scales = n_scales;
+    h->device_bytes = up_bytes;
+  }
+  h->store = std::move(store);
+  *out = h.release();
+  return EGT_OK;
+}
+
+}  // namespace
+
+namespace egt_impl {
+void set_last_error(const std::string& msg) { g_err = msg; }
+}  // namespace egt_impl
+
+egt_impl::DevStorage::~DevStorage() {
+  if (base) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != device) cudaSetDevice(device);
+    cudaFree(base);
+    if (cur != device) cudaSetDevice(cur);
+  }
+}
+
+extern "C" {
+
+int egt_abi_version(void) { return EGT_ABI_VERSION; }
+const char* egt_last_error(void) { return g_err.c_str(); }
+void egt_set_pdl(int enabled) { g_pdl = enabled != 0; }
+uint64_t egt_launch_count(void) { return launch_counter(); }
+
+egt_status egt_dev_packed_create(const egt_packed_view* v, void* stream, egt_dev_packed** out) {
+  using namespace egt_fmt;
+  if (!out) return fail(EGT_EINVAL, "egt_dev_packed_create: null output");
+  *out = nullptr;
+  egt_status st = check_view(v);
+  if (st != EGT_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const uint32_t rows = v->rows, cols = v->cols;
+  const uint64_t nnz = static_cast<uint64_t>(rows) * cols * v->n / 4;
+  const bool i4 = v->kind == EGT_KIND_INT4;
+  const int format = i4 ? (v->n == 2 ? I4_SP24 : I4_SP14) : (v->n == 2 ? F16_SP24 : F16_SP14);
+  if (v->n != 1 && v->n != 2) return fail(EGT_EFORMAT, "packed matrix: bad keep count");
+
+  Upload up;
+  Carve c;
+  const size_t o_words = c.add(v->n_index_words * 2);
+  const size_t o_codes = i4 ? c.add(v->n_value_bytes) : 0;
+  const size_t o_f32 = i4 ? 0 : c.add(nnz * 4);
+  const size_t o_f16 = i4 ? 0 : c.add(nnz * 2);
+  const size_t o_gs = i4 ? c.add(rows * 4ull) : 0;
+  const size_t o_goff = i4 ? c.add((rows + 1ull) * 4) : 0;
+  const size_t o_sc = i4 ? c.add(v->n_scales * 4) : 0;
+  const size_t o_zp = i4 ? c.add(v->n_scales) : 0;
+  const size_t o_err = c.add(16);
+  CUDA_TRY(cudaMalloc(&up.base, c.total));
+  uint8_t* b = static_cast<uint8_t*>(up.base);
+  up.words = reinterpret_cast<uint16_t*>(b + o_words);
+  up.err = reinterpret_cast<uint32_t*>(b + o_err);
+  CUDA_TRY(cudaMemsetAsync(up.err, 0, 16, s));
+  if (v->n_index_words)
+    CUDA_TRY(cudaMemcpyAsync(up.words, v->index_words, v->n_index_words * 2, cudaMemcpyHostToDevice, s));
+  if (i4) {
+    up.codes = b + o_codes;
+    up.gs = reinterpret_cast<uint32_t*>(b + o_gs);
+    up.goff = reinterpret_cast<uint32_t*>(b + o_goff);
+    up.scales = reinterpret_cast<float*>(b + o_sc);
+    up.zps = b + o_zp;
+    if (v->n_value_bytes)
+      CUDA_TRY(cudaMemcpyAsync(up.codes, v->value_bytes, v->n_value_bytes, cudaMemcpyHostToDevice, s));
+    if (rows) {
+      CUDA_TRY(cudaMemcpyAsync(up.gs, v->group_sizes, rows * 4ull, cudaMemcpyHostToDevice, s));
+      CUDA_TRY(cudaMemcpyAsync(up.goff, v->group_offsets, (rows + 1ull) * 4, cudaMemcpyHostToDevice, s));
+    }
+    if (v->n_scales) {
+      CUDA_TRY(cudaMemcpyAsync(up.scales, v->scales, v->n_scales * 4, cudaMemcpyHostToDevice, s));
+      CUDA_TRY(cudaMemcpyAsync(up.zps, v->zero_points, v->n_scales, cudaMemcpyHostToDevice, s));
+    }
+    CUDA_TRY(launch_validate_groups(up.gs, up.goff, rows, cols, v->n_scales, up.err, s));
+  } else {
+    up.f32 = reinterpret_cast<float*>(b + o_f32);
+    up.f16 = reinterpret_cast<__half*>(b + o_f16);
+    if (nnz) CUDA_TRY(cudaMemcpyAsync(up.f32, v->values, nnz * 4, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(launch_f32_to_f16(up.f32, up.f16, nnz, s));
+  }
+  CUDA_TRY(launch_validate_offsets(up.words, rows, cols, v->n, up.err, s));
+  st = finish_error_flag(up.err, s);
+  if (st != EGT_OK) return st;
+  return build_handle(format, v->n, v->kind, rows, cols, nnz, v->group_sizes, v->n_scales, up,
+                      c.total, s, out);
+}
+
+egt_status egt_dev_dense_i4_create(const egt_quant_view* q, void* stream, egt_dev_packed** out) {
+  using namespace egt_fmt;
+  if (!out || !q) return fail(EGT_EINVAL, "egt_dev_dense_i4_create: null argument");
+  *out = nullptr;
+  const uint32_t rows = q->rows, cols = q->cols;
+  if (q->n_codes != static_cast<size_t>(rows) * cols)
+    return fail(EGT_EINVAL, "dense int4: code count differs from rows x cols");
+  if (rows && (!q->group_offsets || q->group_offsets[rows] != q->n_scales))
+    return fail(EGT_EFORMAT, "packed matrix: scale table size mismatch");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Upload up;
+  Carve c;
+  const size_t o_dense = c.add(q->n_codes);
+  const size_t o_gs = c.add(rows * 4ull);
+  const size_t o_goff = c.add((rows + 1ull) * 4);
+  const size_t o_sc = c.add(q->n_scales * 4);
+  const size_t o_zp = c.add(q->n_scales);
+  const size_t o_err = c.add(16);
+  CUDA_TRY(cudaMalloc(&up.base, c.total));
+  uint8_t* b = static_cast<uint8_t*>(up.base);
+  up.dense = b + o_dense;
+  up.gs = reinterpret_cast<uint32_t*>(b + o_gs);
+  up.goff = reinterpret_cast<uint32_t*>(b + o_goff);
+  up.scales = reinterpret_cast<float*>(b + o_sc);
+  up.zps = b + o_zp;
+  up.err = reinterpret_cast<uint32_t*>(b + o_err);
+  CUDA_TRY(cudaMemsetAsync(up.err, 0, 16, s));
+  if (q->n_codes) CUDA_TRY(cudaMemcpyAsync(up.dense, q->codes, q->n_codes, cudaMemcpyHostToDevice, s));
+  if (rows) {
+    CUDA_TRY(cudaMemcpyAsync(up.gs, q->group_sizes, rows * 4ull, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(up.goff, q->group_offsets, (rows + 1ull) * 4, cudaMemcpyHostToDevice, s));
+  }
+  if (q->n_scales) {
+    CUDA_TRY(cudaMemcpyAsync(up.scales, q->scales, q->n_scales * 4, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(up.zps, q->zero_points, q->n_scales, cudaMemcpyHostToDevice, s));
+  }
+  CUDA_TRY(launch_validate_groups(up.gs, up.goff, rows, cols, q->n_scales, up.err, s));
+  egt_status st = finish_error_flag(up.err, s);
+  if (st != EGT_OK) return st;
+  return build_handle(I4_DENSE, 4, EGT_KIND_INT4, rows, cols, static_cast<uint64_t>(rows) * cols,
+                      q->group_sizes, q->n_scales, up, c.total, s, out);
+}
+
+egt_status egt_dev_packed_slice_rows(const egt_dev_packed* h, uint32_t r0, uint32_t r1,
+                                     egt_dev_packed** out) {
+  if (!h || !out) return fail(EGT_EINVAL, "slice_rows: null argument");
+  *out = nullptr;
+  if (r0 > r1 || r1 > h->rows) return fail(EGT_EINVAL, "slice_rows: row range outside the matrix");
+  auto s = std::make_unique<egt_dev_packed>();
+  s->store = h->store;
+  s->rows = r1 - r0;
+  s->cols = h->cols;
+  s->n = h->n;
+  s->m = h->m;
+  s->kind = h->kind;
+  s->format = h->format;
+  s->path = h->path;
+  s->raw = h->raw;
+  s->tiled = h->tiled;
+  const double frac = h->rows ? static_cast<double>(r1 - r0) / h->rows : 0.0;
+  s->nnz = static_cast<uint64_t>(s->rows) * (h->rows ? h->nnz / h->rows : 0);
+  s->algorithmic_bytes = static_cast<uint64_t>(frac * h->algorithmic_bytes + 0.5);
+  s->device_bytes = static_cast<uint64_t>(frac * h->device_bytes + 0.5);
+  if (h->path == EGT_PATH_TILED) {
+    if (r0 % 16 != 0 || (r1 % 16 != 0 && r1 != h->rows))
+      return fail(EGT_EINVAL, "slice_rows: tiled shards must start and end on 16-row tiles");
+    s->tiled.rt_begin = h->tiled.rt_begin + static_cast<int>(r0 / 16);
+    s->tiled.RT = static_cast<int>((s->rows + 15) / 16);
+  } else {
+    s->raw.row_begin = h->raw.row_begin + r0;
+  }
+  *out = s.release();
+  return EGT_OK;
+}
+
+egt_status egt_dev_packed_destroy(egt_dev_packed* h) {
+  delete h;
+  return EGT_OK;
+}
+
+egt_status egt_dev_packed_query(const egt_dev_packed* h, egt_dev_packed_info* info) {
+  if (!h || !info) return fail(EGT_EINVAL, "query: null argument");
+  info->rows = h->rows;
+  info->cols = h->cols;
+  info->n = h->n;
+  info->m = h->m;
+  info->kind = h->kind;
+  info->format = h->format;
+  info->path = h->path;
+  info->device_bytes = h->device_bytes;
+  info->algorithmic_bytes = h->algorithmic_bytes;
+  info->nnz = h->nnz;
+  return EGT_OK;
+}
+
+egt_status egt_spmv(const egt_dev_packed* h, const float* x, float* y, uint32_t M, uint32_t ldx,
+                    uint32_t ldy, void* stream) {
+  if (!h) return fail(EGT_EINVAL, "spmv: null matrix");
+  if (M == 0) return EGT_OK;
+  if (ldx < h->cols) return fail(EGT_EINVAL, "spmv: input length differs from columns");
+  if (M > 1 && ldy < h->rows) return fail(EGT_EINVAL, "spmv: output stride below rows");
+  if (h->rows == 0) return EGT_OK;
+  if (!x || !y) return fail(EGT_EINVAL, "spmv: null vector");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  LaunchCtx ctx;
+  ctx.stream = s;
+  ctx.pdl = g_pdl;
+  if (h->cols == 0) {
+    for (uint32_t m = 0; m < M; ++m)
+      CUDA_TRY(cudaMemsetAsync(y + static_cast<size_t>(m) * ldy, 0, h->rows * sizeof(float), s));
+    return EGT_OK;
+  }
+  if (h->path == EGT_PATH_GENERAL) {
+    CUDA_TRY(launch_general(h, x, static_cast<int>(ldx), static_cast<int>(M), y,
+                            static_cast<int>(ldy), ctx));
+    return EGT_OK;
+  }
+  TiledSchedule sc;
+  {
+    std::lock_guard<std::mutex> lk(h->plan_mu);
+    auto it = h->plans.find(static_cast<int>(M));
+    if (it == h->plans.end()) it = h->plans.emplace(static_cast<int>(M), plan_tiled(h, M, num_sms())).first;
+    sc = it->second;
+  }
+  if (sc.S > 1) {
+    Workspace* w = nullptr;
+    egt_status st = get_workspace(s, tiled_workspace_floats(h, sc, M),
+                                  static_cast<size_t>(sc.grid_x) * sc.grid_z, &w);
+    if (st != EGT_OK) return st;
+    ctx.partial = w->partial;
+    ctx.counters = w->counters;
+  }
+  CUDA_TRY(launch_tiled(h, sc, x, static_cast<int>(ldx), static_cast<int>(M), y,
+                        static_cast<int>(ldy), ctx));
+  return EGT_OK;
+}
+
+egt_status egt_spmv_host(const egt_dev_packed* h, const float* x_host, size_t x_len, float* y_host,
+                         void* stream) {
+  if (!h) return fail(EGT_EINVAL, "spmv: null matrix");
+  if (x_len != h->cols) return fail(EGT_EINVAL, "spmv: input length differs from columns");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  float* dx = nullptr;
+  float* dy = nullptr;
+  const size_t xb = std::max<size_t>(h->cols, 1) * sizeof(float);
+  const size_t yb = std::max<size_t>(h->rows, 1) * sizeof(float);
+  CUDA_TRY(cudaMallocAsync(reinterpret_cast<void**>(&dx), xb + yb, s));
+  dy = dx + std::max<size_t>(h->cols, 1);
+  egt_status st = EGT_OK;
+  cudaError_t e = cudaMemcpyAsync(dx, x_host, h->cols * sizeof(float), cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) {
+    st = egt_spmv(h, dx, dy, 1, h->cols, h->rows, stream);
+    if (st == EGT_OK)
+      e = cudaMemcpyAsync(y_host, dy, h->rows * sizeof(float), cudaMemcpyDeviceToHost, s);
+  }
+  cudaFreeAsync(dx, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (st != EGT_OK) return st;
+  if (e != cudaSuccess) return fail(EGT_ECUDA, std::string("spmv_host: ") + cudaGetErrorString(e));
+  return EGT_OK;
+}
+
+egt_status egt_dequant(const egt_dev_packed* h, float* w, uint8_t* mask, void* stream) {
+  if (!h || (!w && h->rows && h->cols)) return fail(EGT_EINVAL, "dequant: null argument");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t n = static_cast<size_t>(h->rows) * h->cols;
+  if (n == 0) return EGT_OK;
+  CUDA_TRY(cudaMemsetAsync(w, 0, n * sizeof(float), s));
+  if (mask) {
+    // the kernel ORs whole 32-bit words: the buffer holds ceil(n/32) words
+    CUDA_TRY(cudaMemsetAsync(mask, 0, (n + 31) / 32 * 4, s));
+  }
+  CUDA_TRY(launch_dequant(h, w, mask, s));
+  return EGT_OK;
+}
+
+}  // extern "C"

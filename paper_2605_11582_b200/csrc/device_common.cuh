@@ -1,0 +1,113 @@
+// Device helpers shared by the SparseGemv kernels (sm_100a only).
+#pragma once
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "egt_b200 is built for sm_100a only"
+#endif
+
+namespace egt_dev {
+
+constexpr int kWarp = 32;
+
+// Streamed, read-once weight loads: no L1 allocation, and an L2 evict-first
+// policy so the packed stream does not push x / partial sums out of L2.
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint4 ldg_stream_v4(const void* ptr, uint64_t pol) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u32 {%0,%1,%2,%3}, [%4], %5;\n"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(ptr), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ uint2 ldg_stream_v2(const void* ptr, uint64_t pol) {
+  uint2 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;\n"
+               : "=r"(r.x), "=r"(r.y)
+               : "l"(ptr), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ uint32_t ldg_stream_u32(const void* ptr, uint64_t pol) {
+  uint32_t r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;\n"
+               : "=r"(r)
+               : "l"(ptr), "l"(pol));
+  return r;
+}
+__device__ __forceinline__ uint32_t ldg_stream_u16(const void* ptr, uint64_t pol) {
+  uint16_t r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u16 %0, [%1], %2;\n"
+               : "=h"(r)
+               : "l"(ptr), "l"(pol));
+  return r;
+}
+
+// Programmatic dependent launch: weights do not depend on the previous
+// kernel, x does.  Everything before pdl_wait() may overlap the producer.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+
+// INT4 nibble pair -> half2 {1024 + lo, 1024 + hi}: the nibbles at bits
+// [0,4) and [16,20) of v land in the fp16 mantissas under exponent 0x64.
+__device__ __forceinline__ uint32_t nib2_magic(uint32_t v) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;\n" : "=r"(r) : "r"(v), "r"(0x000F000Fu), "r"(0x64006400u));
+  return r;  // (v & mask) | magic
+}
+
+__device__ __forceinline__ uint32_t hsub2_u32(uint32_t a, uint32_t b) {
+  __half2 r = __hsub2(*reinterpret_cast<__half2*>(&a), *reinterpret_cast<__half2*>(&b));
+  return *reinterpret_cast<uint32_t*>(&r);
+}
+
+// half2 {1024 + z0, 1024 + z1} for two zero points.
+__device__ __forceinline__ uint32_t zp_magic(uint32_t z0, uint32_t z1) {
+  return (0x6400u | z0) | ((0x6400u | z1) << 16);
+}
+
+__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
+  uint32_t r;
+  asm("prmt.b32 %0, %1, %2, %3;\n" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+  return r;
+}
+
+// D[16x8] (+)= A[16x32, 2:4 sparse] * B[32x8], f16 inputs, f32 accumulate.
+// Metadata register e is read from lanes {0,1} (sel 0) or {2,3} (sel 1) of
+// each quad: lane 2*sel holds row g, lane 2*sel+1 row g+8; nibble q of the
+// register = group q (columns 4q..4q+3): bits[1:0] first index, [3:2] second.
+template <int kSel>
+__device__ __forceinline__ void mma_sp_16832(float (&d)[4], const uint32_t (&a)[4],
+                                             const uint32_t (&b)[4], uint32_t e) {
+  asm volatile(
+      "mma.sp::ordered_metadata.sync.aligned.m16n8k32.row.col.f32.f16.f16.f32 "
+      "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9,%10,%11}, {%0,%1,%2,%3}, %12, %13;\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]), "r"(b[2]), "r"(b[3]),
+        "r"(e), "n"(kSel));
+}
+
+// Dense D[16x8] (+)= A[16x16] * B[16x8], f16 inputs, f32 accumulate.
+__device__ __forceinline__ void mma_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                          uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 "
+      "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+}  // namespace egt_dev

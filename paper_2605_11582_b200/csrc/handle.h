@@ -1,0 +1,109 @@
+// Internal device-handle representation shared by the C-ABI and the kernels.
+#pragma once
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <map>
+#include <memory>
+#include <mutex>
+
+#include "tiled_format.h"
+
+namespace egt_impl {
+
+struct DevStorage {
+  int device = 0;
+  void* base = nullptr;
+  size_t bytes = 0;
+  ~DevStorage();
+};
+
+// Raw (reference-order) stream, used by the general CUDA-core path and as
+// the source of the upload-time re-tiling.
+struct RawStream {
+  const uint16_t* words = nullptr;       // index words
+  const uint8_t* codes = nullptr;        // nibble-packed codes (INT4 sparse)
+  const uint8_t* dense_codes = nullptr;  // one code per byte (dense INT4)
+  const __half* values = nullptr;        // FP16 values (sparse FP)
+  const uint32_t* group_sizes = nullptr;
+  const uint32_t* group_offsets = nullptr;
+  const float* scales = nullptr;
+  const uint8_t* zps = nullptr;
+  uint64_t n_scales = 0;
+  uint32_t row_begin = 0;  // first row of this handle within the stream
+};
+
+// Fragment-tiled stream (tiled_format.h), used by the tensor-core path.
+struct TiledStream {
+  const uint8_t* vals = nullptr;
+  const uint8_t* meta = nullptr;
+  const float* scales = nullptr;
+  const uint8_t* zps = nullptr;
+  int KQ = 0;        // k-quads per row tile (storage)
+  int rt_begin = 0;  // first row tile of this handle
+  int RT = 0;        // row tiles covered by this handle
+  int SS = 4;        // k-tiles per scale entry
+  int E = 1;         // scale entries per k-quad (4 / SS)
+};
+
+struct TiledSchedule {
+  int RB = 1;  // row tiles per CTA
+  int WK = 1;  // warps per row tile (split of the CTA's k-quads)
+  int KC = 1;  // k-quads per CTA
+  int S = 1;   // K splits (CTAs along K, reduced by the last arriver)
+  int NT = 1;  // mma n-tiles (4 tokens each) per CTA
+  int NB = 1;  // n-blocks (CTAs along tokens)
+  int grid_x = 1, grid_y = 1, grid_z = 1;
+  size_t smem = 0;
+};
+
+}  // namespace egt_impl
+
+struct egt_dev_packed {
+  std::shared_ptr<egt_impl::DevStorage> store;
+  uint32_t rows = 0, cols = 0;
+  uint8_t n = 2, m = 4, kind = 1, format = 0, path = 0;
+  egt_impl::RawStream raw;
+  egt_impl::TiledStream tiled;
+  uint64_t nnz = 0;
+  uint64_t algorithmic_bytes = 0;
+  uint64_t device_bytes = 0;
+  // Launch plans keyed by M (logically const: a plan depends only on shape).
+  mutable std::mutex plan_mu;
+  mutable std::map<int, egt_impl::TiledSchedule> plans;
+};
+
+namespace egt_impl {
+
+// Per-call launch context.
+struct LaunchCtx {
+  cudaStream_t stream = nullptr;
+  bool pdl = true;
+  float* partial = nullptr;      // split-K partial sums
+  uint32_t* counters = nullptr;  // split-K arrival counters (self-resetting)
+};
+
+TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms);
+size_t tiled_workspace_floats(const egt_dev_packed* h, const TiledSchedule& sc, int M);
+
+cudaError_t launch_tiled(const egt_dev_packed* h, const TiledSchedule& sc, const float* x, int ldx,
+                         int M, float* y, int ldy, const LaunchCtx& ctx);
+cudaError_t launch_general(const egt_dev_packed* h, const float* x, int ldx, int M, float* y,
+                           int ldy, const LaunchCtx& ctx);
+
+// Upload-time kernels; the raw arrays live on the device.
+cudaError_t launch_validate_offsets(const uint16_t* words, uint32_t rows, uint32_t cols, int n,
+                                    uint32_t* err_flag, cudaStream_t s);
+cudaError_t launch_validate_groups(const uint32_t* gsizes, const uint32_t* goffs, uint32_t rows,
+                                   uint32_t cols, uint64_t n_scales, uint32_t* err_flag,
+                                   cudaStream_t s);
+cudaError_t launch_f32_to_f16(const float* src, __half* dst, uint64_t n, cudaStream_t s);
+cudaError_t launch_relayout(const RawStream& raw, int format, uint32_t rows, uint32_t cols,
+                            const TiledStream& dst_shape, uint8_t* vals, uint8_t* meta,
+                            float* scales, uint8_t* zps, cudaStream_t s);
+cudaError_t launch_dequant(const egt_dev_packed* h, float* w, uint8_t* mask, cudaStream_t s);
+
+uint64_t& launch_counter();
+
+}  // namespace egt_impl

@@ -1,0 +1,516 @@
+// Upload-time validation and re-tiling, the general (reference-order) CUDA-core
+// SpGEMV, and the bit-exact device unpack.
+#include "device_common.cuh"
+#include "handle.h"
+
+namespace egt_impl {
+using namespace egt_dev;
+using namespace egt_fmt;
+
+uint64_t& launch_counter() {
+  static thread_local uint64_t n = 0;
+  return n;
+}
+
+// offset_at (packed.hpp:64-66)
+__device__ __forceinline__ uint32_t offset_at(const uint16_t* words, uint64_t k) {
+  return (static_cast<uint32_t>(words[k >> 3]) >> (14 - 2 * (k & 7))) & 3u;
+}
+__device__ __forceinline__ uint32_t nibble_at(const uint8_t* codes, uint64_t k) {
+  return (codes[k >> 1] >> (4 * (k & 1))) & 0xFu;
+}
+// decode_value (compress.cpp:98-101), with explicit rounding so nothing is
+// contracted: (f32(code) - f32(zp)) * scale.
+__device__ __forceinline__ float decode(uint32_t code, uint32_t zp, float scale) {
+  return __fmul_rn(__fsub_rn(static_cast<float>(code), static_cast<float>(zp)), scale);
+}
+
+// ------------------------------------------------------------- validation
+// for_each_nonzero's order check (packed.cpp:176-178): within a group of n
+// kept entries the offsets strictly increase.  Done once at upload.
+__global__ void validate_offsets_kernel(const uint16_t* words, uint32_t rows, uint32_t cols, int n,
+                                        uint32_t* err) {
+  const uint64_t groups = static_cast<uint64_t>(rows) * (cols / 4);
+  for (uint64_t G = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; G < groups;
+       G += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t k = G * n;
+    uint32_t prev = offset_at(words, k);
+    for (int i = 1; i < n; ++i) {
+      const uint32_t off = offset_at(words, k + i);
+      if (off <= prev) atomicOr(err, 1u);
+      prev = off;
+    }
+  }
+}
+
+// Group tables must index inside the scale table for every column (the
+// reference indexes them unchecked, packed.cpp:189-191).
+__global__ void validate_groups_kernel(const uint32_t* gs, const uint32_t* goff, uint32_t rows,
+                                       uint32_t cols, uint64_t n_scales, uint32_t* err) {
+  const uint32_t r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  const uint32_t g = gs[r];
+  if (g == 0) {
+    atomicOr(err, 2u);
+    return;
+  }
+  const uint64_t ng = (static_cast<uint64_t>(cols) + g - 1) / g;
+  if (static_cast<uint64_t>(goff[r]) + ng > n_scales) atomicOr(err, 4u);
+}
+
+cudaError_t launch_validate_offsets(const uint16_t* words, uint32_t rows, uint32_t cols, int n,
+                                    uint32_t* err, cudaStream_t s) {
+  if (n < 2 || rows == 0 || cols == 0) return cudaSuccess;
+  validate_offsets_kernel<<<1184, 256, 0, s>>>(words, rows, cols, n, err);
+  ++launch_counter();
+  return cudaGetLastError();
+}
+
+cudaError_t launch_validate_groups(const uint32_t* gs, const uint32_t* goff, uint32_t rows,
+                                   uint32_t cols, uint64_t n_scales, uint32_t* err,
+                                   cudaStream_t s) {
+  if (rows == 0) return cudaSuccess;
+  validate_groups_kernel<<<(rows + 255) / 256, 256, 0, s>>>(gs, goff, rows, cols, n_scales, err);
+  ++launch_counter();
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------- re-tiling
+// One thread per (row tile, k-quad, lane): gathers exactly the bits the lane
+// will consume (tiled_format.h) from the reference-order stream.
+struct RelayoutArgs {
+  RawStream raw;
+  int format;
+  uint32_t rows, cols;
+  int KQ, RT, SS, E;
+  uint8_t* vals;
+  uint8_t* meta;
+  float* scales;
+  uint8_t* zps;
+};
+
+__device__ __forceinline__ bool group_valid(const RelayoutArgs& a, uint32_t r, uint32_t G) {
+  return r < a.rows && G * 4 < a.cols;
+}
+
+__global__ void relayout_kernel(const RelayoutArgs a) {
+  const uint64_t total = static_cast<uint64_t>(a.RT) * a.KQ * 32;
+  const uint64_t idx = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (idx >= total) return;
+  const int lane = static_cast<int>(idx & 31);
+  const uint64_t blk = idx >> 5;
+  const int kq = static_cast<int>(blk % a.KQ);
+  const int rt = static_cast<int>(blk / a.KQ);
+  const int g = lane >> 2, t = lane & 3;
+  const int f = a.format;
+  const int n = keep_n(f);
+  const uint64_t row_nnz = static_cast<uint64_t>(a.cols) * (n == 4 ? 4 : n) / 4;
+  const RawStream& raw = a.raw;
+
+  if (f == I4_SP24 || f == F16_SP24) {
+    uint32_t v[16] = {0};
+    for (int j = 0; j < 4; ++j)
+      for (int h = 0; h < 2; ++h)
+        for (int q = 0; q < 2; ++q) {
+          const uint32_t r = rt * 16 + g + 8 * h;
+          const uint32_t G = (kq * 4 + j) * 8 + t + 4 * q;
+          const int p = h + 2 * q;
+          if (!group_valid(a, r, G)) {
+            continue;  // codes 0 / values 0 (scale 0 / x 0 make them inert)
+          }
+          const uint64_t k0 = (raw.row_begin + r) * row_nnz + 2ull * G;
+          if (f == I4_SP24) {
+            v[j] |= nibble_at(raw.codes, k0) << (4 * p);
+            v[j] |= nibble_at(raw.codes, k0 + 1) << (16 + 4 * p);
+          } else {
+            v[4 * j + p] = static_cast<uint32_t>(__half_as_ushort(raw.values[k0])) |
+                           (static_cast<uint32_t>(__half_as_ushort(raw.values[k0 + 1])) << 16);
+          }
+        }
+    const int VB = val_lane_bytes(f);
+    uint32_t* vo = reinterpret_cast<uint32_t*>(a.vals + blk * 32 * VB + lane * VB);
+    for (int i = 0; i < VB / 4; ++i) vo[i] = v[i];
+    uint32_t m[2];
+    for (int sl = 0; sl < 2; ++sl) {
+      const int j = (t >> 1) + 2 * sl, h = t & 1;
+      const uint32_t r = rt * 16 + g + 8 * h;
+      uint32_t word = 0;
+      for (int q8 = 0; q8 < 8; ++q8) {
+        const uint32_t G = (kq * 4 + j) * 8 + q8;
+        uint32_t nib = 0x4u;  // (0,1): a valid ordered pattern for padding
+        if (group_valid(a, r, G)) {
+          const uint64_t k0 = (raw.row_begin + r) * row_nnz + 2ull * G;
+          nib = offset_at(raw.words, k0) | (offset_at(raw.words, k0 + 1) << 2);
+        }
+        word |= nib << (4 * q8);
+      }
+      m[sl] = word;
+    }
+    uint32_t* mo = reinterpret_cast<uint32_t*>(a.meta + blk * 32 * 8 + lane * 8);
+    mo[0] = m[0];
+    mo[1] = m[1];
+  } else if (f == I4_SP14 || f == F16_SP14) {
+    uint32_t v[8] = {0};
+    uint32_t ms = 0;
+    for (int j = 0; j < 4; ++j)
+      for (int h = 0; h < 2; ++h)
+        for (int q = 0; q < 2; ++q) {
+          const uint32_t r = rt * 16 + g + 8 * h;
+          const uint32_t G = (kq * 4 + j) * 8 + t + 4 * q;
+          if (!group_valid(a, r, G)) continue;
+          const uint64_t k = (raw.row_begin + r) * row_nnz + G;
+          const uint32_t off = offset_at(raw.words, k);
+          ms |= (off & 1u) << (4 * j + h + 2 * q);
+          if (f == I4_SP14) {
+            v[j >> 1] |= nibble_at(raw.codes, k) << (4 * (2 * (j & 1) + q) + 16 * h);
+          } else {
+            v[2 * j + q] |= static_cast<uint32_t>(__half_as_ushort(raw.values[k])) << (16 * h);
+          }
+        }
+    for (int sl = 0; sl < 2; ++sl) {
+      const int j = (t >> 1) + 2 * sl, h = t & 1;
+      const uint32_t r = rt * 16 + g + 8 * h;
+      for (int q8 = 0; q8 < 8; ++q8) {
+        const uint32_t G = (kq * 4 + j) * 8 + q8;
+        if (!group_valid(a, r, G)) continue;
+        const uint64_t k = (raw.row_begin + r) * row_nnz + G;
+        ms |= ((offset_at(raw.words, k) >> 1) & 1u) << (16 + 8 * sl + q8);
+      }
+    }
+    const int VB = val_lane_bytes(f);
+    uint32_t* vo = reinterpret_cast<uint32_t*>(a.vals + blk * 32 * VB + lane * VB);
+    for (int i = 0; i < VB / 4; ++i) vo[i] = v[i];
+    *reinterpret_cast<uint32_t*>(a.meta + blk * 32 * 4 + lane * 4) = ms;
+  } else {  // I4_DENSE: 8 k16 tiles per k-quad
+    uint32_t v[8] = {0};
+    for (int w = 0; w < 8; ++w)
+      for (int h = 0; h < 2; ++h)
+        for (int q = 0; q < 2; ++q) {
+          const uint32_t r = rt * 16 + g + 8 * h;
+          const uint32_t c = kq * 128 + 16 * w + 2 * t + 8 * q;
+          const int p = h + 2 * q;
+          if (r >= a.rows || c >= a.cols) continue;
+          const uint64_t k = static_cast<uint64_t>(raw.row_begin + r) * a.cols + c;
+          v[w] |= static_cast<uint32_t>(raw.dense_codes[k] & 0xF) << (4 * p);
+          v[w] |= static_cast<uint32_t>(raw.dense_codes[k + 1] & 0xF) << (16 + 4 * p);
+        }
+    uint32_t* vo = reinterpret_cast<uint32_t*>(a.vals + blk * 32 * 32 + lane * 32);
+    for (int i = 0; i < 8; ++i) vo[i] = v[i];
+  }
+}
+
+// Per (row tile, k-quad, scale entry, row): the group covering k-tiles
+// [e*SS, (e+1)*SS) of the quad.  Group boundaries are multiples of 32
+// columns on the tiled path, so a k-tile never straddles two groups.
+__global__ void relayout_scales_kernel(const RelayoutArgs a) {
+  const uint64_t total = static_cast<uint64_t>(a.RT) * a.KQ * a.E * 16;
+  const uint64_t idx = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (idx >= total) return;
+  const int slot = static_cast<int>(idx & 15);
+  const uint64_t be = idx >> 4;
+  const int e = static_cast<int>(be % a.E);
+  const uint64_t blk = be / a.E;
+  const int kq = static_cast<int>(blk % a.KQ);
+  const int rt = static_cast<int>(blk / a.KQ);
+  const int g = slot >> 1, h = slot & 1;
+  const uint32_t r = rt * 16 + g + 8 * h;
+  const uint32_t col = kq * 128 + e * a.SS * 32;
+  float s = 0.f;
+  uint8_t z = 0;
+  if (r < a.rows && col < a.cols) {
+    const uint32_t R = a.raw.row_begin + r;
+    const uint64_t gi = static_cast<uint64_t>(a.raw.group_offsets[R]) + col / a.raw.group_sizes[R];
+    s = a.raw.scales[gi];
+    z = a.raw.zps[gi];
+  }
+  a.scales[idx] = s;
+  a.zps[idx] = z;
+}
+
+cudaError_t launch_relayout(const RawStream& raw, int format, uint32_t rows, uint32_t cols,
+                            const TiledStream& dst, uint8_t* vals, uint8_t* meta, float* scales,
+                            uint8_t* zps, cudaStream_t s) {
+  RelayoutArgs a;
+  a.raw = raw;
+  a.format = format;
+  a.rows = rows;
+  a.cols = cols;
+  a.KQ = dst.KQ;
+  a.RT = dst.RT;
+  a.SS = dst.SS;
+  a.E = dst.E;
+  a.vals = vals;
+  a.meta = meta;
+  a.scales = scales;
+  a.zps = zps;
+  const uint64_t total = static_cast<uint64_t>(dst.RT) * dst.KQ * 32;
+  relayout_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(a);
+  ++launch_counter();
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess || !has_scales(format)) return err;
+  const uint64_t tot_s = static_cast<uint64_t>(dst.RT) * dst.KQ * dst.E * 16;
+  relayout_scales_kernel<<<static_cast<unsigned>((tot_s + 255) / 256), 256, 0, s>>>(a);
+  ++launch_counter();
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------- general path
+// Reference-order stream, one warp per output row, lanes stride over the
+// row's kept entries; any group size, any cols % 4 == 0.  Used when the
+// group sizes are not multiples of 32 (the tiled path's k-tile).
+struct GeneralArgs {
+  RawStream raw;
+  int kind;  // 0 sparse INT4, 1 sparse FP16, 2 dense INT4
+  uint32_t rows, cols;
+  int n;
+  const float* x;
+  int ldx, M;
+  float* y;
+  int ldy;
+};
+
+__global__ void __launch_bounds__(256) general_spmm_kernel(const GeneralArgs a) {
+  pdl_launch_dependents();
+  pdl_wait();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t r = blockIdx.x * 8 + warp;
+  if (r >= a.rows) return;
+  const uint64_t R = a.raw.row_begin + r;
+  const uint64_t row_nnz = a.kind == 2 ? a.cols : static_cast<uint64_t>(a.cols) * a.n / 4;
+  const uint32_t gsz = a.kind == 1 ? 1u : a.raw.group_sizes[R];
+  const uint32_t gbase = a.kind == 1 ? 0u : a.raw.group_offsets[R];
+  for (int m0 = 0; m0 < a.M; m0 += 8) {
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (uint64_t j = lane; j < row_nnz; j += 32) {
+      const uint64_t k = R * row_nnz + j;
+      uint32_t col;
+      float v;
+      if (a.kind == 2) {
+        col = static_cast<uint32_t>(j);
+        const uint32_t gi = gbase + col / gsz;
+        v = decode(a.raw.dense_codes[k], a.raw.zps[gi], a.raw.scales[gi]);
+      } else {
+        col = static_cast<uint32_t>(j / a.n) * 4 + offset_at(a.raw.words, k);
+        if (a.kind == 0) {
+          const uint32_t gi = gbase + col / gsz;
+          v = decode(nibble_at(a.raw.codes, k), a.raw.zps[gi], a.raw.scales[gi]);
+        } else {
+          v = __half2float(a.raw.values[k]);
+        }
+      }
+#pragma unroll
+      for (int mm = 0; mm < 8; ++mm)
+        if (m0 + mm < a.M) acc[mm] = fmaf(v, a.x[static_cast<size_t>(m0 + mm) * a.ldx + col], acc[mm]);
+    }
+#pragma unroll
+    for (int mm = 0; mm < 8; ++mm) {
+      const float s = warp_sum(acc[mm]);
+      if (lane == 0 && m0 + mm < a.M) a.y[static_cast<size_t>(m0 + mm) * a.ldy + r] = s;
+    }
+  }
+}
+
+cudaError_t launch_general(const egt_dev_packed* h, const float* x, int ldx, int M, float* y,
+                           int ldy, const LaunchCtx& ctx) {
+  GeneralArgs a;
+  a.raw = h->raw;
+  a.kind = h->format == I4_DENSE ? 2 : (h->kind == 0 ? 1 : 0);
+  a.rows = h->rows;
+  a.cols = h->cols;
+  a.n = h->n;
+  a.x = x;
+  a.ldx = ldx;
+  a.M = M;
+  a.y = y;
+  a.ldy = ldy;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((h->rows + 7) / 8);
+  cfg.blockDim = dim3(256);
+  cfg.stream = ctx.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = ctx.pdl ? 1 : 0;
+  void* args[] = {&a};
+  cudaError_t err = cudaLaunchKernelExC(&cfg, reinterpret_cast<void*>(&general_spmm_kernel), args);
+  if (err == cudaSuccess) ++launch_counter();
+  return err;
+}
+
+// ------------------------------------------------------------- unpack
+// Bit-exact dense reconstruction (unpack, packed.cpp:197-209).
+__device__ __forceinline__ void set_mask(uint8_t* mask, uint32_t cols, uint32_t r, uint32_t c) {
+  if (!mask) return;
+  const uint64_t i = static_cast<uint64_t>(r) * cols + c;
+  atomicOr(reinterpret_cast<unsigned int*>(mask) + (i >> 5), 1u << (i & 31));
+}
+
+__global__ void dequant_general_kernel(const GeneralArgs a, float* w, uint8_t* mask) {
+  const uint64_t row_nnz = a.kind == 2 ? a.cols : static_cast<uint64_t>(a.cols) * a.n / 4;
+  const uint64_t total = static_cast<uint64_t>(a.rows) * row_nnz;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const uint32_t r = static_cast<uint32_t>(i / row_nnz);
+    const uint64_t j = i % row_nnz;
+    const uint64_t R = a.raw.row_begin + r;
+    const uint64_t k = R * row_nnz + j;
+    uint32_t col;
+    float v;
+    if (a.kind == 2) {
+      col = static_cast<uint32_t>(j);
+      const uint32_t gi = a.raw.group_offsets[R] + col / a.raw.group_sizes[R];
+      v = decode(a.raw.dense_codes[k], a.raw.zps[gi], a.raw.scales[gi]);
+    } else {
+      col = static_cast<uint32_t>(j / a.n) * 4 + offset_at(a.raw.words, k);
+      if (a.kind == 0) {
+        const uint32_t gi = a.raw.group_offsets[R] + col / a.raw.group_sizes[R];
+        v = decode(nibble_at(a.raw.codes, k), a.raw.zps[gi], a.raw.scales[gi]);
+      } else {
+        v = __half2float(a.raw.values[k]);
+      }
+    }
+    w[static_cast<uint64_t>(r) * a.cols + col] = v;
+    set_mask(mask, a.cols, r, col);
+  }
+}
+
+struct DequantTiledArgs {
+  TiledStream ts;
+  int format;
+  uint32_t rows, cols;
+  float* w;
+  uint8_t* mask;
+};
+
+__global__ void dequant_tiled_kernel(const DequantTiledArgs a) {
+  const uint64_t total = static_cast<uint64_t>(a.ts.RT) * a.ts.KQ * 32;
+  const uint64_t idx = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (idx >= total) return;
+  const int lane = static_cast<int>(idx & 31);
+  const uint64_t lblk = idx >> 5;  // block index within this handle
+  const int kq = static_cast<int>(lblk % a.ts.KQ);
+  const int rt = static_cast<int>(lblk / a.ts.KQ);
+  const uint64_t blk = static_cast<uint64_t>(a.ts.rt_begin + rt) * a.ts.KQ + kq;
+  const int g = lane >> 2, t = lane & 3;
+  const int f = a.format;
+  const int VB = val_lane_bytes(f), MB = meta_lane_bytes(f);
+  const uint32_t* v = reinterpret_cast<const uint32_t*>(a.ts.vals + blk * 32 * VB + lane * VB);
+  const uint32_t* mb = reinterpret_cast<const uint32_t*>(a.ts.meta + blk * 32 * MB);
+  auto scale_of = [&](int j, int h, float* s, uint32_t* z) {
+    const int e = j / a.ts.SS;
+    const uint64_t si = (blk * a.ts.E + e) * 16 + 2 * g + h;
+    *s = a.ts.scales[si];
+    *z = a.ts.zps[si];
+  };
+  if (f == I4_DENSE) {
+    for (int w16 = 0; w16 < 8; ++w16)
+      for (int h = 0; h < 2; ++h)
+        for (int q = 0; q < 2; ++q)
+          for (int i = 0; i < 2; ++i) {
+            const uint32_t r = rt * 16 + g + 8 * h;
+            const uint32_t c = kq * 128 + 16 * w16 + 2 * t + 8 * q + i;
+            if (r >= a.rows || c >= a.cols) continue;
+            const int p = h + 2 * q;
+            const uint32_t code = (v[w16] >> (4 * p + 16 * i)) & 0xFu;
+            float s;
+            uint32_t z;
+            scale_of((16 * w16) / 32, h, &s, &z);
+            a.w[static_cast<uint64_t>(r) * a.cols + c] = decode(code, z, s);
+            set_mask(a.mask, a.cols, r, c);
+          }
+    return;
+  }
+  const bool two = (f == I4_SP24 || f == F16_SP24);
+  for (int j = 0; j < 4; ++j)
+    for (int h = 0; h < 2; ++h)
+      for (int q = 0; q < 2; ++q) {
+        const uint32_t r = rt * 16 + g + 8 * h;
+        const uint32_t G = (kq * 4 + j) * 8 + t + 4 * q;
+        if (r >= a.rows || G * 4 >= a.cols) continue;
+        const int holder = 4 * g + 2 * (j & 1) + h;  // lane holding (row, k-tile j) metadata
+        const int grp = t + 4 * q;
+        if (two) {
+          const uint32_t word = mb[holder * 2 + (j >> 1)];
+          const uint32_t nib = (word >> (4 * grp)) & 0xFu;
+          const uint32_t off[2] = {nib & 3u, (nib >> 2) & 3u};
+          for (int i = 0; i < 2; ++i) {
+            const uint32_t c = G * 4 + off[i];
+            float val;
+            if (f == I4_SP24) {
+              const int p = h + 2 * q;
+              const uint32_t code = (v[j] >> (4 * p + 16 * i)) & 0xFu;
+              float s;
+              uint32_t z;
+              scale_of(j, h, &s, &z);
+              val = decode(code, z, s);
+            } else {
+              const uint32_t pair = v[4 * j + h + 2 * q];
+              val = __half2float(__ushort_as_half(static_cast<unsigned short>(pair >> (16 * i))));
+            }
+            a.w[static_cast<uint64_t>(r) * a.cols + c] = val;
+            set_mask(a.mask, a.cols, r, c);
+          }
+        } else {
+          const uint32_t own = mb[lane];
+          const uint32_t slot = (own >> (4 * j + h + 2 * q)) & 1u;
+          const uint32_t hword = mb[holder];
+          const uint32_t hi = (hword >> (16 + 8 * (j >> 1) + grp)) & 1u;
+          const uint32_t c = G * 4 + (hi << 1 | slot);
+          float val;
+          if (f == I4_SP14) {
+            const uint32_t code = (v[j >> 1] >> (4 * (2 * (j & 1) + q) + 16 * h)) & 0xFu;
+            float s;
+            uint32_t z;
+            scale_of(j, h, &s, &z);
+            val = decode(code, z, s);
+          } else {
+            val = __half2float(__ushort_as_half(static_cast<unsigned short>(v[2 * j + q] >> (16 * h))));
+          }
+          a.w[static_cast<uint64_t>(r) * a.cols + c] = val;
+          set_mask(a.mask, a.cols, r, c);
+        }
+      }
+}
+
+cudaError_t launch_dequant(const egt_dev_packed* h, float* w, uint8_t* mask, cudaStream_t s) {
+  if (h->path == 0) {
+    DequantTiledArgs a;
+    a.ts = h->tiled;
+    a.format = h->format;
+    a.rows = h->rows;
+    a.cols = h->cols;
+    a.w = w;
+    a.mask = mask;
+    const uint64_t total = static_cast<uint64_t>(h->tiled.RT) * h->tiled.KQ * 32;
+    if (total == 0) return cudaSuccess;
+    dequant_tiled_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(a);
+  } else {
+    GeneralArgs a;
+    a.raw = h->raw;
+    a.kind = h->format == I4_DENSE ? 2 : (h->kind == 0 ? 1 : 0);
+    a.rows = h->rows;
+    a.cols = h->cols;
+    a.n = h->n;
+    dequant_general_kernel<<<1184, 256, 0, s>>>(a, w, mask);
+  }
+  ++launch_counter();
+  return cudaGetLastError();
+}
+
+}  // namespace egt_impl
+
+namespace egt_impl {
+__global__ void f32_to_f16_kernel(const float* src, __half* dst, uint64_t n) {
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    dst[i] = __float2half_rn(src[i]);
+}
+
+cudaError_t launch_f32_to_f16(const float* src, __half* dst, uint64_t n, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  f32_to_f16_kernel<<<1184, 256, 0, s>>>(src, dst, n);
+  ++launch_counter();
+  return cudaGetLastError();
+}
+}  // namespace egt_impl

@@ -1,0 +1,48 @@
+// Fragment-tiled device layout of the 2bit-CSR stream (host + device).
+//
+// The reference stream (packed.hpp:37-67) is row-major: per row, the kept
+// entries in column order, 2-bit in-group offsets MSB-first in u16 words and
+// INT4 codes low-nibble-first.  On the device the SAME bits are permuted once
+// at upload into blocks of 16 rows x 128 columns ("k-quad", 4 mma k-tiles of
+// 32 columns) so that every lane of a warp fetches exactly the bits its
+// mma.sp / mma fragment consumes with one 16-byte (or 8-byte) coalesced load:
+//
+//   block (rt, kq) = rows [16*rt, 16*rt+16) x cols [128*kq, 128*kq+128)
+//   vals[(rt*KQ + kq)*32*VB + lane*VB .. +VB)   lane's A-operand bits
+//   meta[(rt*KQ + kq)*32*MB + lane*MB .. +MB)   lane's metadata bits
+//   scales/zps[((rt*KQ + kq)*E + e)*16 + 2*g + h]  (row 16rt + g + 8h)
+//
+// lane = 4*g + t (g = groupID 0..7, t = 0..3).  For INT4 2:4 the lane's u32
+// for k-tile j holds 8 nibbles: position p = h + 2q (h: row g / g+8, q: group
+// t / t+4 of the k-tile) -- first kept entry at bits 4p, second at 16+4p, so
+// that one LOP3 with the 0x6400 fp16 exponent yields the half2 register the
+// mma.sp A fragment wants.  Metadata u32 per (row, k-tile) is the mma.sp
+// ordered metadata (nibble q = group q: bits[1:0] first offset, [3:2] second),
+// held by lane t = 2*(j&1) + h of the row's quad (slot j>>1).  Bytes per block
+// equal the reference's bytes for the same entries (no padding unless the
+// matrix edge is ragged).
+#pragma once
+#include <stdint.h>
+
+namespace egt_fmt {
+
+constexpr int kRowsPerTile = 16;
+constexpr int kColsPerQuad = 128;
+constexpr int kKTile = 32;
+
+enum Format : int { I4_SP24 = 0, I4_SP14 = 1, I4_DENSE = 2, F16_SP24 = 3, F16_SP14 = 4 };
+
+// A-operand bytes per lane per k-quad.
+__host__ __device__ constexpr int val_lane_bytes(int f) {
+  return f == I4_SP24 ? 16 : f == I4_SP14 ? 8 : f == I4_DENSE ? 32 : f == F16_SP24 ? 64 : 32;
+}
+// Metadata bytes per lane per k-quad.
+__host__ __device__ constexpr int meta_lane_bytes(int f) {
+  return f == I4_SP24 ? 8 : f == I4_SP14 ? 4 : f == I4_DENSE ? 0 : f == F16_SP24 ? 8 : 4;
+}
+__host__ __device__ constexpr bool has_scales(int f) { return f <= I4_DENSE; }
+__host__ __device__ constexpr int keep_n(int f) {
+  return (f == I4_SP24 || f == F16_SP24) ? 2 : (f == I4_DENSE ? 4 : 1);
+}
+
+}  // namespace egt_fmt

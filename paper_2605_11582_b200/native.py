@@ -1,0 +1,135 @@
+"""ctypes binding of the C-ABI (include/egt_b200.h) -> _lib/libegt_b200.so.
+
+The library is built in-tree by paper_2605_11582_b200._build (nvcc,
+sm_100a).  There is no fallback: if the shared object is missing the import
+fails with the build command to run.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libegt_b200.so")
+
+EGT_OK, EGT_EINVAL, EGT_EFORMAT, EGT_EINTERNAL, EGT_ECUDA = range(5)
+KIND_F32, KIND_INT4 = 0, 1
+FMT_NAMES = {0: "int4-2:4", 1: "int4-1:4", 2: "int4-dense", 3: "fp16-2:4", 4: "fp16-1:4"}
+PATH_NAMES = {0: "tiled-mma.sp", 1: "general"}
+
+u8p = C.POINTER(C.c_uint8)
+u16p = C.POINTER(C.c_uint16)
+u32p = C.POINTER(C.c_uint32)
+u64p = C.POINTER(C.c_uint64)
+f32p = C.POINTER(C.c_float)
+f64p = C.POINTER(C.c_double)
+szp = C.POINTER(C.c_size_t)
+
+
+class PackedView(C.Structure):
+    """egt_packed_view (PackedSparseMatrix, packed.hpp:37-67)."""
+
+    _fields_ = [
+        ("n", C.c_uint8), ("m", C.c_uint8), ("rows", C.c_uint32), ("cols", C.c_uint32),
+        ("kind", C.c_uint8),
+        ("index_words", u16p), ("n_index_words", C.c_size_t),
+        ("value_bytes", u8p), ("n_value_bytes", C.c_size_t),
+        ("group_sizes", u32p), ("n_group_sizes", C.c_size_t),
+        ("group_offsets", u32p), ("n_group_offsets", C.c_size_t),
+        ("scales", f32p), ("n_scales", C.c_size_t),
+        ("zero_points", u8p), ("n_zero_points", C.c_size_t),
+        ("values", f32p), ("n_values", C.c_size_t),
+    ]
+
+
+class QuantView(C.Structure):
+    """egt_quant_view (QuantizedMatrix with every position kept)."""
+
+    _fields_ = [
+        ("rows", C.c_uint32), ("cols", C.c_uint32),
+        ("group_sizes", u32p), ("group_offsets", u32p),
+        ("scales", f32p), ("n_scales", C.c_size_t),
+        ("zero_points", u8p),
+        ("codes", u8p), ("n_codes", C.c_size_t),
+    ]
+
+
+class DevInfo(C.Structure):
+    _fields_ = [
+        ("rows", C.c_uint32), ("cols", C.c_uint32),
+        ("n", C.c_uint8), ("m", C.c_uint8), ("kind", C.c_uint8), ("format", C.c_uint8),
+        ("path", C.c_uint8),
+        ("device_bytes", C.c_uint64), ("algorithmic_bytes", C.c_uint64), ("nnz", C.c_uint64),
+    ]
+
+
+# every symbol include/egt_b200.h declares, with its signature
+SIGNATURES = {
+    "egt_abi_version": (C.c_int, []),
+    "egt_last_error": (C.c_char_p, []),
+    "egt_dev_packed_create": (C.c_int, [C.POINTER(PackedView), C.c_void_p, C.POINTER(C.c_void_p)]),
+    "egt_dev_dense_i4_create": (C.c_int, [C.POINTER(QuantView), C.c_void_p, C.POINTER(C.c_void_p)]),
+    "egt_dev_packed_slice_rows": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.POINTER(C.c_void_p)]),
+    "egt_dev_packed_destroy": (C.c_int, [C.c_void_p]),
+    "egt_dev_packed_query": (C.c_int, [C.c_void_p, C.POINTER(DevInfo)]),
+    "egt_spmv": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p]),
+    "egt_spmv_host": (C.c_int, [C.c_void_p, f32p, C.c_size_t, f32p, C.c_void_p]),
+    "egt_dequant": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "egt_set_pdl": (None, [C.c_int]),
+    "egt_launch_count": (C.c_uint64, []),
+    "egt_host_fit_group": (None, [f64p, C.c_size_t, f32p, u8p]),
+    "egt_host_group_count": (C.c_size_t, [C.c_uint32, C.c_uint32, u32p]),
+    "egt_host_quantize": (C.c_int, [f32p, C.c_uint32, C.c_uint32, u32p, u8p, u32p, f32p, u8p, u8p, szp]),
+    "egt_host_pack_int4": (C.c_int, [u8p, C.c_uint32, C.c_uint32, C.c_int, C.c_int, u8p, C.c_size_t, C.c_int,
+                                     u16p, szp, u8p, szp]),
+    "egt_host_pack_f32": (C.c_int, [u8p, C.c_uint32, C.c_uint32, C.c_int, C.c_int, f32p, u16p, szp, f32p, szp]),
+    "egt_host_footprint": (C.c_int, [C.POINTER(PackedView), u64p, f64p]),
+}
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_2605_11582_b200._build` "
+                "(or __graft_entry__.build()); there is no CPU fallback")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+class EgtError(Exception):
+    """Maps egt_status onto the reference's exception classes."""
+
+    KIND = {EGT_EINVAL: "invalid_argument", EGT_EFORMAT: "FormatError",
+            EGT_EINTERNAL: "InvariantError", EGT_ECUDA: "CudaError"}
+
+    def __init__(self, status: int, msg: str):
+        self.status = status
+        self.kind = self.KIND.get(status, "unknown")
+        super().__init__(f"{self.kind}: {msg}")
+
+
+class InvalidArgument(EgtError, ValueError):
+    pass
+
+
+class FormatError(EgtError):
+    pass
+
+
+def check(status: int) -> None:
+    if status != EGT_OK:
+        msg = lib().egt_last_error().decode(errors="replace")
+        if status == EGT_EINVAL:
+            raise InvalidArgument(status, msg)
+        if status == EGT_EFORMAT:
+            raise FormatError(status, msg)
+        raise EgtError(status, msg)

@@ -1,0 +1,245 @@
+"""GPU parity: the sm_100a kernels (through the C-ABI) against the oracle on
+identical seeded inputs.  Bit-exact for the device copy of the encoding
+(dequantised values + recovered keep mask); |got-want| <= 1e-3 (1+|want|)
+for products (the reference's own convention, test_packed.cpp:279)."""
+import numpy as np
+import pytest
+
+from tests.layers import close, make_f16, make_int4, to_product
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def egt():
+    import paper_2605_11582_b200 as egt
+
+    return egt
+
+
+@pytest.fixture(scope="module")
+def torch():
+    import torch
+
+    torch.cuda.init()
+    return torch
+
+
+def _dev(egt, p):
+    return egt.DeviceMatrix.from_packed(to_product(p))
+
+
+def _check_product(egt, port, torch, p, rng, M=1, expect_path=None):
+    d = _dev(egt, p)
+    if expect_path:
+        assert d.path == expect_path, d.path
+    xs = rng.uniform(-1, 1, (M, p.cols)).astype(np.float32)
+    x = torch.from_numpy(xs).cuda()
+    y = d.spmv(x if M > 1 else x[0]).cpu().numpy().reshape(M, -1)
+    for m in range(M):
+        want = port.spmv(p, xs[m])
+        ok, err = close(y[m], want)
+        assert ok, f"token {m}: max rel err {err:.3e} ({d.format}, {d.path}, {p.rows}x{p.cols})"
+    return d
+
+
+@pytest.mark.parametrize("shape", [(4096, 4096), (11008, 4096), (4096, 11008)])
+def test_int4_2of4_g128_baseline_shapes(egt, port, torch, shape):
+    rng = np.random.default_rng(shape[0] * 7 + shape[1])
+    p, _, _ = make_int4(rng, shape[0], shape[1], 2, 128, port)
+    d = _check_product(egt, port, torch, p, rng, expect_path="tiled-mma.sp")
+    assert d.format == "int4-2:4"
+    assert d.algorithmic_bytes == port.footprint(p)["packed_bytes"]
+
+
+@pytest.mark.parametrize("n", [1, 2])
+@pytest.mark.parametrize("group", [32, 64, 128, 256, "mixed"])
+def test_int4_group_sizes(egt, port, torch, n, group):
+    rng = np.random.default_rng(11 + n)
+    rows, cols = 272, 1024
+    g = np.where(rng.random(rows) < 0.5, 64, 128) if group == "mixed" else group
+    p, _, _ = make_int4(rng, rows, cols, n, g, port)
+    _check_product(egt, port, torch, p, rng, expect_path="tiled-mma.sp")
+
+
+@pytest.mark.parametrize("n", [1, 2])
+def test_int4_ragged_edges(egt, port, torch, n):
+    """rows not a multiple of 16, cols a multiple of 32 but not of 128."""
+    rng = np.random.default_rng(21)
+    for rows, cols in ((1, 32), (17, 96), (33, 160), (250, 4000 - 4000 % 32)):
+        p, _, _ = make_int4(rng, rows, cols, n, 32, port)
+        _check_product(egt, port, torch, p, rng, expect_path="tiled-mma.sp")
+
+
+@pytest.mark.parametrize("n", [1, 2])
+def test_general_path_any_group(egt, port, torch, n):
+    """Group sizes that do not sit on 32-column k-tiles, and cols % 32 != 0,
+    run on the reference-order CUDA-core kernel."""
+    rng = np.random.default_rng(31)
+    for rows, cols, g in ((7, 36, 4), (64, 512, 16), (40, 200, 48), (3, 8, 8), (128, 1000, 100)):
+        p, _, _ = make_int4(rng, rows, cols, n, g, port)
+        _check_product(egt, port, torch, p, rng, expect_path="general")
+
+
+@pytest.mark.parametrize("n", [1, 2])
+def test_sparse_fp16(egt, port, torch, n):
+    rng = np.random.default_rng(41)
+    for rows, cols in ((4096, 4096), (100, 96)):
+        p, _, _ = make_f16(rng, rows, cols, n, port)
+        d = _check_product(egt, port, torch, p, rng, expect_path="tiled-mma.sp")
+        assert d.format == f"fp16-{n}:4"
+    p, _, _ = make_f16(rng, 9, 36, n, port)
+    _check_product(egt, port, torch, p, rng, expect_path="general")
+
+
+def test_dense_int4(egt, port, torch):
+    """quant_dense_gemv semantics (packed.cpp:266-281)."""
+    rng = np.random.default_rng(51)
+    for rows, cols, g, path in ((4096, 4096, 128, "tiled-mma.sp"), (48, 96, 32, "tiled-mma.sp"),
+                                (20, 40, 8, "general")):
+        w = rng.uniform(-1, 1, (rows, cols)).astype(np.float32)
+        q = egt.quantize_matrix(w, g)
+        d = egt.DeviceMatrix.dense_i4(q)
+        assert d.path == path and d.format == "int4-dense"
+        x = rng.uniform(-1, 1, cols).astype(np.float32)
+        y = d.spmv(torch.from_numpy(x).cuda()).cpu().numpy()
+        from oracle.oracle import Quantized
+
+        qo = Quantized(rows, cols, q.group_sizes, q.group_offsets, q.scales, q.zero_points, q.codes)
+        ok, err = close(y, port.quant_dense_gemv(qo, x))
+        assert ok, err
+        vals, bits = d.dequant()
+        assert np.array_equal(vals.cpu().numpy().view(np.uint32), port.dequantize(qo).view(np.uint32))
+        assert np.unpackbits(bits, bitorder="little")[: rows * cols].all()
+
+
+@pytest.mark.parametrize("kind", ["int4-2", "int4-1", "fp16-2", "fp16-1", "int4-general"])
+def test_dequant_bit_exact(egt, port, torch, kind):
+    """The device copy of the encoding reproduces the reference's unpack bit
+    for bit: values (decode_value in f32) and the recovered keep mask."""
+    rng = np.random.default_rng(61)
+    for rows, cols in ((64, 512), (37, 160), (16, 32)):
+        if kind.startswith("int4-general"):
+            p, mask, _ = make_int4(rng, rows, cols + 4, 2, 12, port)
+        elif kind.startswith("int4"):
+            p, mask, _ = make_int4(rng, rows, cols, int(kind[-1]), 32, port)
+        else:
+            p, mask, _ = make_f16(rng, rows, cols, int(kind[-1]), port)
+        want_v, want_m = port.unpack(p)
+        got_v, got_m = _dev(egt, p).dequant()
+        assert np.array_equal(got_v.cpu().numpy().view(np.uint32), want_v.view(np.uint32))
+        assert np.array_equal(got_m, want_m)
+        assert np.array_equal(got_m, mask)
+
+
+@pytest.mark.parametrize("M", [2, 3, 4, 5, 8, 9, 16, 33])
+def test_multi_token(egt, port, torch, M):
+    """M-row products (the verify pass's skinny SpGEMM) per token vs oracle."""
+    rng = np.random.default_rng(71 + M)
+    p, _, _ = make_int4(rng, 528, 768, 2, 128, port)
+    _check_product(egt, port, torch, p, rng, M=M)
+    p, _, _ = make_int4(rng, 130, 256, 1, 64, port)
+    _check_product(egt, port, torch, p, rng, M=M)
+
+
+def test_row_shards_zero_copy(egt, port, torch):
+    rng = np.random.default_rng(81)
+    p, _, _ = make_int4(rng, 1024, 2048, 2, 128, port)
+    d = _dev(egt, p)
+    x = rng.uniform(-1, 1, p.cols).astype(np.float32)
+    xt = torch.from_numpy(x).cuda()
+    full = d.spmv(xt).cpu().numpy()
+    for G in (2, 4, 8):
+        per = p.rows // G
+        parts = [d.slice_rows(i * per, (i + 1) * per).spmv(xt).cpu().numpy() for i in range(G)]
+        assert close(np.concatenate(parts), full, 1e-5)[0]  # split-K plans may differ per shard
+    tail = d.slice_rows(1008, 1024).spmv(xt).cpu().numpy()
+    assert close(tail, full[1008:], 1e-5)[0]
+    with pytest.raises(egt.InvalidArgument):
+        d.slice_rows(8, 40)
+
+
+def test_host_drop_in_and_errors(egt, port, torch):
+    rng = np.random.default_rng(91)
+    p, _, _ = make_int4(rng, 300, 640, 2, 128, port)
+    x = rng.uniform(-1, 1, 640).astype(np.float32)
+    y = egt.spmv(to_product(p), x)
+    assert close(y, port.spmv(p, x))[0]
+    d = _dev(egt, p)
+    assert np.array_equal(d.spmv_host(x), d.spmv(torch.from_numpy(x).cuda()).cpu().numpy())
+    with pytest.raises(egt.InvalidArgument, match="input length differs from columns"):
+        d.spmv_host(np.ones(641, np.float32))
+    bad = to_product(p)
+    bad.index_words = bad.index_words.copy()
+    first = (int(bad.index_words[0]) >> 14) & 3
+    bad.index_words[0] = (int(bad.index_words[0]) & 0x0FFF) | (first << 14) | (first << 12)
+    with pytest.raises(egt.FormatError, match="offsets"):
+        egt.DeviceMatrix.from_packed(bad)
+    short = to_product(p)
+    short.value_bytes = short.value_bytes[:-1]
+    with pytest.raises(egt.FormatError, match="value byte count"):
+        egt.DeviceMatrix.from_packed(short)
+
+
+def test_empty_shapes(egt, port, torch):
+    rng = np.random.default_rng(101)
+    p, _, _ = make_int4(rng, 0, 64, 2, 32, port)
+    d = _dev(egt, p)
+    assert d.spmv_host(np.zeros(64, np.float32)).size == 0
+    p, _, _ = make_int4(rng, 5, 0, 2, 32, port)
+    d = _dev(egt, p)
+    assert np.array_equal(d.spmv_host(np.zeros(0, np.float32)), np.zeros(5, np.float32))
+
+
+def test_graph_replay_chain(egt, port, torch):
+    """A CUDA-graph-captured chain with PDL (y of one GEMV feeds the next)
+    equals eager execution, replayed several times (split-K counters reset)."""
+    rng = np.random.default_rng(111)
+    layers = [make_int4(rng, 4096, 4096, 2, 128, port)[0] for _ in range(3)]
+    ds = [_dev(egt, p) for p in layers]
+    x0 = torch.from_numpy(rng.uniform(-1, 1, 4096).astype(np.float32)).cuda()
+    bufs = [torch.empty(4096, device="cuda") for _ in range(3)]
+
+    def chain(x):
+        for d, b in zip(ds, bufs):
+            d.spmv_into(x, b)
+            x = b
+        return x
+
+    eager = chain(x0).clone()
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        chain(x0)  # warm-up allocates the workspace outside capture
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            chain(x0)
+    for _ in range(3):
+        g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(bufs[-1], eager)
+    want = x0.cpu().numpy()
+    for p in layers:
+        want = port.spmv(p, want)
+    assert close(eager.cpu().numpy(), want)[0]
+
+
+def test_effective_matrix_probe(egt, port, torch, tmp_path):
+    """X = I recovers the matrix the tensor cores actually multiply by; it
+    must equal the reference's unpack exactly (small integers x scale 1)."""
+    import json
+    import os
+
+    rng = np.random.default_rng(121)
+    for n in (2, 1):
+        rows, cols = 16, 128
+        p, _, _ = make_int4(rng, rows, cols, n, 128, port)
+        d = _dev(egt, p)
+        eye = torch.eye(cols, dtype=torch.float32, device="cuda")
+        w_eff = d.spmv(eye).cpu().numpy().T  # [rows x cols]
+        want, _ = port.unpack(p)
+        if not np.allclose(w_eff, want, rtol=1e-5, atol=1e-6):
+            out = os.path.join(os.environ.get("GRAFT_REPO_ROOT", "."), "gpurun_out")
+            os.makedirs(out, exist_ok=True)
+            with open(os.path.join(out, f"probe_n{n}.json"), "w") as f:
+                json.dump({"w_eff": w_eff.tolist(), "want": want.tolist()}, f)
+        assert np.allclose(w_eff, want, rtol=1e-5, atol=1e-6), f"n={n}: tensor-core layout mismatch"
