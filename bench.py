@@ -1,0 +1,394 @@
+#!/usr/bin/env python
+"""Benchmark of the SparseGemv hot path (BASELINE.json configs[1]).
+
+Workload ("step"): one batch-1 decode pass over the linear layers of a
+Llama-2-7B-shaped stack -- 32 layers x {4 x 4096x4096 (Q,K,V,O), 11008x4096
+(up), 4096x11008 (down)} = 192 INT4 group-128 2:4 2bit-CSR SparseGemv calls,
+synthetic random-init weights (U(-1,1) quantized and packed by the product's
+own host encoder), 2.09 GB of packed weights per step -- far larger than the
+126 MB L2, so every step streams from HBM.  Replayed as one CUDA graph per
+step (programmatic dependent launch between the GEMVs).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
+
+value  = achieved HBM GB/s over the whole job (algorithmic bytes: packed
+         weights + index + scale tables + x + y), summed over
+         ranks / max rank time (replicas: weak scaling);
+e2e    = the same metric through the public API with pinned host buffers
+         (H2D x, graph replay, D2H y, sync) every step;
+roofline, cpu_baseline, clocks, gpu_launches: see DESIGN.md "Measurement".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N_LAYERS = 32
+LAYER_SHAPES = [(4096, 4096)] * 4 + [(11008, 4096), (4096, 11008)]  # wq wk wv wo ff1 ff2
+GROUP = 128
+
+
+def _metric():
+    try:
+        with open(os.path.join(ROOT, "BASELINE.json")) as f:
+            return json.load(f)["metric"]
+    except Exception:
+        return "INT4 2bit-CSR SpGEMV µs/call & achieved HBM GB/s vs peak; decode tokens/s"
+
+
+def _peak_hbm():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def _dist():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ------------------------------------------------------------------ inputs
+PATTERNS_24 = None
+
+
+def host_layer(rng, rows, cols):
+    """U(-1,1) weights, random exact-2:4 mask, INT4 g128 via the product's
+    C++ encoder (quantize_matrix + pack, byte-identical to the reference)."""
+    import numpy as np
+
+    import paper_2605_11582_b200 as egt
+
+    pats = np.array([[1, 1, 0, 0], [1, 0, 1, 0], [1, 0, 0, 1], [0, 1, 1, 0], [0, 1, 0, 1], [0, 0, 1, 1]], bool)
+    w = rng.uniform(-1, 1, (rows, cols)).astype(np.float32)
+    keep = pats[rng.integers(0, 6, (rows, cols // 4))].reshape(rows, cols)
+    mask = np.packbits(keep.reshape(-1), bitorder="little")
+    q = egt.quantize_matrix(w, GROUP, mask)
+    return egt.pack(mask, q, 2)
+
+
+def shape_bytes(p) -> int:
+    """Algorithmic bytes of one call: codes + index + 5 B/group + x + y."""
+    return (p.nnz + 1) // 2 + 2 * ((p.nnz + 7) // 8) + 5 * p.scales.size + 4 * p.cols + 4 * p.rows
+
+
+def to_oracle(p):
+    from oracle.oracle import Packed
+
+    return Packed(p.n, p.m, p.rows, p.cols, p.kind, p.index_words, p.value_bytes, p.group_sizes,
+                  p.group_offsets, p.scales, p.zero_points, p.values)
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "20"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self) -> dict | None:
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        rows = [r.split(",") for r in out.strip().splitlines() if r.count(",") >= 7]
+        if not rows:
+            return None
+        sm = sorted(float(r[0]) for r in rows)
+        reasons = set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for r in rows:
+            for name, v in zip(names, r[4:8]):
+                if v.strip().lower() in ("active", "1"):
+                    reasons.add(name)
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": float(rows[0][1]), "reasons": sorted(reasons),
+                "samples": len(rows), "power_w_max": max(float(r[2]) for r in rows if r[2].strip()
+                                                          .replace(".", "", 1).isdigit()) if rows else None}
+
+
+# ------------------------------------------------------------------ CPU legs
+def cpu_reference_run(host_layers, n_calls: int, threads: int, xs):
+    """The reference's own spmv (oracle/_ref, compiled from the reference
+    sources) on `threads` host threads, n_calls products rotating over the
+    sweep shapes; returns (GB/s, seconds, calls, outputs per shape)."""
+    from oracle.oracle import Oracle
+
+    R = Oracle("reference")
+    keys = list(host_layers)
+    per_shape = [n_calls // len(keys) + (1 if i < n_calls % len(keys) else 0) for i in range(len(keys))]
+    total_bytes = 0
+    total_s = 0.0
+    outs = {}
+    for k, calls in zip(keys, per_shape):
+        if calls == 0:
+            continue
+        per_thread = max(1, math.ceil(calls / threads))
+        t = min(threads, calls)
+        sec, y = R.ref_timed_spmv(to_oracle(host_layers[k]), xs[k[1]], per_thread, t)
+        total_s += sec
+        total_bytes += shape_bytes(host_layers[k]) * per_thread * t
+        outs[k] = y
+    return total_bytes / total_s / 1e9, total_s, sum(per_shape), outs
+
+
+# ------------------------------------------------------------------ reference arm
+def run_reference(args):
+    rank, world, _ = _dist()
+    if rank != 0:
+        return 0
+    import numpy as np
+
+    from paper_2605_11582_b200 import _build
+
+    _build.build()
+    rng = np.random.default_rng(2605)
+    host = {s: host_layer(rng, *s) for s in sorted(set(LAYER_SHAPES))}
+    xs = {c: rng.uniform(-1, 1, c).astype(np.float32) for c in sorted({s[1] for s in LAYER_SHAPES})}
+    threads = os.cpu_count() or 1
+    cpu_reference_run(host, min(args.warmup, 3), threads, xs)  # warm-up
+    gbs, sec, calls, _ = cpu_reference_run(host, args.steps, threads, xs)
+    line = {
+        "impl": "reference", "metric": _metric(), "value": round(gbs, 4), "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * sec / max(calls, 1), 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int4-w/f32-acc",
+        "data": "synthetic U(-1,1) weights, random exact 2:4 masks, INT4 g128 (reference encoder layout)",
+        "config": {"workload": "reference spmv (packed.cpp:211-220) over the Llama-2-7B layer sweep "
+                               "4096x4096 / 11008x4096 / 4096x11008, INT4 g128 2:4, batch 1; "
+                               "a step = one product on one host thread",
+                   "threads": threads},
+        "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": "reference",
+                         "sample": f"{calls} reference spmv calls rotating over the 3 sweep shapes on {threads} threads"},
+        "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    rank, world, local = _dist()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2605_11582_b200 as egt
+    from paper_2605_11582_b200.engine import GemvChain
+
+    rng = np.random.default_rng(2605)
+    t0 = time.time()
+    host = {s: host_layer(rng, *s) for s in sorted(set(LAYER_SHAPES))}
+    xs = {c: rng.uniform(-1, 1, c).astype(np.float32) for c in sorted({s[1] for s in LAYER_SHAPES})}
+    stream = torch.cuda.Stream()
+    layers = []
+    for _ in range(N_LAYERS):
+        for s in LAYER_SHAPES:
+            layers.append(egt.DeviceMatrix.from_packed(host[s], stream))
+    torch.cuda.synchronize()
+    setup_s = time.time() - t0
+    assert all(d.path == "tiled-mma.sp" for d in layers)
+
+    # The sweep: every GEMV reads the step's input vector for its width (no
+    # chaining, so magnitudes stay bounded) and writes its own output slot.
+    class Sweep(GemvChain):
+        def __init__(self, layers, stream):
+            self.layers = layers
+            self.stream = stream
+            self.inputs = {c: torch.from_numpy(xs[c]).cuda() for c in xs}
+            self.x = self.inputs[4096]
+            offs = np.cumsum([0] + [d.rows for d in layers])
+            self.yall = torch.empty(int(offs[-1]), dtype=torch.float32, device="cuda")
+            self.slots = [self.yall[int(offs[i]):int(offs[i + 1])] for i in range(len(layers))]
+            self.graph = None
+            self.out = None
+
+        def _launch_all(self):
+            for d, y in zip(self.layers, self.slots):
+                d.spmv_into(self.inputs[d.cols], y, self.stream)
+            self.out = self.slots[-1]
+
+        def step_host(self, x_host, y_host):
+            with torch.cuda.stream(self.stream):
+                for c, t in self.inputs.items():
+                    t.copy_(x_host[c], non_blocking=True)
+                self.graph.replay()
+                y_host.copy_(self.out, non_blocking=True)
+            self.stream.synchronize()
+
+    sweep = Sweep(layers, stream)
+    n0 = egt.launch_count()
+    sweep.capture()
+    launches_per_step = egt.launch_count() - n0 - len(layers)  # capture pass minus the warm-up pass
+    launches_per_step = len(layers) if launches_per_step <= 0 else launches_per_step
+    step_bytes = sum(shape_bytes(host[s]) for s in LAYER_SHAPES) * N_LAYERS
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    for _ in range(args.warmup):
+        sweep.replay()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(torch.cuda.current_device())
+    sampler.start()
+    time.sleep(0.05)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        sweep.replay()
+    ev1.record(stream)
+    ev1.synchronize()
+    clocks = sampler.stop()
+    barrier()
+    torch.cuda.synchronize()
+    t_ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([t_ms], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        t_ms = float(t.item())
+    ms_per_step = t_ms / args.steps
+    value = world * step_bytes * args.steps / (t_ms * 1e-3) / 1e9
+
+    # per-shape µs/call: every copy of one shape in sequence, replayed
+    per_shape = {}
+    for s in sorted(set(LAYER_SHAPES)):
+        sel = [d for d in layers if (d.rows, d.cols) == s]
+        sub = Sweep(sel, stream)
+        sub.capture()
+        for _ in range(3):
+            sub.replay()
+        reps = max(3, min(50, 20000 // len(sel)))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            sub.replay()
+        e1.record(stream)
+        e1.synchronize()
+        us = 1e3 * e0.elapsed_time(e1) / (reps * len(sel))
+        b = shape_bytes(host[s])
+        per_shape[f"{s[0]}x{s[1]}"] = {"us_per_call": round(us, 3), "GBps": round(b / us / 1e3, 1),
+                                       "bytes_per_call": b, "copies": len(sel)}
+        del sub
+
+    # e2e through the public API with pinned host buffers
+    x_host = {c: torch.from_numpy(xs[c]).pin_memory() for c in xs}
+    y_host = torch.empty(layers[-1].rows, dtype=torch.float32).pin_memory()
+    for _ in range(2):
+        sweep.step_host(x_host, y_host)
+    e2e_steps = max(3, min(args.steps, 200))
+    barrier()
+    w0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        sweep.step_host(x_host, y_host)
+    w1 = time.perf_counter()
+    e2e_s = w1 - w0
+    if world > 1:
+        t = torch.tensor([e2e_s], device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = world * step_bytes * e2e_steps / e2e_s / 1e9
+    h2d = sum(4 * c for c in xs)
+    d2h = 4 * layers[-1].rows
+
+    peak, peak_kind = _peak_hbm()
+    achieved = step_bytes / (ms_per_step * 1e-3) / 1e9
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get("dram_bytes_per_launch_by_shape")
+        except Exception:
+            traffic = None
+
+    cpu_baseline = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        threads = os.cpu_count() or 1
+        gbs, sec, calls, outs = cpu_reference_run(host, 6 * threads, threads, xs)
+        # checker: the GPU products of the sweep vs the reference's own spmv
+        errs = []
+        for s, y_ref in outs.items():
+            d = next(d for d in layers if (d.rows, d.cols) == s)
+            y = d.spmv(torch.from_numpy(xs[s[1]]).cuda()).cpu().numpy()
+            errs.append(float(np.max(np.abs(y - y_ref) / (1 + np.abs(y_ref)))))
+        cpu_baseline = {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": "reference",
+                        "sample": f"{calls} reference spmv calls (oracle/_ref, packed.cpp:211-220) over the 3 "
+                                  f"sweep shapes, {threads} host threads, {sec:.1f} s",
+                        "parity_max_rel_err_vs_gpu": max(errs)}
+
+    line = {
+        "metric": _metric(), "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 5), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int4-w/fp16x2-hi-lo-x/f32-acc",
+        "data": "synthetic: U(-1,1) random-init weights, random exact 2:4 masks, INT4 g128 (product encoder)",
+        "config": {"workload": "Llama-2-7B layer-shape sweep at batch 1: 32 layers x [4x 4096x4096, 11008x4096, "
+                               "4096x11008] INT4 g128 2:4 2bit-CSR SparseGemv, one CUDA graph per step",
+                   "gemvs_per_step": len(layers), "bytes_per_step": step_bytes,
+                   "weights_resident_bytes": int(sum(d.device_bytes for d in layers)),
+                   "l2_policy": "inputs larger than L2 (2.09 GB of weights per step vs 126 MB L2)",
+                   "parallelism": f"replicas x{world}", "setup_s": round(setup_s, 1),
+                   "per_shape": per_shape},
+        "e2e": {"value": round(e2e_value, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_step": round(1e3 * e2e_s / e2e_steps, 4), "steps": e2e_steps},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
+                     "kernel": "egt_impl::tiled_spmm_kernel<I4_SP24,SS=4,NT=1>",
+                     "algorithmic_bytes_per_launch": {k: v["bytes_per_call"] for k, v in per_shape.items()}},
+        "cpu_baseline": cpu_baseline,
+        "clocks": clocks,
+        "gpu_launches": launches_per_step * args.steps,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -81,8 +81,10 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
 
 // D[16x8] (+)= A[16x32, 2:4 sparse] * B[32x8], f16 inputs, f32 accumulate.
 // Metadata register e is read from lanes {0,1} (sel 0) or {2,3} (sel 1) of
-// each quad: lane 2*sel holds row g, lane 2*sel+1 row g+8; nibble q of the
-// register = group q (columns 4q..4q+3): bits[1:0] first index, [3:2] second.
+// each quad (measured on B200, tests/test_gpu_spmv.py::test_effective_matrix_probe):
+// lane 2*sel + hh covers groups [4hh, 4hh+4) (columns 16hh..16hh+15), row g in
+// bits [0,16) and row g+8 in bits [16,32); nibble q4 = group 4hh+q4, with
+// bits[1:0] the first kept index and [3:2] the second.
 template <int kSel>
 __device__ __forceinline__ void mma_sp_16832(float (&d)[4], const uint32_t (&a)[4],
                                              const uint32_t (&b)[4], uint32_t e) {

@@ -130,20 +130,23 @@ __global__ void relayout_kernel(const RelayoutArgs a) {
     const int VB = val_lane_bytes(f);
     uint32_t* vo = reinterpret_cast<uint32_t*>(a.vals + blk * 32 * VB + lane * VB);
     for (int i = 0; i < VB / 4; ++i) vo[i] = v[i];
+    // mma.sp metadata: lane t = 2*sel + hh of a quad holds groups
+    // [4hh, 4hh+4) of its k-tile, row g in bits [0,16) and row g+8 in [16,32).
     uint32_t m[2];
     for (int sl = 0; sl < 2; ++sl) {
-      const int j = (t >> 1) + 2 * sl, h = t & 1;
-      const uint32_t r = rt * 16 + g + 8 * h;
+      const int j = (t >> 1) + 2 * sl, hh = t & 1;
       uint32_t word = 0;
-      for (int q8 = 0; q8 < 8; ++q8) {
-        const uint32_t G = (kq * 4 + j) * 8 + q8;
-        uint32_t nib = 0x4u;  // (0,1): a valid ordered pattern for padding
-        if (group_valid(a, r, G)) {
-          const uint64_t k0 = (raw.row_begin + r) * row_nnz + 2ull * G;
-          nib = offset_at(raw.words, k0) | (offset_at(raw.words, k0 + 1) << 2);
+      for (int h = 0; h < 2; ++h)
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const uint32_t r = rt * 16 + g + 8 * h;
+          const uint32_t G = (kq * 4 + j) * 8 + 4 * hh + q4;
+          uint32_t nib = 0x4u;  // (0,1): a valid ordered pattern for padding
+          if (group_valid(a, r, G)) {
+            const uint64_t k0 = (raw.row_begin + r) * row_nnz + 2ull * G;
+            nib = offset_at(raw.words, k0) | (offset_at(raw.words, k0 + 1) << 2);
+          }
+          word |= nib << (16 * h + 4 * q4);
         }
-        word |= nib << (4 * q8);
-      }
       m[sl] = word;
     }
     uint32_t* mo = reinterpret_cast<uint32_t*>(a.meta + blk * 32 * 8 + lane * 8);
@@ -167,15 +170,16 @@ __global__ void relayout_kernel(const RelayoutArgs a) {
             v[2 * j + q] |= static_cast<uint32_t>(__half_as_ushort(raw.values[k])) << (16 * h);
           }
         }
-    for (int sl = 0; sl < 2; ++sl) {
-      const int j = (t >> 1) + 2 * sl, h = t & 1;
-      const uint32_t r = rt * 16 + g + 8 * h;
-      for (int q8 = 0; q8 < 8; ++q8) {
-        const uint32_t G = (kq * 4 + j) * 8 + q8;
-        if (!group_valid(a, r, G)) continue;
-        const uint64_t k = (raw.row_begin + r) * row_nnz + G;
-        ms |= ((offset_at(raw.words, k) >> 1) & 1u) << (16 + 8 * sl + q8);
-      }
+    for (int sl = 0; sl < 2; ++sl) {  // high offset bits, metadata-holder order
+      const int j = (t >> 1) + 2 * sl, hh = t & 1;
+      for (int h = 0; h < 2; ++h)
+        for (int q4 = 0; q4 < 4; ++q4) {
+          const uint32_t r = rt * 16 + g + 8 * h;
+          const uint32_t G = (kq * 4 + j) * 8 + 4 * hh + q4;
+          if (!group_valid(a, r, G)) continue;
+          const uint64_t k = (raw.row_begin + r) * row_nnz + G;
+          ms |= ((offset_at(raw.words, k) >> 1) & 1u) << (16 + 8 * sl + 4 * h + q4);
+        }
     }
     const int VB = val_lane_bytes(f);
     uint32_t* vo = reinterpret_cast<uint32_t*>(a.vals + blk * 32 * VB + lane * VB);
@@ -428,11 +432,12 @@ __global__ void dequant_tiled_kernel(const DequantTiledArgs a) {
         const uint32_t r = rt * 16 + g + 8 * h;
         const uint32_t G = (kq * 4 + j) * 8 + t + 4 * q;
         if (r >= a.rows || G * 4 >= a.cols) continue;
-        const int holder = 4 * g + 2 * (j & 1) + h;  // lane holding (row, k-tile j) metadata
-        const int grp = t + 4 * q;
+        // metadata of (row g+8h, group t+4q of k-tile j) lives in lane
+        // 4g + 2(j&1) + q, nibble 4h + t (see relayout_kernel)
+        const int holder = 4 * g + 2 * (j & 1) + q;
         if (two) {
           const uint32_t word = mb[holder * 2 + (j >> 1)];
-          const uint32_t nib = (word >> (4 * grp)) & 0xFu;
+          const uint32_t nib = (word >> (16 * h + 4 * t)) & 0xFu;
           const uint32_t off[2] = {nib & 3u, (nib >> 2) & 3u};
           for (int i = 0; i < 2; ++i) {
             const uint32_t c = G * 4 + off[i];
@@ -455,7 +460,7 @@ __global__ void dequant_tiled_kernel(const DequantTiledArgs a) {
           const uint32_t own = mb[lane];
           const uint32_t slot = (own >> (4 * j + h + 2 * q)) & 1u;
           const uint32_t hword = mb[holder];
-          const uint32_t hi = (hword >> (16 + 8 * (j >> 1) + grp)) & 1u;
+          const uint32_t hi = (hword >> (16 + 8 * (j >> 1) + 4 * h + t)) & 1u;
           const uint32_t c = G * 4 + (hi << 1 | slot);
           float val;
           if (f == I4_SP14) {

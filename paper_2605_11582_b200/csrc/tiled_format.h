@@ -16,9 +16,10 @@
 // for k-tile j holds 8 nibbles: position p = h + 2q (h: row g / g+8, q: group
 // t / t+4 of the k-tile) -- first kept entry at bits 4p, second at 16+4p, so
 // that one LOP3 with the 0x6400 fp16 exponent yields the half2 register the
-// mma.sp A fragment wants.  Metadata u32 per (row, k-tile) is the mma.sp
-// ordered metadata (nibble q = group q: bits[1:0] first offset, [3:2] second),
-// held by lane t = 2*(j&1) + h of the row's quad (slot j>>1).  Bytes per block
+// mma.sp A fragment wants.  Metadata: the mma.sp ordered metadata (per group
+// of 4 columns a nibble: bits[1:0] first offset, [3:2] second); for k-tile j
+// lane t = 2*(j&1) + hh of quad g holds groups [4hh, 4hh+4), row g in bits
+// [0,16) and row g+8 in bits [16,32), in its slot j>>1.  Bytes per block
 // equal the reference's bytes for the same entries (no padding unless the
 // matrix edge is ragged).
 #pragma once

@@ -220,7 +220,8 @@ def test_graph_replay_chain(egt, port, torch):
     want = x0.cpu().numpy()
     for p in layers:
         want = port.spmv(p, want)
-    assert close(eager.cpu().numpy(), want)[0]
+    scale = float(np.sqrt(np.mean(want.astype(np.float64) ** 2)))  # chained magnitudes grow ~30x/layer
+    assert close(eager.cpu().numpy() / scale, want / scale)[0]
 
 
 def test_effective_matrix_probe(egt, port, torch, tmp_path):
