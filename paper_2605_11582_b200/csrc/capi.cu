@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -449,7 +450,15 @@ egt_status egt_spmv(const egt_dev_packed* h, const float* x, float* y, uint32_t 
   {
     std::lock_guard<std::mutex> lk(h->plan_mu);
     auto it = h->plans.find(static_cast<int>(M));
-    if (it == h->plans.end()) it = h->plans.emplace(static_cast<int>(M), plan_tiled(h, M, num_sms())).first;
+    if (it == h->plans.end()) {
+      it = h->plans.emplace(static_cast<int>(M), plan_tiled(h, M, num_sms())).first;
+      if (getenv("EGT_DEBUG_PLAN")) {
+        const TiledSchedule& p = it->second;
+        fprintf(stderr, "[egt plan] %ux%u fmt=%d M=%u: RB=%d WK=%d nw=%d KC=%d S=%d NT=%d grid=(%d,%d,%d) smem=%zu\n",
+                h->rows, h->cols, h->format, M, p.RB, p.WK, p.nw, p.KC, p.S, p.NT, p.grid_x, p.grid_y,
+                p.grid_z, p.smem);
+      }
+    }
     sc = it->second;
   }
   if (sc.S > 1) {

@@ -230,101 +230,124 @@ __device__ __forceinline__ void compute_unit(const Unit<FMT, 4 / SS>& u, const u
   }
 }
 
-// One CTA = RB row tiles x KC k-quads x 4*NT tokens.  Warp (wi, wj) owns row
-// tile wi over the wj-th part of the CTA's k-quads and streams its units
-// through a D-deep register pipeline (weight loads are issued before the PDL
-// wait: they do not depend on the previous kernel).  Split-K partial sums
-// (S > 1) are reduced by the last-arriving CTA of each row block, in slice
-// order, so the result is deterministic.
+// One CTA = RB row tiles x KC k-quads x 4*NT tokens, nw = blockDim/32 warps
+// arranged as RBw = nw/WK warp rows x WK warp columns.  Warp (wi, wj) owns
+// row tiles wi, wi+RBw, ... over the wj-th part of the CTA's k-quads and
+// streams its units (row tile, k-quad) through a D-deep register pipeline;
+// the first D units are requested before the PDL wait (weights do not depend
+// on the previous kernel).  Split-K partial sums (S > 1) are reduced by the
+// last-arriving CTA of each row block, in slice order: deterministic.
 template <int FMT, int SS, int NT, int D>
-__global__ void __launch_bounds__(512, 1) tiled_spmm_kernel(const TiledArgs a) {
+__global__ void __launch_bounds__(256, 2) tiled_spmm_kernel(const TiledArgs a) {
   constexpr int E = 4 / SS;
+  constexpr int TOK = 4 * NT;                       // tokens per CTA (power of two)
+  constexpr int TOK_SHIFT = NT == 1 ? 2 : (NT == 2 ? 3 : 4);
   extern __shared__ __align__(16) uint32_t smem[];
   pdl_launch_dependents();
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int nwarps = a.RB * a.WK;
+  const int nw = blockDim.x >> 5;
+  const int RBw = nw / a.WK;
   const int wi = warp / a.WK, wj = warp % a.WK;
-  const int rt = blockIdx.x * a.RB + wi;
-  const bool rt_ok = rt < a.RT;
+  const int rt0 = blockIdx.x * a.RB;
+  const int RBc = min(a.RB, a.RT - rt0);
   const int kq0 = blockIdx.y * a.KC;
   const int kq1 = min(a.KQ, kq0 + a.KC);
   const int KTc = (kq1 - kq0) * 4;
   const int per = (kq1 - kq0 + a.WK - 1) / a.WK;
-  const int k0 = kq0 + wj * per;
-  const int k1 = min(kq1, k0 + per);
-  const int nU = rt_ok ? max(0, k1 - k0) : 0;
-  const int m0 = blockIdx.z * 4 * NT;
+  const int k0 = min(kq1, kq0 + wj * per);
+  const int nK = max(0, min(kq1, k0 + per) - k0);
+  const int nR = wi < RBc ? (RBc - wi + RBw - 1) / RBw : 0;
+  const int nU = nR * nK;
+  const int m0 = blockIdx.z * TOK;
   const int M_left = a.M - m0;
+  const int rt_base = a.rt_begin + rt0 + wi;  // storage row tile of the warp's first unit
 
   const uint64_t pol = evict_first_policy();
   Unit<FMT, E> buf[D];
+  int lr = 0, lk = 0;  // (row iteration, k-quad) of the next unit to load
 #pragma unroll
-  for (int s = 0; s < D; ++s)
-    if (s < nU) load_unit<FMT, E>(buf[s], a, a.rt_begin + rt, k0 + s, lane, pol);
+  for (int s = 0; s < D; ++s) {
+    if (s < nU) {
+      load_unit<FMT, E>(buf[s], a, rt_base + lr * RBw, k0 + lk, lane, pol);
+      if (++lk == nK) { lk = 0; ++lr; }
+    }
+  }
 
-  pdl_wait();  // x and the workspace are written by earlier kernels
+  pdl_wait();  // x and the split-K workspace belong to earlier kernels
 
-  // x slice -> fp16 hi/lo B fragments: sB[nt][kt][lane][4].
+  // x slice -> fp16 hi/lo B fragments sB[nt][kt][lane][4]: token m's hi part
+  // is B column 2m (lanes 8m..8m+3), its lo part (the rounding residual)
+  // column 2m+1.  Only the lanes of present tokens are written (load_b skips
+  // the others).
   uint32_t* sB = smem;
   const int nB = NT * KTc * 128;
-  for (int idx = tid; idx < nB; idx += blockDim.x) {
-    const int reg = idx & 3, ln = (idx >> 2) & 31, rest = idx >> 7;
-    const int kt = rest % KTc, nt = rest / KTc;
-    const int col = ln >> 2, t = ln & 3;
-    const int tok = m0 + 4 * nt + (col >> 1);
-    const int k = (kq0 * 4 + kt) * 32 + 2 * t + 8 * reg;
-    float v0 = 0.f, v1 = 0.f;
-    if (tok < a.M && k < a.cols) {
-      const float* xp = a.x + static_cast<size_t>(tok) * a.ldx + k;
-      v0 = xp[0];
-      v1 = xp[1];
+#pragma unroll
+  for (int nt = 0; nt < NT; ++nt) {
+    const int items = KTc * 64;
+    for (int i = tid; i < items; i += blockDim.x) {
+      const int reg = i & 3, t = (i >> 2) & 3, m = (i >> 4) & 3, kt = i >> 6;
+      const int tok = m0 + 4 * nt + m;
+      if (tok >= a.M) continue;
+      const int k = (kq0 * 4 + kt) * 32 + 2 * t + 8 * reg;
+      float v0 = 0.f, v1 = 0.f;
+      if (k < a.cols) {
+        const float* xp = a.x + static_cast<size_t>(tok) * a.ldx + k;
+        v0 = xp[0];
+        v1 = xp[1];
+      }
+      const __half h0 = __float2half_rn(v0), h1 = __float2half_rn(v1);
+      const __half l0 = __float2half_rn(v0 - __half2float(h0));
+      const __half l1 = __float2half_rn(v1 - __half2float(h1));
+      uint32_t* row = sB + static_cast<size_t>(nt * KTc + kt) * 128;
+      row[(8 * m + t) * 4 + reg] = static_cast<uint32_t>(__half_as_ushort(h0)) |
+                                   (static_cast<uint32_t>(__half_as_ushort(h1)) << 16);
+      row[(8 * m + 4 + t) * 4 + reg] = static_cast<uint32_t>(__half_as_ushort(l0)) |
+                                       (static_cast<uint32_t>(__half_as_ushort(l1)) << 16);
     }
-    __half h0 = __float2half_rn(v0), h1 = __float2half_rn(v1);
-    if (col & 1) {  // lo part: the rounding residual of the hi part
-      h0 = __float2half_rn(v0 - __half2float(h0));
-      h1 = __float2half_rn(v1 - __half2float(h1));
-    }
-    sB[idx] = static_cast<uint32_t>(__half_as_ushort(h0)) |
-              (static_cast<uint32_t>(__half_as_ushort(h1)) << 16);
   }
+  float* red = reinterpret_cast<float*>(smem + nB);  // [RB][WK][TOK][16]
+  const int nRed = a.RB * a.WK * TOK * 16;
+  for (int i = tid; i < nRed; i += blockDim.x) red[i] = 0.f;
   __syncthreads();
 
   float acc[NT][2];
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = 0.f;
-
+  int cr = 0, ck = 0;  // (row iteration, k-quad) of the unit being computed
+  const int g = lane >> 2, t = lane & 3;
   for (int base = 0; base < nU; base += D) {
 #pragma unroll
     for (int s = 0; s < D; ++s) {
-      const int u = base + s;
-      if (u < nU) {
-        compute_unit<FMT, SS, NT>(buf[s], sB, KTc, (k0 + u - kq0) * 4, lane, M_left, acc);
-        if (u + D < nU) load_unit<FMT, E>(buf[s], a, a.rt_begin + rt, k0 + u + D, lane, pol);
-      }
-    }
-  }
-
-  // Intra-CTA reduction over the WK warps of each row tile (fixed order).
-  float* red = reinterpret_cast<float*>(smem + nB);  // [wi][wj][4NT tokens][16 rows]
-  {
-    const int g = lane >> 2, t = lane & 3;
-    float* r = red + (static_cast<size_t>(wi) * a.WK + wj) * (4 * NT * 16);
+      if (base + s < nU) {
+        compute_unit<FMT, SS, NT>(buf[s], sB, KTc, (k0 + ck - kq0) * 4, lane, M_left, acc);
+        if (base + s + D < nU) {
+          load_unit<FMT, E>(buf[s], a, rt_base + lr * RBw, k0 + lk, lane, pol);
+          if (++lk == nK) { lk = 0; ++lr; }
+        }
+        if (++ck == nK) {  // row tile done: park its partial sums in smem
+          float* r = red + ((static_cast<size_t>(wi + cr * RBw) * a.WK + wj) * TOK) * 16;
 #pragma unroll
-    for (int nt = 0; nt < NT; ++nt) {
-      r[(4 * nt + t) * 16 + g] = acc[nt][0];
-      r[(4 * nt + t) * 16 + g + 8] = acc[nt][1];
+          for (int nt = 0; nt < NT; ++nt) {
+            r[(4 * nt + t) * 16 + g] = acc[nt][0];
+            r[(4 * nt + t) * 16 + g + 8] = acc[nt][1];
+            acc[nt][0] = acc[nt][1] = 0.f;
+          }
+          ck = 0;
+          ++cr;
+        }
+      }
     }
   }
   __syncthreads();
 
   const int rows_pad = a.RT * 16;
-  const int nOut = a.RB * 4 * NT * 16;
+  const int nOut = RBc * TOK * 16;
   for (int idx = tid; idx < nOut; idx += blockDim.x) {
-    const int row16 = idx & 15, tl = (idx >> 4) % (4 * NT), i = idx / (64 * NT);
+    const int row16 = idx & 15, tl = (idx >> 4) & (TOK - 1), i = idx >> (4 + TOK_SHIFT);
     float v = 0.f;
-    for (int j = 0; j < a.WK; ++j) v += red[((static_cast<size_t>(i) * a.WK + j) * 4 * NT + tl) * 16 + row16];
-    const int row = (blockIdx.x * a.RB + i) * 16 + row16;
+    for (int j = 0; j < a.WK; ++j) v += red[((static_cast<size_t>(i) * a.WK + j) * TOK + tl) * 16 + row16];
+    const int row = (rt0 + i) * 16 + row16;
     const int tok = m0 + tl;
     if (row < a.rows && tok < a.M) {
       if (a.S == 1)
@@ -344,18 +367,17 @@ __global__ void __launch_bounds__(512, 1) tiled_spmm_kernel(const TiledArgs a) {
   if (!s_last) return;
   __threadfence();
   for (int idx = tid; idx < nOut; idx += blockDim.x) {
-    const int row16 = idx & 15, tl = (idx >> 4) % (4 * NT), i = idx / (64 * NT);
-    const int row = (blockIdx.x * a.RB + i) * 16 + row16;
+    const int row16 = idx & 15, tl = (idx >> 4) & (TOK - 1), i = idx >> (4 + TOK_SHIFT);
+    const int row = (rt0 + i) * 16 + row16;
     const int tok = m0 + tl;
     if (row < a.rows && tok < a.M) {
       float v = 0.f;
-      for (int s = 0; s < a.S; ++s)
-        v += __ldcg(a.partial + (static_cast<size_t>(s) * a.M + tok) * rows_pad + row);
+      for (int sidx = 0; sidx < a.S; ++sidx)
+        v += __ldcg(a.partial + (static_cast<size_t>(sidx) * a.M + tok) * rows_pad + row);
       a.y[static_cast<size_t>(tok) * a.ldy + row] = v;
     }
   }
   if (tid == 0) a.counters[cidx] = 0u;  // ready for the next launch / graph replay
-  (void)nwarps;
 }
 
 // ---------------------------------------------------------------- planning
@@ -402,54 +424,68 @@ size_t block_bytes(const egt_dev_packed* h) {
   if (has_scales(f)) b += 16u * 5u * h->tiled.E;
   return b;
 }
+
+size_t smem_bytes(int NT, int KC, int RB, int WK) {
+  return static_cast<size_t>(NT) * KC * 4 * 512 + static_cast<size_t>(RB) * WK * 4 * NT * 16 * 4;
+}
 }  // namespace
 
-// Chooses the CTA tile (RB row tiles x KC k-quads, WK warps per row tile)
-// and split-K factor S minimising a simple model of the slowest SM's bytes
-// plus the x-slice and partial-sum traffic, for grids that fill 148 SMs.
+// Picks the CTA tile (RB row tiles x KC k-quads, nw warps as RBw x WK) and the
+// split-K factor S with a small model of one launch: the busiest SM's HBM
+// bytes at its 1/148 share of bandwidth, the per-scheduler issue time of the
+// dequant + mma.sp stream, the number of waves, and a fixed tail for the
+// split-K reduction.  Everything is resident in one wave whenever possible
+// (2 CTAs/SM leave room for the next kernel's CTAs under PDL).
 TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms) {
   TiledSchedule best;
   const int RT = h->tiled.RT, KQ = h->tiled.KQ;
   const int NT = M <= 4 ? 1 : (M <= 8 ? 2 : 4);
   const int NB = (M + 4 * NT - 1) / (4 * NT);
-  const double bb = static_cast<double>(block_bytes(h));
+  const int tok = std::min(M, 4 * NT);
+  const double unit_b = static_cast<double>(block_bytes(h));
+  const double sm_bw = 44.0;          // B/ns per SM (6.5 TB/s / 148)
+  const double unit_cycles = 60.0 * NT;  // issue slots per (warp, unit)
+  void* fn = pick_kernel(h->format, h->tiled.SS, NT);
   double best_cost = 1e300;
-  for (int S = 1; S <= KQ && S <= 16; ++S) {
+  for (int S = 1; S <= std::min(KQ, 8); ++S) {
     const int KC = (KQ + S - 1) / S;
-    if (S > 1 && (S - 1) * KC >= KQ) continue;  // empty last slice
-    if (NT * KC * 2048 > 160 * 1024) continue;  // x fragments must fit in smem
-    for (int RB = 1; RB <= 16; ++RB) {
-      for (int WK = 1; WK * RB <= 16; ++WK) {
-        if (WK > KC) break;
-        const int warps = RB * WK;
-        if (warps < 4 && RT * S * NB >= 4 * num_sms) continue;
-        const long ctas = static_cast<long>((RT + RB - 1) / RB) * S * NB;
-        // resident CTAs per SM: smem and warps bound
-        const size_t smem = static_cast<size_t>(NT) * KC * 2048 + static_cast<size_t>(RB) * WK * NT * 256;
-        int per_sm = std::min(64 / warps, static_cast<int>((200 * 1024) / (smem + 1024)));
-        per_sm = std::max(1, std::min(per_sm, 8));
-        const double waves = std::ceil(static_cast<double>(ctas) / (static_cast<double>(num_sms) * per_sm));
-        // bytes per CTA: its weight blocks (worst case), its x slice, partials
-        const double w_bytes = static_cast<double>(RB) * KC * bb;
-        const double x_bytes = static_cast<double>(KC) * 512.0 * std::min(M, 4 * NT);
-        const double p_bytes = S > 1 ? 2.0 * RB * 16 * 4 * std::min(M, 4 * NT) : 0.0;
-        const double per_sm_bytes = waves * per_sm * (w_bytes + x_bytes + p_bytes);
-        // per-warp serial latency: units per warp beyond what D hides
-        const double units_per_warp = std::ceil(static_cast<double>(KC) / WK);
-        const double lat = units_per_warp * 40.0 * waves;  // ~40 B-equivalent per unit of issue
-        const double cost = per_sm_bytes + lat + (S > 1 ? 2000.0 : 0.0) + (warps < 4 ? 4000.0 : 0.0);
-        if (cost < best_cost) {
-          best_cost = cost;
-          best.RB = RB;
-          best.WK = WK;
-          best.KC = KC;
-          best.S = S;
-          best.NT = NT;
-          best.NB = NB;
-          best.grid_x = (RT + RB - 1) / RB;
-          best.grid_y = S;
-          best.grid_z = NB;
-          best.smem = smem;
+    if (S > 1 && (S - 1) * KC >= KQ) continue;
+    for (int nw : {4, 8}) {
+      for (int WK : {1, 2, 4, 8}) {
+        if (WK > nw || WK > KC) continue;
+        const int RBw = nw / WK;
+        for (int RB = 1; RB <= 64; ++RB) {
+          const size_t smem = smem_bytes(NT, KC, RB, WK);
+          if (smem > 200 * 1024) continue;
+          int occ = 0;
+          if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 32 * nw, smem) != cudaSuccess ||
+              occ < 1)
+            continue;
+          const long grid = static_cast<long>((RT + RB - 1) / RB) * S * NB;
+          const double ctas_per_sm = std::ceil(static_cast<double>(grid) / num_sms);
+          const double waves = std::ceil(static_cast<double>(grid) / (static_cast<double>(num_sms) * occ));
+          const double units_per_warp = std::ceil(static_cast<double>(RB) / RBw) *
+                                        std::ceil(static_cast<double>(KC) / WK);
+          const double bytes_cta = RB * KC * unit_b + KC * 512.0 * tok + (S > 1 ? 2.0 * RB * 64 * tok : 0.0);
+          const double t_mem = ctas_per_sm * bytes_cta / sm_bw;
+          const double warps_per_sched = std::max(1.0, nw * std::min<double>(occ, ctas_per_sm) / 4.0);
+          const double t_issue = waves * units_per_warp * unit_cycles * warps_per_sched / 1.9;
+          const double t_tail = waves * 700.0 + (S > 1 ? 700.0 : 0.0);
+          const double cost = std::max(t_mem, t_issue) + t_tail;
+          if (cost < best_cost * 0.999) {
+            best_cost = cost;
+            best.RB = RB;
+            best.WK = WK;
+            best.KC = KC;
+            best.S = S;
+            best.NT = NT;
+            best.NB = NB;
+            best.grid_x = (RT + RB - 1) / RB;
+            best.grid_y = S;
+            best.grid_z = NB;
+            best.nw = nw;
+            best.smem = smem;
+          }
         }
       }
     }
@@ -491,7 +527,7 @@ cudaError_t launch_tiled(const egt_dev_packed* h, const TiledSchedule& sc, const
   if (err != cudaSuccess) return err;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(sc.grid_x, sc.grid_y, sc.grid_z);
-  cfg.blockDim = dim3(32 * sc.RB * sc.WK);
+  cfg.blockDim = dim3(32 * sc.nw);
   cfg.dynamicSmemBytes = sc.smem;
   cfg.stream = ctx.stream;
   cudaLaunchAttribute attr[1];
