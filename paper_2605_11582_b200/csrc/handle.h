@@ -54,7 +54,8 @@ struct TiledSchedule {
   int S = 1;   // K splits (CTAs along K, reduced by the last arriver)
   int NT = 1;  // mma n-tiles (4 tokens each) per CTA
   int NB = 1;  // n-blocks (CTAs along tokens)
-  int nw = 8;  // warps per CTA (RBw = nw / WK warp rows)
+  int nw = 8;   // consumer warps per CTA (+1 producer warp)
+  int NST = 1;  // shared-memory stages (row tiles in flight)
   int grid_x = 1, grid_y = 1, grid_z = 1;
   size_t smem = 0;
 };

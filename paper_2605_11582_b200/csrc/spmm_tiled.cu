@@ -38,7 +38,7 @@ struct TiledArgs {
   int ldy;
   float* partial;
   uint32_t* counters;
-  int RB, WK, KC, S;
+  int RB, WK, KC, S, NST;
 };
 
 template <int FMT, int E>
@@ -52,44 +52,48 @@ struct Unit {
   uint32_t z[NS];
 };
 
+// A stage in shared memory holds one row tile's blocks for the CTA's KCs
+// k-quads, copied verbatim from HBM by the bulk-copy engine:
+//   [vals: KCs x 32 lanes x VB][meta: KCs x 32 x MB][scales: KCs x E x 16 f32][zps: KCs x E x 16 u8]
 template <int FMT, int E>
-__device__ __forceinline__ void load_unit(Unit<FMT, E>& u, const TiledArgs& a, int rt_abs, int kq,
-                                          int lane, uint64_t pol) {
+__device__ __forceinline__ void lds_unit(Unit<FMT, E>& u, const uint8_t* st, int KCs, int kql,
+                                         int lane) {
   constexpr int VB = val_lane_bytes(FMT), MB = meta_lane_bytes(FMT);
-  const size_t blk = static_cast<size_t>(rt_abs) * a.KQ + kq;
-  const uint8_t* vp = a.vals + blk * 32 * VB + lane * VB;
+  const uint8_t* vp = st + (kql * 32 + lane) * VB;
   if constexpr (VB == 8) {
-    uint2 t = ldg_stream_v2(vp, pol);
+    const uint2 t = *reinterpret_cast<const uint2*>(vp);
     u.v[0] = t.x;
     u.v[1] = t.y;
   } else {
 #pragma unroll
     for (int i = 0; i < VB / 16; ++i) {
-      uint4 t = ldg_stream_v4(vp + 16 * i, pol);
+      const uint4 t = *reinterpret_cast<const uint4*>(vp + 16 * i);
       u.v[4 * i + 0] = t.x;
       u.v[4 * i + 1] = t.y;
       u.v[4 * i + 2] = t.z;
       u.v[4 * i + 3] = t.w;
     }
   }
+  const uint8_t* mp = st + KCs * 32 * VB + (kql * 32 + lane) * MB;
   if constexpr (MB == 8) {
-    uint2 t = ldg_stream_v2(a.meta + blk * 32 * MB + lane * MB, pol);
+    const uint2 t = *reinterpret_cast<const uint2*>(mp);
     u.m[0] = t.x;
     u.m[1] = t.y;
   } else if constexpr (MB == 4) {
-    u.m[0] = ldg_stream_u32(a.meta + blk * 32 * MB + lane * MB, pol);
+    u.m[0] = *reinterpret_cast<const uint32_t*>(mp);
   } else {
     u.m[0] = 0;
   }
   if constexpr (has_scales(FMT)) {
     const int g = lane >> 2;
+    const uint8_t* sp = st + KCs * 32 * (VB + MB);
+    const uint8_t* zp = sp + KCs * E * 64;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-      const size_t idx = (blk * E + e) * 16 + 2 * g;
-      uint2 sc = ldg_stream_v2(a.scales + idx, pol);
+      const uint2 sc = *reinterpret_cast<const uint2*>(sp + (kql * E + e) * 64 + 8 * g);
       u.s[2 * e] = sc.x;
       u.s[2 * e + 1] = sc.y;
-      u.z[e] = ldg_stream_u16(a.zps + idx, pol);
+      u.z[e] = *reinterpret_cast<const uint16_t*>(zp + (kql * E + e) * 16 + 2 * g);
     }
   }
 }
@@ -230,58 +234,81 @@ __device__ __forceinline__ void compute_unit(const Unit<FMT, 4 / SS>& u, const u
   }
 }
 
-// One CTA = RB row tiles x KC k-quads x 4*NT tokens, nw = blockDim/32 warps
-// arranged as RBw = nw/WK warp rows x WK warp columns.  Warp (wi, wj) owns
-// row tiles wi, wi+RBw, ... over the wj-th part of the CTA's k-quads and
-// streams its units (row tile, k-quad) through a D-deep register pipeline;
-// the first D units are requested before the PDL wait (weights do not depend
-// on the previous kernel).  Split-K partial sums (S > 1) are reduced by the
-// last-arriving CTA of each row block, in slice order: deterministic.
-template <int FMT, int SS, int NT, int D>
-__global__ void __launch_bounds__(256, 2) tiled_spmm_kernel(const TiledArgs a) {
+template <int FMT>
+__host__ __device__ constexpr int stage_bytes(int KCs, int E) {
+  return KCs * 32 * (val_lane_bytes(FMT) + meta_lane_bytes(FMT)) + (has_scales(FMT) ? KCs * E * 80 : 0);
+}
+
+// One CTA = RB row tiles x KC k-quads (one of S K-slices) x 4*NT tokens.
+// Warp specialised: warp nw (the producer) streams whole row tiles -- every
+// block of the tile in the CTA's K-slice, 2-4 contiguous bulk copies -- into
+// an NST-deep ring of shared-memory stages (cp.async.bulk + mbarrier
+// complete_tx); the first NST row tiles are requested before the PDL wait,
+// since weights do not depend on the previous kernel.  The nw consumer warps
+// split each row tile's k-quads, dequantise in registers and issue mma.sp.
+// Per-warp partial sums are reduced in a fixed order; split-K (S > 1) partial
+// rows are summed by the last-arriving CTA of the row block, in slice order,
+// so results are deterministic.
+template <int FMT, int SS, int NT>
+__global__ void __launch_bounds__(288, 1) tiled_spmm_kernel(const TiledArgs a) {
   constexpr int E = 4 / SS;
-  constexpr int TOK = 4 * NT;                       // tokens per CTA (power of two)
-  constexpr int TOK_SHIFT = NT == 1 ? 2 : (NT == 2 ? 3 : 4);
-  extern __shared__ __align__(16) uint32_t smem[];
+  constexpr int TOK = 4 * NT;
+  constexpr int VB = val_lane_bytes(FMT), MB = meta_lane_bytes(FMT);
+  extern __shared__ __align__(128) uint8_t smem_raw[];
   pdl_launch_dependents();
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int nw = blockDim.x >> 5;
-  const int RBw = nw / a.WK;
-  const int wi = warp / a.WK, wj = warp % a.WK;
+  const int nw = (blockDim.x >> 5) - 1;  // consumer warps
   const int rt0 = blockIdx.x * a.RB;
   const int RBc = min(a.RB, a.RT - rt0);
   const int kq0 = blockIdx.y * a.KC;
-  const int kq1 = min(a.KQ, kq0 + a.KC);
-  const int KTc = (kq1 - kq0) * 4;
-  const int per = (kq1 - kq0 + a.WK - 1) / a.WK;
-  const int k0 = min(kq1, kq0 + wj * per);
-  const int nK = max(0, min(kq1, k0 + per) - k0);
-  const int nR = wi < RBc ? (RBc - wi + RBw - 1) / RBw : 0;
-  const int nU = nR * nK;
+  const int KCs = min(a.KQ, kq0 + a.KC) - kq0;
+  const int KTc = KCs * 4;
   const int m0 = blockIdx.z * TOK;
   const int M_left = a.M - m0;
-  const int rt_base = a.rt_begin + rt0 + wi;  // storage row tile of the warp's first unit
+  const int Mc = min(TOK, M_left);  // tokens of this CTA
+  const int sbytes = stage_bytes<FMT>(KCs, E);
+  const int NST = a.NST;
+
+  // shared memory carve-up
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* empty = full + NST;
+  uint32_t* sB = reinterpret_cast<uint32_t*>(smem_raw + 16 * NST + 128 - (16 * NST) % 128);
+  uint8_t* stages = reinterpret_cast<uint8_t*>(sB + NT * KTc * 128);
+  float* red = reinterpret_cast<float*>(stages + static_cast<size_t>(NST) * sbytes);  // [RB][nw][Mc][16]
+
+  if (tid == 0) {
+    for (int s = 0; s < NST; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, nw);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
 
   const uint64_t pol = evict_first_policy();
-  Unit<FMT, E> buf[D];
-  int lr = 0, lk = 0;  // (row iteration, k-quad) of the next unit to load
-#pragma unroll
-  for (int s = 0; s < D; ++s) {
-    if (s < nU) {
-      load_unit<FMT, E>(buf[s], a, rt_base + lr * RBw, k0 + lk, lane, pol);
-      if (++lk == nK) { lk = 0; ++lr; }
+  const size_t blk_stride = static_cast<size_t>(a.KQ);
+  auto issue = [&](int i) {  // row tile i of this CTA -> stage i % NST
+    const int s = i % NST;
+    uint8_t* st = stages + static_cast<size_t>(s) * sbytes;
+    const size_t blk = static_cast<size_t>(a.rt_begin + rt0 + i) * blk_stride + kq0;
+    mbar_expect_tx(full + s, sbytes);
+    bulk_g2s(st, a.vals + blk * 32 * VB, KCs * 32 * VB, full + s, pol);
+    if constexpr (MB > 0) bulk_g2s(st + KCs * 32 * VB, a.meta + blk * 32 * MB, KCs * 32 * MB, full + s, pol);
+    if constexpr (has_scales(FMT)) {
+      uint8_t* sp = st + KCs * 32 * (VB + MB);
+      bulk_g2s(sp, a.scales + blk * E * 16, KCs * E * 64, full + s, pol);
+      bulk_g2s(sp + KCs * E * 64, a.zps + blk * E * 16, KCs * E * 16, full + s, pol);
     }
-  }
+  };
+  if (warp == nw && lane == 0)
+    for (int i = 0; i < min(NST, RBc); ++i) issue(i);
 
   pdl_wait();  // x and the split-K workspace belong to earlier kernels
 
   // x slice -> fp16 hi/lo B fragments sB[nt][kt][lane][4]: token m's hi part
-  // is B column 2m (lanes 8m..8m+3), its lo part (the rounding residual)
-  // column 2m+1.  Only the lanes of present tokens are written (load_b skips
-  // the others).
-  uint32_t* sB = smem;
-  const int nB = NT * KTc * 128;
+  // is B column 2m (lanes 8m..8m+3), its rounding residual column 2m+1.
+  // Lanes of absent tokens are never read (load_b) and not written.
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) {
     const int items = KTc * 64;
@@ -306,50 +333,51 @@ __global__ void __launch_bounds__(256, 2) tiled_spmm_kernel(const TiledArgs a) {
                                        (static_cast<uint32_t>(__half_as_ushort(l1)) << 16);
     }
   }
-  float* red = reinterpret_cast<float*>(smem + nB);  // [RB][WK][TOK][16]
-  const int nRed = a.RB * a.WK * TOK * 16;
-  for (int i = tid; i < nRed; i += blockDim.x) red[i] = 0.f;
   __syncthreads();
 
-  float acc[NT][2];
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = 0.f;
-  int cr = 0, ck = 0;  // (row iteration, k-quad) of the unit being computed
-  const int g = lane >> 2, t = lane & 3;
-  for (int base = 0; base < nU; base += D) {
-#pragma unroll
-    for (int s = 0; s < D; ++s) {
-      if (base + s < nU) {
-        compute_unit<FMT, SS, NT>(buf[s], sB, KTc, (k0 + ck - kq0) * 4, lane, M_left, acc);
-        if (base + s + D < nU) {
-          load_unit<FMT, E>(buf[s], a, rt_base + lr * RBw, k0 + lk, lane, pol);
-          if (++lk == nK) { lk = 0; ++lr; }
-        }
-        if (++ck == nK) {  // row tile done: park its partial sums in smem
-          float* r = red + ((static_cast<size_t>(wi + cr * RBw) * a.WK + wj) * TOK) * 16;
-#pragma unroll
-          for (int nt = 0; nt < NT; ++nt) {
-            r[(4 * nt + t) * 16 + g] = acc[nt][0];
-            r[(4 * nt + t) * 16 + g + 8] = acc[nt][1];
-            acc[nt][0] = acc[nt][1] = 0.f;
-          }
-          ck = 0;
-          ++cr;
-        }
+  if (warp == nw) {
+    // producer: refill each stage once all consumer warps released it
+    if (lane == 0)
+      for (int i = NST; i < RBc; ++i) {
+        mbar_wait(empty + (i % NST), ((i / NST) - 1) & 1);
+        issue(i);
       }
+  } else {
+    const int g = lane >> 2, t = lane & 3;
+    for (int i = 0; i < RBc; ++i) {
+      const int s = i % NST;
+      mbar_wait(full + s, (i / NST) & 1);
+      const uint8_t* st = stages + static_cast<size_t>(s) * sbytes;
+      float acc[NT][2];
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = 0.f;
+      for (int kql = warp; kql < KCs; kql += nw) {
+        Unit<FMT, E> u;
+        lds_unit<FMT, E>(u, st, KCs, kql, lane);
+        compute_unit<FMT, SS, NT>(u, sB, KTc, kql * 4, lane, M_left, acc);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(empty + s);
+      float* r = red + (static_cast<size_t>(i) * nw + warp) * Mc * 16;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt)
+        if (4 * nt + t < Mc) {
+          r[(4 * nt + t) * 16 + g] = acc[nt][0];
+          r[(4 * nt + t) * 16 + g + 8] = acc[nt][1];
+        }
     }
   }
   __syncthreads();
 
   const int rows_pad = a.RT * 16;
-  const int nOut = RBc * TOK * 16;
+  const int nOut = RBc * Mc * 16;
   for (int idx = tid; idx < nOut; idx += blockDim.x) {
-    const int row16 = idx & 15, tl = (idx >> 4) & (TOK - 1), i = idx >> (4 + TOK_SHIFT);
+    const int row16 = idx & 15, tl = (idx >> 4) % Mc, i = (idx >> 4) / Mc;
     float v = 0.f;
-    for (int j = 0; j < a.WK; ++j) v += red[((static_cast<size_t>(i) * a.WK + j) * TOK + tl) * 16 + row16];
+    for (int w = 0; w < nw; ++w) v += red[((static_cast<size_t>(i) * nw + w) * Mc + tl) * 16 + row16];
     const int row = (rt0 + i) * 16 + row16;
     const int tok = m0 + tl;
-    if (row < a.rows && tok < a.M) {
+    if (row < a.rows) {
       if (a.S == 1)
         a.y[static_cast<size_t>(tok) * a.ldy + row] = v;
       else
@@ -367,10 +395,10 @@ __global__ void __launch_bounds__(256, 2) tiled_spmm_kernel(const TiledArgs a) {
   if (!s_last) return;
   __threadfence();
   for (int idx = tid; idx < nOut; idx += blockDim.x) {
-    const int row16 = idx & 15, tl = (idx >> 4) & (TOK - 1), i = idx >> (4 + TOK_SHIFT);
+    const int row16 = idx & 15, tl = (idx >> 4) % Mc, i = (idx >> 4) / Mc;
     const int row = (rt0 + i) * 16 + row16;
     const int tok = m0 + tl;
-    if (row < a.rows && tok < a.M) {
+    if (row < a.rows) {
       float v = 0.f;
       for (int sidx = 0; sidx < a.S; ++sidx)
         v += __ldcg(a.partial + (static_cast<size_t>(sidx) * a.M + tok) * rows_pad + row);
@@ -383,11 +411,10 @@ __global__ void __launch_bounds__(256, 2) tiled_spmm_kernel(const TiledArgs a) {
 // ---------------------------------------------------------------- planning
 
 namespace {
-constexpr int kDepth = 4;
 
 template <int FMT, int SS, int NT>
 void* kernel_ptr() {
-  return reinterpret_cast<void*>(&tiled_spmm_kernel<FMT, SS, NT, kDepth>);
+  return reinterpret_cast<void*>(&tiled_spmm_kernel<FMT, SS, NT>);
 }
 
 template <int FMT, int SS>
@@ -418,74 +445,62 @@ void* pick_kernel(int fmt, int SS, int NT) {
   }
 }
 
-size_t block_bytes(const egt_dev_packed* h) {
-  const int f = h->format;
-  size_t b = 32u * (val_lane_bytes(f) + meta_lane_bytes(f));
-  if (has_scales(f)) b += 16u * 5u * h->tiled.E;
-  return b;
-}
-
-size_t smem_bytes(int NT, int KC, int RB, int WK) {
-  return static_cast<size_t>(NT) * KC * 4 * 512 + static_cast<size_t>(RB) * WK * 4 * NT * 16 * 4;
+int stage_bytes_rt(int fmt, int KCs, int E) {
+  return KCs * 32 * (val_lane_bytes(fmt) + meta_lane_bytes(fmt)) + (has_scales(fmt) ? KCs * E * 80 : 0);
 }
 }  // namespace
 
-// Picks the CTA tile (RB row tiles x KC k-quads, nw warps as RBw x WK) and the
-// split-K factor S with a small model of one launch: the busiest SM's HBM
-// bytes at its 1/148 share of bandwidth, the per-scheduler issue time of the
-// dequant + mma.sp stream, the number of waves, and a fixed tail for the
-// split-K reduction.  Everything is resident in one wave whenever possible
-// (2 CTAs/SM leave room for the next kernel's CTAs under PDL).
+// Picks the CTA tile (RB row tiles x KC k-quads), the split-K factor S, the
+// stage depth NST and the consumer warp count with a small model of one
+// launch: the busiest SM's HBM bytes at its 1/148 share of bandwidth, the
+// issue time of the dequant + mma.sp stream per scheduler, the number of
+// waves, and a fixed tail for the split-K reduction.
 TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms) {
   TiledSchedule best;
-  const int RT = h->tiled.RT, KQ = h->tiled.KQ;
+  const int RT = h->tiled.RT, KQ = h->tiled.KQ, E = h->tiled.E, f = h->format;
   const int NT = M <= 4 ? 1 : (M <= 8 ? 2 : 4);
   const int NB = (M + 4 * NT - 1) / (4 * NT);
   const int tok = std::min(M, 4 * NT);
-  const double unit_b = static_cast<double>(block_bytes(h));
-  const double sm_bw = 44.0;          // B/ns per SM (6.5 TB/s / 148)
-  const double unit_cycles = 60.0 * NT;  // issue slots per (warp, unit)
-  void* fn = pick_kernel(h->format, h->tiled.SS, NT);
+  const double unit_b = static_cast<double>(stage_bytes_rt(f, 1, E));
+  const double sm_bw = 44.0;             // B/ns per SM (6.5 TB/s / 148)
+  const double unit_cycles = 70.0 * NT;  // issue slots per (warp, k-quad unit)
+  const size_t smem_cap = 200 * 1024;
   double best_cost = 1e300;
   for (int S = 1; S <= std::min(KQ, 8); ++S) {
     const int KC = (KQ + S - 1) / S;
     if (S > 1 && (S - 1) * KC >= KQ) continue;
-    for (int nw : {4, 8}) {
-      for (int WK : {1, 2, 4, 8}) {
-        if (WK > nw || WK > KC) continue;
-        const int RBw = nw / WK;
-        for (int RB = 1; RB <= 64; ++RB) {
-          const size_t smem = smem_bytes(NT, KC, RB, WK);
-          if (smem > 200 * 1024) continue;
-          int occ = 0;
-          if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, 32 * nw, smem) != cudaSuccess ||
-              occ < 1)
-            continue;
-          const long grid = static_cast<long>((RT + RB - 1) / RB) * S * NB;
-          const double ctas_per_sm = std::ceil(static_cast<double>(grid) / num_sms);
-          const double waves = std::ceil(static_cast<double>(grid) / (static_cast<double>(num_sms) * occ));
-          const double units_per_warp = std::ceil(static_cast<double>(RB) / RBw) *
-                                        std::ceil(static_cast<double>(KC) / WK);
-          const double bytes_cta = RB * KC * unit_b + KC * 512.0 * tok + (S > 1 ? 2.0 * RB * 64 * tok : 0.0);
-          const double t_mem = ctas_per_sm * bytes_cta / sm_bw;
-          const double warps_per_sched = std::max(1.0, nw * std::min<double>(occ, ctas_per_sm) / 4.0);
-          const double t_issue = waves * units_per_warp * unit_cycles * warps_per_sched / 1.9;
-          const double t_tail = waves * 700.0 + (S > 1 ? 700.0 : 0.0);
-          const double cost = std::max(t_mem, t_issue) + t_tail;
-          if (cost < best_cost * 0.999) {
-            best_cost = cost;
-            best.RB = RB;
-            best.WK = WK;
-            best.KC = KC;
-            best.S = S;
-            best.NT = NT;
-            best.NB = NB;
-            best.grid_x = (RT + RB - 1) / RB;
-            best.grid_y = S;
-            best.grid_z = NB;
-            best.nw = nw;
-            best.smem = smem;
-          }
+    const int sb = stage_bytes_rt(f, KC, E);
+    for (int RB = 1; RB <= 128; ++RB) {
+      const long grid = static_cast<long>((RT + RB - 1) / RB) * S * NB;
+      if (grid > 2L * num_sms && RB < 128) continue;  // keep to (at most) ~1 wave
+      const int nst = std::max(1, std::min(RB, static_cast<int>((smem_cap - 16384) / sb)));
+      for (int nw : {4, 8}) {
+        const size_t smem = (16 * nst + 127) / 128 * 128 + 128 + static_cast<size_t>(NT) * KC * 4 * 512 +
+                            static_cast<size_t>(nst) * sb + static_cast<size_t>(RB) * nw * tok * 64;
+        if (smem > smem_cap) continue;
+        const double ctas_per_sm = std::ceil(static_cast<double>(grid) / num_sms);
+        const double bytes_cta = RB * KC * unit_b + KC * 512.0 * tok + (S > 1 ? 2.0 * RB * 64 * tok : 0.0);
+        const double t_mem = ctas_per_sm * bytes_cta / sm_bw;
+        const double units_per_warp = RB * std::ceil(static_cast<double>(KC) / nw);
+        const double t_issue = ctas_per_sm * units_per_warp * unit_cycles * std::max(1.0, nw / 4.0) / 1.9;
+        const double in_flight = nst * sb;  // bytes a CTA can have outstanding
+        const double t_lat = 900.0 * std::ceil(RB * static_cast<double>(sb) / in_flight);
+        const double t_tail = (S > 1 ? 900.0 : 0.0) + 0.5 * (t_mem / ctas_per_sm);
+        const double cost = std::max(t_mem, t_issue) + t_lat * 0.2 + t_tail + ctas_per_sm * 600.0;
+        if (cost < best_cost * 0.999) {
+          best_cost = cost;
+          best.RB = RB;
+          best.WK = 1;
+          best.KC = KC;
+          best.S = S;
+          best.NT = NT;
+          best.NB = NB;
+          best.grid_x = (RT + RB - 1) / RB;
+          best.grid_y = S;
+          best.grid_z = NB;
+          best.nw = nw;
+          best.NST = nst;
+          best.smem = smem;
         }
       }
     }
@@ -521,13 +536,14 @@ cudaError_t launch_tiled(const egt_dev_packed* h, const TiledSchedule& sc, const
   a.WK = sc.WK;
   a.KC = sc.KC;
   a.S = sc.S;
+  a.NST = sc.NST;
   void* fn = pick_kernel(h->format, h->tiled.SS, sc.NT);
   cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(sc.smem));
   if (err != cudaSuccess) return err;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(sc.grid_x, sc.grid_y, sc.grid_z);
-  cfg.blockDim = dim3(32 * sc.nw);
+  cfg.blockDim = dim3(32 * (sc.nw + 1));
   cfg.dynamicSmemBytes = sc.smem;
   cfg.stream = ctx.stream;
   cudaLaunchAttribute attr[1];
