@@ -160,6 +160,11 @@ EGT_API egt_status egt_dequant(const egt_dev_packed* h, float* w_dev, uint8_t* m
  * the previous kernel in the stream finishes. */
 EGT_API void egt_set_pdl(int enabled);
 
+/* Tuning hook: force the tiled launch plan for subsequent egt_spmv calls on
+ * this thread (row tiles per CTA, K splits, consumer warps, stage depth;
+ * rb = 0 restores the automatic planner).  Used by tools/plan_sweep.py. */
+EGT_API void egt_tune_force_plan(int rb, int s, int nw, int nst);
+
 /* Number of kernels the library has launched on this thread (a counter the
  * benchmark reads to report gpu_launches). */
 EGT_API uint64_t egt_launch_count(void);

@@ -267,6 +267,7 @@ int egt_abi_version(void) { return EGT_ABI_VERSION; }
 const char* egt_last_error(void) { return g_err.c_str(); }
 void egt_set_pdl(int enabled) { g_pdl = enabled != 0; }
 uint64_t egt_launch_count(void) { return launch_counter(); }
+void egt_tune_force_plan(int rb, int s, int nw, int nst) { force_plan(rb, s, nw, nst); }
 
 egt_status egt_dev_packed_create(const egt_packed_view* v, void* stream, egt_dev_packed** out) {
   using namespace egt_fmt;
@@ -447,7 +448,9 @@ egt_status egt_spmv(const egt_dev_packed* h, const float* x, float* y, uint32_t 
     return EGT_OK;
   }
   TiledSchedule sc;
-  {
+  if (plan_forced()) {
+    sc = plan_tiled(h, static_cast<int>(M), num_sms());
+  } else {
     std::lock_guard<std::mutex> lk(h->plan_mu);
     auto it = h->plans.find(static_cast<int>(M));
     if (it == h->plans.end()) {

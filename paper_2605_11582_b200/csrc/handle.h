@@ -87,6 +87,8 @@ struct LaunchCtx {
 };
 
 TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms);
+void force_plan(int RB, int S, int nw, int NST);  // tuning hook (0 = automatic)
+bool plan_forced();
 size_t tiled_workspace_floats(const egt_dev_packed* h, const TiledSchedule& sc, int M);
 
 cudaError_t launch_tiled(const egt_dev_packed* h, const TiledSchedule& sc, const float* x, int ldx,

@@ -309,23 +309,42 @@ __global__ void __launch_bounds__(288, 1) tiled_spmm_kernel(const TiledArgs a) {
   // x slice -> fp16 hi/lo B fragments sB[nt][kt][lane][4]: token m's hi part
   // is B column 2m (lanes 8m..8m+3), its rounding residual column 2m+1.
   // Lanes of absent tokens are never read (load_b) and not written.
+  // Step 1: the f32 slice of every token of the CTA into shared memory
+  // (aliases `red`, unused until the products are done) with all loads of a
+  // thread in flight together; step 2: split and convert from shared memory.
+  float* xs = red;
+  const int n4 = KTc * 8;  // float4s per token
+  const bool vec = ((a.ldx & 3) == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0);
+  for (int m = 0; m < Mc; ++m) {
+    const float* xr = a.x + static_cast<size_t>(m0 + m) * a.ldx + kq0 * 128;
+    float4* xd = reinterpret_cast<float4*>(xs + static_cast<size_t>(m) * KTc * 32);
+    const int lim = a.cols - kq0 * 128;  // valid floats of this slice
+    if (vec) {
+#pragma unroll 8
+      for (int i = tid; i < n4; i += blockDim.x)
+        xd[i] = 4 * i < lim ? __ldg(reinterpret_cast<const float4*>(xr) + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+    } else {
+#pragma unroll 4
+      for (int i = tid; i < n4; i += blockDim.x) {
+        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (4 * i < lim) v = make_float4(xr[4 * i], xr[4 * i + 1], xr[4 * i + 2], xr[4 * i + 3]);
+        xd[i] = v;
+      }
+    }
+  }
+  __syncthreads();
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) {
-    const int items = KTc * 64;
+    const int mc = min(4, Mc - 4 * nt);
+    const int items = KTc * 16 * mc;
     for (int i = tid; i < items; i += blockDim.x) {
-      const int reg = i & 3, t = (i >> 2) & 3, m = (i >> 4) & 3, kt = i >> 6;
-      const int tok = m0 + 4 * nt + m;
-      if (tok >= a.M) continue;
-      const int k = (kq0 * 4 + kt) * 32 + 2 * t + 8 * reg;
-      float v0 = 0.f, v1 = 0.f;
-      if (k < a.cols) {
-        const float* xp = a.x + static_cast<size_t>(tok) * a.ldx + k;
-        v0 = xp[0];
-        v1 = xp[1];
-      }
-      const __half h0 = __float2half_rn(v0), h1 = __float2half_rn(v1);
-      const __half l0 = __float2half_rn(v0 - __half2float(h0));
-      const __half l1 = __float2half_rn(v1 - __half2float(h1));
+      const int reg = i & 3, t = (i >> 2) & 3, r = i >> 4;
+      const int kt = r % KTc, m = r / KTc;
+      const float2 v = *reinterpret_cast<const float2*>(xs + static_cast<size_t>(4 * nt + m) * KTc * 32 +
+                                                        kt * 32 + 2 * t + 8 * reg);
+      const __half h0 = __float2half_rn(v.x), h1 = __float2half_rn(v.y);
+      const __half l0 = __float2half_rn(v.x - __half2float(h0));
+      const __half l1 = __float2half_rn(v.y - __half2float(h1));
       uint32_t* row = sB + static_cast<size_t>(nt * KTc + kt) * 128;
       row[(8 * m + t) * 4 + reg] = static_cast<uint32_t>(__half_as_ushort(h0)) |
                                    (static_cast<uint32_t>(__half_as_ushort(h1)) << 16);
@@ -455,6 +474,16 @@ int stage_bytes_rt(int fmt, int KCs, int E) {
 // launch: the busiest SM's HBM bytes at its 1/148 share of bandwidth, the
 // issue time of the dequant + mma.sp stream per scheduler, the number of
 // waves, and a fixed tail for the split-K reduction.
+static thread_local int g_force[5] = {0, 0, 0, 0, 0};  // RB, S, nw, NST, on
+void force_plan(int RB, int S, int nw, int NST) {
+  g_force[0] = RB;
+  g_force[1] = S;
+  g_force[2] = nw;
+  g_force[3] = NST;
+  g_force[4] = RB > 0;
+}
+bool plan_forced() { return g_force[4] != 0; }
+
 TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms) {
   TiledSchedule best;
   const int RT = h->tiled.RT, KQ = h->tiled.KQ, E = h->tiled.E, f = h->format;
@@ -469,14 +498,19 @@ TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms) {
   for (int S = 1; S <= std::min(KQ, 8); ++S) {
     const int KC = (KQ + S - 1) / S;
     if (S > 1 && (S - 1) * KC >= KQ) continue;
+    if (g_force[4] && S != g_force[1]) continue;
     const int sb = stage_bytes_rt(f, KC, E);
     for (int RB = 1; RB <= 128; ++RB) {
+      if (g_force[4] && RB != g_force[0]) continue;
       const long grid = static_cast<long>((RT + RB - 1) / RB) * S * NB;
-      if (grid > 2L * num_sms && RB < 128) continue;  // keep to (at most) ~1 wave
-      const int nst = std::max(1, std::min(RB, static_cast<int>((smem_cap - 16384) / sb)));
+      if (grid > 2L * num_sms && RB < 128 && !g_force[4]) continue;  // keep to (at most) ~1 wave
+      int nst = std::max(1, std::min(RB, static_cast<int>((smem_cap - 16384) / sb)));
+      if (g_force[4] && g_force[3] > 0) nst = std::min(nst, g_force[3]);
       for (int nw : {4, 8}) {
+        if (g_force[4] && g_force[2] > 0 && nw != g_force[2]) continue;
+        const size_t red = std::max(static_cast<size_t>(RB) * nw * tok * 64, static_cast<size_t>(tok) * KC * 512);
         const size_t smem = (16 * nst + 127) / 128 * 128 + 128 + static_cast<size_t>(NT) * KC * 4 * 512 +
-                            static_cast<size_t>(nst) * sb + static_cast<size_t>(RB) * nw * tok * 64;
+                            static_cast<size_t>(nst) * sb + red;
         if (smem > smem_cap) continue;
         const double ctas_per_sm = std::ceil(static_cast<double>(grid) / num_sms);
         const double bytes_cta = RB * KC * unit_b + KC * 512.0 * tok + (S > 1 ? 2.0 * RB * 64 * tok : 0.0);
