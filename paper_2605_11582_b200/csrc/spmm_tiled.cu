@@ -116,15 +116,16 @@ __device__ __forceinline__ uint32_t place_hi(uint32_t r, uint32_t slot) {
   return prmt(r, 0u, slot ? 0x3244u : 0x4432u);
 }
 
+// B fragments of k-tile kt for every n-tile: lanes whose column (lane >> 2)
+// holds a present token read 16 bytes; the rest multiply by zero.
 template <int NT>
 __device__ __forceinline__ void load_b(uint32_t (&b)[NT][4], const uint32_t* sB, int KTc, int kt,
-                                       int lane, int valid_cols_nt0, int M_left) {
+                                       int lane, int LS, int M_left) {
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) {
-    const int col = lane >> 2;  // B column held by this lane
     const int cols_here = min(8, 2 * (M_left - 4 * nt));
-    if (col < cols_here) {
-      const uint4 t = *reinterpret_cast<const uint4*>(sB + ((nt * KTc + kt) * 32 + lane) * 4);
+    if ((lane >> 2) < cols_here) {
+      const uint4 t = *reinterpret_cast<const uint4*>(sB + ((nt * KTc + kt) * LS + lane) * 4);
       b[nt][0] = t.x;
       b[nt][1] = t.y;
       b[nt][2] = t.z;
@@ -133,7 +134,6 @@ __device__ __forceinline__ void load_b(uint32_t (&b)[NT][4], const uint32_t* sB,
       b[nt][0] = b[nt][1] = b[nt][2] = b[nt][3] = 0u;
     }
   }
-  (void)valid_cols_nt0;
 }
 
 // j is a compile-time constant after unrolling; the branch folds away.
@@ -151,7 +151,7 @@ __device__ __forceinline__ void mma_sp_sel(int j, float (&d)[NT][4], const uint3
 
 template <int FMT, int SS, int NT>
 __device__ __forceinline__ void compute_unit(const Unit<FMT, 4 / SS>& u, const uint32_t* sB, int KTc,
-                                             int kt_base, int lane, int M_left,
+                                             int kt_base, int lane, int LS, int M_left,
                                              float (&acc)[NT][2]) {
   float d[NT][4];
   uint32_t zg = 0, zg8 = 0, zpair = 0;
@@ -169,7 +169,7 @@ __device__ __forceinline__ void compute_unit(const Unit<FMT, 4 / SS>& u, const u
       }
     }
     uint32_t b[NT][4];
-    load_b<NT>(b, sB, KTc, kt_base + j, lane, 0, M_left);
+    load_b<NT>(b, sB, KTc, kt_base + j, lane, LS, M_left);
     if constexpr (FMT == I4_SP24 || FMT == F16_SP24) {
       uint32_t a[4];
       if constexpr (FMT == I4_SP24) {
@@ -250,7 +250,7 @@ __host__ __device__ constexpr int stage_bytes(int KCs, int E) {
 // rows are summed by the last-arriving CTA of the row block, in slice order,
 // so results are deterministic.
 template <int FMT, int SS, int NT>
-__global__ void __launch_bounds__(288, 1) tiled_spmm_kernel(const TiledArgs a) {
+__global__ void __launch_bounds__(288, 2) tiled_spmm_kernel(const TiledArgs a) {
   constexpr int E = 4 / SS;
   constexpr int TOK = 4 * NT;
   constexpr int VB = val_lane_bytes(FMT), MB = meta_lane_bytes(FMT);
@@ -273,8 +273,9 @@ __global__ void __launch_bounds__(288, 1) tiled_spmm_kernel(const TiledArgs a) {
   // shared memory carve-up
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
   uint64_t* empty = full + NST;
+  const int LS = 8 * min(4, Mc);  // sB lanes per (n-tile, k-tile): only present tokens
   uint32_t* sB = reinterpret_cast<uint32_t*>(smem_raw + 16 * NST + 128 - (16 * NST) % 128);
-  uint8_t* stages = reinterpret_cast<uint8_t*>(sB + NT * KTc * 128);
+  uint8_t* stages = reinterpret_cast<uint8_t*>(sB + NT * KTc * LS * 4);
   float* red = reinterpret_cast<float*>(stages + static_cast<size_t>(NST) * sbytes);  // [RB][nw][Mc][16]
 
   if (tid == 0) {
@@ -306,50 +307,33 @@ __global__ void __launch_bounds__(288, 1) tiled_spmm_kernel(const TiledArgs a) {
 
   pdl_wait();  // x and the split-K workspace belong to earlier kernels
 
-  // x slice -> fp16 hi/lo B fragments sB[nt][kt][lane][4]: token m's hi part
-  // is B column 2m (lanes 8m..8m+3), its rounding residual column 2m+1.
-  // Lanes of absent tokens are never read (load_b) and not written.
-  // Step 1: the f32 slice of every token of the CTA into shared memory
-  // (aliases `red`, unused until the products are done) with all loads of a
-  // thread in flight together; step 2: split and convert from shared memory.
-  float* xs = red;
-  const int n4 = KTc * 8;  // float4s per token
-  const bool vec = ((a.ldx & 3) == 0) && ((reinterpret_cast<uintptr_t>(a.x) & 15) == 0);
-  for (int m = 0; m < Mc; ++m) {
-    const float* xr = a.x + static_cast<size_t>(m0 + m) * a.ldx + kq0 * 128;
-    float4* xd = reinterpret_cast<float4*>(xs + static_cast<size_t>(m) * KTc * 32);
-    const int lim = a.cols - kq0 * 128;  // valid floats of this slice
-    if (vec) {
-#pragma unroll 8
-      for (int i = tid; i < n4; i += blockDim.x)
-        xd[i] = 4 * i < lim ? __ldg(reinterpret_cast<const float4*>(xr) + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-    } else {
-#pragma unroll 4
-      for (int i = tid; i < n4; i += blockDim.x) {
-        float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (4 * i < lim) v = make_float4(xr[4 * i], xr[4 * i + 1], xr[4 * i + 2], xr[4 * i + 3]);
-        xd[i] = v;
-      }
-    }
-  }
-  __syncthreads();
+  // x slice -> fp16 hi/lo B fragments sB[nt][kt][lane < LS][4]: token m's hi
+  // part is B column 2m (lanes 8m..8m+3), its rounding residual column 2m+1.
+  // Straight from global (L2) with 8 independent loads per thread in flight.
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) {
     const int mc = min(4, Mc - 4 * nt);
-    const int items = KTc * 16 * mc;
-    for (int i = tid; i < items; i += blockDim.x) {
-      const int reg = i & 3, t = (i >> 2) & 3, r = i >> 4;
-      const int kt = r % KTc, m = r / KTc;
-      const float2 v = *reinterpret_cast<const float2*>(xs + static_cast<size_t>(4 * nt + m) * KTc * 32 +
-                                                        kt * 32 + 2 * t + 8 * reg);
-      const __half h0 = __float2half_rn(v.x), h1 = __float2half_rn(v.y);
-      const __half l0 = __float2half_rn(v.x - __half2float(h0));
-      const __half l1 = __float2half_rn(v.y - __half2float(h1));
-      uint32_t* row = sB + static_cast<size_t>(nt * KTc + kt) * 128;
-      row[(8 * m + t) * 4 + reg] = static_cast<uint32_t>(__half_as_ushort(h0)) |
-                                   (static_cast<uint32_t>(__half_as_ushort(h1)) << 16);
-      row[(8 * m + 4 + t) * 4 + reg] = static_cast<uint32_t>(__half_as_ushort(l0)) |
-                                       (static_cast<uint32_t>(__half_as_ushort(l1)) << 16);
+    for (int m = 0; m < mc; ++m) {
+      const float* xr = a.x + static_cast<size_t>(m0 + 4 * nt + m) * a.ldx;
+      const int items = KTc * 16;
+#pragma unroll 8
+      for (int i = tid; i < items; i += blockDim.x) {
+        const int reg = i & 3, t = (i >> 2) & 3, kt = i >> 4;
+        const int k = (kq0 * 4 + kt) * 32 + 2 * t + 8 * reg;
+        float v0 = 0.f, v1 = 0.f;
+        if (k < a.cols) {
+          v0 = __ldg(xr + k);
+          v1 = __ldg(xr + k + 1);
+        }
+        const __half h0 = __float2half_rn(v0), h1 = __float2half_rn(v1);
+        const __half l0 = __float2half_rn(v0 - __half2float(h0));
+        const __half l1 = __float2half_rn(v1 - __half2float(h1));
+        uint32_t* row = sB + static_cast<size_t>(nt * KTc + kt) * LS * 4;
+        row[(8 * m + t) * 4 + reg] = static_cast<uint32_t>(__half_as_ushort(h0)) |
+                                     (static_cast<uint32_t>(__half_as_ushort(h1)) << 16);
+        row[(8 * m + 4 + t) * 4 + reg] = static_cast<uint32_t>(__half_as_ushort(l0)) |
+                                         (static_cast<uint32_t>(__half_as_ushort(l1)) << 16);
+      }
     }
   }
   __syncthreads();
@@ -373,7 +357,7 @@ __global__ void __launch_bounds__(288, 1) tiled_spmm_kernel(const TiledArgs a) {
       for (int kql = warp; kql < KCs; kql += nw) {
         Unit<FMT, E> u;
         lds_unit<FMT, E>(u, st, KCs, kql, lane);
-        compute_unit<FMT, SS, NT>(u, sB, KTc, kql * 4, lane, M_left, acc);
+        compute_unit<FMT, SS, NT>(u, sB, KTc, kql * 4, lane, LS, M_left, acc);
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + s);
@@ -493,7 +477,9 @@ TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms) {
   const double unit_b = static_cast<double>(stage_bytes_rt(f, 1, E));
   const double sm_bw = 44.0;             // B/ns per SM (6.5 TB/s / 148)
   const double unit_cycles = 70.0 * NT;  // issue slots per (warp, k-quad unit)
-  const size_t smem_cap = 200 * 1024;
+  // <= ~100 KB and <= one CTA per SM: the next kernel's CTAs fit beside this
+  // kernel's (programmatic dependent launch) and prefetch their weights.
+  const size_t smem_cap = 100 * 1024;
   double best_cost = 1e300;
   for (int S = 1; S <= std::min(KQ, 8); ++S) {
     const int KC = (KQ + S - 1) / S;
@@ -503,13 +489,14 @@ TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms) {
     for (int RB = 1; RB <= 128; ++RB) {
       if (g_force[4] && RB != g_force[0]) continue;
       const long grid = static_cast<long>((RT + RB - 1) / RB) * S * NB;
-      if (grid > 2L * num_sms && RB < 128 && !g_force[4]) continue;  // keep to (at most) ~1 wave
-      int nst = std::max(1, std::min(RB, static_cast<int>((smem_cap - 16384) / sb)));
+      if (grid > num_sms && RB < 128 && !g_force[4]) continue;  // one CTA per SM
+      int nst = std::max(1, std::min(RB, static_cast<int>((smem_cap - 24576) / sb)));
       if (g_force[4] && g_force[3] > 0) nst = std::min(nst, g_force[3]);
       for (int nw : {4, 8}) {
         if (g_force[4] && g_force[2] > 0 && nw != g_force[2]) continue;
-        const size_t red = std::max(static_cast<size_t>(RB) * nw * tok * 64, static_cast<size_t>(tok) * KC * 512);
-        const size_t smem = (16 * nst + 127) / 128 * 128 + 128 + static_cast<size_t>(NT) * KC * 4 * 512 +
+        const size_t red = static_cast<size_t>(RB) * nw * tok * 64;
+        const size_t smem = (16 * nst + 127) / 128 * 128 + 128 +
+                            static_cast<size_t>(NT) * KC * 4 * 32 * std::min(4, tok) * 4 +
                             static_cast<size_t>(nst) * sb + red;
         if (smem > smem_cap) continue;
         const double ctas_per_sm = std::ceil(static_cast<double>(grid) / num_sms);
@@ -538,6 +525,12 @@ TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms) {
         }
       }
     }
+  }
+  if (best_cost >= 1e300 && g_force[4]) {  // forced plan infeasible: automatic plan
+    const int saved[5] = {g_force[0], g_force[1], g_force[2], g_force[3], g_force[4]};
+    g_force[4] = 0;
+    best = plan_tiled(h, M, num_sms);
+    for (int i = 0; i < 5; ++i) g_force[i] = saved[i];
   }
   return best;
 }

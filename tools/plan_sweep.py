@@ -28,13 +28,14 @@ def time_plan(layers, x, ys, stream, reps=20):
         with torch.cuda.graph(g, stream=stream):
             for d, y in zip(layers, ys):
                 d.spmv_into(x, y, stream)
-    for _ in range(3):
-        g.replay()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for _ in range(reps):
-        g.replay()
-    e1.record(stream)
+    with torch.cuda.stream(stream):  # replay() runs on the current stream
+        for _ in range(3):
+            g.replay()
+        e0.record(stream)
+        for _ in range(reps):
+            g.replay()
+        e1.record(stream)
     e1.synchronize()
     return 1e3 * e0.elapsed_time(e1) / (reps * len(layers))
 
