@@ -143,6 +143,14 @@ EGT_API egt_status egt_dev_packed_query(const egt_dev_packed* h, egt_dev_packed_
 EGT_API egt_status egt_spmv(const egt_dev_packed* h, const float* x_dev, float* y_dev, uint32_t M,
                     uint32_t ldx, uint32_t ldy, void* stream);
 
+/* egt_spmv with flags.  EGT_SPMV_INDEPENDENT: x is not written by the
+ * kernel issued immediately before this one on the stream, so the product may
+ * overlap that kernel entirely (it still completes after it).  Typical use:
+ * the Q, K, V (or gate/up) products of one decode step. */
+#define EGT_SPMV_INDEPENDENT 1u
+EGT_API egt_status egt_spmv_ex(const egt_dev_packed* h, const float* x_dev, float* y_dev, uint32_t M,
+                               uint32_t ldx, uint32_t ldy, uint32_t flags, void* stream);
+
 /* Same as egt_spmv with host buffers: H2D of x, the product, D2H of y, and a
  * stream synchronize.  x_len must equal cols (else EGT_EINVAL with the
  * reference's "spmv: input length differs from columns"). */

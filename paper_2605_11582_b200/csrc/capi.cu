@@ -425,8 +425,9 @@ egt_status egt_dev_packed_query(const egt_dev_packed* h, egt_dev_packed_info* in
   return EGT_OK;
 }
 
-egt_status egt_spmv(const egt_dev_packed* h, const float* x, float* y, uint32_t M, uint32_t ldx,
-                    uint32_t ldy, void* stream) {
+egt_status egt_spmv_ex(const egt_dev_packed* h, const float* x, float* y, uint32_t M, uint32_t ldx,
+                       uint32_t ldy, uint32_t flags, void* stream) {
+  const bool indep = (flags & EGT_SPMV_INDEPENDENT) != 0;
   if (!h) return fail(EGT_EINVAL, "spmv: null matrix");
   if (M == 0) return EGT_OK;
   if (ldx < h->cols) return fail(EGT_EINVAL, "spmv: input length differs from columns");
@@ -449,12 +450,13 @@ egt_status egt_spmv(const egt_dev_packed* h, const float* x, float* y, uint32_t 
   }
   TiledSchedule sc;
   if (plan_forced()) {
-    sc = plan_tiled(h, static_cast<int>(M), num_sms());
+    sc = plan_tiled(h, static_cast<int>(M), num_sms(), indep);
   } else {
     std::lock_guard<std::mutex> lk(h->plan_mu);
-    auto it = h->plans.find(static_cast<int>(M));
+    const int key = static_cast<int>(M) * 2 + (indep ? 1 : 0);
+    auto it = h->plans.find(key);
     if (it == h->plans.end()) {
-      it = h->plans.emplace(static_cast<int>(M), plan_tiled(h, M, num_sms())).first;
+      it = h->plans.emplace(key, plan_tiled(h, M, num_sms(), indep)).first;
       if (getenv("EGT_DEBUG_PLAN")) {
         const TiledSchedule& p = it->second;
         fprintf(stderr, "[egt plan] %ux%u fmt=%d M=%u: RB=%d WK=%d nw=%d KC=%d S=%d NT=%d grid=(%d,%d,%d) smem=%zu\n",
@@ -473,8 +475,13 @@ egt_status egt_spmv(const egt_dev_packed* h, const float* x, float* y, uint32_t 
     ctx.counters = w->counters;
   }
   CUDA_TRY(launch_tiled(h, sc, x, static_cast<int>(ldx), static_cast<int>(M), y,
-                        static_cast<int>(ldy), ctx));
+                        static_cast<int>(ldy), ctx, indep));
   return EGT_OK;
+}
+
+egt_status egt_spmv(const egt_dev_packed* h, const float* x, float* y, uint32_t M, uint32_t ldx,
+                    uint32_t ldy, void* stream) {
+  return egt_spmv_ex(h, x, y, M, ldx, ldy, 0u, stream);
 }
 
 egt_status egt_spmv_host(const egt_dev_packed* h, const float* x_host, size_t x_len, float* y_host,

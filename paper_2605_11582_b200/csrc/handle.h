@@ -86,13 +86,13 @@ struct LaunchCtx {
   uint32_t* counters = nullptr;  // split-K arrival counters (self-resetting)
 };
 
-TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms);
+TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms, bool indep);
 void force_plan(int RB, int S, int nw, int NST);  // tuning hook (0 = automatic)
 bool plan_forced();
 size_t tiled_workspace_floats(const egt_dev_packed* h, const TiledSchedule& sc, int M);
 
 cudaError_t launch_tiled(const egt_dev_packed* h, const TiledSchedule& sc, const float* x, int ldx,
-                         int M, float* y, int ldy, const LaunchCtx& ctx);
+                         int M, float* y, int ldy, const LaunchCtx& ctx, bool indep);
 cudaError_t launch_general(const egt_dev_packed* h, const float* x, int ldx, int M, float* y,
                            int ldy, const LaunchCtx& ctx);
 

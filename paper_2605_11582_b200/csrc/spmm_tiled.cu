@@ -21,6 +21,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 namespace egt_impl {
 using namespace egt_dev;
@@ -39,6 +40,8 @@ struct TiledArgs {
   float* partial;
   uint32_t* counters;
   int RB, WK, KC, S, NST;
+  int dbg;    // tuning experiments: 1 = empty kernel, 2 = weight stream only
+  int indep;  // x is not produced by the previous kernel in the stream
 };
 
 template <int FMT, int E>
@@ -116,24 +119,23 @@ __device__ __forceinline__ uint32_t place_hi(uint32_t r, uint32_t slot) {
   return prmt(r, 0u, slot ? 0x3244u : 0x4432u);
 }
 
-// B fragments of k-tile kt for every n-tile: lanes whose column (lane >> 2)
-// holds a present token read 16 bytes; the rest multiply by zero.
+// B fragments of k-tile kt for every n-tile.  D column n only depends on B
+// column n, so lanes whose column holds no token (lane >= LS) may read any
+// valid slot: they load lane & 7's without predication and their output
+// columns are never used.
 template <int NT>
 __device__ __forceinline__ void load_b(uint32_t (&b)[NT][4], const uint32_t* sB, int KTc, int kt,
                                        int lane, int LS, int M_left) {
+  const int ln = lane < LS ? lane : (lane & 7);
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) {
-    const int cols_here = min(8, 2 * (M_left - 4 * nt));
-    if ((lane >> 2) < cols_here) {
-      const uint4 t = *reinterpret_cast<const uint4*>(sB + ((nt * KTc + kt) * LS + lane) * 4);
-      b[nt][0] = t.x;
-      b[nt][1] = t.y;
-      b[nt][2] = t.z;
-      b[nt][3] = t.w;
-    } else {
-      b[nt][0] = b[nt][1] = b[nt][2] = b[nt][3] = 0u;
-    }
+    const uint4 t = *reinterpret_cast<const uint4*>(sB + ((nt * KTc + kt) * LS + ln) * 4);
+    b[nt][0] = t.x;
+    b[nt][1] = t.y;
+    b[nt][2] = t.z;
+    b[nt][3] = t.w;
   }
+  (void)M_left;
 }
 
 // j is a compile-time constant after unrolling; the branch folds away.
@@ -256,6 +258,10 @@ __global__ void __launch_bounds__(288, 2) tiled_spmm_kernel(const TiledArgs a) {
   constexpr int VB = val_lane_bytes(FMT), MB = meta_lane_bytes(FMT);
   extern __shared__ __align__(128) uint8_t smem_raw[];
   pdl_launch_dependents();
+  if (a.dbg == 1) {
+    pdl_wait();
+    return;
+  }
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nw = (blockDim.x >> 5) - 1;  // consumer warps
@@ -305,7 +311,10 @@ __global__ void __launch_bounds__(288, 2) tiled_spmm_kernel(const TiledArgs a) {
   if (warp == nw && lane == 0)
     for (int i = 0; i < min(NST, RBc); ++i) issue(i);
 
-  pdl_wait();  // x and the split-K workspace belong to earlier kernels
+  // x and the split-K workspace belong to earlier kernels.  An independent
+  // product (x not written by the previous kernel) skips the wait here and
+  // waits before exiting instead, so stream order stays transitive.
+  if (!a.indep) pdl_wait();
 
   // x slice -> fp16 hi/lo B fragments sB[nt][kt][lane < LS][4]: token m's hi
   // part is B column 2m (lanes 8m..8m+3), its rounding residual column 2m+1.
@@ -354,10 +363,20 @@ __global__ void __launch_bounds__(288, 2) tiled_spmm_kernel(const TiledArgs a) {
       float acc[NT][2];
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = 0.f;
-      for (int kql = warp; kql < KCs; kql += nw) {
-        Unit<FMT, E> u;
-        lds_unit<FMT, E>(u, st, KCs, kql, lane);
-        compute_unit<FMT, SS, NT>(u, sB, KTc, kql * 4, lane, LS, M_left, acc);
+      int kql = warp;
+      if (a.dbg != 2) {
+        for (; kql + nw < KCs; kql += 2 * nw) {  // two independent units in flight
+          Unit<FMT, E> u0, u1;
+          lds_unit<FMT, E>(u0, st, KCs, kql, lane);
+          lds_unit<FMT, E>(u1, st, KCs, kql + nw, lane);
+          compute_unit<FMT, SS, NT>(u0, sB, KTc, kql * 4, lane, LS, M_left, acc);
+          compute_unit<FMT, SS, NT>(u1, sB, KTc, (kql + nw) * 4, lane, LS, M_left, acc);
+        }
+        if (kql < KCs) {
+          Unit<FMT, E> u;
+          lds_unit<FMT, E>(u, st, KCs, kql, lane);
+          compute_unit<FMT, SS, NT>(u, sB, KTc, kql * 4, lane, LS, M_left, acc);
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(empty + s);
@@ -387,7 +406,10 @@ __global__ void __launch_bounds__(288, 2) tiled_spmm_kernel(const TiledArgs a) {
         a.partial[(static_cast<size_t>(blockIdx.y) * a.M + tok) * rows_pad + row] = v;
     }
   }
-  if (a.S == 1) return;
+  if (a.S == 1) {
+    if (a.indep) pdl_wait();
+    return;
+  }
 
   __shared__ int s_last;
   __threadfence();
@@ -468,7 +490,7 @@ void force_plan(int RB, int S, int nw, int NST) {
 }
 bool plan_forced() { return g_force[4] != 0; }
 
-TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms) {
+TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms, bool indep) {
   TiledSchedule best;
   const int RT = h->tiled.RT, KQ = h->tiled.KQ, E = h->tiled.E, f = h->format;
   const int NT = M <= 4 ? 1 : (M <= 8 ? 2 : 4);
@@ -485,6 +507,7 @@ TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms) {
     const int KC = (KQ + S - 1) / S;
     if (S > 1 && (S - 1) * KC >= KQ) continue;
     if (g_force[4] && S != g_force[1]) continue;
+    if (indep && S > 1) continue;  // concurrent independent launches share no workspace
     const int sb = stage_bytes_rt(f, KC, E);
     for (int RB = 1; RB <= 128; ++RB) {
       if (g_force[4] && RB != g_force[0]) continue;
@@ -529,7 +552,7 @@ TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms) {
   if (best_cost >= 1e300 && g_force[4]) {  // forced plan infeasible: automatic plan
     const int saved[5] = {g_force[0], g_force[1], g_force[2], g_force[3], g_force[4]};
     g_force[4] = 0;
-    best = plan_tiled(h, M, num_sms);
+    best = plan_tiled(h, M, num_sms, indep);
     for (int i = 0; i < 5; ++i) g_force[i] = saved[i];
   }
   return best;
@@ -541,7 +564,7 @@ size_t tiled_workspace_floats(const egt_dev_packed* h, const TiledSchedule& sc, 
 }
 
 cudaError_t launch_tiled(const egt_dev_packed* h, const TiledSchedule& sc, const float* x, int ldx,
-                         int M, float* y, int ldy, const LaunchCtx& ctx) {
+                         int M, float* y, int ldy, const LaunchCtx& ctx, bool indep) {
   TiledArgs a;
   a.vals = h->tiled.vals;
   a.meta = h->tiled.meta;
@@ -564,6 +587,9 @@ cudaError_t launch_tiled(const egt_dev_packed* h, const TiledSchedule& sc, const
   a.KC = sc.KC;
   a.S = sc.S;
   a.NST = sc.NST;
+  static const int dbg = getenv("EGT_DEBUG_MODE") ? atoi(getenv("EGT_DEBUG_MODE")) : 0;
+  a.dbg = dbg;
+  a.indep = indep && sc.S == 1 ? 1 : 0;
   void* fn = pick_kernel(h->format, h->tiled.SS, sc.NT);
   cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(sc.smem));

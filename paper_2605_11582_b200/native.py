@@ -73,6 +73,8 @@ SIGNATURES = {
     "egt_dev_packed_destroy": (C.c_int, [C.c_void_p]),
     "egt_dev_packed_query": (C.c_int, [C.c_void_p, C.POINTER(DevInfo)]),
     "egt_spmv": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p]),
+    "egt_spmv_ex": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                              C.c_void_p]),
     "egt_spmv_host": (C.c_int, [C.c_void_p, f32p, C.c_size_t, f32p, C.c_void_p]),
     "egt_dequant": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "egt_set_pdl": (None, [C.c_int]),

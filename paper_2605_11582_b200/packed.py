@@ -218,8 +218,10 @@ class DeviceMatrix:
         return self._h
 
     # products -------------------------------------------------------
-    def spmv_into(self, x, y, stream=None) -> None:
-        """y[M x rows] = x[M x cols] @ W^T on the device (torch CUDA f32 tensors)."""
+    def spmv_into(self, x, y, stream=None, independent: bool = False) -> None:
+        """y[M x rows] = x[M x cols] @ W^T on the device (torch CUDA f32 tensors).
+        independent=True: x was not written by the previous kernel on the
+        stream (EGT_SPMV_INDEPENDENT), so this product may overlap it."""
         if x.dim() == 1:
             M, ldx = 1, x.shape[0]
         else:
@@ -227,8 +229,8 @@ class DeviceMatrix:
         ldy = y.shape[-1] if y.dim() == 1 else y.stride(0)
         if x.dim() == 1 and x.shape[0] != self.cols:
             raise N.InvalidArgument(N.EGT_EINVAL, "spmv: input length differs from columns")
-        check(lib().egt_spmv(self._h, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), M, ldx, ldy,
-                             _stream_ptr(stream)))
+        check(lib().egt_spmv_ex(self._h, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), M, ldx, ldy,
+                                1 if independent else 0, _stream_ptr(stream)))
 
     def spmv(self, x, stream=None):
         """Device product; returns a new tensor [M x rows] (or [rows] for 1-D x)."""

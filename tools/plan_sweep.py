@@ -19,15 +19,15 @@ from bench import host_layer, shape_bytes  # noqa: E402
 from paper_2605_11582_b200 import native  # noqa: E402
 
 
-def time_plan(layers, x, ys, stream, reps=20):
+def time_plan(layers, x, ys, stream, reps=20, indep=False):
     for d, y in zip(layers, ys):  # warm-up (plans + workspace)
-        d.spmv_into(x, y, stream)
+        d.spmv_into(x, y, stream, independent=indep)
     stream.synchronize()
     g = torch.cuda.CUDAGraph()
     with torch.cuda.stream(stream):
         with torch.cuda.graph(g, stream=stream):
             for d, y in zip(layers, ys):
-                d.spmv_into(x, y, stream)
+                d.spmv_into(x, y, stream, independent=indep)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with torch.cuda.stream(stream):  # replay() runs on the current stream
         for _ in range(3):
@@ -44,6 +44,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--shapes", default="4096x4096,11008x4096,4096x11008")
     ap.add_argument("--n", type=int, default=2)
+    ap.add_argument("--indep", action="store_true", help="EGT_SPMV_INDEPENDENT launches")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "plan_sweep.json"))
     args = ap.parse_args()
     rng = np.random.default_rng(7)
@@ -60,17 +61,17 @@ def main():
         RT, KQ = (rows + 15) // 16, (cols + 127) // 128
         res = []
         L.egt_tune_force_plan(0, 0, 0, 0)
-        t = time_plan(layers, x, ys, stream)
+        t = time_plan(layers, x, ys, stream, indep=args.indep)
         res.append({"plan": "auto", "us": t, "GBps": shape_bytes(p) / t / 1e3})
-        for S in (1, 2, 3, 4, 6, 8):
+        for S in ((1,) if args.indep else (1, 2, 3, 4, 6, 8)):
             if S > KQ:
                 continue
-            for ctas in (148, 296):
+            for ctas in (74, 148, 296):
                 RB = max(1, math.ceil(RT * S / ctas))
                 for nw in (4, 8):
                     L.egt_tune_force_plan(RB, S, nw, 0)
                     try:
-                        t = time_plan(layers, x, ys, stream)
+                        t = time_plan(layers, x, ys, stream, indep=args.indep)
                     except Exception as e:  # noqa: BLE001
                         res.append({"plan": [RB, S, nw], "error": str(e)})
                         continue
