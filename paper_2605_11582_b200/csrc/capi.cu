@@ -459,9 +459,10 @@ egt_status egt_spmv_ex(const egt_dev_packed* h, const float* x, float* y, uint32
       it = h->plans.emplace(key, plan_tiled(h, M, num_sms(), indep)).first;
       if (getenv("EGT_DEBUG_PLAN")) {
         const TiledSchedule& p = it->second;
-        fprintf(stderr, "[egt plan] %ux%u fmt=%d M=%u: RB=%d WK=%d nw=%d KC=%d S=%d NT=%d grid=(%d,%d,%d) smem=%zu\n",
-                h->rows, h->cols, h->format, M, p.RB, p.WK, p.nw, p.KC, p.S, p.NT, p.grid_x, p.grid_y,
-                p.grid_z, p.smem);
+        fprintf(stderr,
+                "[egt plan] %ux%u fmt=%d M=%u indep=%d: RB=%d nw=%d KC=%d CH=%d NST=%d S=%d NT=%d grid=(%d,%d,%d) smem=%zu\n",
+                h->rows, h->cols, h->format, M, indep ? 1 : 0, p.RB, p.nw, p.KC, p.CH, p.NST, p.S, p.NT,
+                p.grid_x, p.grid_y, p.grid_z, p.smem);
       }
     }
     sc = it->second;

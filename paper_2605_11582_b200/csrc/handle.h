@@ -55,7 +55,8 @@ struct TiledSchedule {
   int NT = 1;  // mma n-tiles (4 tokens each) per CTA
   int NB = 1;  // n-blocks (CTAs along tokens)
   int nw = 8;   // consumer warps per CTA (+1 producer warp)
-  int NST = 1;  // shared-memory stages (row tiles in flight)
+  int NST = 1;  // shared-memory stages in flight
+  int CH = 1;   // k-quads per stage (chunk of a row tile)
   int grid_x = 1, grid_y = 1, grid_z = 1;
   size_t smem = 0;
 };

@@ -39,7 +39,7 @@ struct TiledArgs {
   int ldy;
   float* partial;
   uint32_t* counters;
-  int RB, WK, KC, S, NST;
+  int RB, WK, KC, S, NST, CH;
   int dbg;    // tuning experiments: 1 = empty kernel, 2 = weight stream only
   int indep;  // x is not produced by the previous kernel in the stream
 };
@@ -273,7 +273,7 @@ __global__ void __launch_bounds__(288, 2) tiled_spmm_kernel(const TiledArgs a) {
   const int m0 = blockIdx.z * TOK;
   const int M_left = a.M - m0;
   const int Mc = min(TOK, M_left);  // tokens of this CTA
-  const int sbytes = stage_bytes<FMT>(KCs, E);
+  const int sbytes = stage_bytes<FMT>(min(a.CH, KCs), E);
   const int NST = a.NST;
 
   // shared memory carve-up
@@ -295,21 +295,27 @@ __global__ void __launch_bounds__(288, 2) tiled_spmm_kernel(const TiledArgs a) {
 
   const uint64_t pol = evict_first_policy();
   const size_t blk_stride = static_cast<size_t>(a.KQ);
-  auto issue = [&](int i) {  // row tile i of this CTA -> stage i % NST
-    const int s = i % NST;
+  // Work is streamed in chunks q = (row tile i, k-quad chunk c) of CH k-quads:
+  // chunk q lands in stage q % NST.
+  const int CH = a.CH;
+  const int NCH = (KCs + CH - 1) / CH;
+  const int NQ = RBc * NCH;
+  auto issue = [&](int q) {
+    const int s = q % NST, i = q / NCH, c = q - i * NCH;
+    const int CHc = min(CH, KCs - c * CH);
     uint8_t* st = stages + static_cast<size_t>(s) * sbytes;
-    const size_t blk = static_cast<size_t>(a.rt_begin + rt0 + i) * blk_stride + kq0;
-    mbar_expect_tx(full + s, sbytes);
-    bulk_g2s(st, a.vals + blk * 32 * VB, KCs * 32 * VB, full + s, pol);
-    if constexpr (MB > 0) bulk_g2s(st + KCs * 32 * VB, a.meta + blk * 32 * MB, KCs * 32 * MB, full + s, pol);
+    const size_t blk = static_cast<size_t>(a.rt_begin + rt0 + i) * blk_stride + kq0 + c * CH;
+    mbar_expect_tx(full + s, stage_bytes<FMT>(CHc, E));
+    bulk_g2s(st, a.vals + blk * 32 * VB, CHc * 32 * VB, full + s, pol);
+    if constexpr (MB > 0) bulk_g2s(st + CHc * 32 * VB, a.meta + blk * 32 * MB, CHc * 32 * MB, full + s, pol);
     if constexpr (has_scales(FMT)) {
-      uint8_t* sp = st + KCs * 32 * (VB + MB);
-      bulk_g2s(sp, a.scales + blk * E * 16, KCs * E * 64, full + s, pol);
-      bulk_g2s(sp + KCs * E * 64, a.zps + blk * E * 16, KCs * E * 16, full + s, pol);
+      uint8_t* sp = st + CHc * 32 * (VB + MB);
+      bulk_g2s(sp, a.scales + blk * E * 16, CHc * E * 64, full + s, pol);
+      bulk_g2s(sp + CHc * E * 64, a.zps + blk * E * 16, CHc * E * 16, full + s, pol);
     }
   };
   if (warp == nw && lane == 0)
-    for (int i = 0; i < min(NST, RBc); ++i) issue(i);
+    for (int q = 0; q < min(NST, NQ); ++q) issue(q);
 
   // x and the split-K workspace belong to earlier kernels.  An independent
   // product (x not written by the previous kernel) skips the wait here and
@@ -350,36 +356,40 @@ __global__ void __launch_bounds__(288, 2) tiled_spmm_kernel(const TiledArgs a) {
   if (warp == nw) {
     // producer: refill each stage once all consumer warps released it
     if (lane == 0)
-      for (int i = NST; i < RBc; ++i) {
-        mbar_wait(empty + (i % NST), ((i / NST) - 1) & 1);
-        issue(i);
+      for (int q = NST; q < NQ; ++q) {
+        mbar_wait(empty + (q % NST), ((q / NST) - 1) & 1);
+        issue(q);
       }
   } else {
     const int g = lane >> 2, t = lane & 3;
+    int q = 0;
     for (int i = 0; i < RBc; ++i) {
-      const int s = i % NST;
-      mbar_wait(full + s, (i / NST) & 1);
-      const uint8_t* st = stages + static_cast<size_t>(s) * sbytes;
       float acc[NT][2];
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = 0.f;
-      int kql = warp;
-      if (a.dbg != 2) {
-        for (; kql + nw < KCs; kql += 2 * nw) {  // two independent units in flight
-          Unit<FMT, E> u0, u1;
-          lds_unit<FMT, E>(u0, st, KCs, kql, lane);
-          lds_unit<FMT, E>(u1, st, KCs, kql + nw, lane);
-          compute_unit<FMT, SS, NT>(u0, sB, KTc, kql * 4, lane, LS, M_left, acc);
-          compute_unit<FMT, SS, NT>(u1, sB, KTc, (kql + nw) * 4, lane, LS, M_left, acc);
+      for (int c = 0; c < NCH; ++c, ++q) {
+        const int s = q % NST;
+        const int CHc = min(CH, KCs - c * CH);
+        mbar_wait(full + s, (q / NST) & 1);
+        const uint8_t* st = stages + static_cast<size_t>(s) * sbytes;
+        int kql = warp;
+        if (a.dbg != 2) {
+          for (; kql + nw < CHc; kql += 2 * nw) {  // two independent units in flight
+            Unit<FMT, E> u0, u1;
+            lds_unit<FMT, E>(u0, st, CHc, kql, lane);
+            lds_unit<FMT, E>(u1, st, CHc, kql + nw, lane);
+            compute_unit<FMT, SS, NT>(u0, sB, KTc, (c * CH + kql) * 4, lane, LS, M_left, acc);
+            compute_unit<FMT, SS, NT>(u1, sB, KTc, (c * CH + kql + nw) * 4, lane, LS, M_left, acc);
+          }
+          if (kql < CHc) {
+            Unit<FMT, E> u;
+            lds_unit<FMT, E>(u, st, CHc, kql, lane);
+            compute_unit<FMT, SS, NT>(u, sB, KTc, (c * CH + kql) * 4, lane, LS, M_left, acc);
+          }
         }
-        if (kql < KCs) {
-          Unit<FMT, E> u;
-          lds_unit<FMT, E>(u, st, KCs, kql, lane);
-          compute_unit<FMT, SS, NT>(u, sB, KTc, kql * 4, lane, LS, M_left, acc);
-        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + s);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(empty + s);
       float* r = red + (static_cast<size_t>(i) * nw + warp) * Mc * 16;
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt)
@@ -498,7 +508,7 @@ TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms, bool indep
   const int tok = std::min(M, 4 * NT);
   const double unit_b = static_cast<double>(stage_bytes_rt(f, 1, E));
   const double sm_bw = 44.0;             // B/ns per SM (6.5 TB/s / 148)
-  const double unit_cycles = 70.0 * NT;  // issue slots per (warp, k-quad unit)
+  const double unit_cycles = 90.0 * NT;  // issue slots per (warp, k-quad unit)
   // <= ~100 KB and <= one CTA per SM: the next kernel's CTAs fit beside this
   // kernel's (programmatic dependent launch) and prefetch their weights.
   const size_t smem_cap = 100 * 1024;
@@ -508,29 +518,36 @@ TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms, bool indep
     if (S > 1 && (S - 1) * KC >= KQ) continue;
     if (g_force[4] && S != g_force[1]) continue;
     if (indep && S > 1) continue;  // concurrent independent launches share no workspace
-    const int sb = stage_bytes_rt(f, KC, E);
     for (int RB = 1; RB <= 128; ++RB) {
       if (g_force[4] && RB != g_force[0]) continue;
       const long grid = static_cast<long>((RT + RB - 1) / RB) * S * NB;
       if (grid > num_sms && RB < 128 && !g_force[4]) continue;  // one CTA per SM
-      int nst = std::max(1, std::min(RB, static_cast<int>((smem_cap - 24576) / sb)));
-      if (g_force[4] && g_force[3] > 0) nst = std::min(nst, g_force[3]);
       for (int nw : {4, 8}) {
         if (g_force[4] && g_force[2] > 0 && nw != g_force[2]) continue;
+        // chunk: all of the CTA's k-quads if that stage is small, else a
+        // multiple of 2*nw k-quads (two units per consumer warp) of ~24 KB
+        int CH = KC;
+        if (stage_bytes_rt(f, KC, E) > 24 * 1024) {
+          CH = std::max(2 * nw, (24 * 1024 / stage_bytes_rt(f, 1, E)) / (2 * nw) * (2 * nw));
+          CH = std::min(CH, KC);
+        }
+        const int sb = stage_bytes_rt(f, CH, E);
+        const int NQ = RB * ((KC + CH - 1) / CH);
         const size_t red = static_cast<size_t>(RB) * nw * tok * 64;
-        const size_t smem = (16 * nst + 127) / 128 * 128 + 128 +
-                            static_cast<size_t>(NT) * KC * 4 * 32 * std::min(4, tok) * 4 +
-                            static_cast<size_t>(nst) * sb + red;
+        const size_t sbx = static_cast<size_t>(NT) * KC * 4 * 32 * std::min(4, tok) * 4;
+        const long room = static_cast<long>(smem_cap) - static_cast<long>(sbx + red + 1280);
+        if (room < sb) continue;
+        int nst = std::max(1, std::min<int>(NQ, static_cast<int>(room / sb)));
+        if (g_force[4] && g_force[3] > 0) nst = std::min(nst, g_force[3]);
+        const size_t smem = (16 * nst + 127) / 128 * 128 + 128 + sbx + static_cast<size_t>(nst) * sb + red;
         if (smem > smem_cap) continue;
         const double ctas_per_sm = std::ceil(static_cast<double>(grid) / num_sms);
         const double bytes_cta = RB * KC * unit_b + KC * 512.0 * tok + (S > 1 ? 2.0 * RB * 64 * tok : 0.0);
         const double t_mem = ctas_per_sm * bytes_cta / sm_bw;
         const double units_per_warp = RB * std::ceil(static_cast<double>(KC) / nw);
         const double t_issue = ctas_per_sm * units_per_warp * unit_cycles * std::max(1.0, nw / 4.0) / 1.9;
-        const double in_flight = nst * sb;  // bytes a CTA can have outstanding
-        const double t_lat = 900.0 * std::ceil(RB * static_cast<double>(sb) / in_flight);
-        const double t_tail = (S > 1 ? 900.0 : 0.0) + 0.5 * (t_mem / ctas_per_sm);
-        const double cost = std::max(t_mem, t_issue) + t_lat * 0.2 + t_tail + ctas_per_sm * 600.0;
+        const double t_tail = (S > 1 ? 900.0 : 0.0) + 0.3 * (t_mem / ctas_per_sm) + (nst < NQ ? 300.0 : 0.0);
+        const double cost = std::max(t_mem, t_issue) + t_tail + ctas_per_sm * 600.0;
         if (cost < best_cost * 0.999) {
           best_cost = cost;
           best.RB = RB;
@@ -544,6 +561,7 @@ TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms, bool indep
           best.grid_z = NB;
           best.nw = nw;
           best.NST = nst;
+          best.CH = CH;
           best.smem = smem;
         }
       }
@@ -554,6 +572,8 @@ TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms, bool indep
     g_force[4] = 0;
     best = plan_tiled(h, M, num_sms, indep);
     for (int i = 0; i < 5; ++i) g_force[i] = saved[i];
+  } else if (best_cost >= 1e300 && indep) {  // no split-free plan fits: dependent plan
+    best = plan_tiled(h, M, num_sms, false);
   }
   return best;
 }
@@ -587,6 +607,7 @@ cudaError_t launch_tiled(const egt_dev_packed* h, const TiledSchedule& sc, const
   a.KC = sc.KC;
   a.S = sc.S;
   a.NST = sc.NST;
+  a.CH = sc.CH;
   static const int dbg = getenv("EGT_DEBUG_MODE") ? atoi(getenv("EGT_DEBUG_MODE")) : 0;
   a.dbg = dbg;
   a.indep = indep && sc.S == 1 ? 1 : 0;
