@@ -151,41 +151,50 @@ __device__ __forceinline__ void mma_sp_sel(int j, float (&d)[NT][4], const uint3
   }
 }
 
+// INT4 dequantisation on the tensor core.  The nibble c itself is the A
+// operand: an fp16 subnormal c * 2^-24 is exact and needs a single LOP3 per
+// pair (no exponent magic, no subtraction).  Row g+8's nibbles sit 4 bits
+// higher (16c * 2^-24), so one shift per k-tile feeds all four A registers;
+// the x16 is folded into row g+8's scale.  The zero point is applied after
+// the fact: a second mma with A = 1.0 under the same sparsity metadata yields
+// the sum of the kept x, and per scale step
+//   y_r += s_r * (2^24 * D_c - zp_r * D_1)      (2^20 for row g+8).
+constexpr float kTwo24 = 16777216.f;
+constexpr float kTwo20 = 1048576.f;
+constexpr uint32_t kOnes = 0x3C003C00u;  // half2(1, 1)
+
 template <int FMT, int SS, int NT>
 __device__ __forceinline__ void compute_unit(const Unit<FMT, 4 / SS>& u, const uint32_t* sB, int KTc,
                                              int kt_base, int lane, int LS, int M_left,
                                              float (&acc)[NT][2]) {
+  constexpr bool kOnesTrick = (FMT == I4_SP24 || FMT == I4_DENSE);
   float d[NT][4];
-  uint32_t zg = 0, zg8 = 0, zpair = 0;
+  float d1[NT][4];
+  uint32_t zpair = 0;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int e = j / SS;
     if (j % SS == 0) {
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) d[nt][0] = d[nt][1] = d[nt][2] = d[nt][3] = 0.f;
-      if constexpr (has_scales(FMT)) {
+      for (int nt = 0; nt < NT; ++nt) {
+        d[nt][0] = d[nt][1] = d[nt][2] = d[nt][3] = 0.f;
+        d1[nt][0] = d1[nt][1] = d1[nt][2] = d1[nt][3] = 0.f;
+      }
+      if constexpr (FMT == I4_SP14) {
         const uint32_t z0 = u.z[e] & 0xFFu, z1 = (u.z[e] >> 8) & 0xFFu;
-        zg = zp_magic(z0, z0);
-        zg8 = zp_magic(z1, z1);
         zpair = zp_magic(z0, z1);
       }
     }
     uint32_t b[NT][4];
     load_b<NT>(b, sB, KTc, kt_base + j, lane, LS, M_left);
-    if constexpr (FMT == I4_SP24 || FMT == F16_SP24) {
-      uint32_t a[4];
-      if constexpr (FMT == I4_SP24) {
-        const uint32_t w = u.v[j];
-        a[0] = hsub2_u32(nib2_magic(w), zg);
-        a[1] = hsub2_u32(nib2_magic(w >> 4), zg8);
-        a[2] = hsub2_u32(nib2_magic(w >> 8), zg);
-        a[3] = hsub2_u32(nib2_magic(w >> 12), zg8);
-      } else {
-        a[0] = u.v[4 * j + 0];
-        a[1] = u.v[4 * j + 1];
-        a[2] = u.v[4 * j + 2];
-        a[3] = u.v[4 * j + 3];
-      }
+    if constexpr (FMT == I4_SP24) {
+      const uint32_t w = u.v[j], w8 = w >> 8;
+      const uint32_t a[4] = {w & 0x000F000Fu, w & 0x00F000F0u, w8 & 0x000F000Fu, w8 & 0x00F000F0u};
+      const uint32_t ones[4] = {kOnes, kOnes, kOnes, kOnes};
+      mma_sp_sel<NT>(j, d, a, b, u.m[j >> 1]);
+      mma_sp_sel<NT>(j, d1, ones, b, u.m[j >> 1]);
+    } else if constexpr (FMT == F16_SP24) {
+      const uint32_t a[4] = {u.v[4 * j + 0], u.v[4 * j + 1], u.v[4 * j + 2], u.v[4 * j + 3]};
       mma_sp_sel<NT>(j, d, a, b, u.m[j >> 1]);
     } else if constexpr (FMT == I4_SP14 || FMT == F16_SP14) {
       uint32_t r0, r1;
@@ -206,19 +215,29 @@ __device__ __forceinline__ void compute_unit(const Unit<FMT, 4 / SS>& u, const u
       const uint32_t plane = (u.m[0] >> (16 + 8 * (j >> 1))) & 0xFFu;
       mma_sp_sel<NT>(j, d, a, b, 0x44444444u | (spread4(plane) * 0xAu));
     } else {  // I4_DENSE: two m16n8k16 per 32-column k-tile
-      const uint32_t w0 = u.v[2 * j], w1 = u.v[2 * j + 1];
-      const uint32_t a0 = hsub2_u32(nib2_magic(w0), zg), a1 = hsub2_u32(nib2_magic(w0 >> 4), zg8);
-      const uint32_t a2 = hsub2_u32(nib2_magic(w0 >> 8), zg), a3 = hsub2_u32(nib2_magic(w0 >> 12), zg8);
-      const uint32_t c0 = hsub2_u32(nib2_magic(w1), zg), c1 = hsub2_u32(nib2_magic(w1 >> 4), zg8);
-      const uint32_t c2 = hsub2_u32(nib2_magic(w1 >> 8), zg), c3 = hsub2_u32(nib2_magic(w1 >> 12), zg8);
+      const uint32_t w0 = u.v[2 * j], w1 = u.v[2 * j + 1], w08 = w0 >> 8, w18 = w1 >> 8;
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) {
-        mma_16816(d[nt], a0, a1, a2, a3, b[nt][0], b[nt][1]);
-        mma_16816(d[nt], c0, c1, c2, c3, b[nt][2], b[nt][3]);
+        mma_16816(d[nt], w0 & 0x000F000Fu, w0 & 0x00F000F0u, w08 & 0x000F000Fu, w08 & 0x00F000F0u, b[nt][0],
+                  b[nt][1]);
+        mma_16816(d[nt], w1 & 0x000F000Fu, w1 & 0x00F000F0u, w18 & 0x000F000Fu, w18 & 0x00F000F0u, b[nt][2],
+                  b[nt][3]);
+        mma_16816(d1[nt], kOnes, kOnes, kOnes, kOnes, b[nt][0], b[nt][1]);
+        mma_16816(d1[nt], kOnes, kOnes, kOnes, kOnes, b[nt][2], b[nt][3]);
       }
     }
     if (j % SS == SS - 1) {
-      if constexpr (has_scales(FMT)) {
+      if constexpr (kOnesTrick) {
+        const float sg = __uint_as_float(u.s[2 * e]), sg8 = __uint_as_float(u.s[2 * e + 1]);
+        const float cg = sg * kTwo24, cg8 = sg8 * kTwo20;
+        const float ng = -sg * static_cast<float>(u.z[e] & 0xFFu);
+        const float ng8 = -sg8 * static_cast<float>((u.z[e] >> 8) & 0xFFu);
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          acc[nt][0] = fmaf(cg, d[nt][0] + d[nt][1], fmaf(ng, d1[nt][0] + d1[nt][1], acc[nt][0]));
+          acc[nt][1] = fmaf(cg8, d[nt][2] + d[nt][3], fmaf(ng8, d1[nt][2] + d1[nt][3], acc[nt][1]));
+        }
+      } else if constexpr (has_scales(FMT)) {
         const float sg = __uint_as_float(u.s[2 * e]), sg8 = __uint_as_float(u.s[2 * e + 1]);
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
@@ -242,15 +261,15 @@ __host__ __device__ constexpr int stage_bytes(int KCs, int E) {
 }
 
 // One CTA = RB row tiles x KC k-quads (one of S K-slices) x 4*NT tokens.
-// Warp specialised: warp nw (the producer) streams whole row tiles -- every
-// block of the tile in the CTA's K-slice, 2-4 contiguous bulk copies -- into
-// an NST-deep ring of shared-memory stages (cp.async.bulk + mbarrier
-// complete_tx); the first NST row tiles are requested before the PDL wait,
-// since weights do not depend on the previous kernel.  The nw consumer warps
-// split each row tile's k-quads, dequantise in registers and issue mma.sp.
-// Per-warp partial sums are reduced in a fixed order; split-K (S > 1) partial
-// rows are summed by the last-arriving CTA of the row block, in slice order,
-// so results are deterministic.
+// Warp specialised: warp nw (the producer) streams chunks of row tiles -- CH
+// k-quads of one row tile, 2-4 contiguous bulk copies -- into an NST-deep
+// ring of shared-memory stages (cp.async.bulk + mbarrier complete_tx); the
+// first NST chunks are requested before the PDL wait, since weights do not
+// depend on the previous kernel.  The nw consumer warps split each chunk's
+// k-quads (two units in flight per warp), dequantise in registers and issue
+// mma.sp.  Per-warp partial sums are reduced in a fixed order; split-K
+// (S > 1) partial rows are summed by the last-arriving CTA of the row block,
+// in slice order, so results are deterministic.
 template <int FMT, int SS, int NT>
 __global__ void __launch_bounds__(288, 2) tiled_spmm_kernel(const TiledArgs a) {
   constexpr int E = 4 / SS;
@@ -524,11 +543,13 @@ TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms, bool indep
       if (grid > num_sms && RB < 128 && !g_force[4]) continue;  // one CTA per SM
       for (int nw : {4, 8}) {
         if (g_force[4] && g_force[2] > 0 && nw != g_force[2]) continue;
+        if (!g_force[4] && nw != 8) continue;
         // chunk: all of the CTA's k-quads if that stage is small, else a
         // multiple of 2*nw k-quads (two units per consumer warp) of ~24 KB
         int CH = KC;
-        if (stage_bytes_rt(f, KC, E) > 24 * 1024) {
-          CH = std::max(2 * nw, (24 * 1024 / stage_bytes_rt(f, 1, E)) / (2 * nw) * (2 * nw));
+        if (stage_bytes_rt(f, KC, E) > 40 * 1024) {  // equal chunks, 2 units per warp
+          const int nch = (stage_bytes_rt(f, KC, E) + 40 * 1024 - 1) / (40 * 1024);
+          CH = ((KC + nch - 1) / nch + 2 * nw - 1) / (2 * nw) * (2 * nw);
           CH = std::min(CH, KC);
         }
         const int sb = stage_bytes_rt(f, CH, E);
