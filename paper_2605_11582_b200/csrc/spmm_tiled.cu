@@ -124,18 +124,15 @@ __device__ __forceinline__ uint32_t place_hi(uint32_t r, uint32_t slot) {
 // valid slot: they load lane & 7's without predication and their output
 // columns are never used.
 template <int NT>
-__device__ __forceinline__ void load_b(uint32_t (&b)[NT][4], const uint32_t* sB, int KTc, int kt,
-                                       int lane, int LS, int M_left) {
-  const int ln = lane < LS ? lane : (lane & 7);
+__device__ __forceinline__ void load_b(uint32_t (&b)[NT][4], const uint32_t* pb, int nt_stride) {
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) {
-    const uint4 t = *reinterpret_cast<const uint4*>(sB + ((nt * KTc + kt) * LS + ln) * 4);
+    const uint4 t = *reinterpret_cast<const uint4*>(pb + nt * nt_stride);
     b[nt][0] = t.x;
     b[nt][1] = t.y;
     b[nt][2] = t.z;
     b[nt][3] = t.w;
   }
-  (void)M_left;
 }
 
 // j is a compile-time constant after unrolling; the branch folds away.
@@ -168,6 +165,11 @@ __device__ __forceinline__ void compute_unit(const Unit<FMT, 4 / SS>& u, const u
                                              int kt_base, int lane, int LS, int M_left,
                                              float (&acc)[NT][2]) {
   constexpr bool kOnesTrick = (FMT == I4_SP24 || FMT == I4_DENSE);
+  // B fragments: lanes whose column holds no token (lane >= LS) read lane&7's
+  // slot unpredicated -- D column n only depends on B column n, and the
+  // columns of absent tokens are never used.
+  const uint32_t* pb = sB + (kt_base * LS + (lane < LS ? lane : (lane & 7))) * 4;
+  (void)M_left;
   float d[NT][4];
   float d1[NT][4];
   uint32_t zpair = 0;
@@ -186,7 +188,7 @@ __device__ __forceinline__ void compute_unit(const Unit<FMT, 4 / SS>& u, const u
       }
     }
     uint32_t b[NT][4];
-    load_b<NT>(b, sB, KTc, kt_base + j, lane, LS, M_left);
+    load_b<NT>(b, pb + j * LS * 4, KTc * LS * 4);
     if constexpr (FMT == I4_SP24) {
       const uint32_t w = u.v[j], w8 = w >> 8;
       const uint32_t a[4] = {w & 0x000F000Fu, w & 0x00F000F0u, w8 & 0x000F000Fu, w8 & 0x00F000F0u};
@@ -271,7 +273,7 @@ __host__ __device__ constexpr int stage_bytes(int KCs, int E) {
 // (S > 1) partial rows are summed by the last-arriving CTA of the row block,
 // in slice order, so results are deterministic.
 template <int FMT, int SS, int NT>
-__global__ void __launch_bounds__(288, 2) tiled_spmm_kernel(const TiledArgs a) {
+__global__ void __launch_bounds__(416, 2) tiled_spmm_kernel(const TiledArgs a) {
   constexpr int E = 4 / SS;
   constexpr int TOK = 4 * NT;
   constexpr int VB = val_lane_bytes(FMT), MB = meta_lane_bytes(FMT);
@@ -319,8 +321,7 @@ __global__ void __launch_bounds__(288, 2) tiled_spmm_kernel(const TiledArgs a) {
   const int CH = a.CH;
   const int NCH = (KCs + CH - 1) / CH;
   const int NQ = RBc * NCH;
-  auto issue = [&](int q) {
-    const int s = q % NST, i = q / NCH, c = q - i * NCH;
+  auto issue = [&](int s, int i, int c) {  // chunk (row tile i, k-quad chunk c) -> stage s
     const int CHc = min(CH, KCs - c * CH);
     uint8_t* st = stages + static_cast<size_t>(s) * sbytes;
     const size_t blk = static_cast<size_t>(a.rt_begin + rt0 + i) * blk_stride + kq0 + c * CH;
@@ -333,8 +334,13 @@ __global__ void __launch_bounds__(288, 2) tiled_spmm_kernel(const TiledArgs a) {
       bulk_g2s(sp + CHc * E * 64, a.zps + blk * E * 16, CHc * E * 16, full + s, pol);
     }
   };
-  if (warp == nw && lane == 0)
-    for (int q = 0; q < min(NST, NQ); ++q) issue(q);
+  if (warp == nw && lane == 0) {
+    int i = 0, c = 0;
+    for (int q = 0; q < min(NST, NQ); ++q) {
+      issue(q, i, c);
+      if (++c == NCH) { c = 0; ++i; }
+    }
+  }
 
   // x and the split-K workspace belong to earlier kernels.  An independent
   // product (x not written by the previous kernel) skips the wait here and
@@ -374,22 +380,27 @@ __global__ void __launch_bounds__(288, 2) tiled_spmm_kernel(const TiledArgs a) {
 
   if (warp == nw) {
     // producer: refill each stage once all consumer warps released it
-    if (lane == 0)
+    if (lane == 0) {
+      int i = NST / NCH, c = NST - (NST / NCH) * NCH, s = 0;
+      uint32_t phase = 0;
       for (int q = NST; q < NQ; ++q) {
-        mbar_wait(empty + (q % NST), ((q / NST) - 1) & 1);
-        issue(q);
+        mbar_wait(empty + s, phase);
+        issue(s, i, c);
+        if (++c == NCH) { c = 0; ++i; }
+        if (++s == NST) { s = 0; phase ^= 1u; }
       }
+    }
   } else {
     const int g = lane >> 2, t = lane & 3;
-    int q = 0;
+    int s = 0;
+    uint32_t phase = 0;
     for (int i = 0; i < RBc; ++i) {
       float acc[NT][2];
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = 0.f;
-      for (int c = 0; c < NCH; ++c, ++q) {
-        const int s = q % NST;
+      for (int c = 0; c < NCH; ++c) {
         const int CHc = min(CH, KCs - c * CH);
-        mbar_wait(full + s, (q / NST) & 1);
+        mbar_wait(full + s, phase);
         const uint8_t* st = stages + static_cast<size_t>(s) * sbytes;
         int kql = warp;
         if (a.dbg != 2) {
@@ -408,6 +419,7 @@ __global__ void __launch_bounds__(288, 2) tiled_spmm_kernel(const TiledArgs a) {
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(empty + s);
+        if (++s == NST) { s = 0; phase ^= 1u; }
       }
       float* r = red + (static_cast<size_t>(i) * nw + warp) * Mc * 16;
 #pragma unroll
@@ -541,7 +553,7 @@ TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms, bool indep
       if (g_force[4] && RB != g_force[0]) continue;
       const long grid = static_cast<long>((RT + RB - 1) / RB) * S * NB;
       if (grid > num_sms && RB < 128 && !g_force[4]) continue;  // one CTA per SM
-      for (int nw : {4, 8}) {
+      for (int nw : {4, 8, 12}) {
         if (g_force[4] && g_force[2] > 0 && nw != g_force[2]) continue;
         if (!g_force[4] && nw != 8) continue;
         // chunk: all of the CTA's k-quads if that stage is small, else a

@@ -68,7 +68,7 @@ def main():
                 continue
             for ctas in ((24, 32, 48, 64, 96, 148) if args.indep else (74, 148, 296)):
                 RB = max(1, math.ceil(RT * S / ctas))
-                for nw in ((8,) if args.indep else (4, 8)):
+                for nw in ((8, 12) if args.indep else (4, 8)):
                     L.egt_tune_force_plan(RB, S, nw, 0)
                     try:
                         t = time_plan(layers, x, ys, stream, indep=args.indep)
