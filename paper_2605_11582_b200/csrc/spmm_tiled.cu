@@ -273,7 +273,7 @@ __host__ __device__ constexpr int stage_bytes(int KCs, int E) {
 // (S > 1) partial rows are summed by the last-arriving CTA of the row block,
 // in slice order, so results are deterministic.
 template <int FMT, int SS, int NT>
-__global__ void __launch_bounds__(416, 2) tiled_spmm_kernel(const TiledArgs a) {
+__global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(const TiledArgs a) {
   constexpr int E = 4 / SS;
   constexpr int TOK = 4 * NT;
   constexpr int VB = val_lane_bytes(FMT), MB = meta_lane_bytes(FMT);
@@ -349,30 +349,41 @@ __global__ void __launch_bounds__(416, 2) tiled_spmm_kernel(const TiledArgs a) {
 
   // x slice -> fp16 hi/lo B fragments sB[nt][kt][lane < LS][4]: token m's hi
   // part is B column 2m (lanes 8m..8m+3), its rounding residual column 2m+1.
-  // Straight from global (L2) with 8 independent loads per thread in flight.
+  // Every load of a thread is issued before the first conversion (one L2
+  // round trip for up to XU items per thread), then converted and stored.
+  constexpr int XU = 24;
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) {
     const int mc = min(4, Mc - 4 * nt);
     for (int m = 0; m < mc; ++m) {
       const float* xr = a.x + static_cast<size_t>(m0 + 4 * nt + m) * a.ldx;
       const int items = KTc * 16;
-#pragma unroll 8
-      for (int i = tid; i < items; i += blockDim.x) {
-        const int reg = i & 3, t = (i >> 2) & 3, kt = i >> 4;
-        const int k = (kq0 * 4 + kt) * 32 + 2 * t + 8 * reg;
-        float v0 = 0.f, v1 = 0.f;
-        if (k < a.cols) {
-          v0 = __ldg(xr + k);
-          v1 = __ldg(xr + k + 1);
+      for (int i0 = 0; i0 < items; i0 += XU * static_cast<int>(blockDim.x)) {
+        float2 v[XU];
+#pragma unroll
+        for (int u = 0; u < XU; ++u) {
+          const int i = i0 + tid + u * blockDim.x;
+          v[u] = make_float2(0.f, 0.f);
+          if (i < items) {
+            const int k = (kq0 * 4 + (i >> 4)) * 32 + 2 * ((i >> 2) & 3) + 8 * (i & 3);
+            if (k < a.cols) v[u] = make_float2(__ldg(xr + k), __ldg(xr + k + 1));
+          }
         }
-        const __half h0 = __float2half_rn(v0), h1 = __float2half_rn(v1);
-        const __half l0 = __float2half_rn(v0 - __half2float(h0));
-        const __half l1 = __float2half_rn(v1 - __half2float(h1));
-        uint32_t* row = sB + static_cast<size_t>(nt * KTc + kt) * LS * 4;
-        row[(8 * m + t) * 4 + reg] = static_cast<uint32_t>(__half_as_ushort(h0)) |
-                                     (static_cast<uint32_t>(__half_as_ushort(h1)) << 16);
-        row[(8 * m + 4 + t) * 4 + reg] = static_cast<uint32_t>(__half_as_ushort(l0)) |
-                                         (static_cast<uint32_t>(__half_as_ushort(l1)) << 16);
+#pragma unroll
+        for (int u = 0; u < XU; ++u) {
+          const int i = i0 + tid + u * blockDim.x;
+          if (i < items) {
+            const int reg = i & 3, t = (i >> 2) & 3, kt = i >> 4;
+            const __half h0 = __float2half_rn(v[u].x), h1 = __float2half_rn(v[u].y);
+            const __half l0 = __float2half_rn(v[u].x - __half2float(h0));
+            const __half l1 = __float2half_rn(v[u].y - __half2float(h1));
+            uint32_t* row = sB + static_cast<size_t>(nt * KTc + kt) * LS * 4;
+            row[(8 * m + t) * 4 + reg] = static_cast<uint32_t>(__half_as_ushort(h0)) |
+                                         (static_cast<uint32_t>(__half_as_ushort(h1)) << 16);
+            row[(8 * m + 4 + t) * 4 + reg] = static_cast<uint32_t>(__half_as_ushort(l0)) |
+                                             (static_cast<uint32_t>(__half_as_ushort(l1)) << 16);
+          }
+        }
       }
     }
   }
@@ -555,6 +566,7 @@ TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms, bool indep
       if (grid > num_sms && RB < 128 && !g_force[4]) continue;  // one CTA per SM
       for (int nw : {4, 8, 12}) {
         if (g_force[4] && g_force[2] > 0 && nw != g_force[2]) continue;
+        if (nw > 8 && NT > 1) continue;  // launch bounds: 288 threads when NT > 1
         if (!g_force[4] && nw != 8) continue;
         // chunk: all of the CTA's k-quads if that stage is small, else a
         // multiple of 2*nw k-quads (two units per consumer warp) of ~24 KB
