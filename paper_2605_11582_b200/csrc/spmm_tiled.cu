@@ -58,45 +58,74 @@ struct Unit {
 // A stage in shared memory holds one row tile's blocks for the CTA's KCs
 // k-quads, copied verbatim from HBM by the bulk-copy engine:
 //   [vals: KCs x 32 lanes x VB][meta: KCs x 32 x MB][scales: KCs x E x 16 f32][zps: KCs x E x 16 u8]
+// Shared-memory read cursor over one stage: a lane's A-operand bits, its
+// metadata, and its rows' scale / zero-point entries for the current unit,
+// plus its B-fragment slot.  Advancing by n units is five additions.
+struct Cursor {
+  const uint8_t* v;
+  const uint8_t* m;
+  const uint8_t* sc;
+  const uint8_t* zp;
+  const uint32_t* b;
+};
+
 template <int FMT, int E>
-__device__ __forceinline__ void lds_unit(Unit<FMT, E>& u, const uint8_t* st, int KCs, int kql,
-                                         int lane) {
+__device__ __forceinline__ Cursor make_cursor(const uint8_t* st, int CHc, int kql, int lane,
+                                              const uint32_t* sB, int kt0, int LS) {
   constexpr int VB = val_lane_bytes(FMT), MB = meta_lane_bytes(FMT);
-  const uint8_t* vp = st + (kql * 32 + lane) * VB;
+  const int g = lane >> 2;
+  Cursor c;
+  c.v = st + (kql * 32 + lane) * VB;
+  c.m = st + CHc * 32 * VB + (kql * 32 + lane) * MB;
+  const uint8_t* sp = st + CHc * 32 * (VB + MB);
+  c.sc = sp + kql * E * 64 + 8 * g;
+  c.zp = sp + CHc * E * 64 + kql * E * 16 + 2 * g;
+  c.b = sB + (kt0 * LS + (lane < LS ? lane : (lane & 7))) * 4;
+  return c;
+}
+
+template <int FMT, int E>
+__device__ __forceinline__ void advance(Cursor& c, int n, int LS) {
+  c.v += n * 32 * val_lane_bytes(FMT);
+  c.m += n * 32 * meta_lane_bytes(FMT);
+  c.sc += n * E * 64;
+  c.zp += n * E * 16;
+  c.b += n * 4 * LS * 4;
+}
+
+template <int FMT, int E>
+__device__ __forceinline__ void lds_unit(Unit<FMT, E>& u, const Cursor& c) {
+  constexpr int VB = val_lane_bytes(FMT), MB = meta_lane_bytes(FMT);
   if constexpr (VB == 8) {
-    const uint2 t = *reinterpret_cast<const uint2*>(vp);
+    const uint2 t = *reinterpret_cast<const uint2*>(c.v);
     u.v[0] = t.x;
     u.v[1] = t.y;
   } else {
 #pragma unroll
     for (int i = 0; i < VB / 16; ++i) {
-      const uint4 t = *reinterpret_cast<const uint4*>(vp + 16 * i);
+      const uint4 t = *reinterpret_cast<const uint4*>(c.v + 16 * i);
       u.v[4 * i + 0] = t.x;
       u.v[4 * i + 1] = t.y;
       u.v[4 * i + 2] = t.z;
       u.v[4 * i + 3] = t.w;
     }
   }
-  const uint8_t* mp = st + KCs * 32 * VB + (kql * 32 + lane) * MB;
   if constexpr (MB == 8) {
-    const uint2 t = *reinterpret_cast<const uint2*>(mp);
+    const uint2 t = *reinterpret_cast<const uint2*>(c.m);
     u.m[0] = t.x;
     u.m[1] = t.y;
   } else if constexpr (MB == 4) {
-    u.m[0] = *reinterpret_cast<const uint32_t*>(mp);
+    u.m[0] = *reinterpret_cast<const uint32_t*>(c.m);
   } else {
     u.m[0] = 0;
   }
   if constexpr (has_scales(FMT)) {
-    const int g = lane >> 2;
-    const uint8_t* sp = st + KCs * 32 * (VB + MB);
-    const uint8_t* zp = sp + KCs * E * 64;
 #pragma unroll
     for (int e = 0; e < E; ++e) {
-      const uint2 sc = *reinterpret_cast<const uint2*>(sp + (kql * E + e) * 64 + 8 * g);
+      const uint2 sc = *reinterpret_cast<const uint2*>(c.sc + e * 64);
       u.s[2 * e] = sc.x;
       u.s[2 * e + 1] = sc.y;
-      u.z[e] = *reinterpret_cast<const uint16_t*>(zp + (kql * E + e) * 16 + 2 * g);
+      u.z[e] = *reinterpret_cast<const uint16_t*>(c.zp + e * 16);
     }
   }
 }
@@ -161,15 +190,12 @@ constexpr float kTwo20 = 1048576.f;
 constexpr uint32_t kOnes = 0x3C003C00u;  // half2(1, 1)
 
 template <int FMT, int SS, int NT>
-__device__ __forceinline__ void compute_unit(const Unit<FMT, 4 / SS>& u, const uint32_t* sB, int KTc,
-                                             int kt_base, int lane, int LS, int M_left,
-                                             float (&acc)[NT][2]) {
+__device__ __forceinline__ void compute_unit(const Unit<FMT, 4 / SS>& u, const uint32_t* pb, int KTc,
+                                             int LS, float (&acc)[NT][2]) {
   constexpr bool kOnesTrick = (FMT == I4_SP24 || FMT == I4_DENSE);
   // B fragments: lanes whose column holds no token (lane >= LS) read lane&7's
   // slot unpredicated -- D column n only depends on B column n, and the
-  // columns of absent tokens are never used.
-  const uint32_t* pb = sB + (kt_base * LS + (lane < LS ? lane : (lane & 7))) * 4;
-  (void)M_left;
+  // columns of absent tokens are never used (make_cursor).
   float d[NT][4];
   float d1[NT][4];
   uint32_t zpair = 0;
@@ -272,7 +298,7 @@ __host__ __device__ constexpr int stage_bytes(int KCs, int E) {
 // mma.sp.  Per-warp partial sums are reduced in a fixed order; split-K
 // (S > 1) partial rows are summed by the last-arriving CTA of the row block,
 // in slice order, so results are deterministic.
-template <int FMT, int SS, int NT>
+template <int FMT, int SS, int NT, bool SINGLE>
 __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(const TiledArgs a) {
   constexpr int E = 4 / SS;
   constexpr int TOK = 4 * NT;
@@ -300,7 +326,8 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
   // shared memory carve-up
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
   uint64_t* empty = full + NST;
-  const int LS = 8 * min(4, Mc);  // sB lanes per (n-tile, k-tile): only present tokens
+  // sB lanes per (n-tile, k-tile): only present tokens (8 per token)
+  const int LS = SINGLE ? 8 : 8 * min(4, Mc);
   uint32_t* sB = reinterpret_cast<uint32_t*>(smem_raw + 16 * NST + 128 - (16 * NST) % 128);
   uint8_t* stages = reinterpret_cast<uint8_t*>(sB + NT * KTc * LS * 4);
   float* red = reinterpret_cast<float*>(stages + static_cast<size_t>(NST) * sbytes);  // [RB][nw][Mc][16]
@@ -413,19 +440,23 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
         const int CHc = min(CH, KCs - c * CH);
         mbar_wait(full + s, phase);
         const uint8_t* st = stages + static_cast<size_t>(s) * sbytes;
-        int kql = warp;
-        if (a.dbg != 2) {
+        if (a.dbg != 2 && warp < CHc) {
+          Cursor c0 = make_cursor<FMT, E>(st, CHc, warp, lane, sB, (c * CH + warp) * 4, LS);
+          int kql = warp;
           for (; kql + nw < CHc; kql += 2 * nw) {  // two independent units in flight
+            Cursor c1 = c0;
+            advance<FMT, E>(c1, nw, LS);
             Unit<FMT, E> u0, u1;
-            lds_unit<FMT, E>(u0, st, CHc, kql, lane);
-            lds_unit<FMT, E>(u1, st, CHc, kql + nw, lane);
-            compute_unit<FMT, SS, NT>(u0, sB, KTc, (c * CH + kql) * 4, lane, LS, M_left, acc);
-            compute_unit<FMT, SS, NT>(u1, sB, KTc, (c * CH + kql + nw) * 4, lane, LS, M_left, acc);
+            lds_unit<FMT, E>(u0, c0);
+            lds_unit<FMT, E>(u1, c1);
+            compute_unit<FMT, SS, NT>(u0, c0.b, KTc, LS, acc);
+            compute_unit<FMT, SS, NT>(u1, c1.b, KTc, LS, acc);
+            advance<FMT, E>(c0, 2 * nw, LS);
           }
           if (kql < CHc) {
             Unit<FMT, E> u;
-            lds_unit<FMT, E>(u, st, CHc, kql, lane);
-            compute_unit<FMT, SS, NT>(u, sB, KTc, (c * CH + kql) * 4, lane, LS, M_left, acc);
+            lds_unit<FMT, E>(u, c0);
+            compute_unit<FMT, SS, NT>(u, c0.b, KTc, LS, acc);
           }
         }
         __syncwarp();
@@ -489,14 +520,15 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
 
 namespace {
 
-template <int FMT, int SS, int NT>
+template <int FMT, int SS, int NT, bool SINGLE = false>
 void* kernel_ptr() {
-  return reinterpret_cast<void*>(&tiled_spmm_kernel<FMT, SS, NT>);
+  return reinterpret_cast<void*>(&tiled_spmm_kernel<FMT, SS, NT, SINGLE>);
 }
 
 template <int FMT, int SS>
-void* pick_nt(int NT) {
+void* pick_nt(int NT) {  // NT == 0: one token (NT = 1, compile-time B stride)
   switch (NT) {
+    case 0: return kernel_ptr<FMT, SS, 1, true>();
     case 1: return kernel_ptr<FMT, SS, 1>();
     case 2: return kernel_ptr<FMT, SS, 2>();
     default: return kernel_ptr<FMT, SS, 4>();
@@ -656,7 +688,7 @@ cudaError_t launch_tiled(const egt_dev_packed* h, const TiledSchedule& sc, const
   static const int dbg = getenv("EGT_DEBUG_MODE") ? atoi(getenv("EGT_DEBUG_MODE")) : 0;
   a.dbg = dbg;
   a.indep = indep && sc.S == 1 ? 1 : 0;
-  void* fn = pick_kernel(h->format, h->tiled.SS, sc.NT);
+  void* fn = pick_kernel(h->format, h->tiled.SS, M == 1 ? 0 : sc.NT);
   cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(sc.smem));
   if (err != cudaSuccess) return err;
