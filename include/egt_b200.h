@@ -169,9 +169,10 @@ EGT_API egt_status egt_dequant(const egt_dev_packed* h, float* w_dev, uint8_t* m
 EGT_API void egt_set_pdl(int enabled);
 
 /* Tuning hook: force the tiled launch plan for subsequent egt_spmv calls on
- * this thread (row tiles per CTA, K splits, consumer warps, stage depth;
- * rb = 0 restores the automatic planner).  Used by tools/plan_sweep.py. */
-EGT_API void egt_tune_force_plan(int rb, int s, int nw, int nst);
+ * this thread (row tiles per CTA, K splits, consumer warps, stage depth,
+ * k-quads per stage; 0 = automatic for that field, rb = 0 restores the
+ * automatic planner).  Used by tools/plan_sweep.py. */
+EGT_API void egt_tune_force_plan(int rb, int s, int nw, int nst, int ch);
 
 /* Number of kernels the library has launched on this thread (a counter the
  * benchmark reads to report gpu_launches). */

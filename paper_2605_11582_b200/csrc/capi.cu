@@ -267,7 +267,7 @@ int egt_abi_version(void) { return EGT_ABI_VERSION; }
 const char* egt_last_error(void) { return g_err.c_str(); }
 void egt_set_pdl(int enabled) { g_pdl = enabled != 0; }
 uint64_t egt_launch_count(void) { return launch_counter(); }
-void egt_tune_force_plan(int rb, int s, int nw, int nst) { force_plan(rb, s, nw, nst); }
+void egt_tune_force_plan(int rb, int s, int nw, int nst, int ch) { force_plan(rb, s, nw, nst, ch); }
 
 egt_status egt_dev_packed_create(const egt_packed_view* v, void* stream, egt_dev_packed** out) {
   using namespace egt_fmt;

@@ -88,7 +88,7 @@ struct LaunchCtx {
 };
 
 TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms, bool indep);
-void force_plan(int RB, int S, int nw, int NST);  // tuning hook (0 = automatic)
+void force_plan(int RB, int S, int nw, int NST, int CH);  // tuning hook (0 = automatic)
 bool plan_forced();
 size_t tiled_workspace_floats(const egt_dev_packed* h, const TiledSchedule& sc, int M);
 

@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
   constexpr int XU = 24;
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) {
-    const int mc = min(4, Mc - 4 * nt);
+    const int mc = a.dbg == 3 ? 0 : min(4, Mc - 4 * nt);
     for (int m = 0; m < mc; ++m) {
       const float* xr = a.x + static_cast<size_t>(m0 + 4 * nt + m) * a.ldx;
       const int items = KTc * 16;
@@ -564,13 +564,14 @@ int stage_bytes_rt(int fmt, int KCs, int E) {
 // launch: the busiest SM's HBM bytes at its 1/148 share of bandwidth, the
 // issue time of the dequant + mma.sp stream per scheduler, the number of
 // waves, and a fixed tail for the split-K reduction.
-static thread_local int g_force[5] = {0, 0, 0, 0, 0};  // RB, S, nw, NST, on
-void force_plan(int RB, int S, int nw, int NST) {
+static thread_local int g_force[6] = {0, 0, 0, 0, 0, 0};  // RB, S, nw, NST, on, CH
+void force_plan(int RB, int S, int nw, int NST, int CH) {
   g_force[0] = RB;
   g_force[1] = S;
   g_force[2] = nw;
   g_force[3] = NST;
   g_force[4] = RB > 0;
+  g_force[5] = CH;
 }
 bool plan_forced() { return g_force[4] != 0; }
 
@@ -602,17 +603,27 @@ TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms, bool indep
         if (!g_force[4] && nw != 8) continue;
         // chunk: all of the CTA's k-quads if that stage is small, else a
         // multiple of 2*nw k-quads (two units per consumer warp) of ~24 KB
-        int CH = KC;
-        if (stage_bytes_rt(f, KC, E) > 40 * 1024) {  // equal chunks, 2 units per warp
-          const int nch = (stage_bytes_rt(f, KC, E) + 40 * 1024 - 1) / (40 * 1024);
-          CH = ((KC + nch - 1) / nch + 2 * nw - 1) / (2 * nw) * (2 * nw);
-          CH = std::min(CH, KC);
-        }
-        const int sb = stage_bytes_rt(f, CH, E);
-        const int NQ = RB * ((KC + CH - 1) / CH);
+        // chunk: the largest multiple of 2*nw k-quads (two units per consumer
+        // warp) that still leaves room for >= 3 stages (>= 2 if it must)
         const size_t red = static_cast<size_t>(RB) * nw * tok * 64;
         const size_t sbx = static_cast<size_t>(NT) * KC * 4 * 32 * std::min(4, tok) * 4;
         const long room = static_cast<long>(smem_cap) - static_cast<long>(sbx + red + 1280);
+        int CH = 0;
+        for (int want : {3, 2, 1}) {
+          for (int ch = (KC + 2 * nw - 1) / (2 * nw) * (2 * nw); ch >= 2 * nw; ch -= 2 * nw) {
+            const int chc = std::min(ch, KC);
+            const int nq = RB * ((KC + chc - 1) / chc);
+            if (room >= static_cast<long>(std::min(want, nq)) * stage_bytes_rt(f, chc, E)) {
+              CH = chc;
+              break;
+            }
+          }
+          if (CH) break;
+        }
+        if (!CH) CH = std::min(KC, 2 * nw);
+        if (g_force[4] && g_force[5] > 0) CH = std::min(g_force[5], KC);
+        const int sb = stage_bytes_rt(f, CH, E);
+        const int NQ = RB * ((KC + CH - 1) / CH);
         if (room < sb) continue;
         int nst = std::max(1, std::min<int>(NQ, static_cast<int>(room / sb)));
         if (g_force[4] && g_force[3] > 0) nst = std::min(nst, g_force[3]);
@@ -645,10 +656,10 @@ TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms, bool indep
     }
   }
   if (best_cost >= 1e300 && g_force[4]) {  // forced plan infeasible: automatic plan
-    const int saved[5] = {g_force[0], g_force[1], g_force[2], g_force[3], g_force[4]};
+    const int saved = g_force[4];
     g_force[4] = 0;
     best = plan_tiled(h, M, num_sms, indep);
-    for (int i = 0; i < 5; ++i) g_force[i] = saved[i];
+    g_force[4] = saved;
   } else if (best_cost >= 1e300 && indep) {  // no split-free plan fits: dependent plan
     best = plan_tiled(h, M, num_sms, false);
   }

@@ -60,7 +60,7 @@ def main():
         ys = [torch.empty(rows, device="cuda") for _ in range(copies)]
         RT, KQ = (rows + 15) // 16, (cols + 127) // 128
         res = []
-        L.egt_tune_force_plan(0, 0, 0, 0)
+        L.egt_tune_force_plan(0, 0, 0, 0, 0)
         t = time_plan(layers, x, ys, stream, indep=args.indep)
         res.append({"plan": "auto", "us": t, "GBps": shape_bytes(p) / t / 1e3})
         for S in ((1,) if args.indep else (1, 2, 3, 4, 6, 8)):
@@ -68,16 +68,16 @@ def main():
                 continue
             for ctas in ((24, 32, 48, 64, 96, 148) if args.indep else (74, 148, 296)):
                 RB = max(1, math.ceil(RT * S / ctas))
-                for nw in ((8, 12) if args.indep else (4, 8)):
-                    L.egt_tune_force_plan(RB, S, nw, 0)
+                for nw, ch in (((8, 0), (8, 16), (8, 32), (12, 24)) if args.indep else ((4, 0), (8, 0))):
+                    L.egt_tune_force_plan(RB, S, nw, 0, ch)
                     try:
                         t = time_plan(layers, x, ys, stream, indep=args.indep)
                     except Exception as e:  # noqa: BLE001
-                        res.append({"plan": [RB, S, nw], "error": str(e)})
+                        res.append({"plan": [RB, S, nw, ch], "error": str(e)})
                         continue
-                    res.append({"plan": [RB, S, nw], "grid": math.ceil(RT / RB) * S, "us": round(t, 3),
+                    res.append({"plan": [RB, S, nw, ch], "grid": math.ceil(RT / RB) * S, "us": round(t, 3),
                                 "GBps": round(shape_bytes(p) / t / 1e3, 1)})
-        L.egt_tune_force_plan(0, 0, 0, 0)
+        L.egt_tune_force_plan(0, 0, 0, 0, 0)
         res.sort(key=lambda r: r.get("us", 1e9))
         results[spec] = res
         print(spec, json.dumps(res[:8]), flush=True)

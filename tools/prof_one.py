@@ -26,7 +26,7 @@ x = torch.from_numpy(rng.uniform(-1, 1, cols).astype(np.float32)).cuda()
 y = torch.empty(rows, device="cuda")
 if a.plan:
     rb, s, nw = map(int, a.plan.split(","))
-    native.lib().egt_tune_force_plan(rb, s, nw, 0)
+    native.lib().egt_tune_force_plan(rb, s, nw, 0, 0)
 for i in range(a.launches):
     layers[i % 4].spmv_into(x, y, independent=a.indep)
 torch.cuda.synchronize()
