@@ -597,6 +597,14 @@ TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms, bool indep
       if (g_force[4] && RB != g_force[0]) continue;
       const long grid = static_cast<long>((RT + RB - 1) / RB) * S * NB;
       if (grid > num_sms && RB < 128 && !g_force[4]) continue;  // one CTA per SM
+      if (indep && !g_force[4]) {
+        // Independent products run several launches side by side on disjoint
+        // SMs; measured best (tools/plan_sweep.py --indep) is ~250 KB of
+        // weights per CTA, i.e. few CTAs per launch.
+        const double total = static_cast<double>(RT) * KQ * unit_b;
+        const int target = std::max(16, std::min(num_sms, static_cast<int>(total / (250.0 * 1024) + 0.5)));
+        if (RB != (RT + target - 1) / target) continue;
+      }
       for (int nw : {4, 8, 12}) {
         if (g_force[4] && g_force[2] > 0 && nw != g_force[2]) continue;
         if (nw > 8 && NT > 1) continue;  // launch bounds: 288 threads when NT > 1
