@@ -347,11 +347,13 @@ def run_ours(args):
 
     peak, peak_kind = _peak_hbm()
     achieved = step_bytes / (ms_per_step * 1e-3) / 1e9
-    traffic = None
+    traffic = traffic_by_shape = None
     tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tf):
+    if os.path.exists(tf):  # committed ncu capture of the same kernels (per launch)
         try:
-            traffic = json.load(open(tf)).get("dram_bytes_per_launch_by_shape")
+            tj = json.load(open(tf))
+            traffic = tj.get("traffic_per_launch_step_average")
+            traffic_by_shape = tj.get("dram_bytes_per_launch_by_shape")
         except Exception:
             traffic = None
 
@@ -389,8 +391,11 @@ def run_ours(args):
                 "ms_per_step": round(1e3 * e2e_s / e2e_steps, 4), "steps": e2e_steps},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "traffic_note": "dram bytes per launch averaged over the step's shape mix; algorithmic "
+                                     f"per-launch average {step_bytes // len(layers)}",
+                     "traffic_by_shape": traffic_by_shape,
                      "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})",
-                     "kernel": "egt_impl::tiled_spmm_kernel<I4_SP24,SS=4,NT=1>",
+                     "kernel": "egt_impl::tiled_spmm_kernel<I4_SP24,SS=4,NT=1,SINGLE>",
                      "algorithmic_bytes_per_launch": {k: v["bytes_per_call"] for k, v in per_shape.items()}},
         "cpu_baseline": cpu_baseline,
         "clocks": clocks,

@@ -612,12 +612,13 @@ TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms, bool indep
         // chunk: all of the CTA's k-quads if that stage is small, else a
         // multiple of 2*nw k-quads (two units per consumer warp) of ~24 KB
         // chunk: the largest multiple of 2*nw k-quads (two units per consumer
-        // warp) that still leaves room for >= 3 stages (>= 2 if it must)
+        // warp) that still leaves room for >= 2 stages (measured: whole
+        // 4096-column row tiles in 2 stages beat 16-k-quad chunks in 5)
         const size_t red = static_cast<size_t>(RB) * nw * tok * 64;
         const size_t sbx = static_cast<size_t>(NT) * KC * 4 * 32 * std::min(4, tok) * 4;
         const long room = static_cast<long>(smem_cap) - static_cast<long>(sbx + red + 1280);
         int CH = 0;
-        for (int want : {3, 2, 1}) {
+        for (int want : {2, 1}) {
           for (int ch = (KC + 2 * nw - 1) / (2 * nw) * (2 * nw); ch >= 2 * nw; ch -= 2 * nw) {
             const int chc = std::min(ch, KC);
             const int nq = RB * ((KC + chc - 1) / chc);
