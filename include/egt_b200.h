@@ -178,6 +178,94 @@ EGT_API void egt_tune_force_plan(int rb, int s, int nw, int nst, int ch);
  * benchmark reads to report gpu_launches). */
 EGT_API uint64_t egt_launch_count(void);
 
+/* ---------------- verify substrate: the multi-token pass -----------------
+ * ModelConfig (model.hpp:32-43) and forward (model.hpp:71-72,
+ * model.cpp:118-202) over packed layers; prefix-tree verification
+ * (verify_parallel, decode.hpp:163-170, decode.cpp:336-421). */
+typedef struct egt_model_config {
+  uint32_t vocab_size, d_model, n_layers, n_heads, d_ff, max_positions;
+} egt_model_config;
+
+typedef struct egt_model egt_model; /* opaque; layer handles must outlive it */
+
+/* embedding: host [vocab x d_model] f32.  layers: n_layers*6 handles in the
+ * order wq, wk, wv, wo, ff1, ff2 (linear_layer_names, model.cpp:379-388),
+ * any mixed-dispatch format; head: [vocab x d_model]. */
+EGT_API egt_status egt_model_create(const egt_model_config* cfg, const float* embedding,
+                                    const egt_dev_packed* const* layers, const egt_dev_packed* head,
+                                    void* stream, egt_model** out);
+EGT_API egt_status egt_model_destroy(egt_model* m);
+
+/* logits_dev[M x vocab] = forward(tokens, mask, positions); host tokens /
+ * positions (int32) and visibility bits (bit q*M+k = query q sees key k,
+ * LSB-first).  A query row with no visible key gets zero attention output. */
+EGT_API egt_status egt_forward(const egt_model* m, const int32_t* tokens, const int32_t* positions,
+                               const uint8_t* mask_bits, uint32_t M, float* logits_dev, void* stream);
+
+/* out[i] = src_dev[rows[i] * ld + cols[i]] (host index lists, host output). */
+EGT_API egt_status egt_gather(const float* src_dev, uint64_t ld, const uint32_t* rows,
+                              const uint32_t* cols, uint32_t n, float* out, void* stream);
+
+/* PrefixTrie (trie.hpp:72-90) as parent links: node 0 is the root, parents
+ * precede children, children are visited in ascending token order. */
+typedef struct egt_trie_view {
+  uint32_t n_nodes;
+  const uint32_t* token;
+  const uint32_t* parent; /* parent[0] ignored */
+  const int64_t* payload; /* kNoPayload = -1 */
+} egt_trie_view;
+
+/* DecodeSession (decode.hpp:43-50): prompt + beams, each beam's generated
+ * tokens concatenated in beam order. */
+typedef struct egt_session_view {
+  const int32_t* prompt;
+  uint32_t prompt_len;
+  uint32_t n_beams;
+  const uint32_t* beam_node;
+  const double* beam_log_prob;
+  const uint32_t* beam_len;
+  const int32_t* beam_tokens;
+} egt_session_view;
+
+typedef struct egt_verify_out {
+  uint32_t n_selected;    /* <= beam_size */
+  double* score;          /* [beam_size] */
+  int64_t* payload;       /* [beam_size] */
+  uint32_t* beam;         /* [beam_size] */
+  uint32_t* len;          /* [beam_size] tokens per selected sequence */
+  int32_t* tokens;        /* [beam_size * tokens_stride] */
+  uint32_t tokens_stride;
+  uint32_t flattened_nodes;
+  uint32_t rows;          /* M of the forward pass */
+} egt_verify_out;
+
+/* flatten_subtree + build_tree_mask + verify_parallel (decode.cpp:209-421):
+ * one masked forward over every remaining node of the beams' subtrees, the
+ * trie-restricted log-softmax, B-score recursion, leaf ranking (ties: beam,
+ * then flat index) and traceback of the top beam_size. */
+EGT_API egt_status egt_verify_parallel(const egt_model* m, const egt_trie_view* trie,
+                                       const egt_session_view* session, int beam_size,
+                                       egt_verify_out* out, void* stream);
+
+/* decode (decode.cpp:423-483): trie-constrained beam steps (one block-diagonal
+ * forward each) until the cost model fires (mode 1), a forced depth is
+ * reached (mode 2) or every beam is finished (mode 0, autoregressive); then
+ * one parallel verification.  stats = {steps, forward_passes, trigger_step,
+ * flattened_nodes}. */
+typedef struct egt_decode_options {
+  int beam_size;
+  int mode; /* 0 autoregressive, 1 ptpv, 2 ptpv forced at depth */
+  int forced_depth;
+  double t_step, alpha, beta; /* CostModel, seconds */
+  uint64_t node_cap;
+} egt_decode_options;
+
+EGT_API egt_status egt_decode(const egt_model* m, const egt_trie_view* trie, const int32_t* prompt,
+                              uint32_t prompt_len, const egt_decode_options* opt, egt_verify_out* out,
+                              int32_t stats[4], void* stream);
+
+EGT_API egt_status egt_model_query(const egt_model* m, egt_model_config* cfg);
+
 /* ---------------- host encoder (C++; byte-identical to the reference) ----
  * Masks are PruneMask bitmaps (bit r*cols+c, LSB-first). */
 

@@ -1,0 +1,332 @@
+// The multi-token pass of prefix-tree verification on the device: the
+// reference's forward_impl (model.cpp:118-202) over packed layers.
+//   x = embedding[token] + positions[pos]                    (model.cpp:141-143)
+//   per layer: a = rmsnorm(x); q,k,v = a W^T (SparseGemv, M rows)
+//              per head: s = (q k^T) * scale, masked softmax, empty row -> 0
+//              x += o Wo^T; b = rmsnorm(x); x += silu(b ff1^T) ff2^T
+//   logits = rmsnorm(x) head^T
+// The linear layers are the tensor-core SpGEMM of spmm_tiled.cu (any of the
+// mixed-dispatch formats); the rest are small f32 kernels here.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "device_common.cuh"
+#include "egt_b200.h"
+#include "handle.h"
+
+namespace egt_impl {
+void set_last_error(const std::string& msg);
+}
+
+struct egt_model {
+  egt_model_config cfg{};
+  float* emb = nullptr;  // [vocab x d]
+  float* pos = nullptr;  // [max_positions x d] sinusoidal table
+  std::vector<const egt_dev_packed*> layers;  // n_layers * 6: wq wk wv wo ff1 ff2
+  const egt_dev_packed* head = nullptr;
+  int device = 0;
+};
+
+namespace {
+
+using egt_impl::launch_counter;
+
+constexpr float kNormEps = 1e-6f;  // model.cpp:27
+
+__global__ void embed_kernel(const int* tok, const int* pos, const float* emb, const float* ptab,
+                             float* x, int M, int d) {
+  const int i = blockIdx.x;
+  for (int c = threadIdx.x; c < d; c += blockDim.x)
+    x[static_cast<size_t>(i) * d + c] = emb[static_cast<size_t>(tok[i]) * d + c] + ptab[static_cast<size_t>(pos[i]) * d + c];
+}
+
+// rmsnorm (model.cpp:57-67): y = x / sqrt(mean(x^2) + eps), one block per row.
+__global__ void rmsnorm_kernel(const float* x, float* y, int d) {
+  const float* xr = x + static_cast<size_t>(blockIdx.x) * d;
+  float ss = 0.f;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) ss = fmaf(xr[c], xr[c], ss);
+  __shared__ float red[32];
+  ss = egt_dev::warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    v = egt_dev::warp_sum(v);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  const float inv = 1.0f / sqrtf(red[0] / static_cast<float>(d) + kNormEps);
+  float* yr = y + static_cast<size_t>(blockIdx.x) * d;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) yr[c] = xr[c] * inv;
+}
+
+// Batched f32 GEMM tile kernel for attention: C[b](i,j) = alpha * sum_k A[b](i,k) * B'[b](k,j)
+// with B' = B^T (BT: B is [n x K] row-major) or B (B is [K x n]).
+template <bool BT>
+__global__ void attn_gemm_kernel(const float* A, int lda, size_t sa, const float* B, int ldb, size_t sb,
+                                 float* C, int ldc, size_t sc, int m, int n, int K, float alpha) {
+  __shared__ float As[16][17];
+  __shared__ float Bs[16][17];
+  const int b = blockIdx.z;
+  const int ty = threadIdx.y, tx = threadIdx.x;
+  const int i = blockIdx.y * 16 + ty, j = blockIdx.x * 16 + tx;
+  A += b * sa;
+  B += b * sb;
+  C += b * sc;
+  float acc = 0.f;
+  for (int k0 = 0; k0 < K; k0 += 16) {
+    const int ka = k0 + tx, kb = k0 + ty;
+    As[ty][tx] = (i < m && ka < K) ? A[static_cast<size_t>(i) * lda + ka] : 0.f;
+    if (BT)
+      Bs[ty][tx] = (blockIdx.x * 16 + ty < n && k0 + tx < K) ? B[static_cast<size_t>(blockIdx.x * 16 + ty) * ldb + k0 + tx] : 0.f;
+    else
+      Bs[ty][tx] = (kb < K && j < n) ? B[static_cast<size_t>(kb) * ldb + j] : 0.f;
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) acc = fmaf(As[ty][kk], BT ? Bs[tx][kk] : Bs[kk][tx], acc);
+    __syncthreads();
+  }
+  if (i < m && j < n) C[static_cast<size_t>(i) * ldc + j] = acc * alpha;
+}
+
+// Masked softmax of one score row per warp (model.cpp:169-182); a query row
+// with no visible key becomes all zeros (model.cpp:173).  mask: bit q*M+k.
+__global__ void masked_softmax_kernel(float* S, const uint8_t* mask, int M, int H) {
+  const int row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= M * H) return;
+  const int q = row % M;
+  float* s = S + static_cast<size_t>(row) * M;
+  auto vis = [&](int k) {
+    const size_t bit = static_cast<size_t>(q) * M + k;
+    return (mask[bit >> 3] >> (bit & 7)) & 1;
+  };
+  float m = -INFINITY;
+  for (int k = lane; k < M; k += 32)
+    if (vis(k)) m = fmaxf(m, s[k]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (!isfinite(m)) {
+    for (int k = lane; k < M; k += 32) s[k] = 0.f;
+    return;
+  }
+  float z = 0.f;
+  for (int k = lane; k < M; k += 32) {
+    const float e = vis(k) ? expf(s[k] - m) : 0.f;
+    s[k] = e;
+    z += e;
+  }
+  z = egt_dev::warp_sum(z);
+  for (int k = lane; k < M; k += 32) s[k] = s[k] / z;
+}
+
+__global__ void silu_kernel(float* f, size_t n) {  // model.cpp:80-84
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const float v = f[i];
+    f[i] = v * (1.0f / (1.0f + expf(-v)));
+  }
+}
+
+__global__ void add_kernel(float* x, const float* t, size_t n) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    x[i] = x[i] + t[i];
+}
+
+__global__ void gather_kernel(const float* src, uint64_t ld, const uint32_t* idx, uint32_t n, float* out) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = src[static_cast<uint64_t>(idx[i]) * ld + idx[n + i]];
+}
+
+egt_status fail(egt_status s, const std::string& m) {
+  egt_impl::set_last_error(m);
+  return s;
+}
+
+#define MCUDA(expr)                                                                   \
+  do {                                                                                \
+    cudaError_t e_ = (expr);                                                          \
+    if (e_ != cudaSuccess) return fail(EGT_ECUDA, std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+unsigned grid_for(size_t n) { return static_cast<unsigned>(std::min<size_t>((n + 255) / 256, 4096)); }
+
+}  // namespace
+
+extern "C" {
+
+egt_status egt_model_create(const egt_model_config* cfg, const float* embedding,
+                            const egt_dev_packed* const* layers, const egt_dev_packed* head,
+                            void* stream, egt_model** out) {
+  if (!cfg || !embedding || !layers || !head || !out) return fail(EGT_EINVAL, "model: null argument");
+  *out = nullptr;
+  const egt_model_config& c = *cfg;  // ModelConfig::validate (model.hpp:41-42)
+  if (!c.vocab_size || !c.d_model || !c.n_layers || !c.n_heads || !c.d_ff || !c.max_positions)
+    return fail(EGT_EINVAL, "model config: every dimension must be positive");
+  if (c.d_model % c.n_heads != 0) return fail(EGT_EINVAL, "model config: d_model must be divisible by n_heads");
+  const uint32_t d = c.d_model;
+  for (uint32_t l = 0; l < c.n_layers; ++l) {
+    const uint32_t shape[6][2] = {{d, d}, {d, d}, {d, d}, {d, d}, {c.d_ff, d}, {d, c.d_ff}};
+    for (int j = 0; j < 6; ++j) {
+      const egt_dev_packed* h = layers[6 * l + j];
+      if (!h || h->rows != shape[j][0] || h->cols != shape[j][1])
+        return fail(EGT_EINVAL, "model: layer " + std::to_string(l) + " matrix " + std::to_string(j) +
+                                    " has the wrong shape");
+    }
+  }
+  if (head->rows != c.vocab_size || head->cols != d) return fail(EGT_EINVAL, "model: head has the wrong shape");
+  auto m = new egt_model();
+  m->cfg = c;
+  m->layers.assign(layers, layers + 6 * c.n_layers);
+  m->head = head;
+  cudaGetDevice(&m->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  // sinusoidal_positions (model.cpp:44-54): double math, stored f32
+  std::vector<float> ptab(static_cast<size_t>(c.max_positions) * d);
+  for (uint32_t p = 0; p < c.max_positions; ++p)
+    for (uint32_t i = 0; i < d; ++i) {
+      const double expo = static_cast<double>(2 * (i / 2)) / static_cast<double>(d);
+      const double angle = static_cast<double>(p) / std::pow(10000.0, expo);
+      ptab[static_cast<size_t>(p) * d + i] = static_cast<float>(i % 2 == 0 ? std::sin(angle) : std::cos(angle));
+    }
+  const size_t eb = static_cast<size_t>(c.vocab_size) * d * sizeof(float);
+  const size_t pb = ptab.size() * sizeof(float);
+  if (cudaMalloc(&m->emb, eb) != cudaSuccess || cudaMalloc(&m->pos, pb) != cudaSuccess) {
+    cudaFree(m->emb);
+    delete m;
+    return fail(EGT_ECUDA, "model: device allocation failed");
+  }
+  cudaMemcpyAsync(m->emb, embedding, eb, cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(m->pos, ptab.data(), pb, cudaMemcpyHostToDevice, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) {
+    cudaFree(m->emb);
+    cudaFree(m->pos);
+    delete m;
+    return fail(EGT_ECUDA, "model: upload failed");
+  }
+  *out = m;
+  return EGT_OK;
+}
+
+egt_status egt_model_query(const egt_model* m, egt_model_config* cfg) {
+  if (!m || !cfg) return fail(EGT_EINVAL, "model: null argument");
+  *cfg = m->cfg;
+  return EGT_OK;
+}
+
+egt_status egt_model_destroy(egt_model* m) {
+  if (m) {
+    cudaFree(m->emb);
+    cudaFree(m->pos);
+    delete m;
+  }
+  return EGT_OK;
+}
+
+egt_status egt_forward(const egt_model* m, const int32_t* tokens, const int32_t* positions,
+                       const uint8_t* mask_bits, uint32_t M, float* logits, void* stream) {
+  if (!m || !tokens || !positions || !mask_bits || !logits) return fail(EGT_EINVAL, "forward: null argument");
+  const egt_model_config& c = m->cfg;
+  if (M == 0) return fail(EGT_EINVAL, "forward: empty token sequence");  // model.cpp:123
+  for (uint32_t i = 0; i < M; ++i) {                                        // model.cpp:128-135
+    if (tokens[i] < 0 || static_cast<uint32_t>(tokens[i]) >= c.vocab_size)
+      return fail(EGT_EINVAL, "forward: token out of range");
+    if (positions[i] < 0 || static_cast<uint32_t>(positions[i]) >= c.max_positions)
+      return fail(EGT_EINVAL, "forward: position out of range");
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t d = c.d_model, dff = c.d_ff, H = c.n_heads, dh = d / H;
+  const size_t Md = M * d;
+  const size_t mask_bytes = (static_cast<size_t>(M) * M + 7) / 8;
+  const size_t floats = 6 * Md + M * dff + H * static_cast<size_t>(M) * M;
+  char* scratch = nullptr;
+  MCUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch),
+                        floats * sizeof(float) + 2 * M * sizeof(int) + mask_bytes + 64, s));
+  float* x = reinterpret_cast<float*>(scratch);
+  float* a = x + Md;
+  float* q = a + Md;
+  float* k = q + Md;
+  float* v = k + Md;
+  float* o = v + Md;
+  float* f1 = o + Md;
+  float* S = f1 + M * dff;
+  int* dtok = reinterpret_cast<int*>(S + H * static_cast<size_t>(M) * M);
+  int* dpos = dtok + M;
+  uint8_t* dmask = reinterpret_cast<uint8_t*>(dpos + M);
+  egt_status st = EGT_OK;
+  auto lin = [&](const egt_dev_packed* h, const float* in, float* outp, uint32_t flags) {
+    if (st == EGT_OK) st = egt_spmv_ex(h, in, outp, M, h->cols, h->rows, flags, stream);
+  };
+  cudaMemcpyAsync(dtok, tokens, M * sizeof(int), cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(dpos, positions, M * sizeof(int), cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(dmask, mask_bits, mask_bytes, cudaMemcpyHostToDevice, s);
+  embed_kernel<<<M, 256, 0, s>>>(dtok, dpos, m->emb, m->pos, x, static_cast<int>(M), static_cast<int>(d));
+  ++launch_counter();
+  const float att_scale = 1.0f / std::sqrt(static_cast<float>(dh));  // model.cpp:139
+  const dim3 tb(16, 16);
+  for (uint32_t l = 0; l < c.n_layers && st == EGT_OK; ++l) {
+    const egt_dev_packed* const* w = m->layers.data() + 6 * l;
+    rmsnorm_kernel<<<M, 256, 0, s>>>(x, a, static_cast<int>(d));
+    ++launch_counter();
+    lin(w[0], a, q, 0);
+    lin(w[1], a, k, EGT_SPMV_INDEPENDENT);  // K and V read `a`, not the previous product
+    lin(w[2], a, v, EGT_SPMV_INDEPENDENT);
+    // scores per head: S[h] = (q_h k_h^T) * scale
+    attn_gemm_kernel<true><<<dim3((M + 15) / 16, (M + 15) / 16, H), tb, 0, s>>>(
+        q, static_cast<int>(d), dh, k, static_cast<int>(d), dh, S, static_cast<int>(M),
+        static_cast<size_t>(M) * M, static_cast<int>(M), static_cast<int>(M), static_cast<int>(dh), att_scale);
+    masked_softmax_kernel<<<(M * H + 7) / 8, 256, 0, s>>>(S, dmask, static_cast<int>(M), static_cast<int>(H));
+    attn_gemm_kernel<false><<<dim3((dh + 15) / 16, (M + 15) / 16, H), tb, 0, s>>>(
+        S, static_cast<int>(M), static_cast<size_t>(M) * M, v, static_cast<int>(d), dh, o, static_cast<int>(d),
+        dh, static_cast<int>(M), static_cast<int>(dh), static_cast<int>(M), 1.0f);
+    launch_counter() += 3;
+    lin(w[3], o, a, 0);  // a <- o Wo^T
+    add_kernel<<<grid_for(Md), 256, 0, s>>>(x, a, Md);
+    rmsnorm_kernel<<<M, 256, 0, s>>>(x, a, static_cast<int>(d));
+    launch_counter() += 2;
+    lin(w[4], a, f1, 0);
+    silu_kernel<<<grid_for(M * dff), 256, 0, s>>>(f1, M * dff);
+    ++launch_counter();
+    lin(w[5], f1, a, 0);
+    add_kernel<<<grid_for(Md), 256, 0, s>>>(x, a, Md);
+    ++launch_counter();
+  }
+  if (st == EGT_OK) {
+    rmsnorm_kernel<<<M, 256, 0, s>>>(x, a, static_cast<int>(d));
+    ++launch_counter();
+    lin(m->head, a, logits, 0);
+  }
+  cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(scratch, s);
+  if (st != EGT_OK) return st;
+  if (e != cudaSuccess) return fail(EGT_ECUDA, std::string("forward: ") + cudaGetErrorString(e));
+  return EGT_OK;
+}
+
+egt_status egt_gather(const float* src, uint64_t ld, const uint32_t* rows, const uint32_t* cols,
+                      uint32_t n, float* out, void* stream) {
+  if (n == 0) return EGT_OK;
+  if (!src || !rows || !cols || !out) return fail(EGT_EINVAL, "gather: null argument");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::vector<uint32_t> idx(2 * static_cast<size_t>(n));
+  std::memcpy(idx.data(), rows, n * sizeof(uint32_t));
+  std::memcpy(idx.data() + n, cols, n * sizeof(uint32_t));
+  char* buf = nullptr;
+  MCUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf), idx.size() * 4 + n * 4, s));
+  uint32_t* didx = reinterpret_cast<uint32_t*>(buf);
+  float* dout = reinterpret_cast<float*>(didx + idx.size());
+  cudaMemcpyAsync(didx, idx.data(), idx.size() * 4, cudaMemcpyHostToDevice, s);
+  gather_kernel<<<(n + 255) / 256, 256, 0, s>>>(src, ld, didx, n, dout);
+  ++launch_counter();
+  cudaMemcpyAsync(out, dout, n * 4, cudaMemcpyDeviceToHost, s);
+  cudaFreeAsync(buf, s);
+  MCUDA(cudaStreamSynchronize(s));
+  return EGT_OK;
+}
+
+}  // extern "C"

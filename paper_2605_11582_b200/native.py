@@ -63,6 +63,32 @@ class DevInfo(C.Structure):
     ]
 
 
+class ModelConfig(C.Structure):
+    _fields_ = [(k, C.c_uint32) for k in ("vocab_size", "d_model", "n_layers", "n_heads", "d_ff", "max_positions")]
+
+
+class TrieView(C.Structure):
+    _fields_ = [("n_nodes", C.c_uint32), ("token", u32p), ("parent", u32p),
+                ("payload", C.POINTER(C.c_int64))]
+
+
+class SessionView(C.Structure):
+    _fields_ = [("prompt", C.POINTER(C.c_int32)), ("prompt_len", C.c_uint32), ("n_beams", C.c_uint32),
+                ("beam_node", u32p), ("beam_log_prob", f64p), ("beam_len", u32p),
+                ("beam_tokens", C.POINTER(C.c_int32))]
+
+
+class VerifyOut(C.Structure):
+    _fields_ = [("n_selected", C.c_uint32), ("score", f64p), ("payload", C.POINTER(C.c_int64)),
+                ("beam", u32p), ("len", u32p), ("tokens", C.POINTER(C.c_int32)),
+                ("tokens_stride", C.c_uint32), ("flattened_nodes", C.c_uint32), ("rows", C.c_uint32)]
+
+
+class DecodeOptions(C.Structure):
+    _fields_ = [("beam_size", C.c_int), ("mode", C.c_int), ("forced_depth", C.c_int), ("t_step", C.c_double),
+                ("alpha", C.c_double), ("beta", C.c_double), ("node_cap", C.c_uint64)]
+
+
 # every symbol include/egt_b200.h declares, with its signature
 SIGNATURES = {
     "egt_abi_version": (C.c_int, []),
@@ -88,6 +114,23 @@ SIGNATURES = {
     "egt_host_pack_f32": (C.c_int, [u8p, C.c_uint32, C.c_uint32, C.c_int, C.c_int, f32p, u16p, szp, f32p, szp]),
     "egt_host_footprint": (C.c_int, [C.POINTER(PackedView), u64p, f64p]),
 }
+
+_MODEL_SIGNATURES = {
+    "egt_model_create": (C.c_int, [C.POINTER(ModelConfig), f32p, C.POINTER(C.c_void_p), C.c_void_p, C.c_void_p,
+                                   C.POINTER(C.c_void_p)]),
+    "egt_model_destroy": (C.c_int, [C.c_void_p]),
+    "egt_model_query": (C.c_int, [C.c_void_p, C.POINTER(ModelConfig)]),
+    "egt_forward": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32), u8p, C.c_uint32,
+                              C.c_void_p, C.c_void_p]),
+    "egt_gather": (C.c_int, [C.c_void_p, C.c_uint64, u32p, u32p, C.c_uint32, f32p, C.c_void_p]),
+    "egt_verify_parallel": (C.c_int, [C.c_void_p, C.POINTER(TrieView), C.POINTER(SessionView), C.c_int,
+                                      C.POINTER(VerifyOut), C.c_void_p]),
+    "egt_decode": (C.c_int, [C.c_void_p, C.POINTER(TrieView), C.POINTER(C.c_int32), C.c_uint32,
+                             C.POINTER(DecodeOptions), C.POINTER(VerifyOut), C.POINTER(C.c_int32), C.c_void_p]),
+}
+
+
+SIGNATURES.update(_MODEL_SIGNATURES)
 
 _lib = None
 
