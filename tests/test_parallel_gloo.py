@@ -51,8 +51,8 @@ def _worker(rank, world, port, q):
         rows, cols = 136, 256
         w = rng.uniform(-1, 1, (rows, cols)).astype(np.float32)
         mask = random_nm_mask(rng, rows, cols, 2)
-        q = port_o.quantize(w, np.full(rows, 128, np.uint32), mask)
-        p = port_o.pack_int4(mask, rows, cols, q, 2)
+        qm = port_o.quantize(w, np.full(rows, 128, np.uint32), mask)
+        p = port_o.pack_int4(mask, rows, cols, qm, 2)
         X = rng.uniform(-1, 1, (3, cols)).astype(np.float32)
         full = np.stack([port_o.spmv(p, x) for x in X])
         plan = RowShardPlan.make(rows, world)
