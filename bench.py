@@ -22,6 +22,8 @@ from __future__ import annotations
 
 import argparse
 import json
+
+import numpy as np
 import math
 import os
 import subprocess
@@ -191,6 +193,60 @@ def run_reference(args):
     return 0
 
 
+# ------------------------------------------------------------------ sharded layers
+SHARDED_SHAPES = [(5120, 13824), (8192, 28672)]
+
+
+def measure_sharded(world, rank, stream, torch, egt, rng):
+    from paper_2605_11582_b200.parallel import RowShardPlan, gather_rows
+
+    out = {}
+    for rows, cols in SHARDED_SHAPES:
+        p = host_layer(np.random.default_rng(rows), rows, cols)  # identical on every rank
+        full = egt.DeviceMatrix.from_packed(p, stream)
+        plan = RowShardPlan.make(rows, world)
+        r0, r1 = plan.local(rank)
+        local = full.slice_rows(r0, r1)
+        x = torch.from_numpy(np.random.default_rng(cols).uniform(-1, 1, cols).astype(np.float32)).cuda()
+        reps = 50
+
+        def run(with_gather):
+            with torch.cuda.stream(stream):
+                y = local.spmv(x, stream)
+                if with_gather and world > 1:
+                    y = gather_rows(y, plan)
+            return y
+
+        for _ in range(5):
+            run(True)
+        torch.cuda.synchronize()
+        res = {}
+        for name, g in (("gemv_only", False), ("gemv_allgather", True)):
+            if world > 1:
+                torch.distributed.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                e0.record(stream)
+                for _ in range(reps):
+                    run(g)
+                e1.record(stream)
+            e1.synchronize()
+            t = torch.tensor([e0.elapsed_time(e1) * 1e3 / reps], device="cuda")
+            if world > 1:
+                torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            res[name + "_us"] = round(float(t.item()), 3)
+        if world > 1:  # parity of the gathered output against this rank's full product
+            yf = full.spmv(x).cpu().numpy()
+            yg = run(True).cpu().numpy()
+            res["gathered_equals_unsharded_max_rel_err"] = float(np.max(np.abs(yg - yf) / (1 + np.abs(yf))))
+        b = shape_bytes(p)
+        res.update({"bytes_total": b, "rows_per_gpu": r1 - r0,
+                    "GBps_per_gpu_gemv": round((b / world) / res["gemv_only_us"] / 1e3, 1)})
+        out[f"{rows}x{cols}"] = res
+        del full, local
+    return out
+
+
 # ------------------------------------------------------------------ our arm
 def run_ours(args):
     import numpy as np
@@ -325,6 +381,10 @@ def run_ours(args):
                                        "bytes_per_call": b, "copies": len(sel)}
         del sub
 
+    # BASELINE configs[4]: 13B/70B-shaped layers row-sharded across the ranks,
+    # local SparseGemv + NCCL all-gather of the y slices (world 1: unsharded)
+    sharded = measure_sharded(world, rank, stream, torch, egt, rng) if not args.no_sharded else None
+
     # e2e through the public API with pinned host buffers
     x_host = {c: torch.from_numpy(xs[c]).pin_memory() for c in xs}
     y_host = torch.empty(layers[-1].rows, dtype=torch.float32).pin_memory()
@@ -386,7 +446,8 @@ def run_ours(args):
                    "launch": "EGT_SPMV_INDEPENDENT (the sweep's GEMVs do not consume each other's output)",
                    "dependent_chain": {"ms_per_step": round(dep_ms, 4),
                                        "GBps": round(step_bytes / (dep_ms * 1e-3) / 1e9, 1)},
-                   "per_shape": per_shape},
+                   "per_shape": per_shape,
+                   "sharded_13b_70b": sharded},
         "e2e": {"value": round(e2e_value, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": round(1e3 * e2e_s / e2e_steps, 4), "steps": e2e_steps},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -415,6 +476,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-sharded", action="store_true", help="skip the 13B/70B row-sharded layers")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -244,3 +244,27 @@ def test_effective_matrix_probe(egt, port, torch, tmp_path):
             with open(os.path.join(out, f"probe_n{n}.json"), "w") as f:
                 json.dump({"w_eff": w_eff.tolist(), "want": want.tolist()}, f)
         assert np.allclose(w_eff, want, rtol=1e-5, atol=1e-6), f"n={n}: tensor-core layout mismatch"
+
+
+def test_sharded_spmv_nccl_single_rank(egt, port, torch):
+    """ShardedSpmv over an NCCL group (world 1 on one GPU): local shard
+    product + all-gather equals the unsharded product."""
+    import os
+
+    import torch.distributed as dist
+
+    from paper_2605_11582_b200.parallel import ShardedSpmv
+
+    if not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        rng = np.random.default_rng(131)
+        p, _, _ = make_int4(rng, 640, 1024, 2, 128, port)
+        d = _dev(egt, p)
+        sh = ShardedSpmv(d)
+        x = torch.from_numpy(rng.uniform(-1, 1, 1024).astype(np.float32)).cuda()
+        assert torch.equal(sh(x), d.spmv(x))
+    finally:
+        dist.destroy_process_group()
