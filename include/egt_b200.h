@@ -266,6 +266,43 @@ EGT_API egt_status egt_decode(const egt_model* m, const egt_trie_view* trie, con
 
 EGT_API egt_status egt_model_query(const egt_model* m, egt_model_config* cfg);
 
+/* ---------------- persistent GEMV programs (decode chains) ----------------
+ * A program is an ordered list of batch-1 products y = residual + W f(x)
+ * executed by ONE persistent launch (one CTA per SM): every CTA streams its
+ * share of each op's weights through one shared-memory ring, so op j+1's
+ * weights are in flight while op j's output is still being produced.
+ * Replaces a chain of spmv calls (packed.cpp:211-220) with the forward_impl
+ * glue fused in: input transforms rmsnorm (model.cpp:57-67) and silu
+ * (model.cpp:80-84), residual epilogue x += t (model.cpp:186,190).
+ *
+ * wait: -1 if x / residual are ready when the launch starts, else the index
+ * w < j such that ops 0..w must be complete before op j reads its inputs.
+ * create rejects (EGT_EINVAL) any read-after-write, write-after-read or
+ * write-after-write overlap with an earlier op that `wait` does not cover.
+ * Pointers are bound at create; run is stream-ordered and graph-capturable.
+ * Only tiled-path matrices (group sizes multiple of 32) are accepted. */
+#define EGT_INPUT_NONE 0u
+#define EGT_INPUT_RMSNORM 1u /* x / sqrt(mean(x^2) + eps) over the whole vector */
+#define EGT_INPUT_SILU 2u    /* x / (1 + exp(-x)) */
+typedef struct egt_program_op {
+  const egt_dev_packed* w;
+  const float* x;        /* cols floats, 16-byte aligned */
+  float* y;              /* rows floats */
+  const float* residual; /* NULL, or rows floats added to the product (may equal y) */
+  uint32_t input;        /* EGT_INPUT_* */
+  float eps;             /* rmsnorm epsilon (model.cpp:27: 1e-6) */
+  int32_t wait;
+} egt_program_op;
+typedef struct egt_program egt_program; /* opaque; matrices must outlive it */
+typedef struct egt_program_info {
+  uint32_t n_ops, grid, stages, stage_bytes, smem_bytes;
+} egt_program_info;
+EGT_API egt_status egt_program_create(const egt_program_op* ops, uint32_t n_ops, void* stream,
+                                      egt_program** out);
+EGT_API egt_status egt_program_run(const egt_program* p, void* stream);
+EGT_API egt_status egt_program_query(const egt_program* p, egt_program_info* info);
+EGT_API egt_status egt_program_destroy(egt_program* p);
+
 /* ---------------- host encoder (C++; byte-identical to the reference) ----
  * Masks are PruneMask bitmaps (bit r*cols+c, LSB-first). */
 

@@ -18,6 +18,7 @@
 // y = sum_g s_g * sum_k (c_k - z_g) x_k.
 #include "device_common.cuh"
 #include "handle.h"
+#include "tiled_compute.cuh"
 
 #include <algorithm>
 #include <cmath>
@@ -44,249 +45,6 @@ struct TiledArgs {
   int indep;  // x is not produced by the previous kernel in the stream
 };
 
-template <int FMT, int E>
-struct Unit {
-  static constexpr int NV = val_lane_bytes(FMT) / 4;
-  static constexpr int NM = meta_lane_bytes(FMT) > 0 ? meta_lane_bytes(FMT) / 4 : 1;
-  static constexpr int NS = has_scales(FMT) ? E : 1;
-  uint32_t v[NV];
-  uint32_t m[NM];
-  uint32_t s[2 * NS];
-  uint32_t z[NS];
-};
-
-// A stage in shared memory holds one row tile's blocks for the CTA's KCs
-// k-quads, copied verbatim from HBM by the bulk-copy engine:
-//   [vals: KCs x 32 lanes x VB][meta: KCs x 32 x MB][scales: KCs x E x 16 f32][zps: KCs x E x 16 u8]
-// Shared-memory read cursor over one stage: a lane's A-operand bits, its
-// metadata, and its rows' scale / zero-point entries for the current unit,
-// plus its B-fragment slot.  Advancing by n units is five additions.
-struct Cursor {
-  const uint8_t* v;
-  const uint8_t* m;
-  const uint8_t* sc;
-  const uint8_t* zp;
-  const uint32_t* b;
-};
-
-template <int FMT, int E>
-__device__ __forceinline__ Cursor make_cursor(const uint8_t* st, int CHc, int kql, int lane,
-                                              const uint32_t* sB, int kt0, int LS) {
-  constexpr int VB = val_lane_bytes(FMT), MB = meta_lane_bytes(FMT);
-  const int g = lane >> 2;
-  Cursor c;
-  c.v = st + (kql * 32 + lane) * VB;
-  c.m = st + CHc * 32 * VB + (kql * 32 + lane) * MB;
-  const uint8_t* sp = st + CHc * 32 * (VB + MB);
-  c.sc = sp + kql * E * 64 + 8 * g;
-  c.zp = sp + CHc * E * 64 + kql * E * 16 + 2 * g;
-  c.b = sB + (kt0 * LS + (lane < LS ? lane : (lane & 7))) * 4;
-  return c;
-}
-
-template <int FMT, int E>
-__device__ __forceinline__ void advance(Cursor& c, int n, int LS) {
-  c.v += n * 32 * val_lane_bytes(FMT);
-  c.m += n * 32 * meta_lane_bytes(FMT);
-  c.sc += n * E * 64;
-  c.zp += n * E * 16;
-  c.b += n * 4 * LS * 4;
-}
-
-template <int FMT, int E>
-__device__ __forceinline__ void lds_unit(Unit<FMT, E>& u, const Cursor& c) {
-  constexpr int VB = val_lane_bytes(FMT), MB = meta_lane_bytes(FMT);
-  if constexpr (VB == 8) {
-    const uint2 t = *reinterpret_cast<const uint2*>(c.v);
-    u.v[0] = t.x;
-    u.v[1] = t.y;
-  } else {
-#pragma unroll
-    for (int i = 0; i < VB / 16; ++i) {
-      const uint4 t = *reinterpret_cast<const uint4*>(c.v + 16 * i);
-      u.v[4 * i + 0] = t.x;
-      u.v[4 * i + 1] = t.y;
-      u.v[4 * i + 2] = t.z;
-      u.v[4 * i + 3] = t.w;
-    }
-  }
-  if constexpr (MB == 8) {
-    const uint2 t = *reinterpret_cast<const uint2*>(c.m);
-    u.m[0] = t.x;
-    u.m[1] = t.y;
-  } else if constexpr (MB == 4) {
-    u.m[0] = *reinterpret_cast<const uint32_t*>(c.m);
-  } else {
-    u.m[0] = 0;
-  }
-  if constexpr (has_scales(FMT)) {
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-      const uint2 sc = *reinterpret_cast<const uint2*>(c.sc + e * 64);
-      u.s[2 * e] = sc.x;
-      u.s[2 * e + 1] = sc.y;
-      u.z[e] = *reinterpret_cast<const uint16_t*>(c.zp + e * 16);
-    }
-  }
-}
-
-// Bit q of the 8-bit plane -> bit 4q.
-__device__ __forceinline__ uint32_t spread4(uint32_t p) {
-  uint32_t x = p & 0xFFu;
-  x = (x | (x << 12)) & 0x000F000Fu;
-  x = (x | (x << 6)) & 0x03030303u;
-  x = (x | (x << 3)) & 0x11111111u;
-  return x;
-}
-
-// 1:4 placement: the kept value (low or high half of r) goes to slot 0 or 1
-// of the 2:4 pair whose metadata is (0,1) or (2,3); the partner is zero.
-__device__ __forceinline__ uint32_t place_lo(uint32_t r, uint32_t slot) {
-  return prmt(r, 0u, slot ? 0x1044u : 0x4410u);
-}
-__device__ __forceinline__ uint32_t place_hi(uint32_t r, uint32_t slot) {
-  return prmt(r, 0u, slot ? 0x3244u : 0x4432u);
-}
-
-// B fragments of k-tile kt for every n-tile.  D column n only depends on B
-// column n, so lanes whose column holds no token (lane >= LS) may read any
-// valid slot: they load lane & 7's without predication and their output
-// columns are never used.
-template <int NT>
-__device__ __forceinline__ void load_b(uint32_t (&b)[NT][4], const uint32_t* pb, int nt_stride) {
-#pragma unroll
-  for (int nt = 0; nt < NT; ++nt) {
-    const uint4 t = *reinterpret_cast<const uint4*>(pb + nt * nt_stride);
-    b[nt][0] = t.x;
-    b[nt][1] = t.y;
-    b[nt][2] = t.z;
-    b[nt][3] = t.w;
-  }
-}
-
-// j is a compile-time constant after unrolling; the branch folds away.
-template <int NT>
-__device__ __forceinline__ void mma_sp_sel(int j, float (&d)[NT][4], const uint32_t (&a)[4],
-                                           const uint32_t (&b)[NT][4], uint32_t ev) {
-  if (j & 1) {
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) mma_sp_16832<1>(d[nt], a, b[nt], ev);
-  } else {
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) mma_sp_16832<0>(d[nt], a, b[nt], ev);
-  }
-}
-
-// INT4 dequantisation on the tensor core.  The nibble c itself is the A
-// operand: an fp16 subnormal c * 2^-24 is exact and needs a single LOP3 per
-// pair (no exponent magic, no subtraction).  Row g+8's nibbles sit 4 bits
-// higher (16c * 2^-24), so one shift per k-tile feeds all four A registers;
-// the x16 is folded into row g+8's scale.  The zero point is applied after
-// the fact: a second mma with A = 1.0 under the same sparsity metadata yields
-// the sum of the kept x, and per scale step
-//   y_r += s_r * (2^24 * D_c - zp_r * D_1)      (2^20 for row g+8).
-constexpr float kTwo24 = 16777216.f;
-constexpr float kTwo20 = 1048576.f;
-constexpr uint32_t kOnes = 0x3C003C00u;  // half2(1, 1)
-
-template <int FMT, int SS, int NT>
-__device__ __forceinline__ void compute_unit(const Unit<FMT, 4 / SS>& u, const uint32_t* pb, int KTc,
-                                             int LS, float (&acc)[NT][2]) {
-  constexpr bool kOnesTrick = (FMT == I4_SP24 || FMT == I4_DENSE);
-  // B fragments: lanes whose column holds no token (lane >= LS) read lane&7's
-  // slot unpredicated -- D column n only depends on B column n, and the
-  // columns of absent tokens are never used (make_cursor).
-  float d[NT][4];
-  float d1[NT][4];
-  uint32_t zpair = 0;
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int e = j / SS;
-    if (j % SS == 0) {
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        d[nt][0] = d[nt][1] = d[nt][2] = d[nt][3] = 0.f;
-        d1[nt][0] = d1[nt][1] = d1[nt][2] = d1[nt][3] = 0.f;
-      }
-      if constexpr (FMT == I4_SP14) {
-        const uint32_t z0 = u.z[e] & 0xFFu, z1 = (u.z[e] >> 8) & 0xFFu;
-        zpair = zp_magic(z0, z1);
-      }
-    }
-    uint32_t b[NT][4];
-    load_b<NT>(b, pb + j * LS * 4, KTc * LS * 4);
-    if constexpr (FMT == I4_SP24) {
-      const uint32_t w = u.v[j], w8 = w >> 8;
-      const uint32_t a[4] = {w & 0x000F000Fu, w & 0x00F000F0u, w8 & 0x000F000Fu, w8 & 0x00F000F0u};
-      const uint32_t ones[4] = {kOnes, kOnes, kOnes, kOnes};
-      mma_sp_sel<NT>(j, d, a, b, u.m[j >> 1]);
-      mma_sp_sel<NT>(j, d1, ones, b, u.m[j >> 1]);
-    } else if constexpr (FMT == F16_SP24) {
-      const uint32_t a[4] = {u.v[4 * j + 0], u.v[4 * j + 1], u.v[4 * j + 2], u.v[4 * j + 3]};
-      mma_sp_sel<NT>(j, d, a, b, u.m[j >> 1]);
-    } else if constexpr (FMT == I4_SP14 || FMT == F16_SP14) {
-      uint32_t r0, r1;
-      if constexpr (FMT == I4_SP14) {
-        const uint32_t w = u.v[j >> 1] >> (8 * (j & 1));
-        r0 = hsub2_u32(nib2_magic(w), zpair);
-        r1 = hsub2_u32(nib2_magic(w >> 4), zpair);
-      } else {
-        r0 = u.v[2 * j];
-        r1 = u.v[2 * j + 1];
-      }
-      const uint32_t sl = (u.m[0] >> (4 * j)) & 0xFu;
-      uint32_t a[4];
-      a[0] = place_lo(r0, sl & 1u);
-      a[1] = place_hi(r0, sl & 2u);
-      a[2] = place_lo(r1, sl & 4u);
-      a[3] = place_hi(r1, sl & 8u);
-      const uint32_t plane = (u.m[0] >> (16 + 8 * (j >> 1))) & 0xFFu;
-      mma_sp_sel<NT>(j, d, a, b, 0x44444444u | (spread4(plane) * 0xAu));
-    } else {  // I4_DENSE: two m16n8k16 per 32-column k-tile
-      const uint32_t w0 = u.v[2 * j], w1 = u.v[2 * j + 1], w08 = w0 >> 8, w18 = w1 >> 8;
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        mma_16816(d[nt], w0 & 0x000F000Fu, w0 & 0x00F000F0u, w08 & 0x000F000Fu, w08 & 0x00F000F0u, b[nt][0],
-                  b[nt][1]);
-        mma_16816(d[nt], w1 & 0x000F000Fu, w1 & 0x00F000F0u, w18 & 0x000F000Fu, w18 & 0x00F000F0u, b[nt][2],
-                  b[nt][3]);
-        mma_16816(d1[nt], kOnes, kOnes, kOnes, kOnes, b[nt][0], b[nt][1]);
-        mma_16816(d1[nt], kOnes, kOnes, kOnes, kOnes, b[nt][2], b[nt][3]);
-      }
-    }
-    if (j % SS == SS - 1) {
-      if constexpr (kOnesTrick) {
-        const float sg = __uint_as_float(u.s[2 * e]), sg8 = __uint_as_float(u.s[2 * e + 1]);
-        const float cg = sg * kTwo24, cg8 = sg8 * kTwo20;
-        const float ng = -sg * static_cast<float>(u.z[e] & 0xFFu);
-        const float ng8 = -sg8 * static_cast<float>((u.z[e] >> 8) & 0xFFu);
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          acc[nt][0] = fmaf(cg, d[nt][0] + d[nt][1], fmaf(ng, d1[nt][0] + d1[nt][1], acc[nt][0]));
-          acc[nt][1] = fmaf(cg8, d[nt][2] + d[nt][3], fmaf(ng8, d1[nt][2] + d1[nt][3], acc[nt][1]));
-        }
-      } else if constexpr (has_scales(FMT)) {
-        const float sg = __uint_as_float(u.s[2 * e]), sg8 = __uint_as_float(u.s[2 * e + 1]);
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          acc[nt][0] = fmaf(sg, d[nt][0] + d[nt][1], acc[nt][0]);
-          acc[nt][1] = fmaf(sg8, d[nt][2] + d[nt][3], acc[nt][1]);
-        }
-      } else {
-#pragma unroll
-        for (int nt = 0; nt < NT; ++nt) {
-          acc[nt][0] += d[nt][0] + d[nt][1];
-          acc[nt][1] += d[nt][2] + d[nt][3];
-        }
-      }
-    }
-  }
-}
-
-template <int FMT>
-__host__ __device__ constexpr int stage_bytes(int KCs, int E) {
-  return KCs * 32 * (val_lane_bytes(FMT) + meta_lane_bytes(FMT)) + (has_scales(FMT) ? KCs * E * 80 : 0);
-}
 
 // One CTA = RB row tiles x KC k-quads (one of S K-slices) x 4*NT tokens.
 // Warp specialised: warp nw (the producer) streams chunks of row tiles -- CH

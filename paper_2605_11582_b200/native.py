@@ -89,6 +89,19 @@ class DecodeOptions(C.Structure):
                 ("alpha", C.c_double), ("beta", C.c_double), ("node_cap", C.c_uint64)]
 
 
+class ProgramOp(C.Structure):
+    """egt_program_op (one product of a persistent GEMV program)."""
+
+    _fields_ = [("w", C.c_void_p), ("x", C.c_void_p), ("y", C.c_void_p), ("residual", C.c_void_p),
+                ("input", C.c_uint32), ("eps", C.c_float), ("wait", C.c_int32)]
+
+
+class ProgramInfo(C.Structure):
+    _fields_ = [(k, C.c_uint32) for k in ("n_ops", "grid", "stages", "stage_bytes", "smem_bytes")]
+
+
+INPUT_NONE, INPUT_RMSNORM, INPUT_SILU = 0, 1, 2
+
 # every symbol include/egt_b200.h declares, with its signature
 SIGNATURES = {
     "egt_abi_version": (C.c_int, []),
@@ -130,7 +143,15 @@ _MODEL_SIGNATURES = {
 }
 
 
+_PROGRAM_SIGNATURES = {
+    "egt_program_create": (C.c_int, [C.POINTER(ProgramOp), C.c_uint32, C.c_void_p, C.POINTER(C.c_void_p)]),
+    "egt_program_run": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "egt_program_query": (C.c_int, [C.c_void_p, C.POINTER(ProgramInfo)]),
+    "egt_program_destroy": (C.c_int, [C.c_void_p]),
+}
+
 SIGNATURES.update(_MODEL_SIGNATURES)
+SIGNATURES.update(_PROGRAM_SIGNATURES)
 
 _lib = None
 
