@@ -296,6 +296,7 @@ typedef struct egt_program_op {
 typedef struct egt_program egt_program; /* opaque; matrices must outlive it */
 typedef struct egt_program_info {
   uint32_t n_ops, grid, stages, stage_bytes, smem_bytes;
+  double max_cta_bytes, avg_cta_bytes; /* planned weight bytes per CTA (busiest, mean) */
 } egt_program_info;
 EGT_API egt_status egt_program_create(const egt_program_op* ops, uint32_t n_ops, void* stream,
                                       egt_program** out);

@@ -9,19 +9,25 @@
 // weights while the consumer warps still wait for op j's output -- weights
 // never depend on activations -- so HBM stays busy across op boundaries.
 //
-// Work split: op j's (row tile, k-quad) blocks are linearised panel-major
-// (panels of <= 96 k-quads, so a panel's x fits in shared memory) and cut
-// into G equal contiguous ranges, one per CTA.  A row tile covered by one CTA
-// in a single panel is stored directly; otherwise each covering CTA writes a
-// 16-float partial and the last to arrive (per-row-tile counter) sums the
-// partials in (panel, CTA) order -- deterministic for a fixed grid.
+// Work split (host-planned, egt_program_create): each CTA owns a contiguous
+// range of whole row tiles of every op, so every output row is reduced inside
+// one CTA and stored directly.  Ops with too few row tiles to occupy the grid
+// are also split along K into S slices (CTA groups); their slice partials are
+// summed by the last-arriving slice in slice order (deterministic).  Within a
+// CTA the K range is walked in panels of <= 96 k-quads (48 KB of x fragments
+// in shared memory), accumulating per row tile across panels.
 //
-// Ordering: after finishing its share of op j (including any reductions it
-// performed) a CTA increments done[j].  Since every CTA processes the ops in
-// order, done[j] == G means ops 0..j are complete; op j waits on done[w_j]
-// before reading x / the residual.  All CTAs are co-resident (cooperative
-// launch, one CTA per SM), spin waits are bounded (trap after 2 s), and the
-// last CTA to exit resets the counters for the next launch / graph replay.
+// Warp roles: 1 producer warp (cp.async.bulk into an mbarrier ring),
+// kProgNW consumer warps (dequant + mma.sp), 1 epilogue warp (cross-warp sums,
+// stores, slice reductions, completion counters) fed through a second
+// mbarrier ring, so the compute warps never wait on global-memory round trips.
+//
+// Ordering: after its share of op j (stores and reductions included) a CTA's
+// epilogue warp increments done[j].  Every CTA processes the ops in order, so
+// done[j] == G means ops 0..j are complete; op j waits on done[w_j] before
+// reading x / the residual.  All CTAs are co-resident (cooperative launch, one
+// CTA per SM), spin waits are bounded (trap after 2 s), and the last CTA to
+// exit resets the counters for the next launch / graph replay.
 //
 // Reference: each op is spmv (packed.cpp:211-220) / quant_dense_gemv
 // (packed.cpp:266-281); the input transforms are rmsnorm (model.cpp:57-67)
@@ -45,6 +51,15 @@ void set_last_error(const std::string& msg);
 constexpr int kProgPanelMax = 96;  // k-quads per panel: 48 KB of x fragments
 constexpr int kProgCH = 16;        // blocks per ring stage (2 per consumer warp)
 constexpr int kProgNW = 8;         // consumer warps
+constexpr int kProgRed = 8;        // consumer -> epilogue ring slots
+constexpr int kProgRowsAcc = 128;  // row tiles accumulated across panels at once
+constexpr int kProgThreads = 32 * (kProgNW + 2);
+
+// One CTA's share of one op: row tiles [rt_a, rt_b) x k-quads [kq_a, kq_b),
+// K slice s of S.
+struct ProgItem {
+  uint16_t rt_a, rt_b, kq_a, kq_b, s, S, pad0, pad1;
+};
 
 struct ProgOp {
   const uint8_t* vals;
@@ -54,14 +69,13 @@ struct ProgOp {
   const float* x;
   float* y;
   const float* res;
-  float* partial;
-  uint32_t* cnt;
-  long long nblk;
+  float* partial;         // S > 1: [RT][S][16]
+  uint32_t* cnt;          // S > 1: [RT] arrival counters
+  const ProgItem* items;  // [G]
   int fmt, SS, E, KQ, rt_begin, RT, rows, cols;
-  int NP, PK, maxp, xform;
-  int wait, blk_bytes;
+  int xform, wait, blk_bytes, need_done;
   float eps;
-  int pad;
+  int pad[3];
 };
 
 struct ProgArgs {
@@ -69,7 +83,7 @@ struct ProgArgs {
   int n_ops;
   uint32_t* done;  // n_ops op counters + 1 exit counter
   uint32_t* err;
-  int NST, stage_bytes, sB_bytes, CH;
+  int NST, stage_bytes, sB_bytes;
 };
 
 namespace {
@@ -88,47 +102,26 @@ __device__ __forceinline__ uint64_t globaltimer() {
   return t;
 }
 
-__device__ __forceinline__ long long range_lo_(long long nblk, int c, int G) { return nblk * c / G; }
-
 // Op descriptors are read-only for the launch: fetched once per op through
 // the non-coherent path into registers (a reference into global memory would
 // be re-read after every mbarrier / barrier asm with a memory clobber).
-__device__ __forceinline__ ProgOp load_op(const ProgOp* src) {
-  static_assert(sizeof(ProgOp) % 16 == 0, "descriptor is copied in 16-byte pieces");
-  ProgOp op;
+template <typename T>
+__device__ __forceinline__ T ldg_struct(const T* src) {
+  static_assert(sizeof(T) % 16 == 0, "copied in 16-byte pieces");
+  T v;
   const int4* s4 = reinterpret_cast<const int4*>(src);
-  int4* d4 = reinterpret_cast<int4*>(&op);
+  int4* d4 = reinterpret_cast<int4*>(&v);
 #pragma unroll
-  for (int i = 0; i < static_cast<int>(sizeof(ProgOp) / 16); ++i) d4[i] = __ldg(s4 + i);
-  return op;
+  for (int i = 0; i < static_cast<int>(sizeof(T) / 16); ++i) d4[i] = __ldg(s4 + i);
+  return v;
 }
 
-// CTAs of [c0, c1] owning at least one block (every CTA does when nblk >= G).
-__device__ __forceinline__ bool cta_nonempty(long long nblk, int c, int G) {
-  return nblk >= G || range_lo_(nblk, c + 1, G) > range_lo_(nblk, c, G);
+// Panels of a CTA's K range: NP equal pieces of <= kProgPanelMax k-quads.
+__device__ __forceinline__ int n_panels(const ProgItem& it) {
+  return (it.kq_b - it.kq_a + kProgPanelMax - 1) / kProgPanelMax;
 }
-
-// Block b of an op -> (panel p, row tile rt, k-quad kq) and its unit (p, rt).
-struct BlockPos {
-  int p, rt, kq, PKp;
-  long long ustart;  // first block of the unit
-};
-__device__ __forceinline__ BlockPos decode_block(const ProgOp& op, long long b) {
-  BlockPos r;
-  const long long pb = static_cast<long long>(op.RT) * op.PK;
-  r.p = static_cast<int>(min(b / pb, static_cast<long long>(op.NP - 1)));
-  const long long off = b - r.p * pb;
-  r.PKp = r.p == op.NP - 1 ? op.KQ - (op.NP - 1) * op.PK : op.PK;
-  r.rt = static_cast<int>(off / r.PKp);
-  r.kq = r.p * op.PK + static_cast<int>(off - static_cast<long long>(r.rt) * r.PKp);
-  r.ustart = r.p * pb + static_cast<long long>(r.rt) * r.PKp;
-  return r;
-}
-__device__ __forceinline__ long long range_lo(long long nblk, int c, int G) {
-  return nblk * c / G;
-}
-__device__ __forceinline__ int cta_of(long long nblk, long long b, int G) {
-  return static_cast<int>(((b + 1) * G - 1) / nblk);
+__device__ __forceinline__ int panel_lo(const ProgItem& it, int p, int NP) {
+  return it.kq_a + (p * (it.kq_b - it.kq_a)) / NP;
 }
 
 // Bulk copies of one chunk (n blocks of one row tile, contiguous in storage).
@@ -146,24 +139,54 @@ __device__ __forceinline__ void issue_chunk(const ProgOp& op, uint8_t* st, uint6
   }
 }
 
-// x panel -> fp16 hi/lo B fragments (SINGLE layout of spmm_tiled.cu: per
-// k-tile 8 lanes x 4 u32; lanes t hold hi, 4+t the residual).  Input
-// transforms: rmsnorm over the whole vector, or silu.
-__device__ void stage_x(const ProgOp& op, int p, uint32_t* sB, float* red_ss, int ctid, int nthr) {
-  const int kq0 = p * op.PK;
-  const int PKp = p == op.NP - 1 ? op.KQ - kq0 : op.PK;
-  const int items = PKp * 4 * 16;
+__device__ __forceinline__ float xform1(float v, int xf, float inv) {
+  if (xf == EGT_INPUT_RMSNORM) return v * inv;
+  if (xf == EGT_INPUT_SILU) return v * (1.0f / (1.0f + expf(-v)));
+  return v;
+}
+
+__device__ __forceinline__ void store_frag(uint32_t* sB, int i, float a, float b) {
+  const int reg = i & 3, t = (i >> 2) & 3, kt = i >> 4;
+  const __half h0 = __float2half_rn(a), h1 = __float2half_rn(b);
+  const __half l0 = __float2half_rn(a - __half2float(h0));
+  const __half l1 = __float2half_rn(b - __half2float(h1));
+  uint32_t* row = sB + static_cast<size_t>(kt) * 32;
+  row[t * 4 + reg] = static_cast<uint32_t>(__half_as_ushort(h0)) | (static_cast<uint32_t>(__half_as_ushort(h1)) << 16);
+  row[(4 + t) * 4 + reg] =
+      static_cast<uint32_t>(__half_as_ushort(l0)) | (static_cast<uint32_t>(__half_as_ushort(l1)) << 16);
+}
+
+// x[k-quads kq0, kq1) -> fp16 hi/lo B fragments (the SINGLE layout of
+// spmm_tiled.cu: per k-tile 8 lanes x 4 u32; lane t holds hi, 4+t the
+// residual).  Item i covers x[k], x[k+1] with k = kt*32 + 2t + 8reg.  When the
+// panel is the whole vector (the usual case) every element is loaded exactly
+// once, into registers, and the rmsnorm sum of squares comes from them.
+__device__ void stage_x(const ProgOp& op, int kq0, int kq1, uint32_t* sB, float* red_ss, int ctid, int nthr) {
+  constexpr int XU = 16;
+  const int items = (kq1 - kq0) * 64;
   const float* x = op.x;
+  const bool whole = kq0 == 0 && kq1 * 128 >= op.cols && items <= XU * nthr;
   float inv = 1.f;
+  float2 v[XU];
   if (op.xform == EGT_INPUT_RMSNORM) {
     float ss = 0.f;
-    const int n4 = op.cols >> 2;
-    for (int i = ctid; i < n4; i += nthr) {
-      const float4 v = __ldcg(reinterpret_cast<const float4*>(x) + i);
-      ss = fmaf(v.x, v.x, ss);
-      ss = fmaf(v.y, v.y, ss);
-      ss = fmaf(v.z, v.z, ss);
-      ss = fmaf(v.w, v.w, ss);
+    if (whole) {
+#pragma unroll
+      for (int u = 0; u < XU; ++u) {
+        const int i = ctid + u * nthr;
+        v[u] = make_float2(0.f, 0.f);
+        if (i < items) {
+          const int k = (i >> 4) * 32 + 2 * ((i >> 2) & 3) + 8 * (i & 3);
+          if (k < op.cols) v[u] = __ldcg(reinterpret_cast<const float2*>(x + k));
+        }
+        ss = fmaf(v[u].x, v[u].x, ss);
+        ss = fmaf(v[u].y, v[u].y, ss);
+      }
+    } else {
+      for (int i = ctid; i < (op.cols >> 2); i += nthr) {
+        const float4 w = __ldcg(reinterpret_cast<const float4*>(x) + i);
+        ss = fmaf(w.x, w.x, fmaf(w.y, w.y, fmaf(w.z, w.z, fmaf(w.w, w.w, ss))));
+      }
     }
     ss = warp_sum(ss);
     if ((ctid & 31) == 0) red_ss[ctid >> 5] = ss;
@@ -171,10 +194,16 @@ __device__ void stage_x(const ProgOp& op, int p, uint32_t* sB, float* red_ss, in
     float tot = 0.f;
     for (int w = 0; w < (nthr >> 5); ++w) tot += red_ss[w];
     inv = 1.0f / sqrtf(tot / static_cast<float>(op.cols) + op.eps);
+    if (whole) {
+#pragma unroll
+      for (int u = 0; u < XU; ++u) {
+        const int i = ctid + u * nthr;
+        if (i < items) store_frag(sB, i, v[u].x * inv, v[u].y * inv);
+      }
+      return;
+    }
   }
-  constexpr int XU = 8;
   for (int i0 = 0; i0 < items; i0 += XU * nthr) {
-    float2 v[XU];
 #pragma unroll
     for (int u = 0; u < XU; ++u) {
       const int i = i0 + ctid + u * nthr;
@@ -187,31 +216,13 @@ __device__ void stage_x(const ProgOp& op, int p, uint32_t* sB, float* red_ss, in
 #pragma unroll
     for (int u = 0; u < XU; ++u) {
       const int i = i0 + ctid + u * nthr;
-      if (i < items) {
-        float a = v[u].x, b = v[u].y;
-        if (op.xform == EGT_INPUT_RMSNORM) {
-          a *= inv;
-          b *= inv;
-        } else if (op.xform == EGT_INPUT_SILU) {
-          a = a * (1.0f / (1.0f + expf(-a)));
-          b = b * (1.0f / (1.0f + expf(-b)));
-        }
-        const int reg = i & 3, t = (i >> 2) & 3, kt = i >> 4;
-        const __half h0 = __float2half_rn(a), h1 = __float2half_rn(b);
-        const __half l0 = __float2half_rn(a - __half2float(h0));
-        const __half l1 = __float2half_rn(b - __half2float(h1));
-        uint32_t* row = sB + static_cast<size_t>(kt) * 32;
-        row[t * 4 + reg] = static_cast<uint32_t>(__half_as_ushort(h0)) |
-                           (static_cast<uint32_t>(__half_as_ushort(h1)) << 16);
-        row[(4 + t) * 4 + reg] = static_cast<uint32_t>(__half_as_ushort(l0)) |
-                                 (static_cast<uint32_t>(__half_as_ushort(l1)) << 16);
-      }
+      if (i < items) store_frag(sB, i, xform1(v[u].x, op.xform, inv), xform1(v[u].y, op.xform, inv));
     }
   }
 }
 
-// One chunk of n blocks (k-quads kq .. kq+n of one row tile) in stage st,
-// consumed by nw warps (units warp, warp+nw, ...), two units in flight.
+// One chunk of n blocks (k-quads of one row tile) in stage st, consumed by nw
+// warps (units warp, warp+nw, ...), two units in flight per warp.
 template <int FMT, int SS>
 __device__ __forceinline__ void consume_chunk(const uint8_t* st, int n, int kt_base, int warp, int nw, int lane,
                                               const uint32_t* sB, float (&acc)[1][2]) {
@@ -253,65 +264,34 @@ __device__ __forceinline__ void consume_dispatch(int fmt, int SS, const uint8_t*
   }
 }
 
-// Warp 0's epilogue of one segment: sum the consumer warps' partial rows, then
-// store (unit complete) or publish a partial and reduce if last.
-__device__ void segment_epilogue(const ProgOp& op, const BlockPos& bp, bool whole, const float* red, int nw, int lane,
-                                 int c, int G) {
-  float v = 0.f;
-  if (lane < 16)
-    for (int w = 0; w < nw; ++w) v += red[w * 16 + lane];
-  const int row = bp.rt * 16 + lane;
-  if (whole) {
-    if (lane < 16 && row < op.rows) op.y[row] = (op.res ? __ldcg(op.res + row) : 0.f) + v;
-    return;
+__device__ __forceinline__ void trap_after(uint64_t t0, uint32_t* err) {
+  if (globaltimer() - t0 > 2000000000ull) {
+    atomicExch(err, 1u);
+    __trap();
   }
-  const long long u = static_cast<long long>(bp.p) * op.RT + bp.rt;
-  const int piece = c - cta_of(op.nblk, bp.ustart, G);
-  if (lane < 16) op.partial[(u * op.maxp + piece) * 16 + lane] = v;
-  __threadfence();
-  __syncwarp();
-  int last = 0;
-  if (lane == 0) {
-    int expected = 0;
-    for (int p = 0; p < op.NP; ++p) {
-      const int PKp = p == op.NP - 1 ? op.KQ - (op.NP - 1) * op.PK : op.PK;
-      const long long us = static_cast<long long>(p) * op.RT * op.PK + static_cast<long long>(bp.rt) * PKp;
-      const int c0 = cta_of(op.nblk, us, G), c1 = cta_of(op.nblk, us + PKp - 1, G);
-      for (int cc = c0; cc <= c1; ++cc) expected += cta_nonempty(op.nblk, cc, G) ? 1 : 0;
-    }
-    last = atomicAdd(op.cnt + bp.rt, 1u) == static_cast<uint32_t>(expected - 1);
-  }
-  last = __shfl_sync(0xffffffffu, last, 0);
-  if (!last) return;
-  __threadfence();
-  float s = 0.f;
-  if (lane < 16) {
-    for (int p = 0; p < op.NP; ++p) {
-      const int PKp = p == op.NP - 1 ? op.KQ - (op.NP - 1) * op.PK : op.PK;
-      const long long us = static_cast<long long>(p) * op.RT * op.PK + static_cast<long long>(bp.rt) * PKp;
-      const int c0 = cta_of(op.nblk, us, G), c1 = cta_of(op.nblk, us + PKp - 1, G);
-      const long long uu = static_cast<long long>(p) * op.RT + bp.rt;
-      for (int k = 0; k <= c1 - c0; ++k)
-        if (cta_nonempty(op.nblk, c0 + k, G)) s += __ldcg(op.partial + (uu * op.maxp + k) * 16 + lane);
-    }
-    if (row < op.rows) op.y[row] = (op.res ? __ldcg(op.res + row) : 0.f) + s;
-  }
-  if (lane == 0) op.cnt[bp.rt] = 0u;  // ready for the next launch
 }
 
 }  // namespace
 
-__global__ void __launch_bounds__(32 * (kProgNW + 1), 1) program_kernel(const ProgArgs a) {
+// The iteration order shared by all three roles (per op, per CTA):
+//   for row-tile block [r0, r1) of <= kProgRowsAcc row tiles of [rt_a, rt_b):
+//     for panel p of [kq_a, kq_b):            (consumers restage x if needed)
+//       for rt in [r0, r1):                    one segment -> one red slot
+//         chunks of <= kProgCH k-quads of (rt, panel p)
+__global__ void __launch_bounds__(kProgThreads, 1) program_kernel(const ProgArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int nw = (blockDim.x >> 5) - 1;
+  constexpr int nw = kProgNW;
   const int G = gridDim.x, c = blockIdx.x;
   const int NST = a.NST;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
   uint64_t* empty = full + NST;
-  float* red = reinterpret_cast<float*>(smem_raw + ((16 * NST + 127) / 128) * 128);  // [2][nw][16]
-  float* red_ss = red + 2 * 16 * kProgNW;                                            // [nw]
-  uint32_t* sB = reinterpret_cast<uint32_t*>(red_ss + 32);
+  uint64_t* rfull = empty + NST;
+  uint64_t* rempty = rfull + kProgRed;
+  float* red = reinterpret_cast<float*>(smem_raw + ((16 * NST + 16 * kProgRed + 127) / 128) * 128);  // [R][nw][16]
+  float* red_ss = red + kProgRed * nw * 16;         // [32]
+  float* acc_s = red_ss + 32;                       // [kProgRowsAcc][16]
+  uint32_t* sB = reinterpret_cast<uint32_t*>(acc_s + kProgRowsAcc * 16);
   uint8_t* stages = reinterpret_cast<uint8_t*>(sB) + a.sB_bytes;
 
   if (tid == 0) {
@@ -319,31 +299,41 @@ __global__ void __launch_bounds__(32 * (kProgNW + 1), 1) program_kernel(const Pr
       mbar_init(full + s, 1);
       mbar_init(empty + s, nw);
     }
+    for (int s = 0; s < kProgRed; ++s) {
+      mbar_init(rfull + s, nw);
+      mbar_init(rempty + s, 1);
+    }
     mbar_fence_init();
   }
   __syncthreads();
 
   if (warp == nw) {
-    // producer: stream every op's block range of this CTA, in program order
+    // ------------------------------------------------------------ producer
     if (lane == 0) {
       const uint64_t pol = evict_first_policy();
       int s = 0;
       uint32_t phase = 0;
       long long q = 0;
       for (int j = 0; j < a.n_ops; ++j) {
-        const ProgOp op = load_op(a.ops + j);
-        const long long b1 = range_lo(op.nblk, c + 1, G);
-        long long b = range_lo(op.nblk, c, G);
-        while (b < b1) {
-          const BlockPos bp = decode_block(op, b);
-          const int n = static_cast<int>(min(min(static_cast<long long>(a.CH), bp.ustart + bp.PKp - b), b1 - b));
-          if (q >= NST) mbar_wait(empty + s, phase ^ 1u);
-          issue_chunk(op, stages + static_cast<size_t>(s) * a.stage_bytes, full + s, bp.rt, bp.kq, n, pol);
-          ++q;
-          b += n;
-          if (++s == NST) {
-            s = 0;
-            phase ^= 1u;
+        const ProgOp op = ldg_struct(a.ops + j);
+        const ProgItem it = ldg_struct(op.items + c);
+        if (it.rt_a >= it.rt_b) continue;
+        const int NP = n_panels(it);
+        for (int r0 = it.rt_a; r0 < it.rt_b; r0 += kProgRowsAcc) {
+          const int r1 = min(static_cast<int>(it.rt_b), r0 + kProgRowsAcc);
+          for (int p = 0; p < NP; ++p) {
+            const int k0 = panel_lo(it, p, NP), k1 = panel_lo(it, p + 1, NP);
+            for (int rt = r0; rt < r1; ++rt)
+              for (int kq = k0; kq < k1; kq += kProgCH) {
+                const int n = min(kProgCH, k1 - kq);
+                if (q >= NST) mbar_wait(empty + s, phase ^ 1u);
+                issue_chunk(op, stages + static_cast<size_t>(s) * a.stage_bytes, full + s, rt, kq, n, pol);
+                ++q;
+                if (++s == NST) {
+                  s = 0;
+                  phase ^= 1u;
+                }
+              }
           }
         }
       }
@@ -351,90 +341,157 @@ __global__ void __launch_bounds__(32 * (kProgNW + 1), 1) program_kernel(const Pr
     return;
   }
 
-  // consumers
-  const int nthr = nw * 32;
-  int s = 0;
-  uint32_t phase = 0;
-  int slot = 0;
-  // the x fragments in shared memory: (x, transform, panel, PK, KQ) of the
-  // op that staged them; any wait invalidates them (x may have been rewritten)
-  const float* staged_x = nullptr;
-  int staged_p = -1, staged_xf = -1, staged_PK = -1, staged_KQ = -1;
-  for (int j = 0; j < a.n_ops; ++j) {
-    const ProgOp op = load_op(a.ops + j);
-    const long long b0 = range_lo(op.nblk, c, G), b1 = range_lo(op.nblk, c + 1, G);
-    if (b0 < b1) {
-      if (op.wait >= 0) {
-        if (tid == 0) {
-          const uint64_t t0 = globaltimer();
-          while (ld_acquire(a.done + op.wait) < static_cast<uint32_t>(G)) {
-            if (globaltimer() - t0 > 2000000000ull) {
-              atomicExch(a.err, 1u);
-              __trap();
+  if (warp == nw + 1) {
+    // ------------------------------------------------------------ epilogue
+    int slot = 0;
+    uint32_t rphase = 0;
+    for (int j = 0; j < a.n_ops; ++j) {
+      const ProgOp op = ldg_struct(a.ops + j);
+      const ProgItem it = ldg_struct(op.items + c);
+      if (it.rt_a < it.rt_b) {
+        const int NP = n_panels(it);
+        for (int r0 = it.rt_a; r0 < it.rt_b; r0 += kProgRowsAcc) {
+          const int r1 = min(static_cast<int>(it.rt_b), r0 + kProgRowsAcc);
+          for (int p = 0; p < NP; ++p)
+            for (int rt = r0; rt < r1; ++rt) {
+              mbar_wait(rfull + slot, rphase);
+              float v = 0.f;
+              if (lane < 16) {
+                const float* rs = red + slot * nw * 16 + lane;
+#pragma unroll
+                for (int w = 0; w < nw; ++w) v += rs[w * 16];
+              }
+              __syncwarp();
+              if (lane == 0) mbar_arrive(rempty + slot);
+              if (++slot == kProgRed) {
+                slot = 0;
+                rphase ^= 1u;
+              }
+              if (NP > 1) {
+                float* as = acc_s + (rt - r0) * 16 + lane;
+                if (lane < 16) v = p == 0 ? v : *as + v;
+                if (p < NP - 1) {
+                  if (lane < 16) *as = v;
+                  continue;
+                }
+              }
+              const int row = rt * 16 + lane;
+              if (lane < 16 && row < op.rows) {
+                if (it.S == 1)
+                  op.y[row] = (op.res ? __ldcg(op.res + row) : 0.f) + v;
+                else
+                  op.partial[(static_cast<size_t>(rt) * it.S + it.s) * 16 + lane] = v;
+              }
+            }
+        }
+        if (it.S > 1) {
+          // slice partials of this CTA's row tiles: one fence, the arrival
+          // counters in parallel, then the last slice of a row tile sums all
+          // slices in slice order
+          __threadfence();
+          __syncwarp();
+          for (int rb = it.rt_a; rb < it.rt_b; rb += 32) {
+            const int rt = rb + lane;
+            uint32_t last = 0;
+            if (rt < it.rt_b) last = atomicAdd(op.cnt + rt, 1u) == static_cast<uint32_t>(it.S - 1);
+            uint32_t mask = __ballot_sync(0xffffffffu, last);
+            if (mask) __threadfence();
+            while (mask) {
+              const int i = __ffs(mask) - 1;
+              mask &= mask - 1;
+              const int rr = rb + i;
+              const int row = rr * 16 + (lane & 15);
+              if (lane < 16 && row < op.rows) {
+                float s = 0.f;
+                for (int k = 0; k < it.S; ++k) s += __ldcg(op.partial + (static_cast<size_t>(rr) * it.S + k) * 16 + lane);
+                op.y[row] = (op.res ? __ldcg(op.res + row) : 0.f) + s;
+              }
+              if (lane == 0) op.cnt[rr] = 0u;  // ready for the next launch
             }
           }
-          __threadfence();
         }
-        staged_x = nullptr;  // the other threads pass the restaging barrier after thread 0
       }
-      long long b = b0;
-      while (b < b1) {
-        const BlockPos bp = decode_block(op, b);
-        const long long seg_end = min(bp.ustart + bp.PKp, b1);
-        const bool whole = op.NP == 1 && b == bp.ustart && seg_end == bp.ustart + bp.PKp;
-        if (staged_x != op.x || staged_xf != op.xform || staged_p != bp.p || staged_PK != op.PK ||
-            staged_KQ != op.KQ) {
+      if (op.need_done) {
+        __threadfence();
+        __syncwarp();
+        if (lane == 0) atomicAdd(a.done + j, 1u);
+      }
+    }
+    // the last CTA out resets the op counters for the next launch
+    if (lane == 0) {
+      __threadfence();
+      if (atomicAdd(a.done + a.n_ops, 1u) == static_cast<uint32_t>(G - 1)) {
+        for (int j = 0; j <= a.n_ops; ++j) a.done[j] = 0u;
+        __threadfence();
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  const int nthr = nw * 32;
+  int s = 0, slot = 0;
+  uint32_t phase = 0, rphase = 0;
+  // the x fragments in shared memory: (x, transform, k-quad range) of the
+  // op that staged them; a wait invalidates them (x may have been rewritten)
+  const float* staged_x = nullptr;
+  int staged_xf = -1, staged_k0 = -1, staged_k1 = -1;
+  for (int j = 0; j < a.n_ops; ++j) {
+    const ProgOp op = ldg_struct(a.ops + j);
+    const ProgItem it = ldg_struct(op.items + c);
+    if (it.rt_a >= it.rt_b) continue;
+    if (op.wait >= 0) {
+      if (tid == 0) {
+        const uint64_t t0 = globaltimer();
+        while (ld_acquire(a.done + op.wait) < static_cast<uint32_t>(G)) trap_after(t0, a.err);
+        __threadfence();
+      }
+      staged_x = nullptr;  // the other threads pass the restaging barrier after thread 0
+    }
+    const int NP = n_panels(it);
+    for (int r0 = it.rt_a; r0 < it.rt_b; r0 += kProgRowsAcc) {
+      const int r1 = min(static_cast<int>(it.rt_b), r0 + kProgRowsAcc);
+      for (int p = 0; p < NP; ++p) {
+        const int k0 = panel_lo(it, p, NP), k1 = panel_lo(it, p + 1, NP);
+        if (staged_x != op.x || staged_xf != op.xform || staged_k0 != k0 || staged_k1 != k1) {
           consumer_bar(nthr);  // every warp is done with the previous fragments
-          stage_x(op, bp.p, sB, red_ss, tid, nthr);
+          stage_x(op, k0, k1, sB, red_ss, tid, nthr);
           consumer_bar(nthr);
           staged_x = op.x;
           staged_xf = op.xform;
-          staged_p = bp.p;
-          staged_PK = op.PK;
-          staged_KQ = op.KQ;
+          staged_k0 = k0;
+          staged_k1 = k1;
         }
-        float acc[1][2] = {{0.f, 0.f}};
-        const int kt_panel0 = bp.p * op.PK * 4;
-        for (long long cb = b; cb < seg_end;) {
-          const int n = static_cast<int>(min(static_cast<long long>(a.CH), seg_end - cb));
-          const int kq = bp.kq + static_cast<int>(cb - b);
-          mbar_wait(full + s, phase);
-          consume_dispatch(op.fmt, op.SS, stages + static_cast<size_t>(s) * a.stage_bytes, n, kq * 4 - kt_panel0,
-                           warp, nw, lane, sB, acc);
-          __syncwarp();
-          if (lane == 0) mbar_arrive(empty + s);
-          if (++s == NST) {
-            s = 0;
-            phase ^= 1u;
+        for (int rt = r0; rt < r1; ++rt) {
+          float acc[1][2] = {{0.f, 0.f}};
+          for (int kq = k0; kq < k1; kq += kProgCH) {
+            const int n = min(kProgCH, k1 - kq);
+            mbar_wait(full + s, phase);
+            consume_dispatch(op.fmt, op.SS, stages + static_cast<size_t>(s) * a.stage_bytes, n, (kq - k0) * 4,
+                             warp, nw, lane, sB, acc);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(empty + s);
+            if (++s == NST) {
+              s = 0;
+              phase ^= 1u;
+            }
           }
-          cb += n;
+          // lane (g, t = 0) holds token 0 (B columns 0 = hi, 1 = lo, summed by
+          // compute_unit): rows g and g+8 of the row tile
+          mbar_wait(rempty + slot, rphase ^ 1u);
+          if ((lane & 3) == 0) {
+            float* rs = red + (slot * nw + warp) * 16;
+            rs[lane >> 2] = acc[0][0];
+            rs[(lane >> 2) + 8] = acc[0][1];
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(rfull + slot);
+          if (++slot == kProgRed) {
+            slot = 0;
+            rphase ^= 1u;
+          }
         }
-        // lane (g, t = 0) holds token 0 (B columns 0 = hi, 1 = lo, summed by
-        // compute_unit): rows g and g+8 of the row tile
-        const float r0 = acc[0][0], r1 = acc[0][1];
-        float* rs = red + (slot * kProgNW + warp) * 16;
-        if ((lane & 3) == 0) {
-          rs[lane >> 2] = r0;
-          rs[(lane >> 2) + 8] = r1;
-        }
-        consumer_bar(nthr);
-        if (warp == 0) segment_epilogue(op, bp, whole, red + slot * kProgNW * 16, nw, lane, c, G);
-        slot ^= 1;
-        b = seg_end;
       }
-    }
-    if (warp == 0) {
-      __threadfence();
-      __syncwarp();
-      if (lane == 0) atomicAdd(a.done + j, 1u);
-    }
-  }
-  // the last CTA out resets the op counters for the next launch
-  if (warp == 0 && lane == 0) {
-    __threadfence();
-    if (atomicAdd(a.done + a.n_ops, 1u) == static_cast<uint32_t>(G - 1)) {
-      for (int j = 0; j <= a.n_ops; ++j) a.done[j] = 0u;
-      __threadfence();
     }
   }
 }
@@ -448,8 +505,8 @@ struct egt_program {
   int G = 0, NST = 0, stage_bytes = 0, sB_bytes = 0, smem = 0;
   uint32_t n_ops = 0;
   bool coop = true;
-  std::vector<egt_program_op> ops;
-  char* dev = nullptr;  // ops descriptors, counters, partial sums
+  double max_load = 0, avg_load = 0;  // bytes per CTA (whole program)
+  char* dev = nullptr;  // descriptors, items, counters, partial sums
   egt_impl::ProgOp* d_ops = nullptr;
   uint32_t* d_done = nullptr;
   uint32_t* d_err = nullptr;
@@ -472,9 +529,64 @@ bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
 
 size_t al256(size_t v) { return (v + 255) / 256 * 256; }
 
+// K slices for an op with RT row tiles of KQ k-quads on G CTAs: S = 1 when
+// the row tiles alone fill the grid; otherwise the S minimising the busiest
+// CTA's blocks (ceil(RT / CTAs per slice) x ceil(KQ / S)) plus a small cost
+// per extra slice (partial stores and the arrival round trip).
+int choose_slices(int RT, int KQ, int G) {
+  if (RT >= 2 * G) return 1;
+  int best_S = 1;
+  double best = 1e300;
+  for (int S = 1; S <= std::min({KQ, G, 64}); ++S) {
+    const int g_min = G / S;  // smallest group
+    const double rows = std::ceil(static_cast<double>(RT) / g_min);
+    const double cost = rows * std::ceil(static_cast<double>(KQ) / S) + (S > 1 ? 4.0 + 0.5 * S : 0.0);
+    if (cost < best * 0.98) {
+      best = cost;
+      best_S = S;
+    }
+  }
+  return best_S;
+}
+
+// Row-tile ranges of one op: slice s is owned by the CTA group
+// [s*G/S, (s+1)*G/S); inside a group the RT row tiles are cut into
+// contiguous ranges of q or q+1, the extra ones going to the CTAs with the
+// least load so far (balances independent ops over the whole program).
+void assign_items(int RT, int KQ, int S, int G, double blk_bytes, std::vector<double>& load,
+                  std::vector<ProgItem>& items) {
+  items.assign(G, ProgItem{0, 0, 0, 0, 0, 1, 0, 0});
+  for (int s = 0; s < S; ++s) {
+    const int g0 = static_cast<int>(static_cast<long long>(s) * G / S);
+    const int g1 = static_cast<int>(static_cast<long long>(s + 1) * G / S);
+    const int n = g1 - g0;
+    const int k0 = static_cast<int>(static_cast<long long>(s) * KQ / S);
+    const int k1 = static_cast<int>(static_cast<long long>(s + 1) * KQ / S);
+    const int q = RT / n, r = RT % n;
+    std::vector<int> order(n);
+    for (int i = 0; i < n; ++i) order[i] = g0 + i;
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return load[x] < load[y]; });
+    std::vector<int> cnt(n, q);
+    for (int i = 0; i < r; ++i) cnt[order[i] - g0] += 1;
+    int rt = 0;
+    for (int i = 0; i < n; ++i) {
+      ProgItem& it = items[g0 + i];
+      it.rt_a = static_cast<uint16_t>(rt);
+      it.rt_b = static_cast<uint16_t>(rt + cnt[i]);
+      it.kq_a = static_cast<uint16_t>(k0);
+      it.kq_b = static_cast<uint16_t>(k1);
+      it.s = static_cast<uint16_t>(s);
+      it.S = static_cast<uint16_t>(S);
+      rt += cnt[i];
+      load[g0 + i] += cnt[i] * static_cast<double>(k1 - k0) * blk_bytes;
+    }
+  }
+}
+
 }  // namespace
 }  // namespace egt_impl
 
+using egt_impl::ProgItem;
 using egt_impl::ProgOp;
 using egt_impl::pfail;
 
@@ -490,9 +602,12 @@ egt_status egt_program_create(const egt_program_op* ops, uint32_t n_ops, void* s
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   if (const char* e = getenv("EGT_PROGRAM_GRID")) sms = std::max(1, std::min(sms, atoi(e)));
+  const int G = sms;
   std::vector<ProgOp> d(n_ops);
+  std::vector<std::vector<ProgItem>> items(n_ops);
+  std::vector<double> load(G, 0.0);
   size_t ws_floats = 0, ws_cnt = 0;
-  int max_blk = 0, max_PK = 1;
+  int max_blk = 0, max_panel = 1;
   for (uint32_t j = 0; j < n_ops; ++j) {
     const egt_program_op& o = ops[j];
     const std::string tag = "program: op " + std::to_string(j) + ": ";
@@ -500,6 +615,7 @@ egt_status egt_program_create(const egt_program_op* ops, uint32_t n_ops, void* s
     const egt_dev_packed* h = o.w;
     if (h->path != EGT_PATH_TILED) return pfail(EGT_EINVAL, tag + "matrix is not on the tiled path");
     if (h->rows == 0 || h->cols == 0) return pfail(EGT_EINVAL, tag + "empty matrix");
+    if (h->tiled.RT > 65535 || h->tiled.KQ > 65535) return pfail(EGT_EINVAL, tag + "matrix too large for a program");
     if (!o.x || !o.y) return pfail(EGT_EINVAL, tag + "null vector");
     if (reinterpret_cast<uintptr_t>(o.x) % 16 != 0) return pfail(EGT_EINVAL, tag + "x must be 16-byte aligned");
     if (o.input > EGT_INPUT_SILU) return pfail(EGT_EINVAL, tag + "unknown input transform");
@@ -537,66 +653,78 @@ egt_status egt_program_create(const egt_program_op* ops, uint32_t n_ops, void* s
     p.RT = h->tiled.RT;
     p.rows = static_cast<int>(h->rows);
     p.cols = static_cast<int>(h->cols);
-    p.NP = (p.KQ + kProgPanelMax - 1) / kProgPanelMax;
-    p.PK = (p.KQ + p.NP - 1) / p.NP;
     p.xform = static_cast<int>(o.input);
     p.eps = o.eps;
     p.wait = o.wait;
     p.blk_bytes = 32 * (val_lane_bytes(p.fmt) + meta_lane_bytes(p.fmt)) + (has_scales(p.fmt) ? p.E * 80 : 0);
-    p.nblk = static_cast<long long>(p.RT) * p.KQ;
-    // partial slots per unit: the most CTAs any (panel, row tile) spans
-    int maxp = 1;
-    auto cta = [&](long long b) { return static_cast<int>(((b + 1) * sms - 1) / p.nblk); };
-    for (int q = 0; q < p.NP; ++q) {
-      const int PKp = q == p.NP - 1 ? p.KQ - (p.NP - 1) * p.PK : p.PK;
-      for (int rt = 0; rt < p.RT; ++rt) {
-        const long long us = static_cast<long long>(q) * p.RT * p.PK + static_cast<long long>(rt) * PKp;
-        maxp = std::max(maxp, cta(us + PKp - 1) - cta(us) + 1);
+    const int S = choose_slices(p.RT, p.KQ, G);
+    assign_items(p.RT, p.KQ, S, G, p.blk_bytes, load, items[j]);
+    for (const ProgItem& it : items[j]) {
+      const int len = it.kq_b - it.kq_a;
+      if (len > 0) {
+        const int NP = (len + kProgPanelMax - 1) / kProgPanelMax;
+        max_panel = std::max(max_panel, (len + NP - 1) / NP);
       }
     }
-    p.maxp = maxp;
-    ws_floats += al256(static_cast<size_t>(p.NP) * p.RT * maxp * 16 * 4) / 4;
-    ws_cnt += al256(static_cast<size_t>(p.RT) * 4) / 4;
+    if (S > 1) {
+      ws_floats += al256(static_cast<size_t>(p.RT) * S * 16 * 4) / 4;
+      ws_cnt += al256(static_cast<size_t>(p.RT) * 4) / 4;
+    }
     max_blk = std::max(max_blk, p.blk_bytes);
-    max_PK = std::max(max_PK, p.PK);
   }
+  for (uint32_t j = 0; j < n_ops; ++j)
+    if (ops[j].wait >= 0) d[ops[j].wait].need_done = 1;
   auto prog = new egt_program();
   prog->device = dev;
-  prog->G = sms;
+  prog->G = G;
   prog->n_ops = n_ops;
-  prog->ops.assign(ops, ops + n_ops);
   prog->coop = getenv("EGT_PROGRAM_NO_COOP") == nullptr;
-  prog->sB_bytes = max_PK * 4 * 128;
+  prog->max_load = *std::max_element(load.begin(), load.end());
+  double tot = 0;
+  for (double v : load) tot += v;
+  prog->avg_load = tot / G;
+  prog->sB_bytes = max_panel * 4 * 128;
   prog->stage_bytes = kProgCH * max_blk;
-  const int fixed = 2 * 16 * kProgNW * 4 + 32 * 4 + prog->sB_bytes + 128;
-  int nst = (smem_optin - fixed - 1024) / (prog->stage_bytes + 16);
+  const int bars = (16 * 64 + 16 * kProgRed + 127) / 128 * 128;  // room for up to 64 stages
+  const int fixed = bars + (kProgRed * kProgNW * 16 + 32 + kProgRowsAcc * 16) * 4 + prog->sB_bytes;
+  int nst = std::min(64, (smem_optin - fixed) / prog->stage_bytes);
   if (const char* e = getenv("EGT_PROGRAM_NST")) nst = std::min(nst, atoi(e));
   if (nst < 2) {
     delete prog;
     return pfail(EGT_EINVAL, "program: shared memory cannot hold two stages");
   }
   prog->NST = nst;
-  prog->smem = (16 * nst + 127) / 128 * 128 + fixed + nst * prog->stage_bytes;
+  prog->smem = (16 * nst + 16 * kProgRed + 127) / 128 * 128 + (fixed - bars) + nst * prog->stage_bytes;
   const size_t ops_b = al256(sizeof(ProgOp) * n_ops);
+  const size_t items_b = al256(sizeof(ProgItem) * static_cast<size_t>(G) * n_ops);
   const size_t done_b = al256(4ull * (n_ops + 2));
-  const size_t total = ops_b + done_b + ws_cnt * 4 + ws_floats * 4;
+  const size_t total = ops_b + items_b + done_b + ws_cnt * 4 + ws_floats * 4;
   if (cudaMalloc(&prog->dev, total) != cudaSuccess) {
     delete prog;
     return pfail(EGT_ECUDA, "program: device allocation failed");
   }
   prog->d_ops = reinterpret_cast<ProgOp*>(prog->dev);
-  prog->d_done = reinterpret_cast<uint32_t*>(prog->dev + ops_b);
+  ProgItem* d_items = reinterpret_cast<ProgItem*>(prog->dev + ops_b);
+  prog->d_done = reinterpret_cast<uint32_t*>(prog->dev + ops_b + items_b);
   prog->d_err = prog->d_done + n_ops + 1;
-  uint32_t* cnt = reinterpret_cast<uint32_t*>(prog->dev + ops_b + done_b);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(prog->dev + ops_b + items_b + done_b);
   float* part = reinterpret_cast<float*>(cnt + ws_cnt);
+  std::vector<ProgItem> all(static_cast<size_t>(G) * n_ops);
   for (uint32_t j = 0; j < n_ops; ++j) {
-    d[j].cnt = cnt;
-    d[j].partial = part;
-    cnt += al256(static_cast<size_t>(d[j].RT) * 4) / 4;
-    part += al256(static_cast<size_t>(d[j].NP) * d[j].RT * d[j].maxp * 16 * 4) / 4;
+    std::copy(items[j].begin(), items[j].end(), all.begin() + static_cast<size_t>(j) * G);
+    d[j].items = d_items + static_cast<size_t>(j) * G;
+    const int S = items[j][0].S;
+    if (S > 1) {
+      d[j].cnt = cnt;
+      d[j].partial = part;
+      cnt += al256(static_cast<size_t>(d[j].RT) * 4) / 4;
+      part += al256(static_cast<size_t>(d[j].RT) * S * 16 * 4) / 4;
+    }
   }
-  cudaError_t e = cudaMemsetAsync(prog->dev + ops_b, 0, done_b + ws_cnt * 4, st);
+  cudaError_t e = cudaMemsetAsync(prog->dev + ops_b + items_b, 0, done_b + ws_cnt * 4, st);
   if (e == cudaSuccess) e = cudaMemcpyAsync(prog->d_ops, d.data(), sizeof(ProgOp) * n_ops, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(d_items, all.data(), sizeof(ProgItem) * all.size(), cudaMemcpyHostToDevice, st);
   if (e == cudaSuccess) e = cudaStreamSynchronize(st);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(reinterpret_cast<const void*>(&program_kernel),
@@ -621,10 +749,9 @@ egt_status egt_program_run(const egt_program* prog, void* stream) {
   a.NST = prog->NST;
   a.stage_bytes = prog->stage_bytes;
   a.sB_bytes = prog->sB_bytes;
-  a.CH = kProgCH;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(prog->G);
-  cfg.blockDim = dim3(32 * (kProgNW + 1));
+  cfg.blockDim = dim3(kProgThreads);
   cfg.dynamicSmemBytes = prog->smem;
   cfg.stream = static_cast<cudaStream_t>(stream);
   cudaLaunchAttribute attr[1];
@@ -646,6 +773,8 @@ egt_status egt_program_query(const egt_program* prog, egt_program_info* info) {
   info->stages = static_cast<uint32_t>(prog->NST);
   info->stage_bytes = static_cast<uint32_t>(prog->stage_bytes);
   info->smem_bytes = static_cast<uint32_t>(prog->smem);
+  info->max_cta_bytes = prog->max_load;
+  info->avg_cta_bytes = prog->avg_load;
   return EGT_OK;
 }
 

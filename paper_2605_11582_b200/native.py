@@ -97,7 +97,8 @@ class ProgramOp(C.Structure):
 
 
 class ProgramInfo(C.Structure):
-    _fields_ = [(k, C.c_uint32) for k in ("n_ops", "grid", "stages", "stage_bytes", "smem_bytes")]
+    _fields_ = [(k, C.c_uint32) for k in ("n_ops", "grid", "stages", "stage_bytes", "smem_bytes")] + [
+        ("max_cta_bytes", C.c_double), ("avg_cta_bytes", C.c_double)]
 
 
 INPUT_NONE, INPUT_RMSNORM, INPUT_SILU = 0, 1, 2
