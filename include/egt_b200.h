@@ -303,6 +303,10 @@ EGT_API egt_status egt_program_create(const egt_program_op* ops, uint32_t n_ops,
 EGT_API egt_status egt_program_run(const egt_program* p, void* stream);
 EGT_API egt_status egt_program_query(const egt_program* p, egt_program_info* info);
 EGT_API egt_status egt_program_destroy(egt_program* p);
+/* Tuning hook: with EGT_PROGRAM_TRACE set at create, CTA 0 records SM clock
+ * stamps per ring chunk: [0,4096) producer issue, [4096,8192) consumer data
+ * ready, [8192,12288) consumer done, [12288,16384) epilogue segment start. */
+EGT_API egt_status egt_program_debug_trace(const egt_program* p, long long* host, size_t n);
 
 /* ---------------- host encoder (C++; byte-identical to the reference) ----
  * Masks are PruneMask bitmaps (bit r*cols+c, LSB-first). */

@@ -45,15 +45,21 @@
 #include "handle.h"
 #include "tiled_compute.cuh"
 
+#ifndef EGT_PROG_NW
+#define EGT_PROG_NW 16
+#endif
+
 namespace egt_impl {
 void set_last_error(const std::string& msg);
 
 constexpr int kProgPanelMax = 96;  // k-quads per panel: 48 KB of x fragments
-constexpr int kProgCH = 16;        // blocks per ring stage (2 per consumer warp)
-constexpr int kProgNW = 8;         // consumer warps
+constexpr int kProgNW = EGT_PROG_NW;   // consumer warps
+constexpr int kProgCH = 2 * kProgNW;  // blocks per ring stage (2 per consumer warp)
+
 constexpr int kProgRed = 8;        // consumer -> epilogue ring slots
 constexpr int kProgRowsAcc = 128;  // row tiles accumulated across panels at once
 constexpr int kProgThreads = 32 * (kProgNW + 2);
+constexpr int kProgDesc = 16;     // op descriptor ring slots (shared memory)
 
 // One CTA's share of one op: row tiles [rt_a, rt_b) x k-quads [kq_a, kq_b),
 // K slice s of S.
@@ -83,8 +89,12 @@ struct ProgArgs {
   int n_ops;
   uint32_t* done;  // n_ops op counters + 1 exit counter
   uint32_t* err;
-  int NST, stage_bytes, sB_bytes;
+  int NST, stage_bytes, sB_bytes, CH, PF;
+  int spin;  // which mbarrier waits poll (test_wait) instead of try_wait: 1 full, 2 rempty, 4 empty, 8 rfull
+  int dbg;  // tuning experiments: 1 = skip the mma compute, 2 = also skip x staging
+  long long* trace;  // tuning: CTA 0 event clocks [4][kTraceN] (producer issue, full, done, epilogue)
 };
+constexpr int kTraceN = 4096;
 
 namespace {
 
@@ -223,11 +233,31 @@ __device__ void stage_x(const ProgOp& op, int kq0, int kq1, uint32_t* sB, float*
 
 // One chunk of n blocks (k-quads of one row tile) in stage st, consumed by nw
 // warps (units warp, warp+nw, ...), two units in flight per warp.
-template <int FMT, int SS>
+template <int FMT, int SS, int MODE = 0>
 __device__ __forceinline__ void consume_chunk(const uint8_t* st, int n, int kt_base, int warp, int nw, int lane,
                                               const uint32_t* sB, float (&acc)[1][2]) {
   constexpr int E = 4 / SS;
+  constexpr bool kB = MODE != 4;
+  constexpr bool kOnesMma = MODE != 11;
   if (warp >= n) return;
+  if constexpr (MODE == 5) {  // tuning experiment: no stage reads
+    Unit<FMT, E> u;
+#pragma unroll
+    for (int i = 0; i < Unit<FMT, E>::NV; ++i) u.v[i] = lane * 0x01010101u + i;
+#pragma unroll
+    for (int i = 0; i < Unit<FMT, E>::NM; ++i) u.m[i] = 0x44444444u;
+#pragma unroll
+    for (int i = 0; i < 2 * Unit<FMT, E>::NS; ++i) u.s[i] = 0x3c000000u;
+#pragma unroll
+    for (int i = 0; i < Unit<FMT, E>::NS; ++i) u.z[i] = 0x0808u;
+    const uint32_t* pb = sB + (kt_base + warp * 4) * 32 + (lane & 7) * 4;
+    for (int kql = warp; kql < n; kql += nw) {
+      compute_unit<FMT, SS, 1>(u, pb, 0, 8, acc);
+      pb += nw * 4 * 32;
+      u.v[0] += acc[0][0] > 0.f;
+    }
+    return;
+  }
   Cursor c0 = make_cursor<FMT, E>(st, n, warp, lane, sB, kt_base + warp * 4, 8);
   int kql = warp;
   for (; kql + nw < n; kql += 2 * nw) {
@@ -236,14 +266,14 @@ __device__ __forceinline__ void consume_chunk(const uint8_t* st, int n, int kt_b
     Unit<FMT, E> u0, u1;
     lds_unit<FMT, E>(u0, c0);
     lds_unit<FMT, E>(u1, c1);
-    compute_unit<FMT, SS, 1>(u0, c0.b, 0, 8, acc);
-    compute_unit<FMT, SS, 1>(u1, c1.b, 0, 8, acc);
+    compute_unit<FMT, SS, 1, kB, kOnesMma>(u0, c0.b, 0, 8, acc);
+    compute_unit<FMT, SS, 1, kB, kOnesMma>(u1, c1.b, 0, 8, acc);
     advance<FMT, E>(c0, 2 * nw, 8);
   }
   if (kql < n) {
     Unit<FMT, E> u;
     lds_unit<FMT, E>(u, c0);
-    compute_unit<FMT, SS, 1>(u, c0.b, 0, 8, acc);
+    compute_unit<FMT, SS, 1, kB, kOnesMma>(u, c0.b, 0, 8, acc);
   }
 }
 
@@ -261,6 +291,123 @@ __device__ __forceinline__ void consume_dispatch(int fmt, int SS, const uint8_t*
     case I4_DENSE * 8 + 1: consume_chunk<I4_DENSE, 1>(st, n, kt_base, warp, nw, lane, sB, acc); break;
     case F16_SP24 * 8 + 4: consume_chunk<F16_SP24, 4>(st, n, kt_base, warp, nw, lane, sB, acc); break;
     default: consume_chunk<F16_SP14, 4>(st, n, kt_base, warp, nw, lane, sB, acc); break;
+  }
+}
+
+// The producer's walk over this CTA's chunks (the iteration order below),
+// holding just what a bulk copy needs.  Two cursors run over the same
+// sequence: the ring's and an L2-prefetch cursor PF chunks ahead of it.
+struct ChunkCursor {
+  const uint8_t* vals;
+  const uint8_t* meta;
+  const float* scales;
+  const uint8_t* zps;
+  int fmt, E, KQ, rt_begin, blk_bytes;
+  int j, NP, r0, r1, p, k0, k1, rt, kq, n;
+  ProgItem it;
+  bool valid;
+
+  __device__ __forceinline__ void begin() {
+    j = -1;
+    valid = true;
+    rt = r1 = 0;
+    p = NP = 0;
+    kq = k1 = 0;
+    n = 0;
+  }
+  // advance to the next chunk; false at the end of the program
+  __device__ __forceinline__ bool next(const ProgArgs& a, int c, int CH) {
+    kq += n;
+    while (true) {
+      if (kq < k1) {
+        n = min(CH, k1 - kq);
+        return true;
+      }
+      if (++rt < r1) {
+        kq = k0;
+        continue;
+      }
+      if (++p < NP) {
+        k0 = panel_lo(it, p, NP);
+        k1 = panel_lo(it, p + 1, NP);
+        rt = r0;
+        kq = k0;
+        continue;
+      }
+      if (r1 < it.rt_b && j >= 0) {
+        r0 = r1;
+        r1 = min(static_cast<int>(it.rt_b), r0 + kProgRowsAcc);
+        p = -1;
+        k1 = kq = 0;
+        rt = r1;
+        continue;
+      }
+      // next op with work for this CTA
+      do {
+        if (++j >= a.n_ops) {
+          valid = false;
+          return false;
+        }
+        const ProgOp* o = a.ops + j;
+        const ProgItem* items =
+            reinterpret_cast<const ProgItem*>(__ldg(reinterpret_cast<const unsigned long long*>(&o->items)));
+        it = ldg_struct(items + c);
+      } while (it.rt_a >= it.rt_b);
+      const ProgOp* o = a.ops + j;
+      vals = reinterpret_cast<const uint8_t*>(__ldg(reinterpret_cast<const unsigned long long*>(&o->vals)));
+      meta = reinterpret_cast<const uint8_t*>(__ldg(reinterpret_cast<const unsigned long long*>(&o->meta)));
+      scales = reinterpret_cast<const float*>(__ldg(reinterpret_cast<const unsigned long long*>(&o->scales)));
+      zps = reinterpret_cast<const uint8_t*>(__ldg(reinterpret_cast<const unsigned long long*>(&o->zps)));
+      fmt = __ldg(&o->fmt);
+      E = __ldg(&o->E);
+      KQ = __ldg(&o->KQ);
+      rt_begin = __ldg(&o->rt_begin);
+      blk_bytes = __ldg(&o->blk_bytes);
+      NP = n_panels(it);
+      r0 = it.rt_a;
+      r1 = min(static_cast<int>(it.rt_b), r0 + kProgRowsAcc);
+      p = 0;
+      k0 = panel_lo(it, 0, NP);
+      k1 = panel_lo(it, 1, NP);
+      rt = r0;
+      kq = k0;
+      n = 0;
+    }
+  }
+  __device__ __forceinline__ size_t blk() const { return static_cast<size_t>(rt_begin + rt) * KQ + kq; }
+};
+
+__device__ __forceinline__ void issue_cursor(const ChunkCursor& q, uint8_t* st, uint64_t* bar, uint64_t pol,
+                                             int dbg = 0) {
+  const int VB = val_lane_bytes(q.fmt), MB = meta_lane_bytes(q.fmt);
+  const size_t blk = q.blk();
+  if (dbg == 6) {  // tuning experiment: one bulk copy of the chunk's byte count
+    mbar_expect_tx(bar, static_cast<uint32_t>(q.n * q.blk_bytes));
+    bulk_g2s(st, q.vals + blk * 32 * VB, q.n * q.blk_bytes, bar, pol);
+    return;
+  }
+  mbar_expect_tx(bar, static_cast<uint32_t>(q.n * q.blk_bytes));
+  bulk_g2s(st, q.vals + blk * 32 * VB, q.n * 32 * VB, bar, pol);
+  if (MB > 0) bulk_g2s(st + q.n * 32 * VB, q.meta + blk * 32 * MB, q.n * 32 * MB, bar, pol);
+  if (has_scales(q.fmt)) {
+    uint8_t* sp = st + q.n * 32 * (VB + MB);
+    bulk_g2s(sp, q.scales + blk * q.E * 16, q.n * q.E * 64, bar, pol);
+    bulk_g2s(sp + q.n * q.E * 64, q.zps + blk * q.E * 16, q.n * q.E * 16, bar, pol);
+  }
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void prefetch_cursor(const ChunkCursor& q) {
+  const int VB = val_lane_bytes(q.fmt), MB = meta_lane_bytes(q.fmt);
+  const size_t blk = q.blk();
+  prefetch_l2(q.vals + blk * 32 * VB, q.n * 32 * VB);
+  if (MB > 0) prefetch_l2(q.meta + blk * 32 * MB, q.n * 32 * MB);
+  if (has_scales(q.fmt)) {
+    prefetch_l2(q.scales + blk * q.E * 16, q.n * q.E * 64);
+    prefetch_l2(q.zps + blk * q.E * 16, q.n * q.E * 16);
   }
 }
 
@@ -288,7 +435,11 @@ __global__ void __launch_bounds__(kProgThreads, 1) program_kernel(const ProgArgs
   uint64_t* empty = full + NST;
   uint64_t* rfull = empty + NST;
   uint64_t* rempty = rfull + kProgRed;
-  float* red = reinterpret_cast<float*>(smem_raw + ((16 * NST + 16 * kProgRed + 127) / 128) * 128);  // [R][nw][16]
+  uint64_t* dfull = rempty + kProgRed;
+  uint64_t* dempty = dfull + kProgDesc;
+  ProgOp* sdesc = reinterpret_cast<ProgOp*>(smem_raw + ((16 * NST + 16 * kProgRed + 16 * kProgDesc + 127) / 128) * 128);
+  ProgItem* sitem = reinterpret_cast<ProgItem*>(sdesc + kProgDesc);
+  float* red = reinterpret_cast<float*>(sitem + kProgDesc);  // [R][nw][16]
   float* red_ss = red + kProgRed * nw * 16;         // [32]
   float* acc_s = red_ss + 32;                       // [kProgRowsAcc][16]
   uint32_t* sB = reinterpret_cast<uint32_t*>(acc_s + kProgRowsAcc * 16);
@@ -303,6 +454,10 @@ __global__ void __launch_bounds__(kProgThreads, 1) program_kernel(const ProgArgs
       mbar_init(rfull + s, nw);
       mbar_init(rempty + s, 1);
     }
+    for (int s = 0; s < kProgDesc; ++s) {
+      mbar_init(dfull + s, 1);
+      mbar_init(dempty + s, nw + 1);
+    }
     mbar_fence_init();
   }
   __syncthreads();
@@ -314,29 +469,44 @@ __global__ void __launch_bounds__(kProgThreads, 1) program_kernel(const ProgArgs
       int s = 0;
       uint32_t phase = 0;
       long long q = 0;
-      for (int j = 0; j < a.n_ops; ++j) {
-        const ProgOp op = ldg_struct(a.ops + j);
-        const ProgItem it = ldg_struct(op.items + c);
-        if (it.rt_a >= it.rt_b) continue;
-        const int NP = n_panels(it);
-        for (int r0 = it.rt_a; r0 < it.rt_b; r0 += kProgRowsAcc) {
-          const int r1 = min(static_cast<int>(it.rt_b), r0 + kProgRowsAcc);
-          for (int p = 0; p < NP; ++p) {
-            const int k0 = panel_lo(it, p, NP), k1 = panel_lo(it, p + 1, NP);
-            for (int rt = r0; rt < r1; ++rt)
-              for (int kq = k0; kq < k1; kq += kProgCH) {
-                const int n = min(kProgCH, k1 - kq);
-                if (q >= NST) mbar_wait(empty + s, phase ^ 1u);
-                issue_chunk(op, stages + static_cast<size_t>(s) * a.stage_bytes, full + s, rt, kq, n, pol);
-                ++q;
-                if (++s == NST) {
-                  s = 0;
-                  phase ^= 1u;
-                }
-              }
-          }
+      ChunkCursor cur, pf;
+      cur.begin();
+      pf.begin();
+      // op descriptors (+ this CTA's item) go into a shared-memory ring for
+      // the consumer and epilogue warps, published ahead of their use
+      int pub = 0;
+      auto publish = [&](int upto) {
+        for (; pub <= upto && pub < a.n_ops; ++pub) {
+          const int ds = pub % kProgDesc;
+          if (pub >= kProgDesc) mbar_wait(dempty + ds, ((pub / kProgDesc) - 1) & 1);
+          const ProgOp o = ldg_struct(a.ops + pub);
+          sdesc[ds] = o;
+          sitem[ds] = ldg_struct(o.items + c);
+          mbar_arrive(dfull + ds);
+        }
+      };
+      publish(1);
+      // L2 prefetch runs a.PF chunks ahead of the ring: DRAM latency under
+      // load is several us, far more than the ring's ~200 KB covers
+      for (int i = 0; i < a.PF && pf.next(a, c, a.CH); ++i) prefetch_cursor(pf);
+      while (cur.next(a, c, a.CH)) {
+        publish(cur.j + 2);
+        if (q >= NST) {
+          if (a.spin & 4)
+            mbar_wait_spin(empty + s, phase ^ 1u);
+          else
+            mbar_wait(empty + s, phase ^ 1u);
+        }
+        if (a.trace && c == 0 && q < kTraceN) a.trace[q] = clock64();
+        issue_cursor(cur, stages + static_cast<size_t>(s) * a.stage_bytes, full + s, pol, a.dbg);
+        if (a.PF > 0 && pf.valid && pf.next(a, c, a.CH)) prefetch_cursor(pf);
+        ++q;
+        if (++s == NST) {
+          s = 0;
+          phase ^= 1u;
         }
       }
+      publish(a.n_ops - 1);
     }
     return;
   }
@@ -344,17 +514,25 @@ __global__ void __launch_bounds__(kProgThreads, 1) program_kernel(const ProgArgs
   if (warp == nw + 1) {
     // ------------------------------------------------------------ epilogue
     int slot = 0;
+    long long qe = 0;
     uint32_t rphase = 0;
     for (int j = 0; j < a.n_ops; ++j) {
-      const ProgOp op = ldg_struct(a.ops + j);
-      const ProgItem it = ldg_struct(op.items + c);
+      const int ds = j % kProgDesc;
+      mbar_wait(dfull + ds, (j / kProgDesc) & 1);
+      const ProgOp& op = sdesc[ds];
+      const ProgItem it = sitem[ds];
       if (it.rt_a < it.rt_b) {
         const int NP = n_panels(it);
         for (int r0 = it.rt_a; r0 < it.rt_b; r0 += kProgRowsAcc) {
           const int r1 = min(static_cast<int>(it.rt_b), r0 + kProgRowsAcc);
           for (int p = 0; p < NP; ++p)
             for (int rt = r0; rt < r1; ++rt) {
-              mbar_wait(rfull + slot, rphase);
+              if (a.spin & 8)
+                mbar_wait_spin(rfull + slot, rphase);
+              else
+                mbar_wait(rfull + slot, rphase);
+              if (a.trace && c == 0 && lane == 0 && qe < kTraceN) a.trace[3 * kTraceN + qe] = clock64();
+              ++qe;
               float v = 0.f;
               if (lane < 16) {
                 const float* rs = red + slot * nw * 16 + lane;
@@ -411,7 +589,10 @@ __global__ void __launch_bounds__(kProgThreads, 1) program_kernel(const ProgArgs
           }
         }
       }
-      if (op.need_done) {
+      const int need_done = op.need_done;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(dempty + ds);
+      if (need_done) {
         __threadfence();
         __syncwarp();
         if (lane == 0) atomicAdd(a.done + j, 1u);
@@ -432,14 +613,21 @@ __global__ void __launch_bounds__(kProgThreads, 1) program_kernel(const ProgArgs
   const int nthr = nw * 32;
   int s = 0, slot = 0;
   uint32_t phase = 0, rphase = 0;
+  long long qc = 0;  // chunk counter (trace)
   // the x fragments in shared memory: (x, transform, k-quad range) of the
   // op that staged them; a wait invalidates them (x may have been rewritten)
   const float* staged_x = nullptr;
   int staged_xf = -1, staged_k0 = -1, staged_k1 = -1;
   for (int j = 0; j < a.n_ops; ++j) {
-    const ProgOp op = ldg_struct(a.ops + j);
-    const ProgItem it = ldg_struct(op.items + c);
-    if (it.rt_a >= it.rt_b) continue;
+    const int ds = j % kProgDesc;
+    mbar_wait(dfull + ds, (j / kProgDesc) & 1);
+    const ProgOp& op = sdesc[ds];
+    const ProgItem it = sitem[ds];
+    if (it.rt_a >= it.rt_b) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(dempty + ds);
+      continue;
+    }
     if (op.wait >= 0) {
       if (tid == 0) {
         const uint64_t t0 = globaltimer();
@@ -453,7 +641,7 @@ __global__ void __launch_bounds__(kProgThreads, 1) program_kernel(const ProgArgs
       const int r1 = min(static_cast<int>(it.rt_b), r0 + kProgRowsAcc);
       for (int p = 0; p < NP; ++p) {
         const int k0 = panel_lo(it, p, NP), k1 = panel_lo(it, p + 1, NP);
-        if (staged_x != op.x || staged_xf != op.xform || staged_k0 != k0 || staged_k1 != k1) {
+        if (a.dbg < 2 && (staged_x != op.x || staged_xf != op.xform || staged_k0 != k0 || staged_k1 != k1)) {
           consumer_bar(nthr);  // every warp is done with the previous fragments
           stage_x(op, k0, k1, sB, red_ss, tid, nthr);
           consumer_bar(nthr);
@@ -464,12 +652,37 @@ __global__ void __launch_bounds__(kProgThreads, 1) program_kernel(const ProgArgs
         }
         for (int rt = r0; rt < r1; ++rt) {
           float acc[1][2] = {{0.f, 0.f}};
-          for (int kq = k0; kq < k1; kq += kProgCH) {
-            const int n = min(kProgCH, k1 - kq);
-            mbar_wait(full + s, phase);
-            consume_dispatch(op.fmt, op.SS, stages + static_cast<size_t>(s) * a.stage_bytes, n, (kq - k0) * 4,
-                             warp, nw, lane, sB, acc);
+          for (int kq = k0; kq < k1; kq += a.CH) {
+            const int n = min(a.CH, k1 - kq);
+            if (a.spin & 1)
+              mbar_wait_spin(full + s, phase);
+            else
+              mbar_wait(full + s, phase);
+            if (a.trace && c == 0 && tid == 0 && qc < kTraceN) a.trace[kTraceN + qc] = clock64();
+            if (a.dbg == 4 && op.fmt == I4_SP24 && op.SS == 4)
+              consume_chunk<I4_SP24, 4, 4>(stages + static_cast<size_t>(s) * a.stage_bytes, n, (kq - k0) * 4, warp,
+                                           nw, lane, sB, acc);
+            else if (a.dbg == 11 && op.fmt == I4_SP24 && op.SS == 4)
+              consume_chunk<I4_SP24, 4, 11>(stages + static_cast<size_t>(s) * a.stage_bytes, n, (kq - k0) * 4, warp,
+                                            nw, lane, sB, acc);
+            else if (a.dbg == 5 && op.fmt == I4_SP24 && op.SS == 4)
+              consume_chunk<I4_SP24, 4, 5>(stages + static_cast<size_t>(s) * a.stage_bytes, n, (kq - k0) * 4, warp,
+                                           nw, lane, sB, acc);
+            else if (a.dbg == 9) {  // tuning experiment: ALU-only busy work of a chunk's length
+              float v = acc[0][0] + lane;
+              for (int i = 0; i < 2 * 60; ++i) v = fmaf(v, 1.0001f, 0.5f);
+              acc[0][0] = v;
+            } else if (a.dbg == 10) {  // tuning experiment: LDS-only reads of the stage
+              const uint4* sp = reinterpret_cast<const uint4*>(stages + static_cast<size_t>(s) * a.stage_bytes);
+              uint32_t t = 0;
+              for (int i = warp * 32 + lane; i < n * 53; i += nw * 32) t ^= sp[i].x ^ sp[i].w;
+              acc[0][0] += static_cast<float>(t & 1);
+            } else if (a.dbg == 0 || a.dbg == 6)
+              consume_dispatch(op.fmt, op.SS, stages + static_cast<size_t>(s) * a.stage_bytes, n, (kq - k0) * 4,
+                               warp, nw, lane, sB, acc);
             __syncwarp();
+            if (a.trace && c == 0 && tid == 0 && qc < kTraceN) a.trace[2 * kTraceN + qc] = clock64();
+            ++qc;
             if (lane == 0) mbar_arrive(empty + s);
             if (++s == NST) {
               s = 0;
@@ -478,7 +691,10 @@ __global__ void __launch_bounds__(kProgThreads, 1) program_kernel(const ProgArgs
           }
           // lane (g, t = 0) holds token 0 (B columns 0 = hi, 1 = lo, summed by
           // compute_unit): rows g and g+8 of the row tile
-          mbar_wait(rempty + slot, rphase ^ 1u);
+          if (a.spin & 2)
+            mbar_wait_spin(rempty + slot, rphase ^ 1u);
+          else
+            mbar_wait(rempty + slot, rphase ^ 1u);
           if ((lane & 3) == 0) {
             float* rs = red + (slot * nw + warp) * 16;
             rs[lane >> 2] = acc[0][0];
@@ -493,6 +709,8 @@ __global__ void __launch_bounds__(kProgThreads, 1) program_kernel(const ProgArgs
         }
       }
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(dempty + ds);
   }
 }
 
@@ -502,7 +720,7 @@ __global__ void __launch_bounds__(kProgThreads, 1) program_kernel(const ProgArgs
 
 struct egt_program {
   int device = 0;
-  int G = 0, NST = 0, stage_bytes = 0, sB_bytes = 0, smem = 0;
+  int G = 0, NST = 0, stage_bytes = 0, sB_bytes = 0, smem = 0, CH = 0;
   uint32_t n_ops = 0;
   bool coop = true;
   double max_load = 0, avg_load = 0;  // bytes per CTA (whole program)
@@ -510,6 +728,7 @@ struct egt_program {
   egt_impl::ProgOp* d_ops = nullptr;
   uint32_t* d_done = nullptr;
   uint32_t* d_err = nullptr;
+  long long* trace = nullptr;  // EGT_PROGRAM_TRACE=1: CTA 0 event clocks
 };
 
 namespace egt_impl {
@@ -529,18 +748,19 @@ bool overlaps(const void* a, size_t na, const void* b, size_t nb) {
 
 size_t al256(size_t v) { return (v + 255) / 256 * 256; }
 
-// K slices for an op with RT row tiles of KQ k-quads on G CTAs: S = 1 when
-// the row tiles alone fill the grid; otherwise the S minimising the busiest
-// CTA's blocks (ceil(RT / CTAs per slice) x ceil(KQ / S)) plus a small cost
-// per extra slice (partial stores and the arrival round trip).
+// K slices for an op with RT row tiles of KQ k-quads on G CTAs.  A slice
+// split costs the epilogue warp a fence + atomic round trip + partial reloads
+// (several us), so S = 1 unless the row tiles leave most of the grid idle;
+// then the S minimising the busiest CTA's blocks, ceil(RT / CTAs per slice)
+// x ceil(KQ / S), plus a per-slice penalty.
 int choose_slices(int RT, int KQ, int G) {
-  if (RT >= 2 * G) return 1;
+  if (2 * RT >= G) return 1;
   int best_S = 1;
   double best = 1e300;
   for (int S = 1; S <= std::min({KQ, G, 64}); ++S) {
     const int g_min = G / S;  // smallest group
     const double rows = std::ceil(static_cast<double>(RT) / g_min);
-    const double cost = rows * std::ceil(static_cast<double>(KQ) / S) + (S > 1 ? 4.0 + 0.5 * S : 0.0);
+    const double cost = rows * std::ceil(static_cast<double>(KQ) / S) + (S > 1 ? 24.0 + 2.0 * S : 0.0);
     if (cost < best * 0.98) {
       best = cost;
       best_S = S;
@@ -684,9 +904,12 @@ egt_status egt_program_create(const egt_program_op* ops, uint32_t n_ops, void* s
   for (double v : load) tot += v;
   prog->avg_load = tot / G;
   prog->sB_bytes = max_panel * 4 * 128;
-  prog->stage_bytes = kProgCH * max_blk;
-  const int bars = (16 * 64 + 16 * kProgRed + 127) / 128 * 128;  // room for up to 64 stages
-  const int fixed = bars + (kProgRed * kProgNW * 16 + 32 + kProgRowsAcc * 16) * 4 + prog->sB_bytes;
+  prog->CH = kProgCH;
+  if (const char* e = getenv("EGT_PROGRAM_CH")) prog->CH = std::max(1, atoi(e));
+  prog->stage_bytes = prog->CH * max_blk;
+  const int bars = (16 * 64 + 16 * kProgRed + 16 * kProgDesc + 127) / 128 * 128;  // room for up to 64 stages
+  const int fixed = bars + kProgDesc * static_cast<int>(sizeof(ProgOp) + sizeof(ProgItem)) +
+                    (kProgRed * kProgNW * 16 + 32 + kProgRowsAcc * 16) * 4 + prog->sB_bytes;
   int nst = std::min(64, (smem_optin - fixed) / prog->stage_bytes);
   if (const char* e = getenv("EGT_PROGRAM_NST")) nst = std::min(nst, atoi(e));
   if (nst < 2) {
@@ -694,7 +917,7 @@ egt_status egt_program_create(const egt_program_op* ops, uint32_t n_ops, void* s
     return pfail(EGT_EINVAL, "program: shared memory cannot hold two stages");
   }
   prog->NST = nst;
-  prog->smem = (16 * nst + 16 * kProgRed + 127) / 128 * 128 + (fixed - bars) + nst * prog->stage_bytes;
+  prog->smem = (16 * nst + 16 * kProgRed + 16 * kProgDesc + 127) / 128 * 128 + (fixed - bars) + nst * prog->stage_bytes;
   const size_t ops_b = al256(sizeof(ProgOp) * n_ops);
   const size_t items_b = al256(sizeof(ProgItem) * static_cast<size_t>(G) * n_ops);
   const size_t done_b = al256(4ull * (n_ops + 2));
@@ -734,7 +957,19 @@ egt_status egt_program_create(const egt_program_op* ops, uint32_t n_ops, void* s
     delete prog;
     return pfail(EGT_ECUDA, std::string("program: setup failed: ") + cudaGetErrorString(e));
   }
+  if (getenv("EGT_PROGRAM_TRACE")) {
+    cudaMalloc(&prog->trace, sizeof(long long) * 4 * egt_impl::kTraceN);
+    cudaMemset(prog->trace, 0, sizeof(long long) * 4 * egt_impl::kTraceN);
+  }
   *out = prog;
+  return EGT_OK;
+}
+
+egt_status egt_program_debug_trace(const egt_program* prog, long long* host, size_t n) {
+  if (!prog || !prog->trace) return pfail(EGT_EINVAL, "program: tracing is off (EGT_PROGRAM_TRACE)");
+  n = std::min<size_t>(n, 4 * egt_impl::kTraceN);
+  if (cudaMemcpy(host, prog->trace, n * sizeof(long long), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return pfail(EGT_ECUDA, "program: trace copy failed");
   return EGT_OK;
 }
 
@@ -749,6 +984,13 @@ egt_status egt_program_run(const egt_program* prog, void* stream) {
   a.NST = prog->NST;
   a.stage_bytes = prog->stage_bytes;
   a.sB_bytes = prog->sB_bytes;
+  a.CH = prog->CH;
+  a.PF = prog->NST;
+  a.spin = getenv("EGT_PROGRAM_SPIN") ? atoi(getenv("EGT_PROGRAM_SPIN")) : 0;
+  if (const char* e = getenv("EGT_PROGRAM_PF")) a.PF = atoi(e);
+  static const int dbg = getenv("EGT_PROGRAM_DEBUG") ? atoi(getenv("EGT_PROGRAM_DEBUG")) : 0;
+  a.dbg = dbg;
+  a.trace = prog->trace;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(prog->G);
   cfg.blockDim = dim3(kProgThreads);
@@ -781,6 +1023,7 @@ egt_status egt_program_query(const egt_program* prog, egt_program_info* info) {
 egt_status egt_program_destroy(egt_program* prog) {
   if (prog) {
     cudaFree(prog->dev);
+    cudaFree(prog->trace);
     delete prog;
   }
   return EGT_OK;

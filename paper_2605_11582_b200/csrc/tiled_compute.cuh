@@ -156,7 +156,7 @@ constexpr float kTwo24 = 16777216.f;
 constexpr float kTwo20 = 1048576.f;
 constexpr uint32_t kOnes = 0x3C003C00u;  // half2(1, 1)
 
-template <int FMT, int SS, int NT>
+template <int FMT, int SS, int NT, bool kLoadB = true, bool kOnesMma = true>
 __device__ __forceinline__ void compute_unit(const Unit<FMT, 4 / SS>& u, const uint32_t* pb, int KTc,
                                              int LS, float (&acc)[NT][2]) {
   constexpr bool kOnesTrick = (FMT == I4_SP24 || FMT == I4_DENSE);
@@ -181,13 +181,18 @@ __device__ __forceinline__ void compute_unit(const Unit<FMT, 4 / SS>& u, const u
       }
     }
     uint32_t b[NT][4];
-    load_b<NT>(b, pb + j * LS * 4, KTc * LS * 4);
+    if constexpr (kLoadB) {
+      load_b<NT>(b, pb + j * LS * 4, KTc * LS * 4);
+    } else {  // tuning experiment: B from registers (results are garbage)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) b[nt][0] = b[nt][1] = b[nt][2] = b[nt][3] = u.m[0] ^ j;
+    }
     if constexpr (FMT == I4_SP24) {
       const uint32_t w = u.v[j], w8 = w >> 8;
       const uint32_t a[4] = {w & 0x000F000Fu, w & 0x00F000F0u, w8 & 0x000F000Fu, w8 & 0x00F000F0u};
       const uint32_t ones[4] = {kOnes, kOnes, kOnes, kOnes};
       mma_sp_sel<NT>(j, d, a, b, u.m[j >> 1]);
-      mma_sp_sel<NT>(j, d1, ones, b, u.m[j >> 1]);
+      if constexpr (kOnesMma) mma_sp_sel<NT>(j, d1, ones, b, u.m[j >> 1]);
     } else if constexpr (FMT == F16_SP24) {
       const uint32_t a[4] = {u.v[4 * j + 0], u.v[4 * j + 1], u.v[4 * j + 2], u.v[4 * j + 3]};
       mma_sp_sel<NT>(j, d, a, b, u.m[j >> 1]);

@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libegt_b200.so")
+LIB_PATH = os.environ.get("EGT_LIB_PATH") or os.path.join(_HERE, "_lib", "libegt_b200.so")
 
 EGT_OK, EGT_EINVAL, EGT_EFORMAT, EGT_EINTERNAL, EGT_ECUDA = range(5)
 KIND_F32, KIND_INT4 = 0, 1
@@ -149,6 +149,7 @@ _PROGRAM_SIGNATURES = {
     "egt_program_run": (C.c_int, [C.c_void_p, C.c_void_p]),
     "egt_program_query": (C.c_int, [C.c_void_p, C.POINTER(ProgramInfo)]),
     "egt_program_destroy": (C.c_int, [C.c_void_p]),
+    "egt_program_debug_trace": (C.c_int, [C.c_void_p, C.POINTER(C.c_longlong), C.c_size_t]),
 }
 
 SIGNATURES.update(_MODEL_SIGNATURES)

@@ -31,8 +31,9 @@ def main():
         cub = [os.path.join(tmp, f) for f in os.listdir(tmp) if f.endswith(".cubin")][0]
     else:
         cub = binpath
-    sass = subprocess.run(["nvdisasm", "-g", "-c", cub], capture_output=True, text=True).stdout
+    sass = subprocess.run(["nvdisasm", "-gi", "-c", cub], capture_output=True, text=True).stdout
     cur = None
+    chain = []
     infn = False
     line_of = {}
     for ln in sass.splitlines():
@@ -43,14 +44,21 @@ def main():
             continue
         m = re.search(r'//## File "([^"]+)", line (\d+)(.*)', ln)
         if m:
-            cur = f"{os.path.basename(m.group(1))}:{m.group(2)}"
+            frame = f"{os.path.basename(m.group(1))}:{m.group(2)}"
             inl = re.search(r'inlined at "([^"]+)", line (\d+)', m.group(3))
+            if not chain:
+                chain = [frame]
             if inl:
-                cur += f" <- {os.path.basename(inl.group(1))}:{inl.group(2)}"
+                chain.append(f"{os.path.basename(inl.group(1))}:{inl.group(2)}")
             continue
         m = re.search(r"/\*([0-9a-f]{4,})\*/", ln)
-        if m and cur:
-            line_of[int(m.group(1), 16)] = cur
+        if m:
+            if chain:
+                # innermost frame and the outermost frame (the kernel body line)
+                cur = chain[0] if len(chain) == 1 else f"{chain[0]} <- {chain[-1]}"
+                chain = []
+            if cur:
+                line_of[int(m.group(1), 16)] = cur
     agg = defaultdict(lambda: [0.0, 0.0])
     tot = 0.0
     for r in data:
