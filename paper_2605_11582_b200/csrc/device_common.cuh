@@ -63,6 +63,13 @@ __device__ __forceinline__ uint32_t nib2_magic(uint32_t v) {
   return r;  // (v & mask) | magic
 }
 
+// INT4 nibble pair at bits [4,8) and [20,24) -> half2 {1024 + 16 lo, 1024 + 16 hi}.
+__device__ __forceinline__ uint32_t nib16_magic(uint32_t v) {
+  uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;\n" : "=r"(r) : "r"(v), "r"(0x00F000F0u), "r"(0x64006400u));
+  return r;
+}
+
 __device__ __forceinline__ uint32_t hsub2_u32(uint32_t a, uint32_t b) {
   __half2 r = __hsub2(*reinterpret_cast<__half2*>(&a), *reinterpret_cast<__half2*>(&b));
   return *reinterpret_cast<uint32_t*>(&r);

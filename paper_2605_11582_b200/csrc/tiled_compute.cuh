@@ -159,13 +159,20 @@ constexpr uint32_t kOnes = 0x3C003C00u;  // half2(1, 1)
 template <int FMT, int SS, int NT, bool kLoadB = true, bool kOnesMma = true>
 __device__ __forceinline__ void compute_unit(const Unit<FMT, 4 / SS>& u, const uint32_t* pb, int KTc,
                                              int LS, float (&acc)[NT][2]) {
-  constexpr bool kOnesTrick = (FMT == I4_SP24 || FMT == I4_DENSE);
+  // INT4 2:4 and dense: the zero point is subtracted in the A operand.  A
+  // nibble under the fp16 exponent 0x64 is exactly 1024 + c (row g) or
+  // 1024 + 16c (row g+8, 4 bits higher); HSUB2 with 1024 + z (1024 + 16z)
+  // leaves c - z (16(c - z)), exact in fp16, so one mma per k-tile suffices.
+  // (kOnesMma = false falls back to the subnormal-nibble path whose zero point
+  // comes from a second mma over A = 1.0.)
+  constexpr bool kZpInA = (FMT == I4_SP24 || FMT == I4_DENSE) && kOnesMma;
+  constexpr bool kOnesTrick = (FMT == I4_SP24 || FMT == I4_DENSE) && !kZpInA;
   // B fragments: lanes whose column holds no token (lane >= LS) read lane&7's
   // slot unpredicated -- D column n only depends on B column n, and the
   // columns of absent tokens are never used (make_cursor).
   float d[NT][4];
   float d1[NT][4];
-  uint32_t zpair = 0;
+  uint32_t zpair = 0, zA = 0, zA8 = 0;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int e = j / SS;
@@ -179,6 +186,10 @@ __device__ __forceinline__ void compute_unit(const Unit<FMT, 4 / SS>& u, const u
         const uint32_t z0 = u.z[e] & 0xFFu, z1 = (u.z[e] >> 8) & 0xFFu;
         zpair = zp_magic(z0, z1);
       }
+      if constexpr (kZpInA) {
+        zA = (0x6400u | (u.z[e] & 0xFFu)) * 0x10001u;
+        zA8 = (0x6400u | ((u.z[e] >> 4) & 0xF0u)) * 0x10001u;
+      }
     }
     uint32_t b[NT][4];
     if constexpr (kLoadB) {
@@ -187,7 +198,12 @@ __device__ __forceinline__ void compute_unit(const Unit<FMT, 4 / SS>& u, const u
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) b[nt][0] = b[nt][1] = b[nt][2] = b[nt][3] = u.m[0] ^ j;
     }
-    if constexpr (FMT == I4_SP24) {
+    if constexpr (FMT == I4_SP24 && kZpInA) {
+      const uint32_t w = u.v[j], w8 = w >> 8;
+      const uint32_t a[4] = {hsub2_u32(nib2_magic(w), zA), hsub2_u32(nib16_magic(w), zA8),
+                             hsub2_u32(nib2_magic(w8), zA), hsub2_u32(nib16_magic(w8), zA8)};
+      mma_sp_sel<NT>(j, d, a, b, u.m[j >> 1]);
+    } else if constexpr (FMT == I4_SP24) {
       const uint32_t w = u.v[j], w8 = w >> 8;
       const uint32_t a[4] = {w & 0x000F000Fu, w & 0x00F000F0u, w8 & 0x000F000Fu, w8 & 0x00F000F0u};
       const uint32_t ones[4] = {kOnes, kOnes, kOnes, kOnes};
@@ -214,6 +230,15 @@ __device__ __forceinline__ void compute_unit(const Unit<FMT, 4 / SS>& u, const u
       a[3] = place_hi(r1, sl & 8u);
       const uint32_t plane = (u.m[0] >> (16 + 8 * (j >> 1))) & 0xFFu;
       mma_sp_sel<NT>(j, d, a, b, 0x44444444u | (spread4(plane) * 0xAu));
+    } else if constexpr (kZpInA) {  // I4_DENSE: two m16n8k16 per 32-column k-tile
+      const uint32_t w0 = u.v[2 * j], w1 = u.v[2 * j + 1], w08 = w0 >> 8, w18 = w1 >> 8;
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) {
+        mma_16816(d[nt], hsub2_u32(nib2_magic(w0), zA), hsub2_u32(nib16_magic(w0), zA8),
+                  hsub2_u32(nib2_magic(w08), zA), hsub2_u32(nib16_magic(w08), zA8), b[nt][0], b[nt][1]);
+        mma_16816(d[nt], hsub2_u32(nib2_magic(w1), zA), hsub2_u32(nib16_magic(w1), zA8),
+                  hsub2_u32(nib2_magic(w18), zA), hsub2_u32(nib16_magic(w18), zA8), b[nt][2], b[nt][3]);
+      }
     } else {  // I4_DENSE: two m16n8k16 per 32-column k-tile
       const uint32_t w0 = u.v[2 * j], w1 = u.v[2 * j + 1], w08 = w0 >> 8, w18 = w1 >> 8;
 #pragma unroll
@@ -227,7 +252,14 @@ __device__ __forceinline__ void compute_unit(const Unit<FMT, 4 / SS>& u, const u
       }
     }
     if (j % SS == SS - 1) {
-      if constexpr (kOnesTrick) {
+      if constexpr (kZpInA) {
+        const float sg = __uint_as_float(u.s[2 * e]), sg8 = __uint_as_float(u.s[2 * e + 1]) * 0.0625f;
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          acc[nt][0] = fmaf(sg, d[nt][0] + d[nt][1], acc[nt][0]);
+          acc[nt][1] = fmaf(sg8, d[nt][2] + d[nt][3], acc[nt][1]);
+        }
+      } else if constexpr (kOnesTrick) {
         const float sg = __uint_as_float(u.s[2 * e]), sg8 = __uint_as_float(u.s[2 * e + 1]);
         const float cg = sg * kTwo24, cg8 = sg8 * kTwo20;
         const float ng = -sg * static_cast<float>(u.z[e] & 0xFFu);
