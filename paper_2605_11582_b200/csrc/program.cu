@@ -442,7 +442,8 @@ __global__ void __launch_bounds__(kProgThreads, 1) program_kernel(const ProgArgs
   float* red = reinterpret_cast<float*>(sitem + kProgDesc);  // [R][nw][16]
   float* red_ss = red + kProgRed * nw * 16;         // [32]
   float* acc_s = red_ss + 32;                       // [kProgRowsAcc][16]
-  uint32_t* sB = reinterpret_cast<uint32_t*>(acc_s + kProgRowsAcc * 16);
+  float* res_s = acc_s + kProgRowsAcc * 16;         // [kProgRowsAcc][16] residual rows of the op
+  uint32_t* sB = reinterpret_cast<uint32_t*>(res_s + kProgRowsAcc * 16);
   uint8_t* stages = reinterpret_cast<uint8_t*>(sB) + a.sB_bytes;
 
   if (tid == 0) {
@@ -523,6 +524,24 @@ __global__ void __launch_bounds__(kProgThreads, 1) program_kernel(const ProgArgs
       const ProgItem it = sitem[ds];
       if (it.rt_a < it.rt_b) {
         const int NP = n_panels(it);
+        // residual rows of the first kProgRowsAcc row tiles, fetched in one
+        // round trip once the op's inputs are complete (not one dependent
+        // load per segment)
+        const bool res_pre = op.res != nullptr && it.S == 1;
+        if (res_pre) {
+          if (op.wait >= 0) {
+            if (lane == 0) {
+              const uint64_t t0 = globaltimer();
+              while (ld_acquire(a.done + op.wait) < static_cast<uint32_t>(G)) trap_after(t0, a.err);
+              __threadfence();
+            }
+            __syncwarp();
+          }
+          const int n = min(static_cast<int>(it.rt_b - it.rt_a), kProgRowsAcc) * 16;
+          const int row0 = it.rt_a * 16;
+          for (int i = lane; i < n; i += 32) res_s[i] = row0 + i < op.rows ? __ldcg(op.res + row0 + i) : 0.f;
+          __syncwarp();
+        }
         for (int r0 = it.rt_a; r0 < it.rt_b; r0 += kProgRowsAcc) {
           const int r1 = min(static_cast<int>(it.rt_b), r0 + kProgRowsAcc);
           for (int p = 0; p < NP; ++p)
@@ -555,8 +574,11 @@ __global__ void __launch_bounds__(kProgThreads, 1) program_kernel(const ProgArgs
               }
               const int row = rt * 16 + lane;
               if (lane < 16 && row < op.rows) {
-                if (it.S == 1)
-                  op.y[row] = (op.res ? __ldcg(op.res + row) : 0.f) + v;
+                if (it.S == 1) {
+                  float r = 0.f;
+                  if (op.res) r = rt - it.rt_a < kProgRowsAcc ? res_s[(rt - it.rt_a) * 16 + lane] : __ldcg(op.res + row);
+                  op.y[row] = r + v;
+                }
                 else
                   op.partial[(static_cast<size_t>(rt) * it.S + it.s) * 16 + lane] = v;
               }
@@ -597,6 +619,7 @@ __global__ void __launch_bounds__(kProgThreads, 1) program_kernel(const ProgArgs
         __syncwarp();
         if (lane == 0) atomicAdd(a.done + j, 1u);
       }
+      if (a.trace && c == 0 && lane == 0 && j < kTraceN) a.trace[7 * kTraceN + j] = clock64();
     }
     // the last CTA out resets the op counters for the next launch
     if (lane == 0) {
@@ -628,11 +651,13 @@ __global__ void __launch_bounds__(kProgThreads, 1) program_kernel(const ProgArgs
       if (lane == 0) mbar_arrive(dempty + ds);
       continue;
     }
+    if (a.trace && c == 0 && tid == 0 && j < kTraceN) a.trace[4 * kTraceN + j] = clock64();
     if (op.wait >= 0) {
       if (tid == 0) {
         const uint64_t t0 = globaltimer();
         while (ld_acquire(a.done + op.wait) < static_cast<uint32_t>(G)) trap_after(t0, a.err);
         __threadfence();
+        if (a.trace && c == 0 && j < kTraceN) a.trace[5 * kTraceN + j] = clock64();
       }
       staged_x = nullptr;  // the other threads pass the restaging barrier after thread 0
     }
@@ -645,6 +670,7 @@ __global__ void __launch_bounds__(kProgThreads, 1) program_kernel(const ProgArgs
           consumer_bar(nthr);  // every warp is done with the previous fragments
           stage_x(op, k0, k1, sB, red_ss, tid, nthr);
           consumer_bar(nthr);
+          if (a.trace && c == 0 && tid == 0 && j < kTraceN) a.trace[6 * kTraceN + j] = clock64();
           staged_x = op.x;
           staged_xf = op.xform;
           staged_k0 = k0;
@@ -909,7 +935,7 @@ egt_status egt_program_create(const egt_program_op* ops, uint32_t n_ops, void* s
   prog->stage_bytes = prog->CH * max_blk;
   const int bars = (16 * 64 + 16 * kProgRed + 16 * kProgDesc + 127) / 128 * 128;  // room for up to 64 stages
   const int fixed = bars + kProgDesc * static_cast<int>(sizeof(ProgOp) + sizeof(ProgItem)) +
-                    (kProgRed * kProgNW * 16 + 32 + kProgRowsAcc * 16) * 4 + prog->sB_bytes;
+                    (kProgRed * kProgNW * 16 + 32 + 2 * kProgRowsAcc * 16) * 4 + prog->sB_bytes;
   int nst = std::min(64, (smem_optin - fixed) / prog->stage_bytes);
   if (const char* e = getenv("EGT_PROGRAM_NST")) nst = std::min(nst, atoi(e));
   if (nst < 2) {
@@ -958,8 +984,8 @@ egt_status egt_program_create(const egt_program_op* ops, uint32_t n_ops, void* s
     return pfail(EGT_ECUDA, std::string("program: setup failed: ") + cudaGetErrorString(e));
   }
   if (getenv("EGT_PROGRAM_TRACE")) {
-    cudaMalloc(&prog->trace, sizeof(long long) * 4 * egt_impl::kTraceN);
-    cudaMemset(prog->trace, 0, sizeof(long long) * 4 * egt_impl::kTraceN);
+    cudaMalloc(&prog->trace, sizeof(long long) * 8 * egt_impl::kTraceN);
+    cudaMemset(prog->trace, 0, sizeof(long long) * 8 * egt_impl::kTraceN);
   }
   *out = prog;
   return EGT_OK;
@@ -967,7 +993,7 @@ egt_status egt_program_create(const egt_program_op* ops, uint32_t n_ops, void* s
 
 egt_status egt_program_debug_trace(const egt_program* prog, long long* host, size_t n) {
   if (!prog || !prog->trace) return pfail(EGT_EINVAL, "program: tracing is off (EGT_PROGRAM_TRACE)");
-  n = std::min<size_t>(n, 4 * egt_impl::kTraceN);
+  n = std::min<size_t>(n, 8 * egt_impl::kTraceN);
   if (cudaMemcpy(host, prog->trace, n * sizeof(long long), cudaMemcpyDeviceToHost) != cudaSuccess)
     return pfail(EGT_ECUDA, "program: trace copy failed");
   return EGT_OK;
