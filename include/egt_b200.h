@@ -148,8 +148,22 @@ EGT_API egt_status egt_spmv(const egt_dev_packed* h, const float* x_dev, float* 
  * overlap that kernel entirely (it still completes after it).  Typical use:
  * the Q, K, V (or gate/up) products of one decode step. */
 #define EGT_SPMV_INDEPENDENT 1u
+/* Input transforms of fused products (egt_spmv_fused, programs). */
+#define EGT_INPUT_NONE 0u
+#define EGT_INPUT_RMSNORM 1u /* x / sqrt(mean(x^2) + eps) over the whole vector */
+#define EGT_INPUT_SILU 2u    /* x / (1 + exp(-x)) */
 EGT_API egt_status egt_spmv_ex(const egt_dev_packed* h, const float* x_dev, float* y_dev, uint32_t M,
                                uint32_t ldx, uint32_t ldy, uint32_t flags, void* stream);
+
+/* egt_spmv_ex with the forward_impl glue fused (model.cpp:155-190):
+ * Y = residual + f(X) * W^T, f = EGT_INPUT_NONE / RMSNORM (per token, eps) /
+ * SILU (the EGT_INPUT_* constants below).  residual may be NULL or equal y
+ * (row stride ldr).  Tiled path only (else EGT_EINVAL).  With
+ * EGT_SPMV_INDEPENDENT neither x nor residual may be written by the
+ * immediately preceding kernel on the stream. */
+EGT_API egt_status egt_spmv_fused(const egt_dev_packed* h, const float* x_dev, float* y_dev, uint32_t M,
+                                  uint32_t ldx, uint32_t ldy, const float* residual_dev, uint32_t ldr,
+                                  uint32_t input, float eps, uint32_t flags, void* stream);
 
 /* Same as egt_spmv with host buffers: H2D of x, the product, D2H of y, and a
  * stream synchronize.  x_len must equal cols (else EGT_EINVAL with the
@@ -266,6 +280,29 @@ EGT_API egt_status egt_decode(const egt_model* m, const egt_trie_view* trie, con
 
 EGT_API egt_status egt_model_query(const egt_model* m, egt_model_config* cfg);
 
+/* ---------------- KV-cached batch-1 decode loop ---------------------------
+ * The reference's decode recomputes the whole prefix each step
+ * (decode.cpp:122-190 -> forward, model.cpp:118-202); the decoder runs one
+ * token per step against a KV cache -- the same attention arithmetic
+ * (model.cpp:161-184) with every linear layer an M = 1 SparseGemv and the
+ * rmsnorm / silu / residual glue fused into the products.  Position and
+ * token live in device memory, so a step is one CUDA graph replay with no
+ * host round trip.  Greedy (argmax, ties -> lowest id) after the prompt.
+ * Every layer and the head must be on the tiled path; head dim 16/32/64/128. */
+typedef struct egt_decoder egt_decoder;
+EGT_API egt_status egt_decoder_create(const egt_model* m, uint32_t max_len, egt_decoder** out);
+/* Resets the position to 0 with the prompt's first token; the next
+ * prompt_len - 1 steps consume the rest of the prompt. */
+EGT_API egt_status egt_decoder_start(egt_decoder* d, const int32_t* prompt, uint32_t prompt_len, void* stream);
+/* n_steps graph replays, stream-ordered after `stream` (asynchronous). */
+EGT_API egt_status egt_decoder_step(egt_decoder* d, uint32_t n_steps, void* stream);
+/* Synchronous read-back: the position t reached (positions [0, t) have been
+ * run), tokens_host[0..t] (t = the pending next token; at most n entries),
+ * and (optionally) the last step's logits into logits_dev [vocab]. */
+EGT_API egt_status egt_decoder_read(const egt_decoder* d, int32_t* tokens_host, uint32_t n, uint32_t* position,
+                                    float* logits_dev, void* stream);
+EGT_API egt_status egt_decoder_destroy(egt_decoder* d);
+
 /* ---------------- persistent GEMV programs (decode chains) ----------------
  * A program is an ordered list of batch-1 products y = residual + W f(x)
  * executed by ONE persistent launch (one CTA per SM): every CTA streams its
@@ -281,9 +318,6 @@ EGT_API egt_status egt_model_query(const egt_model* m, egt_model_config* cfg);
  * write-after-write overlap with an earlier op that `wait` does not cover.
  * Pointers are bound at create; run is stream-ordered and graph-capturable.
  * Only tiled-path matrices (group sizes multiple of 32) are accepted. */
-#define EGT_INPUT_NONE 0u
-#define EGT_INPUT_RMSNORM 1u /* x / sqrt(mean(x^2) + eps) over the whole vector */
-#define EGT_INPUT_SILU 2u    /* x / (1 + exp(-x)) */
 typedef struct egt_program_op {
   const egt_dev_packed* w;
   const float* x;        /* cols floats, 16-byte aligned */

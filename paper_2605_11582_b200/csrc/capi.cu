@@ -425,25 +425,42 @@ egt_status egt_dev_packed_query(const egt_dev_packed* h, egt_dev_packed_info* in
   return EGT_OK;
 }
 
-egt_status egt_spmv_ex(const egt_dev_packed* h, const float* x, float* y, uint32_t M, uint32_t ldx,
-                       uint32_t ldy, uint32_t flags, void* stream) {
+namespace {
+egt_status spmv_impl(const egt_dev_packed* h, const float* x, float* y, uint32_t M, uint32_t ldx, uint32_t ldy,
+                     uint32_t flags, const float* res, uint32_t ldr, uint32_t input, float eps, void* stream) {
   const bool indep = (flags & EGT_SPMV_INDEPENDENT) != 0;
   if (!h) return fail(EGT_EINVAL, "spmv: null matrix");
   if (M == 0) return EGT_OK;
   if (ldx < h->cols) return fail(EGT_EINVAL, "spmv: input length differs from columns");
   if (M > 1 && ldy < h->rows) return fail(EGT_EINVAL, "spmv: output stride below rows");
+  if (input > EGT_INPUT_SILU) return fail(EGT_EINVAL, "spmv: unknown input transform");
+  if (res && M > 1 && ldr < h->rows) return fail(EGT_EINVAL, "spmv: residual stride below rows");
   if (h->rows == 0) return EGT_OK;
   if (!x || !y) return fail(EGT_EINVAL, "spmv: null vector");
+  if (input == EGT_INPUT_RMSNORM && (ldx % 4 != 0 || h->cols % 4 != 0 || reinterpret_cast<uintptr_t>(x) % 16 != 0))
+    return fail(EGT_EINVAL, "spmv: rmsnorm input needs 16-byte aligned rows of a multiple of 4 floats");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   LaunchCtx ctx;
   ctx.stream = s;
   ctx.pdl = g_pdl;
+  ctx.xform = static_cast<int>(input);
+  ctx.eps = eps;
+  ctx.res = res;
+  ctx.ldr = static_cast<int>(M > 1 ? ldr : h->rows);
   if (h->cols == 0) {
-    for (uint32_t m = 0; m < M; ++m)
-      CUDA_TRY(cudaMemsetAsync(y + static_cast<size_t>(m) * ldy, 0, h->rows * sizeof(float), s));
+    for (uint32_t m = 0; m < M; ++m) {
+      float* ym = y + static_cast<size_t>(m) * ldy;
+      if (res)
+        CUDA_TRY(cudaMemcpyAsync(ym, res + static_cast<size_t>(m) * ctx.ldr, h->rows * sizeof(float),
+                                 cudaMemcpyDeviceToDevice, s));
+      else
+        CUDA_TRY(cudaMemsetAsync(ym, 0, h->rows * sizeof(float), s));
+    }
     return EGT_OK;
   }
   if (h->path == EGT_PATH_GENERAL) {
+    if (res || input != EGT_INPUT_NONE)
+      return fail(EGT_EINVAL, "spmv: fused input transforms / residual need the tiled path (group sizes % 32 == 0)");
     CUDA_TRY(launch_general(h, x, static_cast<int>(ldx), static_cast<int>(M), y,
                             static_cast<int>(ldy), ctx));
     return EGT_OK;
@@ -478,6 +495,18 @@ egt_status egt_spmv_ex(const egt_dev_packed* h, const float* x, float* y, uint32
   CUDA_TRY(launch_tiled(h, sc, x, static_cast<int>(ldx), static_cast<int>(M), y,
                         static_cast<int>(ldy), ctx, indep));
   return EGT_OK;
+}
+}  // namespace
+
+egt_status egt_spmv_ex(const egt_dev_packed* h, const float* x, float* y, uint32_t M, uint32_t ldx,
+                       uint32_t ldy, uint32_t flags, void* stream) {
+  return spmv_impl(h, x, y, M, ldx, ldy, flags, nullptr, 0, EGT_INPUT_NONE, 0.f, stream);
+}
+
+egt_status egt_spmv_fused(const egt_dev_packed* h, const float* x, float* y, uint32_t M, uint32_t ldx,
+                          uint32_t ldy, const float* residual, uint32_t ldr, uint32_t input, float eps,
+                          uint32_t flags, void* stream) {
+  return spmv_impl(h, x, y, M, ldx, ldy, flags, residual, ldr, input, eps, stream);
 }
 
 egt_status egt_spmv(const egt_dev_packed* h, const float* x, float* y, uint32_t M, uint32_t ldx,

@@ -85,6 +85,10 @@ struct LaunchCtx {
   bool pdl = true;
   float* partial = nullptr;      // split-K partial sums
   uint32_t* counters = nullptr;  // split-K arrival counters (self-resetting)
+  int xform = 0;                 // EGT_INPUT_* applied to x while staging
+  float eps = 1e-6f;
+  const float* res = nullptr;    // y = res + product (may alias y)
+  int ldr = 0;
 };
 
 TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms, bool indep);

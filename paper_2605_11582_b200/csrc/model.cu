@@ -17,19 +17,11 @@
 #include "device_common.cuh"
 #include "egt_b200.h"
 #include "handle.h"
+#include "model.h"
 
 namespace egt_impl {
 void set_last_error(const std::string& msg);
 }
-
-struct egt_model {
-  egt_model_config cfg{};
-  float* emb = nullptr;  // [vocab x d]
-  float* pos = nullptr;  // [max_positions x d] sinusoidal table
-  std::vector<const egt_dev_packed*> layers;  // n_layers * 6: wq wk wv wo ff1 ff2
-  const egt_dev_packed* head = nullptr;
-  int device = 0;
-};
 
 namespace {
 

@@ -19,6 +19,7 @@
 #include "device_common.cuh"
 #include "handle.h"
 #include "tiled_compute.cuh"
+#include "egt_b200.h"
 
 #include <algorithm>
 #include <cmath>
@@ -43,6 +44,12 @@ struct TiledArgs {
   int RB, WK, KC, S, NST, CH;
   int dbg;    // tuning experiments: 1 = empty kernel, 2 = weight stream only
   int indep;  // x is not produced by the previous kernel in the stream
+  // fused forward_impl glue (model.cpp:155-190): input transform of x
+  // (EGT_INPUT_RMSNORM per token, EGT_INPUT_SILU) and y = res + product
+  int xform;
+  float eps;
+  const float* res;
+  int ldr;
 };
 
 
@@ -62,7 +69,13 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
   constexpr int TOK = 4 * NT;
   constexpr int VB = val_lane_bytes(FMT), MB = meta_lane_bytes(FMT);
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  pdl_launch_dependents();
+  // Programmatic dependent launch.  An independent product lets the next
+  // kernel launch at once; a dependent one only after its own inputs are
+  // complete (below), so that whenever any product starts, every kernel
+  // before its immediate predecessor has finished -- which is what makes
+  // EGT_SPMV_INDEPENDENT (inputs not written by the immediate predecessor)
+  // safe in a chain of PDL launches.
+  if (a.indep) pdl_launch_dependents();
   if (a.dbg == 1) {
     pdl_wait();
     return;
@@ -130,18 +143,45 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
   // x and the split-K workspace belong to earlier kernels.  An independent
   // product (x not written by the previous kernel) skips the wait here and
   // waits before exiting instead, so stream order stays transitive.
-  if (!a.indep) pdl_wait();
+  if (!a.indep) {
+    pdl_wait();
+    pdl_launch_dependents();
+  }
 
   // x slice -> fp16 hi/lo B fragments sB[nt][kt][lane < LS][4]: token m's hi
   // part is B column 2m (lanes 8m..8m+3), its rounding residual column 2m+1.
   // Every load of a thread is issued before the first conversion (one L2
   // round trip for up to XU items per thread), then converted and stored.
   constexpr int XU = 24;
+  // rmsnorm (model.cpp:57-67): inv_m = 1 / sqrt(mean(x_m^2) + eps) over the
+  // whole row of every token of this CTA, applied while converting
+  __shared__ float s_inv[16];
+  __shared__ float s_red[32];
+  if (a.xform == EGT_INPUT_RMSNORM) {
+    for (int m = 0; m < Mc; ++m) {
+      const float4* xr4 = reinterpret_cast<const float4*>(a.x + static_cast<size_t>(m0 + m) * a.ldx);
+      float ss = 0.f;
+      for (int i = tid; i < (a.cols >> 2); i += blockDim.x) {
+        const float4 w = __ldg(xr4 + i);
+        ss = fmaf(w.x, w.x, fmaf(w.y, w.y, fmaf(w.z, w.z, fmaf(w.w, w.w, ss))));
+      }
+      ss = warp_sum(ss);
+      if (lane == 0) s_red[warp] = ss;
+      __syncthreads();
+      if (tid == 0) {
+        float tot = 0.f;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) tot += s_red[w];
+        s_inv[m] = 1.0f / sqrtf(tot / static_cast<float>(a.cols) + a.eps);
+      }
+      __syncthreads();
+    }
+  }
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) {
     const int mc = a.dbg == 3 ? 0 : min(4, Mc - 4 * nt);
     for (int m = 0; m < mc; ++m) {
       const float* xr = a.x + static_cast<size_t>(m0 + 4 * nt + m) * a.ldx;
+      const float inv = a.xform == EGT_INPUT_RMSNORM ? s_inv[4 * nt + m] : 1.f;
       const int items = KTc * 16;
       for (int i0 = 0; i0 < items; i0 += XU * static_cast<int>(blockDim.x)) {
         float2 v[XU];
@@ -159,6 +199,13 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
           const int i = i0 + tid + u * blockDim.x;
           if (i < items) {
             const int reg = i & 3, t = (i >> 2) & 3, kt = i >> 4;
+            if (a.xform == EGT_INPUT_RMSNORM) {
+              v[u].x *= inv;
+              v[u].y *= inv;
+            } else if (a.xform == EGT_INPUT_SILU) {  // model.cpp:80-84
+              v[u].x = v[u].x * (1.0f / (1.0f + expf(-v[u].x)));
+              v[u].y = v[u].y * (1.0f / (1.0f + expf(-v[u].y)));
+            }
             const __half h0 = __float2half_rn(v[u].x), h1 = __float2half_rn(v[u].y);
             const __half l0 = __float2half_rn(v[u].x - __half2float(h0));
             const __half l1 = __float2half_rn(v[u].y - __half2float(h1));
@@ -242,7 +289,7 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
     const int tok = m0 + tl;
     if (row < a.rows) {
       if (a.S == 1)
-        a.y[static_cast<size_t>(tok) * a.ldy + row] = v;
+        a.y[static_cast<size_t>(tok) * a.ldy + row] = (a.res ? a.res[static_cast<size_t>(tok) * a.ldr + row] : 0.f) + v;
       else
         a.partial[(static_cast<size_t>(blockIdx.y) * a.M + tok) * rows_pad + row] = v;
     }
@@ -268,7 +315,7 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
       float v = 0.f;
       for (int sidx = 0; sidx < a.S; ++sidx)
         v += __ldcg(a.partial + (static_cast<size_t>(sidx) * a.M + tok) * rows_pad + row);
-      a.y[static_cast<size_t>(tok) * a.ldy + row] = v;
+      a.y[static_cast<size_t>(tok) * a.ldy + row] = (a.res ? a.res[static_cast<size_t>(tok) * a.ldr + row] : 0.f) + v;
     }
   }
   if (tid == 0) a.counters[cidx] = 0u;  // ready for the next launch / graph replay
@@ -441,6 +488,10 @@ size_t tiled_workspace_floats(const egt_dev_packed* h, const TiledSchedule& sc, 
 cudaError_t launch_tiled(const egt_dev_packed* h, const TiledSchedule& sc, const float* x, int ldx,
                          int M, float* y, int ldy, const LaunchCtx& ctx, bool indep) {
   TiledArgs a;
+  a.xform = ctx.xform;
+  a.eps = ctx.eps;
+  a.res = ctx.res;
+  a.ldr = ctx.ldr;
   a.vals = h->tiled.vals;
   a.meta = h->tiled.meta;
   a.scales = h->tiled.scales;

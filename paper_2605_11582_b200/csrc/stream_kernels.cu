@@ -274,8 +274,8 @@ struct GeneralArgs {
 };
 
 __global__ void __launch_bounds__(256) general_spmm_kernel(const GeneralArgs a) {
+  pdl_wait();  // general path: always dependent; launch the next kernel once the inputs are complete
   pdl_launch_dependents();
-  pdl_wait();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t r = blockIdx.x * 8 + warp;
   if (r >= a.rows) return;

@@ -142,6 +142,50 @@ class DeviceModel:
                                             "trigger_step": stats[2], "flattened_nodes": stats[3]}
 
 
+class Decoder:
+    """KV-cached batch-1 greedy decode loop on the device (egt_decoder_*):
+    one CUDA graph replay per token, position and token device-resident."""
+
+    def __init__(self, model: DeviceModel, max_len: int):
+        self.model = model
+        self.max_len = max_len
+        h = C.c_void_p()
+        check(_lib().egt_decoder_create(model._h, max_len, C.byref(h)))
+        self._h = h
+
+    def start(self, prompt, stream=None) -> None:
+        pr = np.ascontiguousarray(prompt, np.int32)
+        check(_lib().egt_decoder_start(self._h, pr.ctypes.data_as(C.POINTER(C.c_int32)), pr.size,
+                                       _stream_ptr(stream)))
+
+    def step(self, n: int = 1, stream=None) -> None:
+        """n tokens (asynchronous, stream-ordered)."""
+        check(_lib().egt_decoder_step(self._h, n, _stream_ptr(stream)))
+
+    def read(self, logits=None, stream=None):
+        """(tokens at positions [0, position], position); logits: optional
+        torch CUDA tensor [vocab] receiving the last step's logits."""
+        toks = np.zeros(self.max_len, np.int32)
+        pos = C.c_uint32()
+        check(_lib().egt_decoder_read(self._h, toks.ctypes.data_as(C.POINTER(C.c_int32)), self.max_len,
+                                      C.byref(pos), C.c_void_p(logits.data_ptr()) if logits is not None else None,
+                                      _stream_ptr(stream)))
+        return toks[: min(pos.value + 1, self.max_len)], pos.value
+
+    def generate(self, prompt, n_new: int, stream=None):
+        """Greedy continuation: prompt + n_new tokens (host list)."""
+        self.start(prompt, stream)
+        self.step(len(prompt) - 1 + n_new, stream)
+        toks, pos = self.read(stream=stream)
+        return toks.tolist()
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and N is not None and N._lib is not None:
+            N._lib.egt_decoder_destroy(h)
+            self._h = C.c_void_p()
+
+
 def compress_layer(w: np.ndarray, kind: str, group: int):
     """One mixed-dispatch layer from dense weights: kind in {int4-2:4, int4-1:4,
     int4-dense, fp16-2:4, fp16-1:4}.  Masks keep the largest |w| per group of

@@ -115,6 +115,8 @@ SIGNATURES = {
     "egt_spmv": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_void_p]),
     "egt_spmv_ex": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
                               C.c_void_p]),
+    "egt_spmv_fused": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_uint32,
+                                 C.c_void_p, C.c_uint32, C.c_uint32, C.c_float, C.c_uint32, C.c_void_p]),
     "egt_spmv_host": (C.c_int, [C.c_void_p, f32p, C.c_size_t, f32p, C.c_void_p]),
     "egt_dequant": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "egt_set_pdl": (None, [C.c_int]),
@@ -151,6 +153,14 @@ _PROGRAM_SIGNATURES = {
     "egt_program_destroy": (C.c_int, [C.c_void_p]),
     "egt_program_debug_trace": (C.c_int, [C.c_void_p, C.POINTER(C.c_longlong), C.c_size_t]),
 }
+
+_MODEL_SIGNATURES.update({
+    "egt_decoder_create": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(C.c_void_p)]),
+    "egt_decoder_start": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_uint32, C.c_void_p]),
+    "egt_decoder_step": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p]),
+    "egt_decoder_read": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_uint32, u32p, C.c_void_p, C.c_void_p]),
+    "egt_decoder_destroy": (C.c_int, [C.c_void_p]),
+})
 
 SIGNATURES.update(_MODEL_SIGNATURES)
 SIGNATURES.update(_PROGRAM_SIGNATURES)

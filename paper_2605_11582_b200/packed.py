@@ -232,6 +232,22 @@ class DeviceMatrix:
         check(lib().egt_spmv_ex(self._h, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), M, ldx, ldy,
                                 1 if independent else 0, _stream_ptr(stream)))
 
+    def spmv_fused_into(self, x, y, residual=None, input: int = 0, eps: float = 1e-6, stream=None,
+                        independent: bool = False) -> None:
+        """y = residual + f(x) @ W^T with f = identity / rmsnorm (per token) /
+        silu (N.INPUT_*): the forward_impl glue (model.cpp:155-190) fused into
+        the product.  residual may be y itself."""
+        M, ldx = (1, x.shape[0]) if x.dim() == 1 else (x.shape[0], x.stride(0))
+        ldy = y.shape[-1] if y.dim() == 1 else y.stride(0)
+        if x.dim() == 1 and x.shape[0] != self.cols:
+            raise N.InvalidArgument(N.EGT_EINVAL, "spmv: input length differs from columns")
+        rp, ldr = None, 0
+        if residual is not None:
+            rp = residual.data_ptr()
+            ldr = residual.shape[-1] if residual.dim() == 1 else residual.stride(0)
+        check(lib().egt_spmv_fused(self._h, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), M, ldx, ldy,
+                                   rp, ldr, input, eps, 1 if independent else 0, _stream_ptr(stream)))
+
     def spmv(self, x, stream=None):
         """Device product; returns a new tensor [M x rows] (or [rows] for 1-D x)."""
         import torch

@@ -204,3 +204,27 @@ def test_hazards_rejected(egt, port, torch):
     with pytest.raises(InvalidArgument, match="input length"):
         Program([Op(d, torch.zeros(128, device="cuda"), b)])
     Program([Op(d, a, b), Op(d, b, c, wait=0)])      # ordered: accepted
+
+
+@pytest.mark.parametrize("M", [1, 5])
+@pytest.mark.parametrize("shape", [(1024, 2048), (256, 11008)])
+def test_spmv_fused_transforms(egt, port, torch, M, shape):
+    """egt_spmv_fused: rmsnorm / silu input transforms and the residual epilogue
+    (in place) of the per-launch kernel equal the oracle's composition."""
+    from paper_2605_11582_b200.native import INPUT_NONE, INPUT_RMSNORM, INPUT_SILU
+
+    rng = np.random.default_rng(41 + M)
+    rows, cols = shape
+    p = make_int4(rng, rows, cols, 2, 64, port)[0]
+    d = _dev(egt, p)
+    xs = rng.uniform(-2, 2, (M, cols)).astype(np.float32)
+    rs = rng.uniform(-1, 1, (M, rows)).astype(np.float32)
+    for mode, f in ((INPUT_NONE, lambda v: v), (INPUT_RMSNORM, rmsnorm32), (INPUT_SILU, silu32)):
+        x = _cuda(torch, xs)
+        y = _cuda(torch, rs)  # residual in place
+        d.spmv_fused_into(x if M > 1 else x[0], y if M > 1 else y[0], residual=y if M > 1 else y[0], input=mode)
+        got = y.cpu().numpy()
+        for m in range(M):
+            want = rs[m] + port.spmv(p, f(xs[m]))
+            ok, err = close(got[m], want)
+            assert ok, f"mode {mode} token {m}: {err:.3e}"
