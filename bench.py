@@ -198,53 +198,205 @@ SHARDED_SHAPES = [(5120, 13824), (8192, 28672)]
 
 
 def measure_sharded(world, rank, stream, torch, egt, rng):
+    """BASELINE configs[4]: 13B/70B-shaped layers row-sharded across the ranks
+    (zero-copy 16-row shards, parallel.RowShardPlan).  gemv_us: the local
+    SparseGemv per call, CUDA graph over enough distinct weight copies that
+    every call streams from HBM; allgather_us: the NCCL all-gather of the y
+    slices (world > 1); gathered output checked against the unsharded product."""
     from paper_2605_11582_b200.parallel import RowShardPlan, gather_rows
 
     out = {}
+    l2 = 126 * 2**20
     for rows, cols in SHARDED_SHAPES:
         p = host_layer(np.random.default_rng(rows), rows, cols)  # identical on every rank
-        full = egt.DeviceMatrix.from_packed(p, stream)
         plan = RowShardPlan.make(rows, world)
         r0, r1 = plan.local(rank)
-        local = full.slice_rows(r0, r1)
-        x = torch.from_numpy(np.random.default_rng(cols).uniform(-1, 1, cols).astype(np.float32)).cuda()
-        reps = 50
-
-        def run(with_gather):
-            with torch.cuda.stream(stream):
-                y = local.spmv(x, stream)
-                if with_gather and world > 1:
-                    y = gather_rows(y, plan)
-            return y
-
-        for _ in range(5):
-            run(True)
-        torch.cuda.synchronize()
-        res = {}
-        for name, g in (("gemv_only", False), ("gemv_allgather", True)):
-            if world > 1:
-                torch.distributed.barrier()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            with torch.cuda.stream(stream):
-                e0.record(stream)
-                for _ in range(reps):
-                    run(g)
-                e1.record(stream)
-            e1.synchronize()
-            t = torch.tensor([e0.elapsed_time(e1) * 1e3 / reps], device="cuda")
-            if world > 1:
-                torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            res[name + "_us"] = round(float(t.item()), 3)
-        if world > 1:  # parity of the gathered output against this rank's full product
-            yf = full.spmv(x).cpu().numpy()
-            yg = run(True).cpu().numpy()
-            res["gathered_equals_unsharded_max_rel_err"] = float(np.max(np.abs(yg - yf) / (1 + np.abs(yf))))
         b = shape_bytes(p)
-        res.update({"bytes_total": b, "rows_per_gpu": r1 - r0,
-                    "GBps_per_gpu_gemv": round((b / world) / res["gemv_only_us"] / 1e3, 1)})
+        local_bytes = b * (r1 - r0) // rows
+        copies = max(2, -(-2 * l2 // max(local_bytes, 1)))
+        fulls = [egt.DeviceMatrix.from_packed(p, stream) for _ in range(copies)]
+        shards = [f.slice_rows(r0, r1) for f in fulls]
+        x = torch.from_numpy(np.random.default_rng(cols).uniform(-1, 1, cols).astype(np.float32)).cuda()
+        ys = [torch.empty(r1 - r0, device="cuda") for _ in range(copies)]
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(stream):
+            for d, y in zip(shards, ys):  # warm-up outside the capture
+                d.spmv_into(x, y, stream, independent=True)
+            stream.synchronize()
+            with torch.cuda.graph(g, stream=stream):
+                for d, y in zip(shards, ys):
+                    d.spmv_into(x, y, stream, independent=True)
+        reps = max(5, 2000 // copies)
+        for _ in range(3):
+            g.replay()
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+            for _ in range(reps // 10 + 1):
+                g.replay()
+            e1.record(stream)
+        e1.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) * 1e3 / ((reps // 10 + 1) * copies)], device="cuda")
+        if world > 1:
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        res = {"gemv_us": round(float(t.item()), 3), "rows_per_gpu": r1 - r0, "bytes_total": b,
+               "bytes_per_gpu": local_bytes, "copies": copies,
+               "GBps_per_gpu": round(local_bytes / float(t.item()) / 1e3, 1),
+               "GBps_all_gpus": round(world * local_bytes / float(t.item()) / 1e3, 1)}
+        if world > 1:
+            y = ys[0]
+            for _ in range(5):
+                gather_rows(y, plan)
+            torch.cuda.synchronize()
+            torch.distributed.barrier()
+            pad = torch.zeros(plan.max_rows, device="cuda")
+            buf = torch.empty(world * plan.max_rows, device="cuda")
+            e0.record()
+            n_g = 50
+            for _ in range(n_g):
+                torch.distributed.all_gather_into_tensor(buf, pad)
+            e1.record()
+            e1.synchronize()
+            tg = torch.tensor([e0.elapsed_time(e1) * 1e3 / n_g], device="cuda")
+            torch.distributed.all_reduce(tg, op=torch.distributed.ReduceOp.MAX)
+            res["allgather_us"] = round(float(tg.item()), 3)
+            yf = fulls[0].spmv(x).cpu().numpy()
+            yg = gather_rows(shards[0].spmv(x), plan).cpu().numpy()
+            res["gathered_equals_unsharded_max_rel_err"] = float(np.max(np.abs(yg - yf) / (1 + np.abs(yf))))
         out[f"{rows}x{cols}"] = res
-        del full, local
+        del fulls, shards, g
+        torch.cuda.synchronize()
     return out
+
+
+# ------------------------------------------------------------------ decode (configs[2])
+DECODE_CFG = dict(vocab_size=32000, d_model=4096, n_layers=32, n_heads=32, d_ff=11008, max_positions=4096)
+DECODE_PLANS = {
+    # layer-adaptive mixed dispatch (a14): even layers dense INT4, odd layers sparse FP16 2:4
+    "mixed-int4dense-fp16sp24": lambda l: "int4-dense" if l % 2 == 0 else "fp16-2:4",
+    "int4-2:4": lambda l: "int4-2:4",
+}
+
+
+def decode_host_layers(rng, kinds):
+    """One host artifact per (kind, shape): W ~ U(-1/sqrt(in), 1/sqrt(in)) (init_model scale,
+    model.hpp:61-62), compressed by the product's encoder (compress_layer semantics)."""
+    import paper_2605_11582_b200 as egt
+
+    out = {}
+    pats = np.array([[1, 1, 0, 0], [1, 0, 1, 0], [1, 0, 0, 1], [0, 1, 1, 0], [0, 1, 0, 1], [0, 0, 1, 1]], bool)
+    for kind in kinds:
+        for rows, cols in sorted(set(LAYER_SHAPES)):
+            b = 1.0 / np.sqrt(cols)
+            w = rng.uniform(-b, b, (rows, cols)).astype(np.float32)
+            if kind == "int4-dense":
+                out[(kind, rows, cols)] = egt.quantize_matrix(w, GROUP)
+                continue
+            keep = pats[rng.integers(0, 6, (rows, cols // 4))].reshape(rows, cols)
+            mask = np.packbits(keep.reshape(-1), bitorder="little")
+            if kind == "int4-2:4":
+                out[(kind, rows, cols)] = egt.pack(mask, egt.quantize_matrix(w, GROUP, mask), 2)
+            else:
+                out[(kind, rows, cols)] = egt.pack_f32(mask, w.astype(np.float16).astype(np.float32), 2)
+    return out
+
+
+def measure_decode(torch, egt, plan_name, n_tokens=64, prompt_len=16, max_len=256):
+    """Greedy batch-1 decode tokens/s on the 7B-shaped stack (KV cache,
+    egt_decoder: one CUDA graph replay per token)."""
+    from paper_2605_11582_b200.model import Decoder, DeviceModel
+
+    rng = np.random.default_rng(7)
+    plan = DECODE_PLANS[plan_name]
+    cfg = DECODE_CFG
+    kinds = sorted({plan(l) for l in range(cfg["n_layers"])})
+    host = decode_host_layers(rng, kinds)
+    t0 = time.time()
+    layers = []
+    for l in range(cfg["n_layers"]):
+        k = plan(l)
+        for rows, cols in LAYER_SHAPES:
+            a = host[(k, rows, cols)]
+            layers.append(egt.DeviceMatrix.dense_i4(a) if k == "int4-dense" else egt.DeviceMatrix.from_packed(a))
+    hb = 1.0 / np.sqrt(cfg["d_model"])
+    hw = rng.uniform(-hb, hb, (cfg["vocab_size"], cfg["d_model"])).astype(np.float32)
+    hkeep = np.zeros((cfg["vocab_size"], cfg["d_model"] // 4, 4), bool)
+    hkeep[:, :, :2] = True
+    hmask = np.packbits(hkeep.reshape(-1), bitorder="little")
+    head = egt.DeviceMatrix.from_packed(egt.pack(hmask, egt.quantize_matrix(hw, GROUP, hmask), 2))
+    emb = rng.uniform(-hb, hb, (cfg["vocab_size"], cfg["d_model"])).astype(np.float32)
+    model = DeviceModel(cfg, emb, layers, head)
+    del emb, hw
+    dec = Decoder(model, max_len)
+    setup = time.time() - t0
+    prompt = rng.integers(0, cfg["vocab_size"], prompt_len).astype(np.int32)
+    s = torch.cuda.current_stream()
+    dec.start(prompt)
+    dec.step(prompt_len - 1 + 4)  # prefill through the prompt + warm-up tokens
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(s)
+    dec.step(n_tokens)
+    e1.record(s)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1)
+    toks, pos = dec.read()
+    weight_bytes = sum(int(d.algorithmic_bytes) for d in layers) + int(head.algorithmic_bytes)
+    per_tok = ms / n_tokens
+    # e2e through the public API: host prompt in, host tokens out, every step
+    w0 = time.perf_counter()
+    toks2 = dec.generate(prompt, n_tokens)
+    e2e_s = time.perf_counter() - w0
+    # BASELINE configs[3]: one multi-token pass over a prefix-tree (verify_parallel's
+    # forward, decode.cpp:336-421 -> model.cpp:118-202): M tree nodes after a
+    # committed prefix, each row sees the prefix + its ancestors + itself
+    verify = {}
+    for n_nodes in (64, 256):
+        parent = np.array([-1] + [int(rng.integers(0, i)) for i in range(1, n_nodes)])
+        depth = np.zeros(n_nodes, np.int32)
+        for i in range(1, n_nodes):
+            depth[i] = depth[parent[i]] + 1
+        M = prompt_len + n_nodes
+        vis = np.zeros((M, M), bool)
+        vis[:prompt_len, :prompt_len] = np.tril(np.ones((prompt_len, prompt_len), bool))
+        for i in range(n_nodes):
+            r = prompt_len + i
+            vis[r, :prompt_len] = True
+            a = i
+            while a >= 0:
+                vis[r, prompt_len + a] = True
+                a = parent[a]
+        tokens = np.concatenate([prompt, rng.integers(0, cfg["vocab_size"], n_nodes)]).astype(np.int32)
+        positions = np.concatenate([np.arange(prompt_len), prompt_len + depth]).astype(np.int32)
+        for _ in range(2):
+            model.forward(tokens, positions, vis)
+        torch.cuda.synchronize()
+        reps = 5
+        e0.record(s)
+        for _ in range(reps):
+            model.forward(tokens, positions, vis)
+        e1.record(s)
+        e1.synchronize()
+        vms = e0.elapsed_time(e1) / reps
+        verify[f"{n_nodes}_nodes"] = {"rows": M, "ms_per_pass": round(vms, 3),
+                                      "tree_nodes_per_s": round(n_nodes / (vms * 1e-3), 1),
+                                      "vs_sequential_decode": round(n_nodes * per_tok / vms, 2)}
+    res = {"plan": plan_name, "tokens_per_s": round(n_tokens / (ms * 1e-3), 1), "ms_per_token": round(per_tok, 4),
+           "weight_bytes_per_token": weight_bytes,
+           "weight_GBps": round(weight_bytes / (per_tok * 1e-3) / 1e9, 1),
+           "context": f"prompt {prompt_len} + {n_tokens} tokens timed after 4 warm-up tokens (positions "
+                      f"{prompt_len + 3}..{pos - 1})",
+           "e2e_tokens_per_s": round((prompt_len - 1 + n_tokens) / e2e_s, 1),
+           "e2e_note": "generate(): H2D prompt, prefill + n tokens, D2H tokens, host wall clock",
+           "finite_tokens": bool(all(0 <= t < cfg["vocab_size"] for t in toks2)), "setup_s": round(setup, 1),
+           "verify_pass": verify}
+    del dec, model, layers, head
+    torch.cuda.synchronize()
+    return res
 
 
 # ------------------------------------------------------------------ our arm
@@ -384,6 +536,9 @@ def run_ours(args):
     # BASELINE configs[4]: 13B/70B-shaped layers row-sharded across the ranks,
     # local SparseGemv + NCCL all-gather of the y slices (world 1: unsharded)
     sharded = measure_sharded(world, rank, stream, torch, egt, rng) if not args.no_sharded else None
+    decode = None
+    if not args.no_decode:
+        decode = {name: measure_decode(torch, egt, name) for name in DECODE_PLANS}
 
     # e2e through the public API with pinned host buffers
     x_host = {c: torch.from_numpy(xs[c]).pin_memory() for c in xs}
@@ -447,7 +602,8 @@ def run_ours(args):
                    "dependent_chain": {"ms_per_step": round(dep_ms, 4),
                                        "GBps": round(step_bytes / (dep_ms * 1e-3) / 1e9, 1)},
                    "per_shape": per_shape,
-                   "sharded_13b_70b": sharded},
+                   "sharded_13b_70b": sharded,
+                   "decode_7b": decode},
         "e2e": {"value": round(e2e_value, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_step": round(1e3 * e2e_s / e2e_steps, 4), "steps": e2e_steps},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
@@ -477,6 +633,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-sharded", action="store_true", help="skip the 13B/70B row-sharded layers")
+    ap.add_argument("--no-decode", action="store_true", help="skip the 7B decode tokens/s measurement")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -484,6 +484,7 @@ egt_status spmv_impl(const egt_dev_packed* h, const float* x, float* y, uint32_t
     }
     sc = it->second;
   }
+  if (sc.smem == 0) return fail(EGT_EINTERNAL, "spmv: no feasible launch plan for this shape and token count");
   if (sc.S > 1) {
     Workspace* w = nullptr;
     egt_status st = get_workspace(s, tiled_workspace_floats(h, sc, M),

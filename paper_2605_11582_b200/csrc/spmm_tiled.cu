@@ -380,6 +380,8 @@ void force_plan(int RB, int S, int nw, int NST, int CH) {
 }
 bool plan_forced() { return g_force[4] != 0; }
 
+static thread_local bool g_allow_waves = false;  // fallback: several CTAs per SM
+
 TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms, bool indep) {
   TiledSchedule best;
   const int RT = h->tiled.RT, KQ = h->tiled.KQ, E = h->tiled.E, f = h->format;
@@ -401,7 +403,7 @@ TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms, bool indep
     for (int RB = 1; RB <= 128; ++RB) {
       if (g_force[4] && RB != g_force[0]) continue;
       const long grid = static_cast<long>((RT + RB - 1) / RB) * S * NB;
-      if (grid > num_sms && RB < 128 && !g_force[4]) continue;  // one CTA per SM
+      if (grid > num_sms && RB < 128 && !g_force[4] && !g_allow_waves) continue;  // one CTA per SM
       if (indep && !g_force[4]) {
         // Independent products run several launches side by side on disjoint
         // SMs; measured best (tools/plan_sweep.py --indep) is ~250 KB of
@@ -476,6 +478,11 @@ TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms, bool indep
     g_force[4] = saved;
   } else if (best_cost >= 1e300 && indep) {  // no split-free plan fits: dependent plan
     best = plan_tiled(h, M, num_sms, false);
+  } else if (best_cost >= 1e300 && !g_allow_waves) {
+    // nothing fits in one wave (wide rows x many tokens): allow several waves
+    g_allow_waves = true;
+    best = plan_tiled(h, M, num_sms, indep);
+    g_allow_waves = false;
   }
   return best;
 }

@@ -268,3 +268,12 @@ def test_sharded_spmv_nccl_single_rank(egt, port, torch):
         assert torch.equal(sh(x), d.spmv(x))
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("M", [9, 16, 17, 33, 80])
+def test_multi_token_wide(egt, port, torch, M):
+    """M-row products on a 4096-wide layer (the 7B verify pass): the planner
+    must find a (multi-wave) plan when one wave cannot hold the x fragments."""
+    rng = np.random.default_rng(171 + M)
+    p, _, _ = make_int4(rng, 1040, 4096, 2, 128, port)
+    _check_product(egt, port, torch, p, rng, M=M)
