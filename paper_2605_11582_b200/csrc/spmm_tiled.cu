@@ -395,7 +395,7 @@ TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms, bool indep
   // kernel's (programmatic dependent launch) and prefetch their weights.
   const size_t smem_cap = 100 * 1024;
   double best_cost = 1e300;
-  for (int S = 1; S <= std::min(KQ, 8); ++S) {
+  for (int S = 1; S <= std::min(KQ, g_allow_waves ? 64 : 8); ++S) {
     const int KC = (KQ + S - 1) / S;
     if (S > 1 && (S - 1) * KC >= KQ) continue;
     if (g_force[4] && S != g_force[1]) continue;
