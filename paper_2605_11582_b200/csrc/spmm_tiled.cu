@@ -53,6 +53,12 @@ struct TiledArgs {
 };
 
 
+// silu (model.cpp:80-84) out of line: inlined 24x into the unrolled x
+// staging it bloats the kernel past the instruction cache.
+__device__ __noinline__ float2 silu2(float2 v) {
+  return make_float2(v.x * (1.0f / (1.0f + expf(-v.x))), v.y * (1.0f / (1.0f + expf(-v.y))));
+}
+
 // One CTA = RB row tiles x KC k-quads (one of S K-slices) x 4*NT tokens.
 // Warp specialised: warp nw (the producer) streams chunks of row tiles -- CH
 // k-quads of one row tile, 2-4 contiguous bulk copies -- into an NST-deep
@@ -63,7 +69,7 @@ struct TiledArgs {
 // mma.sp.  Per-warp partial sums are reduced in a fixed order; split-K
 // (S > 1) partial rows are summed by the last-arriving CTA of the row block,
 // in slice order, so results are deterministic.
-template <int FMT, int SS, int NT, bool SINGLE>
+template <int FMT, int SS, int NT, bool SINGLE, bool FUSED>
 __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(const TiledArgs a) {
   constexpr int E = 4 / SS;
   constexpr int TOK = 4 * NT;
@@ -157,7 +163,7 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
   // whole row of every token of this CTA, applied while converting
   __shared__ float s_inv[16];
   __shared__ float s_red[32];
-  if (a.xform == EGT_INPUT_RMSNORM) {
+  if (FUSED && a.xform == EGT_INPUT_RMSNORM) {
     for (int m = 0; m < Mc; ++m) {
       const float4* xr4 = reinterpret_cast<const float4*>(a.x + static_cast<size_t>(m0 + m) * a.ldx);
       float ss = 0.f;
@@ -181,7 +187,7 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
     const int mc = a.dbg == 3 ? 0 : min(4, Mc - 4 * nt);
     for (int m = 0; m < mc; ++m) {
       const float* xr = a.x + static_cast<size_t>(m0 + 4 * nt + m) * a.ldx;
-      const float inv = a.xform == EGT_INPUT_RMSNORM ? s_inv[4 * nt + m] : 1.f;
+      const float inv = FUSED && a.xform == EGT_INPUT_RMSNORM ? s_inv[4 * nt + m] : 1.f;
       const int items = KTc * 16;
       for (int i0 = 0; i0 < items; i0 += XU * static_cast<int>(blockDim.x)) {
         float2 v[XU];
@@ -199,12 +205,11 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
           const int i = i0 + tid + u * blockDim.x;
           if (i < items) {
             const int reg = i & 3, t = (i >> 2) & 3, kt = i >> 4;
-            if (a.xform == EGT_INPUT_RMSNORM) {
+            if (FUSED && a.xform == EGT_INPUT_RMSNORM) {
               v[u].x *= inv;
               v[u].y *= inv;
-            } else if (a.xform == EGT_INPUT_SILU) {  // model.cpp:80-84
-              v[u].x = v[u].x * (1.0f / (1.0f + expf(-v[u].x)));
-              v[u].y = v[u].y * (1.0f / (1.0f + expf(-v[u].y)));
+            } else if (FUSED && a.xform == EGT_INPUT_SILU) {
+              v[u] = silu2(v[u]);
             }
             const __half h0 = __float2half_rn(v[u].x), h1 = __float2half_rn(v[u].y);
             const __half l0 = __float2half_rn(v[u].x - __half2float(h0));
@@ -289,7 +294,7 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
     const int tok = m0 + tl;
     if (row < a.rows) {
       if (a.S == 1)
-        a.y[static_cast<size_t>(tok) * a.ldy + row] = (a.res ? a.res[static_cast<size_t>(tok) * a.ldr + row] : 0.f) + v;
+        a.y[static_cast<size_t>(tok) * a.ldy + row] = (FUSED && a.res ? a.res[static_cast<size_t>(tok) * a.ldr + row] : 0.f) + v;
       else
         a.partial[(static_cast<size_t>(blockIdx.y) * a.M + tok) * rows_pad + row] = v;
     }
@@ -315,7 +320,7 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
       float v = 0.f;
       for (int sidx = 0; sidx < a.S; ++sidx)
         v += __ldcg(a.partial + (static_cast<size_t>(sidx) * a.M + tok) * rows_pad + row);
-      a.y[static_cast<size_t>(tok) * a.ldy + row] = (a.res ? a.res[static_cast<size_t>(tok) * a.ldr + row] : 0.f) + v;
+      a.y[static_cast<size_t>(tok) * a.ldy + row] = (FUSED && a.res ? a.res[static_cast<size_t>(tok) * a.ldr + row] : 0.f) + v;
     }
   }
   if (tid == 0) a.counters[cidx] = 0u;  // ready for the next launch / graph replay
@@ -326,36 +331,39 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
 namespace {
 
 template <int FMT, int SS, int NT, bool SINGLE = false>
-void* kernel_ptr() {
-  return reinterpret_cast<void*>(&tiled_spmm_kernel<FMT, SS, NT, SINGLE>);
+void* kernel_ptr(bool fused) {
+  return fused ? reinterpret_cast<void*>(&tiled_spmm_kernel<FMT, SS, NT, SINGLE, true>)
+               : reinterpret_cast<void*>(&tiled_spmm_kernel<FMT, SS, NT, SINGLE, false>);
 }
 
+// FUSED: the variant with the input transform / residual code (decode);
+// the plain variant keeps the x staging minimal.
 template <int FMT, int SS>
-void* pick_nt(int NT) {  // NT == 0: one token (NT = 1, compile-time B stride)
+void* pick_nt(int NT, bool fused) {  // NT == 0: one token (NT = 1, compile-time B stride)
   switch (NT) {
-    case 0: return kernel_ptr<FMT, SS, 1, true>();
-    case 1: return kernel_ptr<FMT, SS, 1>();
-    case 2: return kernel_ptr<FMT, SS, 2>();
-    default: return kernel_ptr<FMT, SS, 4>();
+    case 0: return kernel_ptr<FMT, SS, 1, true>(fused);
+    case 1: return kernel_ptr<FMT, SS, 1>(fused);
+    case 2: return kernel_ptr<FMT, SS, 2>(fused);
+    default: return kernel_ptr<FMT, SS, 4>(fused);
   }
 }
 
 template <int FMT>
-void* pick_ss(int SS, int NT) {
+void* pick_ss(int SS, int NT, bool fused) {
   switch (SS) {
-    case 1: return pick_nt<FMT, 1>(NT);
-    case 2: return pick_nt<FMT, 2>(NT);
-    default: return pick_nt<FMT, 4>(NT);
+    case 1: return pick_nt<FMT, 1>(NT, fused);
+    case 2: return pick_nt<FMT, 2>(NT, fused);
+    default: return pick_nt<FMT, 4>(NT, fused);
   }
 }
 
-void* pick_kernel(int fmt, int SS, int NT) {
+void* pick_kernel(int fmt, int SS, int NT, bool fused) {
   switch (fmt) {
-    case I4_SP24: return pick_ss<I4_SP24>(SS, NT);
-    case I4_SP14: return pick_ss<I4_SP14>(SS, NT);
-    case I4_DENSE: return pick_ss<I4_DENSE>(SS, NT);
-    case F16_SP24: return pick_nt<F16_SP24, 4>(NT);
-    default: return pick_nt<F16_SP14, 4>(NT);
+    case I4_SP24: return pick_ss<I4_SP24>(SS, NT, fused);
+    case I4_SP14: return pick_ss<I4_SP14>(SS, NT, fused);
+    case I4_DENSE: return pick_ss<I4_DENSE>(SS, NT, fused);
+    case F16_SP24: return pick_nt<F16_SP24, 4>(NT, fused);
+    default: return pick_nt<F16_SP14, 4>(NT, fused);
   }
 }
 
@@ -524,7 +532,7 @@ cudaError_t launch_tiled(const egt_dev_packed* h, const TiledSchedule& sc, const
   static const int dbg = getenv("EGT_DEBUG_MODE") ? atoi(getenv("EGT_DEBUG_MODE")) : 0;
   a.dbg = dbg;
   a.indep = indep && sc.S == 1 ? 1 : 0;
-  void* fn = pick_kernel(h->format, h->tiled.SS, M == 1 ? 0 : sc.NT);
+  void* fn = pick_kernel(h->format, h->tiled.SS, M == 1 ? 0 : sc.NT, a.xform != 0 || a.res != nullptr);
   cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(sc.smem));
   if (err != cudaSuccess) return err;
