@@ -465,6 +465,15 @@ egt_status spmv_impl(const egt_dev_packed* h, const float* x, float* y, uint32_t
                             static_cast<int>(ldy), ctx));
     return EGT_OK;
   }
+  static const bool no_wide = getenv("EGT_NO_WIDE") != nullptr;  // tuning: old M > 16 path
+  if (M > 16 && !res && input == EGT_INPUT_NONE && !no_wide && !plan_forced()) {
+    Workspace* w = nullptr;
+    egt_status st = get_workspace(s, (wide_workspace_bytes(h, static_cast<int>(M)) + 3) / 4, 0, &w);
+    if (st != EGT_OK) return st;
+    CUDA_TRY(launch_wide(h, x, static_cast<int>(ldx), static_cast<int>(M), y, static_cast<int>(ldy),
+                         reinterpret_cast<uint32_t*>(w->partial), ctx, num_sms()));
+    return EGT_OK;
+  }
   TiledSchedule sc;
   if (plan_forced()) {
     sc = plan_tiled(h, static_cast<int>(M), num_sms(), indep);

@@ -98,6 +98,11 @@ size_t tiled_workspace_floats(const egt_dev_packed* h, const TiledSchedule& sc, 
 
 cudaError_t launch_tiled(const egt_dev_packed* h, const TiledSchedule& sc, const float* x, int ldx,
                          int M, float* y, int ldy, const LaunchCtx& ctx, bool indep);
+// Many-token products (M > 16): x fragments in global memory (xf_ws of
+// wide_workspace_bytes), weight-streaming CTAs per 16-token block (spmm_wide.cu).
+size_t wide_workspace_bytes(const egt_dev_packed* h, int M);
+cudaError_t launch_wide(const egt_dev_packed* h, const float* x, int ldx, int M, float* y, int ldy,
+                        uint32_t* xf_ws, const LaunchCtx& ctx, int num_sms);
 cudaError_t launch_general(const egt_dev_packed* h, const float* x, int ldx, int M, float* y,
                            int ldy, const LaunchCtx& ctx);
 

@@ -1,0 +1,290 @@
+// Many-token SparseGemv (M >= 17): the X * W^T products of the prefix-tree
+// verification pass (forward_impl, model.cpp:156-195, M = committed prefix +
+// tree nodes, 64-272 rows in the BASELINE configs).
+//
+// The one-wave M <= 16 kernel (spmm_tiled.cu) keeps the CTA's whole K range
+// of x fragments in shared memory; at M = 80 that no longer fits and it falls
+// back to dozens of K slices whose partial sums outweigh the weights.  Here:
+//   1. xfrag_kernel splits X once into fp16 hi/lo B fragments in global
+//      memory, [token block of 16][n-tile][k-tile][32 lanes][4 u32] (the
+//      layout compute_unit reads with LS = 32), zero-padded (L2 resident).
+//   2. wide_spmm_kernel: one CTA = RB row tiles x one 16-token block over the
+//      full K.  A producer warp streams, per chunk of CH k-quads, the x chunk
+//      (4 bulk copies, one per n-tile) into a 2-deep ring and each row tile's
+//      weight blocks into a weight ring; consumer warp w owns row tiles
+//      w, w + nw, ... so every row is reduced inside one warp (no cross-warp
+//      reduction) and stored directly.  Weights are read ceil(M / 16) times,
+//      x fragments once per CTA: at these M the kernel is tensor-pipe bound.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+
+#include "device_common.cuh"
+#include "handle.h"
+#include "tiled_compute.cuh"
+
+namespace egt_impl {
+
+constexpr int kWideNW = 8;      // consumer warps
+constexpr int kWideTok = 16;    // tokens per CTA (4 n-tiles of 4)
+constexpr int kWideMaxRT = 2;   // row tiles per consumer warp
+
+struct WideArgs {
+  const uint8_t* vals;
+  const uint8_t* meta;
+  const float* scales;
+  const uint8_t* zps;
+  const uint32_t* xf;  // x fragments
+  float* y;
+  int KQ, rt_begin, RT, rows, M, ldy, RB, CH, NSTW, wstage_bytes, xstage_bytes, KTtot;
+};
+
+// X [M x cols] (row stride ldx) -> fragments; one thread per (token block,
+// n-tile, k-tile, lane): 4 u32 = the lane's B fragment (k = kt*32 + 2t + 8r,
+// pair (k, k+1); column g = 2m + part, part 0 = fp16 hi, 1 = residual lo).
+__global__ void xfrag_kernel(const float* __restrict__ x, int ldx, int M, int cols, int KTtot, int TB,
+                             uint32_t* __restrict__ xf) {
+  const long long total = static_cast<long long>(TB) * 4 * KTtot * 32;
+  for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int lane = static_cast<int>(idx & 31);
+    const long long r = idx >> 5;
+    const int kt = static_cast<int>(r % KTtot);
+    const int nt = static_cast<int>((r / KTtot) & 3);
+    const int tb = static_cast<int>(r / (4LL * KTtot));
+    const int g = lane >> 2, t = lane & 3;
+    const int tok = tb * kWideTok + nt * 4 + (g >> 1), part = g & 1;
+    uint4 o;
+    uint32_t* op = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+    for (int reg = 0; reg < 4; ++reg) {
+      const int k = kt * 32 + 2 * t + 8 * reg;
+      float a = 0.f, b = 0.f;
+      if (tok < M) {
+        const float* xr = x + static_cast<size_t>(tok) * ldx;
+        if (k < cols) a = xr[k];
+        if (k + 1 < cols) b = xr[k + 1];
+      }
+      __half ha = __float2half_rn(a), hb = __float2half_rn(b);
+      if (part) {
+        ha = __float2half_rn(a - __half2float(ha));
+        hb = __float2half_rn(b - __half2float(hb));
+      }
+      op[reg] = static_cast<uint32_t>(__half_as_ushort(ha)) | (static_cast<uint32_t>(__half_as_ushort(hb)) << 16);
+    }
+    reinterpret_cast<uint4*>(xf)[idx] = o;
+  }
+}
+
+template <int FMT, int SS>
+__global__ void __launch_bounds__(32 * (kWideNW + 1), 1) wide_spmm_kernel(const WideArgs a) {
+  constexpr int E = 4 / SS;
+  constexpr int VB = val_lane_bytes(FMT), MB = meta_lane_bytes(FMT);
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  constexpr int nw = kWideNW;
+  const int rt0 = blockIdx.x * a.RB;
+  const int RBc = min(a.RB, a.RT - rt0);
+  const int tb = blockIdx.y;
+  const int NCH = (a.KQ + a.CH - 1) / a.CH;
+  uint64_t* xfull = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* xempty = xfull + 2;
+  uint64_t* wfull = xempty + 2;
+  uint64_t* wempty = wfull + a.NSTW;
+  uint8_t* xst = smem_raw + ((16 * (4 + 2 * a.NSTW) + 127) / 128) * 128;
+  uint8_t* wst = xst + 2 * a.xstage_bytes;
+  if (tid == 0) {
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(xfull + s, 1);
+      mbar_init(xempty + s, nw);
+    }
+    for (int s = 0; s < a.NSTW; ++s) {
+      mbar_init(wfull + s, 1);
+      mbar_init(wempty + s, 1);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  pdl_launch_dependents();
+  pdl_wait();  // x fragments come from the preceding xfrag_kernel
+
+  if (warp == nw) {
+    if (lane == 0) {
+      const uint64_t pol = evict_first_policy();
+      int ws = 0;
+      uint32_t wph = 0;
+      long long wq = 0;
+      for (int c = 0; c < NCH; ++c) {
+        const int kq0 = c * a.CH, n = min(a.CH, a.KQ - kq0);
+        const int xs = c & 1;
+        if (c >= 2) mbar_wait(xempty + xs, ((c >> 1) - 1) & 1);
+        const uint32_t xb = static_cast<uint32_t>(n) * 4 * 512;  // bytes per n-tile
+        mbar_expect_tx(xfull + xs, 4 * xb);
+        for (int nt = 0; nt < 4; ++nt) {
+          const uint32_t* src = a.xf + ((static_cast<size_t>(tb) * 4 + nt) * a.KTtot + kq0 * 4) * 128;
+          bulk_g2s(xst + xs * a.xstage_bytes + nt * (a.CH * 4 * 512), src, xb, xfull + xs, pol);
+        }
+        for (int i = 0; i < RBc; ++i) {
+          if (wq >= a.NSTW) mbar_wait(wempty + ws, wph ^ 1u);
+          uint8_t* st = wst + static_cast<size_t>(ws) * a.wstage_bytes;
+          const size_t blk = static_cast<size_t>(a.rt_begin + rt0 + i) * a.KQ + kq0;
+          mbar_expect_tx(wfull + ws, stage_bytes<FMT>(n, E));
+          bulk_g2s(st, a.vals + blk * 32 * VB, n * 32 * VB, wfull + ws, pol);
+          if constexpr (MB > 0) bulk_g2s(st + n * 32 * VB, a.meta + blk * 32 * MB, n * 32 * MB, wfull + ws, pol);
+          if constexpr (has_scales(FMT)) {
+            uint8_t* sp = st + n * 32 * (VB + MB);
+            bulk_g2s(sp, a.scales + blk * E * 16, n * E * 64, wfull + ws, pol);
+            bulk_g2s(sp + n * E * 64, a.zps + blk * E * 16, n * E * 16, wfull + ws, pol);
+          }
+          ++wq;
+          if (++ws == a.NSTW) {
+            ws = 0;
+            wph ^= 1u;
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // consumer warp: row tiles warp, warp + nw, ... (at most kWideMaxRT)
+  float acc[kWideMaxRT][4][2];
+#pragma unroll
+  for (int r = 0; r < kWideMaxRT; ++r)
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) acc[r][nt][0] = acc[r][nt][1] = 0.f;
+  for (int c = 0; c < NCH; ++c) {
+    const int n = min(a.CH, a.KQ - c * a.CH);
+    const int xs = c & 1;
+    mbar_wait(xfull + xs, (c >> 1) & 1);
+    const uint32_t* sx = reinterpret_cast<const uint32_t*>(xst + xs * a.xstage_bytes);
+#pragma unroll
+    for (int r = 0; r < kWideMaxRT; ++r) {
+      const int i = warp + r * nw;
+      if (i < RBc) {
+        const long long q = static_cast<long long>(c) * RBc + i;  // weight stage index
+        const int ws = static_cast<int>(q % a.NSTW);
+        mbar_wait(wfull + ws, static_cast<uint32_t>((q / a.NSTW) & 1));
+        const uint8_t* st = wst + static_cast<size_t>(ws) * a.wstage_bytes;
+        const int KTc = a.CH * 4;
+        for (int u = 0; u < n; ++u) {
+          Cursor cu = make_cursor<FMT, E>(st, n, u, lane, sx, u * 4, 32);
+          cu.b = sx + (u * 4 * 32 + lane) * 4;
+          Unit<FMT, E> un;
+          lds_unit<FMT, E>(un, cu);
+          compute_unit<FMT, SS, 4>(un, cu.b, KTc, 32, acc[r]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(wempty + ws);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(xempty + xs);
+  }
+  // lane (g, t): n-tile nt's token 4nt + t, rows g (acc[.][0]) and g + 8 (acc[.][1])
+  const int g = lane >> 2, t = lane & 3;
+#pragma unroll
+  for (int r = 0; r < kWideMaxRT; ++r) {
+    const int i = warp + r * nw;
+    if (i < RBc) {
+#pragma unroll
+      for (int nt = 0; nt < 4; ++nt) {
+        const int tok = tb * kWideTok + 4 * nt + t;
+        if (tok < a.M) {
+          const int row = (rt0 + i) * 16 + g;
+          float* yr = a.y + static_cast<size_t>(tok) * a.ldy;
+          if (row < a.rows) yr[row] = acc[r][nt][0];
+          if (row + 8 < a.rows) yr[row + 8] = acc[r][nt][1];
+        }
+      }
+    }
+  }
+}
+
+namespace {
+template <int FMT, int SS>
+void* wide_ptr() {
+  return reinterpret_cast<void*>(&wide_spmm_kernel<FMT, SS>);
+}
+void* pick_wide(int fmt, int SS) {
+  switch (fmt * 8 + SS) {
+    case I4_SP24 * 8 + 4: return wide_ptr<I4_SP24, 4>();
+    case I4_SP24 * 8 + 2: return wide_ptr<I4_SP24, 2>();
+    case I4_SP24 * 8 + 1: return wide_ptr<I4_SP24, 1>();
+    case I4_SP14 * 8 + 4: return wide_ptr<I4_SP14, 4>();
+    case I4_SP14 * 8 + 2: return wide_ptr<I4_SP14, 2>();
+    case I4_SP14 * 8 + 1: return wide_ptr<I4_SP14, 1>();
+    case I4_DENSE * 8 + 4: return wide_ptr<I4_DENSE, 4>();
+    case I4_DENSE * 8 + 2: return wide_ptr<I4_DENSE, 2>();
+    case I4_DENSE * 8 + 1: return wide_ptr<I4_DENSE, 1>();
+    case F16_SP24 * 8 + 4: return wide_ptr<F16_SP24, 4>();
+    default: return wide_ptr<F16_SP14, 4>();
+  }
+}
+}  // namespace
+
+size_t wide_workspace_bytes(const egt_dev_packed* h, int M) {
+  const int TB = (M + kWideTok - 1) / kWideTok;
+  return static_cast<size_t>(TB) * 4 * h->tiled.KQ * 4 * 512;
+}
+
+cudaError_t launch_wide(const egt_dev_packed* h, const float* x, int ldx, int M, float* y, int ldy,
+                        uint32_t* xf_ws, const LaunchCtx& ctx, int num_sms) {
+  const int KQ = h->tiled.KQ, RT = h->tiled.RT, E = h->tiled.E, fmt = h->format;
+  const int KTtot = KQ * 4;
+  const int TB = (M + kWideTok - 1) / kWideTok;
+  {
+    const long long total = static_cast<long long>(TB) * 4 * KTtot * 32;
+    const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 8LL * num_sms));
+    xfrag_kernel<<<blocks, 256, 0, ctx.stream>>>(x, ldx, M, static_cast<int>(h->cols), KTtot, TB, xf_ws);
+    ++launch_counter();
+  }
+  WideArgs a;
+  a.vals = h->tiled.vals;
+  a.meta = h->tiled.meta;
+  a.scales = h->tiled.scales;
+  a.zps = h->tiled.zps;
+  a.xf = xf_ws;
+  a.y = y;
+  a.KQ = KQ;
+  a.rt_begin = h->tiled.rt_begin;
+  a.RT = RT;
+  a.rows = static_cast<int>(h->rows);
+  a.M = M;
+  a.ldy = ldy;
+  a.KTtot = KTtot;
+  // RB: up to nw * kWideMaxRT row tiles; fewer when the token blocks alone
+  // leave SMs idle (one wave of CTAs at one per SM)
+  int RB = kWideNW * kWideMaxRT;
+  while (RB > kWideNW && static_cast<long long>((RT + RB - 1) / RB) * TB < num_sms) RB -= kWideNW;
+  while (RB > 1 && static_cast<long long>((RT + RB - 1) / RB) * TB < num_sms && RB > 1) --RB;
+  a.RB = RB;
+  a.CH = 4;
+  const int blk = 32 * (val_lane_bytes(fmt) + meta_lane_bytes(fmt)) + (has_scales(fmt) ? E * 80 : 0);
+  a.wstage_bytes = (a.CH * blk + 127) / 128 * 128;
+  a.xstage_bytes = 4 * a.CH * 4 * 512;
+  const int budget = 200 * 1024 - 2 * a.xstage_bytes - 1024;
+  a.NSTW = std::max(2, std::min(32, budget / a.wstage_bytes));
+  const size_t smem = (16 * (4 + 2 * a.NSTW) + 127) / 128 * 128 + 2 * static_cast<size_t>(a.xstage_bytes) +
+                      static_cast<size_t>(a.NSTW) * a.wstage_bytes;
+  void* fn = pick_wide(fmt, h->tiled.SS);
+  cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (err != cudaSuccess) return err;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((RT + RB - 1) / RB, TB, 1);
+  cfg.blockDim = dim3(32 * (kWideNW + 1));
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = ctx.pdl ? 1 : 0;
+  void* args[] = {&a};
+  err = cudaLaunchKernelExC(&cfg, fn, args);
+  if (err == cudaSuccess) ++launch_counter();
+  return err;
+}
+
+}  // namespace egt_impl

@@ -277,3 +277,30 @@ def test_multi_token_wide(egt, port, torch, M):
     rng = np.random.default_rng(171 + M)
     p, _, _ = make_int4(rng, 1040, 4096, 2, 128, port)
     _check_product(egt, port, torch, p, rng, M=M)
+
+
+@pytest.mark.parametrize("kind", ["int4-1:4-g64", "int4-2:4-g32", "fp16-2:4", "fp16-1:4"])
+@pytest.mark.parametrize("M", [17, 40, 272])
+def test_many_token_formats(egt, port, torch, kind, M):
+    """The many-token kernel (spmm_wide.cu, M > 16) for every tiled format."""
+    rng = np.random.default_rng(191 + M + len(kind))
+    if kind.startswith("int4"):
+        n = 1 if "1:4" in kind else 2
+        p, _, _ = make_int4(rng, 272, 1536, n, int(kind.split("-g")[1]), port)
+    else:
+        p, _, _ = make_f16(rng, 272, 1536, 1 if "1:4" in kind else 2, port)
+    _check_product(egt, port, torch, p, rng, M=M)
+
+
+@pytest.mark.parametrize("M", [18, 64])
+def test_many_token_dense_int4(egt, port, torch, M):
+    rng = np.random.default_rng(301 + M)
+    w = rng.uniform(-1, 1, (400, 2048)).astype(np.float32)
+    q = egt.quantize_matrix(w, 64)
+    d = egt.DeviceMatrix.dense_i4(q)
+    xs = rng.uniform(-1, 1, (M, 2048)).astype(np.float32)
+    y = d.spmv(torch.from_numpy(xs).cuda()).cpu().numpy()
+    qo = port.quantize(w, np.full(400, 64, np.uint32), None)
+    for m in (0, M // 2, M - 1):
+        ok, err = close(y[m], port.quant_dense_gemv(qo, xs[m]))
+        assert ok, err
