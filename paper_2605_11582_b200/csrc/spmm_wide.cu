@@ -154,33 +154,46 @@ __global__ void __launch_bounds__(32 * (kWideNW + 1), 1) wide_spmm_kernel(const 
   for (int r = 0; r < kWideMaxRT; ++r)
 #pragma unroll
     for (int nt = 0; nt < 4; ++nt) acc[r][nt][0] = acc[r][nt][1] = 0.f;
+  // own row tiles: warp + r * nw (r < nr); both are consumed in lockstep so
+  // that every B fragment load from shared memory feeds nr row tiles
+  const int nr = warp < RBc ? (warp + nw < RBc ? 2 : 1) : 0;
+  static_assert(kWideMaxRT == 2, "lockstep over two row tiles");
   for (int c = 0; c < NCH; ++c) {
     const int n = min(a.CH, a.KQ - c * a.CH);
     const int xs = c & 1;
     mbar_wait(xfull + xs, (c >> 1) & 1);
     const uint32_t* sx = reinterpret_cast<const uint32_t*>(xst + xs * a.xstage_bytes);
-#pragma unroll
-    for (int r = 0; r < kWideMaxRT; ++r) {
-      const int i = warp + r * nw;
-      if (i < RBc) {
-        const long long q = static_cast<long long>(c) * RBc + i;  // weight stage index
-        const int ws = static_cast<int>(q % a.NSTW);
-        mbar_wait(wfull + ws, static_cast<uint32_t>((q / a.NSTW) & 1));
-        const uint8_t* st = wst + static_cast<size_t>(ws) * a.wstage_bytes;
-        const int KTc = a.CH * 4;
-        for (int u = 0; u < n; ++u) {
-          Cursor cu = make_cursor<FMT, E>(st, n, u, lane, sx, u * 4, 32);
-          cu.b = sx + (u * 4 * 32 + lane) * 4;
-          Unit<FMT, E> un;
-          lds_unit<FMT, E>(un, cu);
-          compute_unit<FMT, SS, 4>(un, cu.b, KTc, 32, acc[r]);
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(wempty + ws);
+    const uint8_t* st[kWideMaxRT] = {nullptr, nullptr};
+    int wsi[kWideMaxRT] = {0, 0};
+    for (int r = 0; r < nr; ++r) {
+      const long long q = static_cast<long long>(c) * RBc + warp + r * nw;  // weight stage index
+      wsi[r] = static_cast<int>(q % a.NSTW);
+      mbar_wait(wfull + wsi[r], static_cast<uint32_t>((q / a.NSTW) & 1));
+      st[r] = wst + static_cast<size_t>(wsi[r]) * a.wstage_bytes;
+    }
+    const int KTc = a.CH * 4;
+    if (nr == 2) {
+      for (int u = 0; u < n; ++u) {
+        Unit<FMT, E> un[2];
+        const Cursor c0 = make_cursor<FMT, E>(st[0], n, u, lane, sx, u * 4, 32);
+        const Cursor c1 = make_cursor<FMT, E>(st[1], n, u, lane, sx, u * 4, 32);
+        lds_unit<FMT, E>(un[0], c0);
+        lds_unit<FMT, E>(un[1], c1);
+        compute_units<FMT, SS, 4, 2>(un, sx + (u * 4 * 32 + lane) * 4, KTc, 32, acc);
+      }
+    } else if (nr == 1) {
+      float (&a1)[1][4][2] = *reinterpret_cast<float (*)[1][4][2]>(&acc[0]);
+      for (int u = 0; u < n; ++u) {
+        Unit<FMT, E> un[1];
+        lds_unit<FMT, E>(un[0], make_cursor<FMT, E>(st[0], n, u, lane, sx, u * 4, 32));
+        compute_units<FMT, SS, 4, 1>(un, sx + (u * 4 * 32 + lane) * 4, KTc, 32, a1);
       }
     }
     __syncwarp();
-    if (lane == 0) mbar_arrive(xempty + xs);
+    if (lane == 0) {
+      for (int r = 0; r < nr; ++r) mbar_arrive(wempty + wsi[r]);
+      mbar_arrive(xempty + xs);
+    }
   }
   // lane (g, t): n-tile nt's token 4nt + t, rows g (acc[.][0]) and g + 8 (acc[.][1])
   const int g = lane >> 2, t = lane & 3;
@@ -260,12 +273,18 @@ cudaError_t launch_wide(const egt_dev_packed* h, const float* x, int ldx, int M,
   while (RB > kWideNW && static_cast<long long>((RT + RB - 1) / RB) * TB < num_sms) RB -= kWideNW;
   while (RB > 1 && static_cast<long long>((RT + RB - 1) / RB) * TB < num_sms && RB > 1) --RB;
   a.RB = RB;
-  a.CH = 4;
+  // A consumer warp holds its two row tiles' stages of one chunk at once
+  // (nw stages apart), so the weight ring needs > nw stages or the producer
+  // could wait on a stage held by the warp waiting for it.
   const int blk = 32 * (val_lane_bytes(fmt) + meta_lane_bytes(fmt)) + (has_scales(fmt) ? E * 80 : 0);
-  a.wstage_bytes = (a.CH * blk + 127) / 128 * 128;
-  a.xstage_bytes = 4 * a.CH * 4 * 512;
-  const int budget = 200 * 1024 - 2 * a.xstage_bytes - 1024;
-  a.NSTW = std::max(2, std::min(32, budget / a.wstage_bytes));
+  for (a.CH = 4;; a.CH /= 2) {
+    a.wstage_bytes = (a.CH * blk + 127) / 128 * 128;
+    a.xstage_bytes = 4 * a.CH * 4 * 512;
+    const int budget = 200 * 1024 - 2 * a.xstage_bytes - 1024;
+    a.NSTW = std::min(32, budget / a.wstage_bytes);
+    if (a.NSTW > kWideNW || a.CH == 1) break;
+  }
+  if (a.NSTW <= kWideNW) return cudaErrorInvalidConfiguration;
   const size_t smem = (16 * (4 + 2 * a.NSTW) + 127) / 128 * 128 + 2 * static_cast<size_t>(a.xstage_bytes) +
                       static_cast<size_t>(a.NSTW) * a.wstage_bytes;
   void* fn = pick_wide(fmt, h->tiled.SS);

@@ -156,9 +156,10 @@ constexpr float kTwo24 = 16777216.f;
 constexpr float kTwo20 = 1048576.f;
 constexpr uint32_t kOnes = 0x3C003C00u;  // half2(1, 1)
 
-template <int FMT, int SS, int NT, bool kLoadB = true, bool kOnesMma = true>
-__device__ __forceinline__ void compute_unit(const Unit<FMT, 4 / SS>& u, const uint32_t* pb, int KTc,
-                                             int LS, float (&acc)[NT][2]) {
+// NR units of the same k-quad (NR row tiles) share every B fragment load.
+template <int FMT, int SS, int NT, int NR, bool kLoadB = true, bool kOnesMma = true>
+__device__ __forceinline__ void compute_units(const Unit<FMT, 4 / SS> (&uu)[NR], const uint32_t* pb, int KTc,
+                                              int LS, float (&acc)[NR][NT][2]) {
   // INT4 2:4 and dense: the zero point is subtracted in the A operand.  A
   // nibble under the fp16 exponent 0x64 is exactly 1024 + c (row g) or
   // 1024 + 16c (row g+8, 4 bits higher); HSUB2 with 1024 + z (1024 + 16z)
@@ -170,25 +171,28 @@ __device__ __forceinline__ void compute_unit(const Unit<FMT, 4 / SS>& u, const u
   // B fragments: lanes whose column holds no token (lane >= LS) read lane&7's
   // slot unpredicated -- D column n only depends on B column n, and the
   // columns of absent tokens are never used (make_cursor).
-  float d[NT][4];
-  float d1[NT][4];
-  uint32_t zpair = 0, zA = 0, zA8 = 0;
+  float dd[NR][NT][4];
+  float dd1[NR][NT][4];
+  uint32_t zpairs[NR], zAs[NR], zA8s[NR];
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     const int e = j / SS;
     if (j % SS == 0) {
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) {
-        d[nt][0] = d[nt][1] = d[nt][2] = d[nt][3] = 0.f;
-        d1[nt][0] = d1[nt][1] = d1[nt][2] = d1[nt][3] = 0.f;
-      }
-      if constexpr (FMT == I4_SP14) {
-        const uint32_t z0 = u.z[e] & 0xFFu, z1 = (u.z[e] >> 8) & 0xFFu;
-        zpair = zp_magic(z0, z1);
-      }
-      if constexpr (kZpInA) {
-        zA = (0x6400u | (u.z[e] & 0xFFu)) * 0x10001u;
-        zA8 = (0x6400u | ((u.z[e] >> 4) & 0xF0u)) * 0x10001u;
+      for (int r = 0; r < NR; ++r) {
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          dd[r][nt][0] = dd[r][nt][1] = dd[r][nt][2] = dd[r][nt][3] = 0.f;
+          dd1[r][nt][0] = dd1[r][nt][1] = dd1[r][nt][2] = dd1[r][nt][3] = 0.f;
+        }
+        if constexpr (FMT == I4_SP14) {
+          const uint32_t z0 = uu[r].z[e] & 0xFFu, z1 = (uu[r].z[e] >> 8) & 0xFFu;
+          zpairs[r] = zp_magic(z0, z1);
+        }
+        if constexpr (kZpInA) {
+          zAs[r] = (0x6400u | (uu[r].z[e] & 0xFFu)) * 0x10001u;
+          zA8s[r] = (0x6400u | ((uu[r].z[e] >> 4) & 0xF0u)) * 0x10001u;
+        }
       }
     }
     uint32_t b[NT][4];
@@ -196,8 +200,18 @@ __device__ __forceinline__ void compute_unit(const Unit<FMT, 4 / SS>& u, const u
       load_b<NT>(b, pb + j * LS * 4, KTc * LS * 4);
     } else {  // tuning experiment: B from registers (results are garbage)
 #pragma unroll
-      for (int nt = 0; nt < NT; ++nt) b[nt][0] = b[nt][1] = b[nt][2] = b[nt][3] = u.m[0] ^ j;
+      for (int nt = 0; nt < NT; ++nt) b[nt][0] = b[nt][1] = b[nt][2] = b[nt][3] = uu[0].m[0] ^ j;
     }
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+    const Unit<FMT, 4 / SS>& u = uu[r];
+    float (&d)[NT][4] = dd[r];
+    float (&d1)[NT][4] = dd1[r];
+    const uint32_t zpair = zpairs[r], zA = zAs[r], zA8 = zA8s[r];
+    (void)zpair;
+    (void)zA;
+    (void)zA8;
+    (void)d1;
     if constexpr (FMT == I4_SP24 && kZpInA) {
       const uint32_t w = u.v[j], w8 = w >> 8;
       const uint32_t a[4] = {hsub2_u32(nib2_magic(w), zA), hsub2_u32(nib16_magic(w), zA8),
@@ -251,13 +265,20 @@ __device__ __forceinline__ void compute_unit(const Unit<FMT, 4 / SS>& u, const u
         mma_16816(d1[nt], kOnes, kOnes, kOnes, kOnes, b[nt][2], b[nt][3]);
       }
     }
+    }  // r (mma)
     if (j % SS == SS - 1) {
+#pragma unroll
+    for (int r = 0; r < NR; ++r) {
+    const Unit<FMT, 4 / SS>& u = uu[r];
+    float (&d)[NT][4] = dd[r];
+    float (&d1)[NT][4] = dd1[r];
+    (void)d1;
       if constexpr (kZpInA) {
         const float sg = __uint_as_float(u.s[2 * e]), sg8 = __uint_as_float(u.s[2 * e + 1]) * 0.0625f;
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-          acc[nt][0] = fmaf(sg, d[nt][0] + d[nt][1], acc[nt][0]);
-          acc[nt][1] = fmaf(sg8, d[nt][2] + d[nt][3], acc[nt][1]);
+          acc[r][nt][0] = fmaf(sg, d[nt][0] + d[nt][1], acc[r][nt][0]);
+          acc[r][nt][1] = fmaf(sg8, d[nt][2] + d[nt][3], acc[r][nt][1]);
         }
       } else if constexpr (kOnesTrick) {
         const float sg = __uint_as_float(u.s[2 * e]), sg8 = __uint_as_float(u.s[2 * e + 1]);
@@ -266,25 +287,34 @@ __device__ __forceinline__ void compute_unit(const Unit<FMT, 4 / SS>& u, const u
         const float ng8 = -sg8 * static_cast<float>((u.z[e] >> 8) & 0xFFu);
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-          acc[nt][0] = fmaf(cg, d[nt][0] + d[nt][1], fmaf(ng, d1[nt][0] + d1[nt][1], acc[nt][0]));
-          acc[nt][1] = fmaf(cg8, d[nt][2] + d[nt][3], fmaf(ng8, d1[nt][2] + d1[nt][3], acc[nt][1]));
+          acc[r][nt][0] = fmaf(cg, d[nt][0] + d[nt][1], fmaf(ng, d1[nt][0] + d1[nt][1], acc[r][nt][0]));
+          acc[r][nt][1] = fmaf(cg8, d[nt][2] + d[nt][3], fmaf(ng8, d1[nt][2] + d1[nt][3], acc[r][nt][1]));
         }
       } else if constexpr (has_scales(FMT)) {
         const float sg = __uint_as_float(u.s[2 * e]), sg8 = __uint_as_float(u.s[2 * e + 1]);
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-          acc[nt][0] = fmaf(sg, d[nt][0] + d[nt][1], acc[nt][0]);
-          acc[nt][1] = fmaf(sg8, d[nt][2] + d[nt][3], acc[nt][1]);
+          acc[r][nt][0] = fmaf(sg, d[nt][0] + d[nt][1], acc[r][nt][0]);
+          acc[r][nt][1] = fmaf(sg8, d[nt][2] + d[nt][3], acc[r][nt][1]);
         }
       } else {
 #pragma unroll
         for (int nt = 0; nt < NT; ++nt) {
-          acc[nt][0] += d[nt][0] + d[nt][1];
-          acc[nt][1] += d[nt][2] + d[nt][3];
+          acc[r][nt][0] += d[nt][0] + d[nt][1];
+          acc[r][nt][1] += d[nt][2] + d[nt][3];
         }
       }
+    }  // r (scale)
     }
   }
+}
+
+template <int FMT, int SS, int NT, bool kLoadB = true, bool kOnesMma = true>
+__device__ __forceinline__ void compute_unit(const Unit<FMT, 4 / SS>& u, const uint32_t* pb, int KTc,
+                                             int LS, float (&acc)[NT][2]) {
+  const Unit<FMT, 4 / SS> uu[1] = {u};
+  float (&a1)[1][NT][2] = *reinterpret_cast<float (*)[1][NT][2]>(&acc);
+  compute_units<FMT, SS, NT, 1, kLoadB, kOnesMma>(uu, pb, KTc, LS, a1);
 }
 
 template <int FMT>
