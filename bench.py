@@ -351,11 +351,15 @@ def measure_decode(torch, egt, plan_name, n_tokens=64, prompt_len=16, max_len=25
     w0 = time.perf_counter()
     toks2 = dec.generate(prompt, n_tokens)
     e2e_s = time.perf_counter() - w0
+    if os.environ.get("EGT_BENCH_NO_VERIFY"):
+        n_nodes_list = ()
+    else:
+        n_nodes_list = (64, 256)
     # BASELINE configs[3]: one multi-token pass over a prefix-tree (verify_parallel's
     # forward, decode.cpp:336-421 -> model.cpp:118-202): M tree nodes after a
     # committed prefix, each row sees the prefix + its ancestors + itself
     verify = {}
-    for n_nodes in (64, 256):
+    for n_nodes in n_nodes_list:
         parent = np.array([-1] + [int(rng.integers(0, i)) for i in range(1, n_nodes)])
         depth = np.zeros(n_nodes, np.int32)
         for i in range(1, n_nodes):

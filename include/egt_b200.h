@@ -160,10 +160,13 @@ EGT_API egt_status egt_spmv_ex(const egt_dev_packed* h, const float* x_dev, floa
  * SILU (the EGT_INPUT_* constants below).  residual may be NULL or equal y
  * (row stride ldr).  Tiled path only (else EGT_EINVAL).  With
  * EGT_SPMV_INDEPENDENT neither x nor residual may be written by the
- * immediately preceding kernel on the stream. */
+ * immediately preceding kernel on the stream.  l2_next (may be NULL): the
+ * matrix the NEXT product will read; its weights are prefetched into L2
+ * while this product runs (decode chains, M <= 16). */
 EGT_API egt_status egt_spmv_fused(const egt_dev_packed* h, const float* x_dev, float* y_dev, uint32_t M,
                                   uint32_t ldx, uint32_t ldy, const float* residual_dev, uint32_t ldr,
-                                  uint32_t input, float eps, uint32_t flags, void* stream);
+                                  uint32_t input, float eps, uint32_t flags, const egt_dev_packed* l2_next,
+                                  void* stream);
 
 /* Same as egt_spmv with host buffers: H2D of x, the product, D2H of y, and a
  * stream synchronize.  x_len must equal cols (else EGT_EINVAL with the

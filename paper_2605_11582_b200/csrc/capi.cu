@@ -427,7 +427,8 @@ egt_status egt_dev_packed_query(const egt_dev_packed* h, egt_dev_packed_info* in
 
 namespace {
 egt_status spmv_impl(const egt_dev_packed* h, const float* x, float* y, uint32_t M, uint32_t ldx, uint32_t ldy,
-                     uint32_t flags, const float* res, uint32_t ldr, uint32_t input, float eps, void* stream) {
+                     uint32_t flags, const float* res, uint32_t ldr, uint32_t input, float eps,
+                     const egt_dev_packed* l2_next, void* stream) {
   const bool indep = (flags & EGT_SPMV_INDEPENDENT) != 0;
   if (!h) return fail(EGT_EINVAL, "spmv: null matrix");
   if (M == 0) return EGT_OK;
@@ -447,6 +448,7 @@ egt_status spmv_impl(const egt_dev_packed* h, const float* x, float* y, uint32_t
   ctx.eps = eps;
   ctx.res = res;
   ctx.ldr = static_cast<int>(M > 1 ? ldr : h->rows);
+  ctx.l2_next = l2_next;
   if (h->cols == 0) {
     for (uint32_t m = 0; m < M; ++m) {
       float* ym = y + static_cast<size_t>(m) * ldy;
@@ -510,13 +512,13 @@ egt_status spmv_impl(const egt_dev_packed* h, const float* x, float* y, uint32_t
 
 egt_status egt_spmv_ex(const egt_dev_packed* h, const float* x, float* y, uint32_t M, uint32_t ldx,
                        uint32_t ldy, uint32_t flags, void* stream) {
-  return spmv_impl(h, x, y, M, ldx, ldy, flags, nullptr, 0, EGT_INPUT_NONE, 0.f, stream);
+  return spmv_impl(h, x, y, M, ldx, ldy, flags, nullptr, 0, EGT_INPUT_NONE, 0.f, nullptr, stream);
 }
 
 egt_status egt_spmv_fused(const egt_dev_packed* h, const float* x, float* y, uint32_t M, uint32_t ldx,
                           uint32_t ldy, const float* residual, uint32_t ldr, uint32_t input, float eps,
-                          uint32_t flags, void* stream) {
-  return spmv_impl(h, x, y, M, ldx, ldy, flags, residual, ldr, input, eps, stream);
+                          uint32_t flags, const egt_dev_packed* l2_next, void* stream) {
+  return spmv_impl(h, x, y, M, ldx, ldy, flags, residual, ldr, input, eps, l2_next, stream);
 }
 
 egt_status egt_spmv(const egt_dev_packed* h, const float* x, float* y, uint32_t M, uint32_t ldx,

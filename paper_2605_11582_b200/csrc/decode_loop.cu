@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <string>
 
 #include "device_common.cuh"
@@ -184,16 +185,21 @@ egt_status enqueue_step(egt_decoder* dd) {
   ++launch_counter();
   const float scale = 1.0f / std::sqrt(static_cast<float>(dh));  // model.cpp:139
   egt_status st = EGT_OK;
+  // optional (EGT_DECODE_L2PF=1): each product prefetches the next product's
+  // weights into L2 (measured slower on B200: 538 vs 576 tok/s, so off)
+  const bool l2pf = getenv("EGT_DECODE_L2PF") != nullptr;
   auto lin = [&](const egt_dev_packed* w, const float* x, float* y, const float* res, uint32_t input,
-                 uint32_t flags) {
-    if (st == EGT_OK) st = egt_spmv_fused(w, x, y, 1, w->cols, w->rows, res, w->rows, input, kNormEps, flags, s);
+                 uint32_t flags, const egt_dev_packed* next) {
+    if (st == EGT_OK)
+      st = egt_spmv_fused(w, x, y, 1, w->cols, w->rows, res, w->rows, input, kNormEps, flags, l2pf ? next : nullptr, s);
   };
   const size_t attn_smem = static_cast<size_t>(dd->max_len) * sizeof(float);
   for (uint32_t l = 0; l < c.n_layers && st == EGT_OK; ++l) {
     const egt_dev_packed* const* w = m->layers.data() + 6 * l;
-    lin(w[0], dd->h, dd->q, nullptr, EGT_INPUT_RMSNORM, 0);
-    lin(w[1], dd->h, dd->k, nullptr, EGT_INPUT_RMSNORM, EGT_SPMV_INDEPENDENT);
-    lin(w[2], dd->h, dd->v, nullptr, EGT_INPUT_RMSNORM, EGT_SPMV_INDEPENDENT);
+    const egt_dev_packed* next_q = l + 1 < c.n_layers ? m->layers[6 * (l + 1)] : m->head;
+    lin(w[0], dd->h, dd->q, nullptr, EGT_INPUT_RMSNORM, 0, w[1]);
+    lin(w[1], dd->h, dd->k, nullptr, EGT_INPUT_RMSNORM, EGT_SPMV_INDEPENDENT, w[2]);
+    lin(w[2], dd->h, dd->v, nullptr, EGT_INPUT_RMSNORM, EGT_SPMV_INDEPENDENT, w[3]);
     float* kc = dd->kc + static_cast<size_t>(l) * dd->max_len * d;
     float* vc = dd->vc + static_cast<size_t>(l) * dd->max_len * d;
     switch (dh) {
@@ -217,11 +223,11 @@ egt_status enqueue_step(egt_decoder* dd) {
         return dfail(EGT_EINVAL, "decoder: head dimension must be 16, 32, 64 or 128");
     }
     ++launch_counter();
-    lin(w[3], dd->o, dd->h, dd->h, EGT_INPUT_NONE, 0);
-    lin(w[4], dd->h, dd->f, nullptr, EGT_INPUT_RMSNORM, 0);
-    lin(w[5], dd->f, dd->h, dd->h, EGT_INPUT_SILU, 0);
+    lin(w[3], dd->o, dd->h, dd->h, EGT_INPUT_NONE, 0, w[4]);
+    lin(w[4], dd->h, dd->f, nullptr, EGT_INPUT_RMSNORM, 0, w[5]);
+    lin(w[5], dd->f, dd->h, dd->h, EGT_INPUT_SILU, 0, next_q);
   }
-  lin(m->head, dd->h, dd->logits, nullptr, EGT_INPUT_RMSNORM, 0);
+  lin(m->head, dd->h, dd->logits, nullptr, EGT_INPUT_RMSNORM, 0, m->layers[0]);
   if (st != EGT_OK) return st;
   dec_next_kernel<<<1, 1024, 0, s>>>(dd->state, dd->prompt, dd->logits, static_cast<int>(c.vocab_size));
   ++launch_counter();

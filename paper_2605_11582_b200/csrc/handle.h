@@ -89,6 +89,7 @@ struct LaunchCtx {
   float eps = 1e-6f;
   const float* res = nullptr;    // y = res + product (may alias y)
   int ldr = 0;
+  const egt_dev_packed* l2_next = nullptr;  // weights to prefetch into L2 meanwhile
 };
 
 TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms, bool indep);

@@ -50,6 +50,10 @@ struct TiledArgs {
   float eps;
   const float* res;
   int ldr;
+  // L2 prefetch of the NEXT product's weights (decode chains): each CTA
+  // requests its share of the four storage arrays while this product runs
+  const uint8_t* pf_ptr[4];
+  uint32_t pf_bytes[4];
 };
 
 
@@ -236,6 +240,21 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
         issue(s, i, c);
         if (++c == NCH) { c = 0; ++i; }
         if (++s == NST) { s = 0; phase ^= 1u; }
+      }
+      // after this CTA's own weights are requested: its share of the next
+      // product's weights into L2 (behind them in the TMA queue)
+      if (a.pf_ptr[0] != nullptr) {
+        const uint32_t nb = gridDim.x * gridDim.y * gridDim.z;
+        const uint32_t bid = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const uint32_t chunk = ((a.pf_bytes[r] + nb - 1) / nb + 15u) & ~15u;
+          const uint32_t off = bid * chunk;
+          if (a.pf_ptr[r] && off < a.pf_bytes[r]) {
+            const uint32_t len = min(chunk, a.pf_bytes[r] - off) & ~15u;
+            if (len) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(a.pf_ptr[r] + off), "r"(len) : "memory");
+          }
+        }
       }
     }
   } else {
@@ -503,6 +522,27 @@ size_t tiled_workspace_floats(const egt_dev_packed* h, const TiledSchedule& sc, 
 cudaError_t launch_tiled(const egt_dev_packed* h, const TiledSchedule& sc, const float* x, int ldx,
                          int M, float* y, int ldy, const LaunchCtx& ctx, bool indep) {
   TiledArgs a;
+  for (int r = 0; r < 4; ++r) {
+    a.pf_ptr[r] = nullptr;
+    a.pf_bytes[r] = 0;
+  }
+  if (const egt_dev_packed* nx = ctx.l2_next; nx && nx->path == EGT_PATH_TILED) {
+    const int VB = val_lane_bytes(nx->format), MB = meta_lane_bytes(nx->format);
+    const size_t blk0 = static_cast<size_t>(nx->tiled.rt_begin) * nx->tiled.KQ;
+    const size_t nblk = static_cast<size_t>(nx->tiled.RT) * nx->tiled.KQ;
+    a.pf_ptr[0] = nx->tiled.vals + blk0 * 32 * VB;
+    a.pf_bytes[0] = static_cast<uint32_t>(std::min<size_t>(nblk * 32 * VB, 0xFFFFFFF0u));
+    if (MB > 0) {
+      a.pf_ptr[1] = nx->tiled.meta + blk0 * 32 * MB;
+      a.pf_bytes[1] = static_cast<uint32_t>(std::min<size_t>(nblk * 32 * MB, 0xFFFFFFF0u));
+    }
+    if (has_scales(nx->format)) {
+      a.pf_ptr[2] = reinterpret_cast<const uint8_t*>(nx->tiled.scales + blk0 * nx->tiled.E * 16);
+      a.pf_bytes[2] = static_cast<uint32_t>(nblk * nx->tiled.E * 64);
+      a.pf_ptr[3] = nx->tiled.zps + blk0 * nx->tiled.E * 16;
+      a.pf_bytes[3] = static_cast<uint32_t>(nblk * nx->tiled.E * 16);
+    }
+  }
   a.xform = ctx.xform;
   a.eps = ctx.eps;
   a.res = ctx.res;
@@ -532,7 +572,7 @@ cudaError_t launch_tiled(const egt_dev_packed* h, const TiledSchedule& sc, const
   static const int dbg = getenv("EGT_DEBUG_MODE") ? atoi(getenv("EGT_DEBUG_MODE")) : 0;
   a.dbg = dbg;
   a.indep = indep && sc.S == 1 ? 1 : 0;
-  void* fn = pick_kernel(h->format, h->tiled.SS, M == 1 ? 0 : sc.NT, a.xform != 0 || a.res != nullptr);
+  void* fn = pick_kernel(h->format, h->tiled.SS, M == 1 ? 0 : sc.NT, a.xform != 0 || a.res != nullptr || a.pf_ptr[0]);
   cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(sc.smem));
   if (err != cudaSuccess) return err;
