@@ -167,7 +167,60 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
   // whole row of every token of this CTA, applied while converting
   __shared__ float s_inv[16];
   __shared__ float s_red[32];
-  if (FUSED && a.xform == EGT_INPUT_RMSNORM) {
+  // residual rows of this CTA fetched now, not after the compute (decode:
+  // the O / ff2 products); one output per thread when the CTA is small
+  float res_pre = 0.f;
+  if (FUSED && a.res != nullptr && a.S == 1 && tid < RBc * Mc * 16) {
+    const int row16 = tid & 15, tl = (tid >> 4) % Mc, i = (tid >> 4) / Mc;
+    const int row = (rt0 + i) * 16 + row16;
+    if (row < a.rows) res_pre = a.res[static_cast<size_t>(m0 + tl) * a.ldr + row];
+  }
+  bool staged = false;
+  if constexpr (FUSED && SINGLE) {
+    // one token, whole row in this CTA: a single pass -- the sum of squares
+    // comes from the values loaded for the conversion (one L2 round trip)
+    const int items = KTc * 16;
+    if (a.xform == EGT_INPUT_RMSNORM && kq0 == 0 && KTc * 32 >= a.cols &&
+        items <= XU * static_cast<int>(blockDim.x)) {
+      const float* xr = a.x + static_cast<size_t>(m0) * a.ldx;
+      float2 v[XU];
+      float ss = 0.f;
+#pragma unroll
+      for (int u = 0; u < XU; ++u) {
+        const int i = tid + u * blockDim.x;
+        v[u] = make_float2(0.f, 0.f);
+        if (i < items) {
+          const int k = (i >> 4) * 32 + 2 * ((i >> 2) & 3) + 8 * (i & 3);
+          if (k < a.cols) v[u] = make_float2(__ldg(xr + k), __ldg(xr + k + 1));
+        }
+        ss = fmaf(v[u].x, v[u].x, fmaf(v[u].y, v[u].y, ss));
+      }
+      ss = warp_sum(ss);
+      if (lane == 0) s_red[warp] = ss;
+      __syncthreads();
+      float tot = 0.f;
+      for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) tot += s_red[w];
+      const float inv = 1.0f / sqrtf(tot / static_cast<float>(a.cols) + a.eps);
+#pragma unroll
+      for (int u = 0; u < XU; ++u) {
+        const int i = tid + u * blockDim.x;
+        if (i < items) {
+          const int reg = i & 3, t = (i >> 2) & 3, kt = i >> 4;
+          const float x0 = v[u].x * inv, x1 = v[u].y * inv;
+          const __half h0 = __float2half_rn(x0), h1 = __float2half_rn(x1);
+          const __half l0 = __float2half_rn(x0 - __half2float(h0));
+          const __half l1 = __float2half_rn(x1 - __half2float(h1));
+          uint32_t* row = sB + static_cast<size_t>(kt) * LS * 4;
+          row[t * 4 + reg] = static_cast<uint32_t>(__half_as_ushort(h0)) |
+                             (static_cast<uint32_t>(__half_as_ushort(h1)) << 16);
+          row[(4 + t) * 4 + reg] = static_cast<uint32_t>(__half_as_ushort(l0)) |
+                                   (static_cast<uint32_t>(__half_as_ushort(l1)) << 16);
+        }
+      }
+      staged = true;
+    }
+  }
+  if (FUSED && !staged && a.xform == EGT_INPUT_RMSNORM) {
     for (int m = 0; m < Mc; ++m) {
       const float4* xr4 = reinterpret_cast<const float4*>(a.x + static_cast<size_t>(m0 + m) * a.ldx);
       float ss = 0.f;
@@ -188,7 +241,7 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
   }
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) {
-    const int mc = a.dbg == 3 ? 0 : min(4, Mc - 4 * nt);
+    const int mc = (a.dbg == 3 || staged) ? 0 : min(4, Mc - 4 * nt);
     for (int m = 0; m < mc; ++m) {
       const float* xr = a.x + static_cast<size_t>(m0 + 4 * nt + m) * a.ldx;
       const float inv = FUSED && a.xform == EGT_INPUT_RMSNORM ? s_inv[4 * nt + m] : 1.f;
@@ -313,7 +366,8 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
     const int tok = m0 + tl;
     if (row < a.rows) {
       if (a.S == 1)
-        a.y[static_cast<size_t>(tok) * a.ldy + row] = (FUSED && a.res ? a.res[static_cast<size_t>(tok) * a.ldr + row] : 0.f) + v;
+        a.y[static_cast<size_t>(tok) * a.ldy + row] =
+            (FUSED && a.res ? (idx == tid ? res_pre : a.res[static_cast<size_t>(tok) * a.ldr + row]) : 0.f) + v;
       else
         a.partial[(static_cast<size_t>(blockIdx.y) * a.M + tok) * rows_pad + row] = v;
     }
@@ -436,7 +490,8 @@ TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms, bool indep
         // SMs; measured best (tools/plan_sweep.py --indep) is ~250 KB of
         // weights per CTA, i.e. few CTAs per launch.
         const double total = static_cast<double>(RT) * KQ * unit_b;
-        const int target = std::max(16, std::min(num_sms, static_cast<int>(total / (250.0 * 1024) + 0.5)));
+        static const double kb = getenv("EGT_INDEP_CTA_KB") ? atof(getenv("EGT_INDEP_CTA_KB")) : 250.0;
+        const int target = std::max(16, std::min(num_sms, static_cast<int>(total / (kb * 1024) + 0.5)));
         if (RB != (RT + target - 1) / target) continue;
       }
       for (int nw : {4, 8, 12}) {
