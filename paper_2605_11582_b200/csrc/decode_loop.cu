@@ -57,6 +57,7 @@ egt_status dfail(egt_status s, const std::string& m) {
 
 __global__ void dec_embed_kernel(const int32_t* state, const float* emb, const float* ptab, float* h, int d,
                                  int32_t* out) {
+  egt_dev::pdl_launch_dependents();  // the first Q product may prefetch its weights
   const int t = state[0], tok = state[1];
   if (threadIdx.x == 0 && blockIdx.x == 0) out[t] = tok;
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < d; c += gridDim.x * blockDim.x)
@@ -73,6 +74,10 @@ __global__ void __launch_bounds__(256) dec_attention_kernel(const int32_t* state
   extern __shared__ float sc[];  // [t + 1] scores
   __shared__ float red[8];
   __shared__ float part[DH];
+  // launched with programmatic serialization: let the O product start
+  // streaming its weights now, wait for q/k/v before reading them
+  egt_dev::pdl_launch_dependents();
+  egt_dev::pdl_wait();
   const int t = state[0], n = t + 1;
   const int hh = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const size_t base = static_cast<size_t>(hh) * DH;
@@ -202,25 +207,28 @@ egt_status enqueue_step(egt_decoder* dd) {
     lin(w[2], dd->h, dd->v, nullptr, EGT_INPUT_RMSNORM, EGT_SPMV_INDEPENDENT, w[3]);
     float* kc = dd->kc + static_cast<size_t>(l) * dd->max_len * d;
     float* vc = dd->vc + static_cast<size_t>(l) * dd->max_len * d;
-    switch (dh) {
-      case 16:
-        dec_attention_kernel<16><<<H, 256, attn_smem, s>>>(dd->state, dd->q, dd->k, dd->v, kc, vc, dd->o,
-                                                           static_cast<int>(d), scale);
-        break;
-      case 32:
-        dec_attention_kernel<32><<<H, 256, attn_smem, s>>>(dd->state, dd->q, dd->k, dd->v, kc, vc, dd->o,
-                                                           static_cast<int>(d), scale);
-        break;
-      case 64:
-        dec_attention_kernel<64><<<H, 256, attn_smem, s>>>(dd->state, dd->q, dd->k, dd->v, kc, vc, dd->o,
-                                                           static_cast<int>(d), scale);
-        break;
-      case 128:
-        dec_attention_kernel<128><<<H, 256, attn_smem, s>>>(dd->state, dd->q, dd->k, dd->v, kc, vc, dd->o,
-                                                            static_cast<int>(d), scale);
-        break;
-      default:
-        return dfail(EGT_EINVAL, "decoder: head dimension must be 16, 32, 64 or 128");
+    {
+      void* fn = dh == 16 ? reinterpret_cast<void*>(&dec_attention_kernel<16>)
+               : dh == 32 ? reinterpret_cast<void*>(&dec_attention_kernel<32>)
+               : dh == 64 ? reinterpret_cast<void*>(&dec_attention_kernel<64>)
+                          : reinterpret_cast<void*>(&dec_attention_kernel<128>);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(H);
+      cfg.blockDim = dim3(256);
+      cfg.dynamicSmemBytes = attn_smem;
+      cfg.stream = s;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      const int32_t* st_ = dd->state;
+      const float *q_ = dd->q, *k_ = dd->k, *v_ = dd->v;
+      float* o_ = dd->o;
+      int d_ = static_cast<int>(d);
+      float sc_ = scale;
+      void* args[] = {&st_, &q_, &k_, &v_, &kc, &vc, &o_, &d_, &sc_};
+      DCUDA(cudaLaunchKernelExC(&cfg, fn, args));
     }
     ++launch_counter();
     lin(w[3], dd->o, dd->h, dd->h, EGT_INPUT_NONE, 0, w[4]);
