@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 
 #include "device_common.cuh"
@@ -273,18 +274,20 @@ cudaError_t launch_wide(const egt_dev_packed* h, const float* x, int ldx, int M,
   while (RB > kWideNW && static_cast<long long>((RT + RB - 1) / RB) * TB < num_sms) RB -= kWideNW;
   while (RB > 1 && static_cast<long long>((RT + RB - 1) / RB) * TB < num_sms && RB > 1) --RB;
   a.RB = RB;
-  // A consumer warp holds its two row tiles' stages of one chunk at once
-  // (nw stages apart), so the weight ring needs > nw stages or the producer
-  // could wait on a stage held by the warp waiting for it.
+  // Consumer warps hold up to two row tiles' stages of one chunk at once, so
+  // the weight ring must cover a whole chunk (NSTW >= RB): then issuing chunk
+  // c only ever waits for stages of chunk c - 1, which complete unconditionally.
   const int blk = 32 * (val_lane_bytes(fmt) + meta_lane_bytes(fmt)) + (has_scales(fmt) ? E * 80 : 0);
-  for (a.CH = 4;; a.CH /= 2) {
+  static const int ch0 = getenv("EGT_WIDE_CH") ? atoi(getenv("EGT_WIDE_CH")) : 4;
+  static const int cap = getenv("EGT_WIDE_NSTW") ? atoi(getenv("EGT_WIDE_NSTW")) : 32;
+  for (a.CH = std::max(1, ch0);; a.CH /= 2) {
     a.wstage_bytes = (a.CH * blk + 127) / 128 * 128;
     a.xstage_bytes = 4 * a.CH * 4 * 512;
     const int budget = 200 * 1024 - 2 * a.xstage_bytes - 1024;
-    a.NSTW = std::min(32, budget / a.wstage_bytes);
-    if (a.NSTW > kWideNW || a.CH == 1) break;
+    a.NSTW = std::min(std::max(cap, RB), budget / a.wstage_bytes);
+    if (a.NSTW >= RB || a.CH == 1) break;
   }
-  if (a.NSTW <= kWideNW) return cudaErrorInvalidConfiguration;
+  if (a.NSTW < RB) return cudaErrorInvalidConfiguration;
   const size_t smem = (16 * (4 + 2 * a.NSTW) + 127) / 128 * 128 + 2 * static_cast<size_t>(a.xstage_bytes) +
                       static_cast<size_t>(a.NSTW) * a.wstage_bytes;
   void* fn = pick_wide(fmt, h->tiled.SS);

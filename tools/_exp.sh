@@ -1,4 +1,4 @@
-python -m pytest tests/test_gpu_verify.py -q --timeout 300 -p no:cacheprovider -x 2>&1 | tail -1
-export EGT_BENCH_NO_VERIFY=1
-python tools/decode_probe.py int4-2:4 2>&1 | grep -v Warn
-python tools/decode_probe.py int4-2:4 2>&1 | grep -v Warn
+for cfg in "4 32" "2 64" "2 96" "4 48" "1 128" "8 32"; do
+  set -- $cfg
+  echo CH=$1 NSTW=$2 $(EGT_WIDE_CH=$1 EGT_WIDE_NSTW=$2 python tools/verify_probe.py 80 8 2>&1 | grep M=) $(EGT_WIDE_CH=$1 EGT_WIDE_NSTW=$2 python tools/verify_probe.py 272 8 2>&1 | grep M=)
+done
