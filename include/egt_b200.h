@@ -148,6 +148,9 @@ EGT_API egt_status egt_spmv(const egt_dev_packed* h, const float* x_dev, float* 
  * overlap that kernel entirely (it still completes after it).  Typical use:
  * the Q, K, V (or gate/up) products of one decode step. */
 #define EGT_SPMV_INDEPENDENT 1u
+/* egt_spmv_fused: apply silu (model.cpp:80-84) to the output instead of the
+ * next product applying it to its input (each element once, not per CTA). */
+#define EGT_SPMV_OUTPUT_SILU 2u
 /* Input transforms of fused products (egt_spmv_fused, programs). */
 #define EGT_INPUT_NONE 0u
 #define EGT_INPUT_RMSNORM 1u /* x / sqrt(mean(x^2) + eps) over the whole vector */

@@ -449,6 +449,7 @@ egt_status spmv_impl(const egt_dev_packed* h, const float* x, float* y, uint32_t
   ctx.res = res;
   ctx.ldr = static_cast<int>(M > 1 ? ldr : h->rows);
   ctx.l2_next = l2_next;
+  ctx.out_silu = (flags & EGT_SPMV_OUTPUT_SILU) != 0 ? 1 : 0;
   if (h->cols == 0) {
     for (uint32_t m = 0; m < M; ++m) {
       float* ym = y + static_cast<size_t>(m) * ldy;
@@ -461,14 +462,14 @@ egt_status spmv_impl(const egt_dev_packed* h, const float* x, float* y, uint32_t
     return EGT_OK;
   }
   if (h->path == EGT_PATH_GENERAL) {
-    if (res || input != EGT_INPUT_NONE)
+    if (res || input != EGT_INPUT_NONE || ctx.out_silu)
       return fail(EGT_EINVAL, "spmv: fused input transforms / residual need the tiled path (group sizes % 32 == 0)");
     CUDA_TRY(launch_general(h, x, static_cast<int>(ldx), static_cast<int>(M), y,
                             static_cast<int>(ldy), ctx));
     return EGT_OK;
   }
   static const bool no_wide = getenv("EGT_NO_WIDE") != nullptr;  // tuning: old M > 16 path
-  if (M > 16 && !res && input == EGT_INPUT_NONE && !no_wide && !plan_forced()) {
+  if (M > 16 && !res && input == EGT_INPUT_NONE && !ctx.out_silu && !no_wide && !plan_forced()) {
     Workspace* w = nullptr;
     egt_status st = get_workspace(s, (wide_workspace_bytes(h, static_cast<int>(M)) + 3) / 4, 0, &w);
     if (st != EGT_OK) return st;

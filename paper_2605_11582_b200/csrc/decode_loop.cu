@@ -232,8 +232,8 @@ egt_status enqueue_step(egt_decoder* dd) {
     }
     ++launch_counter();
     lin(w[3], dd->o, dd->h, dd->h, EGT_INPUT_NONE, 0, w[4]);
-    lin(w[4], dd->h, dd->f, nullptr, EGT_INPUT_RMSNORM, 0, w[5]);
-    lin(w[5], dd->f, dd->h, dd->h, EGT_INPUT_SILU, 0, next_q);
+    lin(w[4], dd->h, dd->f, nullptr, EGT_INPUT_RMSNORM, EGT_SPMV_OUTPUT_SILU, w[5]);  // f = silu(ff1 b)
+    lin(w[5], dd->f, dd->h, dd->h, EGT_INPUT_NONE, 0, next_q);
   }
   lin(m->head, dd->h, dd->logits, nullptr, EGT_INPUT_RMSNORM, 0, m->layers[0]);
   if (st != EGT_OK) return st;

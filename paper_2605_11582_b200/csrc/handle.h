@@ -86,6 +86,7 @@ struct LaunchCtx {
   float* partial = nullptr;      // split-K partial sums
   uint32_t* counters = nullptr;  // split-K arrival counters (self-resetting)
   int xform = 0;                 // EGT_INPUT_* applied to x while staging
+  int out_silu = 0;              // EGT_SPMV_OUTPUT_SILU: y = silu(...)
   float eps = 1e-6f;
   const float* res = nullptr;    // y = res + product (may alias y)
   int ldr = 0;

@@ -50,6 +50,7 @@ struct TiledArgs {
   float eps;
   const float* res;
   int ldr;
+  int out_silu;  // y = silu(res + product): the producer applies the next product's input transform
   // L2 prefetch of the NEXT product's weights (decode chains): each CTA
   // requests its share of the four storage arrays while this product runs
   const uint8_t* pf_ptr[4];
@@ -365,9 +366,11 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
     const int row = (rt0 + i) * 16 + row16;
     const int tok = m0 + tl;
     if (row < a.rows) {
-      if (a.S == 1)
-        a.y[static_cast<size_t>(tok) * a.ldy + row] =
-            (FUSED && a.res ? (idx == tid ? res_pre : a.res[static_cast<size_t>(tok) * a.ldr + row]) : 0.f) + v;
+      if (a.S == 1) {
+        float o = (FUSED && a.res ? (idx == tid ? res_pre : a.res[static_cast<size_t>(tok) * a.ldr + row]) : 0.f) + v;
+        if (FUSED && a.out_silu) o = o * (1.0f / (1.0f + expf(-o)));  // model.cpp:80-84
+        a.y[static_cast<size_t>(tok) * a.ldy + row] = o;
+      }
       else
         a.partial[(static_cast<size_t>(blockIdx.y) * a.M + tok) * rows_pad + row] = v;
     }
@@ -393,7 +396,9 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
       float v = 0.f;
       for (int sidx = 0; sidx < a.S; ++sidx)
         v += __ldcg(a.partial + (static_cast<size_t>(sidx) * a.M + tok) * rows_pad + row);
-      a.y[static_cast<size_t>(tok) * a.ldy + row] = (FUSED && a.res ? a.res[static_cast<size_t>(tok) * a.ldr + row] : 0.f) + v;
+      float o = (FUSED && a.res ? a.res[static_cast<size_t>(tok) * a.ldr + row] : 0.f) + v;
+      if (FUSED && a.out_silu) o = o * (1.0f / (1.0f + expf(-o)));
+      a.y[static_cast<size_t>(tok) * a.ldy + row] = o;
     }
   }
   if (tid == 0) a.counters[cidx] = 0u;  // ready for the next launch / graph replay
@@ -532,7 +537,7 @@ TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms, bool indep
         const double t_mem = ctas_per_sm * bytes_cta / sm_bw;
         const double units_per_warp = RB * std::ceil(static_cast<double>(KC) / nw);
         const double t_issue = ctas_per_sm * units_per_warp * unit_cycles * std::max(1.0, nw / 4.0) / 1.9;
-        const double t_tail = (S > 1 ? 900.0 : 0.0) + 0.3 * (t_mem / ctas_per_sm) + (nst < NQ ? 300.0 : 0.0);
+        const double t_tail = (S > 1 ? 2500.0 : 0.0) + 0.3 * (t_mem / ctas_per_sm) + (nst < NQ ? 300.0 : 0.0);
         const double cost = std::max(t_mem, t_issue) + t_tail + ctas_per_sm * 600.0;
         if (cost < best_cost * 0.999) {
           best_cost = cost;
@@ -599,6 +604,7 @@ cudaError_t launch_tiled(const egt_dev_packed* h, const TiledSchedule& sc, const
     }
   }
   a.xform = ctx.xform;
+  a.out_silu = ctx.out_silu;
   a.eps = ctx.eps;
   a.res = ctx.res;
   a.ldr = ctx.ldr;
@@ -627,7 +633,7 @@ cudaError_t launch_tiled(const egt_dev_packed* h, const TiledSchedule& sc, const
   static const int dbg = getenv("EGT_DEBUG_MODE") ? atoi(getenv("EGT_DEBUG_MODE")) : 0;
   a.dbg = dbg;
   a.indep = indep && sc.S == 1 ? 1 : 0;
-  void* fn = pick_kernel(h->format, h->tiled.SS, M == 1 ? 0 : sc.NT, a.xform != 0 || a.res != nullptr || a.pf_ptr[0]);
+  void* fn = pick_kernel(h->format, h->tiled.SS, M == 1 ? 0 : sc.NT, a.xform != 0 || a.res != nullptr || a.pf_ptr[0] || a.out_silu);
   cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(sc.smem));
   if (err != cudaSuccess) return err;

@@ -233,7 +233,8 @@ class DeviceMatrix:
                                 1 if independent else 0, _stream_ptr(stream)))
 
     def spmv_fused_into(self, x, y, residual=None, input: int = 0, eps: float = 1e-6, stream=None,
-                        independent: bool = False, l2_next: "DeviceMatrix | None" = None) -> None:
+                        independent: bool = False, l2_next: "DeviceMatrix | None" = None,
+                        output_silu: bool = False) -> None:
         """y = residual + f(x) @ W^T with f = identity / rmsnorm (per token) /
         silu (N.INPUT_*): the forward_impl glue (model.cpp:155-190) fused into
         the product.  residual may be y itself."""
@@ -246,7 +247,7 @@ class DeviceMatrix:
             rp = residual.data_ptr()
             ldr = residual.shape[-1] if residual.dim() == 1 else residual.stride(0)
         check(lib().egt_spmv_fused(self._h, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), M, ldx, ldy,
-                                   rp, ldr, input, eps, 1 if independent else 0,
+                                   rp, ldr, input, eps, (1 if independent else 0) | (2 if output_silu else 0),
                                    l2_next.handle if l2_next is not None else None, _stream_ptr(stream)))
 
     def spmv(self, x, stream=None):

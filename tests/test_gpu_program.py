@@ -228,3 +228,18 @@ def test_spmv_fused_transforms(egt, port, torch, M, shape):
             want = rs[m] + port.spmv(p, f(xs[m]))
             ok, err = close(got[m], want)
             assert ok, f"mode {mode} token {m}: {err:.3e}"
+
+
+def test_spmv_fused_output_silu(egt, port, torch):
+    """EGT_SPMV_OUTPUT_SILU: y = silu(W rmsnorm(x)) -- the ff1 product of the
+    decode step applying ff2's input transform once per element."""
+    from paper_2605_11582_b200.native import INPUT_RMSNORM
+
+    rng = np.random.default_rng(61)
+    p = make_int4(rng, 2816, 1024, 2, 128, port)[0]
+    d = _dev(egt, p)
+    x = rng.uniform(-2, 2, 1024).astype(np.float32)
+    y = torch.empty(2816, device="cuda")
+    d.spmv_fused_into(_cuda(torch, x), y, input=INPUT_RMSNORM, output_silu=True)
+    ok, err = close(y.cpu().numpy(), silu32(port.spmv(p, rmsnorm32(x))))
+    assert ok, err

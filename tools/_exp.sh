@@ -1,4 +1,6 @@
-for cfg in "4 32" "2 64" "2 96" "4 48" "1 128" "8 32"; do
-  set -- $cfg
-  echo CH=$1 NSTW=$2 $(EGT_WIDE_CH=$1 EGT_WIDE_NSTW=$2 python tools/verify_probe.py 80 8 2>&1 | grep M=) $(EGT_WIDE_CH=$1 EGT_WIDE_NSTW=$2 python tools/verify_probe.py 272 8 2>&1 | grep M=)
+export EGT_BENCH_NO_VERIFY=1
+for v in t900 t2500; do
+  export EGT_LIB_PATH=$PWD/_variants/lib_$v.so
+  echo $v $(python tools/decode_probe.py int4-2:4 2>&1 | grep plan) $(python tools/decode_probe.py mixed-int4dense-fp16sp24 2>&1 | grep plan)
+  python bench.py --steps 300 --no-cpu --no-decode --no-sharded 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('$v', d['value'], d['config']['dependent_chain'])"
 done

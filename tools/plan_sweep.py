@@ -45,6 +45,7 @@ def main():
     ap.add_argument("--shapes", default="4096x4096,11008x4096,4096x11008")
     ap.add_argument("--n", type=int, default=2)
     ap.add_argument("--indep", action="store_true", help="EGT_SPMV_INDEPENDENT launches")
+    ap.add_argument("--quick", action="store_true", help="dependent sweep over S in {1, 2} only")
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "plan_sweep.json"))
     args = ap.parse_args()
     rng = np.random.default_rng(7)
@@ -63,12 +64,12 @@ def main():
         L.egt_tune_force_plan(0, 0, 0, 0, 0)
         t = time_plan(layers, x, ys, stream, indep=args.indep)
         res.append({"plan": "auto", "us": t, "GBps": shape_bytes(p) / t / 1e3})
-        for S in ((1,) if args.indep else (1, 2, 3, 4, 6, 8)):
+        for S in ((1,) if args.indep else ((1, 2) if args.quick else (1, 2, 3, 4, 6, 8))):
             if S > KQ:
                 continue
-            for ctas in ((24, 32, 48, 64, 96, 148) if args.indep else (74, 148, 296)):
+            for ctas in ((24, 32, 48, 64, 96, 148) if args.indep else (74, 128, 148, 296)):
                 RB = max(1, math.ceil(RT * S / ctas))
-                for nw, ch in (((8, 0), (8, 16), (8, 32), (12, 24)) if args.indep else ((4, 0), (8, 0))):
+                for nw, ch in (((8, 0), (8, 16), (8, 32), (12, 24)) if args.indep else ((4, 0), (8, 0), (12, 0), (12, 24))):
                     L.egt_tune_force_plan(RB, S, nw, 0, ch)
                     try:
                         t = time_plan(layers, x, ys, stream, indep=args.indep)
