@@ -348,6 +348,27 @@ EGT_API egt_status egt_program_destroy(egt_program* p);
  * ready, [8192,12288) consumer done, [12288,16384) epilogue segment start. */
 EGT_API egt_status egt_program_debug_trace(const egt_program* p, long long* host, size_t n);
 
+/* ---------------- EGTQ compressed-model files -> device layers ------------
+ * parse_compressed (egtq_io.cpp:221-235, read_layer :110-210) with the
+ * reference's checks and FormatError messages ("<context>: ..."); upload is
+ * the mixed dispatch on the layer's (pattern, storage) keys without
+ * re-packing: the file's kept INT4 codes are the device stream's value bytes
+ * and its (verified) index section the index words.  Dense fp layers are not
+ * on the SparseGemv path (EGT_EINVAL). */
+typedef struct egt_egtq egt_egtq;
+typedef struct egt_egtq_layer_info {
+  const char* name;          /* valid while the egt_egtq lives */
+  uint8_t pattern;           /* SparsityPattern: 0 dense, 1 one-of-four, 2 two-of-four */
+  uint8_t has_quant;         /* 1 INT4 codes + group tables, 0 fp values */
+  uint8_t has_index;         /* the file carried the 2bit-CSR index section */
+  uint32_t rows, cols;
+} egt_egtq_layer_info;
+EGT_API egt_status egt_egtq_parse(const uint8_t* bytes, size_t n, const char* context, egt_egtq** out);
+EGT_API uint32_t egt_egtq_layer_count(const egt_egtq* e);
+EGT_API egt_status egt_egtq_query(const egt_egtq* e, uint32_t i, egt_egtq_layer_info* info);
+EGT_API egt_status egt_egtq_upload(const egt_egtq* e, uint32_t i, void* stream, egt_dev_packed** out);
+EGT_API egt_status egt_egtq_destroy(egt_egtq* e);
+
 /* ---------------- host encoder (C++; byte-identical to the reference) ----
  * Masks are PruneMask bitmaps (bit r*cols+c, LSB-first). */
 

@@ -359,6 +359,39 @@ class Oracle:
         finally:
             L.ref_packed_free(h)
 
+    def ref_egtq_serialize(self, layers: list) -> bytes:
+        """serialize_compressed (egtq_io.cpp:212-219) of layers given as dicts
+        {name, pattern (0 dense, 1 1:4, 2 2:4), quant (bool), w [rows x cols]
+        f32, mask (bitmap or None), group}."""
+        assert self.which == "reference"
+        n = len(layers)
+        names = (C.c_char_p * n)(*[l["name"].encode() for l in layers])
+        pats = (C.c_uint8 * n)(*[l["pattern"] for l in layers])
+        quant = (C.c_uint8 * n)(*[1 if l["quant"] else 0 for l in layers])
+        rows = (C.c_uint32 * n)(*[l["w"].shape[0] for l in layers])
+        cols = (C.c_uint32 * n)(*[l["w"].shape[1] for l in layers])
+        ws = [np.ascontiguousarray(l["w"], np.float32) for l in layers]
+        ms = [None if l.get("mask") is None else np.ascontiguousarray(l["mask"], np.uint8) for l in layers]
+        wp = (_f32p * n)(*[_ptr(w, _f32p) for w in ws])
+        mp = (_u8p * n)(*[_ptr(m, _u8p) if m is not None else _u8p() for m in ms])
+        groups = (C.c_uint32 * n)(*[l.get("group", 32) for l in layers])
+        cap = sum(w.size * 6 for w in ws) + 4096
+        buf = np.zeros(cap, np.uint8)
+        ln = C.c_size_t()
+        self.lib.ref_egtq_serialize.restype = C.c_int
+        self._check(self.lib.ref_egtq_serialize(n, names, pats, quant, rows, cols, wp, mp, groups, _ptr(buf, _u8p),
+                                                C.c_size_t(cap), C.byref(ln)))
+        return bytes(buf[: ln.value])
+
+    def ref_egtq_parse(self, data: bytes) -> int:
+        """parse_compressed (egtq_io.cpp:221-235): layer count or OracleError."""
+        assert self.which == "reference"
+        arr = np.frombuffer(data, np.uint8).copy() if data else np.zeros(1, np.uint8)
+        n = C.c_uint32()
+        self.lib.ref_egtq_parse.restype = C.c_int
+        self._check(self.lib.ref_egtq_parse(_ptr(arr, _u8p), C.c_size_t(len(data)), C.byref(n)))
+        return n.value
+
     def ref_bench_spmv(self, rows: int, cols: int, reps: int, seed: int):
         assert self.which == "reference"
         med = (C.c_uint64 * 4)()

@@ -253,4 +253,50 @@ int ref_spmv_timed(void* h, const float* x, size_t x_len, int calls, int threads
   });
 }
 
+// EGTQ files written by the reference's own serialize_compressed
+// (egtq_io.cpp:212-219): layer i has name names[i], pattern patterns[i]
+// (0 dense, 1 one-of-four, 2 two-of-four), storage quant[i]; weights w[i]
+// (rows x cols), keep bitmap masks[i] (NULL for dense) and uniform group size
+// groups[i] (quantize_matrix with the mask, compress.cpp:157-197).
+int ref_egtq_serialize(int n_layers, const char* const* names, const uint8_t* patterns, const uint8_t* quant,
+                       const uint32_t* rows, const uint32_t* cols, const float* const* w,
+                       const uint8_t* const* masks, const uint32_t* groups, uint8_t* out, size_t cap,
+                       size_t* len) {
+  return guarded([&] {
+    egt::CompressedModel model;
+    for (int i = 0; i < n_layers; ++i) {
+      egt::CompressedLayer L;
+      L.name = names[i];
+      L.pattern = static_cast<egt::SparsityPattern>(patterns[i]);
+      L.has_quant = quant[i] != 0;
+      L.mask = masks[i] ? make_mask(masks[i], rows[i], cols[i]) : egt::PruneMask::all_kept(rows[i], cols[i]);
+      egt::Matrix m = make_matrix(w[i], rows[i], cols[i]);
+      if (L.has_quant) {
+        egt::GroupQuantSpec spec;
+        spec.group_sizes.assign(rows[i], groups[i]);
+        L.quant = masks[i] ? egt::quantize_matrix(m, spec, L.mask) : egt::quantize_matrix(m, spec);
+      } else {
+        L.dense_values = m;
+        for (uint32_t r = 0; r < rows[i]; ++r)
+          for (uint32_t c = 0; c < cols[i]; ++c)
+            if (!L.mask.at(r, c)) L.dense_values(r, c) = 0.0f;
+      }
+      model.layers.push_back(std::move(L));
+    }
+    const std::string bytes = egt::serialize_compressed(model);
+    *len = bytes.size();
+    if (bytes.size() > cap) throw std::invalid_argument("ref_egtq_serialize: buffer too small");
+    std::memcpy(out, bytes.data(), bytes.size());
+  });
+}
+
+// parse_compressed (egtq_io.cpp:221-235) on a byte buffer: layer count, or
+// the FormatError.
+int ref_egtq_parse(const uint8_t* bytes, size_t n, uint32_t* n_layers) {
+  return guarded([&] {
+    egt::CompressedModel m = egt::parse_compressed(std::string(reinterpret_cast<const char*>(bytes), n), "egtq");
+    *n_layers = static_cast<uint32_t>(m.layers.size());
+  });
+}
+
 }  // extern "C"

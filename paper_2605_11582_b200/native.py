@@ -103,6 +103,11 @@ class ProgramInfo(C.Structure):
 
 INPUT_NONE, INPUT_RMSNORM, INPUT_SILU = 0, 1, 2
 
+
+class EgtqLayerInfo(C.Structure):
+    _fields_ = [("name", C.c_char_p), ("pattern", C.c_uint8), ("has_quant", C.c_uint8), ("has_index", C.c_uint8),
+                ("rows", C.c_uint32), ("cols", C.c_uint32)]
+
 # every symbol include/egt_b200.h declares, with its signature
 SIGNATURES = {
     "egt_abi_version": (C.c_int, []),
@@ -161,6 +166,14 @@ _MODEL_SIGNATURES.update({
     "egt_decoder_step": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p]),
     "egt_decoder_read": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_uint32, u32p, C.c_void_p, C.c_void_p]),
     "egt_decoder_destroy": (C.c_int, [C.c_void_p]),
+})
+
+_MODEL_SIGNATURES.update({
+    "egt_egtq_parse": (C.c_int, [u8p, C.c_size_t, C.c_char_p, C.POINTER(C.c_void_p)]),
+    "egt_egtq_layer_count": (C.c_uint32, [C.c_void_p]),
+    "egt_egtq_query": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(EgtqLayerInfo)]),
+    "egt_egtq_upload": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.POINTER(C.c_void_p)]),
+    "egt_egtq_destroy": (C.c_int, [C.c_void_p]),
 })
 
 SIGNATURES.update(_MODEL_SIGNATURES)
