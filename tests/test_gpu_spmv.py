@@ -304,3 +304,26 @@ def test_many_token_dense_int4(egt, port, torch, M):
     for m in (0, M // 2, M - 1):
         ok, err = close(y[m], port.quant_dense_gemv(qo, xs[m]))
         assert ok, err
+
+
+@pytest.mark.parametrize("shape", [(5120, 13824), (8192, 28672)])
+def test_baseline_sharded_shapes_full_size(egt, port, torch, shape):
+    """BASELINE config[4] at full size: the unsharded product against the
+    oracle, and the 2/4/8-way row shards (parallel.RowShardPlan) reassembled
+    against the unsharded product (the all-gather is a concatenation)."""
+    from paper_2605_11582_b200.parallel import RowShardPlan
+
+    rows, cols = shape
+    rng = np.random.default_rng(rows)
+    p, _, _ = make_int4(rng, rows, cols, 2, 128, port)
+    d = _dev(egt, p)
+    x = rng.uniform(-1, 1, cols).astype(np.float32)
+    xt = torch.from_numpy(x).cuda()
+    full = d.spmv(xt).cpu().numpy()
+    ok, err = close(full, port.spmv(p, x))
+    assert ok, err
+    for G in (2, 4, 8):
+        plan = RowShardPlan.make(rows, G)
+        parts = [d.slice_rows(r0, r1).spmv(xt).cpu().numpy() for r0, r1 in plan.bounds]
+        ok, err = close(np.concatenate(parts), full, 1e-5)
+        assert ok, (G, err)
