@@ -192,6 +192,11 @@ EGT_API void egt_set_pdl(int enabled);
  * this thread (row tiles per CTA, K splits, consumer warps, stage depth,
  * k-quads per stage; 0 = automatic for that field, rb = 0 restores the
  * automatic planner).  Used by tools/plan_sweep.py. */
+/* Tuning hook: with EGT_TILED_TRACE set, every SparseGemv launch stamps
+ * globaltimer ns into slot (launch index % 4096) x 8: CTA-0 start, past the
+ * PDL wait, x staged, compute done, last CTA exit, ~first CTA start.  Copies
+ * n values out (and zeroes the buffer if reset); nonzero if tracing is off. */
+EGT_API int egt_tune_read_trace(unsigned long long* host, size_t n, int reset);
 EGT_API void egt_tune_force_plan(int rb, int s, int nw, int nst, int ch);
 
 /* Number of kernels the library has launched on this thread (a counter the

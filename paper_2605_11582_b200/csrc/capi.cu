@@ -268,6 +268,14 @@ const char* egt_last_error(void) { return g_err.c_str(); }
 void egt_set_pdl(int enabled) { g_pdl = enabled != 0; }
 uint64_t egt_launch_count(void) { return launch_counter(); }
 void egt_tune_force_plan(int rb, int s, int nw, int nst, int ch) { force_plan(rb, s, nw, nst, ch); }
+int egt_tune_read_trace(unsigned long long* host, size_t n, int reset) {
+  unsigned long long* b = tiled_trace_buffer();
+  if (!b) return 1;
+  n = std::min<size_t>(n, 8 * 4096);
+  if (cudaMemcpy(host, b, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost) != cudaSuccess) return 2;
+  if (reset) cudaMemset(b, 0, sizeof(unsigned long long) * 8 * 4096);
+  return 0;
+}
 
 egt_status egt_dev_packed_create(const egt_packed_view* v, void* stream, egt_dev_packed** out) {
   using namespace egt_fmt;

@@ -121,5 +121,6 @@ cudaError_t launch_relayout(const RawStream& raw, int format, uint32_t rows, uin
 cudaError_t launch_dequant(const egt_dev_packed* h, float* w, uint8_t* mask, cudaStream_t s);
 
 uint64_t& launch_counter();
+unsigned long long* tiled_trace_buffer();  // EGT_TILED_TRACE tuning stamps (or null)
 
 }  // namespace egt_impl

@@ -19,6 +19,9 @@
 #include "device_common.cuh"
 #include "handle.h"
 #include "tiled_compute.cuh"
+#ifndef EGT_XU
+#define EGT_XU 8
+#endif
 #include "egt_b200.h"
 
 #include <algorithm>
@@ -55,7 +58,18 @@ struct TiledArgs {
   // requests its share of the four storage arrays while this product runs
   const uint8_t* pf_ptr[4];
   uint32_t pf_bytes[4];
+  // tuning (EGT_TILED_TRACE): globaltimer stamps per launch slot:
+  // [0] CTA 0 start, [1] CTA 0 past the PDL wait, [2] CTA 0 x staged,
+  // [3] CTA 0 compute done, [4] last CTA exit (max), [5] ~first CTA start
+  unsigned long long* trace;
+  int trace_slot;
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;\n" : "=l"(t));
+  return t;
+}
 
 
 // silu (model.cpp:80-84) out of line: inlined 24x into the unrolled x
@@ -87,6 +101,13 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
   // EGT_SPMV_INDEPENDENT (inputs not written by the immediate predecessor)
   // safe in a chain of PDL launches.
   if (a.indep) pdl_launch_dependents();
+  unsigned long long* tr = a.trace ? a.trace + static_cast<size_t>(a.trace_slot) * 8 : nullptr;
+  const bool cta0 = blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0;
+  if (tr && threadIdx.x == 0) {
+    const unsigned long long t = gtimer();
+    if (cta0) tr[0] = t;
+    atomicMax(tr + 5, ~t);
+  }
   if (a.dbg == 1) {
     pdl_wait();
     return;
@@ -158,12 +179,18 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
     pdl_wait();
     pdl_launch_dependents();
   }
+  if (tr && cta0) tr[1] = gtimer();
+  if (a.dbg == 7) {  // tuning: touch x once (timed into tr[6]) before the real staging
+    float acc7 = 0.f;
+    for (int k = tid * 4; k < a.cols; k += blockDim.x * 4)
+      acc7 += __ldcg(reinterpret_cast<const float4*>(a.x + k)).x;
+    if (acc7 == 12345.f) a.y[0] = acc7;
+    __syncthreads();
+    if (tr && cta0) tr[6] = gtimer();
+  }
 
-  // x slice -> fp16 hi/lo B fragments sB[nt][kt][lane < LS][4]: token m's hi
-  // part is B column 2m (lanes 8m..8m+3), its rounding residual column 2m+1.
-  // Every load of a thread is issued before the first conversion (one L2
-  // round trip for up to XU items per thread), then converted and stored.
-  constexpr int XU = 24;
+  const bool bulk_x = false;  // (a TMA bulk copy of x measured slower than these loads)
+  constexpr int XU = EGT_XU;
   // rmsnorm (model.cpp:57-67): inv_m = 1 / sqrt(mean(x_m^2) + eps) over the
   // whole row of every token of this CTA, applied while converting
   __shared__ float s_inv[16];
@@ -192,7 +219,8 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
         v[u] = make_float2(0.f, 0.f);
         if (i < items) {
           const int k = (i >> 4) * 32 + 2 * ((i >> 2) & 3) + 8 * (i & 3);
-          if (k < a.cols) v[u] = make_float2(__ldg(xr + k), __ldg(xr + k + 1));
+          if (k < a.cols)
+            v[u] = bulk_x ? reinterpret_cast<const float2*>(sB)[k >> 1] : make_float2(__ldg(xr + k), __ldg(xr + k + 1));
         }
         ss = fmaf(v[u].x, v[u].x, fmaf(v[u].y, v[u].y, ss));
       }
@@ -251,16 +279,21 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
         float2 v[XU];
 #pragma unroll
         for (int u = 0; u < XU; ++u) {
-          const int i = i0 + tid + u * blockDim.x;
+          int i = i0 + tid + u * blockDim.x;
+          if (a.dbg == 6 && i < items) i = (i + static_cast<int>(blockIdx.x) * 208) % items;  // tuning: spread L2 lines
           v[u] = make_float2(0.f, 0.f);
           if (i < items) {
             const int k = (kq0 * 4 + (i >> 4)) * 32 + 2 * ((i >> 2) & 3) + 8 * (i & 3);
-            if (k < a.cols) v[u] = make_float2(__ldg(xr + k), __ldg(xr + k + 1));
+            if (k < a.cols)
+              v[u] = bulk_x ? reinterpret_cast<const float2*>(sB)[(k - kq0 * 128) >> 1]
+                            : make_float2(__ldg(xr + k), __ldg(xr + k + 1));
           }
         }
+        if (bulk_x) __syncthreads();  // in place: every raw value read before any fragment is written
 #pragma unroll
         for (int u = 0; u < XU; ++u) {
-          const int i = i0 + tid + u * blockDim.x;
+          int i = i0 + tid + u * blockDim.x;
+          if (a.dbg == 6 && i < items) i = (i + static_cast<int>(blockIdx.x) * 208) % items;
           if (i < items) {
             const int reg = i & 3, t = (i >> 2) & 3, kt = i >> 4;
             if (FUSED && a.xform == EGT_INPUT_RMSNORM) {
@@ -283,6 +316,7 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
     }
   }
   __syncthreads();
+  if (tr && cta0) tr[2] = gtimer();
 
   if (warp == nw) {
     // producer: refill each stage once all consumer warps released it
@@ -356,6 +390,7 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
     }
   }
   __syncthreads();
+  if (tr && cta0) tr[3] = gtimer();
 
   const int rows_pad = a.RT * 16;
   const int nOut = RBc * Mc * 16;
@@ -377,6 +412,7 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
   }
   if (a.S == 1) {
     if (a.indep) pdl_wait();
+    if (tr && threadIdx.x == 0) atomicMax(tr + 4, gtimer());
     return;
   }
 
@@ -579,9 +615,25 @@ size_t tiled_workspace_floats(const egt_dev_packed* h, const TiledSchedule& sc, 
   return static_cast<size_t>(sc.S) * M * h->tiled.RT * 16;
 }
 
+unsigned long long* tiled_trace_buffer() {
+  static unsigned long long* b = [] {
+    unsigned long long* p = nullptr;
+    if (getenv("EGT_TILED_TRACE")) {
+      cudaMalloc(&p, sizeof(unsigned long long) * 8 * 4096);
+      cudaMemset(p, 0, sizeof(unsigned long long) * 8 * 4096);
+    }
+    return p;
+  }();
+  return b;
+}
+
 cudaError_t launch_tiled(const egt_dev_packed* h, const TiledSchedule& sc, const float* x, int ldx,
                          int M, float* y, int ldy, const LaunchCtx& ctx, bool indep) {
   TiledArgs a;
+  unsigned long long* trace_buf = tiled_trace_buffer();
+  static int trace_next = 0;
+  a.trace = trace_buf;
+  a.trace_slot = trace_buf ? (trace_next++ % 4096) : 0;
   for (int r = 0; r < 4; ++r) {
     a.pf_ptr[r] = nullptr;
     a.pf_bytes[r] = 0;

@@ -128,6 +128,7 @@ SIGNATURES = {
     "egt_set_pdl": (None, [C.c_int]),
     "egt_launch_count": (C.c_uint64, []),
     "egt_tune_force_plan": (None, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]),
+    "egt_tune_read_trace": (C.c_int, [C.POINTER(C.c_ulonglong), C.c_size_t, C.c_int]),
     "egt_host_fit_group": (None, [f64p, C.c_size_t, f32p, u8p]),
     "egt_host_group_count": (C.c_size_t, [C.c_uint32, C.c_uint32, u32p]),
     "egt_host_quantize": (C.c_int, [f32p, C.c_uint32, C.c_uint32, u32p, u8p, u32p, f32p, u8p, u8p, szp]),

@@ -1,2 +1,5 @@
-python -m pytest tests/test_gpu_spmv.py -q -k "many or wide" --timeout 120 -p no:cacheprovider 2>&1 | tail -1
-for M in 80 272; do echo $(python tools/verify_probe.py $M 32 2>&1 | grep M=); done
+export EGT_BENCH_NO_VERIFY=1
+for v in xu4 xu6 xu8 xu4; do
+  export EGT_LIB_PATH=$PWD/_variants/lib_$v.so
+  echo $v $(python tools/decode_probe.py int4-2:4 2>&1 | grep plan) $(python bench.py --steps 300 --no-cpu --no-decode --no-sharded 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['config']['dependent_chain']['ms_per_step'])")
+done
