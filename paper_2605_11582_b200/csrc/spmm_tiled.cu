@@ -179,6 +179,7 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
     pdl_wait();
     pdl_launch_dependents();
   }
+  if (tr && a.dbg == 8) __syncthreads();  // tuning: all warps past the PDL wait before the stamp
   if (tr && cta0) tr[1] = gtimer();
   if (a.dbg == 7) {  // tuning: touch x once (timed into tr[6]) before the real staging
     float acc7 = 0.f;
@@ -204,11 +205,72 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
     if (row < a.rows) res_pre = a.res[static_cast<size_t>(m0 + tl) * a.ldr + row];
   }
   bool staged = false;
+  if constexpr (SINGLE) {
+    // One token: each thread loads contiguous float4s of the CTA's x slice
+    // (coalesced, trivial addressing) and scatters the two (k, k+1) pairs of
+    // each into their B-fragment slots: pair at window offset w of k-tile kt
+    // -> reg = w / 8, t = (w % 8) / 2.  rmsnorm's sum of squares comes from
+    // the same registers when the slice is the whole row.
+    const float* xb = a.x + static_cast<size_t>(m0) * a.ldx + kq0 * 128;
+    const int nwin = min(KTc * 32, a.cols - kq0 * 128);  // floats of x in this CTA's window
+    const int nf4 = KTc * 8;                             // float4s covering the window (zero past nwin)
+    constexpr int X4 = 4;
+    if (a.dbg != 3 && (reinterpret_cast<uintptr_t>(xb) & 15) == 0 && (nwin & 3) == 0 &&
+        nf4 <= X4 * static_cast<int>(blockDim.x) &&
+        (!FUSED || a.xform != EGT_INPUT_RMSNORM || (kq0 == 0 && nwin == a.cols))) {
+      float4 v[X4];
+      float ss = 0.f;
+#pragma unroll
+      for (int u = 0; u < X4; ++u) {
+        const int j = tid + u * static_cast<int>(blockDim.x);
+        v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (j < nf4 && 4 * j < nwin) v[u] = __ldg(reinterpret_cast<const float4*>(xb) + j);
+        ss = fmaf(v[u].x, v[u].x, fmaf(v[u].y, v[u].y, fmaf(v[u].z, v[u].z, fmaf(v[u].w, v[u].w, ss))));
+      }
+      float inv = 1.f;
+      if (FUSED && a.xform == EGT_INPUT_RMSNORM) {
+        ss = warp_sum(ss);
+        if (lane == 0) s_red[warp] = ss;
+        __syncthreads();
+        float tot = 0.f;
+        for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) tot += s_red[w];
+        inv = 1.0f / sqrtf(tot / static_cast<float>(a.cols) + a.eps);
+      }
+      auto pair = [](float p0, float p1) {
+        const __half h0 = __float2half_rn(p0), h1 = __float2half_rn(p1);
+        const __half l0 = __float2half_rn(p0 - __half2float(h0));
+        const __half l1 = __float2half_rn(p1 - __half2float(h1));
+        return make_uint2(static_cast<uint32_t>(__half_as_ushort(h0)) | (static_cast<uint32_t>(__half_as_ushort(h1)) << 16),
+                          static_cast<uint32_t>(__half_as_ushort(l0)) | (static_cast<uint32_t>(__half_as_ushort(l1)) << 16));
+      };
+#pragma unroll
+      for (int u = 0; u < X4; ++u) {
+        const int j = tid + u * static_cast<int>(blockDim.x);
+        if (j < nf4) {
+          float4 q = v[u];
+          if (FUSED && a.xform == EGT_INPUT_RMSNORM) {
+            q.x *= inv; q.y *= inv; q.z *= inv; q.w *= inv;
+          } else if (FUSED && a.xform == EGT_INPUT_SILU) {
+            const float2 q0 = silu2(make_float2(q.x, q.y)), q1 = silu2(make_float2(q.z, q.w));
+            q = make_float4(q0.x, q0.y, q1.x, q1.y);
+          }
+          const int kt = j >> 3, w = (j & 7) * 4, reg = w >> 3, t = (w & 7) >> 1;
+          uint32_t* row = sB + static_cast<size_t>(kt) * 32;
+          const uint2 a0 = pair(q.x, q.y), a1 = pair(q.z, q.w);
+          row[t * 4 + reg] = a0.x;
+          row[(4 + t) * 4 + reg] = a0.y;
+          row[(t + 1) * 4 + reg] = a1.x;
+          row[(5 + t) * 4 + reg] = a1.y;
+        }
+      }
+      staged = true;
+    }
+  }
   if constexpr (FUSED && SINGLE) {
     // one token, whole row in this CTA: a single pass -- the sum of squares
     // comes from the values loaded for the conversion (one L2 round trip)
     const int items = KTc * 16;
-    if (a.xform == EGT_INPUT_RMSNORM && kq0 == 0 && KTc * 32 >= a.cols &&
+    if (!staged && a.xform == EGT_INPUT_RMSNORM && kq0 == 0 && KTc * 32 >= a.cols &&
         items <= XU * static_cast<int>(blockDim.x)) {
       const float* xr = a.x + static_cast<size_t>(m0) * a.ldx;
       float2 v[XU];

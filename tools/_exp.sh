@@ -1,5 +1,7 @@
+python -m pytest tests -m gpu -q --timeout 300 -p no:cacheprovider 2>&1 | tail -1
 export EGT_BENCH_NO_VERIFY=1
-for v in xu4 xu6 xu8 xu4; do
+for v in old new old new; do
   export EGT_LIB_PATH=$PWD/_variants/lib_$v.so
+  echo $v $(python tools/chain_trace.py 4096x4096 24 2>&1 | tail -1)
   echo $v $(python tools/decode_probe.py int4-2:4 2>&1 | grep plan) $(python bench.py --steps 300 --no-cpu --no-decode --no-sharded 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['config']['dependent_chain']['ms_per_step'])")
 done
