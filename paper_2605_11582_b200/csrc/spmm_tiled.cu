@@ -216,19 +216,19 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
     const int nf4 = KTc * 8;                             // float4s covering the window (zero past nwin)
     constexpr int X4 = 4;
     if (a.dbg != 3 && (reinterpret_cast<uintptr_t>(xb) & 15) == 0 && (nwin & 3) == 0 &&
-        nf4 <= X4 * static_cast<int>(blockDim.x) &&
         (!FUSED || a.xform != EGT_INPUT_RMSNORM || (kq0 == 0 && nwin == a.cols))) {
-      float4 v[X4];
-      float ss = 0.f;
-#pragma unroll
-      for (int u = 0; u < X4; ++u) {
-        const int j = tid + u * static_cast<int>(blockDim.x);
-        v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (j < nf4 && 4 * j < nwin) v[u] = __ldg(reinterpret_cast<const float4*>(xb) + j);
-        ss = fmaf(v[u].x, v[u].x, fmaf(v[u].y, v[u].y, fmaf(v[u].z, v[u].z, fmaf(v[u].w, v[u].w, ss))));
-      }
+      const int per_pass = X4 * static_cast<int>(blockDim.x);
       float inv = 1.f;
       if (FUSED && a.xform == EGT_INPUT_RMSNORM) {
+        // the whole row: from the registers when one pass holds it, else a
+        // separate sum-of-squares pass
+        float ss = 0.f;
+        for (int j = tid; j < nf4; j += blockDim.x) {
+          if (4 * j < nwin) {
+            const float4 q = __ldg(reinterpret_cast<const float4*>(xb) + j);
+            ss = fmaf(q.x, q.x, fmaf(q.y, q.y, fmaf(q.z, q.z, fmaf(q.w, q.w, ss))));
+          }
+        }
         ss = warp_sum(ss);
         if (lane == 0) s_red[warp] = ss;
         __syncthreads();
@@ -243,24 +243,33 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
         return make_uint2(static_cast<uint32_t>(__half_as_ushort(h0)) | (static_cast<uint32_t>(__half_as_ushort(h1)) << 16),
                           static_cast<uint32_t>(__half_as_ushort(l0)) | (static_cast<uint32_t>(__half_as_ushort(l1)) << 16));
       };
+      for (int base = 0; base < nf4; base += per_pass) {
+        float4 v[X4];
 #pragma unroll
-      for (int u = 0; u < X4; ++u) {
-        const int j = tid + u * static_cast<int>(blockDim.x);
-        if (j < nf4) {
-          float4 q = v[u];
-          if (FUSED && a.xform == EGT_INPUT_RMSNORM) {
-            q.x *= inv; q.y *= inv; q.z *= inv; q.w *= inv;
-          } else if (FUSED && a.xform == EGT_INPUT_SILU) {
-            const float2 q0 = silu2(make_float2(q.x, q.y)), q1 = silu2(make_float2(q.z, q.w));
-            q = make_float4(q0.x, q0.y, q1.x, q1.y);
+        for (int u = 0; u < X4; ++u) {
+          const int j = base + tid + u * static_cast<int>(blockDim.x);
+          v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (j < nf4 && 4 * j < nwin) v[u] = __ldg(reinterpret_cast<const float4*>(xb) + j);
+        }
+#pragma unroll
+        for (int u = 0; u < X4; ++u) {
+          const int j = base + tid + u * static_cast<int>(blockDim.x);
+          if (j < nf4) {
+            float4 q = v[u];
+            if (FUSED && a.xform == EGT_INPUT_RMSNORM) {
+              q.x *= inv; q.y *= inv; q.z *= inv; q.w *= inv;
+            } else if (FUSED && a.xform == EGT_INPUT_SILU) {
+              const float2 q0 = silu2(make_float2(q.x, q.y)), q1 = silu2(make_float2(q.z, q.w));
+              q = make_float4(q0.x, q0.y, q1.x, q1.y);
+            }
+            const int kt = j >> 3, w = (j & 7) * 4, reg = w >> 3, t = (w & 7) >> 1;
+            uint32_t* row = sB + static_cast<size_t>(kt) * 32;
+            const uint2 a0 = pair(q.x, q.y), a1 = pair(q.z, q.w);
+            row[t * 4 + reg] = a0.x;
+            row[(4 + t) * 4 + reg] = a0.y;
+            row[(t + 1) * 4 + reg] = a1.x;
+            row[(5 + t) * 4 + reg] = a1.y;
           }
-          const int kt = j >> 3, w = (j & 7) * 4, reg = w >> 3, t = (w & 7) >> 1;
-          uint32_t* row = sB + static_cast<size_t>(kt) * 32;
-          const uint2 a0 = pair(q.x, q.y), a1 = pair(q.z, q.w);
-          row[t * 4 + reg] = a0.x;
-          row[(4 + t) * 4 + reg] = a0.y;
-          row[(t + 1) * 4 + reg] = a1.x;
-          row[(5 + t) * 4 + reg] = a1.y;
         }
       }
       staged = true;

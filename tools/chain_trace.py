@@ -27,6 +27,10 @@ s = torch.cuda.Stream()
 
 
 indep = len(sys.argv) > 3 and sys.argv[3] == "indep"
+for arg in sys.argv[3:]:
+    if arg.startswith("plan="):  # RB,S,nw[,NST,CH]
+        f = [int(v) for v in arg[5:].split(",")] + [0, 0]
+        lib().egt_tune_force_plan(f[0], f[1], f[2], f[3], f[4])
 ys = [torch.empty(rows, device="cuda") for _ in range(n)]
 
 
