@@ -73,7 +73,8 @@ __global__ void __launch_bounds__(256) dec_attention_kernel(const int32_t* state
                                                             float scale) {
   extern __shared__ float sc[];  // [t + 1] scores
   __shared__ float red[8];
-  __shared__ float part[DH];
+  __shared__ __align__(16) float qs[DH];
+  __shared__ float part[8][DH];
   // launched with programmatic serialization: let the O product start
   // streaming its weights now, wait for q/k/v before reading them
   egt_dev::pdl_launch_dependents();
@@ -84,20 +85,22 @@ __global__ void __launch_bounds__(256) dec_attention_kernel(const int32_t* state
   for (int i = tid; i < DH; i += blockDim.x) {
     kc[static_cast<size_t>(t) * d + base + i] = k[base + i];
     vc[static_cast<size_t>(t) * d + base + i] = v[base + i];
+    qs[i] = q[base + i];
   }
   __syncthreads();
-  constexpr int PER = DH >= 32 ? DH / 32 : 1;
-  const bool on = lane * PER < DH;
-  float qv[PER];
-#pragma unroll
-  for (int e = 0; e < PER; ++e) qv[e] = on ? q[base + lane * PER + e] : 0.f;
-  for (int i = warp; i < n; i += 8) {
-    const float* kr = kc + static_cast<size_t>(i) * d + base + lane * PER;
+  // scores: a thread per key, the key's head slice as float4 loads (all of a
+  // thread's loads in flight together); row t was just written by this block
+  static_assert(DH % 4 == 0, "head dimension multiple of 4");
+  for (int i = tid; i < n; i += blockDim.x) {
+    const float4* kr = reinterpret_cast<const float4*>(kc + static_cast<size_t>(i) * d + base);
     float dot = 0.f;
 #pragma unroll
-    for (int e = 0; e < PER; ++e) dot = on ? fmaf(qv[e], kr[e], dot) : dot;
-    dot = egt_dev::warp_sum(dot);
-    if (lane == 0) sc[i] = dot * scale;
+    for (int e = 0; e < DH / 4; ++e) {
+      const float4 kv = kr[e];
+      const float4 qv = reinterpret_cast<const float4*>(qs)[e];
+      dot = fmaf(qv.x, kv.x, fmaf(qv.y, kv.y, fmaf(qv.z, kv.z, fmaf(qv.w, kv.w, dot))));
+    }
+    sc[i] = dot * scale;
   }
   __syncthreads();
   float mx = -INFINITY;
@@ -120,14 +123,39 @@ __global__ void __launch_bounds__(256) dec_attention_kernel(const int32_t* state
   __syncthreads();
   z = 0.f;
   for (int w = 0; w < 8; ++w) z += red[w];
-  // o[dim] = sum_i p_i v_i[dim]: threads [0, DH) even keys, [DH, 2 DH) odd keys
-  const int dim = tid % DH, half = tid / DH;
-  float acc = 0.f;
-  if (half < 2)
-    for (int i = half; i < n; i += 2) acc = fmaf(sc[i], vc[static_cast<size_t>(i) * d + base + dim], acc);
-  if (half == 1) part[dim] = acc;
+  // o = sum_i p_i v_i: warp w takes keys w, w + 8, ..., lane l dims
+  // [l*PER, (l+1)*PER); four keys in flight; then the 8 warp partials
+  constexpr int PER = DH >= 32 ? DH / 32 : 1;
+  const bool on = lane * PER < DH;
+  float acc[PER];
+#pragma unroll
+  for (int e = 0; e < PER; ++e) acc[e] = 0.f;
+  if (on) {
+    int i = warp;
+    for (; i + 24 < n; i += 32) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const float p_ = sc[i + 8 * r];
+        const float* vr = vc + static_cast<size_t>(i + 8 * r) * d + base + lane * PER;
+#pragma unroll
+        for (int e = 0; e < PER; ++e) acc[e] = fmaf(p_, vr[e], acc[e]);
+      }
+    }
+    for (; i < n; i += 8) {
+      const float p_ = sc[i];
+      const float* vr = vc + static_cast<size_t>(i) * d + base + lane * PER;
+#pragma unroll
+      for (int e = 0; e < PER; ++e) acc[e] = fmaf(p_, vr[e], acc[e]);
+    }
+#pragma unroll
+    for (int e = 0; e < PER; ++e) part[warp][lane * PER + e] = acc[e];
+  }
   __syncthreads();
-  if (half == 0) o[base + dim] = (acc + part[dim]) / z;
+  for (int dim = tid; dim < DH; dim += blockDim.x) {
+    float sum = 0.f;
+    for (int w = 0; w < 8; ++w) sum += part[w][dim];
+    o[base + dim] = sum / z;
+  }
 }
 
 // next token: the prompt's while t + 1 is inside it, else argmax (ties ->
