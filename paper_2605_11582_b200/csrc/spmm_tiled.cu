@@ -219,14 +219,30 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
         (!FUSED || a.xform != EGT_INPUT_RMSNORM || (kq0 == 0 && nwin == a.cols))) {
       const int per_pass = X4 * static_cast<int>(blockDim.x);
       float inv = 1.f;
+      const bool one_pass = nf4 <= per_pass;
+      float4 v[X4];
+      if (one_pass) {  // every value in registers up front (rmsnorm reads them twice)
+#pragma unroll
+        for (int u = 0; u < X4; ++u) {
+          const int j = tid + u * static_cast<int>(blockDim.x);
+          v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+          if (j < nf4 && 4 * j < nwin) v[u] = __ldg(reinterpret_cast<const float4*>(xb) + j);
+        }
+      }
       if (FUSED && a.xform == EGT_INPUT_RMSNORM) {
         // the whole row: from the registers when one pass holds it, else a
         // separate sum-of-squares pass
         float ss = 0.f;
-        for (int j = tid; j < nf4; j += blockDim.x) {
-          if (4 * j < nwin) {
-            const float4 q = __ldg(reinterpret_cast<const float4*>(xb) + j);
-            ss = fmaf(q.x, q.x, fmaf(q.y, q.y, fmaf(q.z, q.z, fmaf(q.w, q.w, ss))));
+        if (one_pass) {
+#pragma unroll
+          for (int u = 0; u < X4; ++u)
+            ss = fmaf(v[u].x, v[u].x, fmaf(v[u].y, v[u].y, fmaf(v[u].z, v[u].z, fmaf(v[u].w, v[u].w, ss))));
+        } else {
+          for (int j = tid; j < nf4; j += blockDim.x) {
+            if (4 * j < nwin) {
+              const float4 q = __ldg(reinterpret_cast<const float4*>(xb) + j);
+              ss = fmaf(q.x, q.x, fmaf(q.y, q.y, fmaf(q.z, q.z, fmaf(q.w, q.w, ss))));
+            }
           }
         }
         ss = warp_sum(ss);
@@ -244,12 +260,13 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
                           static_cast<uint32_t>(__half_as_ushort(l0)) | (static_cast<uint32_t>(__half_as_ushort(l1)) << 16));
       };
       for (int base = 0; base < nf4; base += per_pass) {
-        float4 v[X4];
+        if (!one_pass) {
 #pragma unroll
-        for (int u = 0; u < X4; ++u) {
-          const int j = base + tid + u * static_cast<int>(blockDim.x);
-          v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-          if (j < nf4 && 4 * j < nwin) v[u] = __ldg(reinterpret_cast<const float4*>(xb) + j);
+          for (int u = 0; u < X4; ++u) {
+            const int j = base + tid + u * static_cast<int>(blockDim.x);
+            v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (j < nf4 && 4 * j < nwin) v[u] = __ldg(reinterpret_cast<const float4*>(xb) + j);
+          }
         }
 #pragma unroll
         for (int u = 0; u < X4; ++u) {

@@ -92,7 +92,7 @@ class DeviceModel:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value and N._lib is not None:
+        if h is not None and h.value and N is not None and N._lib is not None:
             N._lib.egt_model_destroy(h)
             self._h = C.c_void_p()
 

@@ -209,7 +209,7 @@ class DeviceMatrix:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h is not None and h.value and N._lib is not None:
+        if h is not None and h.value and N is not None and N._lib is not None:
             N._lib.egt_dev_packed_destroy(h)
             self._h = C.c_void_p()
 
