@@ -171,6 +171,13 @@ EGT_API egt_status egt_spmv_fused(const egt_dev_packed* h, const float* x_dev, f
                                   uint32_t input, float eps, uint32_t flags, const egt_dev_packed* l2_next,
                                   void* stream);
 
+/* One launch over n <= 3 matrices of one shape sharing x (the decode step's
+ * Q, K, V): ys[i] = f(x) * W_i^T, M = 1, same transform / flags semantics as
+ * egt_spmv_fused (no residual).  rows must be a multiple of 16 when n > 1. */
+EGT_API egt_status egt_spmv_fused_multi(const egt_dev_packed* const* hs, uint32_t n, const float* x_dev,
+                                        float* const* ys_dev, uint32_t input, float eps, uint32_t flags,
+                                        void* stream);
+
 /* Same as egt_spmv with host buffers: H2D of x, the product, D2H of y, and a
  * stream synchronize.  x_len must equal cols (else EGT_EINVAL with the
  * reference's "spmv: input length differs from columns"). */

@@ -524,6 +524,48 @@ egt_status egt_spmv_ex(const egt_dev_packed* h, const float* x, float* y, uint32
   return spmv_impl(h, x, y, M, ldx, ldy, flags, nullptr, 0, EGT_INPUT_NONE, 0.f, nullptr, stream);
 }
 
+egt_status egt_spmv_fused_multi(const egt_dev_packed* const* hs, uint32_t n, const float* x, float* const* ys,
+                                uint32_t input, float eps, uint32_t flags, void* stream) {
+  if (!hs || !ys || n == 0 || n > 3) return fail(EGT_EINVAL, "spmv multi: 1 to 3 matrices");
+  const egt_dev_packed* h = hs[0];
+  if (!h || !x) return fail(EGT_EINVAL, "spmv multi: null argument");
+  for (uint32_t i = 0; i < n; ++i) {
+    const egt_dev_packed* g = hs[i];
+    if (!g || !ys[i]) return fail(EGT_EINVAL, "spmv multi: null argument");
+    if (g->path != EGT_PATH_TILED || g->rows != h->rows || g->cols != h->cols || g->format != h->format ||
+        g->tiled.KQ != h->tiled.KQ || g->tiled.SS != h->tiled.SS)
+      return fail(EGT_EINVAL, "spmv multi: matrices must share shape, format and group layout on the tiled path");
+  }
+  if (n > 1 && h->rows % 16 != 0) return fail(EGT_EINVAL, "spmv multi: rows must be a multiple of 16");
+  if (input > EGT_INPUT_SILU) return fail(EGT_EINVAL, "spmv: unknown input transform");
+  if (n == 1) return spmv_impl(h, x, ys[0], 1, h->cols, h->rows, flags, nullptr, 0, input, eps, nullptr, stream);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  LaunchCtx ctx;
+  ctx.stream = s;
+  ctx.pdl = g_pdl;
+  ctx.xform = static_cast<int>(input);
+  ctx.eps = eps;
+  ctx.out_silu = (flags & EGT_SPMV_OUTPUT_SILU) != 0 ? 1 : 0;
+  ctx.nseg = static_cast<int>(n);
+  for (uint32_t i = 0; i < n; ++i) {
+    ctx.segs[i] = hs[i];
+    ctx.seg_y[i] = ys[i];
+  }
+  const bool indep = (flags & EGT_SPMV_INDEPENDENT) != 0;
+  const TiledSchedule sc = plan_tiled_rt(h, h->tiled.RT * static_cast<int>(n), 1, num_sms(), indep);
+  if (sc.smem == 0) return fail(EGT_EINTERNAL, "spmv: no feasible launch plan for this shape and token count");
+  if (sc.S > 1) {
+    Workspace* w = nullptr;
+    egt_status st = get_workspace(s, static_cast<size_t>(sc.S) * h->tiled.RT * n * 16,
+                                  static_cast<size_t>(sc.grid_x) * sc.grid_z, &w);
+    if (st != EGT_OK) return st;
+    ctx.partial = w->partial;
+    ctx.counters = w->counters;
+  }
+  CUDA_TRY(launch_tiled(h, sc, x, static_cast<int>(h->cols), 1, ys[0], static_cast<int>(h->rows), ctx, indep));
+  return EGT_OK;
+}
+
 egt_status egt_spmv_fused(const egt_dev_packed* h, const float* x, float* y, uint32_t M, uint32_t ldx,
                           uint32_t ldy, const float* residual, uint32_t ldr, uint32_t input, float eps,
                           uint32_t flags, const egt_dev_packed* l2_next, void* stream) {

@@ -229,10 +229,18 @@ egt_status enqueue_step(egt_decoder* dd) {
   const size_t attn_smem = static_cast<size_t>(dd->max_len) * sizeof(float);
   for (uint32_t l = 0; l < c.n_layers && st == EGT_OK; ++l) {
     const egt_dev_packed* const* w = m->layers.data() + 6 * l;
+    const bool qkv_fused = getenv("EGT_DECODE_NO_QKV") == nullptr && w[0]->format == w[1]->format &&
+                           w[1]->format == w[2]->format && w[0]->tiled.SS == w[1]->tiled.SS &&
+                           w[1]->tiled.SS == w[2]->tiled.SS && w[0]->rows % 16 == 0;
     const egt_dev_packed* next_q = l + 1 < c.n_layers ? m->layers[6 * (l + 1)] : m->head;
-    lin(w[0], dd->h, dd->q, nullptr, EGT_INPUT_RMSNORM, 0, w[1]);
-    lin(w[1], dd->h, dd->k, nullptr, EGT_INPUT_RMSNORM, EGT_SPMV_INDEPENDENT, w[2]);
-    lin(w[2], dd->h, dd->v, nullptr, EGT_INPUT_RMSNORM, EGT_SPMV_INDEPENDENT, w[3]);
+    if (qkv_fused) {  // Q, K, V in one launch: one staging of rmsnorm(h), one wait
+      float* ys[3] = {dd->q, dd->k, dd->v};
+      if (st == EGT_OK) st = egt_spmv_fused_multi(w, 3, dd->h, ys, EGT_INPUT_RMSNORM, kNormEps, 0, s);
+    } else {
+      lin(w[0], dd->h, dd->q, nullptr, EGT_INPUT_RMSNORM, 0, w[1]);
+      lin(w[1], dd->h, dd->k, nullptr, EGT_INPUT_RMSNORM, EGT_SPMV_INDEPENDENT, w[2]);
+      lin(w[2], dd->h, dd->v, nullptr, EGT_INPUT_RMSNORM, EGT_SPMV_INDEPENDENT, w[3]);
+    }
     float* kc = dd->kc + static_cast<size_t>(l) * dd->max_len * d;
     float* vc = dd->vc + static_cast<size_t>(l) * dd->max_len * d;
     {

@@ -91,9 +91,13 @@ struct LaunchCtx {
   const float* res = nullptr;    // y = res + product (may alias y)
   int ldr = 0;
   const egt_dev_packed* l2_next = nullptr;  // weights to prefetch into L2 meanwhile
+  int nseg = 0;                             // > 1: one launch over several same-shape matrices
+  const egt_dev_packed* segs[3] = {nullptr, nullptr, nullptr};
+  float* seg_y[3] = {nullptr, nullptr, nullptr};
 };
 
 TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms, bool indep);
+TiledSchedule plan_tiled_rt(const egt_dev_packed* h, int RT, int M, int num_sms, bool indep);
 void force_plan(int RB, int S, int nw, int NST, int CH);  // tuning hook (0 = automatic)
 bool plan_forced();
 size_t tiled_workspace_floats(const egt_dev_packed* h, const TiledSchedule& sc, int M);

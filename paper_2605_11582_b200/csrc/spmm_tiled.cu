@@ -63,6 +63,15 @@ struct TiledArgs {
   // [3] CTA 0 compute done, [4] last CTA exit (max), [5] ~first CTA start
   unsigned long long* trace;
   int trace_slot;
+  // several matrices of one shape over the same x (decode Q/K/V): a virtual
+  // matrix of nseg * RTs row tiles; segment s reads seg_* and writes seg_y[s]
+  int nseg, RTs, rows_s;
+  const uint8_t* seg_vals[3];
+  const uint8_t* seg_meta[3];
+  const float* seg_scales[3];
+  const uint8_t* seg_zps[3];
+  float* seg_y[3];
+  int seg_rtb[3];
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -154,14 +163,27 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
   auto issue = [&](int s, int i, int c) {  // chunk (row tile i, k-quad chunk c) -> stage s
     const int CHc = min(CH, KCs - c * CH);
     uint8_t* st = stages + static_cast<size_t>(s) * sbytes;
-    const size_t blk = static_cast<size_t>(a.rt_begin + rt0 + i) * blk_stride + kq0 + c * CH;
+    const uint8_t* vals = a.vals;
+    const uint8_t* meta = a.meta;
+    const float* scales = a.scales;
+    const uint8_t* zps = a.zps;
+    int rtg = a.rt_begin + rt0 + i;
+    if (FUSED && a.nseg > 1) {
+      const int g = rt0 + i, sg = g / a.RTs;
+      vals = a.seg_vals[sg];
+      meta = a.seg_meta[sg];
+      scales = a.seg_scales[sg];
+      zps = a.seg_zps[sg];
+      rtg = a.seg_rtb[sg] + (g - sg * a.RTs);
+    }
+    const size_t blk = static_cast<size_t>(rtg) * blk_stride + kq0 + c * CH;
     mbar_expect_tx(full + s, stage_bytes<FMT>(CHc, E));
-    bulk_g2s(st, a.vals + blk * 32 * VB, CHc * 32 * VB, full + s, pol);
-    if constexpr (MB > 0) bulk_g2s(st + CHc * 32 * VB, a.meta + blk * 32 * MB, CHc * 32 * MB, full + s, pol);
+    bulk_g2s(st, vals + blk * 32 * VB, CHc * 32 * VB, full + s, pol);
+    if constexpr (MB > 0) bulk_g2s(st + CHc * 32 * VB, meta + blk * 32 * MB, CHc * 32 * MB, full + s, pol);
     if constexpr (has_scales(FMT)) {
       uint8_t* sp = st + CHc * 32 * (VB + MB);
-      bulk_g2s(sp, a.scales + blk * E * 16, CHc * E * 64, full + s, pol);
-      bulk_g2s(sp + CHc * E * 64, a.zps + blk * E * 16, CHc * E * 16, full + s, pol);
+      bulk_g2s(sp, scales + blk * E * 16, CHc * E * 64, full + s, pol);
+      bulk_g2s(sp + CHc * E * 64, zps + blk * E * 16, CHc * E * 16, full + s, pol);
     }
   };
   if (warp == nw && lane == 0) {
@@ -492,7 +514,12 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
       if (a.S == 1) {
         float o = (FUSED && a.res ? (idx == tid ? res_pre : a.res[static_cast<size_t>(tok) * a.ldr + row]) : 0.f) + v;
         if (FUSED && a.out_silu) o = o * (1.0f / (1.0f + expf(-o)));  // model.cpp:80-84
-        a.y[static_cast<size_t>(tok) * a.ldy + row] = o;
+        if (FUSED && a.nseg > 1) {
+          const int sg = row / a.rows_s;
+          a.seg_y[sg][static_cast<size_t>(tok) * a.ldy + (row - sg * a.rows_s)] = o;
+        } else {
+          a.y[static_cast<size_t>(tok) * a.ldy + row] = o;
+        }
       }
       else
         a.partial[(static_cast<size_t>(blockIdx.y) * a.M + tok) * rows_pad + row] = v;
@@ -522,7 +549,12 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
         v += __ldcg(a.partial + (static_cast<size_t>(sidx) * a.M + tok) * rows_pad + row);
       float o = (FUSED && a.res ? a.res[static_cast<size_t>(tok) * a.ldr + row] : 0.f) + v;
       if (FUSED && a.out_silu) o = o * (1.0f / (1.0f + expf(-o)));
-      a.y[static_cast<size_t>(tok) * a.ldy + row] = o;
+      if (FUSED && a.nseg > 1) {
+        const int sg = row / a.rows_s;
+        a.seg_y[sg][static_cast<size_t>(tok) * a.ldy + (row - sg * a.rows_s)] = o;
+      } else {
+        a.y[static_cast<size_t>(tok) * a.ldy + row] = o;
+      }
     }
   }
   if (tid == 0) a.counters[cidx] = 0u;  // ready for the next launch / graph replay
@@ -592,9 +624,14 @@ bool plan_forced() { return g_force[4] != 0; }
 
 static thread_local bool g_allow_waves = false;  // fallback: several CTAs per SM
 
+TiledSchedule plan_tiled_rt(const egt_dev_packed* h, int RT, int M, int num_sms, bool indep);
 TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms, bool indep) {
+  return plan_tiled_rt(h, h->tiled.RT, M, num_sms, indep);
+}
+
+TiledSchedule plan_tiled_rt(const egt_dev_packed* h, int RT, int M, int num_sms, bool indep) {
   TiledSchedule best;
-  const int RT = h->tiled.RT, KQ = h->tiled.KQ, E = h->tiled.E, f = h->format;
+  const int KQ = h->tiled.KQ, E = h->tiled.E, f = h->format;
   const int NT = M <= 4 ? 1 : (M <= 8 ? 2 : 4);
   const int NB = (M + 4 * NT - 1) / (4 * NT);
   const int tok = std::min(M, 4 * NT);
@@ -685,14 +722,14 @@ TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms, bool indep
   if (best_cost >= 1e300 && g_force[4]) {  // forced plan infeasible: automatic plan
     const int saved = g_force[4];
     g_force[4] = 0;
-    best = plan_tiled(h, M, num_sms, indep);
+    best = plan_tiled_rt(h, RT, M, num_sms, indep);
     g_force[4] = saved;
   } else if (best_cost >= 1e300 && indep) {  // no split-free plan fits: dependent plan
-    best = plan_tiled(h, M, num_sms, false);
+    best = plan_tiled_rt(h, RT, M, num_sms, false);
   } else if (best_cost >= 1e300 && !g_allow_waves) {
     // nothing fits in one wave (wide rows x many tokens): allow several waves
     g_allow_waves = true;
-    best = plan_tiled(h, M, num_sms, indep);
+    best = plan_tiled_rt(h, RT, M, num_sms, indep);
     g_allow_waves = false;
   }
   return best;
@@ -743,6 +780,21 @@ cudaError_t launch_tiled(const egt_dev_packed* h, const TiledSchedule& sc, const
       a.pf_bytes[3] = static_cast<uint32_t>(nblk * nx->tiled.E * 16);
     }
   }
+  a.nseg = 1;
+  a.RTs = h->tiled.RT;
+  a.rows_s = static_cast<int>(h->rows);
+  if (ctx.nseg > 1) {
+    a.nseg = ctx.nseg;
+    for (int g = 0; g < ctx.nseg; ++g) {
+      const egt_dev_packed* hg = ctx.segs[g];
+      a.seg_vals[g] = hg->tiled.vals;
+      a.seg_meta[g] = hg->tiled.meta;
+      a.seg_scales[g] = hg->tiled.scales;
+      a.seg_zps[g] = hg->tiled.zps;
+      a.seg_y[g] = ctx.seg_y[g];
+      a.seg_rtb[g] = hg->tiled.rt_begin;
+    }
+  }
   a.xform = ctx.xform;
   a.out_silu = ctx.out_silu;
   a.eps = ctx.eps;
@@ -754,8 +806,8 @@ cudaError_t launch_tiled(const egt_dev_packed* h, const TiledSchedule& sc, const
   a.zps = h->tiled.zps;
   a.KQ = h->tiled.KQ;
   a.rt_begin = h->tiled.rt_begin;
-  a.RT = h->tiled.RT;
-  a.rows = static_cast<int>(h->rows);
+  a.RT = h->tiled.RT * std::max(1, ctx.nseg);
+  a.rows = static_cast<int>(h->rows) * std::max(1, ctx.nseg);
   a.cols = static_cast<int>(h->cols);
   a.x = x;
   a.ldx = ldx;
@@ -773,7 +825,7 @@ cudaError_t launch_tiled(const egt_dev_packed* h, const TiledSchedule& sc, const
   static const int dbg = getenv("EGT_DEBUG_MODE") ? atoi(getenv("EGT_DEBUG_MODE")) : 0;
   a.dbg = dbg;
   a.indep = indep && sc.S == 1 ? 1 : 0;
-  void* fn = pick_kernel(h->format, h->tiled.SS, M == 1 ? 0 : sc.NT, a.xform != 0 || a.res != nullptr || a.pf_ptr[0] || a.out_silu);
+  void* fn = pick_kernel(h->format, h->tiled.SS, M == 1 ? 0 : sc.NT, a.xform != 0 || a.res != nullptr || a.pf_ptr[0] || a.out_silu || a.nseg > 1);
   cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(sc.smem));
   if (err != cudaSuccess) return err;

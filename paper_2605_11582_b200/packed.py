@@ -279,6 +279,16 @@ class DeviceMatrix:
         return w, bits
 
 
+def spmv_fused_multi(mats, x, ys, input: int = 0, eps: float = 1e-6, stream=None, independent: bool = False):
+    """ys[i] = f(x) @ W_i^T for up to three same-shape matrices in one launch
+    (egt_spmv_fused_multi; the decode step's Q, K, V)."""
+    n = len(mats)
+    hs = (C.c_void_p * n)(*[m.handle.value for m in mats])
+    yp = (C.c_void_p * n)(*[y.data_ptr() for y in ys])
+    check(lib().egt_spmv_fused_multi(hs, n, C.c_void_p(x.data_ptr()), yp, input, eps, 1 if independent else 0,
+                                     _stream_ptr(stream)))
+
+
 def spmv(w, x):
     """spmv (packed.hpp:83-85): host vectors in/out.  w: DeviceMatrix or PackedSparseMatrix."""
     if isinstance(w, PackedSparseMatrix):

@@ -243,3 +243,25 @@ def test_spmv_fused_output_silu(egt, port, torch):
     d.spmv_fused_into(_cuda(torch, x), y, input=INPUT_RMSNORM, output_silu=True)
     ok, err = close(y.cpu().numpy(), silu32(port.spmv(p, rmsnorm32(x))))
     assert ok, err
+
+
+@pytest.mark.parametrize("input_", [0, 1])
+def test_spmv_fused_multi_qkv(egt, port, torch, input_):
+    """egt_spmv_fused_multi: three same-shape matrices over one x in one
+    launch (the decode step's Q, K, V) equal three separate products."""
+    from paper_2605_11582_b200.native import InvalidArgument
+    from paper_2605_11582_b200.packed import spmv_fused_multi
+
+    rng = np.random.default_rng(71 + input_)
+    ps = [make_int4(rng, 1024, 2048, 2, 128, port)[0] for _ in range(3)]
+    ds = [_dev(egt, p) for p in ps]
+    x = rng.uniform(-2, 2, 2048).astype(np.float32)
+    ys = [torch.full((1024,), float("nan"), device="cuda") for _ in range(3)]
+    spmv_fused_multi(ds, _cuda(torch, x), ys, input=input_)
+    xin = rmsnorm32(x) if input_ == 1 else x
+    for p, y in zip(ps, ys):
+        ok, err = close(y.cpu().numpy(), port.spmv(p, xin))
+        assert ok, err
+    other = _dev(egt, make_int4(rng, 512, 2048, 2, 128, port)[0])
+    with pytest.raises(InvalidArgument, match="share shape"):
+        spmv_fused_multi([ds[0], other], _cuda(torch, x), ys[:2])

@@ -27,7 +27,7 @@ keep[:, :, :2] = True
 mask = np.packbits(keep.reshape(-1), bitorder="little")
 head = egt.DeviceMatrix.from_packed(egt.pack(mask, egt.quantize_matrix(hw, 128, mask), 2))
 model = DeviceModel(cfg, rng.uniform(-0.01, 0.01, (cfg["vocab_size"], 4096)).astype(np.float32), layers, head)
-n_per = 6 * L + 1
+n_per = 4 * L + 1  # fused QKV, O, ff1, ff2 per layer + head
 buf = (C.c_ulonglong * (8 * 4096))()
 lib().egt_tune_read_trace(buf, 8 * 4096, 1)  # reset before the decoder's warm-up + capture
 dec = Decoder(model, 128)
@@ -42,12 +42,12 @@ t = np.frombuffer(buf, np.uint64).reshape(4096, 8).astype(np.int64)
 # launch_tiled slots: eager warm-up step = 0 .. n_per-1, captured graph = n_per .. 2 n_per - 1
 sl = t[n_per:2 * n_per]
 base = sl[:, 0].min()
-roles = ["q", "k", "v", "o", "ff1", "ff2"]
+roles = ["qkv", "o", "ff1", "ff2"]
 stats = {r: [] for r in roles + ["head"]}
 prev_exit = None
 rows = []
 for j in range(n_per):
-    role = "head" if j == n_per - 1 else roles[j % 6]
+    role = "head" if j == n_per - 1 else roles[j % 4]
     r = sl[j]
     gap = (r[1] - prev_exit) if prev_exit is not None else 0
     stats[role].append((r[1] - r[0], r[2] - r[1], r[3] - r[2], r[4] - r[3], gap, r[4] - (prev_exit or r[0])))
