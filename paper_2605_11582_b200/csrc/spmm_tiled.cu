@@ -19,6 +19,9 @@
 #include "device_common.cuh"
 #include "handle.h"
 #include "tiled_compute.cuh"
+#ifndef EGT_X4
+#define EGT_X4 4
+#endif
 #ifndef EGT_XU
 #define EGT_XU 8
 #endif
@@ -236,7 +239,7 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
     const float* xb = a.x + static_cast<size_t>(m0) * a.ldx + kq0 * 128;
     const int nwin = min(KTc * 32, a.cols - kq0 * 128);  // floats of x in this CTA's window
     const int nf4 = KTc * 8;                             // float4s covering the window (zero past nwin)
-    constexpr int X4 = 4;
+    constexpr int X4 = EGT_X4;
     if (a.dbg != 3 && (reinterpret_cast<uintptr_t>(xb) & 15) == 0 && (nwin & 3) == 0 &&
         (!FUSED || a.xform != EGT_INPUT_RMSNORM || (kq0 == 0 && nwin == a.cols))) {
       const int per_pass = X4 * static_cast<int>(blockDim.x);
