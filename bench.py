@@ -267,10 +267,80 @@ def measure_sharded(world, rank, stream, torch, egt, rng):
             yf = fulls[0].spmv(x).cpu().numpy()
             yg = gather_rows(shards[0].spmv(x), plan).cpu().numpy()
             res["gathered_equals_unsharded_max_rel_err"] = float(np.max(np.abs(yg - yf) / (1 + np.abs(yf))))
+        res.update(measure_fused_gather(world, rank, stream, torch, fulls, shards, x, plan, reps))
         out[f"{rows}x{cols}"] = res
         del fulls, shards, g
         torch.cuda.synchronize()
     return out
+
+
+def measure_fused_gather(world, rank, stream, torch, fulls, shards, x, plan, reps):
+    """The same shard product with the all-gather fused into the kernel
+    (egt_spmv_allgather: y rows stored into every rank's buffer over NVLink
+    via CUDA IPC, arrival counters exchanged by the last CTA): us per call
+    until the whole y is on every rank (max over ranks).  Setup failures are
+    agreed on by all ranks, so a rank without IPC skips instead of hanging."""
+    from paper_2605_11582_b200.parallel import FusedShardedSpmv
+
+    dist = torch.distributed
+    r0, _ = plan.local(rank)
+    rows = fulls[0].rows
+    err = ""
+    try:
+        fs = FusedShardedSpmv(fulls[0]) if dist.is_initialized() else None
+        if fs is None:
+            from paper_2605_11582_b200.parallel import PeerGroup
+
+            peers = PeerGroup.local_ranks(1, rows)[0]
+        else:
+            peers = fs.peers
+    except Exception as e:  # noqa: BLE001 -- reported, and agreed on below
+        err, peers = repr(e)[:160], None
+    ok = torch.tensor([0 if err else 1], device="cuda")
+    if world > 1:
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if not int(ok.item()):
+        return {"fused_allgather_error": err or "setup failed on another rank"}
+    try:
+        with torch.cuda.stream(stream):
+            for d in shards:
+                peers.spmv(d, x, r0, rows, stream)
+            stream.synchronize()
+        peers.check()
+        good = 1
+    except Exception as e:  # noqa: BLE001
+        err, good = repr(e)[:160], 0
+    ok = torch.tensor([good], device="cuda")
+    if world > 1:
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    if not int(ok.item()):
+        return {"fused_allgather_error": err or "a peer wait timed out"}
+    y_want = fulls[0].spmv(x)
+    torch.cuda.synchronize()
+    rel = float(((peers.y((rows,)) - y_want).abs() / (1 + y_want.abs())).max().item())
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(stream):
+        with torch.cuda.graph(g, stream=stream):
+            for d in shards:
+                peers.spmv(d, x, r0, rows, stream)
+    n_rep = reps // 10 + 1
+    g.replay()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(n_rep):
+            g.replay()
+        e1.record(stream)
+    e1.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) * 1e3 / (n_rep * len(shards))], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    peers.check()
+    return {"fused_gemv_allgather_us": round(float(t.item()), 3),
+            "fused_gathered_max_rel_err": rel}
 
 
 # ------------------------------------------------------------------ decode (configs[2])

@@ -360,6 +360,48 @@ EGT_API egt_status egt_program_destroy(egt_program* p);
  * ready, [8192,12288) consumer done, [12288,16384) epilogue segment start. */
 EGT_API egt_status egt_program_debug_trace(const egt_program* p, long long* host, size_t n);
 
+/* ---------------- row shards with a fused all-gather ---------
+ * Replaces the NCCL all-gather after a row-sharded spmv (the reference is
+ * single-process: spmv packed.cpp:211-220 over the whole matrix).  Each rank
+ * owns one peer buffer: a 512-byte control block (arrival counters of up to
+ * 8 ranks, a gather sequence number, a done counter, an error word) followed
+ * by y (M x ldy floats, the FULL output).  Buffers are exported with CUDA IPC
+ * handles (64 opaque bytes, exchanged by the caller, e.g. over
+ * torch.distributed) and opened by every other rank; a peer group lists all
+ * ranks' buffers in rank order (this rank's own pointer at `rank`).
+ * egt_spmv_allgather runs the shard's product and stores every y row into
+ * every rank's buffer over NVLink; its last CTA signals the peers and waits
+ * until all ranks' slices have landed here, so the gathered y is complete
+ * when the kernel is.  EGT_PEER_NOWAIT skips that wait (then egt_peer_wait
+ * must follow, e.g. when several ranks share one GPU in a test).  A wait
+ * bounded at 2 s records a timeout that egt_peer_group_check reports. */
+#define EGT_PEER_NOWAIT 4u
+#define EGT_PEER_CTRL_BYTES 512u
+#define EGT_MAX_PEERS 8u
+typedef struct egt_ipc_handle {
+  uint8_t bytes[64];
+} egt_ipc_handle;
+typedef struct egt_peer_group egt_peer_group; /* opaque; buffers must outlive it */
+EGT_API egt_status egt_peer_buffer_alloc(size_t y_floats, void** buf_dev, egt_ipc_handle* handle);
+EGT_API egt_status egt_peer_buffer_free(void* buf_dev);
+EGT_API egt_status egt_peer_buffer_open(const egt_ipc_handle* handle, void** buf_dev);
+EGT_API egt_status egt_peer_buffer_close(void* buf_dev);
+EGT_API egt_status egt_peer_group_create(uint32_t world, uint32_t rank, void* const* bufs_dev,
+                                         egt_peer_group** out);
+EGT_API egt_status egt_peer_group_destroy(egt_peer_group* g);
+/* The gathered output in this rank's buffer (M x ldy floats). */
+EGT_API float* egt_peer_group_y(const egt_peer_group* g);
+/* y rows [row0, row0 + shard.rows) of every token, gathered on all ranks.
+ * flags: EGT_SPMV_INDEPENDENT, EGT_PEER_NOWAIT.  Tiled path only. */
+EGT_API egt_status egt_spmv_allgather(const egt_dev_packed* shard, const float* x_dev, uint32_t M,
+                                      uint32_t ldx, egt_peer_group* g, uint32_t row0, uint32_t ldy,
+                                      uint32_t flags, void* stream);
+/* Stream-ordered wait for every rank's current slice (after EGT_PEER_NOWAIT). */
+EGT_API egt_status egt_peer_wait(egt_peer_group* g, void* stream);
+/* Synchronizes the device; EGT_EINTERNAL ("peer wait timed out") if a wait
+ * gave up. */
+EGT_API egt_status egt_peer_group_check(egt_peer_group* g);
+
 /* ---------------- EGTQ compressed-model files -> device layers ------------
  * parse_compressed (egtq_io.cpp:221-235, read_layer :110-210) with the
  * reference's checks and FormatError messages ("<context>: ..."); upload is

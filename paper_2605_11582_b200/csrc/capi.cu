@@ -436,7 +436,8 @@ egt_status egt_dev_packed_query(const egt_dev_packed* h, egt_dev_packed_info* in
 namespace {
 egt_status spmv_impl(const egt_dev_packed* h, const float* x, float* y, uint32_t M, uint32_t ldx, uint32_t ldy,
                      uint32_t flags, const float* res, uint32_t ldr, uint32_t input, float eps,
-                     const egt_dev_packed* l2_next, void* stream) {
+                     const egt_dev_packed* l2_next, void* stream, const egt_peer_group* pg = nullptr,
+                     uint32_t row0 = 0) {
   const bool indep = (flags & EGT_SPMV_INDEPENDENT) != 0;
   if (!h) return fail(EGT_EINVAL, "spmv: null matrix");
   if (M == 0) return EGT_OK;
@@ -444,8 +445,13 @@ egt_status spmv_impl(const egt_dev_packed* h, const float* x, float* y, uint32_t
   if (M > 1 && ldy < h->rows) return fail(EGT_EINVAL, "spmv: output stride below rows");
   if (input > EGT_INPUT_SILU) return fail(EGT_EINVAL, "spmv: unknown input transform");
   if (res && M > 1 && ldr < h->rows) return fail(EGT_EINVAL, "spmv: residual stride below rows");
-  if (h->rows == 0) return EGT_OK;
+  if (h->rows == 0) {
+    if (pg) CUDA_TRY(launch_peer_signal(pg, true, (flags & EGT_PEER_NOWAIT) == 0, static_cast<cudaStream_t>(stream)));
+    return EGT_OK;
+  }
   if (!x || !y) return fail(EGT_EINVAL, "spmv: null vector");
+  if (pg && (h->path != EGT_PATH_TILED || h->cols == 0 || M > 16))
+    return fail(EGT_EINVAL, "spmv allgather: tiled-path shards with columns, at most 16 tokens");
   if (input == EGT_INPUT_RMSNORM && (ldx % 4 != 0 || h->cols % 4 != 0 || reinterpret_cast<uintptr_t>(x) % 16 != 0))
     return fail(EGT_EINVAL, "spmv: rmsnorm input needs 16-byte aligned rows of a multiple of 4 floats");
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -458,6 +464,17 @@ egt_status spmv_impl(const egt_dev_packed* h, const float* x, float* y, uint32_t
   ctx.ldr = static_cast<int>(M > 1 ? ldr : h->rows);
   ctx.l2_next = l2_next;
   ctx.out_silu = (flags & EGT_SPMV_OUTPUT_SILU) != 0 ? 1 : 0;
+  if (pg) {
+    ctx.npeer = static_cast<int>(pg->world);
+    ctx.peer_rank = static_cast<int>(pg->rank);
+    ctx.peer_row0 = static_cast<int>(row0);
+    ctx.peer_wait = (flags & EGT_PEER_NOWAIT) ? 0 : 1;
+    ctx.peer_ctrl = pg->ctrl;
+    for (uint32_t i = 0; i < pg->world; ++i) {
+      ctx.peer_y[i] = pg->y[i];
+      ctx.peer_flag[i] = pg->flags[i];
+    }
+  }
   if (h->cols == 0) {
     for (uint32_t m = 0; m < M; ++m) {
       float* ym = y + static_cast<size_t>(m) * ldy;
@@ -477,7 +494,7 @@ egt_status spmv_impl(const egt_dev_packed* h, const float* x, float* y, uint32_t
     return EGT_OK;
   }
   static const bool no_wide = getenv("EGT_NO_WIDE") != nullptr;  // tuning: old M > 16 path
-  if (M > 16 && !res && input == EGT_INPUT_NONE && !ctx.out_silu && !no_wide && !plan_forced()) {
+  if (M > 16 && !pg && !res && input == EGT_INPUT_NONE && !ctx.out_silu && !no_wide && !plan_forced()) {
     Workspace* w = nullptr;
     egt_status st = get_workspace(s, (wide_workspace_bytes(h, static_cast<int>(M)) + 3) / 4, 0, &w);
     if (st != EGT_OK) return st;
@@ -564,6 +581,17 @@ egt_status egt_spmv_fused_multi(const egt_dev_packed* const* hs, uint32_t n, con
   }
   CUDA_TRY(launch_tiled(h, sc, x, static_cast<int>(h->cols), 1, ys[0], static_cast<int>(h->rows), ctx, indep));
   return EGT_OK;
+}
+
+egt_status egt_spmv_allgather(const egt_dev_packed* shard, const float* x, uint32_t M, uint32_t ldx,
+                              egt_peer_group* g, uint32_t row0, uint32_t ldy, uint32_t flags, void* stream) {
+  if (!g) return fail(EGT_EINVAL, "spmv allgather: null peer group");
+  if (!shard) return fail(EGT_EINVAL, "spmv: null matrix");
+  if (static_cast<uint64_t>(row0) + shard->rows > ldy)
+    return fail(EGT_EINVAL, "spmv allgather: shard rows past the gathered output stride");
+  if (M == 0) return EGT_OK;
+  return spmv_impl(shard, x, g->y[g->rank], M, ldx, ldy, flags & (EGT_SPMV_INDEPENDENT | EGT_PEER_NOWAIT), nullptr,
+                   0, EGT_INPUT_NONE, 0.f, nullptr, stream, g, row0);
 }
 
 egt_status egt_spmv_fused(const egt_dev_packed* h, const float* x, float* y, uint32_t M, uint32_t ldx,

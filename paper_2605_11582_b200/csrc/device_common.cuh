@@ -187,4 +187,32 @@ __device__ __forceinline__ void bulk_g2s_plain(void* dst, const void* src, uint3
       : "memory");
 }
 
+// Fused all-gather wait (one thread): ctrl[0] counts this rank's completed
+// gathers; every rank's arrival counter flags[g] must reach ctrl[0] + 1.
+// Relaxed system-scope polling (peers add over NVLink), one acq_rel fence
+// once all have arrived; bounded by 2 s of globaltimer, after which ctrl[2]
+// records the timeout instead of hanging.
+__device__ __forceinline__ void peer_wait_all(const uint32_t* flags, int n, uint32_t* ctrl) {
+  const uint32_t target = ctrl[0] + 1u;
+  unsigned long long t0 = 0;
+  for (int g = 0; g < n; ++g) {
+    while (true) {
+      uint32_t v;
+      asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + g) : "memory");
+      if (static_cast<int32_t>(v - target) >= 0) break;
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t0 == 0) t0 = t;
+      if (t - t0 > 2000000000ull) {
+        ctrl[2] = 1u;
+        g = n;
+        break;
+      }
+      __nanosleep(32);
+    }
+  }
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  ctrl[0] = target;
+}
+
 }  // namespace egt_dev

@@ -11,6 +11,7 @@
 #include "tiled_format.h"
 
 namespace egt_impl {
+constexpr int kMaxPeers = 8;  // ranks of one NVSwitch node
 
 struct DevStorage {
   int device = 0;
@@ -77,6 +78,21 @@ struct egt_dev_packed {
   mutable std::map<int, egt_impl::TiledSchedule> plans;
 };
 
+// Row-shard peer group (fused all-gather): every rank's buffer in rank order;
+// each is [512-byte control block | y].  Control block: u32 arrival counters
+// [0, 8), then at byte 256 this rank's [sequence, done, error].
+struct egt_peer_group {
+  uint32_t world = 0, rank = 0;
+  uint32_t* flags[egt_impl::kMaxPeers] = {};
+  float* y[egt_impl::kMaxPeers] = {};
+  uint32_t* ctrl = nullptr;
+};
+
+namespace egt_impl {
+// Signal this rank's (empty) slice and optionally wait for every peer's.
+cudaError_t launch_peer_signal(const egt_peer_group* g, bool signal, bool wait, cudaStream_t s);
+}  // namespace egt_impl
+
 namespace egt_impl {
 
 // Per-call launch context.
@@ -94,6 +110,11 @@ struct LaunchCtx {
   int nseg = 0;                             // > 1: one launch over several same-shape matrices
   const egt_dev_packed* segs[3] = {nullptr, nullptr, nullptr};
   float* seg_y[3] = {nullptr, nullptr, nullptr};
+  int npeer = 0;                  // > 0: row shard, y rows stored into every peer (fused all-gather)
+  int peer_rank = 0, peer_row0 = 0, peer_wait = 1;
+  float* peer_y[kMaxPeers] = {};
+  uint32_t* peer_flag[kMaxPeers] = {};
+  uint32_t* peer_ctrl = nullptr;
 };
 
 TiledSchedule plan_tiled(const egt_dev_packed* h, int M, int num_sms, bool indep);

@@ -75,6 +75,13 @@ struct TiledArgs {
   const uint8_t* seg_zps[3];
   float* seg_y[3];
   int seg_rtb[3];
+  // row shard with a fused all-gather: y rows go to every
+  // peer's buffer (NVLink P2P stores) at peer_row0 + row; the last CTA to
+  // finish signals each peer and (peer_wait) waits for every peer's slice
+  int npeer, peer_rank, peer_row0, peer_wait;
+  float* peer_y[kMaxPeers];
+  uint32_t* peer_flag[kMaxPeers];
+  uint32_t* peer_ctrl;  // this rank's [expected, done, error]
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -100,6 +107,40 @@ __device__ __noinline__ float2 silu2(float2 v) {
 // mma.sp.  Per-warp partial sums are reduced in a fixed order; split-K
 // (S > 1) partial rows are summed by the last-arriving CTA of the row block,
 // in slice order, so results are deterministic.
+template <bool FUSED>
+__device__ __forceinline__ void store_out(const TiledArgs& a, int tok, int row, float o) {
+  if (FUSED && a.npeer > 0) {
+    const size_t off = static_cast<size_t>(tok) * a.ldy + a.peer_row0 + row;
+    for (int p = 0; p < a.npeer; ++p) a.peer_y[p][off] = o;
+  } else if (FUSED && a.nseg > 1) {
+    const int sg = row / a.rows_s;
+    a.seg_y[sg][static_cast<size_t>(tok) * a.ldy + (row - sg * a.rows_s)] = o;
+  } else {
+    a.y[static_cast<size_t>(tok) * a.ldy + row] = o;
+  }
+}
+
+// Fused all-gather completion: every storing CTA orders its stores before
+// its done count (gpu scope: the counter is local); the last one, after a
+// system-scope acq_rel fence (cumulative over everything the counter
+// observed), bumps this rank's arrival counter in every peer's flag array
+// and (peer_wait) waits until every rank's counter here reached this call's
+// sequence number.  The wait is bounded (2 s of globaltimer): a missing peer
+// sets the error word instead of hanging.  One rank: kernel completion
+// already orders the (local) stores, so there is nothing to exchange.
+__device__ __forceinline__ void peer_complete(const TiledArgs& a, unsigned expect) {
+  if (a.npeer == 1 && a.dbg != 14) return;
+  __syncthreads();  // the CTA's stores happen-before thread 0's fence
+  if (threadIdx.x != 0) return;
+  __threadfence();
+  if (atomicAdd(a.peer_ctrl + 1, 1u) != expect - 1) return;
+  a.peer_ctrl[1] = 0u;
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  for (int p = 0; p < a.npeer; ++p)
+    asm volatile("red.relaxed.sys.global.add.u32 [%0], 1;" ::"l"(a.peer_flag[p] + a.peer_rank) : "memory");
+  if (a.peer_wait) peer_wait_all(a.peer_flag[a.peer_rank], a.npeer, a.peer_ctrl);
+}
+
 template <int FMT, int SS, int NT, bool SINGLE, bool FUSED>
 __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(const TiledArgs a) {
   constexpr int E = 4 / SS;
@@ -517,18 +558,14 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
       if (a.S == 1) {
         float o = (FUSED && a.res ? (idx == tid ? res_pre : a.res[static_cast<size_t>(tok) * a.ldr + row]) : 0.f) + v;
         if (FUSED && a.out_silu) o = o * (1.0f / (1.0f + expf(-o)));  // model.cpp:80-84
-        if (FUSED && a.nseg > 1) {
-          const int sg = row / a.rows_s;
-          a.seg_y[sg][static_cast<size_t>(tok) * a.ldy + (row - sg * a.rows_s)] = o;
-        } else {
-          a.y[static_cast<size_t>(tok) * a.ldy + row] = o;
-        }
+        store_out<FUSED>(a, tok, row, o);
       }
       else
         a.partial[(static_cast<size_t>(blockIdx.y) * a.M + tok) * rows_pad + row] = v;
     }
   }
   if (a.S == 1) {
+    if (FUSED && a.npeer > 0) peer_complete(a, gridDim.x * gridDim.y * gridDim.z);
     if (a.indep) pdl_wait();
     if (tr && threadIdx.x == 0) atomicMax(tr + 4, gtimer());
     return;
@@ -552,15 +589,11 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
         v += __ldcg(a.partial + (static_cast<size_t>(sidx) * a.M + tok) * rows_pad + row);
       float o = (FUSED && a.res ? a.res[static_cast<size_t>(tok) * a.ldr + row] : 0.f) + v;
       if (FUSED && a.out_silu) o = o * (1.0f / (1.0f + expf(-o)));
-      if (FUSED && a.nseg > 1) {
-        const int sg = row / a.rows_s;
-        a.seg_y[sg][static_cast<size_t>(tok) * a.ldy + (row - sg * a.rows_s)] = o;
-      } else {
-        a.y[static_cast<size_t>(tok) * a.ldy + row] = o;
-      }
+      store_out<FUSED>(a, tok, row, o);
     }
   }
   if (tid == 0) a.counters[cidx] = 0u;  // ready for the next launch / graph replay
+  if (FUSED && a.npeer > 0) peer_complete(a, gridDim.x * gridDim.z);
 }
 
 // ---------------------------------------------------------------- planning
@@ -798,6 +831,15 @@ cudaError_t launch_tiled(const egt_dev_packed* h, const TiledSchedule& sc, const
       a.seg_rtb[g] = hg->tiled.rt_begin;
     }
   }
+  a.npeer = ctx.npeer;
+  a.peer_rank = ctx.peer_rank;
+  a.peer_row0 = ctx.peer_row0;
+  a.peer_wait = ctx.peer_wait;
+  a.peer_ctrl = ctx.peer_ctrl;
+  for (int p = 0; p < kMaxPeers; ++p) {
+    a.peer_y[p] = p < ctx.npeer ? ctx.peer_y[p] : nullptr;
+    a.peer_flag[p] = p < ctx.npeer ? ctx.peer_flag[p] : nullptr;
+  }
   a.xform = ctx.xform;
   a.out_silu = ctx.out_silu;
   a.eps = ctx.eps;
@@ -828,7 +870,7 @@ cudaError_t launch_tiled(const egt_dev_packed* h, const TiledSchedule& sc, const
   static const int dbg = getenv("EGT_DEBUG_MODE") ? atoi(getenv("EGT_DEBUG_MODE")) : 0;
   a.dbg = dbg;
   a.indep = indep && sc.S == 1 ? 1 : 0;
-  void* fn = pick_kernel(h->format, h->tiled.SS, M == 1 ? 0 : sc.NT, a.xform != 0 || a.res != nullptr || a.pf_ptr[0] || a.out_silu || a.nseg > 1);
+  void* fn = pick_kernel(h->format, h->tiled.SS, M == 1 ? 0 : sc.NT, a.xform != 0 || a.res != nullptr || a.pf_ptr[0] || a.out_silu || a.nseg > 1 || a.npeer > 0);
   cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(sc.smem));
   if (err != cudaSuccess) return err;

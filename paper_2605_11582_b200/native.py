@@ -179,7 +179,32 @@ _MODEL_SIGNATURES.update({
     "egt_egtq_destroy": (C.c_int, [C.c_void_p]),
 })
 
+
+
+class IpcHandle(C.Structure):
+    _fields_ = [("bytes", C.c_uint8 * 64)]
+
+
+PEER_NOWAIT = 4
+PEER_CTRL_BYTES = 512
+MAX_PEERS = 8
+
+_PEER_SIGNATURES = {
+    "egt_peer_buffer_alloc": (C.c_int, [C.c_size_t, C.POINTER(C.c_void_p), C.POINTER(IpcHandle)]),
+    "egt_peer_buffer_free": (C.c_int, [C.c_void_p]),
+    "egt_peer_buffer_open": (C.c_int, [C.POINTER(IpcHandle), C.POINTER(C.c_void_p)]),
+    "egt_peer_buffer_close": (C.c_int, [C.c_void_p]),
+    "egt_peer_group_create": (C.c_int, [C.c_uint32, C.c_uint32, C.POINTER(C.c_void_p), C.POINTER(C.c_void_p)]),
+    "egt_peer_group_destroy": (C.c_int, [C.c_void_p]),
+    "egt_peer_group_y": (C.c_void_p, [C.c_void_p]),
+    "egt_spmv_allgather": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.c_uint32,
+                                     C.c_uint32, C.c_uint32, C.c_void_p]),
+    "egt_peer_wait": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "egt_peer_group_check": (C.c_int, [C.c_void_p]),
+}
+
 SIGNATURES.update(_MODEL_SIGNATURES)
+SIGNATURES.update(_PEER_SIGNATURES)
 SIGNATURES.update(_PROGRAM_SIGNATURES)
 
 _lib = None

@@ -85,3 +85,36 @@ def test_row_sharded_allgather_gloo(world):
         pr.join(timeout=60)
         assert pr.exitcode == 0
     assert all(ok and ok1 for _, ok, ok1 in results), results
+
+
+def _handle_worker(rank, world, port, q):
+    import torch.distributed as dist
+
+    from paper_2605_11582_b200.parallel import exchange_handles
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        mine = bytes([rank + 1] * 32 + list(range(32)))  # a 64-byte CUDA IPC handle stand-in
+        got = exchange_handles(mine)
+        q.put((rank, got == [bytes([r + 1] * 32 + list(range(32))) for r in range(world)]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_peer_handle_exchange_gloo(world):
+    """The fused all-gather's setup step: every rank's peer-buffer handle,
+    in rank order, on every rank (parallel.exchange_handles)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_handle_worker, args=(r, world, port, q)) for r in range(world)]
+    for pr in procs:
+        pr.start()
+    results = [q.get(timeout=120) for _ in range(world)]
+    for pr in procs:
+        pr.join(timeout=60)
+        assert pr.exitcode == 0
+    assert all(ok for _, ok in results), results

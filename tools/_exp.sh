@@ -1,6 +1,4 @@
-python -m pytest tests/test_gpu_program.py tests/test_gpu_verify.py -q --timeout 300 -p no:cacheprovider 2>&1 | tail -1
-export EGT_BENCH_NO_VERIFY=1
-python tools/decode_probe.py int4-2:4 2>&1 | grep plan
-EGT_DECODE_NO_QKV=1 python tools/decode_probe.py int4-2:4 2>&1 | grep plan
-python tools/decode_probe.py mixed-int4dense-fp16sp24 2>&1 | grep plan
-python tools/decode_trace.py 8 2>&1 | head -9
+exec > gpurun_out/exp.log 2>&1; set -x
+for m in 0 14; do EGT_DEBUG_MODE=$m timeout 300 python tools/peer_probe.py; done
+timeout 900 python -m pytest tests/test_gpu_peer.py -x -q -m gpu 2>&1 | tail -3
+EGT_DEBUG_MODE=14 timeout 900 python -m pytest tests/test_gpu_peer.py -x -q -m gpu 2>&1 | tail -3
