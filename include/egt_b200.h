@@ -360,6 +360,39 @@ EGT_API egt_status egt_program_destroy(egt_program* p);
  * ready, [8192,12288) consumer done, [12288,16384) epilogue segment start. */
 EGT_API egt_status egt_program_debug_trace(const egt_program* p, long long* host, size_t n);
 
+/* ---------------- GPU compression ----------------------
+ * The step before the path on the device (re-compressing 7B/70B layers),
+ * byte-identical to the host encoder and the reference.  All pointers are
+ * device pointers except group_sizes (host, one per row); stream-ordered. */
+/* importance_scores (compress.cpp:230-244): |w| x_norms[c] + |w| grad_abs. */
+EGT_API egt_status egt_gpu_importance(const float* w_dev, const float* x_norms_dev, const float* grad_abs_dev,
+                                      uint32_t rows, uint32_t cols, float* scores_dev, void* stream);
+/* prune_nm (compress.cpp:246-278): PruneMask bitmap (ceil(rows*cols/8)
+ * bytes) keeping the min(n, #positive) top scores of every group of m = 4
+ * columns, ties to the lower column. */
+EGT_API egt_status egt_gpu_prune_nm(const float* scores_dev, uint32_t rows, uint32_t cols, int n, int m,
+                                    uint8_t* mask_dev, void* stream);
+/* Device arrays in the reference's stream layout (may be NULL members except
+ * index_words / value_bytes): ceil(nnz/8) u16, ceil(nnz/2) bytes, rows + 1,
+ * groups, groups. */
+typedef struct egt_gpu_packed_out {
+  uint16_t* index_words;
+  uint8_t* value_bytes;
+  uint32_t* group_offsets;
+  float* scales;
+  uint8_t* zero_points;
+} egt_gpu_packed_out;
+/* quantize_matrix(w, group_sizes, mask) + pack(mask, q, n, 4)
+ * (compress.cpp:157-197, packed.cpp:92-128) on the device: the exact-n check
+ * with the reference's "keeps" message, the group fit in double, the codes
+ * and the 2bit-CSR index stream.  raw_out (may be NULL) receives the
+ * reference-layout arrays; out (may be NULL) the device matrix, as
+ * egt_dev_packed_create would build it from those arrays. */
+EGT_API egt_status egt_gpu_quantize_pack(const float* w_dev, const uint8_t* mask_dev, uint32_t rows,
+                                         uint32_t cols, int n, const uint32_t* group_sizes,
+                                         const egt_gpu_packed_out* raw_out, void* stream,
+                                         egt_dev_packed** out);
+
 /* ---------------- row shards with a fused all-gather ---------
  * Replaces the NCCL all-gather after a row-sharded spmv (the reference is
  * single-process: spmv packed.cpp:211-220 over the whole matrix).  Each rank

@@ -418,6 +418,53 @@ void egto_magnitude_mask(const float* w, uint32_t rows, uint32_t cols, int n, in
     }
 }
 
+/* importance_scores, compress.cpp:230-244: |w| * x_norms[c] + |w| * grad_abs,
+ * two f32 products and one f32 sum (no contraction: -ffp-contract=off). */
+int egto_importance(const float* w, const float* x_norms, const float* grad_abs, uint32_t rows,
+                    uint32_t cols, float* scores) {
+  for (uint32_t r = 0; r < rows; ++r)
+    for (uint32_t c = 0; c < cols; ++c) {
+      const size_t i = (size_t)r * cols + c;
+      const float a = fabsf(w[i]);
+      const float p = a * x_norms[c];
+      const float q = a * grad_abs[i];
+      scores[i] = p + q;
+    }
+  return 0;
+}
+
+/* prune_nm, compress.cpp:246-278: per row, per group of m columns (the last
+ * may be short), keep the min(n, #positive) largest scores; ties to the lower
+ * column.  bits: PruneMask bitmap, zeroed here. */
+int egto_prune_nm(const float* scores, uint32_t rows, uint32_t cols, int n, int m, uint8_t* bits) {
+  if (m != 4) return fail(1, "prune_nm: group width must be 4");
+  if (n < 1 || n >= m) return fail(1, "prune_nm: keep count must be in [1, group width)");
+  memset(bits, 0, ((size_t)rows * cols + 7) / 8);
+  for (uint32_t r = 0; r < rows; ++r)
+    for (uint32_t start = 0; start < cols; start += (uint32_t)m) {
+      const uint32_t end = start + (uint32_t)m < cols ? start + (uint32_t)m : cols;
+      float a[4];
+      uint32_t idx[4];
+      int cnt = 0;
+      for (uint32_t c = start; c < end; ++c) {
+        const float v = scores[(size_t)r * cols + c];
+        if (v > 0.0f) {
+          a[cnt] = v;
+          idx[cnt++] = c;
+        }
+      }
+      for (int i = 1; i < cnt; ++i)
+        for (int j = i; j > 0; --j) {
+          int before = (a[j] != a[j - 1]) ? (a[j] > a[j - 1]) : (idx[j] < idx[j - 1]);
+          if (!before) break;
+          float ta = a[j]; a[j] = a[j - 1]; a[j - 1] = ta;
+          uint32_t ti = idx[j]; idx[j] = idx[j - 1]; idx[j - 1] = ti;
+        }
+      for (int i = 0; i < n && i < cnt; ++i) mask_set(bits, cols, r, idx[i]);
+    }
+  return 0;
+}
+
 /* ---------------------------------------------------------------- model */
 
 /* sinusoidal_positions, model.cpp:44-54 (double math, stored f32). */

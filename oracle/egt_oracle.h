@@ -111,6 +111,10 @@ void egto_quant_dense_gemv(uint32_t rows, uint32_t cols, const uint32_t* group_s
 
 /* magnitude_mask (packed.cpp:245-264): exactly n kept per group of m by |w|,
  * ties to the lower column. bits must be zeroed, ceil(rows*cols/8) bytes. */
+/* importance_scores (compress.cpp:230-244) and prune_nm (:246-278). */
+int egto_importance(const float* w, const float* x_norms, const float* grad_abs, uint32_t rows,
+                    uint32_t cols, float* scores);
+int egto_prune_nm(const float* scores, uint32_t rows, uint32_t cols, int n, int m, uint8_t* bits);
 void egto_magnitude_mask(const float* w, uint32_t rows, uint32_t cols, int n, int m,
                          uint8_t* bits);
 

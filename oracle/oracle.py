@@ -198,6 +198,24 @@ class Oracle:
         return Quantized(rows, cols, gs.copy(), goff, scales[:total].copy(), zps[:total].copy(),
                          codes[: nc.value].copy(), None if mb is None else mb.copy())
 
+    def importance(self, w: np.ndarray, x_norms: np.ndarray, grad_abs: np.ndarray) -> np.ndarray:
+        """importance_scores (compress.cpp:230-244)."""
+        w = np.ascontiguousarray(w, np.float32)
+        xn = np.ascontiguousarray(x_norms, np.float32)
+        g = np.ascontiguousarray(grad_abs, np.float32)
+        out = np.zeros(w.shape, np.float32)
+        self._check(getattr(self.lib, self.p + "importance")(_ptr(w, _f32p), _ptr(xn, _f32p), _ptr(g, _f32p),
+                                                             w.shape[0], w.shape[1], _ptr(out, _f32p)))
+        return out
+
+    def prune_nm(self, scores: np.ndarray, n: int, m: int = 4) -> np.ndarray:
+        """prune_nm (compress.cpp:246-278): the PruneMask bitmap."""
+        s = np.ascontiguousarray(scores, np.float32)
+        rows, cols = s.shape
+        bits = np.zeros(max(1, (rows * cols + 7) // 8), np.uint8)
+        self._check(getattr(self.lib, self.p + "prune_nm")(_ptr(s, _f32p), rows, cols, n, m, _ptr(bits, _u8p)))
+        return bits[: (rows * cols + 7) // 8]
+
     def dequantize(self, q: Quantized) -> np.ndarray:
         out = np.zeros((q.rows, q.cols), np.float32)
         mb = None if q.mask is None else np.ascontiguousarray(q.mask, np.uint8)

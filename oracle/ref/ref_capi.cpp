@@ -299,4 +299,28 @@ int ref_egtq_parse(const uint8_t* bytes, size_t n, uint32_t* n_layers) {
   });
 }
 
+// importance_scores (compress.cpp:230-244): |w| x_norm[c] + |w| grad_abs.
+int ref_importance(const float* w, const float* x_norms, const float* grad_abs, uint32_t rows,
+                   uint32_t cols, float* scores) {
+  return guarded([&] {
+    egt::Vector xn(cols);
+    for (uint32_t c = 0; c < cols; ++c) xn(c) = x_norms[c];
+    egt::ImportanceMatrix im = egt::importance_scores(make_matrix(w, rows, cols), xn,
+                                                      make_matrix(grad_abs, rows, cols));
+    for (uint32_t r = 0; r < rows; ++r)
+      for (uint32_t c = 0; c < cols; ++c) scores[static_cast<size_t>(r) * cols + c] = im.scores(r, c);
+  });
+}
+
+// prune_nm (compress.cpp:246-278): PruneMask bitmap of the top-n positive
+// scores of every group of m columns.
+int ref_prune_nm(const float* scores, uint32_t rows, uint32_t cols, int n, int m, uint8_t* mask_bits) {
+  return guarded([&] {
+    egt::ImportanceMatrix im;
+    im.scores = make_matrix(scores, rows, cols);
+    egt::PruneMask pm = egt::prune_nm(make_matrix(scores, rows, cols), im, n, m);
+    std::copy(pm.bits.begin(), pm.bits.end(), mask_bits);
+  });
+}
+
 }  // extern "C"

@@ -11,6 +11,9 @@ from .packed import (  # noqa: F401
     PackedSparseMatrix,
     QuantizedMatrix,
     fit_group,
+    gpu_importance,
+    gpu_prune_nm,
+    gpu_quantize_pack,
     footprint,
     launch_count,
     pack,

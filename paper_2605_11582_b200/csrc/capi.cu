@@ -338,6 +338,111 @@ egt_status egt_dev_packed_create(const egt_packed_view* v, void* stream, egt_dev
                       c.total, s, out);
 }
 
+egt_status egt_gpu_importance(const float* w, const float* x_norms, const float* grad_abs, uint32_t rows,
+                              uint32_t cols, float* scores, void* stream) {
+  if (static_cast<uint64_t>(rows) * cols && (!w || !x_norms || !grad_abs || !scores))
+    return fail(EGT_EINVAL, "importance: null argument");
+  CUDA_TRY(launch_importance(w, x_norms, grad_abs, rows, cols, scores, static_cast<cudaStream_t>(stream)));
+  return EGT_OK;
+}
+
+egt_status egt_gpu_prune_nm(const float* scores, uint32_t rows, uint32_t cols, int n, int m, uint8_t* mask,
+                            void* stream) {
+  if (m != 4) return fail(EGT_EINVAL, "prune_nm: group width must be 4");  // compress.cpp:247-249
+  if (n < 1 || n >= m) return fail(EGT_EINVAL, "prune_nm: keep count must be in [1, group width)");
+  if (static_cast<uint64_t>(rows) * cols && (!scores || !mask)) return fail(EGT_EINVAL, "prune_nm: null argument");
+  CUDA_TRY(launch_prune_nm(scores, rows, cols, n, mask, static_cast<cudaStream_t>(stream)));
+  return EGT_OK;
+}
+
+egt_status egt_gpu_quantize_pack(const float* w, const uint8_t* mask, uint32_t rows, uint32_t cols, int n,
+                                 const uint32_t* group_sizes, const egt_gpu_packed_out* raw_out, void* stream,
+                                 egt_dev_packed** out) {
+  using namespace egt_fmt;
+  if (out) *out = nullptr;
+  if (!out && !raw_out) return fail(EGT_EINVAL, "gpu pack: nothing to produce");
+  // pack's checks (packed.cpp:27-49) and quantize's (compress.cpp:157-176)
+  if (n == 4) return fail(EGT_EINVAL, "pack: dense pattern unsupported");
+  if (n < 1 || n > 4) return fail(EGT_EINVAL, "pack: keep count must be in [1, group width)");
+  if (cols % 4 != 0) return fail(EGT_EINVAL, "pack: columns must be a multiple of the group width");
+  if (rows && (!group_sizes || !w || !mask)) return fail(EGT_EINVAL, "gpu pack: null argument");
+  std::vector<uint32_t> goff(rows + 1, 0);
+  for (uint32_t r = 0; r < rows; ++r) {
+    if (group_sizes[r] == 0) return fail(EGT_EINVAL, "quantize: zero group size");
+    goff[r + 1] = goff[r] + (cols + group_sizes[r] - 1) / group_sizes[r];
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const uint64_t nnz = static_cast<uint64_t>(rows) * cols * n / 4;
+  const uint64_t n_scales = goff[rows];
+  Upload up;
+  Carve c;
+  const size_t o_words = c.add(((nnz + 7) / 8) * 2);
+  const size_t o_codes = c.add((nnz + 1) / 2);
+  const size_t o_gs = c.add(rows * 4ull);
+  const size_t o_goff = c.add((rows + 1ull) * 4);
+  const size_t o_sc = c.add(n_scales * 4);
+  const size_t o_zp = c.add(n_scales);
+  const size_t o_err = c.add(16);
+  const size_t o_tmp = c.add(nnz);  // one code per kept entry before nibble packing
+  CUDA_TRY(cudaMalloc(&up.base, c.total));
+  uint8_t* b = static_cast<uint8_t*>(up.base);
+  up.words = reinterpret_cast<uint16_t*>(b + o_words);
+  up.codes = b + o_codes;
+  up.gs = reinterpret_cast<uint32_t*>(b + o_gs);
+  up.goff = reinterpret_cast<uint32_t*>(b + o_goff);
+  up.scales = reinterpret_cast<float*>(b + o_sc);
+  up.zps = b + o_zp;
+  up.err = reinterpret_cast<uint32_t*>(b + o_err);
+  auto* first_bad = reinterpret_cast<unsigned long long*>(up.err);
+  CUDA_TRY(cudaMemsetAsync(up.err, 0xFF, 8, s));
+  CUDA_TRY(cudaMemsetAsync(up.err + 2, 0, 8, s));
+  if (rows) {
+    CUDA_TRY(cudaMemcpyAsync(up.gs, group_sizes, rows * 4ull, cudaMemcpyHostToDevice, s));
+    CUDA_TRY(cudaMemcpyAsync(up.goff, goff.data(), (rows + 1ull) * 4, cudaMemcpyHostToDevice, s));
+  }
+  CUDA_TRY(launch_check_nm(mask, rows, cols, n, first_bad, s));
+  unsigned long long bad = 0;
+  CUDA_TRY(cudaMemcpyAsync(&bad, first_bad, sizeof bad, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(cudaStreamSynchronize(s));
+  if (bad != ~0ull) {
+    const uint32_t r = static_cast<uint32_t>(bad / (cols / 4)), c0 = static_cast<uint32_t>(bad % (cols / 4)) * 4;
+    uint8_t bytes[2] = {0, 0};
+    const uint64_t bit = static_cast<uint64_t>(r) * cols + c0;
+    const uint64_t nbytes = (static_cast<uint64_t>(rows) * cols + 7) / 8;
+    CUDA_TRY(cudaMemcpy(bytes, mask + bit / 8, (bit / 8 + 1 < nbytes) ? 2 : 1, cudaMemcpyDeviceToHost));
+    const uint32_t word = bytes[0] | (static_cast<uint32_t>(bytes[1]) << 8);
+    int kept = 0;
+    for (int j = 0; j < 4; ++j) kept += (word >> ((bit % 8) + j)) & 1u;
+    return fail(EGT_EINVAL, "pack: group at row " + std::to_string(r) + ", column " + std::to_string(c0) +
+                                " keeps " + std::to_string(kept) + " entries (want " + std::to_string(n) + ")");
+  }
+  CUDA_TRY(launch_quantize_pack(w, mask, rows, cols, n, up.gs, up.goff, up.scales, up.zps, b + o_tmp, up.codes,
+                                up.words, s));
+  if (raw_out) {
+    if (nnz && (!raw_out->index_words || !raw_out->value_bytes))
+      return fail(EGT_EINVAL, "gpu pack: null output array");
+    if (nnz) {
+      CUDA_TRY(cudaMemcpyAsync(raw_out->index_words, up.words, ((nnz + 7) / 8) * 2, cudaMemcpyDeviceToDevice, s));
+      CUDA_TRY(cudaMemcpyAsync(raw_out->value_bytes, up.codes, (nnz + 1) / 2, cudaMemcpyDeviceToDevice, s));
+    }
+    if (raw_out->group_offsets)
+      CUDA_TRY(cudaMemcpyAsync(raw_out->group_offsets, up.goff, (rows + 1ull) * 4, cudaMemcpyDeviceToDevice, s));
+    if (n_scales && raw_out->scales)
+      CUDA_TRY(cudaMemcpyAsync(raw_out->scales, up.scales, n_scales * 4, cudaMemcpyDeviceToDevice, s));
+    if (n_scales && raw_out->zero_points)
+      CUDA_TRY(cudaMemcpyAsync(raw_out->zero_points, up.zps, n_scales, cudaMemcpyDeviceToDevice, s));
+  }
+  if (!out) {
+    CUDA_TRY(cudaStreamSynchronize(s));
+    return EGT_OK;
+  }
+  CUDA_TRY(cudaMemsetAsync(up.err, 0, 16, s));
+  const int format = n == 2 ? I4_SP24 : I4_SP14;
+  if (n != 1 && n != 2) return fail(EGT_EINVAL, "pack: keep count must be in [1, group width)");
+  return build_handle(format, static_cast<uint8_t>(n), EGT_KIND_INT4, rows, cols, nnz, group_sizes, n_scales, up,
+                      c.total, s, out);
+}
+
 egt_status egt_dev_dense_i4_create(const egt_quant_view* q, void* stream, egt_dev_packed** out) {
   using namespace egt_fmt;
   if (!out || !q) return fail(EGT_EINVAL, "egt_dev_dense_i4_create: null argument");

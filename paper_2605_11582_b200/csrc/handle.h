@@ -89,6 +89,17 @@ struct egt_peer_group {
 };
 
 namespace egt_impl {
+// GPU compression (compress.cu): importance_scores, prune_nm, the exact-N
+// check, and quantize + pack into the reference's stream layout.
+cudaError_t launch_importance(const float* w, const float* xn, const float* g, uint32_t rows, uint32_t cols,
+                              float* out, cudaStream_t s);
+cudaError_t launch_prune_nm(const float* scores, uint32_t rows, uint32_t cols, int n, uint8_t* mask,
+                            cudaStream_t s);
+cudaError_t launch_check_nm(const uint8_t* mask, uint32_t rows, uint32_t cols, int n,
+                            unsigned long long* first_bad, cudaStream_t s);
+cudaError_t launch_quantize_pack(const float* w, const uint8_t* mask, uint32_t rows, uint32_t cols, int n,
+                                 const uint32_t* gs, const uint32_t* goff, float* scales, uint8_t* zps,
+                                 uint8_t* codes_tmp, uint8_t* value_bytes, uint16_t* words, cudaStream_t s);
 // Signal this rank's (empty) slice and optionally wait for every peer's.
 cudaError_t launch_peer_signal(const egt_peer_group* g, bool signal, bool wait, cudaStream_t s);
 }  // namespace egt_impl

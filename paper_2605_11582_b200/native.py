@@ -203,7 +203,21 @@ _PEER_SIGNATURES = {
     "egt_peer_group_check": (C.c_int, [C.c_void_p]),
 }
 
+class GpuPackedOut(C.Structure):
+    _fields_ = [("index_words", C.c_void_p), ("value_bytes", C.c_void_p), ("group_offsets", C.c_void_p),
+                ("scales", C.c_void_p), ("zero_points", C.c_void_p)]
+
+
+_COMPRESS_SIGNATURES = {
+    "egt_gpu_importance": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p,
+                                     C.c_void_p]),
+    "egt_gpu_prune_nm": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
+    "egt_gpu_quantize_pack": (C.c_int, [C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_int, u32p,
+                                        C.POINTER(GpuPackedOut), C.c_void_p, C.POINTER(C.c_void_p)]),
+}
+
 SIGNATURES.update(_MODEL_SIGNATURES)
+SIGNATURES.update(_COMPRESS_SIGNATURES)
 SIGNATURES.update(_PEER_SIGNATURES)
 SIGNATURES.update(_PROGRAM_SIGNATURES)
 

@@ -313,3 +313,60 @@ def set_pdl(enabled: bool) -> None:
 
 def launch_count() -> int:
     return int(lib().egt_launch_count())
+
+
+# ---------------------------------------------------------------- GPU compression
+# (include/egt_b200.h egt_gpu_*) torch CUDA tensors in/out.
+def gpu_importance(w, x_norms, grad_abs, stream=None):
+    """importance_scores (compress.cpp:230-244) on the device."""
+    import torch
+
+    rows, cols = w.shape
+    out = torch.empty((rows, cols), dtype=torch.float32, device=w.device)
+    check(lib().egt_gpu_importance(C.c_void_p(w.data_ptr()), C.c_void_p(x_norms.data_ptr()),
+                                   C.c_void_p(grad_abs.data_ptr()), rows, cols, C.c_void_p(out.data_ptr()),
+                                   _stream_ptr(stream)))
+    return out
+
+
+def gpu_prune_nm(scores, n: int, m: int = 4, stream=None):
+    """prune_nm (compress.cpp:246-278): PruneMask bitmap (uint8 CUDA tensor)."""
+    import torch
+
+    rows, cols = scores.shape
+    mask = torch.empty(max(1, (rows * cols + 7) // 8), dtype=torch.uint8, device=scores.device)
+    check(lib().egt_gpu_prune_nm(C.c_void_p(scores.data_ptr()), rows, cols, n, m, C.c_void_p(mask.data_ptr()),
+                                 _stream_ptr(stream)))
+    return mask[: (rows * cols + 7) // 8]
+
+
+def gpu_quantize_pack(w, mask, n: int, group_sizes, stream=None, want_raw: bool = True, want_matrix: bool = True):
+    """quantize_matrix + pack on the device.  Returns (DeviceMatrix or None,
+    dict of the reference-layout arrays as CUDA tensors or None)."""
+    import torch
+
+    rows, cols = w.shape
+    gs = np.ascontiguousarray(np.broadcast_to(np.asarray(group_sizes, np.uint32), (rows,)))
+    nnz = rows * cols * n // 4
+    groups = int(sum((cols + int(g) - 1) // int(g) for g in gs)) if rows and np.all(gs > 0) else 0
+    raw = None
+    ro = None
+    if want_raw:
+        dev = w.device
+        raw = {"index_words": torch.empty(max(1, (nnz + 7) // 8), dtype=torch.int16, device=dev),
+               "value_bytes": torch.empty(max(1, (nnz + 1) // 2), dtype=torch.uint8, device=dev),
+               "group_offsets": torch.empty(rows + 1, dtype=torch.int32, device=dev),
+               "scales": torch.empty(max(1, groups), dtype=torch.float32, device=dev),
+               "zero_points": torch.empty(max(1, groups), dtype=torch.uint8, device=dev)}
+        ro = N.GpuPackedOut(*[C.c_void_p(raw[k].data_ptr()) for k in
+                              ("index_words", "value_bytes", "group_offsets", "scales", "zero_points")])
+    h = C.c_void_p()
+    check(lib().egt_gpu_quantize_pack(C.c_void_p(w.data_ptr()), C.c_void_p(mask.data_ptr()), rows, cols, n,
+                                      _p(gs, N.u32p), C.byref(ro) if ro is not None else None, _stream_ptr(stream),
+                                      C.byref(h) if want_matrix else None))
+    if raw is not None:
+        raw["index_words"] = raw["index_words"][: (nnz + 7) // 8]
+        raw["value_bytes"] = raw["value_bytes"][: (nnz + 1) // 2]
+        raw["scales"] = raw["scales"][:groups]
+        raw["zero_points"] = raw["zero_points"][:groups]
+    return (DeviceMatrix(h.value) if want_matrix else None), raw

@@ -271,3 +271,18 @@ def test_port_matches_live_reference(port, ref):
         assert np.array_equal(pp.value_bytes, pr.value_bytes)
         x = rng.uniform(-1, 1, cols).astype(np.float32)
         assert np.array_equal(port.spmv(pp, x).view(np.uint32), ref.spmv(pr, x).view(np.uint32))
+
+
+def test_importance_prune_port_matches_reference(port, ref):
+    """The oracle port's importance_scores / prune_nm against the unmodified
+    reference (compress.cpp:230-278) on ties, zeros and negative scores."""
+    P, R = port, ref
+    rng = np.random.default_rng(17)
+    for rows, cols in [(7, 13), (16, 64), (33, 130)]:
+        w = rng.normal(size=(rows, cols)).astype(np.float32)
+        xn = rng.uniform(0, 2, cols).astype(np.float32)
+        g = np.abs(rng.normal(size=(rows, cols))).astype(np.float32)
+        assert np.array_equal(P.importance(w, xn, g).view(np.uint32), R.importance(w, xn, g).view(np.uint32))
+        s = (np.round(rng.normal(size=(rows, cols)) * 2) / 2).astype(np.float32)
+        for n in (1, 2, 3):
+            assert np.array_equal(P.prune_nm(s, n), R.prune_nm(s, n))
