@@ -234,6 +234,24 @@ EGT_API egt_status egt_model_destroy(egt_model* m);
 EGT_API egt_status egt_forward(const egt_model* m, const int32_t* tokens, const int32_t* positions,
                                const uint8_t* mask_bits, uint32_t M, float* logits_dev, void* stream);
 
+/* The verify pass's forward with the prefix-tree mask built on the device
+ * from the compact encoding flatten_subtree already produces (SURVEY 8(f)
+ * row 4; decode.cpp:209-299) instead of an M x M host bitmap: rows
+ * [b*padded_len, (b+1)*padded_len) are beam b's committed block (left-padded
+ * to committed_len[b] tokens, causal), then one row per flattened node f
+ * (DFS order) that sees its beam's committed block, its ancestors (parent[f],
+ * -1 for a root, always an earlier node of the same beam) and itself.
+ * M = n_beams * padded_len + n_nodes; tokens / positions as egt_forward. */
+typedef struct egt_tree_view {
+  uint32_t n_beams, padded_len;
+  const uint32_t* committed_len; /* [n_beams] */
+  uint32_t n_nodes;
+  const int32_t* parent;         /* [n_nodes] */
+  const uint32_t* beam;          /* [n_nodes] */
+} egt_tree_view;
+EGT_API egt_status egt_forward_tree(const egt_model* m, const int32_t* tokens, const int32_t* positions,
+                                    const egt_tree_view* tree, float* logits_dev, void* stream);
+
 /* out[i] = src_dev[rows[i] * ld + cols[i]] (host index lists, host output). */
 EGT_API egt_status egt_gather(const float* src_dev, uint64_t ld, const uint32_t* rows,
                               const uint32_t* cols, uint32_t n, float* out, void* stream);

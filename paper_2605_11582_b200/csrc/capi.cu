@@ -64,6 +64,7 @@ struct Workspace {
   size_t partial_floats = 0;
   uint32_t* counters = nullptr;
   size_t n_counters = 0;
+  int flip = 0;  // independent split-K launches alternate between two halves
 };
 std::mutex g_ws_mu;
 std::map<std::pair<int, cudaStream_t>, Workspace> g_ws;
@@ -628,12 +629,16 @@ egt_status spmv_impl(const egt_dev_packed* h, const float* x, float* y, uint32_t
   }
   if (sc.smem == 0) return fail(EGT_EINTERNAL, "spmv: no feasible launch plan for this shape and token count");
   if (sc.S > 1) {
+    // Independent launches overlap their predecessor, but a product starts
+    // only after every kernel before its predecessor finished: two
+    // alternating workspace halves are enough.
+    const size_t fl = tiled_workspace_floats(h, sc, M), nc = static_cast<size_t>(sc.grid_x) * sc.grid_z;
     Workspace* w = nullptr;
-    egt_status st = get_workspace(s, tiled_workspace_floats(h, sc, M),
-                                  static_cast<size_t>(sc.grid_x) * sc.grid_z, &w);
+    egt_status st = get_workspace(s, 2 * fl, 2 * nc, &w);
     if (st != EGT_OK) return st;
-    ctx.partial = w->partial;
-    ctx.counters = w->counters;
+    const int half = indep ? (w->flip ^= 1) : 0;
+    ctx.partial = w->partial + half * fl;
+    ctx.counters = w->counters + half * nc;
   }
   CUDA_TRY(launch_tiled(h, sc, x, static_cast<int>(ldx), static_cast<int>(M), y,
                         static_cast<int>(ldy), ctx, indep));
@@ -677,12 +682,13 @@ egt_status egt_spmv_fused_multi(const egt_dev_packed* const* hs, uint32_t n, con
   const TiledSchedule sc = plan_tiled_rt(h, h->tiled.RT * static_cast<int>(n), 1, num_sms(), indep);
   if (sc.smem == 0) return fail(EGT_EINTERNAL, "spmv: no feasible launch plan for this shape and token count");
   if (sc.S > 1) {
+    const size_t fl = static_cast<size_t>(sc.S) * h->tiled.RT * n * 16, nc = static_cast<size_t>(sc.grid_x) * sc.grid_z;
     Workspace* w = nullptr;
-    egt_status st = get_workspace(s, static_cast<size_t>(sc.S) * h->tiled.RT * n * 16,
-                                  static_cast<size_t>(sc.grid_x) * sc.grid_z, &w);
+    egt_status st = get_workspace(s, 2 * fl, 2 * nc, &w);
     if (st != EGT_OK) return st;
-    ctx.partial = w->partial;
-    ctx.counters = w->counters;
+    const int half = indep ? (w->flip ^= 1) : 0;
+    ctx.partial = w->partial + half * fl;
+    ctx.counters = w->counters + half * nc;
   }
   CUDA_TRY(launch_tiled(h, sc, x, static_cast<int>(h->cols), 1, ys[0], static_cast<int>(h->rows), ctx, indep));
   return EGT_OK;

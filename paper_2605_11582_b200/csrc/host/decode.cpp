@@ -6,6 +6,7 @@
 // switch to parallel verification happens.  Only the forward pass changes: it
 // is one egt_forward call on the B200 over the packed layers.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -18,6 +19,8 @@
 #include "egt_b200/packed.hpp"
 
 namespace egt_b200 {
+// EGT_DENSE_TREE_MASK: upload the dense M x M bitmap instead (A/B, tests)
+const bool g_dense_tree_mask = std::getenv("EGT_DENSE_TREE_MASK") != nullptr;
 
 namespace {
 
@@ -53,8 +56,8 @@ struct RowRequest {
 
 std::vector<std::vector<float>> score_rows(const egt_model* model, const PrefixTrie& trie,
                                            const std::vector<int>& tokens, const std::vector<int>& positions,
-                                           const std::vector<uint8_t>& bits, const std::vector<RowRequest>& reqs,
-                                           uint32_t vocab, void* stream) {
+                                           const std::vector<uint8_t>* bits, const egt_tree_view* tree,
+                                           const std::vector<RowRequest>& reqs, uint32_t vocab, void* stream) {
   const uint32_t M = static_cast<uint32_t>(tokens.size());
   std::vector<uint32_t> rows, cols;
   for (const RowRequest& r : reqs)
@@ -71,7 +74,8 @@ std::vector<std::vector<float>> score_rows(const egt_model* model, const PrefixT
       cudaSuccess)
     throw CudaError("decode: logits allocation failed");
   std::vector<float> vals(rows.size());
-  egt_status st = egt_forward(model, tokens.data(), positions.data(), bits.data(), M, logits, stream);
+  egt_status st = tree ? egt_forward_tree(model, tokens.data(), positions.data(), tree, logits, stream)
+                      : egt_forward(model, tokens.data(), positions.data(), bits->data(), M, logits, stream);
   if (st == EGT_OK)
     st = egt_gather(logits, vocab, rows.data(), cols.data(), static_cast<uint32_t>(rows.size()), vals.data(), stream);
   cudaFreeAsync(logits, s);
@@ -196,7 +200,7 @@ FlattenedSubtree flatten_subtree(const DecodeSession& s, const PrefixTrie& trie)
   return f;
 }
 
-TreeMask build_tree_mask(const FlattenedSubtree& flat, const DecodeSession& s) {
+TreeMask build_tree_mask(const FlattenedSubtree& flat, const DecodeSession& s, bool with_bits) {
   require(!s.beams.empty(), "decode: session has no beams");
   require(!flat.nodes.empty(), "decode: empty flattened subtree");
   TreeMask m;
@@ -212,7 +216,7 @@ TreeMask build_tree_mask(const FlattenedSubtree& flat, const DecodeSession& s) {
   m.flat_offset = static_cast<size_t>(nb) * lmax;
   m.rows = static_cast<uint32_t>(m.flat_offset + flat.nodes.size());
   const size_t R = m.rows;
-  m.bits.assign((R * R + 7) / 8, 0);
+  if (with_bits) m.bits.assign((R * R + 7) / 8, 0);
   m.tokens.assign(R, static_cast<int>(kPadToken));  // pad rows: token 0, position 0, invisible
   m.positions.assign(R, 0);
   for (uint32_t b = 0; b < nb; ++b) {  // committed blocks, left-padded, causal
@@ -221,7 +225,8 @@ TreeMask build_tree_mask(const FlattenedSubtree& flat, const DecodeSession& s) {
     for (size_t j = 0; j < seq.size(); ++j) {
       m.tokens[first + j] = seq[j];
       m.positions[first + j] = static_cast<int>(j);
-      for (size_t k = 0; k <= j; ++k) set_bit(m.bits, (first + j) * R + first + k);
+      if (with_bits)
+        for (size_t k = 0; k <= j; ++k) set_bit(m.bits, (first + j) * R + first + k);
     }
   }
   for (size_t f = 0; f < flat.nodes.size(); ++f) {  // node rows: committed + ancestors + self
@@ -234,6 +239,7 @@ TreeMask build_tree_mask(const FlattenedSubtree& flat, const DecodeSession& s) {
     m.tokens[r] = static_cast<int>(fn.token);
     m.positions[r] = static_cast<int>(len + fn.depth);
     const size_t first = static_cast<size_t>(fn.beam) * lmax + (lmax - len);
+    if (!with_bits) continue;
     for (size_t j = 0; j < len; ++j) set_bit(m.bits, r * R + first + j);
     for (int32_t p = static_cast<int32_t>(f); p >= 0; p = flat.nodes[p].parent) set_bit(m.bits, r * R + m.flat_offset + p);
   }
@@ -291,8 +297,20 @@ VerificationResult verify_parallel(const egt_model* model, DecodeSession& s, con
       row_at[f] = static_cast<int>(reqs.size());
       reqs.push_back({static_cast<uint32_t>(mask.flat_offset + f), flat.nodes[f].trie_node});
     }
-  const std::vector<std::vector<float>> scored =
-      score_rows(model, trie, mask.tokens, mask.positions, mask.bits, reqs, vocab_of(model), stream);
+  std::vector<std::vector<float>> scored;
+  if (mask.bits.empty()) {  // compact tree encoding: the device builds the mask
+    std::vector<int32_t> parent(flat.nodes.size());
+    std::vector<uint32_t> beam(flat.nodes.size());
+    for (size_t f = 0; f < flat.nodes.size(); ++f) {
+      parent[f] = flat.nodes[f].parent;
+      beam[f] = flat.nodes[f].beam;
+    }
+    egt_tree_view tv{static_cast<uint32_t>(nb), mask.padded_len, mask.committed_len.data(),
+                     static_cast<uint32_t>(flat.nodes.size()), parent.data(), beam.data()};
+    scored = score_rows(model, trie, mask.tokens, mask.positions, nullptr, &tv, reqs, vocab_of(model), stream);
+  } else {
+    scored = score_rows(model, trie, mask.tokens, mask.positions, &mask.bits, nullptr, reqs, vocab_of(model), stream);
+  }
   s.forward_passes += 1;
   s.flattened_nodes = flat.nodes.size();
 
@@ -370,7 +388,7 @@ void constrained_step(const egt_model* model, DecodeSession& s, const PrefixTrie
   for (size_t a = 0; a < active.size(); ++a)
     reqs.push_back({static_cast<uint32_t>(start[a] + len[a] - 1), s.beams[active[a]].node});
   const std::vector<std::vector<float>> rows =
-      score_rows(model, trie, tokens, positions, bits, reqs, vocab_of(model), stream);
+      score_rows(model, trie, tokens, positions, &bits, nullptr, reqs, vocab_of(model), stream);
   s.forward_passes += 1;
 
   struct Cand {
@@ -450,7 +468,7 @@ DecodeResult decode(const egt_model* model, const PrefixTrie& trie, std::vector<
       fire = s.steps >= opt.forced_depth;
     if (fire) {
       const FlattenedSubtree flat = flatten_subtree(s, trie);
-      const TreeMask mask = build_tree_mask(flat, s);
+      const TreeMask mask = build_tree_mask(flat, s, g_dense_tree_mask);
       const VerificationResult vr = verify_parallel(model, s, trie, flat, mask, opt.beam_size, stream);
       s.trigger_step = s.steps;
       for (const VerifiedLeaf& l : vr.selected) out.sequences.push_back({l.tokens, l.score, l.payload});
@@ -535,7 +553,7 @@ extern "C" EGT_API egt_status egt_verify_parallel(const egt_model* m, const egt_
     const egt_b200::PrefixTrie t = egt_b200::PrefixTrie::from_parents(*trie);
     egt_b200::DecodeSession s = session_of(*session);
     const egt_b200::FlattenedSubtree flat = egt_b200::flatten_subtree(s, t);
-    const egt_b200::TreeMask mask = egt_b200::build_tree_mask(flat, s);
+    const egt_b200::TreeMask mask = egt_b200::build_tree_mask(flat, s, egt_b200::g_dense_tree_mask);
     const egt_b200::VerificationResult r = egt_b200::verify_parallel(m, s, t, flat, mask, beam_size, stream);
     fill_out(out, r.selected, beam_size);
     for (uint32_t j = 0; j < out->n_selected; ++j) out->beam[j] = r.selected[j].beam;

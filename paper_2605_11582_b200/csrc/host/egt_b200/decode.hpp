@@ -119,7 +119,9 @@ struct VerificationResult {
 std::vector<float> restricted_log_softmax(const std::vector<float>& child_logits);
 
 FlattenedSubtree flatten_subtree(const DecodeSession& session, const PrefixTrie& trie);
-TreeMask build_tree_mask(const FlattenedSubtree& flat, const DecodeSession& session);
+// with_bits = false skips the dense M x M bitmap (the device builds the mask
+// from the compact encoding, egt_forward_tree); tokens / positions are kept.
+TreeMask build_tree_mask(const FlattenedSubtree& flat, const DecodeSession& session, bool with_bits = true);
 // rows: per node the restricted log-probs of its children (indexed like
 // trie.nodes[node].children); seeds likewise per beam.
 std::vector<double> accumulate_bscores(const FlattenedSubtree& flat, const PrefixTrie& trie,

@@ -150,6 +150,140 @@ unsigned grid_for(size_t n) { return static_cast<unsigned>(std::min<size_t>((n +
 
 }  // namespace
 
+namespace {
+
+// The prefix-tree mask straight from the compact encoding (SURVEY 8(f) row
+// 4): block per row q; committed rows see their beam's committed tokens up to
+// themselves (left-padded, pad rows see nothing), node rows see their beam's
+// committed block plus their ancestors and themselves (build_tree_mask,
+// decode.cpp:240-299).  mask: u32 words, bit q*M+k LSB-first, zeroed.
+__global__ void tree_mask_kernel(uint32_t* mask, int M, int nb, int lmax, const uint32_t* committed,
+                                 const int32_t* parent, const uint32_t* beam) {
+  extern __shared__ uint8_t anc[];  // [n_nodes] ancestor-or-self flags of this row's node
+  const int q = blockIdx.x, F = nb * lmax, nn = M - F;
+  int lo = 0, hi = 0;  // committed key range [lo, hi) visible to row q
+  bool node = q >= F;
+  if (!node) {
+    const int b = q / lmax, first = b * lmax + (lmax - static_cast<int>(committed[b]));
+    if (q >= first) lo = first, hi = q + 1;
+  } else {
+    const int f = q - F, b = static_cast<int>(beam[f]);
+    lo = b * lmax + (lmax - static_cast<int>(committed[b]));
+    hi = (b + 1) * lmax;
+    for (int i = threadIdx.x; i < nn; i += blockDim.x) anc[i] = 0;
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int p = f; p >= 0; p = parent[p]) anc[p] = 1;
+    __syncthreads();
+  }
+  for (int k = threadIdx.x; k < M; k += blockDim.x) {
+    const bool vis = (k >= lo && k < hi) || (node && k >= F && anc[k - F]);
+    if (vis) {
+      const uint64_t bit = static_cast<uint64_t>(q) * M + k;
+      atomicOr(mask + (bit >> 5), 1u << (bit & 31));
+    }
+  }
+}
+
+egt_status forward_core(const egt_model* m, const int32_t* tokens, const int32_t* positions,
+                        const uint8_t* mask_bits, const egt_tree_view* tree, uint32_t M, float* logits,
+                        void* stream) {
+  if (!m || !tokens || !positions || !logits) return fail(EGT_EINVAL, "forward: null argument");
+  const egt_model_config& c = m->cfg;
+  if (M == 0) return fail(EGT_EINVAL, "forward: empty token sequence");  // model.cpp:123
+  for (uint32_t i = 0; i < M; ++i) {                                        // model.cpp:128-135
+    if (tokens[i] < 0 || static_cast<uint32_t>(tokens[i]) >= c.vocab_size)
+      return fail(EGT_EINVAL, "forward: token out of range");
+    if (positions[i] < 0 || static_cast<uint32_t>(positions[i]) >= c.max_positions)
+      return fail(EGT_EINVAL, "forward: position out of range");
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const size_t d = c.d_model, dff = c.d_ff, H = c.n_heads, dh = d / H;
+  const size_t Md = M * d;
+  const size_t mask_bytes = (static_cast<size_t>(M) * M + 31) / 32 * 4;
+  const size_t tree_ints = tree ? tree->n_beams + 2ull * tree->n_nodes : 0;
+  const size_t floats = 6 * Md + M * dff + H * static_cast<size_t>(M) * M;
+  char* scratch = nullptr;
+  MCUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch),
+                        floats * sizeof(float) + 2 * M * sizeof(int) + mask_bytes + tree_ints * 4 + 64, s));
+  float* x = reinterpret_cast<float*>(scratch);
+  float* a = x + Md;
+  float* q = a + Md;
+  float* k = q + Md;
+  float* v = k + Md;
+  float* o = v + Md;
+  float* f1 = o + Md;
+  float* S = f1 + M * dff;
+  int* dtok = reinterpret_cast<int*>(S + H * static_cast<size_t>(M) * M);
+  int* dpos = dtok + M;
+  uint8_t* dmask = reinterpret_cast<uint8_t*>(dpos + M);
+  egt_status st = EGT_OK;
+  auto lin = [&](const egt_dev_packed* h, const float* in, float* outp, uint32_t flags) {
+    if (st == EGT_OK) st = egt_spmv_ex(h, in, outp, M, h->cols, h->rows, flags, stream);
+  };
+  cudaMemcpyAsync(dtok, tokens, M * sizeof(int), cudaMemcpyHostToDevice, s);
+  cudaMemcpyAsync(dpos, positions, M * sizeof(int), cudaMemcpyHostToDevice, s);
+  if (tree) {
+    uint32_t* dcommit = reinterpret_cast<uint32_t*>(dmask + mask_bytes);
+    int32_t* dparent = reinterpret_cast<int32_t*>(dcommit + tree->n_beams);
+    uint32_t* dbeam = reinterpret_cast<uint32_t*>(dparent + tree->n_nodes);
+    cudaMemsetAsync(dmask, 0, mask_bytes, s);
+    if (tree->n_beams) cudaMemcpyAsync(dcommit, tree->committed_len, tree->n_beams * 4ull, cudaMemcpyHostToDevice, s);
+    if (tree->n_nodes) {
+      cudaMemcpyAsync(dparent, tree->parent, tree->n_nodes * 4ull, cudaMemcpyHostToDevice, s);
+      cudaMemcpyAsync(dbeam, tree->beam, tree->n_nodes * 4ull, cudaMemcpyHostToDevice, s);
+    }
+    tree_mask_kernel<<<M, 256, tree->n_nodes, s>>>(reinterpret_cast<uint32_t*>(dmask), static_cast<int>(M),
+                                                   static_cast<int>(tree->n_beams), static_cast<int>(tree->padded_len),
+                                                   dcommit, dparent, dbeam);
+    ++launch_counter();
+  } else {
+    cudaMemcpyAsync(dmask, mask_bits, (static_cast<size_t>(M) * M + 7) / 8, cudaMemcpyHostToDevice, s);
+  }
+  embed_kernel<<<M, 256, 0, s>>>(dtok, dpos, m->emb, m->pos, x, static_cast<int>(M), static_cast<int>(d));
+  ++launch_counter();
+  const float att_scale = 1.0f / std::sqrt(static_cast<float>(dh));  // model.cpp:139
+  const dim3 tb(16, 16);
+  for (uint32_t l = 0; l < c.n_layers && st == EGT_OK; ++l) {
+    const egt_dev_packed* const* w = m->layers.data() + 6 * l;
+    rmsnorm_kernel<<<M, 256, 0, s>>>(x, a, static_cast<int>(d));
+    ++launch_counter();
+    lin(w[0], a, q, 0);
+    lin(w[1], a, k, EGT_SPMV_INDEPENDENT);  // K and V read `a`, not the previous product
+    lin(w[2], a, v, EGT_SPMV_INDEPENDENT);
+    // scores per head: S[h] = (q_h k_h^T) * scale
+    attn_gemm_kernel<true><<<dim3((M + 15) / 16, (M + 15) / 16, H), tb, 0, s>>>(
+        q, static_cast<int>(d), dh, k, static_cast<int>(d), dh, S, static_cast<int>(M),
+        static_cast<size_t>(M) * M, static_cast<int>(M), static_cast<int>(M), static_cast<int>(dh), att_scale);
+    masked_softmax_kernel<<<(M * H + 7) / 8, 256, 0, s>>>(S, dmask, static_cast<int>(M), static_cast<int>(H));
+    attn_gemm_kernel<false><<<dim3((dh + 15) / 16, (M + 15) / 16, H), tb, 0, s>>>(
+        S, static_cast<int>(M), static_cast<size_t>(M) * M, v, static_cast<int>(d), dh, o, static_cast<int>(d),
+        dh, static_cast<int>(M), static_cast<int>(dh), static_cast<int>(M), 1.0f);
+    launch_counter() += 3;
+    lin(w[3], o, a, 0);  // a <- o Wo^T
+    add_kernel<<<grid_for(Md), 256, 0, s>>>(x, a, Md);
+    rmsnorm_kernel<<<M, 256, 0, s>>>(x, a, static_cast<int>(d));
+    launch_counter() += 2;
+    lin(w[4], a, f1, 0);
+    silu_kernel<<<grid_for(M * dff), 256, 0, s>>>(f1, M * dff);
+    ++launch_counter();
+    lin(w[5], f1, a, 0);
+    add_kernel<<<grid_for(Md), 256, 0, s>>>(x, a, Md);
+    ++launch_counter();
+  }
+  if (st == EGT_OK) {
+    rmsnorm_kernel<<<M, 256, 0, s>>>(x, a, static_cast<int>(d));
+    ++launch_counter();
+    lin(m->head, a, logits, 0);
+  }
+  cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(scratch, s);
+  if (st != EGT_OK) return st;
+  if (e != cudaSuccess) return fail(EGT_ECUDA, std::string("forward: ") + cudaGetErrorString(e));
+  return EGT_OK;
+}
+}  // namespace
+
 extern "C" {
 
 egt_status egt_model_create(const egt_model_config* cfg, const float* embedding,
@@ -220,85 +354,30 @@ egt_status egt_model_destroy(egt_model* m) {
   return EGT_OK;
 }
 
+
 egt_status egt_forward(const egt_model* m, const int32_t* tokens, const int32_t* positions,
                        const uint8_t* mask_bits, uint32_t M, float* logits, void* stream) {
-  if (!m || !tokens || !positions || !mask_bits || !logits) return fail(EGT_EINVAL, "forward: null argument");
-  const egt_model_config& c = m->cfg;
-  if (M == 0) return fail(EGT_EINVAL, "forward: empty token sequence");  // model.cpp:123
-  for (uint32_t i = 0; i < M; ++i) {                                        // model.cpp:128-135
-    if (tokens[i] < 0 || static_cast<uint32_t>(tokens[i]) >= c.vocab_size)
-      return fail(EGT_EINVAL, "forward: token out of range");
-    if (positions[i] < 0 || static_cast<uint32_t>(positions[i]) >= c.max_positions)
-      return fail(EGT_EINVAL, "forward: position out of range");
-  }
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const size_t d = c.d_model, dff = c.d_ff, H = c.n_heads, dh = d / H;
-  const size_t Md = M * d;
-  const size_t mask_bytes = (static_cast<size_t>(M) * M + 7) / 8;
-  const size_t floats = 6 * Md + M * dff + H * static_cast<size_t>(M) * M;
-  char* scratch = nullptr;
-  MCUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch),
-                        floats * sizeof(float) + 2 * M * sizeof(int) + mask_bytes + 64, s));
-  float* x = reinterpret_cast<float*>(scratch);
-  float* a = x + Md;
-  float* q = a + Md;
-  float* k = q + Md;
-  float* v = k + Md;
-  float* o = v + Md;
-  float* f1 = o + Md;
-  float* S = f1 + M * dff;
-  int* dtok = reinterpret_cast<int*>(S + H * static_cast<size_t>(M) * M);
-  int* dpos = dtok + M;
-  uint8_t* dmask = reinterpret_cast<uint8_t*>(dpos + M);
-  egt_status st = EGT_OK;
-  auto lin = [&](const egt_dev_packed* h, const float* in, float* outp, uint32_t flags) {
-    if (st == EGT_OK) st = egt_spmv_ex(h, in, outp, M, h->cols, h->rows, flags, stream);
-  };
-  cudaMemcpyAsync(dtok, tokens, M * sizeof(int), cudaMemcpyHostToDevice, s);
-  cudaMemcpyAsync(dpos, positions, M * sizeof(int), cudaMemcpyHostToDevice, s);
-  cudaMemcpyAsync(dmask, mask_bits, mask_bytes, cudaMemcpyHostToDevice, s);
-  embed_kernel<<<M, 256, 0, s>>>(dtok, dpos, m->emb, m->pos, x, static_cast<int>(M), static_cast<int>(d));
-  ++launch_counter();
-  const float att_scale = 1.0f / std::sqrt(static_cast<float>(dh));  // model.cpp:139
-  const dim3 tb(16, 16);
-  for (uint32_t l = 0; l < c.n_layers && st == EGT_OK; ++l) {
-    const egt_dev_packed* const* w = m->layers.data() + 6 * l;
-    rmsnorm_kernel<<<M, 256, 0, s>>>(x, a, static_cast<int>(d));
-    ++launch_counter();
-    lin(w[0], a, q, 0);
-    lin(w[1], a, k, EGT_SPMV_INDEPENDENT);  // K and V read `a`, not the previous product
-    lin(w[2], a, v, EGT_SPMV_INDEPENDENT);
-    // scores per head: S[h] = (q_h k_h^T) * scale
-    attn_gemm_kernel<true><<<dim3((M + 15) / 16, (M + 15) / 16, H), tb, 0, s>>>(
-        q, static_cast<int>(d), dh, k, static_cast<int>(d), dh, S, static_cast<int>(M),
-        static_cast<size_t>(M) * M, static_cast<int>(M), static_cast<int>(M), static_cast<int>(dh), att_scale);
-    masked_softmax_kernel<<<(M * H + 7) / 8, 256, 0, s>>>(S, dmask, static_cast<int>(M), static_cast<int>(H));
-    attn_gemm_kernel<false><<<dim3((dh + 15) / 16, (M + 15) / 16, H), tb, 0, s>>>(
-        S, static_cast<int>(M), static_cast<size_t>(M) * M, v, static_cast<int>(d), dh, o, static_cast<int>(d),
-        dh, static_cast<int>(M), static_cast<int>(dh), static_cast<int>(M), 1.0f);
-    launch_counter() += 3;
-    lin(w[3], o, a, 0);  // a <- o Wo^T
-    add_kernel<<<grid_for(Md), 256, 0, s>>>(x, a, Md);
-    rmsnorm_kernel<<<M, 256, 0, s>>>(x, a, static_cast<int>(d));
-    launch_counter() += 2;
-    lin(w[4], a, f1, 0);
-    silu_kernel<<<grid_for(M * dff), 256, 0, s>>>(f1, M * dff);
-    ++launch_counter();
-    lin(w[5], f1, a, 0);
-    add_kernel<<<grid_for(Md), 256, 0, s>>>(x, a, Md);
-    ++launch_counter();
-  }
-  if (st == EGT_OK) {
-    rmsnorm_kernel<<<M, 256, 0, s>>>(x, a, static_cast<int>(d));
-    ++launch_counter();
-    lin(m->head, a, logits, 0);
-  }
-  cudaError_t e = cudaGetLastError();
-  cudaFreeAsync(scratch, s);
-  if (st != EGT_OK) return st;
-  if (e != cudaSuccess) return fail(EGT_ECUDA, std::string("forward: ") + cudaGetErrorString(e));
-  return EGT_OK;
+  if (!mask_bits) return fail(EGT_EINVAL, "forward: null argument");
+  return forward_core(m, tokens, positions, mask_bits, nullptr, M, logits, stream);
 }
+
+egt_status egt_forward_tree(const egt_model* m, const int32_t* tokens, const int32_t* positions,
+                            const egt_tree_view* t, float* logits, void* stream) {
+  if (!t || (t->n_beams && !t->committed_len) || (t->n_nodes && (!t->parent || !t->beam)))
+    return fail(EGT_EINVAL, "forward: null argument");
+  const uint64_t M64 = static_cast<uint64_t>(t->n_beams) * t->padded_len + t->n_nodes;
+  if (M64 == 0 || M64 > 65536) return fail(EGT_EINVAL, "forward: tree rows must be 1..65536");
+  for (uint32_t b = 0; b < t->n_beams; ++b)
+    if (t->committed_len[b] > t->padded_len) return fail(EGT_EINVAL, "decode: committed length above the padded length");
+  for (uint32_t f = 0; f < t->n_nodes; ++f) {  // build_tree_mask's checks (decode.cpp:278-281)
+    if (t->beam[f] >= t->n_beams) return fail(EGT_EINVAL, "decode: flattened node references a missing beam");
+    const int32_t p = t->parent[f];
+    if (p >= 0 && (static_cast<uint32_t>(p) >= f || t->beam[p] != t->beam[f]))
+      return fail(EGT_EINVAL, "decode: flattened parent does not precede its child");
+  }
+  return forward_core(m, tokens, positions, nullptr, t, static_cast<uint32_t>(M64), logits, stream);
+}
+
 
 egt_status egt_gather(const float* src, uint64_t ld, const uint32_t* rows, const uint32_t* cols,
                       uint32_t n, float* out, void* stream) {

@@ -577,7 +577,10 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
   const int cidx = blockIdx.x + gridDim.x * blockIdx.z;
   if (tid == 0) s_last = (atomicAdd(a.counters + cidx, 1u) == static_cast<uint32_t>(a.S - 1));
   __syncthreads();
-  if (!s_last) return;
+  if (!s_last) {
+    if (a.indep) pdl_wait();
+    return;
+  }
   __threadfence();
   for (int idx = tid; idx < nOut; idx += blockDim.x) {
     const int row16 = idx & 15, tl = (idx >> 4) % Mc, i = (idx >> 4) / Mc;
@@ -594,6 +597,7 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
   }
   if (tid == 0) a.counters[cidx] = 0u;  // ready for the next launch / graph replay
   if (FUSED && a.npeer > 0) peer_complete(a, gridDim.x * gridDim.z);
+  if (a.indep) pdl_wait();
 }
 
 // ---------------------------------------------------------------- planning
@@ -682,7 +686,7 @@ TiledSchedule plan_tiled_rt(const egt_dev_packed* h, int RT, int M, int num_sms,
     const int KC = (KQ + S - 1) / S;
     if (S > 1 && (S - 1) * KC >= KQ) continue;
     if (g_force[4] && S != g_force[1]) continue;
-    if (indep && S > 1) continue;  // concurrent independent launches share no workspace
+    if (indep && S > 1 && !g_force[4]) continue;  // (forced plans: split-K with the alternating workspaces)
     for (int RB = 1; RB <= 128; ++RB) {
       if (g_force[4] && RB != g_force[0]) continue;
       const long grid = static_cast<long>((RT + RB - 1) / RB) * S * NB;
@@ -869,7 +873,7 @@ cudaError_t launch_tiled(const egt_dev_packed* h, const TiledSchedule& sc, const
   a.CH = sc.CH;
   static const int dbg = getenv("EGT_DEBUG_MODE") ? atoi(getenv("EGT_DEBUG_MODE")) : 0;
   a.dbg = dbg;
-  a.indep = indep && sc.S == 1 ? 1 : 0;
+  a.indep = indep ? 1 : 0;  // split-K workspaces alternate for independent launches (capi.cu)
   void* fn = pick_kernel(h->format, h->tiled.SS, M == 1 ? 0 : sc.NT, a.xform != 0 || a.res != nullptr || a.pf_ptr[0] || a.out_silu || a.nseg > 1 || a.npeer > 0);
   cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(sc.smem));

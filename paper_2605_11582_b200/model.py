@@ -110,6 +110,25 @@ class DeviceModel:
                                  _stream_ptr(stream)))
         return out
 
+    def forward_tree(self, tokens, positions, committed_len, padded_len: int, parent, beam, stream=None):
+        """forward with the prefix-tree mask built on the device from the
+        compact encoding (egt_forward_tree): committed blocks of padded_len rows
+        per beam, then one row per flattened node (parent index, beam)."""
+        import torch
+
+        t = np.ascontiguousarray(tokens, np.int32)
+        p = np.ascontiguousarray(positions, np.int32)
+        cl = np.ascontiguousarray(committed_len, np.uint32)
+        par = np.ascontiguousarray(parent, np.int32)
+        bm = np.ascontiguousarray(beam, np.uint32)
+        view = N.TreeView(cl.size, padded_len, cl.ctypes.data_as(N.u32p), par.size,
+                          par.ctypes.data_as(C.POINTER(C.c_int32)), bm.ctypes.data_as(N.u32p))
+        out = torch.empty((t.size, self.cfg["vocab_size"]), dtype=torch.float32, device="cuda")
+        check(_lib().egt_forward_tree(self._h, t.ctypes.data_as(C.POINTER(C.c_int32)),
+                                      p.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(view),
+                                      C.c_void_p(out.data_ptr()), _stream_ptr(stream)))
+        return out
+
     def verify_parallel(self, trie: Trie, prompt, beams: list, beam_size: int, stream=None):
         """flatten_subtree + build_tree_mask + verify_parallel (decode.cpp:209-421)."""
         tv = trie.view()

@@ -155,6 +155,14 @@ _MODEL_SIGNATURES = {
 }
 
 
+class TreeView(C.Structure):
+    _fields_ = [("n_beams", C.c_uint32), ("padded_len", C.c_uint32), ("committed_len", u32p),
+                ("n_nodes", C.c_uint32), ("parent", C.POINTER(C.c_int32)), ("beam", u32p)]
+
+
+_MODEL_SIGNATURES["egt_forward_tree"] = (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
+                                                   C.POINTER(TreeView), C.c_void_p, C.c_void_p])
+
 _PROGRAM_SIGNATURES = {
     "egt_program_create": (C.c_int, [C.POINTER(ProgramOp), C.c_uint32, C.c_void_p, C.POINTER(C.c_void_p)]),
     "egt_program_run": (C.c_int, [C.c_void_p, C.c_void_p]),

@@ -215,3 +215,34 @@ def test_kv_decoder_matches_forward(port, cfg):
     # a second run from a different prompt reuses the graph and cache
     toks2 = dec.generate([7, 2], 5)
     assert toks2[:2] == [7, 2] and len(toks2) == 7
+
+
+def test_forward_tree_equals_dense_mask(model_pair):
+    """Compact tree encoding (egt_forward_tree): the device
+    builds the same mask as build_tree_mask (decode.cpp:240-299), so the
+    logits equal the dense-bitmap forward bit for bit; bad encodings raise
+    the reference's messages."""
+    import paper_2605_11582_b200 as egt
+    from tests import verify_oracle as vo
+
+    model, _ = model_pair
+    rng = np.random.default_rng(23)
+    trie = random_trie(rng, depth=3, lo=2, hi=3)
+
+    class B:
+        def __init__(self, node, tokens):
+            self.node, self.tokens = node, tokens
+
+    kids = vo.children(trie, 0)
+    beams = [B(0, []), B(int(kids[0]), [int(trie.token[kids[0]])])]
+    prompt = [1, 2, 3]
+    flat = vo.flatten_subtree(trie, beams)
+    vis, tokens, pos, lmax, off = vo.build_tree_mask(flat, prompt, beams)
+    lens = [len(prompt) + len(b.tokens) for b in beams]
+    got = model.forward_tree(tokens, pos, lens, lmax, [f["parent"] for f in flat], [f["beam"] for f in flat])
+    want = model.forward(tokens, pos, vis)
+    assert np.array_equal(got.cpu().numpy(), want.cpu().numpy())
+    with pytest.raises(egt.InvalidArgument, match="parent does not precede"):
+        model.forward_tree(tokens, pos, lens, lmax, [1] + [f["parent"] for f in flat][1:], [f["beam"] for f in flat])
+    with pytest.raises(egt.InvalidArgument, match="missing beam"):
+        model.forward_tree(tokens, pos, lens, lmax, [f["parent"] for f in flat], [5] * len(flat))

@@ -1,2 +1,4 @@
 exec > gpurun_out/exp.log 2>&1
-timeout 900 python -m pytest tests/test_gpu_compress.py -x -q -m gpu 2>&1 | tail -15
+timeout 1500 python -m pytest tests -x -q -m gpu 2>&1 | tail -4
+timeout 300 python tools/verify_probe.py 2>&1 | tail -3
+EGT_DENSE_TREE_MASK=1 timeout 300 python tools/verify_probe.py 2>&1 | tail -3

@@ -64,12 +64,12 @@ def main():
         L.egt_tune_force_plan(0, 0, 0, 0, 0)
         t = time_plan(layers, x, ys, stream, indep=args.indep)
         res.append({"plan": "auto", "us": t, "GBps": shape_bytes(p) / t / 1e3})
-        for S in ((1,) if args.indep else ((1, 2) if args.quick else (1, 2, 3, 4, 6, 8))):
+        for S in ((1, 2, 3, 4) if args.indep else ((1, 2) if args.quick else (1, 2, 3, 4, 6, 8))):
             if S > KQ:
                 continue
-            for ctas in ((24, 32, 48, 64, 96, 148) if args.indep else (74, 128, 148, 296)):
+            for ctas in ((48, 96, 148, 256) if args.indep else (74, 128, 148, 296)):
                 RB = max(1, math.ceil(RT * S / ctas))
-                for nw, ch in (((8, 0), (8, 16), (8, 32), (12, 24)) if args.indep else ((4, 0), (8, 0), (12, 0), (12, 24))):
+                for nw, ch in (((4, 0), (6, 0), (8, 0), (8, 16), (12, 0), (12, 24), (16, 0)) if args.indep else ((4, 0), (8, 0), (12, 0), (12, 24))):
                     L.egt_tune_force_plan(RB, S, nw, 0, ch)
                     try:
                         t = time_plan(layers, x, ys, stream, indep=args.indep)
