@@ -22,12 +22,17 @@
 #include <string>
 
 #include "device_common.cuh"
+
+#include <cmath>
 #include "handle.h"
 #include "tiled_compute.cuh"
 
 namespace egt_impl {
 
-constexpr int kWideNW = 8;      // consumer warps
+#ifndef EGT_WIDE_NW
+#define EGT_WIDE_NW 8
+#endif
+constexpr int kWideNW = EGT_WIDE_NW;  // consumer warps
 constexpr int kWideTok = 16;    // tokens per CTA (4 n-tiles of 4)
 constexpr int kWideMaxRT = 2;   // row tiles per consumer warp
 
@@ -270,9 +275,23 @@ cudaError_t launch_wide(const egt_dev_packed* h, const float* x, int ldx, int M,
   a.KTtot = KTtot;
   // RB: up to nw * kWideMaxRT row tiles; fewer when the token blocks alone
   // leave SMs idle (one wave of CTAs at one per SM)
-  int RB = kWideNW * kWideMaxRT;
-  while (RB > kWideNW && static_cast<long long>((RT + RB - 1) / RB) * TB < num_sms) RB -= kWideNW;
-  while (RB > 1 && static_cast<long long>((RT + RB - 1) / RB) * TB < num_sms && RB > 1) --RB;
+  // RB: the critical path of the busiest SM is waves x (consumer warps per
+  // scheduler) x (row tiles per warp, lockstep pairs cost ~2 singles); ties
+  // go to the larger RB (x fragments re-read by fewer CTAs).
+  int RB = 1;
+  double best = 1e300;
+  for (int rb = 1; rb <= kWideNW * kWideMaxRT; ++rb) {
+    const long long grid = static_cast<long long>((RT + rb - 1) / rb) * TB;
+    const double waves = std::ceil(static_cast<double>(grid) / num_sms);
+    const int busy = std::min(rb, kWideNW);
+    const double cost = waves * ((busy + 3) / 4) * ((rb + kWideNW - 1) / kWideNW);
+    if (cost <= best) {
+      best = cost;
+      RB = rb;
+    }
+  }
+  static const int rb_force = getenv("EGT_WIDE_RB") ? atoi(getenv("EGT_WIDE_RB")) : 0;
+  if (rb_force > 0) RB = std::min(rb_force, kWideNW * kWideMaxRT);
   a.RB = RB;
   // Consumer warps hold up to two row tiles' stages of one chunk at once, so
   // the weight ring must cover a whole chunk (NSTW >= RB): then issuing chunk
