@@ -29,6 +29,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 
 namespace egt_impl {
@@ -693,12 +694,19 @@ TiledSchedule plan_tiled_rt(const egt_dev_packed* h, int RT, int M, int num_sms,
       if (grid > num_sms && RB < 128 && !g_force[4] && !g_allow_waves) continue;  // one CTA per SM
       if (indep && !g_force[4]) {
         // Independent products run several launches side by side on disjoint
-        // SMs; measured best (tools/plan_sweep.py --indep) is ~250 KB of
-        // weights per CTA, i.e. few CTAs per launch.
+        // SMs; measured best (bench sweep, EGT_INDEP_RB_* sweeps) is ~250 KB
+        // of weights per CTA plus ~1.6x the CTA's x staging (KB of f32 x),
+        // i.e. few CTAs per launch, longer rows per CTA when x is wide:
+        // 4096-wide layers 11 row tiles, 11008-wide 5.
         const double total = static_cast<double>(RT) * KQ * unit_b;
-        static const double kb = getenv("EGT_INDEP_CTA_KB") ? atof(getenv("EGT_INDEP_CTA_KB")) : 250.0;
+        static const double kb0 = getenv("EGT_INDEP_CTA_KB") ? atof(getenv("EGT_INDEP_CTA_KB")) : 250.0;
+        static const double kx = getenv("EGT_INDEP_X_W") ? atof(getenv("EGT_INDEP_X_W")) : 1.6;
+        const double kb = kb0 + kx * (h->cols * 4.0 / 1024.0);
         const int target = std::max(16, std::min(num_sms, static_cast<int>(total / (kb * 1024) + 0.5)));
-        if (RB != (RT + target - 1) / target) continue;
+        char key[64];  // tuning: EGT_INDEP_RB_<rows>x<cols> forces this shape's row tiles per CTA
+        snprintf(key, sizeof key, "EGT_INDEP_RB_%ux%u", h->rows, h->cols);
+        const int rb_env = getenv(key) ? atoi(getenv(key)) : 0;
+        if (RB != (rb_env > 0 ? rb_env : (RT + target - 1) / target)) continue;
       }
       for (int nw : {4, 8, 12}) {
         if (g_force[4] && g_force[2] > 0 && nw != g_force[2]) continue;
