@@ -435,24 +435,19 @@ def measure_decode(torch, egt, plan_name, n_tokens=64, prompt_len=16, max_len=25
         for i in range(1, n_nodes):
             depth[i] = depth[parent[i]] + 1
         M = prompt_len + n_nodes
-        vis = np.zeros((M, M), bool)
-        vis[:prompt_len, :prompt_len] = np.tril(np.ones((prompt_len, prompt_len), bool))
-        for i in range(n_nodes):
-            r = prompt_len + i
-            vis[r, :prompt_len] = True
-            a = i
-            while a >= 0:
-                vis[r, prompt_len + a] = True
-                a = parent[a]
         tokens = np.concatenate([prompt, rng.integers(0, cfg["vocab_size"], n_nodes)]).astype(np.int32)
         positions = np.concatenate([np.arange(prompt_len), prompt_len + depth]).astype(np.int32)
+        # the verify path's forward: the mask (prefix causal; node rows see the
+        # prefix, their ancestors and themselves) is built on the device from
+        # the compact tree encoding (egt_forward_tree)
+        tree = ([prompt_len], prompt_len, parent.astype(np.int32), np.zeros(n_nodes, np.uint32))
         for _ in range(2):
-            model.forward(tokens, positions, vis)
+            model.forward_tree(tokens, positions, *tree)
         torch.cuda.synchronize()
         reps = 5
         e0.record(s)
         for _ in range(reps):
-            model.forward(tokens, positions, vis)
+            model.forward_tree(tokens, positions, *tree)
         e1.record(s)
         e1.synchronize()
         vms = e0.elapsed_time(e1) / reps
