@@ -213,7 +213,9 @@ def measure_sharded(world, rank, stream, torch, egt, rng):
         r0, r1 = plan.local(rank)
         b = shape_bytes(p)
         local_bytes = b * (r1 - r0) // rows
-        copies = max(2, -(-2 * l2 // max(local_bytes, 1)))
+        # the same number of copies (and calls) on every rank: the fused
+        # gather's sequence numbers count calls
+        copies = max(2, -(-2 * l2 // max(b * plan.max_rows // rows, 1)))
         fulls = [egt.DeviceMatrix.from_packed(p, stream) for _ in range(copies)]
         shards = [f.slice_rows(r0, r1) for f in fulls]
         x = torch.from_numpy(np.random.default_rng(cols).uniform(-1, 1, cols).astype(np.float32)).cuda()
