@@ -354,6 +354,29 @@ DECODE_PLANS = {
 }
 
 
+FORMAT_ARMS = ("int4-1:4", "int4-2:4-g64/128", "int4-dense", "fp16-2:4", "fp16-1:4")
+
+
+def format_layer(rng, name, rows, cols):
+    """One host artifact of a format arm (product encoder; U(-1,1) weights,
+    random exact-n masks; 'g64/128' alternates 64 and 128 column groups per row)."""
+    import paper_2605_11582_b200 as egt
+
+    w = rng.uniform(-1, 1, (rows, cols)).astype(np.float32)
+    if name == "int4-dense":
+        return egt.quantize_matrix(w, GROUP)
+    n = 1 if "1:4" in name else 2
+    keys = rng.random((rows, cols // 4, 4))
+    order = np.argsort(keys, axis=2)[:, :, :n]
+    keep = np.zeros((rows, cols // 4, 4), bool)
+    np.put_along_axis(keep, order, True, axis=2)
+    mask = np.packbits(keep.reshape(-1), bitorder="little")
+    if name.startswith("fp16"):
+        return egt.pack_f32(mask, w.astype(np.float16).astype(np.float32), n)
+    groups = np.where(np.arange(rows) % 2 == 0, 64, 128).astype(np.uint32) if "g64/128" in name else GROUP
+    return egt.pack(mask, egt.quantize_matrix(w, groups, mask), n)
+
+
 def decode_host_layers(rng, kinds):
     """One host artifact per (kind, shape): W ~ U(-1/sqrt(in), 1/sqrt(in)) (init_model scale,
     model.hpp:61-62), compressed by the product's encoder (compress_layer semantics)."""
@@ -604,6 +627,39 @@ def run_ours(args):
                                        "bytes_per_call": b, "copies": len(sel)}
         del sub
 
+    # the other arms of the path at the 7B shapes -- 1:4, per-row
+    # mixed group sizes, dense INT4 (quant_dense_gemv), sparse FP16 2:4 / 1:4 --
+    # each shape repeated over enough copies to stream from HBM
+    formats = {}
+    if not args.no_formats:
+        peak_gbs = _peak_hbm()[0]
+        for name in FORMAT_ARMS:
+            for s in ((4096, 4096), (11008, 4096)):
+                a = format_layer(np.random.default_rng(s[0] + len(name)), name, *s)
+                mk = (lambda: egt.DeviceMatrix.dense_i4(a)) if name == "int4-dense" else \
+                    (lambda: egt.DeviceMatrix.from_packed(a))
+                d0 = mk()
+                b = int(d0.algorithmic_bytes) + 4 * (s[0] + s[1])
+                sel = [d0] + [mk() for _ in range(min(64, max(4, -(-2 * 126 * 2**20 // b))) - 1)]
+                sub = Sweep(sel, stream)
+                sub.capture()
+                for _ in range(3):
+                    sub.replay()
+                reps = max(3, min(50, 8000 // len(sel)))
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                with torch.cuda.stream(stream):
+                    e0.record(stream)
+                    for _ in range(reps):
+                        sub.replay()
+                    e1.record(stream)
+                e1.synchronize()
+                us = 1e3 * e0.elapsed_time(e1) / (reps * len(sel))
+                formats[f"{name} {s[0]}x{s[1]}"] = {"us_per_call": round(us, 3), "GBps": round(b / us / 1e3, 1),
+                                                   "frac_of_peak": round(b / us / 1e3 / peak_gbs, 4),
+                                                   "bytes_per_call": b, "copies": len(sel)}
+                del sub, sel, d0
+        torch.cuda.synchronize()
+
     # BASELINE configs[4]: 13B/70B-shaped layers row-sharded across the ranks,
     # local SparseGemv + NCCL all-gather of the y slices (world 1: unsharded)
     sharded = measure_sharded(world, rank, stream, torch, egt, rng) if not args.no_sharded else None
@@ -673,6 +729,7 @@ def run_ours(args):
                    "dependent_chain": {"ms_per_step": round(dep_ms, 4),
                                        "GBps": round(step_bytes / (dep_ms * 1e-3) / 1e9, 1)},
                    "per_shape": per_shape,
+                   "formats_7b_shapes": formats,
                    "sharded_13b_70b": sharded,
                    "decode_7b": decode},
         "e2e": {"value": round(e2e_value, 2), "unit": "GB/s", "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
@@ -705,6 +762,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-sharded", action="store_true", help="skip the 13B/70B row-sharded layers")
     ap.add_argument("--no-decode", action="store_true", help="skip the 7B decode tokens/s measurement")
+    ap.add_argument("--no-formats", action="store_true", help="skip the per-format arms (1:4, dense INT4, FP16)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -16,8 +16,8 @@ timeout 900 python bench.py ${BENCH_ARGS:-} > $OUT/bench_$TAG.json 2> $OUT/bench
 if [[ "${SKIP_NCU:-0}" != 1 ]]; then
   timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
       -k regex:tiled_spmm -c 24 --csv --log-file $OUT/launches_$TAG.csv \
-      python bench.py --steps 2 --warmup 1 --no-cpu --no-decode --no-sharded > /dev/null 2> $OUT/ncu_launch_$TAG.err
+      python bench.py --steps 2 --warmup 1 --no-cpu --no-decode --no-sharded --no-formats > /dev/null 2> $OUT/ncu_launch_$TAG.err
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:tiled_spmm -s 10 -c 3 \
-      -o $OUT/prof_$TAG -f python bench.py --steps 2 --warmup 1 --no-cpu --no-decode --no-sharded > /dev/null 2> $OUT/ncu_full_$TAG.err
+      -o $OUT/prof_$TAG -f python bench.py --steps 2 --warmup 1 --no-cpu --no-decode --no-sharded --no-formats > /dev/null 2> $OUT/ncu_full_$TAG.err
   ls -la $OUT/prof_$TAG.ncu-rep 2>&1 | tail -1
 fi
