@@ -1,8 +1,4 @@
-bash tools/gpu_round.sh r01c > gpurun_out/round_r01c.log 2>&1
-python tools/ncu_summary.py gpurun_out/prof_r01c.ncu-rep > gpurun_out/prof_r01c_summary.txt 2>&1
-ncu -i gpurun_out/prof_r01c.ncu-rep --page raw --csv 2>/dev/null | python -c "
-import csv,sys
-r=list(csv.reader(sys.stdin)); h=r[0]
-keep=[i for i,n in enumerate(h) if n in ('dram__bytes_read.sum','dram__bytes_write.sum','gpu__time_duration.sum','launch__grid_size','dram__throughput.avg.pct_of_peak_sustained_elapsed')]
-for v in r[2:]: print({h[i]: v[i] for i in keep})" > gpurun_out/prof_r01c_raw.txt
-rm -f gpurun_out/prof_r01c.ncu-rep
+exec > gpurun_out/exp.log 2>&1
+for kb in 250 125 170; do
+EGT_INDEP_CTA_KB=$kb timeout 900 python bench.py --steps 50 --warmup 5 --no-decode --no-sharded 2>gpurun_out/b.err | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print($kb, d['value'], {k: (v['us_per_call'], v['frac_of_peak']) for k,v in d['config']['formats_7b_shapes'].items()})"
+done
