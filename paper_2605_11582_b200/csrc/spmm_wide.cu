@@ -29,10 +29,6 @@
 
 namespace egt_impl {
 
-#ifndef EGT_WIDE_NW
-#define EGT_WIDE_NW 8
-#endif
-constexpr int kWideNW = EGT_WIDE_NW;  // consumer warps
 constexpr int kWideTok = 16;    // tokens per CTA (4 n-tiles of 4)
 constexpr int kWideMaxRT = 2;   // row tiles per consumer warp
 
@@ -83,13 +79,13 @@ __global__ void xfrag_kernel(const float* __restrict__ x, int ldx, int M, int co
   }
 }
 
-template <int FMT, int SS>
-__global__ void __launch_bounds__(32 * (kWideNW + 1), 1) wide_spmm_kernel(const WideArgs a) {
+template <int FMT, int SS, int NW>
+__global__ void __launch_bounds__(32 * (NW + 1), 1) wide_spmm_kernel(const WideArgs a) {
   constexpr int E = 4 / SS;
   constexpr int VB = val_lane_bytes(FMT), MB = meta_lane_bytes(FMT);
   extern __shared__ __align__(128) uint8_t smem_raw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  constexpr int nw = kWideNW;
+  constexpr int nw = NW;
   const int rt0 = blockIdx.x * a.RB;
   const int RBc = min(a.RB, a.RT - rt0);
   const int tb = blockIdx.y;
@@ -223,22 +219,23 @@ __global__ void __launch_bounds__(32 * (kWideNW + 1), 1) wide_spmm_kernel(const 
 
 namespace {
 template <int FMT, int SS>
-void* wide_ptr() {
-  return reinterpret_cast<void*>(&wide_spmm_kernel<FMT, SS>);
+void* wide_ptr(int nw) {
+  return nw == 12 ? reinterpret_cast<void*>(&wide_spmm_kernel<FMT, SS, 12>)
+                  : reinterpret_cast<void*>(&wide_spmm_kernel<FMT, SS, 8>);
 }
-void* pick_wide(int fmt, int SS) {
+void* pick_wide(int fmt, int SS, int nw) {
   switch (fmt * 8 + SS) {
-    case I4_SP24 * 8 + 4: return wide_ptr<I4_SP24, 4>();
-    case I4_SP24 * 8 + 2: return wide_ptr<I4_SP24, 2>();
-    case I4_SP24 * 8 + 1: return wide_ptr<I4_SP24, 1>();
-    case I4_SP14 * 8 + 4: return wide_ptr<I4_SP14, 4>();
-    case I4_SP14 * 8 + 2: return wide_ptr<I4_SP14, 2>();
-    case I4_SP14 * 8 + 1: return wide_ptr<I4_SP14, 1>();
-    case I4_DENSE * 8 + 4: return wide_ptr<I4_DENSE, 4>();
-    case I4_DENSE * 8 + 2: return wide_ptr<I4_DENSE, 2>();
-    case I4_DENSE * 8 + 1: return wide_ptr<I4_DENSE, 1>();
-    case F16_SP24 * 8 + 4: return wide_ptr<F16_SP24, 4>();
-    default: return wide_ptr<F16_SP14, 4>();
+    case I4_SP24 * 8 + 4: return wide_ptr<I4_SP24, 4>(nw);
+    case I4_SP24 * 8 + 2: return wide_ptr<I4_SP24, 2>(nw);
+    case I4_SP24 * 8 + 1: return wide_ptr<I4_SP24, 1>(nw);
+    case I4_SP14 * 8 + 4: return wide_ptr<I4_SP14, 4>(nw);
+    case I4_SP14 * 8 + 2: return wide_ptr<I4_SP14, 2>(nw);
+    case I4_SP14 * 8 + 1: return wide_ptr<I4_SP14, 1>(nw);
+    case I4_DENSE * 8 + 4: return wide_ptr<I4_DENSE, 4>(nw);
+    case I4_DENSE * 8 + 2: return wide_ptr<I4_DENSE, 2>(nw);
+    case I4_DENSE * 8 + 1: return wide_ptr<I4_DENSE, 1>(nw);
+    case F16_SP24 * 8 + 4: return wide_ptr<F16_SP24, 4>(nw);
+    default: return wide_ptr<F16_SP14, 4>(nw);
   }
 }
 }  // namespace
@@ -278,20 +275,25 @@ cudaError_t launch_wide(const egt_dev_packed* h, const float* x, int ldx, int M,
   // RB: the critical path of the busiest SM is waves x (consumer warps per
   // scheduler) x (row tiles per warp, lockstep pairs cost ~2 singles); ties
   // go to the larger RB (x fragments re-read by fewer CTAs).
+  // Consumer warps: 12 when the token blocks are few (M <= 128: one wave of
+  // 12-row-tile CTAs), else 8 (measured, tools/wide_probe.py / verify_probe.py:
+  // M = 80 products 16-21 % faster with 12, M = 272 8 % slower).
+  static const int nw_env = getenv("EGT_WIDE_NW") ? atoi(getenv("EGT_WIDE_NW")) : 0;
+  const int NW = nw_env == 8 || nw_env == 12 ? nw_env : (TB <= 8 ? 12 : 8);
   int RB = 1;
   double best = 1e300;
-  for (int rb = 1; rb <= kWideNW * kWideMaxRT; ++rb) {
+  for (int rb = 1; rb <= NW * kWideMaxRT; ++rb) {
     const long long grid = static_cast<long long>((RT + rb - 1) / rb) * TB;
     const double waves = std::ceil(static_cast<double>(grid) / num_sms);
-    const int busy = std::min(rb, kWideNW);
-    const double cost = waves * ((busy + 3) / 4) * ((rb + kWideNW - 1) / kWideNW);
+    const int busy = std::min(rb, NW);
+    const double cost = waves * ((busy + 3) / 4) * ((rb + NW - 1) / NW);
     if (cost <= best) {
       best = cost;
       RB = rb;
     }
   }
   static const int rb_force = getenv("EGT_WIDE_RB") ? atoi(getenv("EGT_WIDE_RB")) : 0;
-  if (rb_force > 0) RB = std::min(rb_force, kWideNW * kWideMaxRT);
+  if (rb_force > 0) RB = std::min(rb_force, NW * kWideMaxRT);
   a.RB = RB;
   // Consumer warps hold up to two row tiles' stages of one chunk at once, so
   // the weight ring must cover a whole chunk (NSTW >= RB): then issuing chunk
@@ -309,12 +311,12 @@ cudaError_t launch_wide(const egt_dev_packed* h, const float* x, int ldx, int M,
   if (a.NSTW < RB) return cudaErrorInvalidConfiguration;
   const size_t smem = (16 * (4 + 2 * a.NSTW) + 127) / 128 * 128 + 2 * static_cast<size_t>(a.xstage_bytes) +
                       static_cast<size_t>(a.NSTW) * a.wstage_bytes;
-  void* fn = pick_wide(fmt, h->tiled.SS);
+  void* fn = pick_wide(fmt, h->tiled.SS, NW);
   cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (err != cudaSuccess) return err;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((RT + RB - 1) / RB, TB, 1);
-  cfg.blockDim = dim3(32 * (kWideNW + 1));
+  cfg.blockDim = dim3(32 * (NW + 1));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = ctx.stream;
   cudaLaunchAttribute attr[1];
