@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -54,6 +55,41 @@ __global__ void rmsnorm_kernel(const float* x, float* y, int d) {
   const float inv = 1.0f / sqrtf(red[0] / static_cast<float>(d) + kNormEps);
   float* yr = y + static_cast<size_t>(blockIdx.x) * d;
   for (int c = threadIdx.x; c < d; c += blockDim.x) yr[c] = xr[c] * inv;
+}
+
+// rmsnorm for rows of d % 4 == 0, d <= 4 * 4 * blockDim: one read of x
+// (float4 in registers), then the scaled write.
+__global__ void __launch_bounds__(1024) rmsnorm4_kernel(const float* x, float* y, int d) {
+  const float4* xr = reinterpret_cast<const float4*>(x + static_cast<size_t>(blockIdx.x) * d);
+  float4* yr = reinterpret_cast<float4*>(y + static_cast<size_t>(blockIdx.x) * d);
+  const int n4 = d / 4;
+  float4 vals[4];
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int c = threadIdx.x + i * blockDim.x;
+    vals[i] = c < n4 ? xr[c] : make_float4(0.f, 0.f, 0.f, 0.f);
+    ss = fmaf(vals[i].x, vals[i].x, ss);
+    ss = fmaf(vals[i].y, vals[i].y, ss);
+    ss = fmaf(vals[i].z, vals[i].z, ss);
+    ss = fmaf(vals[i].w, vals[i].w, ss);
+  }
+  __shared__ float red[32];
+  ss = egt_dev::warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
+    v = egt_dev::warp_sum(v);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  const float inv = 1.0f / sqrtf(red[0] / static_cast<float>(d) + kNormEps);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int c = threadIdx.x + i * blockDim.x;
+    if (c < n4) yr[c] = make_float4(vals[i].x * inv, vals[i].y * inv, vals[i].z * inv, vals[i].w * inv);
+  }
 }
 
 // Batched f32 GEMM tile kernel for attention: C[b](i,j) = alpha * sum_k A[b](i,k) * B'[b](k,j)
@@ -114,6 +150,84 @@ __global__ void masked_softmax_kernel(float* S, const uint8_t* mask, int M, int 
   }
   z = egt_dev::warp_sum(z);
   for (int k = lane; k < M; k += 32) s[k] = s[k] / z;
+}
+
+// Fused masked attention for one head and 16 query rows (model.cpp:161-184:
+// s = (q k^T) * scale, masked softmax with an empty row -> 0, o = p V), so the
+// M x M scores never leave shared memory.  Block (query tile, head), 256
+// threads; smem: q tile [16][dh + 4] and scores [16][M].
+constexpr int kAttnRows = 16;
+__global__ void __launch_bounds__(256) fused_attention_kernel(const float* __restrict__ q, const float* __restrict__ k,
+                                                              const float* __restrict__ v, float* __restrict__ o,
+                                                              const uint8_t* __restrict__ mask, int M, int d, int dh,
+                                                              float scale) {
+  extern __shared__ float sm[];
+  const int ldq = dh + 4;
+  float* qs = sm;                          // [16][dh + 4]
+  float* ps = sm + kAttnRows * ldq;        // [16][M]
+  const int q0 = blockIdx.x * kAttnRows, h = blockIdx.y, tid = threadIdx.x;
+  const int nr = min(kAttnRows, M - q0);
+  const size_t hoff = static_cast<size_t>(h) * dh;
+  for (int i = tid; i < kAttnRows * dh; i += blockDim.x) {
+    const int r = i / dh, e = i % dh;
+    qs[r * ldq + e] = r < nr ? q[static_cast<size_t>(q0 + r) * d + hoff + e] : 0.f;
+  }
+  __syncthreads();
+  // scores: thread -> (key j, row r), 16 consecutive threads share key j
+  for (int idx = tid; idx < kAttnRows * M; idx += blockDim.x) {
+    const int r = idx % kAttnRows, j = idx / kAttnRows;
+    float acc = 0.f;
+    if (r < nr) {
+      const float4* kr = reinterpret_cast<const float4*>(k + static_cast<size_t>(j) * d + hoff);
+      const float4* qr = reinterpret_cast<const float4*>(qs + r * ldq);
+      for (int e = 0; e < dh / 4; ++e) {
+        const float4 a = qr[e], b = __ldg(kr + e);
+        acc = fmaf(a.x, b.x, fmaf(a.y, b.y, fmaf(a.z, b.z, fmaf(a.w, b.w, acc))));
+      }
+    }
+    const size_t bit = static_cast<size_t>(q0 + r) * M + j;
+    const bool vis = r < nr && ((mask[bit >> 3] >> (bit & 7)) & 1);
+    ps[r * M + j] = vis ? acc * scale : -INFINITY;
+  }
+  __syncthreads();
+  // softmax: two rows per warp
+  const int lane = tid & 31, warp = tid >> 5;
+  for (int r = warp; r < kAttnRows; r += blockDim.x >> 5) {
+    float* pr = ps + r * M;
+    float m = -INFINITY;
+    for (int j = lane; j < M; j += 32) m = fmaxf(m, pr[j]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+    if (!isfinite(m)) {  // no visible key: zero attention output (model.cpp:173)
+      for (int j = lane; j < M; j += 32) pr[j] = 0.f;
+      continue;
+    }
+    float z = 0.f;
+    for (int j = lane; j < M; j += 32) {
+      const float e = pr[j] == -INFINITY ? 0.f : expf(pr[j] - m);
+      pr[j] = e;
+      z += e;
+    }
+    z = egt_dev::warp_sum(z);
+    const float iz = 1.0f / z;
+    for (int j = lane; j < M; j += 32) pr[j] *= iz;
+  }
+  __syncthreads();
+  // o = p V: thread -> column e, rows rg*8 .. rg*8+7
+  for (int c = tid; c < dh * (kAttnRows / 8); c += blockDim.x) {
+    const int e = c % dh, rg = c / dh;
+    float acc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+    for (int j = 0; j < M; ++j) {
+      const float vv = __ldg(v + static_cast<size_t>(j) * d + hoff + e);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] = fmaf(ps[(rg * 8 + i) * M + j], vv, acc[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (rg * 8 + i < nr) o[static_cast<size_t>(q0 + rg * 8 + i) * d + hoff + e] = acc[i];
+  }
 }
 
 __global__ void silu_kernel(float* f, size_t n) {  // model.cpp:80-84
@@ -242,16 +356,35 @@ egt_status forward_core(const egt_model* m, const int32_t* tokens, const int32_t
   }
   embed_kernel<<<M, 256, 0, s>>>(dtok, dpos, m->emb, m->pos, x, static_cast<int>(M), static_cast<int>(d));
   ++launch_counter();
+  auto rmsnorm = [&](const float* in, float* outp) {
+    if (d % 4 == 0 && d <= 16 * 1024)
+      rmsnorm4_kernel<<<M, static_cast<unsigned>(std::min<size_t>(1024, (d / 4 + 31) / 32 * 32)), 0, s>>>(
+          in, outp, static_cast<int>(d));
+    else
+      rmsnorm_kernel<<<M, 256, 0, s>>>(in, outp, static_cast<int>(d));
+  };
   const float att_scale = 1.0f / std::sqrt(static_cast<float>(dh));  // model.cpp:139
+  // fused attention while the 16-row score tile fits in shared memory
+  const size_t attn_smem = (kAttnRows * (dh + 4) + static_cast<size_t>(kAttnRows) * M) * sizeof(float);
+  static const bool no_fused = getenv("EGT_UNFUSED_ATTENTION") != nullptr;
+  const bool fused_attn = !no_fused && dh % 4 == 0 && attn_smem <= 200 * 1024;
+  if (fused_attn && attn_smem > 48 * 1024)
+    MCUDA(cudaFuncSetAttribute(fused_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(attn_smem)));
   const dim3 tb(16, 16);
   for (uint32_t l = 0; l < c.n_layers && st == EGT_OK; ++l) {
     const egt_dev_packed* const* w = m->layers.data() + 6 * l;
-    rmsnorm_kernel<<<M, 256, 0, s>>>(x, a, static_cast<int>(d));
+    rmsnorm(x, a);
     ++launch_counter();
     lin(w[0], a, q, 0);
     lin(w[1], a, k, EGT_SPMV_INDEPENDENT);  // K and V read `a`, not the previous product
     lin(w[2], a, v, EGT_SPMV_INDEPENDENT);
     // scores per head: S[h] = (q_h k_h^T) * scale
+    if (fused_attn) {
+      fused_attention_kernel<<<dim3((M + kAttnRows - 1) / kAttnRows, H), 256, attn_smem, s>>>(
+          q, k, v, o, dmask, static_cast<int>(M), static_cast<int>(d), static_cast<int>(dh), att_scale);
+      ++launch_counter();
+    } else {
     attn_gemm_kernel<true><<<dim3((M + 15) / 16, (M + 15) / 16, H), tb, 0, s>>>(
         q, static_cast<int>(d), dh, k, static_cast<int>(d), dh, S, static_cast<int>(M),
         static_cast<size_t>(M) * M, static_cast<int>(M), static_cast<int>(M), static_cast<int>(dh), att_scale);
@@ -260,9 +393,10 @@ egt_status forward_core(const egt_model* m, const int32_t* tokens, const int32_t
         S, static_cast<int>(M), static_cast<size_t>(M) * M, v, static_cast<int>(d), dh, o, static_cast<int>(d),
         dh, static_cast<int>(M), static_cast<int>(dh), static_cast<int>(M), 1.0f);
     launch_counter() += 3;
+    }
     lin(w[3], o, a, 0);  // a <- o Wo^T
     add_kernel<<<grid_for(Md), 256, 0, s>>>(x, a, Md);
-    rmsnorm_kernel<<<M, 256, 0, s>>>(x, a, static_cast<int>(d));
+    rmsnorm(x, a);
     launch_counter() += 2;
     lin(w[4], a, f1, 0);
     silu_kernel<<<grid_for(M * dff), 256, 0, s>>>(f1, M * dff);
@@ -272,7 +406,7 @@ egt_status forward_core(const egt_model* m, const int32_t* tokens, const int32_t
     ++launch_counter();
   }
   if (st == EGT_OK) {
-    rmsnorm_kernel<<<M, 256, 0, s>>>(x, a, static_cast<int>(d));
+    rmsnorm(x, a);
     ++launch_counter();
     lin(m->head, a, logits, 0);
   }
