@@ -600,7 +600,7 @@ egt_status spmv_impl(const egt_dev_packed* h, const float* x, float* y, uint32_t
     return EGT_OK;
   }
   static const bool no_wide = getenv("EGT_NO_WIDE") != nullptr;  // tuning: old M > 16 path
-  if (M > 16 && !pg && !res && input == EGT_INPUT_NONE && !ctx.out_silu && !no_wide && !plan_forced()) {
+  if (M > 16 && !pg && input == EGT_INPUT_NONE && !no_wide && !plan_forced()) {  // residual / output silu in its epilogue
     Workspace* w = nullptr;
     egt_status st = get_workspace(s, (wide_workspace_bytes(h, static_cast<int>(M)) + 3) / 4, 0, &w);
     if (st != EGT_OK) return st;

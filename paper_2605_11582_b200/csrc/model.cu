@@ -394,16 +394,32 @@ egt_status forward_core(const egt_model* m, const int32_t* tokens, const int32_t
         dh, static_cast<int>(M), static_cast<int>(dh), static_cast<int>(M), 1.0f);
     launch_counter() += 3;
     }
-    lin(w[3], o, a, 0);  // a <- o Wo^T
-    add_kernel<<<grid_for(Md), 256, 0, s>>>(x, a, Md);
-    rmsnorm(x, a);
-    launch_counter() += 2;
-    lin(w[4], a, f1, 0);
-    silu_kernel<<<grid_for(M * dff), 256, 0, s>>>(f1, M * dff);
-    ++launch_counter();
-    lin(w[5], f1, a, 0);
-    add_kernel<<<grid_for(Md), 256, 0, s>>>(x, a, Md);
-    ++launch_counter();
+    // x += o Wo^T; f = silu(rmsnorm(x) ff1^T); x += f ff2^T -- the residual
+    // adds and the silu in the products' epilogues where the path allows
+    auto fused = [&](const egt_dev_packed* h, const float* in, float* outp, const float* res, uint32_t flags) {
+      if (st == EGT_OK)
+        st = egt_spmv_fused(h, in, outp, M, h->cols, h->rows, res, res ? static_cast<uint32_t>(d) : 0,
+                            EGT_INPUT_NONE, kNormEps, flags, nullptr, stream);
+    };
+    const bool glue = w[3]->path == EGT_PATH_TILED && w[4]->path == EGT_PATH_TILED && w[5]->path == EGT_PATH_TILED;
+    if (glue) {
+      fused(w[3], o, x, x, 0);
+      rmsnorm(x, a);
+      ++launch_counter();
+      fused(w[4], a, f1, nullptr, EGT_SPMV_OUTPUT_SILU);
+      fused(w[5], f1, x, x, 0);
+    } else {
+      lin(w[3], o, a, 0);  // a <- o Wo^T
+      add_kernel<<<grid_for(Md), 256, 0, s>>>(x, a, Md);
+      rmsnorm(x, a);
+      launch_counter() += 2;
+      lin(w[4], a, f1, 0);
+      silu_kernel<<<grid_for(M * dff), 256, 0, s>>>(f1, M * dff);
+      ++launch_counter();
+      lin(w[5], f1, a, 0);
+      add_kernel<<<grid_for(Md), 256, 0, s>>>(x, a, Md);
+      ++launch_counter();
+    }
   }
   if (st == EGT_OK) {
     rmsnorm(x, a);

@@ -40,6 +40,9 @@ struct WideArgs {
   const uint32_t* xf;  // x fragments
   float* y;
   int KQ, rt_begin, RT, rows, M, ldy, RB, CH, NSTW, wstage_bytes, xstage_bytes, KTtot;
+  const float* res;  // y = res + product (may alias y; row stride ldr), model.cpp:186/190
+  int ldr;
+  int out_silu;      // y = silu(...), model.cpp:80-84 (the next product's input)
 };
 
 // X [M x cols] (row stride ldx) -> fragments; one thread per (token block,
@@ -209,8 +212,16 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) wide_spmm_kernel(const WideA
         if (tok < a.M) {
           const int row = (rt0 + i) * 16 + g;
           float* yr = a.y + static_cast<size_t>(tok) * a.ldy;
-          if (row < a.rows) yr[row] = acc[r][nt][0];
-          if (row + 8 < a.rows) yr[row + 8] = acc[r][nt][1];
+          const float* rr = a.res ? a.res + static_cast<size_t>(tok) * a.ldr : nullptr;
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            const int rw = row + 8 * hh;
+            if (rw < a.rows) {
+              float val = (rr ? rr[rw] : 0.f) + acc[r][nt][hh];
+              if (a.out_silu) val = val * (1.0f / (1.0f + expf(-val)));
+              yr[rw] = val;
+            }
+          }
         }
       }
     }
@@ -270,6 +281,9 @@ cudaError_t launch_wide(const egt_dev_packed* h, const float* x, int ldx, int M,
   a.M = M;
   a.ldy = ldy;
   a.KTtot = KTtot;
+  a.res = ctx.res;
+  a.ldr = ctx.ldr;
+  a.out_silu = ctx.out_silu;
   // RB: up to nw * kWideMaxRT row tiles; fewer when the token blocks alone
   // leave SMs idle (one wave of CTAs at one per SM)
   // RB: the critical path of the busiest SM is waves x (consumer warps per

@@ -327,3 +327,24 @@ def test_baseline_sharded_shapes_full_size(egt, port, torch, shape):
         parts = [d.slice_rows(r0, r1).spmv(xt).cpu().numpy() for r0, r1 in plan.bounds]
         ok, err = close(np.concatenate(parts), full, 1e-5)
         assert ok, (G, err)
+
+
+@pytest.mark.parametrize("M", [17, 80])
+def test_many_token_fused_epilogue(egt, port, torch, M):
+    """The many-token kernel's epilogue glue (the verify forward's
+    x += o Wo^T and silu(b ff1^T), model.cpp:186-190): y = silu(res + X W^T)
+    and y = y + X W^T in place, against the plain product."""
+    rng = np.random.default_rng(300 + M)
+    p, _, _ = make_int4(rng, 272, 1536, 2, 128, port)
+    d = _dev(egt, p)
+    x = torch.from_numpy(rng.uniform(-1, 1, (M, p.cols)).astype(np.float32)).cuda()
+    res = torch.from_numpy(rng.uniform(-1, 1, (M, p.rows)).astype(np.float32)).cuda()
+    plain = d.spmv(x)
+    y = torch.empty_like(res)
+    d.spmv_fused_into(x, y, residual=res, output_silu=True)
+    want = res + plain
+    want = want * torch.sigmoid(want)
+    assert torch.allclose(y, want, rtol=1e-6, atol=1e-6)
+    acc = res.clone()
+    d.spmv_fused_into(x, acc, residual=acc)
+    assert torch.equal(acc, res + plain)
