@@ -183,6 +183,16 @@ egt_status build_handle(int format, uint8_t n, uint8_t kind, uint32_t rows, uint
   int ss = 4;
   const bool tiled = rows > 0 && cols > 0 && cols % 32 == 0 &&
                      (kind == EGT_KIND_F32 || groups_k_aligned(rows, cols, host_gs, &ss));
+  // INT4 1:4 on the tiled path is stored as 2:4 with a zero-valued partner per
+  // kept entry: one mma.sp per k-tile either way, but without the per-k-tile
+  // placement and metadata ALU work (issue-bound otherwise; DESIGN 5).  The
+  // algorithmic bytes above stay the 1:4 stream's.
+  static const bool sp14_native = getenv("EGT_SP14_NATIVE") != nullptr;
+  const bool pad14 = tiled && format == I4_SP14 && !sp14_native;
+  if (pad14) {
+    format = I4_SP24;
+    h->format = static_cast<uint8_t>(I4_SP24);
+  }
   int dev = 0;
   CUDA_TRY(cudaGetDevice(&dev));
   auto store = std::make_shared<DevStorage>();
@@ -193,6 +203,7 @@ egt_status build_handle(int format, uint8_t n, uint8_t kind, uint32_t rows, uint
     ts.RT = static_cast<int>((rows + 15) / 16);
     ts.SS = kind == EGT_KIND_INT4 ? ss : 4;
     ts.E = 4 / ts.SS;
+    ts.pad14 = pad14 ? 1 : 0;
     const size_t blocks = static_cast<size_t>(ts.RT) * ts.KQ;
     Carve c;
     const size_t o_vals = c.add(blocks * 32 * val_lane_bytes(format));
@@ -531,7 +542,7 @@ egt_status egt_dev_packed_query(const egt_dev_packed* h, egt_dev_packed_info* in
   info->n = h->n;
   info->m = h->m;
   info->kind = h->kind;
-  info->format = h->format;
+  info->format = h->tiled.pad14 ? egt_fmt::I4_SP14 : h->format;  // the stream's format (1:4 stored as 2:4)
   info->path = h->path;
   info->device_bytes = h->device_bytes;
   info->algorithmic_bytes = h->algorithmic_bytes;

@@ -46,6 +46,7 @@ struct TiledStream {
   int RT = 0;        // row tiles covered by this handle
   int SS = 4;        // k-tiles per scale entry
   int E = 1;         // scale entries per k-quad (4 / SS)
+  int pad14 = 0;     // INT4 1:4 stored as 2:4 (each kept entry paired with a zero-valued one)
 };
 
 struct TiledSchedule {
@@ -153,7 +154,7 @@ cudaError_t launch_validate_groups(const uint32_t* gsizes, const uint32_t* goffs
 cudaError_t launch_f32_to_f16(const float* src, __half* dst, uint64_t n, cudaStream_t s);
 cudaError_t launch_relayout(const RawStream& raw, int format, uint32_t rows, uint32_t cols,
                             const TiledStream& dst_shape, uint8_t* vals, uint8_t* meta,
-                            float* scales, uint8_t* zps, cudaStream_t s);
+                            float* scales, uint8_t* zps, cudaStream_t s);  // dst_shape.pad14: raw is 1:4
 cudaError_t launch_dequant(const egt_dev_packed* h, float* w, uint8_t* mask, cudaStream_t s);
 
 uint64_t& launch_counter();

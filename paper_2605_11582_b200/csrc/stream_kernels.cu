@@ -87,6 +87,7 @@ struct RelayoutArgs {
   uint8_t* meta;
   float* scales;
   uint8_t* zps;
+  int pad14;  // raw stream is INT4 1:4, written as 2:4 with zero-valued partners
 };
 
 __device__ __forceinline__ bool group_valid(const RelayoutArgs& a, uint32_t r, uint32_t G) {
@@ -103,9 +104,24 @@ __global__ void relayout_kernel(const RelayoutArgs a) {
   const int rt = static_cast<int>(blk / a.KQ);
   const int g = lane >> 2, t = lane & 3;
   const int f = a.format;
-  const int n = keep_n(f);
+  const int n = a.pad14 ? 1 : keep_n(f);
   const uint64_t row_nnz = static_cast<uint64_t>(a.cols) * (n == 4 ? 4 : n) / 4;
   const RawStream& raw = a.raw;
+  // INT4 1:4 as 2:4: the kept entry at offset o of its group of 4 is paired
+  // with a partner carrying the group's zero point (so c - z = 0 exactly):
+  // o = 0,1,2 -> (o, o+1) kept first; o = 3 -> (1, 3) kept second.
+  auto pad_pair = [&](uint32_t r, uint32_t G, uint32_t* c0, uint32_t* c1, uint32_t* nib) {
+    const uint64_t R = raw.row_begin + r;
+    const uint64_t k = R * row_nnz + G;
+    const uint32_t off = offset_at(raw.words, k), code = nibble_at(raw.codes, k);
+    const uint32_t col = G * 4 + off;
+    const uint32_t z = raw.zps[raw.group_offsets[R] + col / raw.group_sizes[R]];
+    if (off < 3) {
+      *c0 = code, *c1 = z, *nib = off | ((off + 1) << 2);
+    } else {
+      *c0 = z, *c1 = code, *nib = 1u | (3u << 2);
+    }
+  };
 
   if (f == I4_SP24 || f == F16_SP24) {
     uint32_t v[16] = {0};
@@ -119,7 +135,12 @@ __global__ void relayout_kernel(const RelayoutArgs a) {
             continue;  // codes 0 / values 0 (scale 0 / x 0 make them inert)
           }
           const uint64_t k0 = (raw.row_begin + r) * row_nnz + 2ull * G;
-          if (f == I4_SP24) {
+          if (a.pad14) {
+            uint32_t c0, c1, nib;
+            pad_pair(r, G, &c0, &c1, &nib);
+            v[j] |= c0 << (4 * p);
+            v[j] |= c1 << (16 + 4 * p);
+          } else if (f == I4_SP24) {
             v[j] |= nibble_at(raw.codes, k0) << (4 * p);
             v[j] |= nibble_at(raw.codes, k0 + 1) << (16 + 4 * p);
           } else {
@@ -142,8 +163,13 @@ __global__ void relayout_kernel(const RelayoutArgs a) {
           const uint32_t G = (kq * 4 + j) * 8 + 4 * hh + q4;
           uint32_t nib = 0x4u;  // (0,1): a valid ordered pattern for padding
           if (group_valid(a, r, G)) {
-            const uint64_t k0 = (raw.row_begin + r) * row_nnz + 2ull * G;
-            nib = offset_at(raw.words, k0) | (offset_at(raw.words, k0 + 1) << 2);
+            if (a.pad14) {
+              uint32_t c0, c1;
+              pad_pair(r, G, &c0, &c1, &nib);
+            } else {
+              const uint64_t k0 = (raw.row_begin + r) * row_nnz + 2ull * G;
+              nib = offset_at(raw.words, k0) | (offset_at(raw.words, k0 + 1) << 2);
+            }
           }
           word |= nib << (16 * h + 4 * q4);
         }
@@ -247,6 +273,7 @@ cudaError_t launch_relayout(const RawStream& raw, int format, uint32_t rows, uin
   a.meta = meta;
   a.scales = scales;
   a.zps = zps;
+  a.pad14 = dst.pad14;
   const uint64_t total = static_cast<uint64_t>(dst.RT) * dst.KQ * 32;
   relayout_kernel<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(a);
   ++launch_counter();
@@ -439,7 +466,10 @@ __global__ void dequant_tiled_kernel(const DequantTiledArgs a) {
           const uint32_t word = mb[holder * 2 + (j >> 1)];
           const uint32_t nib = (word >> (16 * h + 4 * t)) & 0xFu;
           const uint32_t off[2] = {nib & 3u, (nib >> 2) & 3u};
+          // pad14: only the kept entry of the pair (the second one iff (1, 3))
+          const int only = a.ts.pad14 ? ((off[0] == 1u && off[1] == 3u) ? 1 : 0) : -1;
           for (int i = 0; i < 2; ++i) {
+            if (only >= 0 && i != only) continue;
             const uint32_t c = G * 4 + off[i];
             float val;
             if (f == I4_SP24) {
