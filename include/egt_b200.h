@@ -378,6 +378,23 @@ EGT_API egt_status egt_program_destroy(egt_program* p);
  * ready, [8192,12288) consumer done, [12288,16384) epilogue segment start. */
 EGT_API egt_status egt_program_debug_trace(const egt_program* p, long long* host, size_t n);
 
+/* y = W x for a dense row-major f32 W (device pointers): the mixed
+ * dispatch's (dense, !quant) baseline arm, which the reference densifies
+ * (materialize_model, compress.cpp:395-414), and bench_spmv's dense-fp. */
+EGT_API egt_status egt_gemv_f32(const float* w_dev, const float* x_dev, float* y_dev, uint32_t rows,
+                                uint32_t cols, void* stream);
+
+/* bench_spmv (packed.cpp:310-383) on the device: per shape the reference's
+ * seeded U(-1,1) W and x (mt19937_64, seed + 0x9e3779b97f4a7c15 (si + 1)),
+ * g = min(64, cols), magnitude masks; variants dense-fp, quant-dense,
+ * packed-2:4, packed-1:4; one warm-up, then reps products each timed with
+ * CUDA events (device ns per product, inputs resident); bytes = the
+ * reference's analytic weight-side bytes.  Writes bench_csv's text
+ * (packed.cpp:385-393) into csv (cap bytes, NUL-terminated); *len = its
+ * length.  EGT_EINVAL with the reference's messages for bad shapes / reps. */
+EGT_API egt_status egt_bench_spmv(const uint32_t* rows, const uint32_t* cols, uint32_t n_shapes, int reps,
+                                  uint64_t seed, char* csv, size_t cap, size_t* len);
+
 /* ---------------- GPU compression ----------------------
  * The step before the path on the device (re-compressing 7B/70B layers),
  * byte-identical to the host encoder and the reference.  All pointers are

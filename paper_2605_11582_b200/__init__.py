@@ -10,7 +10,9 @@ from .packed import (  # noqa: F401
     DeviceMatrix,
     PackedSparseMatrix,
     QuantizedMatrix,
+    bench_spmv,
     fit_group,
+    gemv_f32,
     gpu_importance,
     gpu_prune_nm,
     gpu_quantize_pack,

@@ -350,6 +350,12 @@ egt_status egt_dev_packed_create(const egt_packed_view* v, void* stream, egt_dev
                       c.total, s, out);
 }
 
+egt_status egt_gemv_f32(const float* w, const float* x, float* y, uint32_t rows, uint32_t cols, void* stream) {
+  if (static_cast<uint64_t>(rows) * cols && (!w || !x || !y)) return fail(EGT_EINVAL, "gemv: null argument");
+  CUDA_TRY(launch_gemv_f32(w, x, y, rows, cols, static_cast<cudaStream_t>(stream)));
+  return EGT_OK;
+}
+
 egt_status egt_gpu_importance(const float* w, const float* x_norms, const float* grad_abs, uint32_t rows,
                               uint32_t cols, float* scores, void* stream) {
   if (static_cast<uint64_t>(rows) * cols && (!w || !x_norms || !grad_abs || !scores))

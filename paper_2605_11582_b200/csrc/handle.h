@@ -101,6 +101,8 @@ cudaError_t launch_check_nm(const uint8_t* mask, uint32_t rows, uint32_t cols, i
 cudaError_t launch_quantize_pack(const float* w, const uint8_t* mask, uint32_t rows, uint32_t cols, int n,
                                  const uint32_t* gs, const uint32_t* goff, float* scales, uint8_t* zps,
                                  uint8_t* codes_tmp, uint8_t* value_bytes, uint16_t* words, cudaStream_t s);
+// Dense f32 GEMV (the dense-FP baseline arm, bench_spmv's dense-fp).
+cudaError_t launch_gemv_f32(const float* w, const float* x, float* y, uint32_t rows, uint32_t cols, cudaStream_t s);
 // Signal this rank's (empty) slice and optionally wait for every peer's.
 cudaError_t launch_peer_signal(const egt_peer_group* g, bool signal, bool wait, cudaStream_t s);
 }  // namespace egt_impl

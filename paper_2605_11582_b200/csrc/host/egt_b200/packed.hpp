@@ -115,6 +115,25 @@ struct FootprintReport {
 };
 FootprintReport footprint(const PackedSparseMatrix& packed);
 
+// bench_spmv / bench_csv (packed.hpp:100-113, packed.cpp:310-393): the
+// reference harness with its seeded inputs and analytic bytes; the timing
+// columns are device nanoseconds per product (CUDA events, inputs resident).
+struct BenchShape {
+  uint32_t rows = 0;
+  uint32_t cols = 0;
+};
+struct BenchRow {
+  std::string variant;  // dense-fp | quant-dense | packed-2:4 | packed-1:4
+  uint32_t rows = 0;
+  uint32_t cols = 0;
+  std::string pattern;
+  uint64_t median_ns = 0;
+  uint64_t p95_ns = 0;
+  uint64_t bytes = 0;
+};
+std::vector<BenchRow> bench_spmv(const std::vector<BenchShape>& shapes, int reps, uint64_t seed);
+std::string bench_csv(const std::vector<BenchRow>& rows);
+
 // Throws the exception class the reference would for an egt_status.
 [[noreturn]] void throw_status(egt_status st);
 inline void check(egt_status st) {

@@ -549,3 +549,43 @@ cudaError_t launch_f32_to_f16(const float* src, __half* dst, uint64_t n, cudaStr
   return cudaGetLastError();
 }
 }  // namespace egt_impl
+
+// ------------------------------------------------------------- dense FP32
+// y = W x for a dense row-major f32 W: the mixed dispatch's (dense, !quant)
+// baseline arm (compress.cpp:395-414 materialises it) and bench_spmv's
+// "dense-fp" variant (packed.cpp:337-347).  Warp per row, float4 loads,
+// HBM-bound (4 B per weight).
+namespace egt_impl {
+namespace {
+__global__ void __launch_bounds__(256) gemv_f32_kernel(const float* __restrict__ w, const float* __restrict__ x,
+                                                       float* __restrict__ y, uint32_t rows, uint32_t cols) {
+  pdl_wait();
+  pdl_launch_dependents();
+  const uint32_t r = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  const float* wr = w + static_cast<size_t>(r) * cols;
+  float acc = 0.f;
+  if ((cols & 3u) == 0 && (reinterpret_cast<uintptr_t>(w) & 15) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0) {
+    const float4* w4 = reinterpret_cast<const float4*>(wr);
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+    for (uint32_t c = lane; c < cols / 4; c += 32) {
+      const float4 a = __ldcs(w4 + c), b = x4[c];
+      acc = fmaf(a.x, b.x, fmaf(a.y, b.y, fmaf(a.z, b.z, fmaf(a.w, b.w, acc))));
+    }
+  } else {
+    for (uint32_t c = lane; c < cols; c += 32) acc = fmaf(wr[c], x[c], acc);
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) y[r] = acc;
+}
+}  // namespace
+
+cudaError_t launch_gemv_f32(const float* w, const float* x, float* y, uint32_t rows, uint32_t cols, cudaStream_t s) {
+  if (rows == 0) return cudaSuccess;
+  gemv_f32_kernel<<<(rows + 7) / 8, 256, 0, s>>>(w, x, y, rows, cols);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) ++launch_counter();
+  return e;
+}
+}  // namespace egt_impl

@@ -226,6 +226,9 @@ _COMPRESS_SIGNATURES = {
 
 SIGNATURES.update(_MODEL_SIGNATURES)
 SIGNATURES.update(_COMPRESS_SIGNATURES)
+SIGNATURES["egt_gemv_f32"] = (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p])
+SIGNATURES["egt_bench_spmv"] = (C.c_int, [u32p, u32p, C.c_uint32, C.c_int, C.c_uint64, C.c_char_p, C.c_size_t,
+                                          C.POINTER(C.c_size_t)])
 SIGNATURES.update(_PEER_SIGNATURES)
 SIGNATURES.update(_PROGRAM_SIGNATURES)
 

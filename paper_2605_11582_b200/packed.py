@@ -370,3 +370,27 @@ def gpu_quantize_pack(w, mask, n: int, group_sizes, stream=None, want_raw: bool 
         raw["scales"] = raw["scales"][:groups]
         raw["zero_points"] = raw["zero_points"][:groups]
     return (DeviceMatrix(h.value) if want_matrix else None), raw
+
+
+def gemv_f32(w, x, stream=None):
+    """y = W x for a dense f32 CUDA tensor W (the dense-FP baseline arm)."""
+    import torch
+
+    rows, cols = w.shape
+    y = torch.empty(rows, dtype=torch.float32, device=w.device)
+    check(lib().egt_gemv_f32(C.c_void_p(w.data_ptr()), C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), rows,
+                             cols, _stream_ptr(stream)))
+    return y
+
+
+def bench_spmv(shapes, reps: int = 5, seed: int = 0) -> str:
+    """bench_spmv + bench_csv (packed.cpp:310-393) on the device: the CSV text
+    (variant,rows,cols,pattern,median_ns,p95_ns,bytes)."""
+    rows = np.ascontiguousarray([s[0] for s in shapes], np.uint32)
+    cols = np.ascontiguousarray([s[1] for s in shapes], np.uint32)
+    n = C.c_size_t()
+    cap = 256 + 160 * 4 * max(1, len(shapes))
+    buf = C.create_string_buffer(cap)
+    check(lib().egt_bench_spmv(_p(rows, N.u32p), _p(cols, N.u32p), len(shapes), reps, C.c_uint64(seed), buf, cap,
+                               C.byref(n)))
+    return buf.value.decode()

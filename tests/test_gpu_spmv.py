@@ -348,3 +348,40 @@ def test_many_token_fused_epilogue(egt, port, torch, M):
     acc = res.clone()
     d.spmv_fused_into(x, acc, residual=acc)
     assert torch.equal(acc, res + plain)
+
+
+def test_gemv_f32_dense_baseline(egt, torch):
+    """The dense-FP arm (egt_gemv_f32) against a float64 product."""
+    rng = np.random.default_rng(55)
+    for rows, cols in [(7, 13), (300, 1024)]:
+        w = rng.uniform(-1, 1, (rows, cols)).astype(np.float32)
+        x = rng.uniform(-1, 1, cols).astype(np.float32)
+        y = egt.gemv_f32(torch.from_numpy(w).cuda(), torch.from_numpy(x).cuda()).cpu().numpy()
+        want = w.astype(np.float64) @ x.astype(np.float64)
+        assert np.max(np.abs(y - want) / (1 + np.abs(want))) < 1e-5
+
+
+def test_bench_spmv_harness(egt, torch):
+    """bench_spmv / bench_csv (packed.cpp:310-393) on the device: the
+    reference's CSV layout, variant order and analytic bytes (checked against
+    the unmodified reference harness when oracle/_ref is built), its errors."""
+    import os
+
+    csv = egt.bench_spmv([(256, 512)], reps=3, seed=11)
+    lines = csv.strip().split("\n")
+    assert lines[0] == "variant,rows,cols,pattern,median_ns,p95_ns,bytes"
+    rows = [l.split(",") for l in lines[1:]]
+    assert [(r[0], r[3]) for r in rows] == [("dense-fp", "dense"), ("quant-dense", "dense"),
+                                            ("packed-2:4", "2:4"), ("packed-1:4", "1:4")]
+    assert all(int(r[4]) > 0 and int(r[5]) >= int(r[4]) for r in rows)
+    ref_lib = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref",
+                           "libegt_ref.so")
+    if os.path.exists(ref_lib):
+        from oracle.oracle import Oracle
+
+        _, _, ref_bytes = Oracle("reference").ref_bench_spmv(256, 512, 1, 11)
+        assert [int(r[6]) for r in rows] == ref_bytes
+    with pytest.raises(egt.InvalidArgument, match="repetitions must be positive"):
+        egt.bench_spmv([(16, 64)], reps=0)
+    with pytest.raises(egt.InvalidArgument, match="multiple of 4"):
+        egt.bench_spmv([(16, 66)], reps=1)
