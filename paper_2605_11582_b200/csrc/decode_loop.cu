@@ -67,32 +67,53 @@ __global__ void dec_embed_kernel(const int32_t* state, const float* emb, const f
 // One block per head: append k,v at row t, scores over keys 0..t (warp per
 // key, coalesced 4 floats per lane), softmax (max-subtracted, model.cpp:
 // 169-182), o = p V (thread per head dimension, two key halves).
+constexpr int kKvPre = 64;  // cached keys / values staged into shared memory before the PDL wait
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem) : "memory");
+}
+
 template <int DH>
 __global__ void __launch_bounds__(256) dec_attention_kernel(const int32_t* state, const float* q, const float* k,
                                                             const float* v, float* kc, float* vc, float* o, int d,
-                                                            float scale) {
-  extern __shared__ float sc[];  // [t + 1] scores
+                                                            float scale, int sc_cap) {
+  extern __shared__ __align__(16) float smx[];
+  float* sc = smx;                      // [t + 1] scores (sc_cap floats)
+  float* kp = smx + sc_cap;             // [kKvPre][DH] cached keys
+  float* vp = kp + kKvPre * DH;         // [kKvPre][DH] cached values
   __shared__ float red[8];
   __shared__ __align__(16) float qs[DH];
   __shared__ float part[8][DH];
   // launched with programmatic serialization: let the O product start
-  // streaming its weights now, wait for q/k/v before reading them
+  // streaming its weights now.  Cache rows [0, t) were written by earlier
+  // steps (complete: every kernel before this one's predecessor has
+  // finished), so they are staged while the Q/K/V product still runs; q, k,
+  // v (row t) only after the wait.
   egt_dev::pdl_launch_dependents();
-  egt_dev::pdl_wait();
   const int t = state[0], n = t + 1;
   const int hh = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const size_t base = static_cast<size_t>(hh) * DH;
+  const int npre = min(t, kKvPre);
+  for (int idx = tid; idx < npre * (DH / 4); idx += blockDim.x) {
+    const int i = idx / (DH / 4), e4 = (idx % (DH / 4)) * 4;
+    cp_async16(kp + i * DH + e4, kc + static_cast<size_t>(i) * d + base + e4);
+    cp_async16(vp + i * DH + e4, vc + static_cast<size_t>(i) * d + base + e4);
+  }
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  egt_dev::pdl_wait();
   for (int i = tid; i < DH; i += blockDim.x) {
     kc[static_cast<size_t>(t) * d + base + i] = k[base + i];
     vc[static_cast<size_t>(t) * d + base + i] = v[base + i];
     qs[i] = q[base + i];
   }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
   __syncthreads();
   // scores: a thread per key, the key's head slice as float4 loads (all of a
   // thread's loads in flight together); row t was just written by this block
   static_assert(DH % 4 == 0, "head dimension multiple of 4");
   for (int i = tid; i < n; i += blockDim.x) {
-    const float4* kr = reinterpret_cast<const float4*>(kc + static_cast<size_t>(i) * d + base);
+    const float4* kr = reinterpret_cast<const float4*>(i < npre ? kp + i * DH : kc + static_cast<size_t>(i) * d + base);
     float dot = 0.f;
 #pragma unroll
     for (int e = 0; e < DH / 4; ++e) {
@@ -136,14 +157,15 @@ __global__ void __launch_bounds__(256) dec_attention_kernel(const int32_t* state
 #pragma unroll
       for (int r = 0; r < 4; ++r) {
         const float p_ = sc[i + 8 * r];
-        const float* vr = vc + static_cast<size_t>(i + 8 * r) * d + base + lane * PER;
+        const int ii = i + 8 * r;
+        const float* vr = (ii < npre ? vp + ii * DH : vc + static_cast<size_t>(ii) * d + base) + lane * PER;
 #pragma unroll
         for (int e = 0; e < PER; ++e) acc[e] = fmaf(p_, vr[e], acc[e]);
       }
     }
     for (; i < n; i += 8) {
       const float p_ = sc[i];
-      const float* vr = vc + static_cast<size_t>(i) * d + base + lane * PER;
+      const float* vr = (i < npre ? vp + i * DH : vc + static_cast<size_t>(i) * d + base) + lane * PER;
 #pragma unroll
       for (int e = 0; e < PER; ++e) acc[e] = fmaf(p_, vr[e], acc[e]);
     }
@@ -226,7 +248,8 @@ egt_status enqueue_step(egt_decoder* dd) {
     if (st == EGT_OK)
       st = egt_spmv_fused(w, x, y, 1, w->cols, w->rows, res, w->rows, input, kNormEps, flags, l2pf ? next : nullptr, s);
   };
-  const size_t attn_smem = static_cast<size_t>(dd->max_len) * sizeof(float);
+  const int sc_cap = static_cast<int>((dd->max_len + 3) / 4 * 4);
+  const size_t attn_smem = (static_cast<size_t>(sc_cap) + 2ull * kKvPre * dh) * sizeof(float);
   for (uint32_t l = 0; l < c.n_layers && st == EGT_OK; ++l) {
     const egt_dev_packed* const* w = m->layers.data() + 6 * l;
     const bool qkv_fused = getenv("EGT_DECODE_NO_QKV") == nullptr && w[0]->format == w[1]->format &&
@@ -248,6 +271,8 @@ egt_status enqueue_step(egt_decoder* dd) {
                : dh == 32 ? reinterpret_cast<void*>(&dec_attention_kernel<32>)
                : dh == 64 ? reinterpret_cast<void*>(&dec_attention_kernel<64>)
                           : reinterpret_cast<void*>(&dec_attention_kernel<128>);
+      if (attn_smem > 48 * 1024) DCUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                          static_cast<int>(attn_smem)));
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(H);
       cfg.blockDim = dim3(256);
@@ -263,7 +288,8 @@ egt_status enqueue_step(egt_decoder* dd) {
       float* o_ = dd->o;
       int d_ = static_cast<int>(d);
       float sc_ = scale;
-      void* args[] = {&st_, &q_, &k_, &v_, &kc, &vc, &o_, &d_, &sc_};
+      int cap_ = sc_cap;
+      void* args[] = {&st_, &q_, &k_, &v_, &kc, &vc, &o_, &d_, &sc_, &cap_};
       DCUDA(cudaLaunchKernelExC(&cfg, fn, args));
     }
     ++launch_counter();
