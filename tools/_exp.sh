@@ -1,3 +1,4 @@
-bash tools/gpu_round.sh r01d > gpurun_out/round_r01d.log 2>&1
-python tools/ncu_summary.py gpurun_out/prof_r01d.ncu-rep > gpurun_out/prof_r01d_summary.txt 2>&1
-rm -f gpurun_out/prof_r01d.ncu-rep
+exec > gpurun_out/exp.log 2>&1
+for st in 300 1000 300 3000; do
+timeout 600 python bench.py --steps $st --warmup 10 --no-decode --no-sharded --no-formats 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print($st, d['value'], d['roofline']['frac'], d['clocks'])"
+done
