@@ -194,3 +194,20 @@ def test_fused_allgather_two_processes_ipc(egt, torch):
     for pr in procs:
         pr.join(timeout=60)
     assert all(ok for _, ok, _ in res), res
+
+
+def test_fused_allgather_empty_shards(egt, port, torch):
+    """More ranks than row tiles: empty shards still signal, so every rank's
+    wait completes and the gathered y is whole."""
+    from paper_2605_11582_b200.parallel import PeerGroup, RowShardPlan
+
+    rng = np.random.default_rng(9)
+    p, d = _layer(egt, port, rng, "int4-2:4", 32, 256)
+    plan = RowShardPlan.make(d.rows, 4)
+    assert any(r1 == r0 for r0, r1 in plan.bounds)
+    groups = PeerGroup.local_ranks(4, d.rows)
+    xs = rng.uniform(-1, 1, d.cols).astype(np.float32)
+    ys, want = _run_local(torch, d, groups, plan, torch.from_numpy(xs).cuda(), 1)
+    assert all(torch.equal(y, want) for y in ys)
+    for g in groups:
+        g.check()
