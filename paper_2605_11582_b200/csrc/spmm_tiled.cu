@@ -681,7 +681,8 @@ TiledSchedule plan_tiled_rt(const egt_dev_packed* h, int RT, int M, int num_sms,
   const double unit_cycles = 90.0 * NT;  // issue slots per (warp, k-quad unit)
   // <= ~100 KB and <= one CTA per SM: the next kernel's CTAs fit beside this
   // kernel's (programmatic dependent launch) and prefetch their weights.
-  const size_t smem_cap = 100 * 1024;
+  static const size_t indep_cap = getenv("EGT_INDEP_SMEM_KB") ? atoi(getenv("EGT_INDEP_SMEM_KB")) * 1024 : 100 * 1024;
+  const size_t smem_cap = indep ? indep_cap : 100 * 1024;
   double best_cost = 1e300;
   for (int S = 1; S <= std::min(KQ, g_allow_waves ? 64 : 8); ++S) {
     const int KC = (KQ + S - 1) / S;
