@@ -40,6 +40,7 @@ struct WideArgs {
   const uint32_t* xf;  // x fragments
   float* y;
   int KQ, rt_begin, RT, rows, M, ldy, RB, CH, NSTW, wstage_bytes, xstage_bytes, KTtot;
+  int XS;  // x chunk stages
   const float* res;  // y = res + product (may alias y; row stride ldr), model.cpp:186/190
   int ldr;
   int out_silu;      // y = silu(...), model.cpp:80-84 (the next product's input)
@@ -94,13 +95,13 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) wide_spmm_kernel(const WideA
   const int tb = blockIdx.y;
   const int NCH = (a.KQ + a.CH - 1) / a.CH;
   uint64_t* xfull = reinterpret_cast<uint64_t*>(smem_raw);
-  uint64_t* xempty = xfull + 2;
-  uint64_t* wfull = xempty + 2;
+  uint64_t* xempty = xfull + a.XS;
+  uint64_t* wfull = xempty + a.XS;
   uint64_t* wempty = wfull + a.NSTW;
-  uint8_t* xst = smem_raw + ((16 * (4 + 2 * a.NSTW) + 127) / 128) * 128;
-  uint8_t* wst = xst + 2 * a.xstage_bytes;
+  uint8_t* xst = smem_raw + ((16 * (2 * a.XS + 2 * a.NSTW) + 127) / 128) * 128;
+  uint8_t* wst = xst + static_cast<size_t>(a.XS) * a.xstage_bytes;
   if (tid == 0) {
-    for (int s = 0; s < 2; ++s) {
+    for (int s = 0; s < a.XS; ++s) {
       mbar_init(xfull + s, 1);
       mbar_init(xempty + s, nw);
     }
@@ -122,8 +123,8 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) wide_spmm_kernel(const WideA
       long long wq = 0;
       for (int c = 0; c < NCH; ++c) {
         const int kq0 = c * a.CH, n = min(a.CH, a.KQ - kq0);
-        const int xs = c & 1;
-        if (c >= 2) mbar_wait(xempty + xs, ((c >> 1) - 1) & 1);
+        const int xs = c % a.XS;
+        if (c >= a.XS) mbar_wait(xempty + xs, ((c / a.XS) - 1) & 1);
         const uint32_t xb = static_cast<uint32_t>(n) * 4 * 512;  // bytes per n-tile
         mbar_expect_tx(xfull + xs, 4 * xb);
         for (int nt = 0; nt < 4; ++nt) {
@@ -165,8 +166,8 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) wide_spmm_kernel(const WideA
   static_assert(kWideMaxRT == 2, "lockstep over two row tiles");
   for (int c = 0; c < NCH; ++c) {
     const int n = min(a.CH, a.KQ - c * a.CH);
-    const int xs = c & 1;
-    mbar_wait(xfull + xs, (c >> 1) & 1);
+    const int xs = c % a.XS;
+    mbar_wait(xfull + xs, (c / a.XS) & 1);
     const uint32_t* sx = reinterpret_cast<const uint32_t*>(xst + xs * a.xstage_bytes);
     const uint8_t* st[kWideMaxRT] = {nullptr, nullptr};
     int wsi[kWideMaxRT] = {0, 0};
@@ -315,15 +316,17 @@ cudaError_t launch_wide(const egt_dev_packed* h, const float* x, int ldx, int M,
   const int blk = 32 * (val_lane_bytes(fmt) + meta_lane_bytes(fmt)) + (has_scales(fmt) ? E * 80 : 0);
   static const int ch0 = getenv("EGT_WIDE_CH") ? atoi(getenv("EGT_WIDE_CH")) : 4;
   static const int cap = getenv("EGT_WIDE_NSTW") ? atoi(getenv("EGT_WIDE_NSTW")) : 32;
+  static const int xs_env = getenv("EGT_WIDE_XS") ? atoi(getenv("EGT_WIDE_XS")) : 2;
+  a.XS = std::max(2, std::min(8, xs_env));
   for (a.CH = std::max(1, ch0);; a.CH /= 2) {
     a.wstage_bytes = (a.CH * blk + 127) / 128 * 128;
     a.xstage_bytes = 4 * a.CH * 4 * 512;
-    const int budget = 200 * 1024 - 2 * a.xstage_bytes - 1024;
+    const int budget = 200 * 1024 - a.XS * a.xstage_bytes - 1024;
     a.NSTW = std::min(std::max(cap, RB), budget / a.wstage_bytes);
     if (a.NSTW >= RB || a.CH == 1) break;
   }
   if (a.NSTW < RB) return cudaErrorInvalidConfiguration;
-  const size_t smem = (16 * (4 + 2 * a.NSTW) + 127) / 128 * 128 + 2 * static_cast<size_t>(a.xstage_bytes) +
+  const size_t smem = (16 * (2 * a.XS + 2 * a.NSTW) + 127) / 128 * 128 + static_cast<size_t>(a.XS) * a.xstage_bytes +
                       static_cast<size_t>(a.NSTW) * a.wstage_bytes;
   void* fn = pick_wide(fmt, h->tiled.SS, NW);
   cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
