@@ -295,13 +295,35 @@ cudaError_t launch_wide(const egt_dev_packed* h, const float* x, int ldx, int M,
   // M = 80 products 16-21 % faster with 12, M = 272 8 % slower).
   static const int nw_env = getenv("EGT_WIDE_NW") ? atoi(getenv("EGT_WIDE_NW")) : 0;
   const int NW = nw_env == 8 || nw_env == 12 ? nw_env : (TB <= 8 ? 12 : 8);
+  // Consumer warps hold up to two row tiles' stages of one chunk at once, so
+  // the weight ring must cover a whole chunk (NSTW >= RB): then issuing chunk
+  // c only ever waits for stages of chunk c - 1, which complete unconditionally.
+  const int blk = 32 * (val_lane_bytes(fmt) + meta_lane_bytes(fmt)) + (has_scales(fmt) ? E * 80 : 0);
+  static const int ch0 = getenv("EGT_WIDE_CH") ? atoi(getenv("EGT_WIDE_CH")) : 8;
+  static const int cap = getenv("EGT_WIDE_NSTW") ? atoi(getenv("EGT_WIDE_NSTW")) : 32;
+  static const int xs_env = getenv("EGT_WIDE_XS") ? atoi(getenv("EGT_WIDE_XS")) : 2;
+  a.XS = std::max(2, std::min(8, xs_env));
+  // k-quads per stage for rb row tiles: the largest CH <= ch0 whose ring
+  // still holds a whole chunk
+  auto chunk_for = [&](int rb) {
+    int ch = std::max(1, ch0);
+    for (;; ch /= 2) {
+      const int wsb = (ch * blk + 127) / 128 * 128;
+      const int budget = 200 * 1024 - a.XS * 4 * ch * 4 * 512 - 1024;
+      if ((budget > 0 && std::min(std::max(cap, rb), budget / wsb) >= rb) || ch == 1) return ch;
+    }
+  };
+  // RB: critical path of the busiest SM = waves x (consumer warps per
+  // scheduler) x (row tiles per warp), x1.35 when the ring only fits chunks
+  // of < 8 k-quads (the single producer thread's TMA issue rate then bounds
+  // the kernel: measured, tools/wide_probe.py); ties -> the larger RB.
   int RB = 1;
   double best = 1e300;
   for (int rb = 1; rb <= NW * kWideMaxRT; ++rb) {
     const long long grid = static_cast<long long>((RT + rb - 1) / rb) * TB;
     const double waves = std::ceil(static_cast<double>(grid) / num_sms);
     const int busy = std::min(rb, NW);
-    const double cost = waves * ((busy + 3) / 4) * ((rb + NW - 1) / NW);
+    const double cost = waves * ((busy + 3) / 4) * ((rb + NW - 1) / NW) * (chunk_for(rb) >= 8 ? 1.0 : 1.35);
     if (cost <= best) {
       best = cost;
       RB = rb;
@@ -310,14 +332,6 @@ cudaError_t launch_wide(const egt_dev_packed* h, const float* x, int ldx, int M,
   static const int rb_force = getenv("EGT_WIDE_RB") ? atoi(getenv("EGT_WIDE_RB")) : 0;
   if (rb_force > 0) RB = std::min(rb_force, NW * kWideMaxRT);
   a.RB = RB;
-  // Consumer warps hold up to two row tiles' stages of one chunk at once, so
-  // the weight ring must cover a whole chunk (NSTW >= RB): then issuing chunk
-  // c only ever waits for stages of chunk c - 1, which complete unconditionally.
-  const int blk = 32 * (val_lane_bytes(fmt) + meta_lane_bytes(fmt)) + (has_scales(fmt) ? E * 80 : 0);
-  static const int ch0 = getenv("EGT_WIDE_CH") ? atoi(getenv("EGT_WIDE_CH")) : 4;
-  static const int cap = getenv("EGT_WIDE_NSTW") ? atoi(getenv("EGT_WIDE_NSTW")) : 32;
-  static const int xs_env = getenv("EGT_WIDE_XS") ? atoi(getenv("EGT_WIDE_XS")) : 2;
-  a.XS = std::max(2, std::min(8, xs_env));
   for (a.CH = std::max(1, ch0);; a.CH /= 2) {
     a.wstage_bytes = (a.CH * blk + 127) / 128 * 128;
     a.xstage_bytes = 4 * a.CH * 4 * 512;
