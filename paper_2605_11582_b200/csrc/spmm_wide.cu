@@ -314,16 +314,16 @@ cudaError_t launch_wide(const egt_dev_packed* h, const float* x, int ldx, int M,
     }
   };
   // RB: critical path of the busiest SM = waves x (consumer warps per
-  // scheduler) x (row tiles per warp), x1.35 when the ring only fits chunks
-  // of < 8 k-quads (the single producer thread's TMA issue rate then bounds
-  // the kernel: measured, tools/wide_probe.py); ties -> the larger RB.
+  // scheduler) x (row tiles per warp), x1.35 when the ring only fits weight
+  // stages under 6 KB (the single producer thread's TMA issue rate then
+  // bounds the kernel: measured, tools/wide_probe.py); ties -> the larger RB.
   int RB = 1;
   double best = 1e300;
   for (int rb = 1; rb <= NW * kWideMaxRT; ++rb) {
     const long long grid = static_cast<long long>((RT + rb - 1) / rb) * TB;
     const double waves = std::ceil(static_cast<double>(grid) / num_sms);
     const int busy = std::min(rb, NW);
-    const double cost = waves * ((busy + 3) / 4) * ((rb + NW - 1) / NW) * (chunk_for(rb) >= 8 ? 1.0 : 1.35);
+    const double cost = waves * ((busy + 3) / 4) * ((rb + NW - 1) / NW) * (chunk_for(rb) * blk >= 6144 ? 1.0 : 1.35);
     if (cost <= best) {
       best = cost;
       RB = rb;
