@@ -51,6 +51,10 @@ struct WideArgs {
 // pair (k, k+1); column g = 2m + part, part 0 = fp16 hi, 1 = residual lo).
 __global__ void xfrag_kernel(const float* __restrict__ x, int ldx, int M, int cols, int KTtot, int TB,
                              uint32_t* __restrict__ xf) {
+  // launched programmatically: x (and the fragment workspace the previous
+  // product reads) belong to the preceding kernel
+  pdl_wait();
+  pdl_launch_dependents();
   const long long total = static_cast<long long>(TB) * 4 * KTtot * 32;
   for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
        idx += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -265,7 +269,20 @@ cudaError_t launch_wide(const egt_dev_packed* h, const float* x, int ldx, int M,
   {
     const long long total = static_cast<long long>(TB) * 4 * KTtot * 32;
     const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 8LL * num_sms));
-    xfrag_kernel<<<blocks, 256, 0, ctx.stream>>>(x, ldx, M, static_cast<int>(h->cols), KTtot, TB, xf_ws);
+    cudaLaunchConfig_t xc = {};
+    xc.gridDim = dim3(blocks);
+    xc.blockDim = dim3(256);
+    xc.stream = ctx.stream;
+    cudaLaunchAttribute xa[1];
+    xa[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    xa[0].val.programmaticStreamSerializationAllowed = 1;
+    xc.attrs = xa;
+    xc.numAttrs = ctx.pdl ? 1 : 0;
+    const int cols_ = static_cast<int>(h->cols);
+    void* xargs[] = {const_cast<float**>(&x), &ldx, &M, const_cast<int*>(&cols_), const_cast<int*>(&KTtot),
+                     const_cast<int*>(&TB), &xf_ws};
+    cudaError_t xe = cudaLaunchKernelExC(&xc, reinterpret_cast<void*>(&xfrag_kernel), xargs);
+    if (xe != cudaSuccess) return xe;
     ++launch_counter();
   }
   WideArgs a;
