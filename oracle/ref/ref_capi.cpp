@@ -90,6 +90,8 @@ egt::QuantizedMatrix make_quant(uint32_t rows, uint32_t cols, const uint32_t* gs
 }
 }  // namespace
 
+void ref_set_error(const std::string& m) { g_err = m; }  // ref_model_capi.cpp
+
 extern "C" {
 
 const char* ref_last_error(void) { return g_err.c_str(); }

@@ -64,7 +64,6 @@ struct Workspace {
   size_t partial_floats = 0;
   uint32_t* counters = nullptr;
   size_t n_counters = 0;
-  int flip = 0;  // independent split-K launches alternate between two halves
 };
 std::mutex g_ws_mu;
 std::map<std::pair<int, cudaStream_t>, Workspace> g_ws;
@@ -645,20 +644,20 @@ egt_status spmv_impl(const egt_dev_packed* h, const float* x, float* y, uint32_t
     sc = it->second;
   }
   if (sc.smem == 0) return fail(EGT_EINTERNAL, "spmv: no feasible launch plan for this shape and token count");
+  // A split-K plan (the planner's fallback when no split-free independent
+  // plan fits) always launches dependent: its partials and arrival counters
+  // live in the shared workspace, which only stream order protects.
+  const bool run_indep = indep && sc.S <= 1;
   if (sc.S > 1) {
-    // Independent launches overlap their predecessor, but a product starts
-    // only after every kernel before its predecessor finished: two
-    // alternating workspace halves are enough.
     const size_t fl = tiled_workspace_floats(h, sc, M), nc = static_cast<size_t>(sc.grid_x) * sc.grid_z;
     Workspace* w = nullptr;
-    egt_status st = get_workspace(s, 2 * fl, 2 * nc, &w);
+    egt_status st = get_workspace(s, fl, nc, &w);
     if (st != EGT_OK) return st;
-    const int half = indep ? (w->flip ^= 1) : 0;
-    ctx.partial = w->partial + half * fl;
-    ctx.counters = w->counters + half * nc;
+    ctx.partial = w->partial;
+    ctx.counters = w->counters;
   }
   CUDA_TRY(launch_tiled(h, sc, x, static_cast<int>(ldx), static_cast<int>(M), y,
-                        static_cast<int>(ldy), ctx, indep));
+                        static_cast<int>(ldy), ctx, run_indep));
   return EGT_OK;
 }
 }  // namespace
@@ -698,16 +697,16 @@ egt_status egt_spmv_fused_multi(const egt_dev_packed* const* hs, uint32_t n, con
   const bool indep = (flags & EGT_SPMV_INDEPENDENT) != 0;
   const TiledSchedule sc = plan_tiled_rt(h, h->tiled.RT * static_cast<int>(n), 1, num_sms(), indep);
   if (sc.smem == 0) return fail(EGT_EINTERNAL, "spmv: no feasible launch plan for this shape and token count");
+  const bool run_indep = indep && sc.S <= 1;  // split-K plans launch dependent (see spmv_impl)
   if (sc.S > 1) {
     const size_t fl = static_cast<size_t>(sc.S) * h->tiled.RT * n * 16, nc = static_cast<size_t>(sc.grid_x) * sc.grid_z;
     Workspace* w = nullptr;
-    egt_status st = get_workspace(s, 2 * fl, 2 * nc, &w);
+    egt_status st = get_workspace(s, fl, nc, &w);
     if (st != EGT_OK) return st;
-    const int half = indep ? (w->flip ^= 1) : 0;
-    ctx.partial = w->partial + half * fl;
-    ctx.counters = w->counters + half * nc;
+    ctx.partial = w->partial;
+    ctx.counters = w->counters;
   }
-  CUDA_TRY(launch_tiled(h, sc, x, static_cast<int>(h->cols), 1, ys[0], static_cast<int>(h->rows), ctx, indep));
+  CUDA_TRY(launch_tiled(h, sc, x, static_cast<int>(h->cols), 1, ys[0], static_cast<int>(h->rows), ctx, run_indep));
   return EGT_OK;
 }
 
@@ -718,7 +717,11 @@ egt_status egt_spmv_allgather(const egt_dev_packed* shard, const float* x, uint3
   if (static_cast<uint64_t>(row0) + shard->rows > ldy)
     return fail(EGT_EINVAL, "spmv allgather: shard rows past the gathered output stride");
   if (M == 0) return EGT_OK;
-  return spmv_impl(shard, x, g->y[g->rank], M, ldx, ldy, flags & (EGT_SPMV_INDEPENDENT | EGT_PEER_NOWAIT), nullptr,
+  // With peers, calls on one group share the arrival counter (peer_ctrl[1])
+  // and the sequence target: two calls in flight at once would mix their
+  // counts, so exchanging calls always launch dependent (stream-ordered).
+  const uint32_t keep = g->world > 1 ? EGT_PEER_NOWAIT : (EGT_SPMV_INDEPENDENT | EGT_PEER_NOWAIT);
+  return spmv_impl(shard, x, g->y[g->rank], M, ldx, ldy, flags & keep, nullptr,
                    0, EGT_INPUT_NONE, 0.f, nullptr, stream, g, row0);
 }
 

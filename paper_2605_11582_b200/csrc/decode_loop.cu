@@ -43,6 +43,7 @@ struct egt_decoder {
   int32_t* out = nullptr;     // [max_len] token at each position
   cudaGraphExec_t exec = nullptr;
   cudaEvent_t ev_in = nullptr, ev_out = nullptr;
+  uint32_t host_t = 0;  // positions run so far (host mirror of state[0])
 };
 
 namespace {
@@ -56,9 +57,10 @@ egt_status dfail(egt_status s, const std::string& m) {
 }
 
 __global__ void dec_embed_kernel(const int32_t* state, const float* emb, const float* ptab, float* h, int d,
-                                 int32_t* out) {
+                                 int32_t* out, int max_len) {
   egt_dev::pdl_launch_dependents();  // the first Q product may prefetch its weights
   const int t = state[0], tok = state[1];
+  if (t >= max_len) return;  // replay past the cache: no-op (the host also refuses)
   if (threadIdx.x == 0 && blockIdx.x == 0) out[t] = tok;
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < d; c += gridDim.x * blockDim.x)
     h[c] = emb[static_cast<size_t>(tok) * d + c] + ptab[static_cast<size_t>(t) * d + c];
@@ -77,7 +79,7 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 template <int DH>
 __global__ void __launch_bounds__(256) dec_attention_kernel(const int32_t* state, const float* q, const float* k,
                                                             const float* v, float* kc, float* vc, float* o, int d,
-                                                            float scale, int sc_cap) {
+                                                            float scale, int sc_cap, int max_len) {
   extern __shared__ __align__(16) float smx[];
   float* sc = smx;                      // [t + 1] scores (sc_cap floats)
   float* kp = smx + sc_cap;             // [kKvPre][DH] cached keys
@@ -92,6 +94,7 @@ __global__ void __launch_bounds__(256) dec_attention_kernel(const int32_t* state
   // v (row t) only after the wait.
   egt_dev::pdl_launch_dependents();
   const int t = state[0], n = t + 1;
+  if (t >= max_len) return;  // past the cache rows / score buffer: no-op
   const int hh = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const size_t base = static_cast<size_t>(hh) * DH;
   const int npre = min(t, kKvPre);
@@ -183,7 +186,7 @@ __global__ void __launch_bounds__(256) dec_attention_kernel(const int32_t* state
 // next token: the prompt's while t + 1 is inside it, else argmax (ties ->
 // lowest id); advances t.
 __global__ void __launch_bounds__(1024) dec_next_kernel(int32_t* state, const int32_t* prompt, const float* logits,
-                                                        int vocab) {
+                                                        int vocab, int max_len) {
   __shared__ float bv[32];
   __shared__ int bi[32];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -219,8 +222,10 @@ __global__ void __launch_bounds__(1024) dec_next_kernel(int32_t* state, const in
         idx = bi[w];
       }
     const int t = state[0];
-    state[1] = t + 1 < state[2] ? prompt[t + 1] : idx;
-    state[0] = t + 1;
+    if (t < max_len) {  // never advance past the cache
+      state[1] = t + 1 < state[2] ? prompt[t + 1] : idx;
+      state[0] = t + 1;
+    }
   }
 }
 
@@ -236,7 +241,8 @@ egt_status enqueue_step(egt_decoder* dd) {
   const egt_model_config& c = m->cfg;
   const uint32_t d = c.d_model, H = c.n_heads, dh = d / H;
   cudaStream_t s = dd->s;
-  dec_embed_kernel<<<(d + 255) / 256, 256, 0, s>>>(dd->state, m->emb, m->pos, dd->h, static_cast<int>(d), dd->out);
+  dec_embed_kernel<<<(d + 255) / 256, 256, 0, s>>>(dd->state, m->emb, m->pos, dd->h, static_cast<int>(d), dd->out,
+                                                    static_cast<int>(dd->max_len));
   ++launch_counter();
   const float scale = 1.0f / std::sqrt(static_cast<float>(dh));  // model.cpp:139
   egt_status st = EGT_OK;
@@ -289,7 +295,8 @@ egt_status enqueue_step(egt_decoder* dd) {
       int d_ = static_cast<int>(d);
       float sc_ = scale;
       int cap_ = sc_cap;
-      void* args[] = {&st_, &q_, &k_, &v_, &kc, &vc, &o_, &d_, &sc_, &cap_};
+      int ml_ = static_cast<int>(dd->max_len);
+      void* args[] = {&st_, &q_, &k_, &v_, &kc, &vc, &o_, &d_, &sc_, &cap_, &ml_};
       DCUDA(cudaLaunchKernelExC(&cfg, fn, args));
     }
     ++launch_counter();
@@ -299,7 +306,8 @@ egt_status enqueue_step(egt_decoder* dd) {
   }
   lin(m->head, dd->h, dd->logits, nullptr, EGT_INPUT_RMSNORM, 0, m->layers[0]);
   if (st != EGT_OK) return st;
-  dec_next_kernel<<<1, 1024, 0, s>>>(dd->state, dd->prompt, dd->logits, static_cast<int>(c.vocab_size));
+  dec_next_kernel<<<1, 1024, 0, s>>>(dd->state, dd->prompt, dd->logits, static_cast<int>(c.vocab_size),
+                                     static_cast<int>(dd->max_len));
   ++launch_counter();
   DCUDA(cudaGetLastError());
   return EGT_OK;
@@ -386,11 +394,15 @@ egt_status egt_decoder_start(egt_decoder* dd, const int32_t* prompt, uint32_t pr
   DCUDA(cudaMemcpyAsync(dd->state, st, sizeof(st), cudaMemcpyHostToDevice, dd->s));
   DCUDA(cudaMemcpyAsync(dd->prompt, prompt, prompt_len * sizeof(int32_t), cudaMemcpyHostToDevice, dd->s));
   DCUDA(cudaStreamSynchronize(dd->s));  // the host buffers may be reused on return
+  dd->host_t = 0;
   return EGT_OK;
 }
 
 egt_status egt_decoder_step(egt_decoder* dd, uint32_t n_steps, void* stream) {
   if (!dd) return dfail(EGT_EINVAL, "decoder: null decoder");
+  if (static_cast<uint64_t>(dd->host_t) + n_steps > dd->max_len)
+    return dfail(EGT_EINVAL, "decoder: step past max_len");
+  dd->host_t += n_steps;
   cudaStream_t us = static_cast<cudaStream_t>(stream);
   DCUDA(cudaEventRecord(dd->ev_in, us));
   DCUDA(cudaStreamWaitEvent(dd->s, dd->ev_in, 0));
