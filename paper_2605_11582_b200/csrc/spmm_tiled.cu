@@ -19,6 +19,7 @@
 #include "device_common.cuh"
 #include "handle.h"
 #include "tiled_compute.cuh"
+#include "xrange.cuh"
 #ifndef EGT_X4
 #define EGT_X4 4
 #endif
@@ -83,6 +84,10 @@ struct TiledArgs {
   float* peer_y[kMaxPeers];
   uint32_t* peer_flag[kMaxPeers];
   uint32_t* peer_ctrl;  // this rank's [expected, done, error]
+  // INT4 1:4 stored as 2:4 with zero-valued partners (the non-finite x
+  // fix-up must skip the partners: they are not kept entries)
+  int pad14;
+  int seg_pad14[3];
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -142,6 +147,31 @@ __device__ __forceinline__ void peer_complete(const TiledArgs& a, unsigned expec
   if (a.peer_wait) peer_wait_all(a.peer_flag[a.peer_rank], a.npeer, a.peer_ctrl);
 }
 
+// Non-finite x (xrange.cuh): sum of W[row][c] * x'[c] over the kept entries
+// of row whose transformed input x'[c] is inf / NaN, c in [c0, c1).
+template <int FMT, int SS, bool FUSED>
+__device__ __noinline__ float nonfinite_terms(const TiledArgs& a, int row, int tok, int c0, int c1, float inv) {
+  TiledRef m{a.vals, a.meta, a.scales, a.zps, a.KQ, a.rt_begin, SS, a.pad14};
+  int r = row;
+  if (FUSED && a.nseg > 1) {
+    const int sg = row / a.rows_s;
+    m = TiledRef{a.seg_vals[sg], a.seg_meta[sg], a.seg_scales[sg], a.seg_zps[sg], a.KQ, a.seg_rtb[sg], SS,
+                 a.seg_pad14[sg]};
+    r = row - sg * a.rows_s;
+  }
+  const float* xr = a.x + static_cast<size_t>(tok) * a.ldx;
+  float add = 0.f;
+  for (int c = c0; c < c1; ++c) {
+    float xv = xr[c];
+    if (FUSED && a.xform == EGT_INPUT_RMSNORM) xv *= inv;
+    else if (FUSED && a.xform == EGT_INPUT_SILU) xv = xv * (1.0f / (1.0f + expf(-xv)));
+    if ((__float_as_uint(xv) & 0x7fffffffu) < 0x7f800000u) continue;
+    float w;
+    if (tiled_value<FMT>(m, r, c, &w)) add += w * xv;
+  }
+  return add;
+}
+
 template <int FMT, int SS, int NT, bool SINGLE, bool FUSED>
 __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(const TiledArgs a) {
   constexpr int E = 4 / SS;
@@ -188,6 +218,9 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
   uint32_t* sB = reinterpret_cast<uint32_t*>(smem_raw + 16 * NST + 128 - (16 * NST) % 128);
   uint8_t* stages = reinterpret_cast<uint8_t*>(sB + NT * KTc * LS * 4);
   float* red = reinterpret_cast<float*>(stages + static_cast<size_t>(NST) * sbytes);  // [RB][nw][Mc][16]
+  // per token of the CTA: x window range (xrange.cuh) and the 2^-e rescale
+  __shared__ uint32_t s_xmx[16], s_xnf[16];
+  __shared__ float s_unsc[16];
 
   if (tid == 0) {
     for (int s = 0; s < NST; ++s) {
@@ -195,6 +228,11 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
       mbar_init(empty + s, nw);
     }
     mbar_fence_init();
+  }
+  if (tid < 16) {
+    s_xmx[tid] = 0u;
+    s_xnf[tid] = 0u;
+    s_unsc[tid] = 1.f;
   }
   __syncthreads();
 
@@ -319,7 +357,43 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
         for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) tot += s_red[w];
         inv = 1.0f / sqrtf(tot / static_cast<float>(a.cols) + a.eps);
       }
-      auto pair = [](float p0, float p1) {
+      auto xform4 = [&](float4 q) {
+        if (FUSED && a.xform == EGT_INPUT_RMSNORM) {
+          q.x *= inv; q.y *= inv; q.z *= inv; q.w *= inv;
+        } else if (FUSED && a.xform == EGT_INPUT_SILU) {
+          const float2 q0 = silu2(make_float2(q.x, q.y)), q1 = silu2(make_float2(q.z, q.w));
+          q = make_float4(q0.x, q0.y, q1.x, q1.y);
+        }
+        return q;
+      };
+      // window range (xrange.cuh): from the registers in one pass, else a
+      // separate read of the window
+      {
+        uint32_t mx = 0u, nf = 0u;
+        if (one_pass) {
+#pragma unroll
+          for (int u = 0; u < X4; ++u) {
+            v[u] = xform4(v[u]);
+            xr_note(mx, nf, v[u].x); xr_note(mx, nf, v[u].y); xr_note(mx, nf, v[u].z); xr_note(mx, nf, v[u].w);
+          }
+        } else {
+          for (int j = tid; j < nf4; j += blockDim.x) {
+            if (4 * j < nwin) {
+              const float4 q = xform4(__ldg(reinterpret_cast<const float4*>(xb) + j));
+              xr_note(mx, nf, q.x); xr_note(mx, nf, q.y); xr_note(mx, nf, q.z); xr_note(mx, nf, q.w);
+            }
+          }
+        }
+        xr_commit(mx, nf, s_xmx, s_xnf);
+        if (tid == 0) s_inv[0] = inv;
+        __syncthreads();
+      }
+      const int xe = xr_exp(s_xmx[0]);
+      const float xsc = xr_pow2(xe);
+      if (tid == 0) s_unsc[0] = xr_pow2(-xe);
+      auto pair = [xsc](float p0, float p1) {
+        p0 = xr_scaled(p0, xsc);
+        p1 = xr_scaled(p1, xsc);
         const __half h0 = __float2half_rn(p0), h1 = __float2half_rn(p1);
         const __half l0 = __float2half_rn(p0 - __half2float(h0));
         const __half l1 = __float2half_rn(p1 - __half2float(h1));
@@ -339,13 +413,7 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
         for (int u = 0; u < X4; ++u) {
           const int j = base + tid + u * static_cast<int>(blockDim.x);
           if (j < nf4) {
-            float4 q = v[u];
-            if (FUSED && a.xform == EGT_INPUT_RMSNORM) {
-              q.x *= inv; q.y *= inv; q.z *= inv; q.w *= inv;
-            } else if (FUSED && a.xform == EGT_INPUT_SILU) {
-              const float2 q0 = silu2(make_float2(q.x, q.y)), q1 = silu2(make_float2(q.z, q.w));
-              q = make_float4(q0.x, q0.y, q1.x, q1.y);
-            }
+            const float4 q = one_pass ? v[u] : xform4(v[u]);  // one pass: transformed above
             const int kt = j >> 3, w = (j & 7) * 4, reg = w >> 3, t = (w & 7) >> 1;
             uint32_t* row = sB + static_cast<size_t>(kt) * 32;
             const uint2 a0 = pair(q.x, q.y), a1 = pair(q.z, q.w);
@@ -385,12 +453,26 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
       float tot = 0.f;
       for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) tot += s_red[w];
       const float inv = 1.0f / sqrtf(tot / static_cast<float>(a.cols) + a.eps);
+      uint32_t mx = 0u, nf = 0u;
+#pragma unroll
+      for (int u = 0; u < XU; ++u) {
+        v[u].x *= inv;
+        v[u].y *= inv;
+        xr_note(mx, nf, v[u].x);
+        xr_note(mx, nf, v[u].y);
+      }
+      xr_commit(mx, nf, s_xmx, s_xnf);
+      if (tid == 0) s_inv[0] = inv;
+      __syncthreads();
+      const int xe = xr_exp(s_xmx[0]);
+      const float xsc = xr_pow2(xe);
+      if (tid == 0) s_unsc[0] = xr_pow2(-xe);
 #pragma unroll
       for (int u = 0; u < XU; ++u) {
         const int i = tid + u * blockDim.x;
         if (i < items) {
           const int reg = i & 3, t = (i >> 2) & 3, kt = i >> 4;
-          const float x0 = v[u].x * inv, x1 = v[u].y * inv;
+          const float x0 = xr_scaled(v[u].x, xsc), x1 = xr_scaled(v[u].y, xsc);
           const __half h0 = __float2half_rn(x0), h1 = __float2half_rn(x1);
           const __half l0 = __float2half_rn(x0 - __half2float(h0));
           const __half l1 = __float2half_rn(x1 - __half2float(h1));
@@ -423,12 +505,31 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
       __syncthreads();
     }
   }
+  if (!staged && a.dbg != 3) {
+    // window range per token (xrange.cuh): one read of each token's window
+    const int k1 = min(a.cols, (kq0 + KCs) * 128);
+    for (int tl = 0; tl < Mc; ++tl) {
+      const float* xr = a.x + static_cast<size_t>(m0 + tl) * a.ldx;
+      const float inv = FUSED && a.xform == EGT_INPUT_RMSNORM ? s_inv[tl] : 1.f;
+      uint32_t mx = 0u, nf = 0u;
+      for (int k = kq0 * 128 + tid; k < k1; k += blockDim.x) {
+        float xv = __ldg(xr + k);
+        if (FUSED && a.xform == EGT_INPUT_RMSNORM) xv *= inv;
+        else if (FUSED && a.xform == EGT_INPUT_SILU) xv = silu2(make_float2(xv, 0.f)).x;
+        xr_note(mx, nf, xv);
+      }
+      xr_commit(mx, nf, s_xmx + tl, s_xnf + tl);
+    }
+    __syncthreads();
+    if (tid < Mc) s_unsc[tid] = xr_pow2(-xr_exp(s_xmx[tid]));
+  }
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) {
     const int mc = (a.dbg == 3 || staged) ? 0 : min(4, Mc - 4 * nt);
     for (int m = 0; m < mc; ++m) {
       const float* xr = a.x + static_cast<size_t>(m0 + 4 * nt + m) * a.ldx;
       const float inv = FUSED && a.xform == EGT_INPUT_RMSNORM ? s_inv[4 * nt + m] : 1.f;
+      const float xsc = xr_pow2(xr_exp(s_xmx[4 * nt + m]));
       const int items = KTc * 16;
       for (int i0 = 0; i0 < items; i0 += XU * static_cast<int>(blockDim.x)) {
         float2 v[XU];
@@ -457,6 +558,8 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
             } else if (FUSED && a.xform == EGT_INPUT_SILU) {
               v[u] = silu2(v[u]);
             }
+            v[u].x = xr_scaled(v[u].x, xsc);
+            v[u].y = xr_scaled(v[u].y, xsc);
             const __half h0 = __float2half_rn(v[u].x), h1 = __float2half_rn(v[u].y);
             const __half l0 = __float2half_rn(v[u].x - __half2float(h0));
             const __half l1 = __float2half_rn(v[u].y - __half2float(h1));
@@ -556,6 +659,9 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
     const int row = (rt0 + i) * 16 + row16;
     const int tok = m0 + tl;
     if (row < a.rows) {
+      v *= s_unsc[tl];  // undo the window's 2^e (xrange.cuh)
+      if (s_xnf[tl]) v += nonfinite_terms<FMT, SS, FUSED>(a, row, tok, kq0 * 128, min(a.cols, (kq0 + KCs) * 128),
+                                                         s_inv[tl]);
       if (a.S == 1) {
         float o = (FUSED && a.res ? (idx == tid ? res_pre : a.res[static_cast<size_t>(tok) * a.ldr + row]) : 0.f) + v;
         if (FUSED && a.out_silu) o = o * (1.0f / (1.0f + expf(-o)));  // model.cpp:80-84
@@ -842,8 +948,10 @@ cudaError_t launch_tiled(const egt_dev_packed* h, const TiledSchedule& sc, const
       a.seg_zps[g] = hg->tiled.zps;
       a.seg_y[g] = ctx.seg_y[g];
       a.seg_rtb[g] = hg->tiled.rt_begin;
+      a.seg_pad14[g] = hg->tiled.pad14;
     }
   }
+  a.pad14 = h->tiled.pad14;
   a.npeer = ctx.npeer;
   a.peer_rank = ctx.peer_rank;
   a.peer_row0 = ctx.peer_row0;
