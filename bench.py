@@ -83,7 +83,38 @@ def host_layer(rng, rows, cols):
 
 def shape_bytes(p) -> int:
     """Algorithmic bytes of one call: codes + index + 5 B/group + x + y."""
-    return (p.nnz + 1) // 2 + 2 * ((p.nnz + 7) // 8) + 5 * p.scales.size + 4 * p.cols + 4 * p.rows
+    nnz = p.nnz() if callable(p.nnz) else p.nnz
+    return (nnz + 1) // 2 + 2 * ((nnz + 7) // 8) + 5 * p.scales.size + 4 * p.cols + 4 * p.rows
+
+
+def ref_host_layers(seed):
+    """The sweep's layers encoded by the REFERENCE's own quantize_matrix +
+    pack (compress.cpp:157-197, packed.cpp:92-128, oracle/_ref) from the same
+    seeded weights / masks as host_layer: {shape: oracle Packed}."""
+    from oracle.oracle import Oracle
+
+    R = Oracle("reference")
+    rng = np.random.default_rng(seed)
+    pats = np.array([[1, 1, 0, 0], [1, 0, 1, 0], [1, 0, 0, 1], [0, 1, 1, 0], [0, 1, 0, 1], [0, 0, 1, 1]], bool)
+    out = {}
+    for rows, cols in sorted(set(LAYER_SHAPES)):
+        w = rng.uniform(-1, 1, (rows, cols)).astype(np.float32)
+        keep = pats[rng.integers(0, 6, (rows, cols // 4))].reshape(rows, cols)
+        mask = np.packbits(keep.reshape(-1), bitorder="little")
+        q = R.quantize(w, np.full(rows, GROUP, np.uint32), mask)
+        out[(rows, cols)] = R.pack_int4(mask, rows, cols, q, 2)
+    xs = {c: rng.uniform(-1, 1, c).astype(np.float32) for c in sorted({s[1] for s in LAYER_SHAPES})}
+    return out, xs
+
+
+def _cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
 
 
 def to_oracle(p):
@@ -136,57 +167,52 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ CPU legs
-def cpu_reference_run(host_layers, n_calls: int, threads: int, xs):
+def cpu_reference_run(ref_layers, steps: int, threads: int, xs):
     """The reference's own spmv (oracle/_ref, compiled from the reference
-    sources) on `threads` host threads, n_calls products rotating over the
-    sweep shapes; returns (GB/s, seconds, calls, outputs per shape)."""
+    sources) on `threads` host threads.  One CPU step = every thread runs one
+    product of each sweep shape (the whole host busy, the SPEC's permitted
+    per-call parallelism over independent requests); returns (GB/s, seconds,
+    calls, outputs per shape)."""
     from oracle.oracle import Oracle
 
     R = Oracle("reference")
-    keys = list(host_layers)
-    per_shape = [n_calls // len(keys) + (1 if i < n_calls % len(keys) else 0) for i in range(len(keys))]
     total_bytes = 0
     total_s = 0.0
     outs = {}
-    for k, calls in zip(keys, per_shape):
-        if calls == 0:
-            continue
-        per_thread = max(1, math.ceil(calls / threads))
-        t = min(threads, calls)
-        sec, y = R.ref_timed_spmv(to_oracle(host_layers[k]), xs[k[1]], per_thread, t)
+    for k, p in ref_layers.items():
+        sec, y = R.ref_timed_spmv(p, xs[k[1]], steps, threads)
         total_s += sec
-        total_bytes += shape_bytes(host_layers[k]) * per_thread * t
+        total_bytes += shape_bytes(p) * steps * threads
         outs[k] = y
-    return total_bytes / total_s / 1e9, total_s, sum(per_shape), outs
+    return total_bytes / total_s / 1e9, total_s, steps * threads * len(ref_layers), outs
 
 
 # ------------------------------------------------------------------ reference arm
 def run_reference(args):
+    """The reference arm: the reference's OWN encoder and spmv (oracle/_ref,
+    compiled unmodified from the reference sources), nothing of this
+    package; rank 0 only."""
     rank, world, _ = _dist()
     if rank != 0:
         return 0
-    import numpy as np
-
-    from paper_2605_11582_b200 import _build
-
-    _build.build()
-    rng = np.random.default_rng(2605)
-    host = {s: host_layer(rng, *s) for s in sorted(set(LAYER_SHAPES))}
-    xs = {c: rng.uniform(-1, 1, c).astype(np.float32) for c in sorted({s[1] for s in LAYER_SHAPES})}
+    ref_layers, xs = ref_host_layers(2605)
     threads = os.cpu_count() or 1
-    cpu_reference_run(host, min(args.warmup, 3), threads, xs)  # warm-up
-    gbs, sec, calls, _ = cpu_reference_run(host, args.steps, threads, xs)
+    cpu_reference_run(ref_layers, 1, threads, xs)  # warm-up
+    # a CPU step is ~0.5 s on 16 threads: at most 10 timed steps keep the arm within a minute
+    steps = max(1, min(args.steps, 10))
+    gbs, sec, calls, _ = cpu_reference_run(ref_layers, steps, threads, xs)
     line = {
         "impl": "reference", "metric": _metric(), "value": round(gbs, 4), "unit": "GB/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(1e3 * sec / max(calls, 1), 3),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int4-w/f32-acc",
-        "data": "synthetic U(-1,1) weights, random exact 2:4 masks, INT4 g128 (reference encoder layout)",
+        "data": "synthetic U(-1,1) weights, random exact 2:4 masks, INT4 g128 (the reference's own encoder)",
         "config": {"workload": "reference spmv (packed.cpp:211-220) over the Llama-2-7B layer sweep "
-                               "4096x4096 / 11008x4096 / 4096x11008, INT4 g128 2:4, batch 1; "
-                               "a step = one product on one host thread",
-                   "threads": threads},
+                               "4096x4096 / 11008x4096 / 4096x11008, INT4 g128 2:4, batch 1; a CPU step = "
+                               "every host thread runs one product of each shape",
+                   "threads": threads, "cpu_model": _cpu_model(), "timed_steps": steps},
         "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": "reference",
-                         "sample": f"{calls} reference spmv calls rotating over the 3 sweep shapes on {threads} threads"},
+                         "sample": f"{calls} reference spmv calls ({steps} steps x {threads} threads x 3 sweep "
+                                   f"shapes), {sec:.1f} s, {_cpu_model()}"},
         "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -484,8 +510,9 @@ def measure_decode(torch, egt, plan_name, n_tokens=64, prompt_len=16, max_len=25
            "weight_GBps": round(weight_bytes / (per_tok * 1e-3) / 1e9, 1),
            "context": f"prompt {prompt_len} + {n_tokens} tokens timed after 4 warm-up tokens (positions "
                       f"{prompt_len + 3}..{pos - 1})",
-           "e2e_tokens_per_s": round((prompt_len - 1 + n_tokens) / e2e_s, 1),
-           "e2e_note": "generate(): H2D prompt, prefill + n tokens, D2H tokens, host wall clock",
+           "e2e_tokens_per_s": round(n_tokens / e2e_s, 1),
+           "e2e_note": f"generate(): H2D prompt, {prompt_len - 1} prefill positions + {n_tokens} generated tokens, "
+                       "D2H tokens, host wall clock; tokens/s counts the generated tokens only",
            "finite_tokens": bool(all(0 <= t < cfg["vocab_size"] for t in toks2)), "setup_s": round(setup, 1),
            "verify_pass": verify}
     del dec, model, layers, head
@@ -549,7 +576,7 @@ def run_ours(args):
                 for c, t in self.inputs.items():
                     t.copy_(x_host[c], non_blocking=True)
                 self.graph.replay()
-                y_host.copy_(self.out, non_blocking=True)
+                y_host.copy_(self.yall, non_blocking=True)  # every GEMV's output
             self.stream.synchronize()
 
     sweep = Sweep(layers, stream)
@@ -669,7 +696,7 @@ def run_ours(args):
 
     # e2e through the public API with pinned host buffers
     x_host = {c: torch.from_numpy(xs[c]).pin_memory() for c in xs}
-    y_host = torch.empty(layers[-1].rows, dtype=torch.float32).pin_memory()
+    y_host = torch.empty(sweep.yall.numel(), dtype=torch.float32).pin_memory()
     for _ in range(2):
         sweep.step_host(x_host, y_host)
     e2e_steps = max(3, min(args.steps, 200))
@@ -685,7 +712,7 @@ def run_ours(args):
         e2e_s = float(t.item())
     e2e_value = world * step_bytes * e2e_steps / e2e_s / 1e9
     h2d = sum(4 * c for c in xs)
-    d2h = 4 * layers[-1].rows
+    d2h = 4 * sweep.yall.numel()
 
     peak, peak_kind = _peak_hbm()
     achieved = step_bytes / (ms_per_step * 1e-3) / 1e9
@@ -702,16 +729,25 @@ def run_ours(args):
     cpu_baseline = None
     if rank == 0 and world == 1 and not args.no_cpu:
         threads = os.cpu_count() or 1
-        gbs, sec, calls, outs = cpu_reference_run(host, 6 * threads, threads, xs)
+        ref_layers, ref_xs = ref_host_layers(2605)
+        # the reference's encoder produced the bytes the product's did
+        encodings_identical = all(
+            np.array_equal(ref_layers[s].index_words, host[s].index_words)
+            and np.array_equal(ref_layers[s].value_bytes, host[s].value_bytes)
+            and np.array_equal(ref_layers[s].scales.view(np.uint32), host[s].scales.view(np.uint32))
+            for s in ref_layers)
+        cpu_reference_run(ref_layers, 1, threads, ref_xs)  # warm-up
+        gbs, sec, calls, outs = cpu_reference_run(ref_layers, 2, threads, ref_xs)
         # checker: the GPU products of the sweep vs the reference's own spmv
         errs = []
         for s, y_ref in outs.items():
             d = next(d for d in layers if (d.rows, d.cols) == s)
-            y = d.spmv(torch.from_numpy(xs[s[1]]).cuda()).cpu().numpy()
+            y = d.spmv(torch.from_numpy(ref_xs[s[1]]).cuda()).cpu().numpy()
             errs.append(float(np.max(np.abs(y - y_ref) / (1 + np.abs(y_ref)))))
         cpu_baseline = {"value": round(gbs, 4), "unit": "GB/s", "cores": threads, "kind": "reference",
-                        "sample": f"{calls} reference spmv calls (oracle/_ref, packed.cpp:211-220) over the 3 "
-                                  f"sweep shapes, {threads} host threads, {sec:.1f} s",
+                        "sample": f"{calls} reference spmv calls (oracle/_ref, packed.cpp:211-220; 2 steps x "
+                                  f"{threads} threads x 3 sweep shapes), {sec:.1f} s, {_cpu_model()}",
+                        "encodings_identical_to_product": bool(encodings_identical),
                         "parity_max_rel_err_vs_gpu": max(errs)}
 
     line = {
@@ -764,6 +800,15 @@ def main():
     ap.add_argument("--no-decode", action="store_true", help="skip the 7B decode tokens/s measurement")
     ap.add_argument("--no-formats", action="store_true", help="skip the per-format arms (1:4, dense INT4, FP16)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command under torchrun
+        port = 29500 + os.getpid() % 1000
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+        os.execv(sys.executable, cmd)
+    rank, world, _ = _dist()
+    if world != args.gpus:
+        raise SystemExit(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}")
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

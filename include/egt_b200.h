@@ -124,8 +124,15 @@ typedef struct egt_dev_packed_info {
 
 /* Validates (check_packed + in-group offset order, packed.cpp:145-184) and
  * uploads.  stream may be NULL (legacy default stream); the call is
- * synchronous.  Device memory is allocated on the current device. */
+ * synchronous.  Device memory is allocated on the current device.
+ * Sparse-FP (EGT_KIND_F32) values are stored as fp16 on the device: values
+ * fp16 cannot hold exactly (precision or |v| > 65504) are rejected with
+ * EGT_EINVAL unless egt_dev_packed_create_ex is given EGT_UPLOAD_ROUND_FP16,
+ * which rounds them to nearest (the reference keeps f32, packed.hpp:33). */
 EGT_API egt_status egt_dev_packed_create(const egt_packed_view* view, void* stream, egt_dev_packed** out);
+#define EGT_UPLOAD_ROUND_FP16 1u
+EGT_API egt_status egt_dev_packed_create_ex(const egt_packed_view* view, uint32_t flags, void* stream,
+                                           egt_dev_packed** out);
 
 /* Dense INT4 layer (quant_dense_gemv semantics, packed.cpp:266-281). */
 EGT_API egt_status egt_dev_dense_i4_create(const egt_quant_view* view, void* stream, egt_dev_packed** out);
@@ -151,7 +158,7 @@ EGT_API egt_status egt_spmv(const egt_dev_packed* h, const float* x_dev, float* 
 /* egt_spmv_fused: apply silu (model.cpp:80-84) to the output instead of the
  * next product applying it to its input (each element once, not per CTA). */
 #define EGT_SPMV_OUTPUT_SILU 2u
-/* Input transforms of fused products (egt_spmv_fused, programs). */
+/* Input transforms of fused products (egt_spmv_fused). */
 #define EGT_INPUT_NONE 0u
 #define EGT_INPUT_RMSNORM 1u /* x / sqrt(mean(x^2) + eps) over the whole vector */
 #define EGT_INPUT_SILU 2u    /* x / (1 + exp(-x)) */
@@ -339,44 +346,39 @@ EGT_API egt_status egt_decoder_read(const egt_decoder* d, int32_t* tokens_host, 
                                     float* logits_dev, void* stream);
 EGT_API egt_status egt_decoder_destroy(egt_decoder* d);
 
-/* ---------------- persistent GEMV programs (decode chains) ----------------
- * A program is an ordered list of batch-1 products y = residual + W f(x)
- * executed by ONE persistent launch (one CTA per SM): every CTA streams its
- * share of each op's weights through one shared-memory ring, so op j+1's
- * weights are in flight while op j's output is still being produced.
- * Replaces a chain of spmv calls (packed.cpp:211-220) with the forward_impl
- * glue fused in: input transforms rmsnorm (model.cpp:57-67) and silu
- * (model.cpp:80-84), residual epilogue x += t (model.cpp:186,190).
- *
- * wait: -1 if x / residual are ready when the launch starts, else the index
- * w < j such that ops 0..w must be complete before op j reads its inputs.
- * create rejects (EGT_EINVAL) any read-after-write, write-after-read or
- * write-after-write overlap with an earlier op that `wait` does not cover.
- * Pointers are bound at create; run is stream-ordered and graph-capturable.
- * Only tiled-path matrices (group sizes multiple of 32) are accepted. */
-typedef struct egt_program_op {
-  const egt_dev_packed* w;
-  const float* x;        /* cols floats, 16-byte aligned */
-  float* y;              /* rows floats */
-  const float* residual; /* NULL, or rows floats added to the product (may equal y) */
-  uint32_t input;        /* EGT_INPUT_* */
-  float eps;             /* rmsnorm epsilon (model.cpp:27: 1e-6) */
-  int32_t wait;
-} egt_program_op;
-typedef struct egt_program egt_program; /* opaque; matrices must outlive it */
-typedef struct egt_program_info {
-  uint32_t n_ops, grid, stages, stage_bytes, smem_bytes;
-  double max_cta_bytes, avg_cta_bytes; /* planned weight bytes per CTA (busiest, mean) */
-} egt_program_info;
-EGT_API egt_status egt_program_create(const egt_program_op* ops, uint32_t n_ops, void* stream,
-                                      egt_program** out);
-EGT_API egt_status egt_program_run(const egt_program* p, void* stream);
-EGT_API egt_status egt_program_query(const egt_program* p, egt_program_info* info);
-EGT_API egt_status egt_program_destroy(egt_program* p);
-/* Tuning hook: with EGT_PROGRAM_TRACE set at create, CTA 0 records SM clock
- * stamps per ring chunk: [0,4096) producer issue, [4096,8192) consumer data
- * ready, [8192,12288) consumer done, [12288,16384) epilogue segment start. */
-EGT_API egt_status egt_program_debug_trace(const egt_program* p, long long* host, size_t n);
+/* ---------------- planning around the hot path (host) ----------------
+ * plan_sparsity (compress.cpp:298-326): patterns[l] = 2 (2:4) for the
+ * ceil(rho_s * L) layers of highest mean(score) / mean(|w|) (ties keep layer
+ * order), 1 (1:4) for the rest.  scores / weights: row-major f32. */
+EGT_API egt_status egt_host_plan_sparsity(uint32_t n_layers, const uint32_t* rows, const uint32_t* cols,
+                                          const float* const* scores, const float* const* weights, double rho_s,
+                                          uint8_t* patterns);
+/* CostModelEstimator (decode.cpp:84-120): EMA 0.9 of step times, 32-sample
+ * least squares of verify time over node count.  egt_measure_cost_model
+ * feeds it device-measured (CUDA event) times of this model's forward. */
+typedef struct egt_cost_estimator egt_cost_estimator;
+EGT_API egt_status egt_cost_estimator_create(double t_step, double alpha, double beta, egt_cost_estimator** out);
+EGT_API egt_status egt_cost_estimator_observe_step(egt_cost_estimator* e, double seconds);
+EGT_API egt_status egt_cost_estimator_observe_verify(egt_cost_estimator* e, uint64_t nodes, double seconds);
+EGT_API egt_status egt_cost_estimator_model(const egt_cost_estimator* e, double out[3]); /* t_step, alpha, beta */
+EGT_API egt_status egt_cost_estimator_destroy(egt_cost_estimator* e);
+/* Times (CUDA events, reps each, after one warm-up) this model's constrained
+ * step forward (n_beams beams of prompt_len + 1 committed rows) and its
+ * verify forward over every node count in node_counts (a random tree under
+ * n_beams committed blocks), feeding observe_step / observe_verify. */
+EGT_API egt_status egt_measure_cost_model(const egt_model* m, uint32_t prompt_len, uint32_t n_beams,
+                                          const uint32_t* node_counts, uint32_t n_counts, int reps,
+                                          egt_cost_estimator* e, void* stream);
+/* estimate_trigger (decode.cpp:192-207) and flatten_subtree + build_tree_mask
+ * (decode.cpp:209-299) on host views (no device work). */
+EGT_API egt_status egt_host_estimate_trigger(const egt_trie_view* trie, const egt_session_view* session,
+                                             double t_step, double alpha, double beta, uint64_t node_cap,
+                                             int* trigger, double* saving);
+EGT_API egt_status egt_host_tree_mask(const egt_trie_view* trie, const egt_session_view* session, uint32_t cap_nodes,
+                                      uint32_t* n_nodes, uint32_t* fn_token, int32_t* fn_parent, uint32_t* fn_depth,
+                                      uint32_t* fn_trie, uint32_t* fn_beam, uint32_t cap_rows, uint32_t* n_rows,
+                                      int32_t* tokens, int32_t* positions, uint8_t* vis_bits, size_t cap_bits,
+                                      uint32_t* padded_len, uint32_t* flat_offset);
 
 /* y = W x for a dense row-major f32 W (device pointers): the mixed
  * dispatch's (dense, !quant) baseline arm, which the reference densifies
@@ -489,6 +491,10 @@ EGT_API egt_status egt_egtq_parse(const uint8_t* bytes, size_t n, const char* co
 EGT_API uint32_t egt_egtq_layer_count(const egt_egtq* e);
 EGT_API egt_status egt_egtq_query(const egt_egtq* e, uint32_t i, egt_egtq_layer_info* info);
 EGT_API egt_status egt_egtq_upload(const egt_egtq* e, uint32_t i, void* stream, egt_dev_packed** out);
+/* flags: EGT_UPLOAD_ROUND_FP16 (sparse-FP layers whose f32 values fp16
+ * cannot hold exactly are rounded instead of rejected) */
+EGT_API egt_status egt_egtq_upload_ex(const egt_egtq* e, uint32_t i, uint32_t flags, void* stream,
+                                      egt_dev_packed** out);
 EGT_API egt_status egt_egtq_destroy(egt_egtq* e);
 
 /* ---------------- host encoder (C++; byte-identical to the reference) ----

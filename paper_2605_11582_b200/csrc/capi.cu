@@ -139,6 +139,9 @@ egt_status finish_error_flag(uint32_t* d_err, cudaStream_t s) {
   if (h_err & 1u) return fail(EGT_EFORMAT, "packed matrix: in-group offsets not increasing");
   if (h_err & 2u) return fail(EGT_EFORMAT, "packed matrix: zero group size");
   if (h_err & 4u) return fail(EGT_EFORMAT, "packed matrix: group table does not cover the row");
+  if (h_err & 8u)
+    return fail(EGT_EINVAL,
+                "packed matrix: values not representable in fp16 (pass EGT_UPLOAD_ROUND_FP16 to round them)");
   return EGT_OK;
 }
 
@@ -289,7 +292,12 @@ int egt_tune_read_trace(unsigned long long* host, size_t n, int reset) {
 }
 
 egt_status egt_dev_packed_create(const egt_packed_view* v, void* stream, egt_dev_packed** out) {
+  return egt_dev_packed_create_ex(v, 0u, stream, out);
+}
+
+egt_status egt_dev_packed_create_ex(const egt_packed_view* v, uint32_t flags, void* stream, egt_dev_packed** out) {
   using namespace egt_fmt;
+  if ((flags & ~EGT_UPLOAD_ROUND_FP16) != 0u) return fail(EGT_EINVAL, "egt_dev_packed_create: unknown flags");
   if (!out) return fail(EGT_EINVAL, "egt_dev_packed_create: null output");
   *out = nullptr;
   egt_status st = check_view(v);
@@ -340,7 +348,7 @@ egt_status egt_dev_packed_create(const egt_packed_view* v, void* stream, egt_dev
     up.f32 = reinterpret_cast<float*>(b + o_f32);
     up.f16 = reinterpret_cast<__half*>(b + o_f16);
     if (nnz) CUDA_TRY(cudaMemcpyAsync(up.f32, v->values, nnz * 4, cudaMemcpyHostToDevice, s));
-    CUDA_TRY(launch_f32_to_f16(up.f32, up.f16, nnz, s));
+    CUDA_TRY(launch_f32_to_f16(up.f32, up.f16, nnz, (flags & EGT_UPLOAD_ROUND_FP16) == 0u, up.err, s));
   }
   CUDA_TRY(launch_validate_offsets(up.words, rows, cols, v->n, up.err, s));
   st = finish_error_flag(up.err, s);

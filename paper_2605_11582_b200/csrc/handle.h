@@ -153,7 +153,7 @@ cudaError_t launch_validate_offsets(const uint16_t* words, uint32_t rows, uint32
 cudaError_t launch_validate_groups(const uint32_t* gsizes, const uint32_t* goffs, uint32_t rows,
                                    uint32_t cols, uint64_t n_scales, uint32_t* err_flag,
                                    cudaStream_t s);
-cudaError_t launch_f32_to_f16(const float* src, __half* dst, uint64_t n, cudaStream_t s);
+cudaError_t launch_f32_to_f16(const float* src, __half* dst, uint64_t n, bool check, uint32_t* err, cudaStream_t s);
 cudaError_t launch_relayout(const RawStream& raw, int format, uint32_t rows, uint32_t cols,
                             const TiledStream& dst_shape, uint8_t* vals, uint8_t* meta,
                             float* scales, uint8_t* zps, cudaStream_t s);  // dst_shape.pad14: raw is 1:4

@@ -19,8 +19,6 @@
 #include "egt_b200/packed.hpp"
 
 namespace egt_b200 {
-// EGT_DENSE_TREE_MASK: upload the dense M x M bitmap instead (A/B, tests)
-const bool g_dense_tree_mask = std::getenv("EGT_DENSE_TREE_MASK") != nullptr;
 
 namespace {
 
@@ -468,7 +466,7 @@ DecodeResult decode(const egt_model* model, const PrefixTrie& trie, std::vector<
       fire = s.steps >= opt.forced_depth;
     if (fire) {
       const FlattenedSubtree flat = flatten_subtree(s, trie);
-      const TreeMask mask = build_tree_mask(flat, s, g_dense_tree_mask);
+      const TreeMask mask = build_tree_mask(flat, s, false);  // compact encoding: the device builds the mask
       const VerificationResult vr = verify_parallel(model, s, trie, flat, mask, opt.beam_size, stream);
       s.trigger_step = s.steps;
       for (const VerifiedLeaf& l : vr.selected) out.sequences.push_back({l.tokens, l.score, l.payload});
@@ -553,7 +551,7 @@ extern "C" EGT_API egt_status egt_verify_parallel(const egt_model* m, const egt_
     const egt_b200::PrefixTrie t = egt_b200::PrefixTrie::from_parents(*trie);
     egt_b200::DecodeSession s = session_of(*session);
     const egt_b200::FlattenedSubtree flat = egt_b200::flatten_subtree(s, t);
-    const egt_b200::TreeMask mask = egt_b200::build_tree_mask(flat, s, egt_b200::g_dense_tree_mask);
+    const egt_b200::TreeMask mask = egt_b200::build_tree_mask(flat, s, false);
     const egt_b200::VerificationResult r = egt_b200::verify_parallel(m, s, t, flat, mask, beam_size, stream);
     fill_out(out, r.selected, beam_size);
     for (uint32_t j = 0; j < out->n_selected; ++j) out->beam[j] = r.selected[j].beam;
@@ -587,5 +585,89 @@ extern "C" EGT_API egt_status egt_decode(const egt_model* m, const egt_trie_view
       stats[2] = r.trigger_step;
       stats[3] = static_cast<int32_t>(r.flattened_nodes);
     }
+  });
+}
+
+// Device-measured cost model: the constrained step's and the
+// verify pass's forwards of THIS model, timed with CUDA events on the stream,
+// feed CostModelEstimator (decode.cpp:84-120) -- on the B200 the verify cost
+// is nearly flat in the node count up to the tensor ridge, so the trigger
+// (decode.cpp:192-207) fires earlier than a CPU-calibrated model would.
+extern "C" EGT_API egt_status egt_measure_cost_model(const egt_model* m, uint32_t prompt_len, uint32_t n_beams,
+                                                     const uint32_t* node_counts, uint32_t n_counts, int reps,
+                                                     egt_cost_estimator* e, void* stream) {
+  return guarded([&] {
+    if (!m || !e || (n_counts && !node_counts)) throw std::invalid_argument("cost model: null argument");
+    if (prompt_len == 0 || n_beams == 0 || reps < 1) throw std::invalid_argument("cost model: empty measurement");
+    egt_model_config c;
+    egt_b200::check(egt_model_query(m, &c));
+    const uint32_t L = prompt_len + 1;
+    if (L > c.max_positions) throw std::invalid_argument("cost model: prompt longer than max_positions");
+    uint32_t max_nodes = 0;
+    for (uint32_t i = 0; i < n_counts; ++i) max_nodes = std::max(max_nodes, node_counts[i]);
+    const uint32_t max_rows = std::max(n_beams * L + max_nodes, n_beams * L);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    float* logits = nullptr;
+    if (cudaMallocAsync(reinterpret_cast<void**>(&logits), static_cast<size_t>(max_rows) * c.vocab_size * 4, s) !=
+        cudaSuccess)
+      throw egt_b200::CudaError("cost model: logits allocation failed");
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    auto timed = [&](auto&& launch) {
+      launch();  // warm-up (plans, workspaces)
+      cudaEventRecord(e0, s);
+      for (int r = 0; r < reps; ++r) launch();
+      cudaEventRecord(e1, s);
+      cudaEventSynchronize(e1);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      return static_cast<double>(ms) * 1e-3 / reps;
+    };
+    // constrained step: n_beams committed blocks, block-diagonal causal
+    const uint32_t M = n_beams * L;
+    std::vector<int32_t> tok(max_rows), pos(max_rows);
+    for (uint32_t i = 0; i < max_rows; ++i) tok[i] = static_cast<int32_t>(4 + i % std::max(1u, c.vocab_size - 4));
+    for (uint32_t b = 0; b < n_beams; ++b)
+      for (uint32_t j = 0; j < L; ++j) pos[b * L + j] = static_cast<int32_t>(j);
+    std::vector<uint8_t> bits((static_cast<size_t>(M) * M + 7) / 8, 0);
+    for (uint32_t b = 0; b < n_beams; ++b)
+      for (uint32_t q = 0; q < L; ++q)
+        for (uint32_t k = 0; k <= q; ++k) {
+          const size_t i = static_cast<size_t>(b * L + q) * M + b * L + k;
+          bits[i >> 3] |= static_cast<uint8_t>(1u << (i & 7));
+        }
+    const double t_step =
+        timed([&] { egt_b200::check(egt_forward(m, tok.data(), pos.data(), bits.data(), M, logits, stream)); });
+    egt_b200::check(egt_cost_estimator_observe_step(e, t_step));
+    // verify: a random tree of n nodes over the same committed blocks
+    uint64_t rng = 0x9e3779b97f4a7c15ull;
+    for (uint32_t ci = 0; ci < n_counts; ++ci) {
+      const uint32_t n = node_counts[ci];
+      if (n == 0) continue;
+      std::vector<uint32_t> committed(n_beams, L), beam(n);
+      std::vector<int32_t> parent(n), depth(n);
+      for (uint32_t f = 0; f < n; ++f) {
+        rng = rng * 6364136223846793005ull + 1442695040888963407ull;
+        beam[f] = f < n_beams ? f : static_cast<uint32_t>((rng >> 33) % n_beams);
+        // parent: the latest earlier node of the same beam, or a root
+        int32_t p = -1;
+        for (int32_t g = static_cast<int32_t>(f) - 1; g >= 0 && ((rng >> 20) & 3u); --g)
+          if (beam[g] == beam[f]) {
+            p = g;
+            break;
+          }
+        parent[f] = p;
+        depth[f] = p < 0 ? 0 : depth[p] + 1;
+        pos[M + f] = static_cast<int32_t>(std::min<uint32_t>(L + depth[f], c.max_positions - 1));
+      }
+      const egt_tree_view tv{n_beams, L, committed.data(), n, parent.data(), beam.data()};
+      const double t = timed([&] { egt_b200::check(egt_forward_tree(m, tok.data(), pos.data(), &tv, logits, stream)); });
+      egt_b200::check(egt_cost_estimator_observe_verify(e, n, t));
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFreeAsync(logits, s);
+    cudaStreamSynchronize(s);
   });
 }

@@ -135,6 +135,12 @@ std::vector<BenchRow> bench_spmv(const std::vector<BenchShape>& shapes, int reps
 std::string bench_csv(const std::vector<BenchRow>& rows);
 
 // Throws the exception class the reference would for an egt_status.
+// Layer-adaptive sparsity (compress.hpp:115-119, plan_sparsity
+// compress.cpp:298-326): the mixed-dispatch keys of a compressed stack.
+enum class SparsityPattern : uint8_t { kDense = 0, kOneOfFour = 1, kTwoOfFour = 2 };
+std::vector<SparsityPattern> plan_sparsity(const std::vector<const Matrix*>& scores,
+                                           const std::vector<const Matrix*>& weights, double rho_s);
+
 [[noreturn]] void throw_status(egt_status st);
 inline void check(egt_status st) {
   if (st != EGT_OK) throw_status(st);

@@ -281,6 +281,11 @@ EGT_API egt_status egt_egtq_query(const egt_egtq* e, uint32_t i, egt_egtq_layer_
 }
 
 EGT_API egt_status egt_egtq_upload(const egt_egtq* e, uint32_t i, void* stream, egt_dev_packed** out) {
+  return egt_egtq_upload_ex(e, i, 0u, stream, out);
+}
+
+EGT_API egt_status egt_egtq_upload_ex(const egt_egtq* e, uint32_t i, uint32_t flags, void* stream,
+                                      egt_dev_packed** out) {
   return egtq_guard([&]() -> egt_status {
     if (!e || !out || i >= e->layers.size()) throw std::invalid_argument("egtq: layer index out of range");
     *out = nullptr;
@@ -330,7 +335,7 @@ EGT_API egt_status egt_egtq_upload(const egt_egtq* e, uint32_t i, void* stream, 
       p = egt_b200::pack(L.mask, dense, n, 4);
     }
     const egt_packed_view v = egt_b200::view_of(p);
-    return egt_dev_packed_create(&v, stream, out);
+    return egt_dev_packed_create_ex(&v, flags, stream, out);
   });
 }
 

@@ -26,6 +26,7 @@
 #include <cmath>
 #include "handle.h"
 #include "tiled_compute.cuh"
+#include "xrange.cuh"
 
 namespace egt_impl {
 
@@ -44,27 +45,50 @@ struct WideArgs {
   const float* res;  // y = res + product (may alias y; row stride ldr), model.cpp:186/190
   int ldr;
   int out_silu;      // y = silu(...), model.cpp:80-84 (the next product's input)
+  // x range (xrange.cuh): per token 2^-e rescale and non-finite flag
+  // (written by xfrag_kernel), and x itself for the non-finite fix-up
+  const float* unsc;
+  const uint32_t* nonfin;
+  const float* x;
+  int ldx, cols, SS, pad14;
 };
 
-// X [M x cols] (row stride ldx) -> fragments; one thread per (token block,
-// n-tile, k-tile, lane): 4 u32 = the lane's B fragment (k = kt*32 + 2t + 8r,
-// pair (k, k+1); column g = 2m + part, part 0 = fp16 hi, 1 = residual lo).
-__global__ void xfrag_kernel(const float* __restrict__ x, int ldx, int M, int cols, int KTtot, int TB,
-                             uint32_t* __restrict__ xf) {
+// X [M x cols] (row stride ldx) -> fragments, one CTA per (padded) token:
+// the token's row range first (xrange.cuh: finite max |x| -> 2^e, non-finite
+// flag), then one thread per (k-tile, part, t): 4 u32 = lane (g, t)'s B
+// fragment (k = kt*32 + 2t + 8r, pair (k, k+1); g = 2 (tok % 4) + part,
+// part 0 = fp16 hi, 1 = residual lo), at [token block][n-tile][k-tile][lane].
+__global__ void __launch_bounds__(256) xfrag_kernel(const float* __restrict__ x, int ldx, int M, int cols,
+                                                    int KTtot, uint32_t* __restrict__ xf, float* __restrict__ unsc,
+                                                    uint32_t* __restrict__ nonfin) {
   // launched programmatically: x (and the fragment workspace the previous
   // product reads) belong to the preceding kernel
   pdl_wait();
   pdl_launch_dependents();
-  const long long total = static_cast<long long>(TB) * 4 * KTtot * 32;
-  for (long long idx = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x; idx < total;
-       idx += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const int lane = static_cast<int>(idx & 31);
-    const long long r = idx >> 5;
-    const int kt = static_cast<int>(r % KTtot);
-    const int nt = static_cast<int>((r / KTtot) & 3);
-    const int tb = static_cast<int>(r / (4LL * KTtot));
-    const int g = lane >> 2, t = lane & 3;
-    const int tok = tb * kWideTok + nt * 4 + (g >> 1), part = g & 1;
+  __shared__ uint32_t s_mx, s_nf;
+  const int tok = blockIdx.x, tid = threadIdx.x;
+  if (tid == 0) {
+    s_mx = 0u;
+    s_nf = 0u;
+  }
+  __syncthreads();
+  const float* xr = x + static_cast<size_t>(tok) * ldx;
+  if (tok < M) {
+    uint32_t mx = 0u, nf = 0u;
+    for (int k = tid; k < cols; k += blockDim.x) xr_note(mx, nf, __ldg(xr + k));
+    xr_commit(mx, nf, &s_mx, &s_nf);
+  }
+  __syncthreads();
+  const int e = xr_exp(s_mx);
+  const float sc = xr_pow2(e);
+  if (tid == 0) {
+    unsc[tok] = xr_pow2(-e);
+    nonfin[tok] = s_nf;
+  }
+  const int tb = tok / kWideTok, nt = (tok % kWideTok) / 4, m4 = tok % 4;
+  for (int idx = tid; idx < KTtot * 8; idx += blockDim.x) {
+    const int kt = idx >> 3, part = (idx >> 2) & 1, t = idx & 3;
+    const int lane = 4 * (2 * m4 + part) + t;
     uint4 o;
     uint32_t* op = reinterpret_cast<uint32_t*>(&o);
 #pragma unroll
@@ -72,9 +96,8 @@ __global__ void xfrag_kernel(const float* __restrict__ x, int ldx, int M, int co
       const int k = kt * 32 + 2 * t + 8 * reg;
       float a = 0.f, b = 0.f;
       if (tok < M) {
-        const float* xr = x + static_cast<size_t>(tok) * ldx;
-        if (k < cols) a = xr[k];
-        if (k + 1 < cols) b = xr[k + 1];
+        if (k < cols) a = xr_scaled(__ldg(xr + k), sc);
+        if (k + 1 < cols) b = xr_scaled(__ldg(xr + k + 1), sc);
       }
       __half ha = __float2half_rn(a), hb = __float2half_rn(b);
       if (part) {
@@ -83,8 +106,23 @@ __global__ void xfrag_kernel(const float* __restrict__ x, int ldx, int M, int co
       }
       op[reg] = static_cast<uint32_t>(__half_as_ushort(ha)) | (static_cast<uint32_t>(__half_as_ushort(hb)) << 16);
     }
-    reinterpret_cast<uint4*>(xf)[idx] = o;
+    reinterpret_cast<uint4*>(xf)[((static_cast<size_t>(tb) * 4 + nt) * KTtot + kt) * 32 + lane] = o;
   }
+}
+
+// sum of W[row][c] * x[c] over the kept entries of row with non-finite x[c]
+template <int FMT>
+__device__ __noinline__ float wide_nonfinite_terms(const WideArgs& a, int row, int tok) {
+  const TiledRef m{a.vals, a.meta, a.scales, a.zps, a.KQ, a.rt_begin, a.SS, a.pad14};
+  const float* xr = a.x + static_cast<size_t>(tok) * a.ldx;
+  float add = 0.f;
+  for (int c = 0; c < a.cols; ++c) {
+    const float xv = xr[c];
+    if ((__float_as_uint(xv) & 0x7fffffffu) < 0x7f800000u) continue;
+    float w;
+    if (tiled_value<FMT>(m, row, c, &w)) add += w * xv;
+  }
+  return add;
 }
 
 template <int FMT, int SS, int NW>
@@ -222,7 +260,9 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1) wide_spmm_kernel(const WideA
           for (int hh = 0; hh < 2; ++hh) {
             const int rw = row + 8 * hh;
             if (rw < a.rows) {
-              float val = (rr ? rr[rw] : 0.f) + acc[r][nt][hh];
+              float p = acc[r][nt][hh] * a.unsc[tok];  // undo the token's 2^e (xrange.cuh)
+              if (a.nonfin[tok]) p += wide_nonfinite_terms<FMT>(a, rw, tok);
+              float val = (rr ? rr[rw] : 0.f) + p;
               if (a.out_silu) val = val * (1.0f / (1.0f + expf(-val)));
               yr[rw] = val;
             }
@@ -258,7 +298,8 @@ void* pick_wide(int fmt, int SS, int nw) {
 
 size_t wide_workspace_bytes(const egt_dev_packed* h, int M) {
   const int TB = (M + kWideTok - 1) / kWideTok;
-  return static_cast<size_t>(TB) * 4 * h->tiled.KQ * 4 * 512;
+  // fragments, then per padded token the rescale and the non-finite flag
+  return static_cast<size_t>(TB) * 4 * h->tiled.KQ * 4 * 512 + static_cast<size_t>(TB) * kWideTok * 8;
 }
 
 cudaError_t launch_wide(const egt_dev_packed* h, const float* x, int ldx, int M, float* y, int ldy,
@@ -266,11 +307,11 @@ cudaError_t launch_wide(const egt_dev_packed* h, const float* x, int ldx, int M,
   const int KQ = h->tiled.KQ, RT = h->tiled.RT, E = h->tiled.E, fmt = h->format;
   const int KTtot = KQ * 4;
   const int TB = (M + kWideTok - 1) / kWideTok;
+  float* unsc = reinterpret_cast<float*>(xf_ws + static_cast<size_t>(TB) * 4 * KTtot * 128);
+  uint32_t* nonfin = reinterpret_cast<uint32_t*>(unsc + TB * kWideTok);
   {
-    const long long total = static_cast<long long>(TB) * 4 * KTtot * 32;
-    const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 8LL * num_sms));
     cudaLaunchConfig_t xc = {};
-    xc.gridDim = dim3(blocks);
+    xc.gridDim = dim3(TB * kWideTok);
     xc.blockDim = dim3(256);
     xc.stream = ctx.stream;
     cudaLaunchAttribute xa[1];
@@ -280,7 +321,7 @@ cudaError_t launch_wide(const egt_dev_packed* h, const float* x, int ldx, int M,
     xc.numAttrs = ctx.pdl ? 1 : 0;
     const int cols_ = static_cast<int>(h->cols);
     void* xargs[] = {const_cast<float**>(&x), &ldx, &M, const_cast<int*>(&cols_), const_cast<int*>(&KTtot),
-                     const_cast<int*>(&TB), &xf_ws};
+                     &xf_ws, &unsc, &nonfin};
     cudaError_t xe = cudaLaunchKernelExC(&xc, reinterpret_cast<void*>(&xfrag_kernel), xargs);
     if (xe != cudaSuccess) return xe;
     ++launch_counter();
@@ -302,6 +343,13 @@ cudaError_t launch_wide(const egt_dev_packed* h, const float* x, int ldx, int M,
   a.res = ctx.res;
   a.ldr = ctx.ldr;
   a.out_silu = ctx.out_silu;
+  a.unsc = unsc;
+  a.nonfin = nonfin;
+  a.x = x;
+  a.ldx = ldx;
+  a.cols = static_cast<int>(h->cols);
+  a.SS = h->tiled.SS;
+  a.pad14 = h->tiled.pad14;
   // RB: up to nw * kWideMaxRT row tiles; fewer when the token blocks alone
   // leave SMs idle (one wave of CTAs at one per SM)
   // RB: the critical path of the busiest SM is waves x (consumer warps per

@@ -536,15 +536,25 @@ cudaError_t launch_dequant(const egt_dev_packed* h, float* w, uint8_t* mask, cud
 }  // namespace egt_impl
 
 namespace egt_impl {
-__global__ void f32_to_f16_kernel(const float* src, __half* dst, uint64_t n) {
+// Sparse-FP upload: the reference keeps f32 values (packed.hpp:33
+// kFloat32); the device stores fp16.  Values that fp16 cannot hold exactly
+// (precision or range) set err bit 8 unless rounding was requested.
+__global__ void f32_to_f16_kernel(const float* src, __half* dst, uint64_t n, int check, uint32_t* err) {
+  bool bad = false;
   for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < n;
-       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
-    dst[i] = __float2half_rn(src[i]);
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+    const float v = src[i];
+    const __half h = __float2half_rn(v);
+    dst[i] = h;
+    if (check && __half2float(h) != v && v == v) bad = true;  // NaN stays NaN
+  }
+  if (check && __any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(err, 8u);
 }
 
-cudaError_t launch_f32_to_f16(const float* src, __half* dst, uint64_t n, cudaStream_t s) {
+cudaError_t launch_f32_to_f16(const float* src, __half* dst, uint64_t n, bool check, uint32_t* err,
+                              cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  f32_to_f16_kernel<<<1184, 256, 0, s>>>(src, dst, n);
+  f32_to_f16_kernel<<<1184, 256, 0, s>>>(src, dst, n, check ? 1 : 0, err);
   ++launch_counter();
   return cudaGetLastError();
 }

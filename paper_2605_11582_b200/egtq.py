@@ -43,10 +43,13 @@ class EgtqFile:
         with open(path, "rb") as f:
             return cls(f.read(), path)
 
-    def upload(self, i: int, stream=None) -> DeviceMatrix:
-        """Layer i as a device matrix (mixed dispatch on pattern x storage)."""
+    def upload(self, i: int, stream=None, round_fp16: bool = False) -> DeviceMatrix:
+        """Layer i as a device matrix (mixed dispatch on pattern x storage).
+        Sparse-FP layers whose f32 values fp16 cannot hold exactly raise
+        InvalidArgument unless round_fp16."""
         h = C.c_void_p()
-        check(lib().egt_egtq_upload(self._h, i, _stream_ptr(stream), C.byref(h)))
+        check(lib().egt_egtq_upload_ex(self._h, i, N.UPLOAD_ROUND_FP16 if round_fp16 else 0, _stream_ptr(stream),
+                                       C.byref(h)))
         return DeviceMatrix(h.value)
 
     def __del__(self):

@@ -89,19 +89,8 @@ class DecodeOptions(C.Structure):
                 ("alpha", C.c_double), ("beta", C.c_double), ("node_cap", C.c_uint64)]
 
 
-class ProgramOp(C.Structure):
-    """egt_program_op (one product of a persistent GEMV program)."""
-
-    _fields_ = [("w", C.c_void_p), ("x", C.c_void_p), ("y", C.c_void_p), ("residual", C.c_void_p),
-                ("input", C.c_uint32), ("eps", C.c_float), ("wait", C.c_int32)]
-
-
-class ProgramInfo(C.Structure):
-    _fields_ = [(k, C.c_uint32) for k in ("n_ops", "grid", "stages", "stage_bytes", "smem_bytes")] + [
-        ("max_cta_bytes", C.c_double), ("avg_cta_bytes", C.c_double)]
-
-
 INPUT_NONE, INPUT_RMSNORM, INPUT_SILU = 0, 1, 2
+UPLOAD_ROUND_FP16 = 1  # egt_dev_packed_create_ex flag
 
 
 class EgtqLayerInfo(C.Structure):
@@ -113,6 +102,7 @@ SIGNATURES = {
     "egt_abi_version": (C.c_int, []),
     "egt_last_error": (C.c_char_p, []),
     "egt_dev_packed_create": (C.c_int, [C.POINTER(PackedView), C.c_void_p, C.POINTER(C.c_void_p)]),
+    "egt_dev_packed_create_ex": (C.c_int, [C.POINTER(PackedView), C.c_uint32, C.c_void_p, C.POINTER(C.c_void_p)]),
     "egt_dev_dense_i4_create": (C.c_int, [C.POINTER(QuantView), C.c_void_p, C.POINTER(C.c_void_p)]),
     "egt_dev_packed_slice_rows": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.POINTER(C.c_void_p)]),
     "egt_dev_packed_destroy": (C.c_int, [C.c_void_p]),
@@ -163,12 +153,20 @@ class TreeView(C.Structure):
 _MODEL_SIGNATURES["egt_forward_tree"] = (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32),
                                                    C.POINTER(TreeView), C.c_void_p, C.c_void_p])
 
-_PROGRAM_SIGNATURES = {
-    "egt_program_create": (C.c_int, [C.POINTER(ProgramOp), C.c_uint32, C.c_void_p, C.POINTER(C.c_void_p)]),
-    "egt_program_run": (C.c_int, [C.c_void_p, C.c_void_p]),
-    "egt_program_query": (C.c_int, [C.c_void_p, C.POINTER(ProgramInfo)]),
-    "egt_program_destroy": (C.c_int, [C.c_void_p]),
-    "egt_program_debug_trace": (C.c_int, [C.c_void_p, C.POINTER(C.c_longlong), C.c_size_t]),
+_PLANNING_SIGNATURES = {
+    "egt_host_plan_sparsity": (C.c_int, [C.c_uint32, u32p, u32p, C.POINTER(f32p), C.POINTER(f32p), C.c_double, u8p]),
+    "egt_cost_estimator_create": (C.c_int, [C.c_double, C.c_double, C.c_double, C.POINTER(C.c_void_p)]),
+    "egt_cost_estimator_observe_step": (C.c_int, [C.c_void_p, C.c_double]),
+    "egt_cost_estimator_observe_verify": (C.c_int, [C.c_void_p, C.c_uint64, C.c_double]),
+    "egt_cost_estimator_model": (C.c_int, [C.c_void_p, f64p]),
+    "egt_cost_estimator_destroy": (C.c_int, [C.c_void_p]),
+    "egt_measure_cost_model": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, u32p, C.c_uint32, C.c_int, C.c_void_p,
+                                         C.c_void_p]),
+    "egt_host_estimate_trigger": (C.c_int, [C.POINTER(TrieView), C.POINTER(SessionView), C.c_double, C.c_double,
+                                            C.c_double, C.c_uint64, C.POINTER(C.c_int), f64p]),
+    "egt_host_tree_mask": (C.c_int, [C.POINTER(TrieView), C.POINTER(SessionView), C.c_uint32, u32p, u32p,
+                                     C.POINTER(C.c_int32), u32p, u32p, u32p, C.c_uint32, u32p, C.POINTER(C.c_int32),
+                                     C.POINTER(C.c_int32), u8p, C.c_size_t, u32p, u32p]),
 }
 
 _MODEL_SIGNATURES.update({
@@ -184,6 +182,7 @@ _MODEL_SIGNATURES.update({
     "egt_egtq_layer_count": (C.c_uint32, [C.c_void_p]),
     "egt_egtq_query": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(EgtqLayerInfo)]),
     "egt_egtq_upload": (C.c_int, [C.c_void_p, C.c_uint32, C.c_void_p, C.POINTER(C.c_void_p)]),
+    "egt_egtq_upload_ex": (C.c_int, [C.c_void_p, C.c_uint32, C.c_uint32, C.c_void_p, C.POINTER(C.c_void_p)]),
     "egt_egtq_destroy": (C.c_int, [C.c_void_p]),
 })
 
@@ -230,7 +229,7 @@ SIGNATURES["egt_gemv_f32"] = (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_
 SIGNATURES["egt_bench_spmv"] = (C.c_int, [u32p, u32p, C.c_uint32, C.c_int, C.c_uint64, C.c_char_p, C.c_size_t,
                                           C.POINTER(C.c_size_t)])
 SIGNATURES.update(_PEER_SIGNATURES)
-SIGNATURES.update(_PROGRAM_SIGNATURES)
+SIGNATURES.update(_PLANNING_SIGNATURES)
 
 _lib = None
 

@@ -182,10 +182,13 @@ class DeviceMatrix:
         self.nnz = info.nnz
 
     @classmethod
-    def from_packed(cls, p: PackedSparseMatrix, stream=None) -> "DeviceMatrix":
+    def from_packed(cls, p: PackedSparseMatrix, stream=None, round_fp16: bool = False) -> "DeviceMatrix":
+        """Upload (egt_dev_packed_create_ex).  Sparse-FP values fp16 cannot
+        hold exactly raise InvalidArgument unless round_fp16."""
         v = p.view()
         h = C.c_void_p()
-        check(lib().egt_dev_packed_create(C.byref(v), _stream_ptr(stream), C.byref(h)))
+        check(lib().egt_dev_packed_create_ex(C.byref(v), N.UPLOAD_ROUND_FP16 if round_fp16 else 0,
+                                             _stream_ptr(stream), C.byref(h)))
         return cls(h.value)
 
     @classmethod

@@ -85,8 +85,11 @@ def test_upload_dispatch_parity(ref, port, data):
             with pytest.raises(InvalidArgument, match="not on the SparseGemv path"):
                 f.upload(i)
             continue
-        d = f.upload(i)
         w, mask = spec["w"], spec["mask"]
+        if not info.has_quant and not np.array_equal(w.astype(np.float16).astype(np.float32), w):
+            with pytest.raises(InvalidArgument, match="not representable in fp16"):
+                f.upload(i)
+        d = f.upload(i, round_fp16=not info.has_quant)
         rows, cols = w.shape
         if info.has_quant:
             gs = np.full(rows, spec["group"], np.uint32)
@@ -95,8 +98,9 @@ def test_upload_dispatch_parity(ref, port, data):
                 want_w = port.dequantize(q)
             else:
                 want_w, _ = port.unpack(port.pack_int4(mask, rows, cols, q, 2 if info.pattern == "2:4" else 1))
-        else:  # sparse fp: f32 in the file, FP16 on the device (egt_dev_packed_create's F32 view)
+        else:  # sparse fp: f32 in the file, FP16 on the device when rounding is requested
             want_w, _ = port.unpack(port.pack_f32(mask, rows, cols, w, 2 if info.pattern == "2:4" else 1))
+            raw_w = want_w.copy()
             want_w = want_w.astype(np.float16).astype(np.float32)
         got_w, _ = d.dequant()
         assert np.array_equal(got_w.cpu().numpy().view(np.uint32), want_w.astype(np.float32).view(np.uint32)), info.name
@@ -104,3 +108,9 @@ def test_upload_dispatch_parity(ref, port, data):
         y = d.spmv(torch.from_numpy(x).cuda()).cpu().numpy()
         ok, err = close(y, want_w.astype(np.float64) @ x.astype(np.float64))
         assert ok, (info.name, err)
+        if not info.has_quant:
+            # against the reference's f32 spmv on the RAW f32 weights: the
+            # rounding error of the opted-in fp16 storage, measured
+            raw = port.pack_f32(mask, rows, cols, w, 2 if info.pattern == "2:4" else 1)
+            ok, err = close(y, port.spmv(raw, x), tol=2e-3)
+            assert ok, (info.name, "fp16 rounding vs raw f32", err)

@@ -246,3 +246,29 @@ def test_forward_tree_equals_dense_mask(model_pair):
         model.forward_tree(tokens, pos, lens, lmax, [1] + [f["parent"] for f in flat][1:], [f["beam"] for f in flat])
     with pytest.raises(egt.InvalidArgument, match="missing beam"):
         model.forward_tree(tokens, pos, lens, lmax, [f["parent"] for f in flat], [5] * len(flat))
+
+
+def test_cost_model_from_device_timings(model_pair):
+    """CostModelEstimator (decode.cpp:84-120) fed CUDA-event timings of this
+    model's constrained-step and verify forwards (egt_measure_cost_model,
+    SURVEY 8(a) a20); decode with the measured model fires where
+    estimate_trigger says and returns the exhaustive autoregressive result
+    (switch-point invariance, test_decode.cpp:605-646)."""
+    from paper_2605_11582_b200 import planning as P
+
+    model, _ = model_pair
+    est = P.CostModelEstimator()
+    t_step, alpha, beta = est.measure(model, prompt_len=3, n_beams=2, node_counts=[4, 8, 16, 32], reps=3)
+    assert t_step > 0 and np.isfinite(alpha) and np.isfinite(beta)
+    assert alpha * 32 + beta > 0  # a verify pass costs time
+    rng = np.random.default_rng(15)
+    trie = random_trie(rng, depth=3, lo=2, hi=3)
+    n_leaves = sum(1 for i in range(len(trie.token)) if vo.is_leaf(trie, i))
+    prompt = [1, 22, 7]
+    fire, _ = P.estimate_trigger(trie, prompt, [type("B", (), dict(tokens=[], log_prob=0.0, node=0))()],
+                                 (t_step, alpha, beta))
+    ar, _ = model.decode(trie, prompt, n_leaves, mode="autoregressive")
+    got, st = model.decode(trie, prompt, n_leaves, mode="ptpv", cost=(t_step, alpha, beta))
+    assert (st["trigger_step"] == 0) == fire
+    assert sorted(tuple(s["tokens"]) for s in got) == sorted(tuple(s["tokens"]) for s in ar)
+    assert np.allclose(sorted(s["score"] for s in got), sorted(s["score"] for s in ar), atol=1e-4)
