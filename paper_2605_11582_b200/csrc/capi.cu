@@ -623,6 +623,21 @@ egt_status spmv_impl(const egt_dev_packed* h, const float* x, float* y, uint32_t
                             static_cast<int>(ldy), ctx));
     return EGT_OK;
   }
+  if (M > 16 && !pg && input == EGT_INPUT_NONE && !plan_forced() && umma_eligible(h, static_cast<int>(M))) {
+    // tcgen05 / TMEM many-token kernel (umma_spmm.cu): x stages + per-token
+    // range, then split-K partials, in one per-stream workspace
+    const int ns = num_sms();
+    const size_t xs = (umma_workspace_bytes(h, static_cast<int>(M)) + 255) / 256 * 256;
+    const size_t pf = umma_partial_floats(h, static_cast<int>(M), ns);
+    Workspace* w = nullptr;
+    egt_status st = get_workspace(s, xs / 4 + pf, umma_counters(h, static_cast<int>(M), ns), &w);
+    if (st != EGT_OK) return st;
+    ctx.partial = w->partial + xs / 4;
+    ctx.counters = w->counters;
+    CUDA_TRY(launch_umma(h, x, static_cast<int>(ldx), static_cast<int>(M), y, static_cast<int>(ldy),
+                         reinterpret_cast<uint8_t*>(w->partial), ctx, ns));
+    return EGT_OK;
+  }
   static const bool no_wide = getenv("EGT_NO_WIDE") != nullptr;  // tuning: old M > 16 path
   if (M > 16 && !pg && input == EGT_INPUT_NONE && !no_wide && !plan_forced()) {  // residual / output silu in its epilogue
     Workspace* w = nullptr;

@@ -141,6 +141,16 @@ cudaError_t launch_tiled(const egt_dev_packed* h, const TiledSchedule& sc, const
                          int M, float* y, int ldy, const LaunchCtx& ctx, bool indep);
 // Many-token products (M > 16): x fragments in global memory (xf_ws of
 // wide_workspace_bytes), weight-streaming CTAs per 16-token block (spmm_wide.cu).
+// Many-token products on tcgen05 / TMEM (umma_spmm.cu): INT4 2:4 (and 1:4
+// stored as 2:4), dense INT4 and FP16 2:4 layers with 64/128-column scale
+// groups; ws = umma_workspace_bytes (x stages + per-token range), split-K
+// partials / counters in ctx.
+bool umma_eligible(const egt_dev_packed* h, int M);
+size_t umma_workspace_bytes(const egt_dev_packed* h, int M);
+size_t umma_partial_floats(const egt_dev_packed* h, int M, int num_sms);
+size_t umma_counters(const egt_dev_packed* h, int M, int num_sms);
+cudaError_t launch_umma(const egt_dev_packed* h, const float* x, int ldx, int M, float* y, int ldy,
+                        uint8_t* ws, const LaunchCtx& ctx, int num_sms);
 size_t wide_workspace_bytes(const egt_dev_packed* h, int M);
 cudaError_t launch_wide(const egt_dev_packed* h, const float* x, int ldx, int M, float* y, int ldy,
                         uint32_t* xf_ws, const LaunchCtx& ctx, int num_sms);
