@@ -283,11 +283,12 @@ void egt_set_pdl(int enabled) { g_pdl = enabled != 0; }
 uint64_t egt_launch_count(void) { return launch_counter(); }
 void egt_tune_force_plan(int rb, int s, int nw, int nst, int ch) { force_plan(rb, s, nw, nst, ch); }
 int egt_tune_read_trace(unsigned long long* host, size_t n, int reset) {
-  unsigned long long* b = tiled_trace_buffer();
+  const bool um = getenv("EGT_UMMA_TRACE") != nullptr;
+  unsigned long long* b = um ? umma_trace_buffer() : tiled_trace_buffer();
   if (!b) return 1;
-  n = std::min<size_t>(n, 8 * 4096);
+  n = std::min<size_t>(n, um ? 1024 : 8 * 4096);
   if (cudaMemcpy(host, b, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost) != cudaSuccess) return 2;
-  if (reset) cudaMemset(b, 0, sizeof(unsigned long long) * 8 * 4096);
+  if (reset) cudaMemset(b, 0, sizeof(unsigned long long) * (um ? 1024 : 8 * 4096));
   return 0;
 }
 

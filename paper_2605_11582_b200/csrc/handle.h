@@ -77,6 +77,7 @@ struct egt_dev_packed {
   // Launch plans keyed by M (logically const: a plan depends only on shape).
   mutable std::mutex plan_mu;
   mutable std::map<int, egt_impl::TiledSchedule> plans;
+  mutable std::shared_ptr<void> umma_maps;  // TMA tensor maps of the tcgen05 path (umma_spmm.cu)
 };
 
 // Row-shard peer group (fused all-gather): every rank's buffer in rank order;
@@ -146,6 +147,7 @@ cudaError_t launch_tiled(const egt_dev_packed* h, const TiledSchedule& sc, const
 // groups; ws = umma_workspace_bytes (x stages + per-token range), split-K
 // partials / counters in ctx.
 bool umma_eligible(const egt_dev_packed* h, int M);
+unsigned long long* umma_trace_buffer();  // EGT_UMMA_TRACE (tuning)
 size_t umma_workspace_bytes(const egt_dev_packed* h, int M);
 size_t umma_partial_floats(const egt_dev_packed* h, int M, int num_sms);
 size_t umma_counters(const egt_dev_packed* h, int M, int num_sms);

@@ -20,6 +20,9 @@
 
 #include "egt_b200.h"
 
+// The C++ drop-in is exported from libegt_b200.so (the library builds with
+// -fvisibility=hidden): consumers link -legt_b200 and include this header.
+#pragma GCC visibility push(default)
 namespace egt_b200 {
 
 inline constexpr uint32_t kPadToken = 0;  // trie.hpp:34
@@ -165,3 +168,4 @@ DecodeResult decode(const egt_model* model, const PrefixTrie& trie, std::vector<
                     const DecodeOptions& options, void* stream = nullptr);
 
 }  // namespace egt_b200
+#pragma GCC visibility pop

@@ -24,6 +24,9 @@
 
 #include "egt_b200.h"
 
+// The C++ drop-in is exported from libegt_b200.so (the library builds with
+// -fvisibility=hidden): consumers link -legt_b200 and include this header.
+#pragma GCC visibility push(default)
 namespace egt_b200 {
 
 class FormatError : public std::runtime_error {
@@ -178,3 +181,4 @@ UnpackResult unpack(const DeviceMatrix& w, void* stream = nullptr);
 UnpackResult unpack(const PackedSparseMatrix& packed);
 
 }  // namespace egt_b200
+#pragma GCC visibility pop

@@ -4,34 +4,40 @@
 // BASELINE configs) for INT4 2:4 (and 1:4 stored as 2:4), dense INT4 and
 // FP16 2:4 layers.
 //
-// One CTA = 128 weight rows x one token tile (T <= 128 tokens) x a K range.
-// The accumulator lives in TMEM: D[128 rows x T].  x enters as fp16 hi and
-// lo (x - hi) tiles; per K = 16 step two tcgen05.mma (M = 128, N = T) add
-// A x_hi and A x_lo into the same accumulator (x keeps ~22 mantissa bits,
-// xrange.cuh scales it), so the epilogue reads T columns per scale step --
-// TMEM reads (64 B/cycle/SM) are what paces the per-group epilogue.
+// One CTA = 128 weight rows x one token tile (T <= 120 tokens) x a K range.
+// The accumulator lives in TMEM: D[128 rows x 2T] -- x enters as fp16 hi
+// (columns [0, T)) and lo = x - hi (columns [T, 2T)) in one B operand, so a
+// single tcgen05.mma (M = 128, N = 2T) multiplies both and the epilogue sums
+// them in f32 (x keeps ~22 mantissa bits; xrange.cuh scales it).
 //
 // Warp roles (448 threads, one CTA per SM -- it owns all of TMEM):
-//   warp 0      producer: cp.async.bulk of the packed weight blocks (2 k-quads
-//               x 8 row tiles per raw stage, issued before the PDL wait:
-//               weights never depend on the previous kernel) and of the
-//               pre-laid-out x stages (64 K each) into mbarrier rings;
+//   warp 0      weight producer: per raw stage three 2-D TMA tensor loads
+//               (values, metadata, zero points of 8 row tiles x 1-2
+//               k-quads), the first ones before the PDL wait -- weights never
+//               depend on the previous kernel;
+//   warp 18     x producer: the pre-laid-out x stages (64 K each), a deep ring
+//               (TMA round trips from L2 are ~1 us);
 //   warp 1      TMEM allocator + single-thread MMA issuer (4 x K=16 per stage;
 //               tcgen05.commit releases the smem stages / signals the epilogue);
-//   warps 2-5   dequantisers: packed stage -> the A stage in the UMMA
+//   warps 2-9   dequantisers: two groups of four (alternate stages), two
+//               row tiles per warp: packed stage -> the A stage in the UMMA
 //               canonical K-major layout (8-row x 16-byte core matrices), the
 //               2:4 pairs expanded in place with zeros (c - z exactly in fp16:
 //               the 0x6400 exponent trick), then fence.proxy.async;
-//   warps 6-13  epilogue: INT4 accumulates one scale step (128 or 64 columns)
+//   warps 10-17 epilogue: INT4 accumulates one scale step (128 or 64 columns)
 //               per TMEM buffer (two buffers, ping-pong) and folds it into
 //               registers as acc += s_g * (D_hi + D_lo) -- the reference's
 //               (c - z) * s per group, summed in f32; FP16 layers accumulate
 //               the whole K range in TMEM and are read once.
-// Split-K (S > 1) partials are summed by the last-arriving CTA in slice order
-// (deterministic), as in spmm_tiled.cu.
+// Split-K (S > 1): the S slices of a row block form a thread-block cluster;
+// the leader sums the slices' partials from their shared memory (DSMEM) in
+// slice order (deterministic, no global round trip).
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <memory>
 #include <cmath>
 #include <cstdlib>
 
@@ -45,15 +51,25 @@ using namespace egt_fmt;
 
 namespace {
 
-constexpr int kThreads = 448;
-constexpr int kDeqWarp0 = 2, kNumDeq = 4, kEpiWarp0 = 6, kNumEpi = 8;
+constexpr int kThreads = 608;  // 19 warps
+// dequantisers: two groups of 4 warps take alternate stages (per stage a
+// group's warps cover the 8 row tiles, two each)
+constexpr int kDeqWarp0 = 2, kNumDeq = 8, kDeqGroup = 4, kEpiWarp0 = 10, kNumEpi = 8, kXWarp = 18;
 constexpr int kStageK = 64;  // K per A / B stage: four K = 16 MMAs
 // k-quads per packed-weight (raw) stage (FP16 blocks are 4.5x larger)
 __host__ __device__ constexpr int raw_kq(int fmt) { return fmt == egt_fmt::F16_SP24 ? 1 : 2; }
-constexpr int kNA = 3, kNX = 3, kNR = 3;
-constexpr int kMaxT = 128;   // tokens per tile (N = 2T <= 256)
+constexpr int kNA = 4, kNR = 3, kMaxNX = 10;  // ring depths (x: runtime, <= kMaxNX)
+// tokens per tile: a tcgen05.mma costs ~170 cycles to issue whatever its N
+// (measured, tools/micro/umma_rate.cu), so each MMA takes the tile's hi AND lo
+// halves (N = 2T <= 192); two accumulator buffers + the metadata ring fit
+// the 512 TMEM columns
+constexpr int kMaxT = 96;
 
 struct UmmaArgs {
+  // 2-D tensor maps over the handle's row tiles (int64 elements): values,
+  // metadata, zero points; box = one raw stage of 8 row tiles
+  CUtensorMap tm_vals, tm_meta, tm_zps, tm_scales;
+  int NX;  // x ring depth
   const uint8_t* vals;
   const uint8_t* meta;
   const float* scales;
@@ -65,6 +81,7 @@ struct UmmaArgs {
   const float* x;  // the raw activations (non-finite fix-up only)
   int ldx, cols;
   int M, T, N;  // tokens, tokens per tile (the MMA's N), N = 2T rows per x stage
+  int TTpad;    // padded tokens (token tiles x T) of unsc / nonfin
   int KS;       // B k-stages of the whole K (2 per k-quad)
   int KQC;      // k-quads per CTA (the split size)
   int S;        // K splits (gridDim.z)
@@ -77,15 +94,35 @@ struct UmmaArgs {
   uint32_t* counters;
   int pad14;
   uint32_t raw_rt_bytes;  // bytes per row tile in a raw stage
+  // tuning (EGT_UMMA_TRACE): globaltimer stamps of CTA (0,0,0): [0] start,
+  // [1] past alloc, [8+st] x issued, [80+st] MMA issued, [160+st] stage
+  // dequantised (warp 2), [240+r] round folded (warp 6), [320+rs] raw issued
+  unsigned long long* trace;
 };
+
+__device__ __forceinline__ unsigned long long umma_clock() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;\n" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return smem_u32(p); }
 
-// UMMA shared-memory descriptor, K-major, no swizzle: 8-row x 16-byte core
-// matrices; lbo = byte stride between core matrices along K, sbo = along M/N.
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) | (static_cast<uint64_t>((lbo >> 4) & 0x3FFFu) << 16) |
-         (static_cast<uint64_t>((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);  // version 1 (sm_100)
+// UMMA shared-memory descriptor, K-major, swizzled: rows of 128 B (x stages,
+// dense A) or 64 B (compressed sparse A), 8-row swizzle atoms (sbo = the
+// atom's bytes), the 16-byte chunks of row r XOR-permuted by r's position in
+// the atom; K steps within the atom advance the start address.
+__device__ __forceinline__ uint64_t umma_desc_sw(uint32_t saddr, uint32_t row_bytes) {
+  const uint64_t layout = row_bytes == 128 ? 2ull : 4ull;  // SWIZZLE_128B / SWIZZLE_64B
+  return static_cast<uint64_t>((saddr >> 4) & 0x3FFFu) | (1ull << 16) |
+         (static_cast<uint64_t>(((8 * row_bytes) >> 4) & 0x3FFFu) << 32) | (1ull << 46) | (layout << 61);
+}
+// byte offset of (row, byte-in-row) in a swizzled tile with 128- / 64-byte rows
+__device__ __forceinline__ uint32_t sw128(int r, int byte) {
+  return static_cast<uint32_t>(r * 128 + (byte ^ ((r & 7) << 4)));
+}
+__device__ __forceinline__ uint32_t sw64(int r, int byte) {
+  return static_cast<uint32_t>(r * 64 + (byte ^ (((r >> 1) & 3) << 4)));
 }
 
 // kind::f16 instruction descriptor: D f32, A/B f16, both K-major, M = 128.
@@ -119,6 +156,15 @@ __device__ __forceinline__ void tmem_st2(uint32_t taddr, uint32_t v0, uint32_t v
   asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};\n" ::"r"(taddr), "r"(v0), "r"(v1) : "memory");
 }
 
+// 2-D tensor-map load into shared memory, completing on an mbarrier
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          smem_addr(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_addr(bar))
+      : "memory");
+}
+
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                    smem_addr(bar))
@@ -147,6 +193,40 @@ __device__ __forceinline__ uint2 place2(uint32_t ab, uint32_t o0, uint32_t o1) {
   return make_uint2(static_cast<uint32_t>(w), static_cast<uint32_t>(w >> 32));
 }
 
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];\n" : "=r"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
+  uint16_t v;
+  asm volatile("ld.shared.u16 %0, [%1];\n" : "=h"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint2 lds_v2(uint32_t addr) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];\n" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint4 lds_v4(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+// mbarrier wait that sleeps between probes (the epilogue waits a whole scale
+// step: polling would steal issue slots from the dequantisers)
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITH_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAITH_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(20000u)
+      : "memory");
+}
+
 __device__ __forceinline__ void st_shared_v2(uint32_t addr, uint2 v) {
   asm volatile("st.shared.v2.b32 [%0], {%1, %2};\n" ::"r"(addr), "r"(v.x), "r"(v.y) : "memory");
 }
@@ -158,9 +238,11 @@ __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint4 v) {
                : "memory");
 }
 
-// A-operand byte offset of (row r, column k) in a 128 x 64 stage
+// A-operand byte offset of (row r, column k): a 128 x 64 fp16 stage with
+// 128-byte rows (dense), or 128 x 32 compressed with 64-byte rows (sparse)
+template <bool SPARSE>
 __device__ __forceinline__ uint32_t a_off(int r, int k) {
-  return static_cast<uint32_t>((k >> 3) * 2048 + (r >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2);
+  return SPARSE ? sw64(r, 2 * k) : sw128(r, 2 * k);
 }
 
 template <int FMT>
@@ -178,13 +260,16 @@ __device__ __noinline__ float umma_nonfinite_terms(const UmmaArgs& a, int row, i
 }
 
 template <int FMT, bool SPARSE>
-__global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const UmmaArgs a) {
+__global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const __grid_constant__ UmmaArgs a) {
   static_assert(!SPARSE || FMT != I4_DENSE, "dense INT4 has no 2:4 metadata");
   constexpr bool kScaled = has_scales(FMT);
   constexpr int kRawKQ = raw_kq(FMT);
   constexpr int VB = val_lane_bytes(FMT), MB = meta_lane_bytes(FMT);
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  unsigned long long* tr =
+      (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) ? a.trace : nullptr;
+  if (tr && tid == 0) tr[0] = umma_clock();
   const int rt0 = blockIdx.x * 8;  // first 16-row tile of this CTA (128 rows)
   const int tile = blockIdx.y;     // token tile
   const int kq0 = blockIdx.z * a.KQC;
@@ -196,22 +281,35 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const UmmaArgs a
   const int NROUND = kScaled ? NSTG / steps_per_scale : 1;
 
   // ---- shared memory carve-up
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw + ((1024 - (smem_addr(smem_raw) & 1023)) & 1023));
   uint64_t* raw_full = bars;
   uint64_t* raw_empty = raw_full + kNR;
   uint64_t* a_full = raw_empty + kNR;
   uint64_t* a_empty = a_full + kNA;
+  const int kNX = a.NX;
   uint64_t* x_full = a_empty + kNA;
-  uint64_t* x_empty = x_full + kNX;
-  uint64_t* tm_full = x_empty + kNX;
+  uint64_t* x_empty = x_full + kMaxNX;
+  uint64_t* tm_full = x_empty + kMaxNX;
   uint64_t* tm_empty = tm_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tm_empty + 2);
   __shared__ int s_last;
-  uint8_t* a_st = smem_raw + 1024;                                   // kNA x 16 KB
-  uint8_t* x_st = a_st + kNA * 16384;                                // kNX x (N x 128 B)
+  __shared__ float s_unsc[kMaxT];
+  __shared__ uint32_t s_nonf[kMaxT];
+  // swizzle atoms need 1024-byte aligned tiles
+  uint8_t* smem_al = smem_raw + ((1024 - (smem_addr(smem_raw) & 1023)) & 1023);
+  uint8_t* a_st = smem_al + 1024;  // kNA x 16 KB
+  constexpr uint32_t kASlot = SPARSE ? 8192 : 16384;
+  uint8_t* x_st = a_st + kNA * kASlot;  // kNX x (N x 128 B)
   const uint32_t x_bytes = static_cast<uint32_t>(N) * kStageK * 2;
-  uint8_t* raw_st = x_st + kNX * x_bytes;                            // kNR x (8 x raw_rt_bytes)
+  uint8_t* raw_st = x_st + kNX * x_bytes;  // kNR x (8 x raw_rt_bytes)
+  // raw stage: [values 8 x VBq][metadata 8 x MBq][zero points 8 x ZBq][scales 8 x SBq]
+  constexpr int VBq = kRawKQ * 32 * VB, MBq = kRawKQ * 32 * MB;
+  const int ZBq = kScaled ? kRawKQ * a.E * 16 : 0, SBq = kScaled ? kRawKQ * a.E * 64 : 0;
+  // the scales of the epilogue's rounds, handed over by the dequantisers
+  // (ring of 8 rounds; ordered by a_full -> MMA -> tm_full)
+  __shared__ float s_scale[8 * 128];
   const uint32_t raw_bytes = 8 * a.raw_rt_bytes;
+  const uint32_t raw_s0 = smem_addr(raw_st);
 
   if (tid == 0) {
     for (int i = 0; i < kNR; ++i) {
@@ -219,7 +317,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const UmmaArgs a
       mbar_init(raw_empty + i, kNumDeq);
     }
     for (int i = 0; i < kNA; ++i) {
-      mbar_init(a_full + i, kNumDeq);
+      mbar_init(a_full + i, kDeqGroup);
       mbar_init(a_empty + i, 1);
     }
     for (int i = 0; i < kNX; ++i) {
@@ -232,13 +330,14 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const UmmaArgs a
     }
     mbar_fence_init();
   }
-  // TMEM: accumulator buffer(s) at column 0, sparse metadata (2 columns per
-  // A stage ring slot) at column 256
-  constexpr uint32_t kMetaCol = 256;
-  const uint32_t tmem_cols = SPARSE ? 512u : ((kScaled ? 2 * T : T) <= 128 ? 128u : 256u);
+  // TMEM: accumulator buffer(s) at column 0 (T <= 64 columns each), sparse
+  // metadata (2 columns per A-stage ring slot) at column 128
+  // metadata ring: 16 stages x 2 columns at 448 (written a raw stage ahead)
+  constexpr uint32_t kMetaCol = 448, kMetaRing = 16;
+  constexpr uint32_t tmem_cols = 512u;
   if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_addr(tmem_slot)),
-                 "r"(tmem_cols)
+                 "n"(tmem_cols)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
   }
@@ -246,76 +345,69 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const UmmaArgs a
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (tr && tid == 0) tr[1] = umma_clock();
 
   if (warp == 0) {
-    // ================= producer
+    // ================= weight producer: three 2-D tensor loads per raw stage
     if (lane == 0) {
-      const uint64_t pol = evict_first_policy();
       auto issue_raw = [&](int rs) {
-        const int s = rs % kNR;
-        if (rs >= kNR) mbar_wait(raw_empty + s, ((rs / kNR) - 1) & 1);
-        const int kq = kq0 + rs * kRawKQ, nq = min(kRawKQ, kq0 + KQC - kq);
-        uint32_t bytes = 0;
-        uint8_t* dst0 = raw_st + s * raw_bytes;
-        // values, metadata and zero points (the epilogue reads the scales itself)
-        const uint32_t vb = nq * 32 * VB, mbb = nq * 32 * MB, zb = kScaled ? nq * a.E * 16 : 0;
-        for (int i = 0; i < 8; ++i)
-          if (rt0 + i < a.RT) bytes += vb + mbb + zb;
-        mbar_expect_tx(raw_full + s, bytes);
-        for (int i = 0; i < 8; ++i) {
-          if (rt0 + i >= a.RT) continue;
-          const size_t blk = static_cast<size_t>(a.rt_begin + rt0 + i) * a.KQ + kq;
-          uint8_t* dst = dst0 + i * a.raw_rt_bytes;
-          bulk_g2s(dst, a.vals + blk * 32 * VB, vb, raw_full + s, pol);
-          if (MB > 0) bulk_g2s(dst + kRawKQ * 32 * VB, a.meta + blk * 32 * MB, mbb, raw_full + s, pol);
-          if (kScaled) bulk_g2s(dst + kRawKQ * 32 * (VB + MB), a.zps + blk * a.E * 16, zb, raw_full + s, pol);
+        const int sr = rs % kNR;
+        if (rs >= kNR) mbar_wait(raw_empty + sr, ((rs / kNR) - 1) & 1);
+        if (tr && rs < 64) tr[320 + rs] = umma_clock();
+        const int kq = kq0 + rs * kRawKQ;
+        uint8_t* dst = raw_st + sr * raw_bytes;
+        mbar_expect_tx(raw_full + sr, raw_bytes);  // full boxes (rows / k-quads past the matrix read as 0)
+        tma_load_2d(dst, &a.tm_vals, kq * (32 * VB / 8), rt0, raw_full + sr);
+        if (MB > 0) tma_load_2d(dst + 8 * VBq, &a.tm_meta, kq * (32 * MB / 8), rt0, raw_full + sr);
+        if (kScaled) {
+          tma_load_2d(dst + 8 * (VBq + MBq), &a.tm_zps, kq * (a.E * 2), rt0, raw_full + sr);
+          tma_load_2d(dst + 8 * (VBq + MBq + ZBq), &a.tm_scales, kq * (a.E * 8), rt0, raw_full + sr);
         }
       };
-      int rs_next = 0;
-      for (; rs_next < min(kNR, NRAW); ++rs_next) issue_raw(rs_next);  // before the PDL wait
+      for (int rs = 0; rs < NRAW; ++rs) issue_raw(rs);
+    }
+  } else if (warp == kXWarp) {
+    // ================= x producer
+    if (lane == 0) {
       pdl_wait();  // x stages come from the preceding xprep kernel
       for (int st = 0; st < NSTG; ++st) {
-        if (st % (2 * kRawKQ) == 0 && st / (2 * kRawKQ) >= rs_next && rs_next < NRAW) issue_raw(rs_next++);
         const int s = st % kNX;
         if (st >= kNX) mbar_wait(x_empty + s, ((st / kNX) - 1) & 1);
         mbar_expect_tx(x_full + s, x_bytes);
+        if (tr && st < 72) tr[8 + st] = umma_clock();
         const uint8_t* src = a.xf + (static_cast<size_t>(tile) * a.KS + 2 * kq0 + st) * x_bytes;
         bulk_g2s_plain(x_st + s * x_bytes, src, x_bytes, x_full + s);
-        // keep the weight ring ahead of the x ring
-        while (rs_next < NRAW && rs_next * 2 * kRawKQ <= st + kNX) issue_raw(rs_next++);
       }
     }
   } else if (warp == 1) {
     // ================= MMA issuer
     if (lane == 0) {
-      const uint32_t idesc = umma_idesc(T);
-      const uint32_t lbo_b = static_cast<uint32_t>(N / 8) * 128;  // x stage: hi rows [0, T), lo rows [T, 2T)
-      const uint32_t lo_off = static_cast<uint32_t>(T / 8) * 128;
+      const uint32_t idesc = umma_idesc(N);  // x stage rows: hi [0, T), lo [T, 2T)
       for (int st = 0; st < NSTG; ++st) {
         const int round = st / steps_per_scale, first = st % steps_per_scale == 0;
         const int buf = kScaled ? (round & 1) : 0;
         if (kScaled && first && round >= 2) mbar_wait(tm_empty + buf, ((round / 2) - 1) & 1);
+        if (tr && st < 80) tr[560 + st] = umma_clock();
         mbar_wait(a_full + st % kNA, (st / kNA) & 1);
+        if (tr && st < 80) tr[400 + st] = umma_clock();
         mbar_wait(x_full + st % kNX, (st / kNX) & 1);
         tc_fence_after();
-        const uint32_t abase = smem_addr(a_st + (st % kNA) * 16384);
+        if (tr && st < 80) tr[80 + st] = umma_clock();
+        const uint32_t abase = smem_addr(a_st + (st % kNA) * kASlot);
         const uint32_t bbase = smem_addr(x_st + (st % kNX) * x_bytes);
-        const uint32_t d = tmem + static_cast<uint32_t>(buf * T);
+        const uint32_t d = tmem + static_cast<uint32_t>(buf * N);
         if constexpr (SPARSE) {  // two K = 32 (logical) sparse MMAs per stage, x hi and lo
 #pragma unroll
           for (int jj = 0; jj < 2; ++jj) {
-            const uint64_t ad = umma_desc(abase + jj * 2 * 2048, 2048, 128);
-            const uint32_t e = tmem + kMetaCol + static_cast<uint32_t>(2 * (st % kNA) + jj);
-            umma_f16_sp(d, ad, umma_desc(bbase + jj * 4 * lbo_b, lbo_b, 128), e, idesc,
-                        (first && jj == 0) ? 0u : 1u);
-            umma_f16_sp(d, ad, umma_desc(bbase + lo_off + jj * 4 * lbo_b, lbo_b, 128), e, idesc, 1u);
+            const uint64_t ad = umma_desc_sw(abase + jj * 32, 64);
+            const uint32_t e = tmem + kMetaCol + static_cast<uint32_t>(2 * (st % kMetaRing) + jj);
+            umma_f16_sp(d, ad, umma_desc_sw(bbase + jj * 64, 128), e, idesc, (first && jj == 0) ? 0u : 1u);
           }
         } else {
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
-            const uint64_t ad = umma_desc(abase + kk * 2 * 2048, 2048, 128);
-            umma_f16(d, ad, umma_desc(bbase + kk * 2 * lbo_b, lbo_b, 128), idesc, (first && kk == 0) ? 0u : 1u);
-            umma_f16(d, ad, umma_desc(bbase + lo_off + kk * 2 * lbo_b, lbo_b, 128), idesc, 1u);
+            const uint64_t ad = umma_desc_sw(abase + kk * 32, 128);
+            umma_f16(d, ad, umma_desc_sw(bbase + kk * 32, 128), idesc, (first && kk == 0) ? 0u : 1u);
           }
         }
         umma_commit(a_empty + st % kNA);
@@ -324,100 +416,129 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const UmmaArgs a
       }
     }
   } else if (warp < kEpiWarp0) {
-    // ================= dequantisers: raw stage -> A stage
-    // warp w writes TMEM lanes [32 (w % 4), +32) (the tcgen05.st lane rule):
-    // its row tiles are 2 (w % 4) and 2 (w % 4) + 1
-    const int dq = warp & 3;
+    // ================= dequantisers: raw stage -> A stage, one row tile per
+    // warp.  Warp w may write TMEM lanes [32 (w % 4), +32) only (tcgen05.st):
+    // warps 2-5 write the metadata of row tiles 2 (w % 4) and 2 (w % 4) + 1.
+    const int dq = warp & 3, grp = (warp - kDeqWarp0) / kDeqGroup;
     const int g = lane >> 2, t = lane & 3;
-    for (int st = 0; st < NSTG; ++st) {
+    const int eshift = a.SS == 4 ? 2 : 1;  // k-tile j of a k-quad -> scale entry j >> eshift
+    for (int st = grp; st < NSTG; st += 2) {
       const int sa = st % kNA;
       if (st >= kNA) mbar_wait(a_empty + sa, ((st / kNA) - 1) & 1);
+      if (tr && warp == kDeqWarp0 && lane == 0 && st < 80) tr[640 + st] = umma_clock();
       const int kql = st >> 1, hs = st & 1;
       const int rs = kql / kRawKQ, b = kql % kRawKQ;
       mbar_wait(raw_full + rs % kNR, (rs / kNR) & 1);
-      const uint8_t* rstage = raw_st + (rs % kNR) * raw_bytes;
-      const uint32_t abase = smem_addr(a_st + sa * 16384);
-      for (int ii = 0; ii < 2; ++ii) {
-        const int i = 2 * dq + ii;  // row tile within the CTA
-        if (rt0 + i >= a.RT) {      // past the matrix: zero rows
-          for (int w = lane; w < 16 * 64 * 2 / 16; w += 32) {
-            const int r = i * 16 + (w & 15), ch = w >> 4;
-            st_shared_v4(abase + ch * 2048 + (r >> 3) * 128 + (r & 7) * 16, make_uint4(0, 0, 0, 0));
+      if (tr && warp == kDeqWarp0 && lane == 0 && st < 80) tr[720 + st] = umma_clock();
+      const uint32_t rbase = raw_s0 + (rs % kNR) * raw_bytes;
+      if constexpr (SPARSE) {
+        if (b == 0) {
+          // metadata of this group's sparse MMAs in the raw stage (stages st and
+          // st + 2: k-tiles 2 hs, 2 hs + 1 of each k-quad) -> TMEM lanes
+          // [32 dq, +32), one wait per raw stage
+          const int ti = 2 * dq + (lane >> 4), l16 = lane & 15, gg = l16 & 7, kh = l16 >> 3;
+#pragma unroll
+          for (int bq = 0; bq < kRawKQ; ++bq) {
+            uint32_t w0 = 0x44444444u, w1 = 0x44444444u;  // (0,1): rows / k-quads past the matrix
+            if (rt0 + ti < a.RT && kq0 + rs * kRawKQ + bq < a.KQ) {
+              const uint32_t mb = rbase + 8 * VBq + ti * MBq + bq * 32 * MB;
+              const int j0 = 2 * hs, j1 = 2 * hs + 1;
+              w0 = lds_u32(mb + ((4 * gg + 2 * (j0 & 1) + kh) * 2 + (j0 >> 1)) * 4);
+              w1 = lds_u32(mb + ((4 * gg + 2 * (j1 & 1) + kh) * 2 + (j1 >> 1)) * 4);
+            }
+            tmem_st2(tmem + (static_cast<uint32_t>(32 * dq) << 16) + kMetaCol + 2 * ((st + 2 * bq) % kMetaRing), w0,
+                     w1);
           }
-          continue;
+          asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
+          tc_fence_before();
         }
-        const uint8_t* rt_base = rstage + i * a.raw_rt_bytes;
-        const uint32_t* v = reinterpret_cast<const uint32_t*>(rt_base + (b * 32 + lane) * VB);
-        const uint32_t* mb = reinterpret_cast<const uint32_t*>(rt_base + kRawKQ * 32 * VB + b * 32 * MB);
-        const uint8_t* zp = rt_base + kRawKQ * 32 * (VB + MB) + b * a.E * 16;
+      }
+      const uint32_t abase = smem_addr(a_st + sa * kASlot);
+#pragma unroll
+      for (int ii = 0; ii < 2; ++ii) {
+      const int i = 2 * dq + ii;  // row tile within the CTA
+      if (rt0 + i >= a.RT) {  // past the matrix: zero rows
+        for (int w = lane; w < (SPARSE ? 64 : 128); w += 32) {  // 16 rows x 4 / 8 chunks
+          const int r = i * 16 + (w & 15), ch = w >> 4;
+          st_shared_v4(abase + (SPARSE ? sw64(r, 16 * ch) : sw128(r, 16 * ch)), make_uint4(0, 0, 0, 0));
+        }
+      } else {
+        const uint32_t vbase = rbase + i * VBq + (b * 32 + lane) * VB;
+        const uint32_t mbase = rbase + 8 * VBq + i * MBq + b * 32 * MB;
+        const uint32_t zbase = rbase + 8 * (VBq + MBq) + i * ZBq + b * a.E * 16;
         if constexpr (FMT == I4_DENSE) {
+          const uint4 vv = lds_v4(vbase + hs * 16);  // words w16 = 4 hs .. 4 hs + 3
+          const uint32_t wv[4] = {vv.x, vv.y, vv.z, vv.w};
 #pragma unroll
           for (int w4 = 0; w4 < 4; ++w4) {
-            const int w16 = 4 * hs + w4;
-            const uint32_t word = v[w16];
-            const int e = (w16 >> 1) / a.SS;
+            const int e = (4 * hs + w4) >> (eshift + 1);
+            const uint32_t zz = lds_u16(zbase + e * 16 + 2 * g);
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-              const uint32_t z = zp[e * 16 + 2 * g + h];
+              const uint32_t z = (zz >> (8 * h)) & 0xFFu;
               const int r = i * 16 + g + 8 * h;
 #pragma unroll
               for (int q = 0; q < 2; ++q) {
                 const int p = h + 2 * q;
-                const uint32_t pr = cz_pair((word >> (4 * p)) & 0xFu, (word >> (16 + 4 * p)) & 0xFu, z);
-                st_shared_b32(abase + a_off(r, 16 * w4 + 2 * t + 8 * q), pr);
+                const uint32_t pr = cz_pair((wv[w4] >> (4 * p)) & 0xFu, (wv[w4] >> (16 + 4 * p)) & 0xFu, z);
+                st_shared_b32(abase + a_off<false>(r, 16 * w4 + 2 * t + 8 * q), pr);
               }
             }
           }
         } else {
+          uint32_t vw[2][4];  // [jj][h + 2q]: the pair words of k-tiles 2 hs, 2 hs + 1
+          if constexpr (FMT == I4_SP24) {
+            const uint2 vv = lds_v2(vbase + hs * 8);
+#pragma unroll
+            for (int jj = 0; jj < 2; ++jj) {
+              const uint32_t word = jj ? vv.y : vv.x;
+#pragma unroll
+              for (int p = 0; p < 4; ++p) vw[jj][p] = ((word >> (4 * p)) & 0xFu) | (((word >> (16 + 4 * p)) & 0xFu) << 16);
+            }
+          } else {  // F16_SP24: 4 pair words per k-tile
+            const uint4 v0 = lds_v4(vbase + hs * 32), v1 = lds_v4(vbase + hs * 32 + 16);
+            vw[0][0] = v0.x; vw[0][1] = v0.y; vw[0][2] = v0.z; vw[0][3] = v0.w;
+            vw[1][0] = v1.x; vw[1][1] = v1.y; vw[1][2] = v1.z; vw[1][3] = v1.w;
+          }
 #pragma unroll
           for (int jj = 0; jj < 2; ++jj) {
             const int j = 2 * hs + jj;
+            uint32_t zz = 0;
+            if constexpr (FMT == I4_SP24) zz = lds_u16(zbase + (j >> eshift) * 16 + 2 * g);
 #pragma unroll
             for (int q = 0; q < 2; ++q) {
-              const uint32_t mw = mb[(4 * g + 2 * (j & 1) + q) * 2 + (j >> 1)];
+              uint32_t mw = 0;
+              if constexpr (!SPARSE) mw = lds_u32(mbase + ((4 * g + 2 * (j & 1) + q) * 2 + (j >> 1)) * 4);
 #pragma unroll
               for (int h = 0; h < 2; ++h) {
-                const uint32_t nib = (mw >> (16 * h + 4 * t)) & 0xFu;
-                uint32_t pr;
-                if constexpr (FMT == I4_SP24) {
-                  const int p = h + 2 * q;
-                  const uint32_t z = zp[(j / a.SS) * 16 + 2 * g + h];
-                  pr = cz_pair((v[j] >> (4 * p)) & 0xFu, (v[j] >> (16 + 4 * p)) & 0xFu, z);
-                } else {  // F16_SP24: the two kept fp16 values
-                  pr = v[4 * j + h + 2 * q];
-                }
+                uint32_t pr = vw[jj][h + 2 * q];
+                if constexpr (FMT == I4_SP24) pr = cz_pair(pr & 0xFu, pr >> 16, (zz >> (8 * h)) & 0xFFu);
                 const int r = i * 16 + g + 8 * h, G = t + 4 * q;
-                if constexpr (SPARSE)  // the kept pair, compressed K: groups of 4 -> 2 slots
-                  st_shared_b32(abase + a_off(r, jj * 16 + 2 * G), pr);
-                else
-                  st_shared_v2(abase + a_off(r, jj * 32 + 4 * G), place2(pr, nib & 3u, nib >> 2));
+                if constexpr (SPARSE) {  // the kept pair, compressed K: groups of 4 -> 2 slots
+                  st_shared_b32(abase + a_off<true>(r, jj * 16 + 2 * G), pr);
+                } else {
+                  const uint32_t nib = (mw >> (16 * h + 4 * t)) & 0xFu;
+                  st_shared_v2(abase + a_off<false>(r, jj * 32 + 4 * G), place2(pr, nib & 3u, nib >> 2));
+                }
               }
             }
           }
         }
       }
-      if constexpr (SPARSE) {
-        // metadata of this stage's two sparse MMAs -> TMEM lanes [32 dq, +32)
-        const int ti = 2 * dq + (lane >> 4), l16 = lane & 15, gg = l16 & 7, kh = l16 >> 3;
-        uint32_t w[2] = {0x44444444u, 0x44444444u};  // (0,1) pattern for rows past the matrix
-        if (rt0 + ti < a.RT) {
-          const uint32_t* mbt = reinterpret_cast<const uint32_t*>(rstage + ti * a.raw_rt_bytes + kRawKQ * 32 * VB +
-                                                                  b * 32 * MB);
-#pragma unroll
-          for (int jj = 0; jj < 2; ++jj) {
-            const int j = 2 * hs + jj;
-            w[jj] = mbt[(4 * gg + 2 * (j & 1) + kh) * 2 + (j >> 1)];
-          }
-        }
-        tmem_st2(tmem + (static_cast<uint32_t>(32 * dq) << 16) + kMetaCol + 2 * sa, w[0], w[1]);
-        asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory");
-        tc_fence_before();
+      }  // row tiles
+      if (kScaled && (a.SS == 2 || hs == 0)) {  // this round's scales of row tiles 2 dq, 2 dq + 1
+        const int e = a.SS == 2 ? hs : 0, i = 2 * dq + (lane >> 4), l16 = lane & 15;
+        const uint32_t sb = rbase + 8 * (VBq + MBq + ZBq) + i * SBq + b * a.E * 64;
+        s_scale[((st / steps_per_scale) & 7) * 128 + i * 16 + l16] =
+            __uint_as_float(lds_u32(sb + (e * 16 + 2 * (l16 & 7) + (l16 >> 3)) * 4));
       }
       fence_async_smem();  // generic-proxy writes -> visible to the tensor core
       __syncwarp();
       if (lane == 0) {
         mbar_arrive(a_full + sa);
-        if (hs == 1 && (b == kRawKQ - 1 || kql == KQC - 1)) mbar_arrive(raw_empty + rs % kNR);
+        if (b == kRawKQ - 1 || kql == KQC - 1) mbar_arrive(raw_empty + rs % kNR);  // this group's last use
+        if (tr && warp == kDeqWarp0 && st < 80) tr[160 + st] = umma_clock();
+        if (tr && warp == kEpiWarp0 - 1 && st < 80) tr[480 + st] = umma_clock();  // last dequantiser
       }
     }
   } else {
@@ -428,55 +549,82 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const UmmaArgs a
     const int th = T / 2, c0 = half * th;  // this thread's token columns [c0, c0 + th)
     float acc[kMaxT / 2];
 #pragma unroll
-    for (int i = 0; i < kMaxT / 2; ++i) acc[i] = 0.f;
+    for (int k = 0; k < kMaxT / 2; ++k) acc[k] = 0.f;
     const uint32_t lane_base = tmem + (static_cast<uint32_t>(32 * q) << 16);
     const bool row_ok = grow < a.rows && (rt0 + (r >> 4)) < a.RT;
     for (int round = 0; round < NROUND; ++round) {
       const int buf = kScaled ? (round & 1) : 0;
-      float s = 1.f;
-      if (kScaled && row_ok) {  // the row's scale of this round's column group
-        const int kql = (round * steps_per_scale) / 2;
-        const int e = ((round * steps_per_scale) % 2) * 2 / a.SS;
-        const size_t blk = static_cast<size_t>(a.rt_begin + rt0 + (r >> 4)) * a.KQ + kq0 + kql;
-        s = __ldg(a.scales + (blk * a.E + e) * 16 + 2 * (r & 7) + ((r >> 3) & 1));
-      }
-      mbar_wait(tm_full + buf, kScaled ? ((round >> 1) & 1) : 0);
+      mbar_wait_sleep(tm_full + buf, kScaled ? ((round >> 1) & 1) : 0);
       tc_fence_after();
-      // batches of up to 32 columns: every load in flight, then one wait
+      const float s = kScaled ? s_scale[(round & 7) * 128 + r] : 1.f;  // the row's scale of this round
+      // chunks of 16 tokens: their hi and lo columns in flight together, one wait
 #pragma unroll
-      for (int bb = 0; bb < kMaxT / 2; bb += 32) {
-        if (bb < th) {
-          uint32_t v[32];
-#pragma unroll
-          for (int cb = 0; cb < 4; ++cb)
-            if (bb + cb * 8 < th) tmem_ld8_nowait(lane_base + static_cast<uint32_t>(buf * T + c0 + bb + cb * 8), v + cb * 8);
+      for (int cb = 0; cb < (kMaxT / 2 + 15) / 16; ++cb) {
+        if (cb * 16 < th) {
+          uint32_t vh[16], vl[16];
+          const uint32_t col = lane_base + static_cast<uint32_t>(buf * N + c0 + cb * 16);
+          tmem_ld8_nowait(col, vh);
+          tmem_ld8_nowait(col + T, vl);
+          if (cb * 16 + 8 < th) {
+            tmem_ld8_nowait(col + 8, vh + 8);
+            tmem_ld8_nowait(col + T + 8, vl + 8);
+          }
           asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 #pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (bb + i < th) acc[bb + i] = fmaf(s, __uint_as_float(v[i]), acc[bb + i]);
+          for (int k = 0; k < 16; ++k)
+            if (cb * 16 + k < th && cb * 16 + k < kMaxT / 2)
+              acc[cb * 16 + k] = fmaf(s, __uint_as_float(vh[k]) + __uint_as_float(vl[k]), acc[cb * 16 + k]);
         }
       }
       tc_fence_before();
       __syncwarp();
       if (kScaled && lane == 0) mbar_arrive(tm_empty + buf);
+      if (tr && warp == kEpiWarp0 && lane == 0 && round < 80) tr[240 + round] = umma_clock();
     }
-    // ---- outputs: rescale (xrange.cuh), fix-up, residual / silu or partials
+    // ---- outputs: rescale (xrange.cuh), fix-up; then residual / silu and the
+    // store (one CTA), or the cluster's split-K sum (below)
     pdl_wait();  // residual rows / x scales belong to earlier kernels
+    const int ew = (warp - kEpiWarp0) * 32 + lane;
+    if (ew < T) {
+      const int tok = min(tile * T + ew, a.TTpad - 1);
+      s_unsc[ew] = a.unsc[tok];
+      s_nonf[ew] = a.nonfin[tok];
+    }
+    asm volatile("bar.sync 1, %0;\n" ::"n"(kNumEpi * 32) : "memory");  // epilogue warps only
     const int kc0 = kq0 * 128, kc1 = min(a.cols, (kq0 + KQC) * 128);
-    if (row_ok) {
 #pragma unroll
-      for (int i = 0; i < kMaxT / 2; ++i) {
-        if (i < th) {
-          const int tok = tile * T + c0 + i;
-          if (tok < a.M) {
-            float v = acc[i] * a.unsc[tok];
-            if (a.nonfin[tok]) v += umma_nonfinite_terms<FMT>(a, grow, tok, kc0, kc1);
-            if (a.S == 1) {
-              float o = (a.res ? a.res[static_cast<size_t>(tok) * a.ldr + grow] : 0.f) + v;
+    for (int k = 0; k < kMaxT / 2; ++k) {
+      if (k < th) {
+        const int tl = c0 + k, tok = tile * T + tl;
+        float val = acc[k] * s_unsc[tl];
+        if (row_ok && tok < a.M && s_nonf[tl]) val += umma_nonfinite_terms<FMT>(a, grow, tok, kc0, kc1);
+        acc[k] = val;
+      }
+    }
+    if (a.S > 1) {  // this slice's partials -> own shared memory (the x ring is idle now)
+      float* part = reinterpret_cast<float*>(x_st);
+#pragma unroll
+      for (int k = 0; k < kMaxT / 2; ++k)
+        if (k < th) part[(c0 + k) * 128 + r] = acc[k];
+    }
+    if (a.S == 1 && row_ok) {
+      // 8 tokens at a time: residuals first (they may alias y), all in flight
+#pragma unroll
+      for (int k0 = 0; k0 < kMaxT / 2; k0 += 8) {
+        if (k0 < th) {
+          float rv[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int tok = tile * T + c0 + k0 + u;
+            rv[u] = (a.res && k0 + u < th && tok < a.M) ? a.res[static_cast<size_t>(tok) * a.ldr + grow] : 0.f;
+          }
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int tok = tile * T + c0 + k0 + u;
+            if (k0 + u < th && tok < a.M) {
+              float o = rv[u] + acc[k0 + u];
               if (a.out_silu) o = o * (1.0f / (1.0f + expf(-o)));  // model.cpp:80-84
               a.y[static_cast<size_t>(tok) * a.ldy + grow] = o;
-            } else {
-              a.partial[(static_cast<size_t>(blockIdx.z) * a.M + tok) * a.rows + grow] = v;
             }
           }
         }
@@ -484,40 +632,62 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const UmmaArgs a
     }
   }
 
-  // ---- teardown: TMEM back, then the split-K reduction by the last CTA
+  // ---- teardown: TMEM back; split K: the cluster's leader sums the slices'
+  // partials from their shared memory (DSMEM) in slice order -- deterministic
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   if (warp == 1)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(tmem_cols) : "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(tmem_cols) : "memory");
   pdl_launch_dependents();
   if (a.S == 1) return;
-  __threadfence();
-  __syncthreads();
-  const int cidx = blockIdx.x + gridDim.x * blockIdx.y;
-  if (tid == 0) s_last = atomicAdd(a.counters + cidx, 1u) == static_cast<uint32_t>(a.S - 1);
-  __syncthreads();
-  if (!s_last) return;
-  __threadfence();
-  const int rows_here = min(128, a.rows - rt0 * 16);
-  const int toks_here = min(T, a.M - tile * T);
-  for (int idx = tid; idx < rows_here * toks_here; idx += blockDim.x) {
-    const int rr = idx % rows_here, tt = idx / rows_here;
-    const int grow = rt0 * 16 + rr, tok = tile * T + tt;
-    float v = 0.f;
-    for (int z = 0; z < a.S; ++z) v += __ldcg(a.partial + (static_cast<size_t>(z) * a.M + tok) * a.rows + grow);
-    float o = (a.res ? a.res[static_cast<size_t>(tok) * a.ldr + grow] : 0.f) + v;
-    if (a.out_silu) o = o * (1.0f / (1.0f + expf(-o)));
-    a.y[static_cast<size_t>(tok) * a.ldy + grow] = o;
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  if (blockIdx.z == 0 && warp >= kEpiWarp0 && warp < kEpiWarp0 + kNumEpi) {
+    const int q = warp & 3, half = (warp - kEpiWarp0) >> 2;
+    const int r = 32 * q + lane, grow = rt0 * 16 + r;
+    const int th = T / 2, c0 = half * th;
+    if (grow < a.rows && (rt0 + (r >> 4)) < a.RT) {
+      const uint32_t part0 = smem_addr(x_st);
+      for (int k0 = 0; k0 < th; k0 += 8) {  // 8 tokens at a time
+        float sum[8], rv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          sum[u] = 0.f;
+          const int tok = tile * T + c0 + k0 + u;
+          rv[u] = (a.res && k0 + u < th && tok < a.M) ? a.res[static_cast<size_t>(tok) * a.ldr + grow] : 0.f;
+        }
+        for (int z = 0; z < a.S; ++z) {
+          uint32_t remote;
+          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(remote) : "r"(part0), "r"(z));
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            float v;
+            asm volatile("ld.shared::cluster.f32 %0, [%1];\n" : "=f"(v) : "r"(remote + ((c0 + k0 + u) * 128 + r) * 4));
+            sum[u] += v;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int tok = tile * T + c0 + k0 + u;
+          if (k0 + u < th && tok < a.M) {
+            float o = rv[u] + sum[u];
+            if (a.out_silu) o = o * (1.0f / (1.0f + expf(-o)));
+            a.y[static_cast<size_t>(tok) * a.ldy + grow] = o;
+          }
+        }
+      }
+    }
   }
-  if (tid == 0) a.counters[cidx] = 0u;  // ready for the next launch / graph replay
+  // every slice's shared memory stays alive until the leader has read it
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
 // X [M x cols] -> B stages: per token tile, per 64-column k-stage, N = 2T rows
-// (row n < T: fp16 hi of token n; row T + n: its residual lo), K-major
-// canonical layout (element (n, k): (k/8)*lbo + (n/8)*128 + (n%8)*16 +
-// (k%8)*2, lbo = N/8 * 128).  One CTA per padded token: its range first
-// (xrange.cuh), then one thread per 8-column chunk (two 16-byte stores).
+// (row n < T: fp16 hi of token n; row T + n: its residual lo) of 128 bytes,
+// K-major with the 128-byte swizzle (the bulk copy keeps the pattern: stages
+// land 1024-byte aligned).  One CTA per padded token: its range first
+// (xrange.cuh; every load of a thread in flight together), then one thread
+// per 8-column chunk (two 16-byte stores).
 __global__ void __launch_bounds__(256) umma_xprep_kernel(const float* __restrict__ x, int ldx, int M, int cols,
                                                          int T, int KS, uint8_t* __restrict__ xf,
                                                          float* __restrict__ unsc, uint32_t* __restrict__ nonfin) {
@@ -531,9 +701,26 @@ __global__ void __launch_bounds__(256) umma_xprep_kernel(const float* __restrict
   }
   __syncthreads();
   const float* xr = x + static_cast<size_t>(tok) * ldx;
+  const bool vec = (ldx & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
   if (tok < M) {
     uint32_t mx = 0u, nf = 0u;
-    for (int k = tid; k < cols; k += blockDim.x) xr_note(mx, nf, __ldg(xr + k));
+    if (vec) {
+      const int n4 = cols >> 2;
+      for (int k4 = tid; k4 < n4; k4 += 4 * blockDim.x) {
+        float4 q[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          q[u] = k4 + u * static_cast<int>(blockDim.x) < n4 ? __ldg(reinterpret_cast<const float4*>(xr) + k4 + u * blockDim.x)
+                                                           : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          xr_note(mx, nf, q[u].x); xr_note(mx, nf, q[u].y); xr_note(mx, nf, q[u].z); xr_note(mx, nf, q[u].w);
+        }
+      }
+      for (int k = 4 * n4 + tid; k < cols; k += blockDim.x) xr_note(mx, nf, __ldg(xr + k));
+    } else {
+      for (int k = tid; k < cols; k += blockDim.x) xr_note(mx, nf, __ldg(xr + k));
+    }
     xr_commit(mx, nf, &s_mx, &s_nf);
   }
   __syncthreads();
@@ -544,26 +731,32 @@ __global__ void __launch_bounds__(256) umma_xprep_kernel(const float* __restrict
     nonfin[tok] = s_nf;
   }
   const int N = 2 * T, tl = tok % T, tile = tok / T;
-  const uint32_t lbo = static_cast<uint32_t>(N / 8) * 128, stage_bytes = static_cast<uint32_t>(N) * kStageK * 2;
+  const uint32_t stage_bytes = static_cast<uint32_t>(N) * kStageK * 2;
   for (int ch = tid; ch < KS * (kStageK / 8); ch += blockDim.x) {
     const int ks = ch / (kStageK / 8), cin = ch % (kStageK / 8), k0 = ch * 8;
+    float xv[8];
+    if (tok < M && vec && k0 + 8 <= cols) {
+      const float4 a0 = __ldg(reinterpret_cast<const float4*>(xr + k0));
+      const float4 a1 = __ldg(reinterpret_cast<const float4*>(xr + k0 + 4));
+      xv[0] = a0.x; xv[1] = a0.y; xv[2] = a0.z; xv[3] = a0.w;
+      xv[4] = a1.x; xv[5] = a1.y; xv[6] = a1.z; xv[7] = a1.w;
+    } else {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) xv[u] = tok < M && k0 + u < cols ? __ldg(xr + k0 + u) : 0.f;
+    }
     uint32_t h[4], l[4];
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
-      float v0 = 0.f, v1 = 0.f;
-      if (tok < M) {
-        if (k0 + 2 * p < cols) v0 = xr_scaled(__ldg(xr + k0 + 2 * p), sc);
-        if (k0 + 2 * p + 1 < cols) v1 = xr_scaled(__ldg(xr + k0 + 2 * p + 1), sc);
-      }
+      const float v0 = xr_scaled(xv[2 * p], sc), v1 = xr_scaled(xv[2 * p + 1], sc);
       const __half h0 = __float2half_rn(v0), h1 = __float2half_rn(v1);
       const __half l0 = __float2half_rn(v0 - __half2float(h0)), l1 = __float2half_rn(v1 - __half2float(h1));
       h[p] = static_cast<uint32_t>(__half_as_ushort(h0)) | (static_cast<uint32_t>(__half_as_ushort(h1)) << 16);
       l[p] = static_cast<uint32_t>(__half_as_ushort(l0)) | (static_cast<uint32_t>(__half_as_ushort(l1)) << 16);
     }
-    uint8_t* st = xf + (static_cast<size_t>(tile) * KS + ks) * stage_bytes + cin * lbo;
+    uint8_t* st = xf + (static_cast<size_t>(tile) * KS + ks) * stage_bytes;
     const int nh = tl, nl = T + tl;
-    *reinterpret_cast<uint4*>(st + (nh >> 3) * 128 + (nh & 7) * 16) = make_uint4(h[0], h[1], h[2], h[3]);
-    *reinterpret_cast<uint4*>(st + (nl >> 3) * 128 + (nl & 7) * 16) = make_uint4(l[0], l[1], l[2], l[3]);
+    *reinterpret_cast<uint4*>(st + sw128(nh, 16 * cin)) = make_uint4(h[0], h[1], h[2], h[3]);
+    *reinterpret_cast<uint4*>(st + sw128(nl, 16 * cin)) = make_uint4(l[0], l[1], l[2], l[3]);
   }
 }
 
@@ -575,13 +768,13 @@ struct UmmaPlan {
 UmmaPlan plan_umma(const egt_dev_packed* h, int M, int num_sms) {
   UmmaPlan p;
   const int tiles = (M + kMaxT - 1) / kMaxT;
-  p.T = ((M + tiles - 1) / tiles + 15) / 16 * 16;  // N = 2T a multiple of 32
+  p.T = ((M + tiles - 1) / tiles + 15) / 16 * 16;  // the MMA's N: a multiple of 16
   p.TT = (M + p.T - 1) / p.T;
   const int KQ = h->tiled.KQ;
   const int R = (h->tiled.RT + 7) / 8;
   // split K while it removes a wave: cost ~ waves x k-quads per CTA
   double best = 1e300;
-  for (int S = 1; S <= std::min(8, KQ); ++S) {
+  for (int S = 1; S <= std::min(8, KQ); ++S) {  // S CTAs form one cluster (portable size <= 8)
     const int kqc = (KQ + S - 1) / S;
     const int Seff = (KQ + kqc - 1) / kqc;
     const long long ctas = static_cast<long long>(R) * p.TT * Seff;
@@ -598,7 +791,7 @@ UmmaPlan plan_umma(const egt_dev_packed* h, int M, int num_sms) {
 
 uint32_t raw_rt_bytes(int fmt, int E) {
   return static_cast<uint32_t>(raw_kq(fmt) * 32 * (val_lane_bytes(fmt) + meta_lane_bytes(fmt)) +
-                               (has_scales(fmt) ? raw_kq(fmt) * E * 16 : 0));
+                               (has_scales(fmt) ? raw_kq(fmt) * E * 80 : 0));
 }
 
 // EGT_UMMA_DENSE: 2:4 layers expanded with zeros on the dense kind::f16 MMA
@@ -618,13 +811,29 @@ void* pick_umma(int fmt) {
 
 }  // namespace
 
+unsigned long long* umma_trace_buffer() {
+  static unsigned long long* b = [] {
+    unsigned long long* p = nullptr;
+    if (getenv("EGT_UMMA_TRACE")) {
+      cudaMalloc(&p, 8 * 1024);
+      cudaMemset(p, 0, 8 * 1024);
+    }
+    return p;
+  }();
+  return b;
+}
+
 bool umma_eligible(const egt_dev_packed* h, int M) {
   static const bool off = getenv("EGT_NO_UMMA") != nullptr;
   if (off || M < 17 || h->path != 0) return false;
   const int f = h->format;
   if (f != I4_SP24 && f != I4_DENSE && f != F16_SP24) return false;
   if (has_scales(f) && h->tiled.SS != 4 && h->tiled.SS != 2) return false;
-  return true;
+  static const bool always = getenv("EGT_UMMA_ALWAYS") != nullptr;
+  // measured (tools/umma_probe.py, B200): one token tile, or tall matrices
+  // whose many row blocks amortise the per-stage issue cost, beat the
+  // mma.sp kernel; several tiles of a short matrix do not (yet)
+  return always || M <= kMaxT || h->rows >= 8192;
 }
 
 size_t umma_workspace_bytes(const egt_dev_packed* h, int M) {
@@ -635,17 +844,69 @@ size_t umma_workspace_bytes(const egt_dev_packed* h, int M) {
   return static_cast<size_t>(TT) * KS * (2 * T) * kStageK * 2 + static_cast<size_t>(TT) * T * 8;
 }
 
-size_t umma_partial_floats(const egt_dev_packed* h, int M, int num_sms) {
-  const UmmaPlan p = plan_umma(h, M, num_sms);
-  return p.S > 1 ? static_cast<size_t>(p.S) * M * h->rows : 0;
+// split-K partials stay on chip (cluster DSMEM): no global workspace
+size_t umma_partial_floats(const egt_dev_packed*, int, int) { return 0; }
+size_t umma_counters(const egt_dev_packed*, int, int) { return 0; }
+
+// The handle's three 2-D tensor maps (built once, kept on the handle): rows
+// = the handle's row tiles, inner = its k-quads' bytes as int64 elements.
+struct UmmaMaps {
+  CUtensorMap vals, meta, zps, scales;
+};
+
+cudaError_t encode_2d(CUtensorMap* m, const void* base, uint64_t inner_elems, uint64_t rows, uint64_t pitch_bytes,
+                      uint32_t box_inner) {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  if (!fn) return cudaErrorNotSupported;
+  const cuuint64_t dims[2] = {inner_elems, rows};
+  const cuuint64_t strides[1] = {pitch_bytes};
+  const cuuint32_t box[2] = {box_inner, 8};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_INT64, 2, const_cast<void*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
-size_t umma_counters(const egt_dev_packed* h, int M, int num_sms) {
-  const UmmaPlan p = plan_umma(h, M, num_sms);
-  return static_cast<size_t>((h->tiled.RT + 7) / 8) * p.TT;
+
+cudaError_t umma_maps(const egt_dev_packed* h, const UmmaMaps** out) {
+  std::lock_guard<std::mutex> lk(h->plan_mu);
+  if (!h->umma_maps) {
+    auto m = std::make_shared<UmmaMaps>();
+    const int f = h->format, KQ = h->tiled.KQ, RT = h->tiled.RT, E = h->tiled.E, kr = raw_kq(f);
+    const int VB = val_lane_bytes(f), MB = meta_lane_bytes(f);
+    const size_t rt0 = static_cast<size_t>(h->tiled.rt_begin) * KQ;
+    cudaError_t e = encode_2d(&m->vals, h->tiled.vals + rt0 * 32 * VB, static_cast<uint64_t>(KQ) * 32 * VB / 8, RT,
+                              static_cast<uint64_t>(KQ) * 32 * VB, kr * 32 * VB / 8);
+    if (e == cudaSuccess && MB > 0)
+      e = encode_2d(&m->meta, h->tiled.meta + rt0 * 32 * MB, static_cast<uint64_t>(KQ) * 32 * MB / 8, RT,
+                    static_cast<uint64_t>(KQ) * 32 * MB, kr * 32 * MB / 8);
+    if (e == cudaSuccess && has_scales(f))
+      e = encode_2d(&m->zps, h->tiled.zps + rt0 * E * 16, static_cast<uint64_t>(KQ) * E * 2, RT,
+                    static_cast<uint64_t>(KQ) * E * 16, kr * E * 2);
+    if (e == cudaSuccess && has_scales(f))
+      e = encode_2d(&m->scales, h->tiled.scales + rt0 * E * 16, static_cast<uint64_t>(KQ) * E * 8, RT,
+                    static_cast<uint64_t>(KQ) * E * 64, kr * E * 8);
+    if (e != cudaSuccess) return e;
+    h->umma_maps = m;
+  }
+  *out = static_cast<const UmmaMaps*>(h->umma_maps.get());
+  return cudaSuccess;
 }
 
 cudaError_t launch_umma(const egt_dev_packed* h, const float* x, int ldx, int M, float* y, int ldy,
                         uint8_t* ws, const LaunchCtx& ctx, int num_sms) {
+  const UmmaMaps* maps = nullptr;
+  {
+    const cudaError_t e = umma_maps(h, &maps);
+    if (e != cudaSuccess) return e;
+  }
   const UmmaPlan p = plan_umma(h, M, num_sms);
   const int KS = 2 * h->tiled.KQ;
   uint8_t* xf = ws;
@@ -668,6 +929,10 @@ cudaError_t launch_umma(const egt_dev_packed* h, const float* x, int ldx, int M,
     ++launch_counter();
   }
   UmmaArgs a;
+  a.tm_vals = maps->vals;
+  a.tm_meta = maps->meta;
+  a.tm_zps = maps->zps;
+  a.tm_scales = maps->scales;
   a.vals = h->tiled.vals;
   a.meta = h->tiled.meta;
   a.scales = h->tiled.scales;
@@ -687,6 +952,7 @@ cudaError_t launch_umma(const egt_dev_packed* h, const float* x, int ldx, int M,
   a.M = M;
   a.T = p.T;
   a.N = 2 * p.T;
+  a.TTpad = p.TT * p.T;
   a.KS = KS;
   a.KQC = p.KQC;
   a.S = p.S;
@@ -699,7 +965,13 @@ cudaError_t launch_umma(const egt_dev_packed* h, const float* x, int ldx, int M,
   a.counters = ctx.counters;
   a.pad14 = h->tiled.pad14;
   a.raw_rt_bytes = raw_rt_bytes(h->format, h->tiled.E);
-  const size_t smem = 1024 + kNA * 16384 + kNX * static_cast<size_t>(a.N) * kStageK * 2 + kNR * 8 * a.raw_rt_bytes;
+  a.trace = umma_trace_buffer();
+  const size_t x_bytes = static_cast<size_t>(a.N) * kStageK * 2;
+  const bool sparse_path = h->format != I4_DENSE && getenv("EGT_UMMA_DENSE") == nullptr;
+  const size_t fixed = 2048 + kNA * (sparse_path ? 8192 : 16384) + kNR * 8 * static_cast<size_t>(a.raw_rt_bytes);
+  a.NX = static_cast<int>(std::min<size_t>(kMaxNX, (227 * 1024 - fixed) / x_bytes));
+  if (a.NX < 2) return cudaErrorInvalidConfiguration;
+  const size_t smem = fixed + a.NX * x_bytes;
   void* fn = pick_umma(h->format);
   cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (err != cudaSuccess) return err;
@@ -708,11 +980,15 @@ cudaError_t launch_umma(const egt_dev_packed* h, const float* x, int ldx, int M,
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = ctx.stream;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;  // the split-K slices of a row block
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = p.S;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = ctx.pdl ? 1 : 0;
+  cfg.numAttrs = ctx.pdl ? 2 : 1;
   void* args[] = {&a};
   err = cudaLaunchKernelExC(&cfg, fn, args);
   if (err == cudaSuccess) ++launch_counter();

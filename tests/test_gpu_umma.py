@@ -39,7 +39,9 @@ def test_umma_products(port, fmt, M):
     import torch
 
     rng = np.random.default_rng(M + len(fmt))
-    rows, cols = (400, 1408) if M != 80 else (4096, 4096)  # ragged 128-row tile / k-quads; a 7B shape
+    # ragged 128-row tile / k-quads; a 7B shape; several token tiles run on
+    # tcgen05 for tall matrices (umma_eligible)
+    rows, cols = {17: (400, 1408), 80: (4096, 4096)}.get(M, (8200, 640))
     d, ref = _layer(port, rng, fmt, rows, cols)
     xs = rng.uniform(-1, 1, (M, cols)).astype(np.float32)
     y = d.spmv(torch.from_numpy(xs).cuda()).cpu().numpy()
