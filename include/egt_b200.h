@@ -259,6 +259,22 @@ typedef struct egt_tree_view {
 EGT_API egt_status egt_forward_tree(const egt_model* m, const int32_t* tokens, const int32_t* positions,
                                     const egt_tree_view* tree, float* logits_dev, void* stream);
 
+/* KV pool for the KV-cached trie-constrained beam step (
+ * the reference recomputes every prefix, decode.cpp:122-190): the keys and
+ * values of committed rows, [n_layers][capacity][d_model], a row written once
+ * and shared by every beam whose prefix holds it. */
+typedef struct egt_kv_pool egt_kv_pool;
+EGT_API egt_status egt_kv_pool_create(const egt_model* m, uint32_t capacity, egt_kv_pool** out);
+EGT_API egt_status egt_kv_pool_destroy(egt_kv_pool* p);
+/* forward over M rows storing each row's keys / values at pool row
+ * out_rows[i].  With key lists (key_ptr [M+1], key_rows): row i attends to
+ * pool rows key_rows[key_ptr[i] .. key_ptr[i+1]) then itself (its causal
+ * prefix, position order) -- no mask.  Without: mask_bits as egt_forward. */
+EGT_API egt_status egt_forward_kv(const egt_model* m, egt_kv_pool* pool, const int32_t* tokens,
+                                  const int32_t* positions, uint32_t M, const uint8_t* mask_bits,
+                                  const uint32_t* out_rows, const uint32_t* key_ptr, const uint32_t* key_rows,
+                                  float* logits_dev, void* stream);
+
 /* out[i] = src_dev[rows[i] * ld + cols[i]] (host index lists, host output). */
 EGT_API egt_status egt_gather(const float* src_dev, uint64_t ld, const uint32_t* rows,
                               const uint32_t* cols, uint32_t n, float* out, void* stream);
@@ -315,6 +331,7 @@ typedef struct egt_decode_options {
   int forced_depth;
   double t_step, alpha, beta; /* CostModel, seconds */
   uint64_t node_cap;
+  int kv_cache; /* 1: constrained steps on a KV pool (egt_forward_kv), one new row per beam per step */
 } egt_decode_options;
 
 EGT_API egt_status egt_decode(const egt_model* m, const egt_trie_view* trie, const int32_t* prompt,

@@ -10,6 +10,7 @@
 #include <cmath>
 #include <cstring>
 #include <limits>
+#include <memory>
 #include <stdexcept>
 #include <string>
 
@@ -52,11 +53,9 @@ struct RowRequest {
   uint32_t node;  // trie node whose children are scored
 };
 
-std::vector<std::vector<float>> score_rows(const egt_model* model, const PrefixTrie& trie,
-                                           const std::vector<int>& tokens, const std::vector<int>& positions,
-                                           const std::vector<uint8_t>* bits, const egt_tree_view* tree,
-                                           const std::vector<RowRequest>& reqs, uint32_t vocab, void* stream) {
-  const uint32_t M = static_cast<uint32_t>(tokens.size());
+template <class Forward>
+std::vector<std::vector<float>> score_rows_with(const PrefixTrie& trie, uint32_t M, Forward&& forward,
+                                                const std::vector<RowRequest>& reqs, uint32_t vocab, void* stream) {
   std::vector<uint32_t> rows, cols;
   for (const RowRequest& r : reqs)
     for (uint32_t c : trie.nodes[r.node].children) {
@@ -72,8 +71,7 @@ std::vector<std::vector<float>> score_rows(const egt_model* model, const PrefixT
       cudaSuccess)
     throw CudaError("decode: logits allocation failed");
   std::vector<float> vals(rows.size());
-  egt_status st = tree ? egt_forward_tree(model, tokens.data(), positions.data(), tree, logits, stream)
-                      : egt_forward(model, tokens.data(), positions.data(), bits->data(), M, logits, stream);
+  egt_status st = forward(logits);
   if (st == EGT_OK)
     st = egt_gather(logits, vocab, rows.data(), cols.data(), static_cast<uint32_t>(rows.size()), vals.data(), stream);
   cudaFreeAsync(logits, s);
@@ -87,6 +85,20 @@ std::vector<std::vector<float>> score_rows(const egt_model* model, const PrefixT
     at += n;
   }
   return out;
+}
+
+std::vector<std::vector<float>> score_rows(const egt_model* model, const PrefixTrie& trie,
+                                           const std::vector<int>& tokens, const std::vector<int>& positions,
+                                           const std::vector<uint8_t>* bits, const egt_tree_view* tree,
+                                           const std::vector<RowRequest>& reqs, uint32_t vocab, void* stream) {
+  const uint32_t M = static_cast<uint32_t>(tokens.size());
+  return score_rows_with(
+      trie, M,
+      [&](float* logits) {
+        return tree ? egt_forward_tree(model, tokens.data(), positions.data(), tree, logits, stream)
+                    : egt_forward(model, tokens.data(), positions.data(), bits->data(), M, logits, stream);
+      },
+      reqs, vocab, stream);
 }
 
 void set_bit(std::vector<uint8_t>& bits, size_t i) { bits[i >> 3] |= static_cast<uint8_t>(1u << (i & 7)); }
@@ -424,6 +436,103 @@ void constrained_step(const egt_model* model, DecodeSession& s, const PrefixTrie
   s.steps += 1;
 }
 
+// The trie-constrained beam step with a KV pool: the same
+// candidates, ranking and ties as constrained_step (decode.cpp:122-190), but
+// each step runs only the newest committed token of every unfinished beam
+// against its cached prefix (M = active beams, not the sum of their lengths).
+// kv.rows[b]: pool rows of beam b's committed positions 0 .. len - 2 (its
+// last committed token is pending); the first step prefills the prompt.
+void constrained_step_kv(const egt_model* model, DecodeSession& s, const PrefixTrie& trie, int beam_size,
+                         KvBeams& kv, void* stream) {
+  require(beam_size >= 1, "decode: beam_size must be positive");
+  check_beams(s, trie);
+  std::vector<size_t> active;
+  for (size_t i = 0; i < s.beams.size(); ++i)
+    if (!trie.is_leaf(s.beams[i].node)) active.push_back(i);
+  require(!active.empty(), "decode: every beam is finished");
+  if (kv.rows.size() != s.beams.size()) kv.rows.assign(s.beams.size(), {});
+  std::vector<int> tokens, positions;
+  std::vector<uint32_t> out_rows, key_ptr{0}, key_rows;
+  std::vector<RowRequest> reqs;
+  std::vector<uint8_t> bits;
+  const bool prefill = active.size() == 1 && kv.rows[active[0]].empty();
+  if (prefill) {  // the whole committed sequence, causal, into the pool
+    const std::vector<int> seq = committed(s, s.beams[active[0]]);
+    const size_t L = seq.size();
+    bits.assign((L * L + 7) / 8, 0);
+    for (size_t q = 0; q < L; ++q) {
+      tokens.push_back(seq[q]);
+      positions.push_back(static_cast<int>(q));
+      out_rows.push_back(kv.next++);
+      for (size_t k = 0; k <= q; ++k) set_bit(bits, q * L + k);
+    }
+    reqs.push_back({static_cast<uint32_t>(L - 1), s.beams[active[0]].node});
+  } else {
+    for (size_t a = 0; a < active.size(); ++a) {
+      const std::vector<int> seq = committed(s, s.beams[active[a]]);
+      const std::vector<uint32_t>& pre = kv.rows[active[a]];
+      require(pre.size() + 1 == seq.size(), "decode: kv cache out of step with the beam");
+      tokens.push_back(seq.back());
+      positions.push_back(static_cast<int>(seq.size() - 1));
+      out_rows.push_back(kv.next++);
+      key_rows.insert(key_rows.end(), pre.begin(), pre.end());
+      key_ptr.push_back(static_cast<uint32_t>(key_rows.size()));
+      reqs.push_back({static_cast<uint32_t>(a), s.beams[active[a]].node});
+    }
+  }
+  require(kv.next <= kv.capacity, "decode: kv pool exhausted");
+  const uint32_t M = static_cast<uint32_t>(tokens.size());
+  const std::vector<std::vector<float>> rows = score_rows_with(
+      trie, M,
+      [&](float* logits) {
+        return egt_forward_kv(model, kv.pool, tokens.data(), positions.data(), M, prefill ? bits.data() : nullptr,
+                              out_rows.data(), prefill ? nullptr : key_ptr.data(), key_rows.data(), logits, stream);
+      },
+      reqs, vocab_of(model), stream);
+  s.forward_passes += 1;
+  if (prefill) {
+    kv.rows[active[0]] = out_rows;
+  } else {
+    for (size_t a = 0; a < active.size(); ++a) kv.rows[active[a]].push_back(out_rows[a]);
+  }
+  struct Cand {
+    double score;
+    size_t beam;
+    uint32_t token;
+    uint32_t child;
+    bool carry;
+  };
+  std::vector<Cand> cands;
+  for (size_t i = 0; i < s.beams.size(); ++i)
+    if (trie.is_leaf(s.beams[i].node)) cands.push_back({s.beams[i].log_prob, i, 0, 0, true});
+  for (size_t a = 0; a < active.size(); ++a) {
+    const BeamHypothesis& b = s.beams[active[a]];
+    const std::vector<uint32_t>& ch = trie.nodes[b.node].children;
+    for (size_t c = 0; c < ch.size(); ++c)
+      cands.push_back({b.log_prob + rows[a][c], active[a], trie.nodes[ch[c]].token, ch[c], false});
+  }
+  std::sort(cands.begin(), cands.end(), [](const Cand& x, const Cand& y) {  // step_candidate_before
+    if (x.score != y.score) return x.score > y.score;
+    if (x.beam != y.beam) return x.beam < y.beam;
+    return x.token < y.token;
+  });
+  std::vector<BeamHypothesis> next;
+  std::vector<std::vector<uint32_t>> next_rows;
+  for (size_t j = 0; j < std::min(static_cast<size_t>(beam_size), cands.size()); ++j) {
+    BeamHypothesis b = s.beams[cands[j].beam];
+    if (!cands[j].carry) {
+      b.tokens.push_back(static_cast<int>(cands[j].token));
+      b.log_prob = cands[j].score;
+      b.node = cands[j].child;
+    }
+    next.push_back(std::move(b));
+    next_rows.push_back(kv.rows[cands[j].beam]);  // shared prefix rows (no copy of the cache itself)
+  }
+  s.beams = std::move(next);
+  kv.rows = std::move(next_rows);
+  s.steps += 1;
+}
+
 TriggerEstimate estimate_trigger(const CostModel& cost, const DecodeSession& s, const PrefixTrie& trie,
                                  size_t node_cap) {
   check_beams(s, trie);
@@ -451,6 +560,18 @@ DecodeResult decode(const egt_model* model, const PrefixTrie& trie, std::vector<
     require(static_cast<int>(trie.nodes[i].token) < vocab, "decode: trie token outside the model vocabulary");
   require(!trie.nodes.empty() && !trie.nodes[0].children.empty(), "decode: trie has no identifiers");
   DecodeSession s = make_session(std::move(prompt));
+  // KV pool: the prompt, then at most one row per beam per step
+  KvBeams kv;
+  std::unique_ptr<egt_kv_pool, egt_status (*)(egt_kv_pool*)> pool(nullptr, egt_kv_pool_destroy);
+  if (opt.kv_cache) {
+    uint32_t depth = 0;
+    for (uint32_t d : trie.max_depth_below) depth = std::max(depth, d);
+    kv.capacity = static_cast<uint32_t>(s.prompt.size()) + (depth + 1) * static_cast<uint32_t>(opt.beam_size) + 1;
+    egt_kv_pool* p = nullptr;
+    check(egt_kv_pool_create(model, kv.capacity, &p));
+    pool.reset(p);
+    kv.pool = p;
+  }
   auto finished = [&] {
     for (const BeamHypothesis& b : s.beams)
       if (!trie.is_leaf(b.node)) return false;
@@ -473,7 +594,10 @@ DecodeResult decode(const egt_model* model, const PrefixTrie& trie, std::vector<
       verified = true;
       break;
     }
-    constrained_step(model, s, trie, opt.beam_size, stream);
+    if (opt.kv_cache)
+      constrained_step_kv(model, s, trie, opt.beam_size, kv, stream);
+    else
+      constrained_step(model, s, trie, opt.beam_size, stream);
   }
   if (!verified)
     for (const BeamHypothesis& b : s.beams) out.sequences.push_back({b.tokens, b.log_prob, trie.nodes[b.node].payload});
@@ -573,6 +697,7 @@ extern "C" EGT_API egt_status egt_decode(const egt_model* m, const egt_trie_view
     o.forced_depth = opt->forced_depth;
     o.cost_model = {opt->t_step, opt->alpha, opt->beta};
     o.node_cap = opt->node_cap;
+    o.kv_cache = opt->kv_cache != 0;
     const egt_b200::DecodeResult r =
         egt_b200::decode(m, t, std::vector<int>(prompt, prompt + prompt_len), o, stream);
     fill_out(out, r.sequences, opt->beam_size);

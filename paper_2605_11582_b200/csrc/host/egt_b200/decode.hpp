@@ -139,6 +139,18 @@ VerificationResult verify_parallel(const egt_model* model, DecodeSession& sessio
 void constrained_step(const egt_model* model, DecodeSession& session, const PrefixTrie& trie, int beam_size,
                       void* stream = nullptr);
 
+// KV-cached variant: the pool keeps every committed
+// row's keys / values; rows[b] lists beam b's cached positions (the beam's
+// last committed token is pending: it runs in the next step).  Same result
+// as constrained_step up to f32 rounding.
+struct KvBeams {
+  egt_kv_pool* pool = nullptr;
+  uint32_t capacity = 0, next = 0;
+  std::vector<std::vector<uint32_t>> rows;
+};
+void constrained_step_kv(const egt_model* model, DecodeSession& session, const PrefixTrie& trie, int beam_size,
+                         KvBeams& kv, void* stream = nullptr);
+
 struct TriggerEstimate {
   bool trigger = false;
   double predicted_saving = 0.0;
@@ -153,6 +165,7 @@ struct DecodeOptions {
   int forced_depth = 0;
   CostModel cost_model;
   size_t node_cap = 4096;
+  bool kv_cache = false;  // constrained steps on the KV pool (constrained_step_kv)
 };
 struct DecodedSequence {
   std::vector<int> tokens;

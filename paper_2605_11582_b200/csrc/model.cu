@@ -230,6 +230,77 @@ __global__ void __launch_bounds__(256) fused_attention_kernel(const float* __res
   }
 }
 
+// KV pool: the keys / values of committed rows persist
+// across the constrained beam steps; a row is written once and shared by
+// every beam whose prefix contains it (beams re-rank by list, never copy).
+// store: pool[l][rows[i]] <- k / v row i of this pass.
+__global__ void kv_store_kernel(const float* __restrict__ k, const float* __restrict__ v, float* kp, float* vp,
+                                const uint32_t* __restrict__ rows, int M, int d) {
+  const int i = blockIdx.x;
+  if (i >= M) return;
+  const size_t dst = static_cast<size_t>(rows[i]) * d, src = static_cast<size_t>(i) * d;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    kp[dst + c] = k[src + c];
+    vp[dst + c] = v[src + c];
+  }
+}
+
+// One query row per block x head: keys / values = pool rows key_rows[
+// key_ptr[i] .. key_ptr[i+1]) (its committed prefix, in position order) then
+// its own row of this pass -- model.cpp:161-184's masked softmax over exactly
+// the causal prefix of that row.  Scores in shared memory.
+__global__ void __launch_bounds__(128) kv_attention_kernel(const float* __restrict__ q, const float* __restrict__ k,
+                                                           const float* __restrict__ v, const float* __restrict__ kp,
+                                                           const float* __restrict__ vp,
+                                                           const uint32_t* __restrict__ key_ptr,
+                                                           const uint32_t* __restrict__ key_rows, float* o, int d,
+                                                           int dh, float scale) {
+  extern __shared__ float sc[];  // [n keys]
+  const int i = blockIdx.x, h = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t k0 = key_ptr[i], n = key_ptr[i + 1] - k0 + 1;
+  const size_t hoff = static_cast<size_t>(h) * dh;
+  const float* qr = q + static_cast<size_t>(i) * d + hoff;
+  // scores: a warp per key, lanes over the head dimension
+  for (uint32_t j = warp; j < n; j += blockDim.x >> 5) {
+    const float* kr = j + 1 < n ? kp + static_cast<size_t>(key_rows[k0 + j]) * d + hoff
+                                : k + static_cast<size_t>(i) * d + hoff;
+    float acc = 0.f;
+    for (int e = lane; e < dh; e += 32) acc = fmaf(qr[e], kr[e], acc);
+    acc = egt_dev::warp_sum(acc);
+    if (lane == 0) sc[j] = acc * scale;
+  }
+  __syncthreads();
+  __shared__ float red[4];
+  float m = -INFINITY;
+  for (uint32_t j = tid; j < n; j += blockDim.x) m = fmaxf(m, sc[j]);
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+  if (lane == 0) red[warp] = m;
+  __syncthreads();
+  m = fmaxf(fmaxf(red[0], red[1]), fmaxf(red[2], red[3]));
+  __syncthreads();
+  float z = 0.f;
+  for (uint32_t j = tid; j < n; j += blockDim.x) {
+    const float e = expf(sc[j] - m);
+    sc[j] = e;
+    z += e;
+  }
+  z = egt_dev::warp_sum(z);
+  if (lane == 0) red[warp] = z;
+  __syncthreads();
+  const float iz = 1.0f / (red[0] + red[1] + red[2] + red[3]);
+  // o = p V: thread per head dimension
+  for (int e = tid; e < dh; e += blockDim.x) {
+    float acc = 0.f;
+    for (uint32_t j = 0; j < n; ++j) {
+      const float* vr = j + 1 < n ? vp + static_cast<size_t>(key_rows[k0 + j]) * d + hoff
+                                  : v + static_cast<size_t>(i) * d + hoff;
+      acc = fmaf(sc[j] * iz, vr[e], acc);
+    }
+    o[static_cast<size_t>(i) * d + hoff + e] = acc;
+  }
+}
+
 __global__ void silu_kernel(float* f, size_t n) {  // model.cpp:80-84
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
@@ -299,9 +370,19 @@ __global__ void tree_mask_kernel(uint32_t* mask, int M, int nb, int lmax, const 
   }
 }
 
+// KV-pool pass: rows of this pass are stored at pool rows out_rows; with
+// key lists (key_ptr != null) the attention of row i reads the pool rows
+// key_rows[key_ptr[i] .. key_ptr[i+1]) then its own row (no M x M mask).
+struct KvPass {
+  egt_kv_pool* pool = nullptr;
+  const uint32_t* out_rows = nullptr;  // host [M]
+  const uint32_t* key_ptr = nullptr;   // host [M + 1] or null
+  const uint32_t* key_rows = nullptr;  // host [key_ptr[M]]
+};
+
 egt_status forward_core(const egt_model* m, const int32_t* tokens, const int32_t* positions,
                         const uint8_t* mask_bits, const egt_tree_view* tree, uint32_t M, float* logits,
-                        void* stream) {
+                        void* stream, const KvPass* kv = nullptr) {
   if (!m || !tokens || !positions || !logits) return fail(EGT_EINVAL, "forward: null argument");
   const egt_model_config& c = m->cfg;
   if (M == 0) return fail(EGT_EINVAL, "forward: empty token sequence");  // model.cpp:123
@@ -316,10 +397,13 @@ egt_status forward_core(const egt_model* m, const int32_t* tokens, const int32_t
   const size_t Md = M * d;
   const size_t mask_bytes = (static_cast<size_t>(M) * M + 31) / 32 * 4;
   const size_t tree_ints = tree ? tree->n_beams + 2ull * tree->n_nodes : 0;
-  const size_t floats = 6 * Md + M * dff + H * static_cast<size_t>(M) * M;
+  const bool gather = kv && kv->key_ptr;
+  const size_t kv_ints = kv ? M + (gather ? M + 1ull + kv->key_ptr[M] : 0) : 0;
+  const size_t floats = 6 * Md + M * dff + (gather ? 0 : H * static_cast<size_t>(M) * M);
   char* scratch = nullptr;
   MCUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch),
-                        floats * sizeof(float) + 2 * M * sizeof(int) + mask_bytes + tree_ints * 4 + 64, s));
+                        floats * sizeof(float) + 2 * M * sizeof(int) + mask_bytes + tree_ints * 4 + kv_ints * 4 + 64,
+                        s));
   float* x = reinterpret_cast<float*>(scratch);
   float* a = x + Md;
   float* q = a + Md;
@@ -328,7 +412,7 @@ egt_status forward_core(const egt_model* m, const int32_t* tokens, const int32_t
   float* o = v + Md;
   float* f1 = o + Md;
   float* S = f1 + M * dff;
-  int* dtok = reinterpret_cast<int*>(S + H * static_cast<size_t>(M) * M);
+  int* dtok = reinterpret_cast<int*>(S + (gather ? 0 : H * static_cast<size_t>(M) * M));
   int* dpos = dtok + M;
   uint8_t* dmask = reinterpret_cast<uint8_t*>(dpos + M);
   egt_status st = EGT_OK;
@@ -351,8 +435,19 @@ egt_status forward_core(const egt_model* m, const int32_t* tokens, const int32_t
                                                    static_cast<int>(tree->n_beams), static_cast<int>(tree->padded_len),
                                                    dcommit, dparent, dbeam);
     ++launch_counter();
-  } else {
+  } else if (mask_bits) {
     cudaMemcpyAsync(dmask, mask_bits, (static_cast<size_t>(M) * M + 7) / 8, cudaMemcpyHostToDevice, s);
+  }
+  uint32_t *d_out_rows = nullptr, *d_key_ptr = nullptr, *d_key_rows = nullptr;
+  if (kv) {
+    d_out_rows = reinterpret_cast<uint32_t*>(dmask + mask_bytes) + tree_ints;
+    cudaMemcpyAsync(d_out_rows, kv->out_rows, M * 4ull, cudaMemcpyHostToDevice, s);
+    if (gather) {
+      d_key_ptr = d_out_rows + M;
+      d_key_rows = d_key_ptr + M + 1;
+      cudaMemcpyAsync(d_key_ptr, kv->key_ptr, (M + 1ull) * 4, cudaMemcpyHostToDevice, s);
+      if (kv->key_ptr[M]) cudaMemcpyAsync(d_key_rows, kv->key_rows, kv->key_ptr[M] * 4ull, cudaMemcpyHostToDevice, s);
+    }
   }
   embed_kernel<<<M, 256, 0, s>>>(dtok, dpos, m->emb, m->pos, x, static_cast<int>(M), static_cast<int>(d));
   ++launch_counter();
@@ -379,8 +474,20 @@ egt_status forward_core(const egt_model* m, const int32_t* tokens, const int32_t
     lin(w[0], a, q, 0);
     lin(w[1], a, k, EGT_SPMV_INDEPENDENT);  // K and V read `a`, not the previous product
     lin(w[2], a, v, EGT_SPMV_INDEPENDENT);
+    if (kv) {  // this pass's keys / values into the pool (the rows later passes attend to)
+      const size_t lo = static_cast<size_t>(l) * kv->pool->capacity * d;
+      kv_store_kernel<<<M, 256, 0, s>>>(k, v, kv->pool->k + lo, kv->pool->v + lo, d_out_rows, static_cast<int>(M),
+                                        static_cast<int>(d));
+      ++launch_counter();
+    }
     // scores per head: S[h] = (q_h k_h^T) * scale
-    if (fused_attn) {
+    if (gather) {
+      const size_t lo = static_cast<size_t>(l) * kv->pool->capacity * d;
+      kv_attention_kernel<<<dim3(M, H), 128, (c.max_positions + 1) * sizeof(float), s>>>(
+          q, k, v, kv->pool->k + lo, kv->pool->v + lo, d_key_ptr, d_key_rows, o, static_cast<int>(d),
+          static_cast<int>(dh), att_scale);
+      ++launch_counter();
+    } else if (fused_attn) {
       fused_attention_kernel<<<dim3((M + kAttnRows - 1) / kAttnRows, H), 256, attn_smem, s>>>(
           q, k, v, o, dmask, static_cast<int>(M), static_cast<int>(d), static_cast<int>(dh), att_scale);
       ++launch_counter();
@@ -528,6 +635,53 @@ egt_status egt_forward_tree(const egt_model* m, const int32_t* tokens, const int
   return forward_core(m, tokens, positions, nullptr, t, static_cast<uint32_t>(M64), logits, stream);
 }
 
+
+egt_status egt_kv_pool_create(const egt_model* m, uint32_t capacity, egt_kv_pool** out) {
+  if (!m || !out || capacity == 0) return fail(EGT_EINVAL, "kv pool: null argument or zero capacity");
+  *out = nullptr;
+  const size_t floats = static_cast<size_t>(m->cfg.n_layers) * capacity * m->cfg.d_model;
+  auto p = new egt_kv_pool();
+  p->capacity = capacity;
+  p->d = m->cfg.d_model;
+  p->layers = m->cfg.n_layers;
+  if (cudaMalloc(&p->k, floats * sizeof(float)) != cudaSuccess ||
+      cudaMalloc(&p->v, floats * sizeof(float)) != cudaSuccess) {
+    cudaFree(p->k);
+    delete p;
+    return fail(EGT_ECUDA, "kv pool: device allocation failed");
+  }
+  *out = p;
+  return EGT_OK;
+}
+
+egt_status egt_kv_pool_destroy(egt_kv_pool* p) {
+  if (p) {
+    cudaFree(p->k);
+    cudaFree(p->v);
+    delete p;
+  }
+  return EGT_OK;
+}
+
+egt_status egt_forward_kv(const egt_model* m, egt_kv_pool* pool, const int32_t* tokens, const int32_t* positions,
+                          uint32_t M, const uint8_t* mask_bits, const uint32_t* out_rows, const uint32_t* key_ptr,
+                          const uint32_t* key_rows, float* logits, void* stream) {
+  if (!m || !pool || !out_rows || (!mask_bits && !key_ptr)) return fail(EGT_EINVAL, "forward kv: null argument");
+  if (pool->d != m->cfg.d_model || pool->layers != m->cfg.n_layers)
+    return fail(EGT_EINVAL, "forward kv: pool built for another model");
+  for (uint32_t i = 0; i < M; ++i) {
+    if (out_rows[i] >= pool->capacity) return fail(EGT_EINVAL, "forward kv: pool row out of range");
+    if (key_ptr) {
+      if (key_ptr[i + 1] < key_ptr[i]) return fail(EGT_EINVAL, "forward kv: key lists must be ascending ranges");
+      if (key_ptr[i + 1] - key_ptr[i] >= m->cfg.max_positions)
+        return fail(EGT_EINVAL, "forward kv: prefix longer than max_positions");
+      for (uint32_t j = key_ptr[i]; j < key_ptr[i + 1]; ++j)
+        if (key_rows[j] >= pool->capacity) return fail(EGT_EINVAL, "forward kv: pool row out of range");
+    }
+  }
+  KvPass kv{pool, out_rows, key_ptr, key_rows};
+  return forward_core(m, tokens, positions, key_ptr ? nullptr : mask_bits, nullptr, M, logits, stream, &kv);
+}
 
 egt_status egt_gather(const float* src, uint64_t ld, const uint32_t* rows, const uint32_t* cols,
                       uint32_t n, float* out, void* stream) {

@@ -15,3 +15,10 @@ struct egt_model {
   int device = 0;
 };
 
+// Keys / values of committed rows, [n_layers][capacity][d_model] each.
+struct egt_kv_pool {
+  float* k = nullptr;
+  float* v = nullptr;
+  uint32_t capacity = 0, d = 0, layers = 0;
+};
+

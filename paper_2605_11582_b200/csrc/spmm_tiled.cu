@@ -172,8 +172,54 @@ __device__ __noinline__ float nonfinite_terms(const TiledArgs& a, int row, int t
   return add;
 }
 
+// One token's window staged again with the window scale 2^e (the optimistic
+// unscaled staging found its range unsuitable): the single-token B layout,
+// pair (k, k+1) at window offset w of k-tile kt -> reg = w / 8, t = (w % 8) / 2.
+template <bool FUSED>
+__device__ __noinline__ void restage_window(const TiledArgs& a, uint32_t* sB, int m0, int kq0, int KTc, float inv,
+                                            uint32_t* s_mx, uint32_t* s_nf, float* s_unsc) {
+  const float* xb = a.x + static_cast<size_t>(m0) * a.ldx + kq0 * 128;
+  const int nwin = min(KTc * 32, a.cols - kq0 * 128);
+  uint32_t mx = 0u, nf = 0u;
+  for (int k = threadIdx.x; k < nwin; k += blockDim.x) {
+    float xv = xb[k];
+    if (FUSED && a.xform == EGT_INPUT_RMSNORM) xv *= inv;
+    else if (FUSED && a.xform == EGT_INPUT_SILU) xv = silu2(make_float2(xv, 0.f)).x;
+    xr_note(mx, nf, xv);
+  }
+  xr_commit(mx, nf, s_mx, s_nf);
+  __syncthreads();
+  const int e = xr_exp(*s_mx);
+  const float sc = xr_pow2(e);
+  if (threadIdx.x == 0) *s_unsc = xr_pow2(-e);
+  for (int p = threadIdx.x; p < KTc * 16; p += blockDim.x) {  // pairs of the window
+    const int k = 2 * p;
+    float x0 = 0.f, x1 = 0.f;
+    if (k < nwin) {
+      x0 = xb[k];
+      x1 = xb[k + 1];
+      if (FUSED && a.xform == EGT_INPUT_RMSNORM) {
+        x0 *= inv;
+        x1 *= inv;
+      } else if (FUSED && a.xform == EGT_INPUT_SILU) {
+        const float2 q = silu2(make_float2(x0, x1));
+        x0 = q.x;
+        x1 = q.y;
+      }
+    }
+    x0 = xr_scaled(x0, sc);
+    x1 = xr_scaled(x1, sc);
+    const __half h0 = __float2half_rn(x0), h1 = __float2half_rn(x1);
+    const __half l0 = __float2half_rn(x0 - __half2float(h0)), l1 = __float2half_rn(x1 - __half2float(h1));
+    const int kt = k >> 5, w = k & 31, reg = w >> 3, t = (w & 7) >> 1;
+    uint32_t* row = sB + static_cast<size_t>(kt) * 32;
+    row[t * 4 + reg] = static_cast<uint32_t>(__half_as_ushort(h0)) | (static_cast<uint32_t>(__half_as_ushort(h1)) << 16);
+    row[(4 + t) * 4 + reg] = static_cast<uint32_t>(__half_as_ushort(l0)) | (static_cast<uint32_t>(__half_as_ushort(l1)) << 16);
+  }
+}
+
 template <int FMT, int SS, int NT, bool SINGLE, bool FUSED>
-__global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(const TiledArgs a) {
+__global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(const __grid_constant__ TiledArgs a) {
   constexpr int E = 4 / SS;
   constexpr int TOK = 4 * NT;
   constexpr int VB = val_lane_bytes(FMT), MB = meta_lane_bytes(FMT);
@@ -219,8 +265,11 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
   uint8_t* stages = reinterpret_cast<uint8_t*>(sB + NT * KTc * LS * 4);
   float* red = reinterpret_cast<float*>(stages + static_cast<size_t>(NST) * sbytes);  // [RB][nw][Mc][16]
   // per token of the CTA: x window range (xrange.cuh) and the 2^-e rescale
-  __shared__ uint32_t s_xmx[16], s_xnf[16];
-  __shared__ float s_unsc[16];
+  // (static shared memory is kept minimal: independent launches pack several
+  // CTAs per SM, and 128 more bytes per CTA measured -23 % on the sweep)
+  constexpr int kTokS = SINGLE ? 1 : TOK;
+  __shared__ uint32_t s_xmx[kTokS], s_xnf[kTokS];
+  __shared__ float s_unsc[kTokS];
 
   if (tid == 0) {
     for (int s = 0; s < NST; ++s) {
@@ -229,7 +278,7 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
     }
     mbar_fence_init();
   }
-  if (tid < 16) {
+  if (tid < kTokS) {
     s_xmx[tid] = 0u;
     s_xnf[tid] = 0u;
     s_unsc[tid] = 1.f;
@@ -299,8 +348,8 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
   constexpr int XU = EGT_XU;
   // rmsnorm (model.cpp:57-67): inv_m = 1 / sqrt(mean(x_m^2) + eps) over the
   // whole row of every token of this CTA, applied while converting
-  __shared__ float s_inv[16];
-  __shared__ float s_red[32];
+  __shared__ float s_inv[kTokS];
+  __shared__ float s_red[FUSED ? 16 : 1];  // rmsnorm: one partial per warp (<= 13 warps)
   // residual rows of this CTA fetched now, not after the compute (decode:
   // the O / ff2 products); one output per thread when the CTA is small
   float res_pre = 0.f;
@@ -310,6 +359,8 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
     if (row < a.rows) res_pre = a.res[static_cast<size_t>(m0 + tl) * a.ldr + row];
   }
   bool staged = false;
+  bool optimistic = false;  // x staged unscaled; the range is checked at the barrier
+  uint32_t xbits = 0u;      // max |x| bits of this thread's share (optimistic staging)
   if constexpr (SINGLE) {
     // One token: each thread loads contiguous float4s of the CTA's x slice
     // (coalesced, trivial addressing) and scatters the two (k, k+1) pairs of
@@ -366,34 +417,19 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
         }
         return q;
       };
-      // window range (xrange.cuh): from the registers in one pass, else a
-      // separate read of the window
-      {
-        uint32_t mx = 0u, nf = 0u;
-        if (one_pass) {
-#pragma unroll
-          for (int u = 0; u < X4; ++u) {
-            v[u] = xform4(v[u]);
-            xr_note(mx, nf, v[u].x); xr_note(mx, nf, v[u].y); xr_note(mx, nf, v[u].z); xr_note(mx, nf, v[u].w);
-          }
-        } else {
-          for (int j = tid; j < nf4; j += blockDim.x) {
-            if (4 * j < nwin) {
-              const float4 q = xform4(__ldg(reinterpret_cast<const float4*>(xb) + j));
-              xr_note(mx, nf, q.x); xr_note(mx, nf, q.y); xr_note(mx, nf, q.z); xr_note(mx, nf, q.w);
-            }
-          }
-        }
-        xr_commit(mx, nf, s_xmx, s_xnf);
-        if (tid == 0) s_inv[0] = inv;
-        __syncthreads();
-      }
-      const int xe = xr_exp(s_xmx[0]);
-      const float xsc = xr_pow2(xe);
-      if (tid == 0) s_unsc[0] = xr_pow2(-xe);
-      auto pair = [xsc](float p0, float p1) {
-        p0 = xr_scaled(p0, xsc);
-        p1 = xr_scaled(p1, xsc);
+      // Optimistic range (xrange.cuh): x is converted unscaled right away
+      // while each thread keeps max |x| bits; the barrier that ends staging
+      // anyway ORs two predicates over the CTA.  Scale 1 is kept when the
+      // window has no |x| >= 2^15 (nor inf / NaN) and some |x| >= 2^-3: no
+      // overflow, and every value down to 2^-22 of the window max splits
+      // as exactly as under the window scale.  Any other window is staged
+      // again with its 2^e (restage_window).  A CTA-wide max in front of the
+      // conversion measured +0.2 us per call: x staging is on the critical
+      // path.
+      optimistic = true;
+      if (tid == 0) s_inv[0] = inv;
+      auto pair = [&xbits](float p0, float p1) {
+        xbits = max(xbits, max(__float_as_uint(p0) & 0x7fffffffu, __float_as_uint(p1) & 0x7fffffffu));
         const __half h0 = __float2half_rn(p0), h1 = __float2half_rn(p1);
         const __half l0 = __float2half_rn(p0 - __half2float(h0));
         const __half l1 = __float2half_rn(p1 - __half2float(h1));
@@ -413,7 +449,7 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
         for (int u = 0; u < X4; ++u) {
           const int j = base + tid + u * static_cast<int>(blockDim.x);
           if (j < nf4) {
-            const float4 q = one_pass ? v[u] : xform4(v[u]);  // one pass: transformed above
+            const float4 q = xform4(v[u]);
             const int kt = j >> 3, w = (j & 7) * 4, reg = w >> 3, t = (w & 7) >> 1;
             uint32_t* row = sB + static_cast<size_t>(kt) * 32;
             const uint2 a0 = pair(q.x, q.y), a1 = pair(q.z, q.w);
@@ -573,7 +609,14 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
       }
     }
   }
-  __syncthreads();
+  const int x_big = __syncthreads_or(xbits >= 0x47000000u);  // some |x| >= 2^15, inf or NaN
+  if (SINGLE && optimistic) {
+    const int x_mid = __syncthreads_or(xbits >= 0x3e000000u);  // some |x| >= 2^-3
+    if (x_big || !x_mid) {
+      restage_window<FUSED>(a, sB, m0, kq0, KTc, s_inv[0], s_xmx, s_xnf, s_unsc);
+      __syncthreads();
+    }
+  }
   if (tr && cta0) tr[2] = gtimer();
 
   if (warp == nw) {

@@ -126,7 +126,7 @@ __device__ __noinline__ float wide_nonfinite_terms(const WideArgs& a, int row, i
 }
 
 template <int FMT, int SS, int NW>
-__global__ void __launch_bounds__(32 * (NW + 1), 1) wide_spmm_kernel(const WideArgs a) {
+__global__ void __launch_bounds__(32 * (NW + 1), 1) wide_spmm_kernel(const __grid_constant__ WideArgs a) {
   constexpr int E = 4 / SS;
   constexpr int VB = val_lane_bytes(FMT), MB = meta_lane_bytes(FMT);
   extern __shared__ __align__(128) uint8_t smem_raw[];

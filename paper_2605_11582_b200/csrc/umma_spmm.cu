@@ -966,14 +966,18 @@ cudaError_t launch_umma(const egt_dev_packed* h, const float* x, int ldx, int M,
   a.pad14 = h->tiled.pad14;
   a.raw_rt_bytes = raw_rt_bytes(h->format, h->tiled.E);
   a.trace = umma_trace_buffer();
+  void* fn = pick_umma(h->format);
+  cudaFuncAttributes fa{};
+  cudaError_t err = cudaFuncGetAttributes(&fa, fn);
+  if (err != cudaSuccess) return err;
+  const size_t budget = 227 * 1024 - fa.sharedSizeBytes;  // dynamic + static shared memory per block
   const size_t x_bytes = static_cast<size_t>(a.N) * kStageK * 2;
   const bool sparse_path = h->format != I4_DENSE && getenv("EGT_UMMA_DENSE") == nullptr;
   const size_t fixed = 2048 + kNA * (sparse_path ? 8192 : 16384) + kNR * 8 * static_cast<size_t>(a.raw_rt_bytes);
-  a.NX = static_cast<int>(std::min<size_t>(kMaxNX, (227 * 1024 - fixed) / x_bytes));
+  a.NX = fixed < budget ? static_cast<int>(std::min<size_t>(kMaxNX, (budget - fixed) / x_bytes)) : 0;
   if (a.NX < 2) return cudaErrorInvalidConfiguration;
   const size_t smem = fixed + a.NX * x_bytes;
-  void* fn = pick_umma(h->format);
-  cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (err != cudaSuccess) return err;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((h->tiled.RT + 7) / 8, p.TT, p.S);

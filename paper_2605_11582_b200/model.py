@@ -146,12 +146,13 @@ class DeviceModel:
         return _read_out(o, arrs, stride), {"flattened_nodes": o.flattened_nodes, "rows": o.rows}
 
     def decode(self, trie: Trie, prompt, beam_size=4, mode="ptpv", forced_depth=0, cost=(0.0, 0.0, 0.0),
-               node_cap=4096, stream=None):
-        """decode (decode.cpp:423-483); mode: autoregressive | ptpv | forced."""
+               node_cap=4096, kv_cache=False, stream=None):
+        """decode (decode.cpp:423-483); mode: autoregressive | ptpv | forced.
+        kv_cache: constrained steps on a KV pool (one new row per beam per step)."""
         tv = trie.view()
         pr = np.ascontiguousarray(prompt, np.int32)
         m = {"autoregressive": 0, "ptpv": 1, "forced": 2}[mode]
-        opt = DecodeOptions(beam_size, m, forced_depth, cost[0], cost[1], cost[2], node_cap)
+        opt = DecodeOptions(beam_size, m, forced_depth, cost[0], cost[1], cost[2], node_cap, 1 if kv_cache else 0)
         stride = 64
         o, arrs = _verify_out(beam_size, stride)
         stats = (C.c_int32 * 4)()

@@ -86,7 +86,7 @@ class VerifyOut(C.Structure):
 
 class DecodeOptions(C.Structure):
     _fields_ = [("beam_size", C.c_int), ("mode", C.c_int), ("forced_depth", C.c_int), ("t_step", C.c_double),
-                ("alpha", C.c_double), ("beta", C.c_double), ("node_cap", C.c_uint64)]
+                ("alpha", C.c_double), ("beta", C.c_double), ("node_cap", C.c_uint64), ("kv_cache", C.c_int)]
 
 
 INPUT_NONE, INPUT_RMSNORM, INPUT_SILU = 0, 1, 2
@@ -142,6 +142,11 @@ _MODEL_SIGNATURES = {
                                       C.POINTER(VerifyOut), C.c_void_p]),
     "egt_decode": (C.c_int, [C.c_void_p, C.POINTER(TrieView), C.POINTER(C.c_int32), C.c_uint32,
                              C.POINTER(DecodeOptions), C.POINTER(VerifyOut), C.POINTER(C.c_int32), C.c_void_p]),
+    "egt_kv_pool_create": (C.c_int, [C.c_void_p, C.c_uint32, C.POINTER(C.c_void_p)]),
+    "egt_kv_pool_destroy": (C.c_int, [C.c_void_p]),
+    "egt_forward_kv": (C.c_int, [C.c_void_p, C.c_void_p, C.POINTER(C.c_int32), C.POINTER(C.c_int32), C.c_uint32,
+                                 C.POINTER(C.c_uint8), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
+                                 C.POINTER(C.c_uint32), C.c_void_p, C.c_void_p]),
 }
 
 

@@ -272,3 +272,52 @@ def test_cost_model_from_device_timings(model_pair):
     assert (st["trigger_step"] == 0) == fire
     assert sorted(tuple(s["tokens"]) for s in got) == sorted(tuple(s["tokens"]) for s in ar)
     assert np.allclose(sorted(s["score"] for s in got), sorted(s["score"] for s in ar), atol=1e-4)
+
+
+@pytest.mark.parametrize("beam", [1, 3, 8])
+def test_kv_cached_beam_decode_matches_reference(port, beam):
+    """The KV-cached trie-constrained beam step (SURVEY 8(f) row 1,
+    constrained_step_kv: one new row per beam per step against its cached
+    prefix) against the REFERENCE's full-recompute decode (decode.cpp:122-190,
+    423-483, oracle/_ref) on the dense reconstructions of the same layers:
+    the same sequences, payloads and step counts, scores within 1e-4; and the
+    same as the product's own full-recompute steps."""
+    import os
+
+    from oracle.oracle import REF_LIB
+
+    if not os.path.exists(REF_LIB):
+        pytest.skip("oracle/_ref not built")
+    from oracle.ref_model import RefModel
+    from paper_2605_11582_b200.model import DeviceModel, compress_layer
+
+    rng = np.random.default_rng(40 + beam)
+    cfg = dict(vocab_size=64, d_model=128, n_layers=2, n_heads=4, d_ff=256, max_positions=64)
+    d, dff, V = cfg["d_model"], cfg["d_ff"], cfg["vocab_size"]
+    b = 1.0 / np.sqrt(d)
+    emb = rng.uniform(-b, b, (V, d)).astype(np.float32)
+    shapes = [(d, d)] * 4 + [(dff, d), (d, dff)]
+    handles, dense = [], []
+    for li in range(cfg["n_layers"]):
+        layer = {}
+        for part, shape, kind in zip(("wq", "wk", "wv", "wo", "ff1", "ff2"), shapes, PLAN[li % len(PLAN)]):
+            w = rng.uniform(-b, b, shape).astype(np.float32)
+            h, art = compress_layer(w, kind, 32)
+            handles.append(h)
+            layer[part] = _dense_of(port, art)
+        dense.append(layer)
+    hw = rng.uniform(-b, b, (V, d)).astype(np.float32)
+    head, hart = compress_layer(hw, "int4-2:4", 32)
+    model = DeviceModel(cfg, emb, handles, head)
+    model._keep = handles
+    ref = RefModel(cfg, emb, dense, _dense_of(port, hart))
+    trie = random_trie(rng, depth=4, lo=2, hi=4)
+    prompt = [1, 17, 5, 33, 9]
+    got, gst = model.decode(trie, prompt, beam, mode="autoregressive", kv_cache=True)
+    full, fst = model.decode(trie, prompt, beam, mode="autoregressive")
+    want, wst = ref.decode(trie, prompt, beam, mode="autoregressive")
+    assert gst == fst and gst["steps"] == wst["steps"] and gst["forward_passes"] == wst["forward_passes"]
+    for g, f, w in zip(got, full, want):
+        assert g["tokens"] == f["tokens"] == w["tokens"] and g["payload"] == w["payload"]
+        assert abs(g["score"] - w["score"]) <= 1e-4 and abs(g["score"] - f["score"]) <= 1e-4
+    assert len(got) == len(want)
