@@ -172,49 +172,53 @@ __device__ __noinline__ float nonfinite_terms(const TiledArgs& a, int row, int t
   return add;
 }
 
-// One token's window staged again with the window scale 2^e (the optimistic
-// unscaled staging found its range unsuitable): the single-token B layout,
-// pair (k, k+1) at window offset w of k-tile kt -> reg = w / 8, t = (w % 8) / 2.
+// One token's window staged again with its window scale 2^e (the optimistic
+// unscaled staging found the range unsuitable): the window's finite max and
+// non-finite flag into s_mx / s_nf (zero on entry), 2^-e into s_unsc, and
+// the B fragments of token slot (nt, m): pair (k, k+1) at window offset
+// 32 kt + 8 reg + 2 t.
 template <bool FUSED>
-__device__ __noinline__ void restage_window(const TiledArgs& a, uint32_t* sB, int m0, int kq0, int KTc, float inv,
-                                            uint32_t* s_mx, uint32_t* s_nf, float* s_unsc) {
-  const float* xb = a.x + static_cast<size_t>(m0) * a.ldx + kq0 * 128;
-  const int nwin = min(KTc * 32, a.cols - kq0 * 128);
+__device__ __noinline__ void restage_token(const TiledArgs& a, uint32_t* sB, int tok, int nt, int m, int kq0,
+                                           int KTc, int LS, float inv, uint32_t* s_mx, uint32_t* s_nf,
+                                           float* s_unsc) {
+  const float* xr = a.x + static_cast<size_t>(tok) * a.ldx;
+  auto xform = [&](float2 q) {
+    if (FUSED && a.xform == EGT_INPUT_RMSNORM) {
+      q.x *= inv;
+      q.y *= inv;
+    } else if (FUSED && a.xform == EGT_INPUT_SILU) {
+      q = silu2(q);
+    }
+    return q;
+  };
+  const int items = KTc * 16;
   uint32_t mx = 0u, nf = 0u;
-  for (int k = threadIdx.x; k < nwin; k += blockDim.x) {
-    float xv = xb[k];
-    if (FUSED && a.xform == EGT_INPUT_RMSNORM) xv *= inv;
-    else if (FUSED && a.xform == EGT_INPUT_SILU) xv = silu2(make_float2(xv, 0.f)).x;
-    xr_note(mx, nf, xv);
+  for (int i = threadIdx.x; i < items; i += blockDim.x) {
+    const int k = kq0 * 128 + i * 2;
+    if (k < a.cols) {
+      const float2 q = xform(make_float2(xr[k], xr[k + 1]));
+      xr_note(mx, nf, q.x);
+      xr_note(mx, nf, q.y);
+    }
   }
   xr_commit(mx, nf, s_mx, s_nf);
   __syncthreads();
   const int e = xr_exp(*s_mx);
   const float sc = xr_pow2(e);
   if (threadIdx.x == 0) *s_unsc = xr_pow2(-e);
-  for (int p = threadIdx.x; p < KTc * 16; p += blockDim.x) {  // pairs of the window
-    const int k = 2 * p;
-    float x0 = 0.f, x1 = 0.f;
-    if (k < nwin) {
-      x0 = xb[k];
-      x1 = xb[k + 1];
-      if (FUSED && a.xform == EGT_INPUT_RMSNORM) {
-        x0 *= inv;
-        x1 *= inv;
-      } else if (FUSED && a.xform == EGT_INPUT_SILU) {
-        const float2 q = silu2(make_float2(x0, x1));
-        x0 = q.x;
-        x1 = q.y;
-      }
-    }
-    x0 = xr_scaled(x0, sc);
-    x1 = xr_scaled(x1, sc);
+  for (int i = threadIdx.x; i < items; i += blockDim.x) {
+    const int reg = i & 3, t = (i >> 2) & 3, kt = i >> 4;
+    const int k = (kq0 * 4 + kt) * 32 + 2 * t + 8 * reg;
+    float2 q = make_float2(0.f, 0.f);
+    if (k < a.cols) q = xform(make_float2(xr[k], xr[k + 1]));
+    const float x0 = xr_scaled(q.x, sc), x1 = xr_scaled(q.y, sc);
     const __half h0 = __float2half_rn(x0), h1 = __float2half_rn(x1);
     const __half l0 = __float2half_rn(x0 - __half2float(h0)), l1 = __float2half_rn(x1 - __half2float(h1));
-    const int kt = k >> 5, w = k & 31, reg = w >> 3, t = (w & 7) >> 1;
-    uint32_t* row = sB + static_cast<size_t>(kt) * 32;
-    row[t * 4 + reg] = static_cast<uint32_t>(__half_as_ushort(h0)) | (static_cast<uint32_t>(__half_as_ushort(h1)) << 16);
-    row[(4 + t) * 4 + reg] = static_cast<uint32_t>(__half_as_ushort(l0)) | (static_cast<uint32_t>(__half_as_ushort(l1)) << 16);
+    uint32_t* row = sB + static_cast<size_t>(nt * KTc + kt) * LS * 4;
+    row[(8 * m + t) * 4 + reg] =
+        static_cast<uint32_t>(__half_as_ushort(h0)) | (static_cast<uint32_t>(__half_as_ushort(h1)) << 16);
+    row[(8 * m + 4 + t) * 4 + reg] =
+        static_cast<uint32_t>(__half_as_ushort(l0)) | (static_cast<uint32_t>(__half_as_ushort(l1)) << 16);
   }
 }
 
@@ -270,6 +274,7 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
   constexpr int kTokS = SINGLE ? 1 : TOK;
   __shared__ uint32_t s_xmx[kTokS], s_xnf[kTokS];
   __shared__ float s_unsc[kTokS];
+  __shared__ uint32_t s_rng[2];  // several tokens: per-token masks of the optimistic range check
 
   if (tid == 0) {
     for (int s = 0; s < NST; ++s) {
@@ -278,6 +283,7 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
     }
     mbar_fence_init();
   }
+  if (tid < 2) s_rng[tid] = 0u;
   if (tid < kTokS) {
     s_xmx[tid] = 0u;
     s_xnf[tid] = 0u;
@@ -359,8 +365,22 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
     if (row < a.rows) res_pre = a.res[static_cast<size_t>(m0 + tl) * a.ldr + row];
   }
   bool staged = false;
-  bool optimistic = false;  // x staged unscaled; the range is checked at the barrier
-  uint32_t xbits = 0u;      // max |x| bits of this thread's share (optimistic staging)
+  // Optimistic range (xrange.cuh): every staging path converts x unscaled
+  // right away and notes, per token slot, whether this thread saw a value
+  // >= 2^15 (or inf / NaN) and one >= 2^-3; the barrier that ends staging
+  // anyway combines them.  A token keeps scale 1 when its window has no
+  // |x| >= 2^15 and some |x| >= 2^-3: no overflow, and every value down to
+  // 2^-22 of the window max splits as exactly as under the window scale.
+  // Any other token is staged again with its 2^e (restage_token).  A
+  // separate range pass (or a CTA-wide max) in front of the conversion
+  // measured +0.2 us per call: x staging is on the critical path.
+  uint32_t xbig = 0u, xmid = 0u;  // bit tl: this thread's share of token slot tl
+  uint32_t xbits = 0u;            // max |x| bits of the current token's share
+  auto note_token = [&](int tl) {
+    xbig |= static_cast<uint32_t>(xbits >= 0x47000000u) << tl;
+    xmid |= static_cast<uint32_t>(xbits >= 0x3e000000u) << tl;
+    xbits = 0u;
+  };
   if constexpr (SINGLE) {
     // One token: each thread loads contiguous float4s of the CTA's x slice
     // (coalesced, trivial addressing) and scatters the two (k, k+1) pairs of
@@ -417,16 +437,6 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
         }
         return q;
       };
-      // Optimistic range (xrange.cuh): x is converted unscaled right away
-      // while each thread keeps max |x| bits; the barrier that ends staging
-      // anyway ORs two predicates over the CTA.  Scale 1 is kept when the
-      // window has no |x| >= 2^15 (nor inf / NaN) and some |x| >= 2^-3: no
-      // overflow, and every value down to 2^-22 of the window max splits
-      // as exactly as under the window scale.  Any other window is staged
-      // again with its 2^e (restage_window).  A CTA-wide max in front of the
-      // conversion measured +0.2 us per call: x staging is on the critical
-      // path.
-      optimistic = true;
       if (tid == 0) s_inv[0] = inv;
       auto pair = [&xbits](float p0, float p1) {
         xbits = max(xbits, max(__float_as_uint(p0) & 0x7fffffffu, __float_as_uint(p1) & 0x7fffffffu));
@@ -460,6 +470,7 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
           }
         }
       }
+      note_token(0);
       staged = true;
     }
   }
@@ -489,26 +500,14 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
       float tot = 0.f;
       for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) tot += s_red[w];
       const float inv = 1.0f / sqrtf(tot / static_cast<float>(a.cols) + a.eps);
-      uint32_t mx = 0u, nf = 0u;
-#pragma unroll
-      for (int u = 0; u < XU; ++u) {
-        v[u].x *= inv;
-        v[u].y *= inv;
-        xr_note(mx, nf, v[u].x);
-        xr_note(mx, nf, v[u].y);
-      }
-      xr_commit(mx, nf, s_xmx, s_xnf);
       if (tid == 0) s_inv[0] = inv;
-      __syncthreads();
-      const int xe = xr_exp(s_xmx[0]);
-      const float xsc = xr_pow2(xe);
-      if (tid == 0) s_unsc[0] = xr_pow2(-xe);
 #pragma unroll
       for (int u = 0; u < XU; ++u) {
         const int i = tid + u * blockDim.x;
         if (i < items) {
           const int reg = i & 3, t = (i >> 2) & 3, kt = i >> 4;
-          const float x0 = xr_scaled(v[u].x, xsc), x1 = xr_scaled(v[u].y, xsc);
+          const float x0 = v[u].x * inv, x1 = v[u].y * inv;
+          xbits = max(xbits, max(__float_as_uint(x0) & 0x7fffffffu, __float_as_uint(x1) & 0x7fffffffu));
           const __half h0 = __float2half_rn(x0), h1 = __float2half_rn(x1);
           const __half l0 = __float2half_rn(x0 - __half2float(h0));
           const __half l1 = __float2half_rn(x1 - __half2float(h1));
@@ -519,6 +518,7 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
                                    (static_cast<uint32_t>(__half_as_ushort(l1)) << 16);
         }
       }
+      note_token(0);
       staged = true;
     }
   }
@@ -541,31 +541,12 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
       __syncthreads();
     }
   }
-  if (!staged && a.dbg != 3) {
-    // window range per token (xrange.cuh): one read of each token's window
-    const int k1 = min(a.cols, (kq0 + KCs) * 128);
-    for (int tl = 0; tl < Mc; ++tl) {
-      const float* xr = a.x + static_cast<size_t>(m0 + tl) * a.ldx;
-      const float inv = FUSED && a.xform == EGT_INPUT_RMSNORM ? s_inv[tl] : 1.f;
-      uint32_t mx = 0u, nf = 0u;
-      for (int k = kq0 * 128 + tid; k < k1; k += blockDim.x) {
-        float xv = __ldg(xr + k);
-        if (FUSED && a.xform == EGT_INPUT_RMSNORM) xv *= inv;
-        else if (FUSED && a.xform == EGT_INPUT_SILU) xv = silu2(make_float2(xv, 0.f)).x;
-        xr_note(mx, nf, xv);
-      }
-      xr_commit(mx, nf, s_xmx + tl, s_xnf + tl);
-    }
-    __syncthreads();
-    if (tid < Mc) s_unsc[tid] = xr_pow2(-xr_exp(s_xmx[tid]));
-  }
 #pragma unroll
   for (int nt = 0; nt < NT; ++nt) {
     const int mc = (a.dbg == 3 || staged) ? 0 : min(4, Mc - 4 * nt);
     for (int m = 0; m < mc; ++m) {
       const float* xr = a.x + static_cast<size_t>(m0 + 4 * nt + m) * a.ldx;
       const float inv = FUSED && a.xform == EGT_INPUT_RMSNORM ? s_inv[4 * nt + m] : 1.f;
-      const float xsc = xr_pow2(xr_exp(s_xmx[4 * nt + m]));
       const int items = KTc * 16;
       for (int i0 = 0; i0 < items; i0 += XU * static_cast<int>(blockDim.x)) {
         float2 v[XU];
@@ -594,8 +575,7 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
             } else if (FUSED && a.xform == EGT_INPUT_SILU) {
               v[u] = silu2(v[u]);
             }
-            v[u].x = xr_scaled(v[u].x, xsc);
-            v[u].y = xr_scaled(v[u].y, xsc);
+            xbits = max(xbits, max(__float_as_uint(v[u].x) & 0x7fffffffu, __float_as_uint(v[u].y) & 0x7fffffffu));
             const __half h0 = __float2half_rn(v[u].x), h1 = __float2half_rn(v[u].y);
             const __half l0 = __float2half_rn(v[u].x - __half2float(h0));
             const __half l1 = __float2half_rn(v[u].y - __half2float(h1));
@@ -607,15 +587,30 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
           }
         }
       }
+      note_token(4 * nt + m);
     }
   }
-  const int x_big = __syncthreads_or(xbits >= 0x47000000u);  // some |x| >= 2^15, inf or NaN
-  if (SINGLE && optimistic) {
-    const int x_mid = __syncthreads_or(xbits >= 0x3e000000u);  // some |x| >= 2^-3
-    if (x_big || !x_mid) {
-      restage_window<FUSED>(a, sB, m0, kq0, KTc, s_inv[0], s_xmx, s_xnf, s_unsc);
-      __syncthreads();
+  // the range check at the end-of-staging barrier (see note_token)
+  uint32_t restage = 0u;  // token slots to stage again (CTA-uniform)
+  if constexpr (SINGLE) {
+    const int any_big = __syncthreads_or(xbig & 1u);
+    const int any_mid = __syncthreads_or(xmid & 1u);
+    restage = (a.dbg != 3 && (any_big || !any_mid)) ? 1u : 0u;
+  } else {
+    const uint32_t big = __reduce_or_sync(0xffffffffu, xbig), mid = __reduce_or_sync(0xffffffffu, xmid);
+    if (lane == 0 && (big | mid)) {
+      atomicOr(s_rng, big);
+      atomicOr(s_rng + 1, mid);
     }
+    __syncthreads();
+    if (a.dbg != 3) restage = (s_rng[0] | ~s_rng[1]) & ((1u << Mc) - 1u);
+  }
+  if (restage) {
+    for (int tl = 0; tl < Mc; ++tl)
+      if ((restage >> tl) & 1u)
+        restage_token<FUSED>(a, sB, m0 + tl, tl >> 2, tl & 3, kq0, KTc, LS, s_inv[tl], s_xmx + tl, s_xnf + tl,
+                             s_unsc + tl);
+    __syncthreads();
   }
   if (tr && cta0) tr[2] = gtimer();
 
