@@ -230,6 +230,144 @@ __global__ void __launch_bounds__(256) fused_attention_kernel(const float* __res
   }
 }
 
+// The same masked attention for 32 query rows per block, the head's keys
+// and values streamed through shared memory in double-buffered chunks of 32
+// rows (cp.async, zero-filled past M): scores s[r][j] (phase 1, thread = key
+// of the chunk x 4 rows), the exact two-pass masked softmax per row (phase
+// 2, as above), o = p V (phase 3, thread = float4 column x 4 rows).  256
+// threads, two blocks per SM; smem: q [32][dh + 4], scores [32][ldp], K / V
+// chunks 2 x [32][dh + 4].
+// The 16-row kernel above re-read every key row from L2 per (row, key) pair
+// and ran latency-bound (152 us per layer at M = 272, dh = 128).
+constexpr int kAttnRows2 = 32, kAttnKeys = 32;
+__host__ __device__ inline size_t attn2_smem(int M, int dh) {
+  const int ldp = (M + kAttnKeys - 1) / kAttnKeys * kAttnKeys;
+  return (static_cast<size_t>(kAttnRows2) * (dh + 4) + static_cast<size_t>(kAttnRows2) * ldp +
+          2 * static_cast<size_t>(kAttnKeys) * (dh + 4)) * sizeof(float);
+}
+__device__ __forceinline__ void cp_async16(float* dst, const float* src, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(egt_dev::smem_u32(dst)), "l"(src),
+               "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+
+__global__ void __launch_bounds__(256) attention_tile_kernel(const float* __restrict__ q, const float* __restrict__ k,
+                                                             const float* __restrict__ v, float* __restrict__ o,
+                                                             const uint8_t* __restrict__ mask, int M, int d, int dh,
+                                                             float scale) {
+  extern __shared__ __align__(16) float sm[];
+  const int ldq = dh + 4, ldp = (M + kAttnKeys - 1) / kAttnKeys * kAttnKeys, n4 = dh / 4;
+  float* qs = sm;                     // [32][dh + 4]
+  float* ps = qs + kAttnRows2 * ldq;  // [32][ldp]
+  float* kb = ps + kAttnRows2 * ldp;  // 2 x [32][dh + 4]
+  const int q0 = blockIdx.x * kAttnRows2, h = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nr = min(kAttnRows2, M - q0);
+  const size_t hoff = static_cast<size_t>(h) * dh;
+  const int nchunk = (M + kAttnKeys - 1) / kAttnKeys;
+  // chunk c of keys (src = k) or values (src = v) into buffer c & 1
+  auto stage = [&](const float* src, int c) {
+    float* dst = kb + (c & 1) * kAttnKeys * ldq;
+    for (int f = tid; f < kAttnKeys * n4; f += blockDim.x) {
+      const int key = f / n4, e4 = f % n4, kk = c * kAttnKeys + key;
+      cp_async16(dst + key * ldq + 4 * e4, src + static_cast<size_t>(kk < M ? kk : 0) * d + hoff + 4 * e4, kk < M);
+    }
+    cp_async_commit();
+  };
+  stage(k, 0);
+  for (int f = tid; f < kAttnRows2 * n4; f += blockDim.x) {
+    const int r = f / n4, e4 = f % n4;
+    cp_async16(qs + r * ldq + 4 * e4, q + static_cast<size_t>(r < nr ? q0 + r : q0) * d + hoff + 4 * e4, r < nr);
+  }
+  cp_async_commit();
+  // ---- phase 1: scores; thread -> key `lane` of the chunk, rows 4 warp .. 4 warp + 3
+  for (int c = 0; c < nchunk; ++c) {
+    if (c + 1 < nchunk) stage(k, c + 1); else cp_async_commit();
+    cp_async_wait1();  // chunk c (and q) landed
+    __syncthreads();
+    const float* ks = kb + (c & 1) * kAttnKeys * ldq;
+    float acc[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) acc[i] = 0.f;
+    const float4* kr = reinterpret_cast<const float4*>(ks + lane * ldq);
+#pragma unroll 4
+    for (int e4 = 0; e4 < n4; ++e4) {
+      const float4 b = kr[e4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float4 a = *reinterpret_cast<const float4*>(qs + (4 * warp + i) * ldq + 4 * e4);
+        acc[i] = fmaf(a.x, b.x, fmaf(a.y, b.y, fmaf(a.z, b.z, fmaf(a.w, b.w, acc[i]))));
+      }
+    }
+    const int kk = c * kAttnKeys + lane;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int r = 4 * warp + i;
+      const size_t bit = static_cast<size_t>(q0 + r) * M + kk;
+      const bool vis = r < nr && kk < M && ((mask[bit >> 3] >> (bit & 7)) & 1);
+      ps[r * ldp + kk] = vis ? acc[i] * scale : -INFINITY;
+    }
+    __syncthreads();  // buffer c & 1 free for chunk c + 2
+  }
+  stage(v, 0);  // values stream in while the softmax runs
+  // ---- phase 2: masked softmax, one warp per row (an empty row -> 0)
+  for (int r = warp; r < kAttnRows2; r += blockDim.x >> 5) {
+    float* pr = ps + r * ldp;
+    float m = -INFINITY;
+    for (int j = lane; j < M; j += 32) m = fmaxf(m, pr[j]);
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, off));
+    if (!isfinite(m)) {  // no visible key: zero attention output (model.cpp:173)
+      for (int j = lane; j < ldp; j += 32) pr[j] = 0.f;
+      continue;
+    }
+    float z = 0.f;
+    for (int j = lane; j < M; j += 32) {
+      const float e = pr[j] == -INFINITY ? 0.f : expf(pr[j] - m);
+      pr[j] = e;
+      z += e;
+    }
+    z = egt_dev::warp_sum(z);
+    const float iz = 1.0f / z;
+    for (int j = lane; j < ldp; j += 32) pr[j] = j < M ? pr[j] * iz : 0.f;
+  }
+  // ---- phase 3: o = p V; thread -> float4 column e4, rows 4 rg .. 4 rg + 3
+  const int items = (kAttnRows2 / 4) * n4;
+  const int e4 = tid % n4, rg = tid / n4;
+  float4 acc[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int c = 0; c < nchunk; ++c) {
+    if (c + 1 < nchunk) stage(v, c + 1); else cp_async_commit();
+    cp_async_wait1();
+    __syncthreads();  // chunk c landed; scores final
+    if (tid < items) {
+      const float* vs = kb + (c & 1) * kAttnKeys * ldq;
+      const float* pc = ps + (4 * rg) * ldp + c * kAttnKeys;
+#pragma unroll 4
+      for (int j = 0; j < kAttnKeys; ++j) {  // keys past M: zero values and zero p
+        const float4 vv = *reinterpret_cast<const float4*>(vs + j * ldq + 4 * e4);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float p = pc[i * ldp + j];
+          acc[i].x = fmaf(p, vv.x, acc[i].x);
+          acc[i].y = fmaf(p, vv.y, acc[i].y);
+          acc[i].z = fmaf(p, vv.z, acc[i].z);
+          acc[i].w = fmaf(p, vv.w, acc[i].w);
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (tid < items) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (4 * rg + i < nr)
+        reinterpret_cast<float4*>(o + static_cast<size_t>(q0 + 4 * rg + i) * d + hoff)[e4] = acc[i];
+  }
+}
+
 // KV pool: the keys / values of committed rows persist
 // across the constrained beam steps; a row is written once and shared by
 // every beam whose prefix contains it (beams re-rank by list, never copy).
@@ -466,6 +604,14 @@ egt_status forward_core(const egt_model* m, const int32_t* tokens, const int32_t
   if (fused_attn && attn_smem > 48 * 1024)
     MCUDA(cudaFuncSetAttribute(fused_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(attn_smem)));
+  // the 64-row staged kernel where its tiles fit (dh <= 128)
+  static const bool old_attn = getenv("EGT_ATTN16") != nullptr;
+  const size_t attn2 = attn2_smem(static_cast<int>(M), static_cast<int>(dh));
+  const bool tile_attn = !no_fused && !old_attn && dh % 4 == 0 && dh / 4 <= 256 / (kAttnRows2 / 4) &&
+                         attn2 <= 200 * 1024;
+  if (tile_attn && attn2 > 48 * 1024)
+    MCUDA(cudaFuncSetAttribute(attention_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(attn2)));
   const dim3 tb(16, 16);
   for (uint32_t l = 0; l < c.n_layers && st == EGT_OK; ++l) {
     const egt_dev_packed* const* w = m->layers.data() + 6 * l;
@@ -486,6 +632,10 @@ egt_status forward_core(const egt_model* m, const int32_t* tokens, const int32_t
       kv_attention_kernel<<<dim3(M, H), 128, (c.max_positions + 1) * sizeof(float), s>>>(
           q, k, v, kv->pool->k + lo, kv->pool->v + lo, d_key_ptr, d_key_rows, o, static_cast<int>(d),
           static_cast<int>(dh), att_scale);
+      ++launch_counter();
+    } else if (tile_attn) {
+      attention_tile_kernel<<<dim3((M + kAttnRows2 - 1) / kAttnRows2, H), 256, attn2, s>>>(
+          q, k, v, o, dmask, static_cast<int>(M), static_cast<int>(d), static_cast<int>(dh), att_scale);
       ++launch_counter();
     } else if (fused_attn) {
       fused_attention_kernel<<<dim3((M + kAttnRows - 1) / kAttnRows, H), 256, attn_smem, s>>>(

@@ -58,7 +58,16 @@ constexpr int kDeqWarp0 = 2, kNumDeq = 8, kDeqGroup = 4, kEpiWarp0 = 10, kNumEpi
 constexpr int kStageK = 64;  // K per A / B stage: four K = 16 MMAs
 // k-quads per packed-weight (raw) stage (FP16 blocks are 4.5x larger)
 __host__ __device__ constexpr int raw_kq(int fmt) { return fmt == egt_fmt::F16_SP24 ? 1 : 2; }
-constexpr int kNA = 4, kNR = 3, kMaxNX = 10;  // ring depths (x: runtime, <= kMaxNX)
+// ring depths: raw weight stages kNR; A stages and x stages runtime (a.NA,
+// a.NX).  The A ring spans the MMA -> commit -> dequantiser -> MMA round
+// trip (~2 us measured with EGT_UMMA_TRACE): 4 slots capped the kernel at
+// ~0.5 us per stage whatever the work.
+constexpr int kNR = 3, kMaxNA = 12, kMaxNX = 10;
+// scale hand-off ring (rounds): the dequantisers run up to kMaxNA stages
+// (= rounds at 64-column groups) ahead of the MMA, the epilogue up to two
+// rounds behind it
+constexpr int kScaleRing = 16;
+static_assert(kScaleRing > kMaxNA + 2, "scale ring too shallow");
 // tokens per tile: a tcgen05.mma costs ~170 cycles to issue whatever its N
 // (measured, tools/micro/umma_rate.cu), so each MMA takes the tile's hi AND lo
 // halves (N = 2T <= 192); two accumulator buffers + the metadata ring fit
@@ -70,6 +79,7 @@ struct UmmaArgs {
   // metadata, zero points; box = one raw stage of 8 row tiles
   CUtensorMap tm_vals, tm_meta, tm_zps, tm_scales;
   int NX;  // x ring depth
+  int NA;  // A ring depth
   const uint8_t* vals;
   const uint8_t* meta;
   const float* scales;
@@ -98,6 +108,7 @@ struct UmmaArgs {
   // [1] past alloc, [8+st] x issued, [80+st] MMA issued, [160+st] stage
   // dequantised (warp 2), [240+r] round folded (warp 6), [320+rs] raw issued
   unsigned long long* trace;
+  int dbg;  // tuning (EGT_UMMA_DBG): 1 dequantisers skip the A writes, 2 epilogue skips TMEM loads, 4 no MMAs
 };
 
 __device__ __forceinline__ unsigned long long umma_clock() {
@@ -285,9 +296,10 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const __grid_con
   uint64_t* raw_full = bars;
   uint64_t* raw_empty = raw_full + kNR;
   uint64_t* a_full = raw_empty + kNR;
-  uint64_t* a_empty = a_full + kNA;
+  const int kNA = a.NA;
+  uint64_t* a_empty = a_full + kMaxNA;
   const int kNX = a.NX;
-  uint64_t* x_full = a_empty + kNA;
+  uint64_t* x_full = a_empty + kMaxNA;
   uint64_t* x_empty = x_full + kMaxNX;
   uint64_t* tm_full = x_empty + kMaxNX;
   uint64_t* tm_empty = tm_full + 2;
@@ -295,6 +307,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const __grid_con
   __shared__ int s_last;
   __shared__ float s_unsc[kMaxT];
   __shared__ uint32_t s_nonf[kMaxT];
+  __shared__ int s_anynf;  // some token of the tile has a non-finite x
   // swizzle atoms need 1024-byte aligned tiles
   uint8_t* smem_al = smem_raw + ((1024 - (smem_addr(smem_raw) & 1023)) & 1023);
   uint8_t* a_st = smem_al + 1024;  // kNA x 16 KB
@@ -306,12 +319,13 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const __grid_con
   constexpr int VBq = kRawKQ * 32 * VB, MBq = kRawKQ * 32 * MB;
   const int ZBq = kScaled ? kRawKQ * a.E * 16 : 0, SBq = kScaled ? kRawKQ * a.E * 64 : 0;
   // the scales of the epilogue's rounds, handed over by the dequantisers
-  // (ring of 8 rounds; ordered by a_full -> MMA -> tm_full)
-  __shared__ float s_scale[8 * 128];
+  // (ring of kScaleRing rounds; ordered by a_full -> MMA -> tm_full)
+  __shared__ float s_scale[kScaleRing * 128];
   const uint32_t raw_bytes = 8 * a.raw_rt_bytes;
   const uint32_t raw_s0 = smem_addr(raw_st);
 
   if (tid == 0) {
+    s_anynf = 0;
     for (int i = 0; i < kNR; ++i) {
       mbar_init(raw_full + i, 1);
       mbar_init(raw_empty + i, kNumDeq);
@@ -396,7 +410,8 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const __grid_con
         const uint32_t abase = smem_addr(a_st + (st % kNA) * kASlot);
         const uint32_t bbase = smem_addr(x_st + (st % kNX) * x_bytes);
         const uint32_t d = tmem + static_cast<uint32_t>(buf * N);
-        if constexpr (SPARSE) {  // two K = 32 (logical) sparse MMAs per stage, x hi and lo
+        if (a.dbg & 4) {
+        } else if constexpr (SPARSE) {  // two K = 32 (logical) sparse MMAs per stage, x hi and lo
 #pragma unroll
           for (int jj = 0; jj < 2; ++jj) {
             const uint64_t ad = umma_desc_sw(abase + jj * 32, 64);
@@ -456,6 +471,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const __grid_con
       const uint32_t abase = smem_addr(a_st + sa * kASlot);
 #pragma unroll
       for (int ii = 0; ii < 2; ++ii) {
+      if (a.dbg & 1) break;
       const int i = 2 * dq + ii;  // row tile within the CTA
       if (rt0 + i >= a.RT) {  // past the matrix: zero rows
         for (int w = lane; w < (SPARSE ? 64 : 128); w += 32) {  // 16 rows x 4 / 8 chunks
@@ -529,7 +545,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const __grid_con
       if (kScaled && (a.SS == 2 || hs == 0)) {  // this round's scales of row tiles 2 dq, 2 dq + 1
         const int e = a.SS == 2 ? hs : 0, i = 2 * dq + (lane >> 4), l16 = lane & 15;
         const uint32_t sb = rbase + 8 * (VBq + MBq + ZBq) + i * SBq + b * a.E * 64;
-        s_scale[((st / steps_per_scale) & 7) * 128 + i * 16 + l16] =
+        s_scale[((st / steps_per_scale) % kScaleRing) * 128 + i * 16 + l16] =
             __uint_as_float(lds_u32(sb + (e * 16 + 2 * (l16 & 7) + (l16 >> 3)) * 4));
       }
       fence_async_smem();  // generic-proxy writes -> visible to the tensor core
@@ -552,15 +568,27 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const __grid_con
     for (int k = 0; k < kMaxT / 2; ++k) acc[k] = 0.f;
     const uint32_t lane_base = tmem + (static_cast<uint32_t>(32 * q) << 16);
     const bool row_ok = grow < a.rows && (rt0 + (r >> 4)) < a.RT;
+    // x scales / non-finite flags (the xprep kernel) and, below, residual
+    // rows belong to earlier kernels: wait now, while the first round runs
+    pdl_wait();
+    {
+      const int ew = (warp - kEpiWarp0) * 32 + lane;
+      if (ew < T) {
+        const int tok = min(tile * T + ew, a.TTpad - 1);
+        s_unsc[ew] = a.unsc[tok];
+        s_nonf[ew] = a.nonfin[tok];
+        if (s_nonf[ew]) s_anynf = 1;
+      }
+    }
     for (int round = 0; round < NROUND; ++round) {
       const int buf = kScaled ? (round & 1) : 0;
       mbar_wait_sleep(tm_full + buf, kScaled ? ((round >> 1) & 1) : 0);
       tc_fence_after();
-      const float s = kScaled ? s_scale[(round & 7) * 128 + r] : 1.f;  // the row's scale of this round
+      const float s = kScaled ? s_scale[(round % kScaleRing) * 128 + r] : 1.f;  // the row's scale of this round
       // chunks of 16 tokens: their hi and lo columns in flight together, one wait
 #pragma unroll
       for (int cb = 0; cb < (kMaxT / 2 + 15) / 16; ++cb) {
-        if (cb * 16 < th) {
+        if (cb * 16 < th && !(a.dbg & 2)) {
           uint32_t vh[16], vl[16];
           const uint32_t col = lane_base + static_cast<uint32_t>(buf * N + c0 + cb * 16);
           tmem_ld8_nowait(col, vh);
@@ -583,103 +611,126 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const __grid_con
     }
     // ---- outputs: rescale (xrange.cuh), fix-up; then residual / silu and the
     // store (one CTA), or the cluster's split-K sum (below)
-    pdl_wait();  // residual rows / x scales belong to earlier kernels
-    const int ew = (warp - kEpiWarp0) * 32 + lane;
-    if (ew < T) {
-      const int tok = min(tile * T + ew, a.TTpad - 1);
-      s_unsc[ew] = a.unsc[tok];
-      s_nonf[ew] = a.nonfin[tok];
-    }
-    asm volatile("bar.sync 1, %0;\n" ::"n"(kNumEpi * 32) : "memory");  // epilogue warps only
-    const int kc0 = kq0 * 128, kc1 = min(a.cols, (kq0 + KQC) * 128);
+    if (tr && lane == 0) tr[800 + warp - kEpiWarp0] = umma_clock();
+    asm volatile("bar.sync 1, %0;\n" ::"n"(kNumEpi * 32) : "memory");  // s_unsc / s_nonf written
+    // The accumulators, times the tokens' 2^-e (xrange.cuh), into shared
+    // memory (the x ring is idle now): row-major, tokens contiguous, PT = T + 4
+    // (conflict-free float4s).  Straight-line code run once per CTA is kept
+    // short -- its instruction fetches are cold (an unrolled per-token tail
+    // measured 3.4 us).
+    float* part = reinterpret_cast<float*>(x_st);
+    {
+      float* pr = part + r * (T + 4) + c0;
 #pragma unroll
-    for (int k = 0; k < kMaxT / 2; ++k) {
-      if (k < th) {
-        const int tl = c0 + k, tok = tile * T + tl;
-        float val = acc[k] * s_unsc[tl];
-        if (row_ok && tok < a.M && s_nonf[tl]) val += umma_nonfinite_terms<FMT>(a, grow, tok, kc0, kc1);
-        acc[k] = val;
-      }
-    }
-    if (a.S > 1) {  // this slice's partials -> own shared memory (the x ring is idle now)
-      float* part = reinterpret_cast<float*>(x_st);
-#pragma unroll
-      for (int k = 0; k < kMaxT / 2; ++k)
-        if (k < th) part[(c0 + k) * 128 + r] = acc[k];
-    }
-    if (a.S == 1 && row_ok) {
-      // 8 tokens at a time: residuals first (they may alias y), all in flight
-#pragma unroll
-      for (int k0 = 0; k0 < kMaxT / 2; k0 += 8) {
-        if (k0 < th) {
-          float rv[8];
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int tok = tile * T + c0 + k0 + u;
-            rv[u] = (a.res && k0 + u < th && tok < a.M) ? a.res[static_cast<size_t>(tok) * a.ldr + grow] : 0.f;
-          }
-#pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            const int tok = tile * T + c0 + k0 + u;
-            if (k0 + u < th && tok < a.M) {
-              float o = rv[u] + acc[k0 + u];
-              if (a.out_silu) o = o * (1.0f / (1.0f + expf(-o)));  // model.cpp:80-84
-              a.y[static_cast<size_t>(tok) * a.ldy + grow] = o;
-            }
-          }
+      for (int k = 0; k < kMaxT / 2; k += 4)
+        if (k < th) {
+          const float4 u = *reinterpret_cast<const float4*>(s_unsc + c0 + k);
+          *reinterpret_cast<float4*>(pr + k) = make_float4(acc[k] * u.x, acc[k + 1] * u.y, acc[k + 2] * u.z, acc[k + 3] * u.w);
         }
+    }
+    if (s_anynf) {  // non-finite x somewhere in the tile: exact fix-up, token by token
+      const int kc0 = kq0 * 128, kc1 = min(a.cols, (kq0 + KQC) * 128);
+      for (int k = 0; k < th; ++k) {
+        const int tl = c0 + k, tok = tile * T + tl;
+        if (row_ok && tok < a.M && s_nonf[tl])
+          part[r * (T + 4) + tl] += umma_nonfinite_terms<FMT>(a, grow, tok, kc0, kc1);
       }
     }
+    if (tr && lane == 0) tr[840 + warp - kEpiWarp0] = umma_clock();
   }
 
   // ---- teardown: TMEM back; split K: the cluster's leader sums the slices'
   // partials from their shared memory (DSMEM) in slice order -- deterministic
+  if (tr && tid == kEpiWarp0 * 32) tr[2] = umma_clock();
+  if (tr && warp >= kEpiWarp0 && warp < kEpiWarp0 + kNumEpi && lane == 0) tr[820 + warp - kEpiWarp0] = umma_clock();
   tc_fence_before();
   __syncthreads();
+  if (tr && tid == 0) tr[3] = umma_clock();
   tc_fence_after();
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "n"(tmem_cols) : "memory");
   pdl_launch_dependents();
-  if (a.S == 1) return;
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
-  if (blockIdx.z == 0 && warp >= kEpiWarp0 && warp < kEpiWarp0 + kNumEpi) {
-    const int q = warp & 3, half = (warp - kEpiWarp0) >> 2;
-    const int r = 32 * q + lane, grow = rt0 * 16 + r;
-    const int th = T / 2, c0 = half * th;
-    if (grow < a.rows && (rt0 + (r >> 4)) < a.RT) {
-      const uint32_t part0 = smem_addr(x_st);
-      for (int k0 = 0; k0 < th; k0 += 8) {  // 8 tokens at a time
-        float sum[8], rv[8];
+  if (a.S > 1)
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  if (tr && tid == 0) tr[4] = umma_clock();
+  // each slice reduces a 1/S share of the token groups (4 tokens) for all
+  // 128 rows: the S partials in slice order (deterministic), float4 DSMEM
+  // loads all in flight, then residual / silu and the store (S = 1: this
+  // CTA's own rows, consecutive threads on consecutive rows)
+  if (warp >= kEpiWarp0 && warp < kEpiWarp0 + kNumEpi) {
+    const int PT = T + 4, G4 = T / 4, per = (G4 + a.S - 1) / a.S;
+    const int g0 = blockIdx.z * per, g1 = min(G4, g0 + per);
+    const uint32_t part0 = smem_addr(x_st);
+    constexpr int kB = 2;  // items per thread in flight: all their S DSMEM loads issued before any use
+    const int nit = (g1 - g0) * 128;
+    for (int it0 = (warp - kEpiWarp0) * 32 + lane; it0 < nit; it0 += kB * kNumEpi * 32) {
+      float4 sum[kB], rv[kB], v[kB][8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          sum[u] = 0.f;
-          const int tok = tile * T + c0 + k0 + u;
-          rv[u] = (a.res && k0 + u < th && tok < a.M) ? a.res[static_cast<size_t>(tok) * a.ldr + grow] : 0.f;
-        }
-        for (int z = 0; z < a.S; ++z) {
-          uint32_t remote;
-          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(remote) : "r"(part0), "r"(z));
+      for (int b = 0; b < kB; ++b) {
+        const int it = min(it0 + b * kNumEpi * 32, nit - 1);
+        const int r = it & 127, gq = g0 + (it >> 7);
+        const uint32_t off = static_cast<uint32_t>((r * PT + 4 * gq) * 4);
 #pragma unroll
-          for (int u = 0; u < 8; ++u) {
-            float v;
-            asm volatile("ld.shared::cluster.f32 %0, [%1];\n" : "=f"(v) : "r"(remote + ((c0 + k0 + u) * 128 + r) * 4));
-            sum[u] += v;
+        for (int z = 0; z < 8; ++z) {
+          if (z < a.S) {
+            uint32_t remote;
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(remote) : "r"(part0 + off), "r"(z));
+            asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+                         : "=f"(v[b][z].x), "=f"(v[b][z].y), "=f"(v[b][z].z), "=f"(v[b][z].w)
+                         : "r"(remote));
           }
         }
+      }
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int tok = tile * T + c0 + k0 + u;
-          if (k0 + u < th && tok < a.M) {
-            float o = rv[u] + sum[u];
-            if (a.out_silu) o = o * (1.0f / (1.0f + expf(-o)));
+      for (int b = 0; b < kB; ++b) {
+        const int it = it0 + b * kNumEpi * 32;
+        sum[b] = make_float4(0.f, 0.f, 0.f, 0.f);
+        rv[b] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (it >= nit) continue;
+        const int r = it & 127, gq = g0 + (it >> 7), grow = rt0 * 16 + r;
+#pragma unroll
+        for (int z = 0; z < 8; ++z) {  // slice order
+          if (z < a.S) {
+            sum[b].x += v[b][z].x;
+            sum[b].y += v[b][z].y;
+            sum[b].z += v[b][z].z;
+            sum[b].w += v[b][z].w;
+          }
+        }
+        if (a.res && grow < a.rows) {
+          const int tok = tile * T + 4 * gq;
+          const float* rp = a.res + static_cast<size_t>(tok) * a.ldr + grow;
+          rv[b].x = tok < a.M ? rp[0] : 0.f;
+          rv[b].y = tok + 1 < a.M ? rp[a.ldr] : 0.f;
+          rv[b].z = tok + 2 < a.M ? rp[2 * static_cast<size_t>(a.ldr)] : 0.f;
+          rv[b].w = tok + 3 < a.M ? rp[3 * static_cast<size_t>(a.ldr)] : 0.f;
+        }
+      }
+      if (tr && tid == kEpiWarp0 * 32 && it0 == lane) tr[7] = umma_clock();
+#pragma unroll
+      for (int b = 0; b < kB; ++b) {
+        const int it = it0 + b * kNumEpi * 32;
+        if (it >= nit) continue;
+        const int r = it & 127, gq = g0 + (it >> 7), grow = rt0 * 16 + r;
+        if (grow >= a.rows || (rt0 + (r >> 4)) >= a.RT) continue;
+        const float o4[4] = {rv[b].x + sum[b].x, rv[b].y + sum[b].y, rv[b].z + sum[b].z, rv[b].w + sum[b].w};
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int tok = tile * T + 4 * gq + u;
+          if (tok < a.M) {
+            float o = o4[u];
+            if (a.out_silu) o = o * (1.0f / (1.0f + expf(-o)));  // model.cpp:80-84
             a.y[static_cast<size_t>(tok) * a.ldy + grow] = o;
           }
         }
       }
     }
   }
+  if (tr && tid == kEpiWarp0 * 32) tr[5] = umma_clock();
+  if (a.S == 1) return;
   // every slice's shared memory stays alive until the leader has read it
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+  if (tr && tid == 0) tr[6] = umma_clock();
 }
 
 // X [M x cols] -> B stages: per token tile, per 64-column k-stage, N = 2T rows
@@ -966,6 +1017,8 @@ cudaError_t launch_umma(const egt_dev_packed* h, const float* x, int ldx, int M,
   a.pad14 = h->tiled.pad14;
   a.raw_rt_bytes = raw_rt_bytes(h->format, h->tiled.E);
   a.trace = umma_trace_buffer();
+  static const int udbg = getenv("EGT_UMMA_DBG") ? atoi(getenv("EGT_UMMA_DBG")) : 0;
+  a.dbg = udbg;
   void* fn = pick_umma(h->format);
   cudaFuncAttributes fa{};
   cudaError_t err = cudaFuncGetAttributes(&fa, fn);
@@ -973,10 +1026,25 @@ cudaError_t launch_umma(const egt_dev_packed* h, const float* x, int ldx, int M,
   const size_t budget = 227 * 1024 - fa.sharedSizeBytes;  // dynamic + static shared memory per block
   const size_t x_bytes = static_cast<size_t>(a.N) * kStageK * 2;
   const bool sparse_path = h->format != I4_DENSE && getenv("EGT_UMMA_DENSE") == nullptr;
-  const size_t fixed = 2048 + kNA * (sparse_path ? 8192 : 16384) + kNR * 8 * static_cast<size_t>(a.raw_rt_bytes);
-  a.NX = fixed < budget ? static_cast<int>(std::min<size_t>(kMaxNX, (budget - fixed) / x_bytes)) : 0;
-  if (a.NX < 2) return cudaErrorInvalidConfiguration;
-  const size_t smem = fixed + a.NX * x_bytes;
+  const size_t a_bytes = sparse_path ? 8192 : 16384;
+  const size_t fixed = 2048 + kNR * 8 * static_cast<size_t>(a.raw_rt_bytes);
+  // x stages first (a few suffice: the x producer runs ahead), then the A
+  // ring as deep as the rest allows
+  static const int nx_env = getenv("EGT_UMMA_NX") ? atoi(getenv("EGT_UMMA_NX")) : 0;
+  static const int na_env = getenv("EGT_UMMA_NA") ? atoi(getenv("EGT_UMMA_NA")) : 0;
+  // split K: the x ring also holds the slice's partials, 128 x (T + 4) f32
+  const int nx_min = p.S > 1 ? static_cast<int>((512 * static_cast<size_t>(p.T + 4) + x_bytes - 1) / x_bytes) : 2;
+  a.NX = std::max(nx_min, nx_env > 0 ? std::min(nx_env, kMaxNX) : 4);
+  const long room = static_cast<long>(budget) - static_cast<long>(fixed + a.NX * x_bytes);
+  a.NA = room > 0 ? static_cast<int>(std::min<long>(kMaxNA, room / static_cast<long>(a_bytes))) : 0;
+  if (na_env > 0) a.NA = std::min(a.NA, na_env);
+  if (a.NA < 2) {  // huge token tiles: fewer x stages
+    a.NX = std::max(nx_min, 2);
+    const long room2 = static_cast<long>(budget) - static_cast<long>(fixed + a.NX * x_bytes);
+    a.NA = room2 > 0 ? static_cast<int>(std::min<long>(kMaxNA, room2 / static_cast<long>(a_bytes))) : 0;
+  }
+  if (a.NA < 2) return cudaErrorInvalidConfiguration;
+  const size_t smem = fixed + a.NA * a_bytes + a.NX * x_bytes;
   err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (err != cudaSuccess) return err;
   cudaLaunchConfig_t cfg = {};

@@ -43,5 +43,11 @@ for st in range(0, 72):
     print(f"stage {st:2d}: x {us(t[8 + st]):>6} | deq2 a_empty {us(t[640 + st]):>6} raw {us(t[720 + st]):>6} "
           f"done {us(t[160 + st]):>6} | deq9 done {us(t[480 + st]):>6} | mma tm_empty {us(t[560 + st]):>6} "
           f"a_full {us(t[400 + st]):>6} issued {us(t[80 + st]):>6}")
+print(f"outputs done {us(t[2])}, teardown barrier {us(t[3])}, cluster barrier {us(t[4])}, loads {us(t[7])}, leader sum {us(t[5])}, "
+      f"end {us(t[6])}")
+print("epilogue warps: rounds done", [us(v) for v in t[800:808]], "\n  past bar", [us(v) for v in t[810:818]],
+      "\n  partials", [us(v) for v in t[840:848]],
+      "\n  outputs", [us(v) for v in t[820:828]])
+print("reduce pass starts", us(t[900]), us(t[901]))
 print("raw issued:", [us(v) for v in t[320:340] if v])
 print("epilogue rounds:", [us(v) for v in t[240:280] if v])
