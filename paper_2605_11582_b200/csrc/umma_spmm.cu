@@ -62,12 +62,12 @@ __host__ __device__ constexpr int raw_kq(int fmt) { return fmt == egt_fmt::F16_S
 // a.NX).  The A ring spans the MMA -> commit -> dequantiser -> MMA round
 // trip (~2 us measured with EGT_UMMA_TRACE): 4 slots capped the kernel at
 // ~0.5 us per stage whatever the work.
-constexpr int kNR = 3, kMaxNA = 12, kMaxNX = 10;
+constexpr int kNR = 3, kMaxNA = 6, kMaxNX = 6;
 // scale hand-off ring (rounds): the dequantisers run up to kMaxNA stages
 // (= rounds at 64-column groups) ahead of the MMA, the epilogue up to two
 // rounds behind it
 constexpr int kScaleRing = 16;
-static_assert(kScaleRing > kMaxNA + 2, "scale ring too shallow");
+static_assert(kScaleRing > 2 * kMaxNA + 2, "scale ring too shallow");
 // tokens per tile: a tcgen05.mma costs ~170 cycles to issue whatever its N
 // (measured, tools/micro/umma_rate.cu), so each MMA takes the tile's hi AND lo
 // halves (N = 2T <= 192); two accumulator buffers + the metadata ring fit
@@ -224,6 +224,19 @@ __device__ __forceinline__ uint4 lds_v4(uint32_t addr) {
   asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
   return v;
 }
+// Non-suspending probe of an mbarrier phase.  Any mbarrier probe costs
+// ~220 cycles of latency (measured in the MMA loop, clock64): the MMA thread
+// probes the next stage's barriers before issuing this stage's MMAs and
+// commits, and only blocks when a probe said "not yet".
+__device__ __forceinline__ uint32_t mbar_probe(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok;
+}
 // mbarrier wait that sleeps between probes (the epilogue waits a whole scale
 // step: polling would steal issue slots from the dequantisers)
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
@@ -312,9 +325,13 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const __grid_con
   uint8_t* smem_al = smem_raw + ((1024 - (smem_addr(smem_raw) & 1023)) & 1023);
   uint8_t* a_st = smem_al + 1024;  // kNA x 16 KB
   constexpr uint32_t kASlot = SPARSE ? 8192 : 16384;
-  uint8_t* x_st = a_st + kNA * kASlot;  // kNX x (N x 128 B)
+  // ring slots hold one k-quad = two 64-column sub-stages: every mbarrier
+  // probe / tcgen05.commit in the MMA thread's chain costs ~100-220 cycles
+  // (clock64, EGT_UMMA_TRACE), so the chain runs once per k-quad, not per
+  // sub-stage
+  uint8_t* x_st = a_st + kNA * 2 * kASlot;  // kNX x 2 x (N x 128 B)
   const uint32_t x_bytes = static_cast<uint32_t>(N) * kStageK * 2;
-  uint8_t* raw_st = x_st + kNX * x_bytes;  // kNR x (8 x raw_rt_bytes)
+  uint8_t* raw_st = x_st + kNX * 2 * x_bytes;  // kNR x (8 x raw_rt_bytes)
   // raw stage: [values 8 x VBq][metadata 8 x MBq][zero points 8 x ZBq][scales 8 x SBq]
   constexpr int VBq = kRawKQ * 32 * VB, MBq = kRawKQ * 32 * MB;
   const int ZBq = kScaled ? kRawKQ * a.E * 16 : 0, SBq = kScaled ? kRawKQ * a.E * 64 : 0;
@@ -331,7 +348,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const __grid_con
       mbar_init(raw_empty + i, kNumDeq);
     }
     for (int i = 0; i < kNA; ++i) {
-      mbar_init(a_full + i, kDeqGroup);
+      mbar_init(a_full + i, kNumDeq);  // both dequantiser groups (one sub-stage each)
       mbar_init(a_empty + i, 1);
     }
     for (int i = 0; i < kNX; ++i) {
@@ -384,50 +401,66 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const __grid_con
     // ================= x producer
     if (lane == 0) {
       pdl_wait();  // x stages come from the preceding xprep kernel
-      for (int st = 0; st < NSTG; ++st) {
-        const int s = st % kNX;
-        if (st >= kNX) mbar_wait(x_empty + s, ((st / kNX) - 1) & 1);
-        mbar_expect_tx(x_full + s, x_bytes);
-        if (tr && st < 72) tr[8 + st] = umma_clock();
-        const uint8_t* src = a.xf + (static_cast<size_t>(tile) * a.KS + 2 * kq0 + st) * x_bytes;
-        bulk_g2s_plain(x_st + s * x_bytes, src, x_bytes, x_full + s);
+      for (int u = 0; u < KQC; ++u) {  // one k-quad (two contiguous x stages) per slot
+        const int s = u % kNX;
+        if (u >= kNX) mbar_wait(x_empty + s, ((u / kNX) - 1) & 1);
+        mbar_expect_tx(x_full + s, 2 * x_bytes);
+        if (tr && u < 72) tr[8 + u] = umma_clock();
+        const uint8_t* src = a.xf + (static_cast<size_t>(tile) * a.KS + 2 * (kq0 + u)) * x_bytes;
+        bulk_g2s_plain(x_st + s * 2 * x_bytes, src, 2 * x_bytes, x_full + s);
       }
     }
   } else if (warp == 1) {
     // ================= MMA issuer
     if (lane == 0) {
       const uint32_t idesc = umma_idesc(N);  // x stage rows: hi [0, T), lo [T, 2T)
-      for (int st = 0; st < NSTG; ++st) {
-        const int round = st / steps_per_scale, first = st % steps_per_scale == 0;
-        const int buf = kScaled ? (round & 1) : 0;
-        if (kScaled && first && round >= 2) mbar_wait(tm_empty + buf, ((round / 2) - 1) & 1);
-        if (tr && st < 80) tr[560 + st] = umma_clock();
-        mbar_wait(a_full + st % kNA, (st / kNA) & 1);
-        if (tr && st < 80) tr[400 + st] = umma_clock();
-        mbar_wait(x_full + st % kNX, (st / kNX) & 1);
+      for (int u = 0; u < KQC; ++u) {
+        const bool ck = tr && u >= 2 && u < 10;
+        const long long c0 = ck ? clock64() : 0;
+        if (tr && u < 80) tr[560 + u] = umma_clock();
+        mbar_wait(a_full + u % kNA, (u / kNA) & 1);
+        if (tr && u < 80) tr[400 + u] = umma_clock();
+        mbar_wait(x_full + u % kNX, (u / kNX) & 1);
         tc_fence_after();
-        if (tr && st < 80) tr[80 + st] = umma_clock();
-        const uint32_t abase = smem_addr(a_st + (st % kNA) * kASlot);
-        const uint32_t bbase = smem_addr(x_st + (st % kNX) * x_bytes);
-        const uint32_t d = tmem + static_cast<uint32_t>(buf * N);
-        if (a.dbg & 4) {
-        } else if constexpr (SPARSE) {  // two K = 32 (logical) sparse MMAs per stage, x hi and lo
+        const long long c1 = ck ? clock64() : 0;
+        if (tr && u < 80) tr[80 + u] = umma_clock();
 #pragma unroll
-          for (int jj = 0; jj < 2; ++jj) {
-            const uint64_t ad = umma_desc_sw(abase + jj * 32, 64);
-            const uint32_t e = tmem + kMetaCol + static_cast<uint32_t>(2 * (st % kMetaRing) + jj);
-            umma_f16_sp(d, ad, umma_desc_sw(bbase + jj * 64, 128), e, idesc, (first && jj == 0) ? 0u : 1u);
+        for (int hs = 0; hs < 2; ++hs) {
+          const int st = 2 * u + hs;
+          const int round = st / steps_per_scale, first = st % steps_per_scale == 0;
+          const int buf = kScaled ? (round & 1) : 0;
+          if (kScaled && first && round >= 2) {
+            mbar_wait(tm_empty + buf, ((round / 2) - 1) & 1);
+            tc_fence_after();
           }
-        } else {
+          const uint32_t abase = smem_addr(a_st + ((u % kNA) * 2 + hs) * kASlot);
+          const uint32_t bbase = smem_addr(x_st + ((u % kNX) * 2 + hs) * x_bytes);
+          const uint32_t d = tmem + static_cast<uint32_t>(buf * N);
+          if (a.dbg & 4) {
+          } else if constexpr (SPARSE) {  // two K = 32 (logical) sparse MMAs per sub-stage, x hi and lo
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const uint64_t ad = umma_desc_sw(abase + kk * 32, 128);
-            umma_f16(d, ad, umma_desc_sw(bbase + kk * 32, 128), idesc, (first && kk == 0) ? 0u : 1u);
+            for (int jj = 0; jj < 2; ++jj) {
+              const uint64_t ad = umma_desc_sw(abase + jj * 32, 64);
+              const uint32_t e = tmem + kMetaCol + static_cast<uint32_t>(2 * (st % kMetaRing) + jj);
+              umma_f16_sp(d, ad, umma_desc_sw(bbase + jj * 64, 128), e, idesc, (first && jj == 0) ? 0u : 1u);
+            }
+          } else {
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+              const uint64_t ad = umma_desc_sw(abase + kk * 32, 128);
+              umma_f16(d, ad, umma_desc_sw(bbase + kk * 32, 128), idesc, (first && kk == 0) ? 0u : 1u);
+            }
           }
+          if ((st + 1) % steps_per_scale == 0 || st + 1 == NSTG) umma_commit(tm_full + buf);
         }
-        umma_commit(a_empty + st % kNA);
-        umma_commit(x_empty + st % kNX);
-        if ((st + 1) % steps_per_scale == 0 || st + 1 == NSTG) umma_commit(tm_full + buf);
+        const long long c2 = ck ? clock64() : 0;
+        umma_commit(a_empty + u % kNA);
+        umma_commit(x_empty + u % kNX);
+        if (ck) {
+          const long long c3 = clock64();
+          unsigned long long* o = tr + 900 + 8 * (u - 2);
+          o[0] = c1 - c0; o[1] = c2 - c1; o[2] = c3 - c2; o[3] = c3 - c0;
+        }
       }
     }
   } else if (warp < kEpiWarp0) {
@@ -437,9 +470,9 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const __grid_con
     const int dq = warp & 3, grp = (warp - kDeqWarp0) / kDeqGroup;
     const int g = lane >> 2, t = lane & 3;
     const int eshift = a.SS == 4 ? 2 : 1;  // k-tile j of a k-quad -> scale entry j >> eshift
-    for (int st = grp; st < NSTG; st += 2) {
-      const int sa = st % kNA;
-      if (st >= kNA) mbar_wait(a_empty + sa, ((st / kNA) - 1) & 1);
+    for (int st = grp; st < NSTG; st += 2) {  // group grp: sub-stage hs = grp of every k-quad
+      const int un = st >> 1, sa = un % kNA;
+      if (un >= kNA) mbar_wait(a_empty + sa, ((un / kNA) - 1) & 1);
       if (tr && warp == kDeqWarp0 && lane == 0 && st < 80) tr[640 + st] = umma_clock();
       const int kql = st >> 1, hs = st & 1;
       const int rs = kql / kRawKQ, b = kql % kRawKQ;
@@ -468,7 +501,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const __grid_con
           tc_fence_before();
         }
       }
-      const uint32_t abase = smem_addr(a_st + sa * kASlot);
+      const uint32_t abase = smem_addr(a_st + (sa * 2 + (st & 1)) * kASlot);
 #pragma unroll
       for (int ii = 0; ii < 2; ++ii) {
       if (a.dbg & 1) break;
@@ -1026,25 +1059,30 @@ cudaError_t launch_umma(const egt_dev_packed* h, const float* x, int ldx, int M,
   const size_t budget = 227 * 1024 - fa.sharedSizeBytes;  // dynamic + static shared memory per block
   const size_t x_bytes = static_cast<size_t>(a.N) * kStageK * 2;
   const bool sparse_path = h->format != I4_DENSE && getenv("EGT_UMMA_DENSE") == nullptr;
-  const size_t a_bytes = sparse_path ? 8192 : 16384;
+  // ring slots are k-quads: two A stages (8 / 16 KB each), two x stages
+  const size_t a_bytes = 2 * (sparse_path ? 8192 : 16384), xu_bytes = 2 * x_bytes;
   const size_t fixed = 2048 + kNR * 8 * static_cast<size_t>(a.raw_rt_bytes);
-  // x stages first (a few suffice: the x producer runs ahead), then the A
-  // ring as deep as the rest allows
+  // split K: the x ring also holds the slice's partials, 128 x (T + 4) f32
+  const int nx_min = p.S > 1 ? static_cast<int>((512 * static_cast<size_t>(p.T + 4) + xu_bytes - 1) / xu_bytes) : 2;
   static const int nx_env = getenv("EGT_UMMA_NX") ? atoi(getenv("EGT_UMMA_NX")) : 0;
   static const int na_env = getenv("EGT_UMMA_NA") ? atoi(getenv("EGT_UMMA_NA")) : 0;
-  // split K: the x ring also holds the slice's partials, 128 x (T + 4) f32
-  const int nx_min = p.S > 1 ? static_cast<int>((512 * static_cast<size_t>(p.T + 4) + x_bytes - 1) / x_bytes) : 2;
-  a.NX = std::max(nx_min, nx_env > 0 ? std::min(nx_env, kMaxNX) : 4);
-  const long room = static_cast<long>(budget) - static_cast<long>(fixed + a.NX * x_bytes);
-  a.NA = room > 0 ? static_cast<int>(std::min<long>(kMaxNA, room / static_cast<long>(a_bytes))) : 0;
-  if (na_env > 0) a.NA = std::min(a.NA, na_env);
-  if (a.NA < 2) {  // huge token tiles: fewer x stages
-    a.NX = std::max(nx_min, 2);
-    const long room2 = static_cast<long>(budget) - static_cast<long>(fixed + a.NX * x_bytes);
-    a.NA = room2 > 0 ? static_cast<int>(std::min<long>(kMaxNA, room2 / static_cast<long>(a_bytes))) : 0;
+  auto na_for = [&](int nx) {
+    const long room = static_cast<long>(budget) - static_cast<long>(fixed + nx * xu_bytes);
+    int na = room > 0 ? static_cast<int>(std::min<long>(kMaxNA, room / static_cast<long>(a_bytes))) : 0;
+    return na_env > 0 ? std::min(na, na_env) : na;
+  };
+  // the deepest x ring (<= 4) that still leaves at least as deep an A ring (>= 2)
+  a.NX = 0;
+  for (int nx = nx_env > 0 ? std::min(nx_env, kMaxNX) : 4; nx >= std::max(2, nx_min); --nx) {
+    const int na = na_for(nx);
+    if (na >= 2 && (na >= nx || nx == std::max(2, nx_min) || nx_env > 0)) {
+      a.NX = nx;
+      a.NA = na;
+      break;
+    }
   }
-  if (a.NA < 2) return cudaErrorInvalidConfiguration;
-  const size_t smem = fixed + a.NA * a_bytes + a.NX * x_bytes;
+  if (a.NX == 0 || a.NA < 2) return cudaErrorInvalidConfiguration;
+  const size_t smem = fixed + a.NA * a_bytes + a.NX * xu_bytes;
   err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (err != cudaSuccess) return err;
   cudaLaunchConfig_t cfg = {};

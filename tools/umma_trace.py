@@ -37,7 +37,7 @@ def us(v):
 
 
 print(f"{rows}x{cols} M={M}: alloc done {us(t[1])}")
-for st in range(0, 72):
+for st in range(0, 36):
     if t[8 + st] == 0 and t[80 + st] == 0:
         break
     print(f"stage {st:2d}: x {us(t[8 + st]):>6} | deq2 a_empty {us(t[640 + st]):>6} raw {us(t[720 + st]):>6} "
@@ -49,5 +49,8 @@ print("epilogue warps: rounds done", [us(v) for v in t[800:808]], "\n  past bar"
       "\n  partials", [us(v) for v in t[840:848]],
       "\n  outputs", [us(v) for v in t[820:828]])
 print("reduce pass starts", us(t[900]), us(t[901]))
+print("MMA loop cycles per k-quad (waits, MMAs + round commits, slot commits, total):")
+for i in range(8):
+    print("  k-quad", 2 + i, [int(v) for v in t[900 + 8 * i:904 + 8 * i]])
 print("raw issued:", [us(v) for v in t[320:340] if v])
 print("epilogue rounds:", [us(v) for v in t[240:280] if v])
