@@ -62,7 +62,7 @@ __host__ __device__ constexpr int raw_kq(int fmt) { return fmt == egt_fmt::F16_S
 // a.NX).  The A ring spans the MMA -> commit -> dequantiser -> MMA round
 // trip (~2 us measured with EGT_UMMA_TRACE): 4 slots capped the kernel at
 // ~0.5 us per stage whatever the work.
-constexpr int kNR = 3, kMaxNA = 6, kMaxNX = 6;
+constexpr int kNR = 3, kMaxNA = 6;
 // scale hand-off ring (rounds): the dequantisers run up to kMaxNA stages
 // (= rounds at 64-column groups) ahead of the MMA, the epilogue up to two
 // rounds behind it
@@ -312,9 +312,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const __grid_con
   const int kNA = a.NA;
   uint64_t* a_empty = a_full + kMaxNA;
   const int kNX = a.NX;
-  uint64_t* x_full = a_empty + kMaxNA;
-  uint64_t* x_empty = x_full + kMaxNX;
-  uint64_t* tm_full = x_empty + kMaxNX;
+  uint64_t* tm_full = a_empty + kMaxNA;
   uint64_t* tm_empty = tm_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tm_empty + 2);
   __shared__ int s_last;
@@ -348,12 +346,11 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const __grid_con
       mbar_init(raw_empty + i, kNumDeq);
     }
     for (int i = 0; i < kNA; ++i) {
-      mbar_init(a_full + i, kNumDeq);  // both dequantiser groups (one sub-stage each)
+      // one ring of k-quad slots for A and x: full = both dequantiser groups
+      // (one sub-stage each) + the x producer's arrive.expect_tx (and its
+      // bytes); empty = one MMA commit
+      mbar_init(a_full + i, kNumDeq + 1);
       mbar_init(a_empty + i, 1);
-    }
-    for (int i = 0; i < kNX; ++i) {
-      mbar_init(x_full + i, 1);
-      mbar_init(x_empty + i, 1);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(tm_full + i, 1);
@@ -402,12 +399,12 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const __grid_con
     if (lane == 0) {
       pdl_wait();  // x stages come from the preceding xprep kernel
       for (int u = 0; u < KQC; ++u) {  // one k-quad (two contiguous x stages) per slot
-        const int s = u % kNX;
-        if (u >= kNX) mbar_wait(x_empty + s, ((u / kNX) - 1) & 1);
-        mbar_expect_tx(x_full + s, 2 * x_bytes);
+        const int s = u % kNA;
+        if (u >= kNA) mbar_wait(a_empty + s, ((u / kNA) - 1) & 1);
+        mbar_expect_tx(a_full + s, 2 * x_bytes);
         if (tr && u < 72) tr[8 + u] = umma_clock();
         const uint8_t* src = a.xf + (static_cast<size_t>(tile) * a.KS + 2 * (kq0 + u)) * x_bytes;
-        bulk_g2s_plain(x_st + s * 2 * x_bytes, src, 2 * x_bytes, x_full + s);
+        bulk_g2s_plain(x_st + s * 2 * x_bytes, src, 2 * x_bytes, a_full + s);
       }
     }
   } else if (warp == 1) {
@@ -418,9 +415,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const __grid_con
         const bool ck = tr && u >= 2 && u < 10;
         const long long c0 = ck ? clock64() : 0;
         if (tr && u < 80) tr[560 + u] = umma_clock();
-        mbar_wait(a_full + u % kNA, (u / kNA) & 1);
-        if (tr && u < 80) tr[400 + u] = umma_clock();
-        mbar_wait(x_full + u % kNX, (u / kNX) & 1);
+        mbar_wait(a_full + u % kNA, (u / kNA) & 1);  // A and x of the slot
         tc_fence_after();
         const long long c1 = ck ? clock64() : 0;
         if (tr && u < 80) tr[80 + u] = umma_clock();
@@ -434,7 +429,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const __grid_con
             tc_fence_after();
           }
           const uint32_t abase = smem_addr(a_st + ((u % kNA) * 2 + hs) * kASlot);
-          const uint32_t bbase = smem_addr(x_st + ((u % kNX) * 2 + hs) * x_bytes);
+          const uint32_t bbase = smem_addr(x_st + ((u % kNA) * 2 + hs) * x_bytes);
           const uint32_t d = tmem + static_cast<uint32_t>(buf * N);
           if (a.dbg & 4) {
           } else if constexpr (SPARSE) {  // two K = 32 (logical) sparse MMAs per sub-stage, x hi and lo
@@ -455,7 +450,6 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const __grid_con
         }
         const long long c2 = ck ? clock64() : 0;
         umma_commit(a_empty + u % kNA);
-        umma_commit(x_empty + u % kNX);
         if (ck) {
           const long long c3 = clock64();
           unsigned long long* o = tr + 900 + 8 * (u - 2);
@@ -1064,24 +1058,12 @@ cudaError_t launch_umma(const egt_dev_packed* h, const float* x, int ldx, int M,
   const size_t fixed = 2048 + kNR * 8 * static_cast<size_t>(a.raw_rt_bytes);
   // split K: the x ring also holds the slice's partials, 128 x (T + 4) f32
   const int nx_min = p.S > 1 ? static_cast<int>((512 * static_cast<size_t>(p.T + 4) + xu_bytes - 1) / xu_bytes) : 2;
-  static const int nx_env = getenv("EGT_UMMA_NX") ? atoi(getenv("EGT_UMMA_NX")) : 0;
   static const int na_env = getenv("EGT_UMMA_NA") ? atoi(getenv("EGT_UMMA_NA")) : 0;
-  auto na_for = [&](int nx) {
-    const long room = static_cast<long>(budget) - static_cast<long>(fixed + nx * xu_bytes);
-    int na = room > 0 ? static_cast<int>(std::min<long>(kMaxNA, room / static_cast<long>(a_bytes))) : 0;
-    return na_env > 0 ? std::min(na, na_env) : na;
-  };
-  // the deepest x ring (<= 4) that still leaves at least as deep an A ring (>= 2)
-  a.NX = 0;
-  for (int nx = nx_env > 0 ? std::min(nx_env, kMaxNX) : 4; nx >= std::max(2, nx_min); --nx) {
-    const int na = na_for(nx);
-    if (na >= 2 && (na >= nx || nx == std::max(2, nx_min) || nx_env > 0)) {
-      a.NX = nx;
-      a.NA = na;
-      break;
-    }
-  }
-  if (a.NX == 0 || a.NA < 2) return cudaErrorInvalidConfiguration;
+  const long room = static_cast<long>(budget) - static_cast<long>(fixed);
+  a.NA = room > 0 ? static_cast<int>(std::min<long>(kMaxNA, room / static_cast<long>(a_bytes + xu_bytes))) : 0;
+  if (na_env > 0) a.NA = std::min(a.NA, na_env);
+  a.NX = a.NA;  // one ring
+  if (a.NA < std::max(2, nx_min)) return cudaErrorInvalidConfiguration;
   const size_t smem = fixed + a.NA * a_bytes + a.NX * xu_bytes;
   err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (err != cudaSuccess) return err;
