@@ -380,12 +380,14 @@ DECODE_PLANS = {
 }
 
 
-FORMAT_ARMS = ("int4-1:4", "int4-2:4-g64/128", "int4-dense", "fp16-2:4", "fp16-1:4")
+FORMAT_ARMS = ("int4-1:4", "int4-2:4-g64/128", "int4-2:4-g16", "int4-2:4-g16/64", "int4-dense", "fp16-2:4",
+               "fp16-1:4")
 
 
 def format_layer(rng, name, rows, cols):
     """One host artifact of a format arm (product encoder; U(-1,1) weights,
-    random exact-n masks; 'g64/128' alternates 64 and 128 column groups per row)."""
+    random exact-n masks; 'g64/128' alternates 64 and 128 column groups per row, 'g16/64' the
+    reference's default fine / coarse groups (config.hpp:50-51) the same way)."""
     import paper_2605_11582_b200 as egt
 
     w = rng.uniform(-1, 1, (rows, cols)).astype(np.float32)
@@ -399,7 +401,14 @@ def format_layer(rng, name, rows, cols):
     mask = np.packbits(keep.reshape(-1), bitorder="little")
     if name.startswith("fp16"):
         return egt.pack_f32(mask, w.astype(np.float16).astype(np.float32), n)
-    groups = np.where(np.arange(rows) % 2 == 0, 64, 128).astype(np.uint32) if "g64/128" in name else GROUP
+    if "g64/128" in name:
+        groups = np.where(np.arange(rows) % 2 == 0, 64, 128).astype(np.uint32)
+    elif "g16/64" in name:
+        groups = np.where(np.arange(rows) % 2 == 0, 16, 64).astype(np.uint32)
+    elif "g16" in name:
+        groups = 16
+    else:
+        groups = GROUP
     return egt.pack(mask, egt.quantize_matrix(w, groups, mask), n)
 
 

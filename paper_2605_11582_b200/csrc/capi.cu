@@ -243,6 +243,14 @@ egt_status build_handle(int format, uint8_t n, uint8_t kind, uint32_t rows, uint
     store->bytes = up_bytes;
     up.base = nullptr;  // ownership moves to the handle
     h->path = EGT_PATH_GENERAL;
+    if (kind == EGT_KIND_INT4 && format == I4_SP24 && cols % 16 == 0) {
+      bool ok = true;
+      for (uint32_t r = 0; r < rows && ok; ++r) {
+        const uint32_t g = host_gs[r];
+        ok = g >= cols || (g >= 16 && (g & (g - 1)) == 0);
+      }
+      h->grouped_ok = ok ? 1 : 0;
+    }
     h->raw.words = up.words;
     h->raw.codes = up.codes;
     h->raw.dense_codes = up.dense;
@@ -526,6 +534,7 @@ egt_status egt_dev_packed_slice_rows(const egt_dev_packed* h, uint32_t r0, uint3
   s->kind = h->kind;
   s->format = h->format;
   s->path = h->path;
+  s->grouped_ok = h->grouped_ok;
   s->raw = h->raw;
   s->tiled = h->tiled;
   const double frac = h->rows ? static_cast<double>(r1 - r0) / h->rows : 0.0;
@@ -615,6 +624,12 @@ egt_status spmv_impl(const egt_dev_packed* h, const float* x, float* y, uint32_t
       else
         CUDA_TRY(cudaMemsetAsync(ym, 0, h->rows * sizeof(float), s));
     }
+    return EGT_OK;
+  }
+  static const bool no_grouped = getenv("EGT_NO_GROUPED") != nullptr;  // tuning: the warp-per-row kernel
+  if (h->path == EGT_PATH_GENERAL && !no_grouped && grouped_stream_ok(h, static_cast<int>(M)) && !pg && ldx % 4 == 0 &&
+      reinterpret_cast<uintptr_t>(x) % 16 == 0) {
+    CUDA_TRY(launch_grouped_stream(h, x, static_cast<int>(ldx), static_cast<int>(M), y, static_cast<int>(ldy), ctx));
     return EGT_OK;
   }
   if (h->path == EGT_PATH_GENERAL) {

@@ -69,6 +69,9 @@ struct egt_dev_packed {
   std::shared_ptr<egt_impl::DevStorage> store;
   uint32_t rows = 0, cols = 0;
   uint8_t n = 2, m = 4, kind = 1, format = 0, path = 0;
+  // general path, INT4 2:4 with every row's group size a power of two >= 16
+  // (or one group per row) and cols % 16 == 0: the grouped-stream kernel
+  uint8_t grouped_ok = 0;
   egt_impl::RawStream raw;
   egt_impl::TiledStream tiled;
   uint64_t nnz = 0;
@@ -156,6 +159,12 @@ cudaError_t launch_umma(const egt_dev_packed* h, const float* x, int ldx, int M,
 size_t wide_workspace_bytes(const egt_dev_packed* h, int M);
 cudaError_t launch_wide(const egt_dev_packed* h, const float* x, int ldx, int M, float* y, int ldy,
                         uint32_t* xf_ws, const LaunchCtx& ctx, int num_sms);
+// Reference-order INT4 2:4 stream with power-of-two groups >= 16 (the
+// reference's default g_fine = 16), M <= 4, fused input / epilogue
+// (stream_kernels.cu); false when the shape is not covered.
+bool grouped_stream_ok(const egt_dev_packed* h, int M);
+cudaError_t launch_grouped_stream(const egt_dev_packed* h, const float* x, int ldx, int M, float* y, int ldy,
+                                  const LaunchCtx& ctx);
 cudaError_t launch_general(const egt_dev_packed* h, const float* x, int ldx, int M, float* y,
                            int ldy, const LaunchCtx& ctx);
 

@@ -2,6 +2,7 @@
 // SpGEMV, and the bit-exact device unpack.
 #include "device_common.cuh"
 #include "handle.h"
+#include "egt_b200.h"
 
 namespace egt_impl {
 using namespace egt_dev;
@@ -365,6 +366,204 @@ cudaError_t launch_general(const egt_dev_packed* h, const float* x, int ldx, int
   cfg.numAttrs = ctx.pdl ? 1 : 0;
   void* args[] = {&a};
   cudaError_t err = cudaLaunchKernelExC(&cfg, reinterpret_cast<void*>(&general_spmm_kernel), args);
+  if (err == cudaSuccess) ++launch_counter();
+  return err;
+}
+
+// ------------------------------------------------------------- grouped stream
+// INT4 2:4 in the reference's own stream order with power-of-two group sizes
+// >= 16 -- the reference's default fine groups (config.hpp:50-51, g_fine =
+// 16) do not fit the tiled path's 32-column k-tiles.  A lane takes chunks of
+// 8 kept entries: one u16 index word, one u32 of codes, and (16 columns,
+// 16-aligned) exactly one group, so one scale / zero point per chunk:
+//   y_r += s_g * sum_j (c_j - z_g) x[col_j]      (c - z exact in f32)
+// x (after the fused rmsnorm / silu) is staged once per block in shared
+// memory with one pad float per 16 (lane stride 16 floats -> 17: no bank
+// conflicts).  Bytes per 8 entries at g16: 4 codes + 2 index + 5 table.
+struct GroupedArgs {
+  RawStream raw;
+  uint32_t rows, cols;
+  const float* x;
+  int ldx, M;
+  float* y;
+  int ldy;
+  const float* res;
+  int ldr, xform, out_silu;
+  float eps;
+};
+// one row per warp, 8 chunks per lane in flight (~45 KB of weights in
+// flight per SM at full occupancy: the bandwidth-delay product of HBM)
+// (16 rows per block: x staged once per 16 rows; two blocks per SM)
+constexpr int kGroupedRowsPerWarp = 1, kGroupedWarps = 16, kGroupedMaxX = 24 * 1024;  // x floats staged
+
+__device__ __forceinline__ int xpad(int c) { return c + (c >> 4); }
+
+template <int M>
+__global__ void __launch_bounds__(32 * kGroupedWarps, 2) grouped_stream_kernel(const GroupedArgs a) {
+  extern __shared__ float xs[];  // [M][cols + cols / 16]
+  pdl_wait();
+  pdl_launch_dependents();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ldxs = xpad(static_cast<int>(a.cols));
+  // ---- stage x (rmsnorm: inv_m over the whole row, model.cpp:57-67)
+  __shared__ float s_red[kGroupedWarps][M];
+  float inv[M];
+#pragma unroll
+  for (int m = 0; m < M; ++m) inv[m] = 1.f;
+  // x into registers first (float4s, every load of a thread in flight
+  // together: x staging is on the critical path of a dependent product),
+  // then the row sums (rmsnorm), then the transformed values into smem
+  constexpr int kXV = 6;  // float4s per thread per token: cols <= 4 * 512 * 6
+  const int n4 = static_cast<int>(a.cols / 4);
+  for (int m = 0; m < M; ++m) {
+    float4 v[kXV];
+    const float4* xr = reinterpret_cast<const float4*>(a.x + static_cast<size_t>(m) * a.ldx);
+#pragma unroll
+    for (int u = 0; u < kXV; ++u) {
+      const int j = static_cast<int>(threadIdx.x) + u * static_cast<int>(blockDim.x);
+      v[u] = j < n4 ? __ldg(xr + j) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    float iv = 1.f;
+    if (a.xform == EGT_INPUT_RMSNORM) {
+      float ss = 0.f;
+#pragma unroll
+      for (int u = 0; u < kXV; ++u)
+        ss = fmaf(v[u].x, v[u].x, fmaf(v[u].y, v[u].y, fmaf(v[u].z, v[u].z, fmaf(v[u].w, v[u].w, ss))));
+      ss = warp_sum(ss);
+      if (lane == 0) s_red[warp][m] = ss;
+      __syncthreads();
+      float tot = 0.f;
+      for (int w = 0; w < kGroupedWarps; ++w) tot += s_red[w][m];
+      iv = 1.0f / sqrtf(tot / static_cast<float>(a.cols) + a.eps);
+    }
+    inv[m] = iv;
+#pragma unroll
+    for (int u = 0; u < kXV; ++u) {
+      const int j = static_cast<int>(threadIdx.x) + u * static_cast<int>(blockDim.x);
+      if (j < n4) {
+        float e[4] = {v[u].x, v[u].y, v[u].z, v[u].w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (a.xform == EGT_INPUT_RMSNORM) e[q] *= iv;
+          else if (a.xform == EGT_INPUT_SILU) e[q] = e[q] * (1.0f / (1.0f + expf(-e[q])));  // model.cpp:80-84
+        }
+        float* dst = xs + m * ldxs + xpad(4 * j);  // 4 j .. 4 j + 3 never straddle a pad (16 | 4 j + 16)
+        dst[0] = e[0];
+        dst[1] = e[1];
+        dst[2] = e[2];
+        dst[3] = e[3];
+      }
+    }
+  }
+  __syncthreads();
+  // ---- rows
+  const uint32_t row_nnz = a.cols / 2, nchunk = a.cols / 16;
+  for (int i = 0; i < kGroupedRowsPerWarp; ++i) {
+    const uint32_t r = (blockIdx.x * kGroupedWarps + warp) * kGroupedRowsPerWarp + i;
+    if (r >= a.rows) break;
+    const uint64_t R = a.raw.row_begin + r;
+    const uint32_t gsz = a.raw.group_sizes[R], gbase = a.raw.group_offsets[R];
+    const int lg = gsz >= a.cols ? 31 : __ffs(gsz) - 1;  // one group per row: col >> 31 == 0
+    const uint16_t* wr = a.raw.words + R * (row_nnz / 8);
+    const uint32_t* cr = reinterpret_cast<const uint32_t*>(a.raw.codes) + R * (row_nnz / 8);
+    float acc[M];
+#pragma unroll
+    for (int m = 0; m < M; ++m) acc[m] = 0.f;
+    constexpr int U = 8;  // chunks per lane in flight
+    for (uint32_t c0 = lane; c0 < nchunk; c0 += 32 * U) {
+      uint32_t w[U], cw[U];
+      float s[U];
+      uint32_t z[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t c = c0 + 32 * u;
+        w[u] = 0u;
+        cw[u] = 0u;
+        s[u] = 0.f;
+        z[u] = 0u;
+        if (c < nchunk) {
+          w[u] = __ldg(wr + c);
+          cw[u] = __ldg(cr + c);
+          const uint32_t gi = gbase + ((16 * c) >> lg);
+          s[u] = __ldg(a.raw.scales + gi);
+          z[u] = __ldg(a.raw.zps + gi);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t c = c0 + 32 * u;
+        if (c >= nchunk) break;
+        // c - z exactly: 2^23 + c (the code under the exponent of 2^23) minus 2^23 + z
+        const float zf = 8388608.0f + static_cast<float>(z[u]);
+        // the chunk's 16 columns sit between two pads: xpad(16 c + i) = 17 c + i
+        const float* xc = xs + 17 * static_cast<int>(c);
+        float part[M];
+#pragma unroll
+        for (int m = 0; m < M; ++m) part[m] = 0.f;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int col = 4 * (j >> 1) + static_cast<int>((w[u] >> (14 - 2 * j)) & 3u);
+          const float d = __uint_as_float(0x4B000000u | ((cw[u] >> (4 * j)) & 0xFu)) - zf;
+#pragma unroll
+          for (int m = 0; m < M; ++m) part[m] = fmaf(d, xc[m * ldxs + col], part[m]);
+        }
+#pragma unroll
+        for (int m = 0; m < M; ++m) acc[m] = fmaf(s[u], part[m], acc[m]);
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+      const float v = warp_sum(acc[m]);
+      if (lane == m) {
+        float o = (a.res ? a.res[static_cast<size_t>(m) * a.ldr + r] : 0.f) + v;
+        if (a.out_silu) o = o * (1.0f / (1.0f + expf(-o)));  // model.cpp:80-84
+        a.y[static_cast<size_t>(m) * a.ldy + r] = o;
+      }
+    }
+  }
+}
+
+bool grouped_stream_ok(const egt_dev_packed* h, int M) {
+  return h->grouped_ok && M >= 1 && M <= 4 && static_cast<size_t>(M) * (h->cols + h->cols / 16) <= kGroupedMaxX &&
+         h->cols <= 4u * 32 * kGroupedWarps * 6;
+}
+
+cudaError_t launch_grouped_stream(const egt_dev_packed* h, const float* x, int ldx, int M, float* y, int ldy,
+                                  const LaunchCtx& ctx) {
+  GroupedArgs a;
+  a.raw = h->raw;
+  a.rows = h->rows;
+  a.cols = h->cols;
+  a.x = x;
+  a.ldx = ldx;
+  a.M = M;
+  a.y = y;
+  a.ldy = ldy;
+  a.res = ctx.res;
+  a.ldr = ctx.ldr;
+  a.xform = ctx.xform;
+  a.out_silu = ctx.out_silu;
+  a.eps = ctx.eps;
+  void* fn = M == 1 ? reinterpret_cast<void*>(&grouped_stream_kernel<1>)
+           : M == 2 ? reinterpret_cast<void*>(&grouped_stream_kernel<2>)
+           : M == 3 ? reinterpret_cast<void*>(&grouped_stream_kernel<3>)
+                    : reinterpret_cast<void*>(&grouped_stream_kernel<4>);
+  const size_t smem = static_cast<size_t>(M) * (h->cols + h->cols / 16) * sizeof(float);
+  cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (err != cudaSuccess) return err;
+  cudaLaunchConfig_t cfg = {};
+  const uint32_t rows_per_block = kGroupedWarps * kGroupedRowsPerWarp;
+  cfg.gridDim = dim3((h->rows + rows_per_block - 1) / rows_per_block);
+  cfg.blockDim = dim3(32 * kGroupedWarps);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = ctx.stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = ctx.pdl ? 1 : 0;
+  void* args[] = {&a};
+  err = cudaLaunchKernelExC(&cfg, fn, args);
   if (err == cudaSuccess) ++launch_counter();
   return err;
 }

@@ -1,0 +1,97 @@
+"""The grouped-stream kernel (stream_kernels.cu): INT4 2:4 with the
+reference's default fine groups (g_fine = 16, config.hpp:50-51; mixed with
+g_coarse = 64 per row) in the reference's own stream order, against the
+port's f32 spmv (packed.cpp:211-220): 7B shapes, M = 1..4, the fused rmsnorm
+/ silu inputs and residual / silu epilogue (model.cpp:57-67, 80-84, 186-190),
+and x over the whole f32 range (the kernel multiplies in f32)."""
+import numpy as np
+import pytest
+
+from tests.layers import close, make_int4, to_product
+
+pytestmark = pytest.mark.gpu
+
+
+def _layer(port, rng, rows, cols, g):
+    import paper_2605_11582_b200 as egt
+
+    p, _, _ = make_int4(rng, rows, cols, 2, g, port)
+    d = egt.DeviceMatrix.from_packed(to_product(p))
+    assert d.path == "general"
+    return p, d
+
+
+@pytest.mark.parametrize("shape", [(4096, 4096), (11008, 4096), (4096, 11008), (40, 96)])
+@pytest.mark.parametrize("groups", ["g16", "g16/64"])
+@pytest.mark.parametrize("M", [1, 2, 4])
+def test_grouped_products(port, shape, groups, M):
+    import torch
+
+    rows, cols = shape
+    rng = np.random.default_rng(rows + cols + M)
+    g = 16 if groups == "g16" else np.where(np.arange(rows) % 2 == 0, 16, 64).astype(np.uint32)
+    p, d = _layer(port, rng, rows, cols, g)
+    xs = rng.uniform(-1, 1, (M, cols)).astype(np.float32)
+    y = d.spmv(torch.from_numpy(xs).cuda() if M > 1 else torch.from_numpy(xs[0]).cuda()).cpu().numpy()
+    y = y.reshape(M, rows)
+    for m in range(M):
+        ok, err = close(y[m], port.spmv(p, xs[m]))
+        assert ok, (shape, groups, M, m, err)
+
+
+def test_grouped_fused(port):
+    """y = silu(res + rmsnorm(x) W^T) and y = silu(x) W^T on the grouped path."""
+    import torch
+
+    from paper_2605_11582_b200 import native as N
+
+    rng = np.random.default_rng(5)
+    rows, cols, M = 256, 1024, 2
+    p, d = _layer(port, rng, rows, cols, 16)
+    xs = rng.uniform(-2, 2, (M, cols)).astype(np.float32)
+    res = rng.uniform(-1, 1, (M, rows)).astype(np.float32)
+    eps = 1e-6
+    y = torch.empty((M, rows), device="cuda")
+    d.spmv_fused_into(torch.from_numpy(xs).cuda(), y, input=N.INPUT_RMSNORM, eps=eps,
+                      residual=torch.from_numpy(res).cuda(), output_silu=True)
+    got = y.cpu().numpy()
+    for m in range(M):
+        xn = (xs[m] / np.sqrt(np.mean(xs[m].astype(np.float64) ** 2) + eps)).astype(np.float32)
+        pre = res[m] + port.spmv(p, xn)
+        ok, err = close(got[m], pre / (1 + np.exp(-pre.astype(np.float64))))
+        assert ok, (m, err)
+    y2 = torch.empty((M, rows), device="cuda")
+    d.spmv_fused_into(torch.from_numpy(xs).cuda(), y2, input=N.INPUT_SILU)
+    got2 = y2.cpu().numpy()
+    for m in range(M):
+        xsil = (xs[m] / (1 + np.exp(-xs[m].astype(np.float64)))).astype(np.float32)
+        ok, err = close(got2[m], port.spmv(p, xsil))
+        assert ok, (m, err)
+
+
+def test_grouped_x_range(port):
+    """f32 arithmetic: huge / tiny / non-finite x give the reference's values,
+    NaN / inf at the same positions."""
+    import torch
+
+    rng = np.random.default_rng(9)
+    rows, cols = 64, 512
+    p, d = _layer(port, rng, rows, cols, 16)
+    for kind in ("huge", "tiny", "inf", "nan"):
+        x = rng.uniform(-1, 1, cols).astype(np.float32)
+        if kind == "huge":
+            x *= 1e5
+        elif kind == "tiny":
+            x *= 1e-6
+        elif kind == "inf":
+            x[rng.integers(0, cols, 3)] = np.inf
+        else:
+            x[rng.integers(0, cols, 3)] = np.nan
+        got = d.spmv(torch.from_numpy(x).cuda()).cpu().numpy()
+        want = port.spmv(p, x)
+        assert np.array_equal(np.isnan(got), np.isnan(want)), kind
+        assert np.array_equal(np.isposinf(got), np.isposinf(want)), kind
+        fin = np.isfinite(want)
+        scale = np.abs(x[np.isfinite(x)]).max()
+        ok, err = close(got[fin] / scale, want[fin] / scale)
+        assert ok, (kind, err)
