@@ -627,9 +627,19 @@ egt_status spmv_impl(const egt_dev_packed* h, const float* x, float* y, uint32_t
     return EGT_OK;
   }
   static const bool no_grouped = getenv("EGT_NO_GROUPED") != nullptr;  // tuning: the warp-per-row kernel
-  if (h->path == EGT_PATH_GENERAL && !no_grouped && grouped_stream_ok(h, static_cast<int>(M)) && !pg && ldx % 4 == 0 &&
+  if (h->path == EGT_PATH_GENERAL && !no_grouped && grouped_stream_ok(h, 1) && !pg && ldx % 4 == 0 &&
       reinterpret_cast<uintptr_t>(x) % 16 == 0) {
-    CUDA_TRY(launch_grouped_stream(h, x, static_cast<int>(ldx), static_cast<int>(M), y, static_cast<int>(ldy), ctx));
+    // up to four tokens per launch (x staged in shared memory); more tokens
+    // run as several launches over token groups (rows and tokens independent)
+    uint32_t mt = 4;
+    while (mt > 1 && !grouped_stream_ok(h, static_cast<int>(mt))) --mt;
+    for (uint32_t m0 = 0; m0 < M; m0 += mt) {
+      const int mc = static_cast<int>(std::min<uint32_t>(mt, M - m0));
+      LaunchCtx c2 = ctx;
+      if (c2.res) c2.res += static_cast<size_t>(m0) * c2.ldr;
+      CUDA_TRY(launch_grouped_stream(h, x + static_cast<size_t>(m0) * ldx, static_cast<int>(ldx), mc,
+                                     y + static_cast<size_t>(m0) * ldy, static_cast<int>(ldy), c2));
+    }
     return EGT_OK;
   }
   if (h->path == EGT_PATH_GENERAL) {

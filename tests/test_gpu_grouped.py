@@ -95,3 +95,35 @@ def test_grouped_x_range(port):
         scale = np.abs(x[np.isfinite(x)]).max()
         ok, err = close(got[fin] / scale, want[fin] / scale)
         assert ok, (kind, err)
+
+
+@pytest.mark.parametrize("M", [3, 9])
+def test_grouped_many_tokens_wide(port, M):
+    """4096 x 11008 (x of 11008 floats: two tokens per launch) and M > 4
+    (token groups over several launches)."""
+    import torch
+
+    rng = np.random.default_rng(M)
+    p, d = _layer(port, rng, 256, 11008, 16)
+    xs = rng.uniform(-1, 1, (M, 11008)).astype(np.float32)
+    y = d.spmv(torch.from_numpy(xs).cuda()).cpu().numpy()
+    for m in range(M):
+        ok, err = close(y[m], port.spmv(p, xs[m]))
+        assert ok, (m, err)
+
+
+def test_grouped_model_forward(port):
+    """A model whose layers use the reference's default g_fine = 16 runs the
+    fused forward (rmsnorm / silu / residual on the grouped path) and matches
+    the oracle forward (model.cpp:118-202)."""
+    from tests.test_gpu_verify import CFG, _close, build_model
+
+    model, oracle_forward = build_model(port, plan=[["int4-2:4"] * 6], group=16)
+    rng = np.random.default_rng(3)
+    for M in (1, 6):
+        tokens = rng.integers(0, CFG["vocab_size"], M).astype(np.int32)
+        pos = rng.integers(0, CFG["max_positions"], M).astype(np.int32)
+        vis = np.tril(np.ones((M, M), bool))
+        got = model.forward(tokens, pos, vis).cpu().numpy()
+        want = oracle_forward(tokens, pos, vis)
+        assert _close(got, want) <= 1e-3, (M, _close(got, want))

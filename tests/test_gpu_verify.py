@@ -28,7 +28,7 @@ def _dense_of(port, art):
     return port.dequantize(q)
 
 
-def build_model(port, cfg=CFG, plan=PLAN, seed=5):
+def build_model(port, cfg=CFG, plan=PLAN, seed=5, group=32):
     """init_model-style weights U(-1/sqrt(d), 1/sqrt(d)) (model.hpp:61-62),
     each linear layer compressed by the product's encoder."""
     from paper_2605_11582_b200.model import DeviceModel, compress_layer
@@ -43,7 +43,7 @@ def build_model(port, cfg=CFG, plan=PLAN, seed=5):
         layer = {}
         for part, shape, kind in zip(("wq", "wk", "wv", "wo", "ff1", "ff2"), shapes, plan[li % len(plan)]):
             w = rng.uniform(-bound, bound, shape).astype(np.float32)
-            h, art = compress_layer(w, kind, 32)
+            h, art = compress_layer(w, kind, group)
             handles.append(h)
             layer[part] = _dense_of(port, art)
         dense_layers.append(layer)
