@@ -119,16 +119,25 @@ egt_status check_view(const egt_packed_view* v) {
 }
 
 // Whether every row's quant groups start on 32-column (k-tile) boundaries.
-bool groups_k_aligned(uint32_t rows, uint32_t cols, const uint32_t* gs, int* ss_out) {
+// Scale entries per k-tile (tiled_format.h ss_entries): every group a
+// multiple of 32 columns -> SS in {4, 2, 1}; otherwise, when `half_ok` (INT4
+// 2:4) and every group is a multiple of 16 -> SS = 0 (16-column entries, the
+// reference's default g_fine = 16).
+bool groups_k_aligned(uint32_t rows, uint32_t cols, const uint32_t* gs, int* ss_out, bool half_ok = false) {
   int ss = 4;
+  bool half = false;
   for (uint32_t r = 0; r < rows; ++r) {
     const uint32_t g = gs[r];
     if (g >= cols) continue;  // one group per row
-    if (g % 32 != 0) return false;
+    if (g % 32 != 0) {
+      if (!half_ok || g % 16 != 0) return false;
+      half = true;
+      continue;
+    }
     const uint32_t kt = g / 32;
     while (kt % ss != 0) ss >>= 1;
   }
-  *ss_out = ss;
+  *ss_out = half ? 0 : ss;
   return true;
 }
 
@@ -183,8 +192,11 @@ egt_status build_handle(int format, uint8_t n, uint8_t kind, uint32_t rows, uint
   h->algorithmic_bytes = idx_b + val_b + (kind == EGT_KIND_INT4 ? 5 * n_scales : 0);
 
   int ss = 4;
+  static const bool no_g16 = getenv("EGT_NO_TILED_G16") != nullptr;  // tuning: g16 on the reference-order stream
+  const bool half_ok = !no_g16 && kind == EGT_KIND_INT4 &&
+                       (format == I4_SP24 || (format == I4_SP14 && getenv("EGT_SP14_NATIVE") == nullptr));
   const bool tiled = rows > 0 && cols > 0 && cols % 32 == 0 &&
-                     (kind == EGT_KIND_F32 || groups_k_aligned(rows, cols, host_gs, &ss));
+                     (kind == EGT_KIND_F32 || groups_k_aligned(rows, cols, host_gs, &ss, half_ok));
   // INT4 1:4 on the tiled path is stored as 2:4 with a zero-valued partner per
   // kept entry: one mma.sp per k-tile either way, but without the per-k-tile
   // placement and metadata ALU work (issue-bound otherwise; DESIGN 5).  The
@@ -204,7 +216,7 @@ egt_status build_handle(int format, uint8_t n, uint8_t kind, uint32_t rows, uint
     ts.KQ = static_cast<int>((cols + 127) / 128);
     ts.RT = static_cast<int>((rows + 15) / 16);
     ts.SS = kind == EGT_KIND_INT4 ? ss : 4;
-    ts.E = 4 / ts.SS;
+    ts.E = ss_entries(ts.SS);
     ts.pad14 = pad14 ? 1 : 0;
     const size_t blocks = static_cast<size_t>(ts.RT) * ts.KQ;
     Carve c;
@@ -665,7 +677,8 @@ egt_status spmv_impl(const egt_dev_packed* h, const float* x, float* y, uint32_t
     return EGT_OK;
   }
   static const bool no_wide = getenv("EGT_NO_WIDE") != nullptr;  // tuning: old M > 16 path
-  if (M > 16 && !pg && input == EGT_INPUT_NONE && !no_wide && !plan_forced()) {  // residual / output silu in its epilogue
+  // (16-column groups: the token-tiled kernel below, 16 tokens per block)
+  if (M > 16 && !pg && input == EGT_INPUT_NONE && !no_wide && !plan_forced() && h->tiled.SS != 0) {
     Workspace* w = nullptr;
     egt_status st = get_workspace(s, (wide_workspace_bytes(h, static_cast<int>(M)) + 3) / 4, 0, &w);
     if (st != EGT_OK) return st;

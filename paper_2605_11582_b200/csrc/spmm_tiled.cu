@@ -224,7 +224,7 @@ __device__ __noinline__ void restage_token(const TiledArgs& a, uint32_t* sB, int
 
 template <int FMT, int SS, int NT, bool SINGLE, bool FUSED>
 __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(const __grid_constant__ TiledArgs a) {
-  constexpr int E = 4 / SS;
+  constexpr int E = ss_entries(SS);
   constexpr int TOK = 4 * NT;
   constexpr int VB = val_lane_bytes(FMT), MB = meta_lane_bytes(FMT);
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -778,7 +778,7 @@ void* pick_ss(int SS, int NT, bool fused) {
 
 void* pick_kernel(int fmt, int SS, int NT, bool fused) {
   switch (fmt) {
-    case I4_SP24: return pick_ss<I4_SP24>(SS, NT, fused);
+    case I4_SP24: return SS == 0 ? pick_nt<I4_SP24, 0>(NT, fused) : pick_ss<I4_SP24>(SS, NT, fused);
     case I4_SP14: return pick_ss<I4_SP14>(SS, NT, fused);
     case I4_DENSE: return pick_ss<I4_DENSE>(SS, NT, fused);
     case F16_SP24: return pick_nt<F16_SP24, 4>(NT, fused);

@@ -231,8 +231,9 @@ __global__ void relayout_kernel(const RelayoutArgs a) {
 }
 
 // Per (row tile, k-quad, scale entry, row): the group covering k-tiles
-// [e*SS, (e+1)*SS) of the quad.  Group boundaries are multiples of 32
-// columns on the tiled path, so a k-tile never straddles two groups.
+// [e*SS, (e+1)*SS) of the quad, or (SS = 0) columns [16e, 16e + 16).  Group
+// boundaries are multiples of 32 columns on the tiled path (16 with SS = 0),
+// so an entry never straddles two groups.
 __global__ void relayout_scales_kernel(const RelayoutArgs a) {
   const uint64_t total = static_cast<uint64_t>(a.RT) * a.KQ * a.E * 16;
   const uint64_t idx = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
@@ -245,7 +246,7 @@ __global__ void relayout_scales_kernel(const RelayoutArgs a) {
   const int rt = static_cast<int>(blk / a.KQ);
   const int g = slot >> 1, h = slot & 1;
   const uint32_t r = rt * 16 + g + 8 * h;
-  const uint32_t col = kq * 128 + e * a.SS * 32;
+  const uint32_t col = kq * 128 + (a.SS ? e * a.SS * 32 : e * 16);
   float s = 0.f;
   uint8_t z = 0;
   if (r < a.rows && col < a.cols) {
@@ -627,8 +628,8 @@ __global__ void dequant_tiled_kernel(const DequantTiledArgs a) {
   const int VB = val_lane_bytes(f), MB = meta_lane_bytes(f);
   const uint32_t* v = reinterpret_cast<const uint32_t*>(a.ts.vals + blk * 32 * VB + lane * VB);
   const uint32_t* mb = reinterpret_cast<const uint32_t*>(a.ts.meta + blk * 32 * MB);
-  auto scale_of = [&](int j, int h, float* s, uint32_t* z) {
-    const int e = j / a.ts.SS;
+  auto scale_of = [&](int j, int q, int h, float* s, uint32_t* z) {  // k-tile j, 16-column half q
+    const int e = a.ts.SS ? j / a.ts.SS : 2 * j + q;
     const uint64_t si = (blk * a.ts.E + e) * 16 + 2 * g + h;
     *s = a.ts.scales[si];
     *z = a.ts.zps[si];
@@ -645,7 +646,7 @@ __global__ void dequant_tiled_kernel(const DequantTiledArgs a) {
             const uint32_t code = (v[w16] >> (4 * p + 16 * i)) & 0xFu;
             float s;
             uint32_t z;
-            scale_of((16 * w16) / 32, h, &s, &z);
+            scale_of((16 * w16) / 32, w16 & 1, h, &s, &z);
             a.w[static_cast<uint64_t>(r) * a.cols + c] = decode(code, z, s);
             set_mask(a.mask, a.cols, r, c);
           }
@@ -676,7 +677,7 @@ __global__ void dequant_tiled_kernel(const DequantTiledArgs a) {
               const uint32_t code = (v[j] >> (4 * p + 16 * i)) & 0xFu;
               float s;
               uint32_t z;
-              scale_of(j, h, &s, &z);
+              scale_of(j, q, h, &s, &z);
               val = decode(code, z, s);
             } else {
               const uint32_t pair = v[4 * j + h + 2 * q];
@@ -696,7 +697,7 @@ __global__ void dequant_tiled_kernel(const DequantTiledArgs a) {
             const uint32_t code = (v[j >> 1] >> (4 * (2 * (j & 1) + q) + 16 * h)) & 0xFu;
             float s;
             uint32_t z;
-            scale_of(j, h, &s, &z);
+            scale_of(j, q, h, &s, &z);
             val = decode(code, z, s);
           } else {
             val = __half2float(__ushort_as_half(static_cast<unsigned short>(v[2 * j + q] >> (16 * h))));

@@ -15,11 +15,14 @@ template <int FMT, int E>
 struct Unit {
   static constexpr int NV = val_lane_bytes(FMT) / 4;
   static constexpr int NM = meta_lane_bytes(FMT) > 0 ? meta_lane_bytes(FMT) / 4 : 1;
-  static constexpr int NS = has_scales(FMT) ? E : 1;
+  // 16-column groups (E = 8): the scales / zero points stay in shared memory
+  // and are read per k-tile (24 more registers per unit would spill)
+  static constexpr int NS = has_scales(FMT) && E <= 4 ? E : 1;
   uint32_t v[NV];
   uint32_t m[NM];
   uint32_t s[2 * NS];
   uint32_t z[NS];
+  uint32_t sca, zpa;  // E = 8: shared-memory addresses of this lane's rows' entries
 };
 
 // A stage in shared memory holds one row tile's blocks for the CTA's KCs
@@ -86,7 +89,10 @@ __device__ __forceinline__ void lds_unit(Unit<FMT, E>& u, const Cursor& c) {
   } else {
     u.m[0] = 0;
   }
-  if constexpr (has_scales(FMT)) {
+  if constexpr (has_scales(FMT) && E == 8) {
+    u.sca = smem_u32(c.sc);
+    u.zpa = smem_u32(c.zp);
+  } else if constexpr (has_scales(FMT)) {
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       const uint2 sc = *reinterpret_cast<const uint2*>(c.sc + e * 64);
@@ -158,8 +164,48 @@ constexpr uint32_t kOnes = 0x3C003C00u;  // half2(1, 1)
 
 // NR units of the same k-quad (NR row tiles) share every B fragment load.
 template <int FMT, int SS, int NT, int NR, bool kLoadB = true, bool kOnesMma = true>
-__device__ __forceinline__ void compute_units(const Unit<FMT, 4 / SS> (&uu)[NR], const uint32_t* pb, int KTc,
+__device__ __forceinline__ void compute_units(const Unit<FMT, ss_entries(SS)> (&uu)[NR], const uint32_t* pb, int KTc,
                                               int LS, float (&acc)[NR][NT][2]) {
+  if constexpr (SS == 0) {
+    // 16-column groups (INT4 2:4): per k-tile two mma.sp, the first half's A
+    // registers (a0, a1: logical columns 0-15) with its zero points and the
+    // second half's (a2, a3: columns 16-31) with theirs, the other half zero
+    // (the metadata stays valid); each half's sum times its own scale.
+    static_assert(FMT == I4_SP24, "16-column groups: INT4 2:4 only");
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      uint32_t b[NT][4];
+      load_b<NT>(b, pb + j * LS * 4, KTc * LS * 4);
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        const Unit<FMT, 8>& u = uu[r];
+        float dA[NT][4], dB[NT][4];
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) dA[nt][i] = dB[nt][i] = 0.f;
+        uint32_t z0, z1;  // zero points of rows g (low byte) and g + 8, entries 2j and 2j + 1
+        asm volatile("ld.shared.u16 %0, [%1];\n" : "=r"(z0) : "r"(u.zpa + 32 * j));
+        asm volatile("ld.shared.u16 %0, [%1];\n" : "=r"(z1) : "r"(u.zpa + 32 * j + 16));
+        const uint32_t zA0 = (0x6400u | (z0 & 0xFFu)) * 0x10001u, zA80 = (0x6400u | ((z0 >> 4) & 0xF0u)) * 0x10001u;
+        const uint32_t zA1 = (0x6400u | (z1 & 0xFFu)) * 0x10001u, zA81 = (0x6400u | ((z1 >> 4) & 0xF0u)) * 0x10001u;
+        const uint32_t w = u.v[j], w8 = w >> 8;
+        const uint32_t aA[4] = {hsub2_u32(nib2_magic(w), zA0), hsub2_u32(nib16_magic(w), zA80), 0u, 0u};
+        const uint32_t aB[4] = {0u, 0u, hsub2_u32(nib2_magic(w8), zA1), hsub2_u32(nib16_magic(w8), zA81)};
+        mma_sp_sel<NT>(j, dA, aA, b, u.m[j >> 1]);
+        mma_sp_sel<NT>(j, dB, aB, b, u.m[j >> 1]);
+        float s0, s08, s1, s18;  // scales of rows g, g + 8 for entries 2j, 2j + 1
+        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];\n" : "=f"(s0), "=f"(s08) : "r"(u.sca + 128 * j));
+        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];\n" : "=f"(s1), "=f"(s18) : "r"(u.sca + 128 * j + 64));
+#pragma unroll
+        for (int nt = 0; nt < NT; ++nt) {
+          acc[r][nt][0] = fmaf(s0, dA[nt][0] + dA[nt][1], fmaf(s1, dB[nt][0] + dB[nt][1], acc[r][nt][0]));
+          acc[r][nt][1] = fmaf(s08 * 0.0625f, dA[nt][2] + dA[nt][3],
+                               fmaf(s18 * 0.0625f, dB[nt][2] + dB[nt][3], acc[r][nt][1]));
+        }
+      }
+    }
+  } else {
   // INT4 2:4 and dense: the zero point is subtracted in the A operand.  A
   // nibble under the fp16 exponent 0x64 is exactly 1024 + c (row g) or
   // 1024 + 16c (row g+8, 4 bits higher); HSUB2 with 1024 + z (1024 + 16z)
@@ -204,7 +250,7 @@ __device__ __forceinline__ void compute_units(const Unit<FMT, 4 / SS> (&uu)[NR],
     }
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
-    const Unit<FMT, 4 / SS>& u = uu[r];
+    const Unit<FMT, ss_entries(SS)>& u = uu[r];
     float (&d)[NT][4] = dd[r];
     float (&d1)[NT][4] = dd1[r];
     const uint32_t zpair = zpairs[r], zA = zAs[r], zA8 = zA8s[r];
@@ -269,7 +315,7 @@ __device__ __forceinline__ void compute_units(const Unit<FMT, 4 / SS> (&uu)[NR],
     if (j % SS == SS - 1) {
 #pragma unroll
     for (int r = 0; r < NR; ++r) {
-    const Unit<FMT, 4 / SS>& u = uu[r];
+    const Unit<FMT, ss_entries(SS)>& u = uu[r];
     float (&d)[NT][4] = dd[r];
     float (&d1)[NT][4] = dd1[r];
     (void)d1;
@@ -307,12 +353,13 @@ __device__ __forceinline__ void compute_units(const Unit<FMT, 4 / SS> (&uu)[NR],
     }  // r (scale)
     }
   }
+  }  // SS != 0
 }
 
 template <int FMT, int SS, int NT, bool kLoadB = true, bool kOnesMma = true>
-__device__ __forceinline__ void compute_unit(const Unit<FMT, 4 / SS>& u, const uint32_t* pb, int KTc,
+__device__ __forceinline__ void compute_unit(const Unit<FMT, ss_entries(SS)>& u, const uint32_t* pb, int KTc,
                                              int LS, float (&acc)[NT][2]) {
-  const Unit<FMT, 4 / SS> uu[1] = {u};
+  const Unit<FMT, ss_entries(SS)> uu[1] = {u};
   float (&a1)[1][NT][2] = *reinterpret_cast<float (*)[1][NT][2]>(&acc);
   compute_units<FMT, SS, NT, 1, kLoadB, kOnesMma>(uu, pb, KTc, LS, a1);
 }

@@ -42,6 +42,13 @@ __host__ __device__ constexpr int meta_lane_bytes(int f) {
   return f == I4_SP24 ? 8 : f == I4_SP14 ? 4 : f == I4_DENSE ? 0 : f == F16_SP24 ? 8 : 4;
 }
 __host__ __device__ constexpr bool has_scales(int f) { return f <= I4_DENSE; }
+// Scale layout of a tiled handle: SS = k-tiles (32 columns) per scale entry
+// (4, 2, 1: groups of 128, 64, 32 columns), or 0 for 16-column entries (the
+// reference's default g_fine = 16: two entries per k-tile, one per half --
+// the A fragment's registers a0 / a1 hold the first 16 columns, a2 / a3 the
+// second).  Entries per k-quad, and the entry of column c (within the quad):
+__host__ __device__ constexpr int ss_entries(int SS) { return SS ? 4 / SS : 8; }
+__host__ __device__ constexpr int ss_entry(int SS, int cin) { return SS ? (cin >> 5) / SS : cin >> 4; }
 __host__ __device__ constexpr int keep_n(int f) {
   return (f == I4_SP24 || f == F16_SP24) ? 2 : (f == I4_DENSE ? 4 : 1);
 }

@@ -82,12 +82,12 @@ __device__ bool tiled_value(const TiledRef& m, int r, int c, float* out) {
   const int r16 = r & 15, g = r16 & 7, h = r16 >> 3;
   const int cin = c & 127, j = cin >> 5, gi = (cin & 31) >> 2, t = gi & 3, q = gi >> 2;
   const size_t blk = static_cast<size_t>(m.rt_begin + (r >> 4)) * m.KQ + (c >> 7);
-  const int E = 4 / m.SS;
+  const int E = ss_entries(m.SS);
   auto vword = [&](int lane, int idx) {
     return reinterpret_cast<const uint32_t*>(m.vals + blk * 32 * VB + lane * VB)[idx];
   };
-  auto scaled = [&](uint32_t code, int jj) {
-    const size_t si = (blk * E + jj / m.SS) * 16 + 2 * g + h;
+  auto scaled = [&](uint32_t code, int jj) {  // jj: the k-tile (32 columns) of c within the quad
+    const size_t si = (blk * E + (m.SS ? jj / m.SS : ss_entry(0, cin))) * 16 + 2 * g + h;
     return xr_decode(code, m.zps[si], m.scales[si]);
   };
   if constexpr (FMT == I4_DENSE) {

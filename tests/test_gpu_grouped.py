@@ -1,9 +1,10 @@
-"""The grouped-stream kernel (stream_kernels.cu): INT4 2:4 with the
-reference's default fine groups (g_fine = 16, config.hpp:50-51; mixed with
-g_coarse = 64 per row) in the reference's own stream order, against the
-port's f32 spmv (packed.cpp:211-220): 7B shapes, M = 1..4, the fused rmsnorm
-/ silu inputs and residual / silu epilogue (model.cpp:57-67, 80-84, 186-190),
-and x over the whole f32 range (the kernel multiplies in f32)."""
+"""INT4 2:4 with the reference's default fine groups (g_fine = 16,
+config.hpp:50-51; mixed with g_coarse = 64 per row) against the port's f32
+spmv (packed.cpp:211-220): on the tiled path (16-column scale entries, two
+mma.sp per k-tile; cols % 32 == 0) and on the grouped-stream kernel
+(reference-order stream, cols % 32 == 16): 7B shapes, M = 1..9, the fused
+rmsnorm / silu inputs and residual / silu epilogue (model.cpp:57-67, 80-84,
+186-190), x over the whole f32 range, bit-exact unpack."""
 import numpy as np
 import pytest
 
@@ -17,13 +18,13 @@ def _layer(port, rng, rows, cols, g):
 
     p, _, _ = make_int4(rng, rows, cols, 2, g, port)
     d = egt.DeviceMatrix.from_packed(to_product(p))
-    assert d.path == "general"
+    assert d.path == ("tiled-mma.sp" if cols % 32 == 0 else "general"), (cols, d.path)
     return p, d
 
 
-@pytest.mark.parametrize("shape", [(4096, 4096), (11008, 4096), (4096, 11008), (40, 96)])
+@pytest.mark.parametrize("shape", [(4096, 4096), (11008, 4096), (4096, 11008), (40, 96), (4096, 4080), (33, 112)])
 @pytest.mark.parametrize("groups", ["g16", "g16/64"])
-@pytest.mark.parametrize("M", [1, 2, 4])
+@pytest.mark.parametrize("M", [1, 2, 4, 9])
 def test_grouped_products(port, shape, groups, M):
     import torch
 
@@ -39,14 +40,15 @@ def test_grouped_products(port, shape, groups, M):
         assert ok, (shape, groups, M, m, err)
 
 
-def test_grouped_fused(port):
-    """y = silu(res + rmsnorm(x) W^T) and y = silu(x) W^T on the grouped path."""
+@pytest.mark.parametrize("cols", [1024, 1008])
+def test_grouped_fused(port, cols):
+    """y = silu(res + rmsnorm(x) W^T) and y = silu(x) W^T (tiled / stream)."""
     import torch
 
     from paper_2605_11582_b200 import native as N
 
     rng = np.random.default_rng(5)
-    rows, cols, M = 256, 1024, 2
+    rows, M = 256, 2
     p, d = _layer(port, rng, rows, cols, 16)
     xs = rng.uniform(-2, 2, (M, cols)).astype(np.float32)
     res = rng.uniform(-1, 1, (M, rows)).astype(np.float32)
@@ -69,13 +71,14 @@ def test_grouped_fused(port):
         assert ok, (m, err)
 
 
-def test_grouped_x_range(port):
-    """f32 arithmetic: huge / tiny / non-finite x give the reference's values,
-    NaN / inf at the same positions."""
+@pytest.mark.parametrize("cols", [512, 496])
+def test_grouped_x_range(port, cols):
+    """Huge / tiny / non-finite x give the reference's values, NaN / inf at
+    the same positions (tiled: window scaling + exact fix-up; stream: f32)."""
     import torch
 
     rng = np.random.default_rng(9)
-    rows, cols = 64, 512
+    rows = 64
     p, d = _layer(port, rng, rows, cols, 16)
     for kind in ("huge", "tiny", "inf", "nan"):
         x = rng.uniform(-1, 1, cols).astype(np.float32)
@@ -104,7 +107,7 @@ def test_grouped_many_tokens_wide(port, M):
     import torch
 
     rng = np.random.default_rng(M)
-    p, d = _layer(port, rng, 256, 11008, 16)
+    p, d = _layer(port, rng, 256, 11008, 16)  # tiled; the stream kernel's wide case is 4080 above
     xs = rng.uniform(-1, 1, (M, 11008)).astype(np.float32)
     y = d.spmv(torch.from_numpy(xs).cuda()).cpu().numpy()
     for m in range(M):
@@ -127,3 +130,16 @@ def test_grouped_model_forward(port):
         got = model.forward(tokens, pos, vis).cpu().numpy()
         want = oracle_forward(tokens, pos, vis)
         assert _close(got, want) <= 1e-3, (M, _close(got, want))
+
+
+@pytest.mark.parametrize("groups", ["g16", "g16/64"])
+def test_grouped_unpack_bit_exact(port, groups):
+    """unpack (packed.cpp:197-209) of a tiled g16 handle: values and keep mask."""
+    rng = np.random.default_rng(13)
+    rows, cols = 48, 256
+    g = 16 if groups == "g16" else np.where(np.arange(rows) % 2 == 0, 16, 64).astype(np.uint32)
+    p, d = _layer(port, rng, rows, cols, g)
+    want_v, want_m = port.unpack(p)
+    got_v, got_m = d.dequant()
+    assert np.array_equal(got_v.cpu().numpy().view(np.uint32), want_v.view(np.uint32))
+    assert np.array_equal(got_m, want_m)

@@ -78,7 +78,9 @@ def test_general_path_any_group(egt, port, torch, n):
     rng = np.random.default_rng(31)
     for rows, cols, g in ((7, 36, 4), (64, 512, 16), (40, 200, 48), (3, 8, 8), (128, 1000, 100)):
         p, _, _ = make_int4(rng, rows, cols, n, g, port)
-        _check_product(egt, port, torch, p, rng, expect_path="general")
+        # 16-column groups on 32-column k-tiles run tiled (two mma.sp per k-tile)
+        path = "tiled-mma.sp" if g % 16 == 0 and cols % 32 == 0 else "general"
+        _check_product(egt, port, torch, p, rng, expect_path=path)
 
 
 @pytest.mark.parametrize("n", [1, 2])
