@@ -850,14 +850,19 @@ UmmaPlan plan_umma(const egt_dev_packed* h, int M, int num_sms) {
   p.TT = (M + p.T - 1) / p.T;
   const int KQ = h->tiled.KQ;
   const int R = (h->tiled.RT + 7) / 8;
-  // split K while it removes a wave: cost ~ waves x k-quads per CTA
+  // cost ~ waves x (k-quads per CTA + a fixed CTA cost in k-quads: ~8 for
+  // the prologue and output tail, ~14 with the cluster's split-K reduction);
+  // fitted to EGT_UMMA_S sweeps of tools/umma_probe.py (7B shapes, M = 80 /
+  // 272: e.g. 4096^2 at M = 272 S = 1 49 us vs S = 3 66 us)
   double best = 1e300;
+  static const int s_env = getenv("EGT_UMMA_S") ? atoi(getenv("EGT_UMMA_S")) : 0;  // tuning
   for (int S = 1; S <= std::min(8, KQ); ++S) {  // S CTAs form one cluster (portable size <= 8)
+    if (s_env > 0 && S != std::min(s_env, KQ)) continue;
     const int kqc = (KQ + S - 1) / S;
     const int Seff = (KQ + kqc - 1) / kqc;
     const long long ctas = static_cast<long long>(R) * p.TT * Seff;
     const double waves = std::ceil(static_cast<double>(ctas) / num_sms);
-    const double cost = waves * (kqc + 1.5) + (Seff > 1 ? 0.75 : 0.0);
+    const double cost = waves * (kqc + (Seff > 1 ? 14.0 : 8.0));
     if (cost < best - 1e-9) {
       best = cost;
       p.S = Seff;
@@ -907,11 +912,9 @@ bool umma_eligible(const egt_dev_packed* h, int M) {
   const int f = h->format;
   if (f != I4_SP24 && f != I4_DENSE && f != F16_SP24) return false;
   if (has_scales(f) && h->tiled.SS != 4 && h->tiled.SS != 2) return false;
-  static const bool always = getenv("EGT_UMMA_ALWAYS") != nullptr;
-  // measured (tools/umma_probe.py, B200): one token tile, or tall matrices
-  // whose many row blocks amortise the per-stage issue cost, beat the
-  // mma.sp kernel; several tiles of a short matrix do not (yet)
-  return always || M <= kMaxT || h->rows >= 8192;
+  // measured (tools/umma_probe.py, B200, k-quad ring slots): faster than the
+  // mma.sp kernel at every 7B verify shape, M = 80 and 272
+  return true;
 }
 
 size_t umma_workspace_bytes(const egt_dev_packed* h, int M) {
