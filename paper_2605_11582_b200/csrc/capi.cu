@@ -729,6 +729,44 @@ egt_status egt_spmv_ex(const egt_dev_packed* h, const float* x, float* y, uint32
   return spmv_impl(h, x, y, M, ldx, ldy, flags, nullptr, 0, EGT_INPUT_NONE, 0.f, nullptr, stream);
 }
 
+egt_status egt_spmm_multi(const egt_dev_packed* const* hs, uint32_t n, const float* x, uint32_t M, uint32_t ldx,
+                          float* const* ys, uint32_t ldy, void* stream) {
+  if (!hs || !ys || n == 0 || n > 3) return fail(EGT_EINVAL, "spmm multi: 1 to 3 matrices");
+  const egt_dev_packed* h = hs[0];
+  if (!h || (!x && M > 0)) return fail(EGT_EINVAL, "spmm multi: null argument");
+  bool same = true;
+  for (uint32_t i = 0; i < n; ++i) {
+    const egt_dev_packed* g = hs[i];
+    if (!g || !ys[i]) return fail(EGT_EINVAL, "spmm multi: null argument");
+    if (g->cols != h->cols) return fail(EGT_EINVAL, "spmm multi: matrices must share their columns");
+    same = same && g->path == h->path && g->rows == h->rows && g->format == h->format &&
+           g->tiled.KQ == h->tiled.KQ && g->tiled.SS == h->tiled.SS && g->tiled.pad14 == h->tiled.pad14;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (n > 1 && same && M > 16 && h->cols > 0 && h->rows > 0 && umma_eligible(h, static_cast<int>(M))) {
+    if (ldx < h->cols || ldy < h->rows) return fail(EGT_EINVAL, "spmm multi: leading dimension too small");
+    LaunchCtx ctx;
+    ctx.stream = s;
+    ctx.pdl = g_pdl;
+    const int ns = num_sms();
+    const size_t xs = (umma_workspace_bytes(h, static_cast<int>(M)) + 255) / 256 * 256;
+    const size_t pf = umma_partial_floats(h, static_cast<int>(M), ns);
+    Workspace* w = nullptr;
+    egt_status st = get_workspace(s, xs / 4 + pf, umma_counters(h, static_cast<int>(M), ns), &w);
+    if (st != EGT_OK) return st;
+    ctx.partial = w->partial + xs / 4;
+    ctx.counters = w->counters;
+    CUDA_TRY(launch_umma_multi(hs, static_cast<int>(n), x, static_cast<int>(ldx), static_cast<int>(M), ys,
+                               static_cast<int>(ldy), reinterpret_cast<uint8_t*>(w->partial), ctx, ns));
+    return EGT_OK;
+  }
+  for (uint32_t i = 0; i < n; ++i) {
+    const egt_status st = egt_spmv_ex(hs[i], x, ys[i], M, ldx, ldy, i ? EGT_SPMV_INDEPENDENT : 0u, stream);
+    if (st != EGT_OK) return st;
+  }
+  return EGT_OK;
+}
+
 egt_status egt_spmv_fused_multi(const egt_dev_packed* const* hs, uint32_t n, const float* x, float* const* ys,
                                 uint32_t input, float eps, uint32_t flags, void* stream) {
   if (!hs || !ys || n == 0 || n > 3) return fail(EGT_EINVAL, "spmv multi: 1 to 3 matrices");

@@ -156,6 +156,9 @@ size_t umma_partial_floats(const egt_dev_packed* h, int M, int num_sms);
 size_t umma_counters(const egt_dev_packed* h, int M, int num_sms);
 cudaError_t launch_umma(const egt_dev_packed* h, const float* x, int ldx, int M, float* y, int ldy,
                         uint8_t* ws, const LaunchCtx& ctx, int num_sms);
+// nseg (<= 3) same-shape matrices over the same x in one launch (no residual)
+cudaError_t launch_umma_multi(const egt_dev_packed* const* hs, int nseg, const float* x, int ldx, int M,
+                              float* const* ys, int ldy, uint8_t* ws, const LaunchCtx& ctx, int num_sms);
 size_t wide_workspace_bytes(const egt_dev_packed* h, int M);
 cudaError_t launch_wide(const egt_dev_packed* h, const float* x, int ldx, int M, float* y, int ldy,
                         uint32_t* xf_ws, const LaunchCtx& ctx, int num_sms);

@@ -539,6 +539,21 @@ egt_status forward_core(const egt_model* m, const int32_t* tokens, const int32_t
   const size_t kv_ints = kv ? M + (gather ? M + 1ull + kv->key_ptr[M] : 0) : 0;
   const size_t floats = 6 * Md + M * dff + (gather ? 0 : H * static_cast<size_t>(M) * M);
   char* scratch = nullptr;
+  {
+    // keep the stream-ordered pool's memory across passes: with the default
+    // release threshold (0) every synchronisation returns it and the next
+    // pass maps it again (measured: verify passes jittering 6.8 -> 11 ms)
+    static bool pool_kept = false;
+    if (!pool_kept) {
+      int dev = 0;
+      cudaMemPool_t pool;
+      if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t keep = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+      pool_kept = true;
+    }
+  }
   MCUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch),
                         floats * sizeof(float) + 2 * M * sizeof(int) + mask_bytes + tree_ints * 4 + kv_ints * 4 + 64,
                         s));
@@ -617,9 +632,16 @@ egt_status forward_core(const egt_model* m, const int32_t* tokens, const int32_t
     const egt_dev_packed* const* w = m->layers.data() + 6 * l;
     rmsnorm(x, a);
     ++launch_counter();
-    lin(w[0], a, q, 0);
-    lin(w[1], a, k, EGT_SPMV_INDEPENDENT);  // K and V read `a`, not the previous product
-    lin(w[2], a, v, EGT_SPMV_INDEPENDENT);
+    static const bool no_multi = getenv("EGT_NO_QKV_MULTI") != nullptr;  // tuning: three launches
+    if (M > 16 && !no_multi) {  // one tcgen05 launch over Q, K, V (one x preparation)
+      const egt_dev_packed* qkv[3] = {w[0], w[1], w[2]};
+      float* outs[3] = {q, k, v};
+      if (st == EGT_OK) st = egt_spmm_multi(qkv, 3, a, static_cast<uint32_t>(M), w[0]->cols, outs, w[0]->rows, stream);
+    } else {
+      lin(w[0], a, q, 0);
+      lin(w[1], a, k, EGT_SPMV_INDEPENDENT);  // K and V read `a`, not the previous product
+      lin(w[2], a, v, EGT_SPMV_INDEPENDENT);
+    }
     if (kv) {  // this pass's keys / values into the pool (the rows later passes attend to)
       const size_t lo = static_cast<size_t>(l) * kv->pool->capacity * d;
       kv_store_kernel<<<M, 256, 0, s>>>(k, v, kv->pool->k + lo, kv->pool->v + lo, d_out_rows, static_cast<int>(M),

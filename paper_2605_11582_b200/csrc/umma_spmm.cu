@@ -74,17 +74,22 @@ static_assert(kScaleRing > 2 * kMaxNA + 2, "scale ring too shallow");
 // the 512 TMEM columns
 constexpr int kMaxT = 96;
 
+constexpr int kMaxSeg = 3;  // same-shape matrices of one launch (Q, K, V)
+
 struct UmmaArgs {
-  // 2-D tensor maps over the handle's row tiles (int64 elements): values,
-  // metadata, zero points; box = one raw stage of 8 row tiles
-  CUtensorMap tm_vals, tm_meta, tm_zps, tm_scales;
+  // per segment (matrix): 2-D tensor maps over the handle's row tiles (int64
+  // elements) of values, metadata, zero points, scales; box = one raw stage
+  // of 8 row tiles
+  CUtensorMap tm[kMaxSeg][4];
+  int nseg, RB1;  // segments; 128-row blocks per segment (blockIdx.x = seg * RB1 + block)
   int NX;  // x ring depth
   int NA;  // A ring depth
-  const uint8_t* vals;
-  const uint8_t* meta;
-  const float* scales;
-  const uint8_t* zps;
-  int KQ, rt_begin, RT, rows, SS, E;
+  const uint8_t* vals[kMaxSeg];
+  const uint8_t* meta[kMaxSeg];
+  const float* scales[kMaxSeg];
+  const uint8_t* zps[kMaxSeg];
+  int rt_begin[kMaxSeg];
+  int KQ, RT, rows, SS, E;
   const uint8_t* xf;  // B stages [tile][k-stage][N rows x 64 K fp16, canonical K-major]
   const float* unsc;  // per padded token: 2^-e (xrange.cuh)
   const uint32_t* nonfin;
@@ -95,7 +100,7 @@ struct UmmaArgs {
   int KS;       // B k-stages of the whole K (2 per k-quad)
   int KQC;      // k-quads per CTA (the split size)
   int S;        // K splits (gridDim.z)
-  float* y;
+  float* y[kMaxSeg];
   int ldy;
   const float* res;
   int ldr;
@@ -270,8 +275,8 @@ __device__ __forceinline__ uint32_t a_off(int r, int k) {
 }
 
 template <int FMT>
-__device__ __noinline__ float umma_nonfinite_terms(const UmmaArgs& a, int row, int tok, int c0, int c1) {
-  const TiledRef m{a.vals, a.meta, a.scales, a.zps, a.KQ, a.rt_begin, a.SS, a.pad14};
+__device__ __noinline__ float umma_nonfinite_terms(const UmmaArgs& a, int sg, int row, int tok, int c0, int c1) {
+  const TiledRef m{a.vals[sg], a.meta[sg], a.scales[sg], a.zps[sg], a.KQ, a.rt_begin[sg], a.SS, a.pad14};
   const float* xr = a.x + static_cast<size_t>(tok) * a.ldx;
   float add = 0.f;
   for (int c = c0; c < c1; ++c) {
@@ -294,7 +299,8 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const __grid_con
   unsigned long long* tr =
       (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) ? a.trace : nullptr;
   if (tr && tid == 0) tr[0] = umma_clock();
-  const int rt0 = blockIdx.x * 8;  // first 16-row tile of this CTA (128 rows)
+  const int sg = a.nseg > 1 ? static_cast<int>(blockIdx.x) / a.RB1 : 0;  // segment (matrix)
+  const int rt0 = (static_cast<int>(blockIdx.x) - sg * a.RB1) * 8;      // first 16-row tile of this CTA (128 rows)
   const int tile = blockIdx.y;     // token tile
   const int kq0 = blockIdx.z * a.KQC;
   const int KQC = min(a.KQC, a.KQ - kq0);
@@ -385,11 +391,11 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const __grid_con
         const int kq = kq0 + rs * kRawKQ;
         uint8_t* dst = raw_st + sr * raw_bytes;
         mbar_expect_tx(raw_full + sr, raw_bytes);  // full boxes (rows / k-quads past the matrix read as 0)
-        tma_load_2d(dst, &a.tm_vals, kq * (32 * VB / 8), rt0, raw_full + sr);
-        if (MB > 0) tma_load_2d(dst + 8 * VBq, &a.tm_meta, kq * (32 * MB / 8), rt0, raw_full + sr);
+        tma_load_2d(dst, &a.tm[sg][0], kq * (32 * VB / 8), rt0, raw_full + sr);
+        if (MB > 0) tma_load_2d(dst + 8 * VBq, &a.tm[sg][1], kq * (32 * MB / 8), rt0, raw_full + sr);
         if (kScaled) {
-          tma_load_2d(dst + 8 * (VBq + MBq), &a.tm_zps, kq * (a.E * 2), rt0, raw_full + sr);
-          tma_load_2d(dst + 8 * (VBq + MBq + ZBq), &a.tm_scales, kq * (a.E * 8), rt0, raw_full + sr);
+          tma_load_2d(dst + 8 * (VBq + MBq), &a.tm[sg][2], kq * (a.E * 2), rt0, raw_full + sr);
+          tma_load_2d(dst + 8 * (VBq + MBq + ZBq), &a.tm[sg][3], kq * (a.E * 8), rt0, raw_full + sr);
         }
       };
       for (int rs = 0; rs < NRAW; ++rs) issue_raw(rs);
@@ -660,7 +666,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const __grid_con
       for (int k = 0; k < th; ++k) {
         const int tl = c0 + k, tok = tile * T + tl;
         if (row_ok && tok < a.M && s_nonf[tl])
-          part[r * (T + 4) + tl] += umma_nonfinite_terms<FMT>(a, grow, tok, kc0, kc1);
+          part[r * (T + 4) + tl] += umma_nonfinite_terms<FMT>(a, sg, grow, tok, kc0, kc1);
       }
     }
     if (tr && lane == 0) tr[840 + warp - kEpiWarp0] = umma_clock();
@@ -747,7 +753,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const __grid_con
           if (tok < a.M) {
             float o = o4[u];
             if (a.out_silu) o = o * (1.0f / (1.0f + expf(-o)));  // model.cpp:80-84
-            a.y[static_cast<size_t>(tok) * a.ldy + grow] = o;
+            a.y[sg][static_cast<size_t>(tok) * a.ldy + grow] = o;
           }
         }
       }
@@ -843,13 +849,13 @@ struct UmmaPlan {
   size_t smem = 0;
 };
 
-UmmaPlan plan_umma(const egt_dev_packed* h, int M, int num_sms) {
+UmmaPlan plan_umma(const egt_dev_packed* h, int M, int num_sms, int nseg = 1) {
   UmmaPlan p;
   const int tiles = (M + kMaxT - 1) / kMaxT;
   p.T = ((M + tiles - 1) / tiles + 15) / 16 * 16;  // the MMA's N: a multiple of 16
   p.TT = (M + p.T - 1) / p.T;
   const int KQ = h->tiled.KQ;
-  const int R = (h->tiled.RT + 7) / 8;
+  const int R = nseg * ((h->tiled.RT + 7) / 8);
   // cost ~ waves x (k-quads per CTA + a fixed CTA cost in k-quads: ~8 for
   // the prologue and output tail, ~14 with the cluster's split-K reduction);
   // fitted to EGT_UMMA_S sweeps of tools/umma_probe.py (7B shapes, M = 80 /
@@ -983,12 +989,21 @@ cudaError_t umma_maps(const egt_dev_packed* h, const UmmaMaps** out) {
 
 cudaError_t launch_umma(const egt_dev_packed* h, const float* x, int ldx, int M, float* y, int ldy,
                         uint8_t* ws, const LaunchCtx& ctx, int num_sms) {
-  const UmmaMaps* maps = nullptr;
-  {
-    const cudaError_t e = umma_maps(h, &maps);
+  return launch_umma_multi(&h, 1, x, ldx, M, &y, ldy, ws, ctx, num_sms);
+}
+
+// One launch over nseg same-shape matrices (Q, K, V of a layer): one x
+// preparation, CTAs blockIdx.x = segment * RB1 + 128-row block.
+cudaError_t launch_umma_multi(const egt_dev_packed* const* hs, int nseg, const float* x, int ldx, int M,
+                              float* const* ys, int ldy, uint8_t* ws, const LaunchCtx& ctx, int num_sms) {
+  if (nseg < 1 || nseg > kMaxSeg) return cudaErrorInvalidValue;
+  const egt_dev_packed* h = hs[0];
+  const UmmaMaps* segmaps[kMaxSeg] = {};
+  for (int i = 0; i < nseg; ++i) {
+    const cudaError_t e = umma_maps(hs[i], &segmaps[i]);
     if (e != cudaSuccess) return e;
   }
-  const UmmaPlan p = plan_umma(h, M, num_sms);
+  const UmmaPlan p = plan_umma(h, M, num_sms, nseg);
   const int KS = 2 * h->tiled.KQ;
   uint8_t* xf = ws;
   float* unsc = reinterpret_cast<float*>(ws + static_cast<size_t>(p.TT) * KS * (2 * p.T) * kStageK * 2);
@@ -1010,16 +1025,21 @@ cudaError_t launch_umma(const egt_dev_packed* h, const float* x, int ldx, int M,
     ++launch_counter();
   }
   UmmaArgs a;
-  a.tm_vals = maps->vals;
-  a.tm_meta = maps->meta;
-  a.tm_zps = maps->zps;
-  a.tm_scales = maps->scales;
-  a.vals = h->tiled.vals;
-  a.meta = h->tiled.meta;
-  a.scales = h->tiled.scales;
-  a.zps = h->tiled.zps;
+  a.nseg = nseg;
+  a.RB1 = (h->tiled.RT + 7) / 8;
+  for (int i = 0; i < nseg; ++i) {
+    a.tm[i][0] = segmaps[i]->vals;
+    a.tm[i][1] = segmaps[i]->meta;
+    a.tm[i][2] = segmaps[i]->zps;
+    a.tm[i][3] = segmaps[i]->scales;
+    a.vals[i] = hs[i]->tiled.vals;
+    a.meta[i] = hs[i]->tiled.meta;
+    a.scales[i] = hs[i]->tiled.scales;
+    a.zps[i] = hs[i]->tiled.zps;
+    a.rt_begin[i] = hs[i]->tiled.rt_begin;
+    a.y[i] = ys[i];
+  }
   a.KQ = h->tiled.KQ;
-  a.rt_begin = h->tiled.rt_begin;
   a.RT = h->tiled.RT;
   a.rows = static_cast<int>(h->rows);
   a.SS = h->tiled.SS;
@@ -1037,7 +1057,6 @@ cudaError_t launch_umma(const egt_dev_packed* h, const float* x, int ldx, int M,
   a.KS = KS;
   a.KQC = p.KQC;
   a.S = p.S;
-  a.y = y;
   a.ldy = ldy;
   a.res = ctx.res;
   a.ldr = ctx.ldr;
@@ -1071,7 +1090,7 @@ cudaError_t launch_umma(const egt_dev_packed* h, const float* x, int ldx, int M,
   err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (err != cudaSuccess) return err;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((h->tiled.RT + 7) / 8, p.TT, p.S);
+  cfg.gridDim = dim3(nseg * a.RB1, p.TT, p.S);
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = ctx.stream;

@@ -93,3 +93,26 @@ def test_umma_sass_is_tcgen05():
     if out.returncode != 0 or not sass:
         pytest.skip("cuobjdump unavailable")
     assert "UTCHMMA" in sass and "LDTM" in sass and "UBLKCP" in sass
+
+
+@pytest.mark.parametrize("fmt", ["int4-2:4", "fp16-2:4", "int4-dense"])
+@pytest.mark.parametrize("M", [40, 272])
+def test_umma_multi_segments(port, fmt, M):
+    """egt_spmm_multi: Q, K, V in one tcgen05 launch (one x preparation, CTAs
+    per segment) give each matrix's own product."""
+    import torch
+
+    from paper_2605_11582_b200.packed import spmm_multi
+
+    rng = np.random.default_rng(M + 7)
+    rows, cols = 384, 1024
+    mats = [_layer(port, rng, fmt, rows, cols) for _ in range(3)]
+    xs = rng.uniform(-1, 1, (M, cols)).astype(np.float32)
+    x = torch.from_numpy(xs).cuda()
+    ys = [torch.empty((M, rows), device="cuda") for _ in range(3)]
+    spmm_multi([d for d, _ in mats], x, ys)
+    for (d, ref), y in zip(mats, ys):
+        got = y.cpu().numpy()
+        for m in range(0, M, 7):
+            ok, err = close(got[m], ref(xs[m]))
+            assert ok, (fmt, M, m, err)

@@ -31,13 +31,16 @@ def main():
     pos = np.arange(M, dtype=np.int32)
     model.forward(toks, pos, vis)
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(3):
+    ts = []
+    for _ in range(10):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
         model.forward(toks, pos, vis)
-    e1.record()
-    e1.synchronize()
-    print(f"M={M} layers={layers_n}: {e0.elapsed_time(e1) / 3:.2f} ms", flush=True)
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ts.sort()
+    print(f"M={M} layers={layers_n}: median {ts[len(ts) // 2]:.2f} ms (min {ts[0]:.2f}, max {ts[-1]:.2f})", flush=True)
 
 
 if __name__ == "__main__":
