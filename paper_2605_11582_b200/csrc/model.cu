@@ -240,42 +240,84 @@ __global__ void __launch_bounds__(256) fused_attention_kernel(const float* __res
 // The 16-row kernel above re-read every key row from L2 per (row, key) pair
 // and ran latency-bound (152 us per layer at M = 272, dh = 128).
 constexpr int kAttnRows2 = 32, kAttnKeys = 32;
-__host__ __device__ inline size_t attn2_smem(int M, int dh) {
-  const int ldp = (M + kAttnKeys - 1) / kAttnKeys * kAttnKeys;
+__host__ __device__ inline int attn2_ldp(int M) {  // +4: conflict-free A-fragment reads of the scores
+  return (M + kAttnKeys - 1) / kAttnKeys * kAttnKeys + 4;
+}
+// resident: every key / value chunk in shared memory at once (one L2 round
+// trip for K, one for V; otherwise a double-buffered ring of chunks, each a
+// round trip on the critical path: measured latency-bound, 68 us per layer at
+// M = 272 whatever the arithmetic)
+__host__ __device__ inline size_t attn2_smem(int M, int dh, bool resident = false) {
+  const int ldp = attn2_ldp(M), nchunk = (M + kAttnKeys - 1) / kAttnKeys;
   return (static_cast<size_t>(kAttnRows2) * (dh + 4) + static_cast<size_t>(kAttnRows2) * ldp +
-          2 * static_cast<size_t>(kAttnKeys) * (dh + 4)) * sizeof(float);
+          (resident ? nchunk : 2) * static_cast<size_t>(kAttnKeys) * (dh + 4)) * sizeof(float);
 }
 __device__ __forceinline__ void cp_async16(float* dst, const float* src, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(egt_dev::smem_u32(dst)), "l"(src),
                "r"(valid ? 16 : 0)
                : "memory");
 }
+// f32 = tf32 hi + tf32 lo (~21 bits); a product of two split values kept to
+// three tensor-core terms (hi*hi + hi*lo + lo*hi: the dropped lo*lo is
+// ~2^-22 of it), accumulated in f32
+// The tf32 MMA reads the top 19 bits of each f32 register (truncation), so
+// the split is a mask and an exact subtraction (cvt.rna.tf32 compiles to ~5
+// instructions and made the kernel issue-bound: 69 us at M = 272).
+__device__ __forceinline__ void tf32_split(float x, uint32_t& hi, uint32_t& lo) {
+  const uint32_t h = __float_as_uint(x) & 0xffffe000u;
+  hi = h;
+  lo = __float_as_uint(x - __uint_as_float(h));
+}
+__device__ __forceinline__ void mma_tf32(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                         uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+// d += A (16 x 8, rows g / g + 8, columns t / t + 4) * B (8 x 8, k t / t + 4, n g), 3xTF32
+__device__ __forceinline__ void mma_3xtf32(float (&d)[4], const float (&a)[4], const float (&b)[2]) {
+  uint32_t ah[4], al[4], bh[2], bl[2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) tf32_split(a[i], ah[i], al[i]);
+  tf32_split(b[0], bh[0], bl[0]);
+  tf32_split(b[1], bh[1], bl[1]);
+  mma_tf32(d, al[0], al[1], al[2], al[3], bh[0], bh[1]);
+  mma_tf32(d, ah[0], ah[1], ah[2], ah[3], bl[0], bl[1]);
+  mma_tf32(d, ah[0], ah[1], ah[2], ah[3], bh[0], bh[1]);
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
+// MMA: q k^T and p V on the tensor cores in 3xTF32 (dh % 32 == 0): warp w
+// owns rows 16 (w & 1) and keys 8 (w >> 1) of a chunk (scores), rows 16 (w & 1)
+// and columns dh / 4 * (w >> 1) (output).
+template <bool MMA>
 __global__ void __launch_bounds__(256) attention_tile_kernel(const float* __restrict__ q, const float* __restrict__ k,
                                                              const float* __restrict__ v, float* __restrict__ o,
                                                              const uint8_t* __restrict__ mask, int M, int d, int dh,
-                                                             float scale) {
+                                                             float scale, int resident) {
   extern __shared__ __align__(16) float sm[];
-  const int ldq = dh + 4, ldp = (M + kAttnKeys - 1) / kAttnKeys * kAttnKeys, n4 = dh / 4;
+  const int ldq = dh + 4, ldp = attn2_ldp(M), n4 = dh / 4;
   float* qs = sm;                     // [32][dh + 4]
   float* ps = qs + kAttnRows2 * ldq;  // [32][ldp]
-  float* kb = ps + kAttnRows2 * ldp;  // 2 x [32][dh + 4]
+  float* kb = ps + kAttnRows2 * ldp;  // 2 (resident: nchunk) x [32][dh + 4]
   const int q0 = blockIdx.x * kAttnRows2, h = blockIdx.y, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nr = min(kAttnRows2, M - q0);
   const size_t hoff = static_cast<size_t>(h) * dh;
   const int nchunk = (M + kAttnKeys - 1) / kAttnKeys;
-  // chunk c of keys (src = k) or values (src = v) into buffer c & 1
+  // chunk c of keys (src = k) or values (src = v) into buffer c & 1 (resident: c)
+  auto buf = [&](int c) { return kb + (resident ? c : (c & 1)) * kAttnKeys * ldq; };
   auto stage = [&](const float* src, int c) {
-    float* dst = kb + (c & 1) * kAttnKeys * ldq;
+    float* dst = buf(c);
     for (int f = tid; f < kAttnKeys * n4; f += blockDim.x) {
       const int key = f / n4, e4 = f % n4, kk = c * kAttnKeys + key;
       cp_async16(dst + key * ldq + 4 * e4, src + static_cast<size_t>(kk < M ? kk : 0) * d + hoff + 4 * e4, kk < M);
     }
     cp_async_commit();
   };
-  stage(k, 0);
+  for (int c = 0; c < (resident ? nchunk : 1); ++c) stage(k, c);
   for (int f = tid; f < kAttnRows2 * n4; f += blockDim.x) {
     const int r = f / n4, e4 = f % n4;
     cp_async16(qs + r * ldq + 4 * e4, q + static_cast<size_t>(r < nr ? q0 + r : q0) * d + hoff + 4 * e4, r < nr);
@@ -283,10 +325,36 @@ __global__ void __launch_bounds__(256) attention_tile_kernel(const float* __rest
   cp_async_commit();
   // ---- phase 1: scores; thread -> key `lane` of the chunk, rows 4 warp .. 4 warp + 3
   for (int c = 0; c < nchunk; ++c) {
-    if (c + 1 < nchunk) stage(k, c + 1); else cp_async_commit();
-    cp_async_wait1();  // chunk c (and q) landed
-    __syncthreads();
-    const float* ks = kb + (c & 1) * kAttnKeys * ldq;
+    if (!resident) {
+      if (c + 1 < nchunk) stage(k, c + 1); else cp_async_commit();
+      cp_async_wait1();  // chunk c (and q) landed
+      __syncthreads();
+    } else if (c == 0) {
+      cp_async_wait0();  // every chunk and q
+      __syncthreads();
+    }
+    const float* ks = buf(c);
+    if constexpr (MMA) {
+      const int g = lane >> 2, t = lane & 3, rm = 16 * (warp & 1), kn = 8 * (warp >> 1);
+      float dacc[4] = {0.f, 0.f, 0.f, 0.f};
+      const float* qa = qs + (rm + g) * ldq + t;
+      const float* kbp = ks + (kn + g) * ldq + t;
+#pragma unroll 4
+      for (int e0 = 0; e0 < dh; e0 += 8) {
+        const float af[4] = {qa[e0], qa[8 * ldq + e0], qa[e0 + 4], qa[8 * ldq + e0 + 4]};
+        const float bf[2] = {kbp[e0], kbp[e0 + 4]};
+        mma_3xtf32(dacc, af, bf);
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = rm + g + 8 * (i >> 1), kk = c * kAttnKeys + kn + 2 * t + (i & 1);
+        const size_t bit = static_cast<size_t>(q0 + r) * M + kk;
+        const bool vis = r < nr && kk < M && ((mask[bit >> 3] >> (bit & 7)) & 1);
+        ps[r * ldp + kk] = vis ? dacc[i] * scale : -INFINITY;
+      }
+      __syncthreads();
+      continue;
+    }
     float acc[4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) acc[i] = 0.f;
@@ -310,7 +378,9 @@ __global__ void __launch_bounds__(256) attention_tile_kernel(const float* __rest
     }
     __syncthreads();  // buffer c & 1 free for chunk c + 2
   }
-  stage(v, 0);  // values stream in while the softmax runs
+  // values stream in while the softmax runs (the keys' last reads are
+  // behind the loop's final barrier)
+  for (int c = 0; c < (resident ? nchunk : 1); ++c) stage(v, c);
   // ---- phase 2: masked softmax, one warp per row (an empty row -> 0)
   for (int r = warp; r < kAttnRows2; r += blockDim.x >> 5) {
     float* pr = ps + r * ldp;
@@ -338,12 +408,43 @@ __global__ void __launch_bounds__(256) attention_tile_kernel(const float* __rest
   float4 acc[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) acc[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+  float oacc[4][4];  // MMA: n-tiles of 8 columns x (rows g / g + 8, columns 2t / 2t + 1)
+#pragma unroll
+  for (int i = 0; i < 4; ++i) oacc[i][0] = oacc[i][1] = oacc[i][2] = oacc[i][3] = 0.f;
   for (int c = 0; c < nchunk; ++c) {
-    if (c + 1 < nchunk) stage(v, c + 1); else cp_async_commit();
-    cp_async_wait1();
-    __syncthreads();  // chunk c landed; scores final
-    if (tid < items) {
-      const float* vs = kb + (c & 1) * kAttnKeys * ldq;
+    if (!resident) {
+      if (c + 1 < nchunk) stage(v, c + 1); else cp_async_commit();
+      cp_async_wait1();
+      __syncthreads();  // chunk c landed; scores final
+    } else if (c == 0) {
+      cp_async_wait0();
+      __syncthreads();
+    }
+    if constexpr (MMA) {
+      const int g = lane >> 2, t = lane & 3, rm = 16 * (warp & 1), cn = (dh / 4) * (warp >> 1);
+      const float* vs = buf(c);
+      const float* pa = ps + (rm + g) * ldp + c * kAttnKeys + t;
+#pragma unroll
+      for (int k0 = 0; k0 < kAttnKeys; k0 += 8) {
+        const float af[4] = {pa[k0], pa[8 * ldp + k0], pa[k0 + 4], pa[8 * ldp + k0 + 4]};
+        uint32_t ah[4], al[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) tf32_split(af[i], ah[i], al[i]);
+#pragma unroll
+        for (int nt = 0; nt < 4; ++nt) {
+          if (8 * nt < dh / 4) {
+            const float* vb = vs + (k0 + t) * ldq + cn + 8 * nt + g;
+            uint32_t bh0, bl0, bh1, bl1;
+            tf32_split(vb[0], bh0, bl0);
+            tf32_split(vb[4 * ldq], bh1, bl1);
+            mma_tf32(oacc[nt], al[0], al[1], al[2], al[3], bh0, bh1);
+            mma_tf32(oacc[nt], ah[0], ah[1], ah[2], ah[3], bl0, bl1);
+            mma_tf32(oacc[nt], ah[0], ah[1], ah[2], ah[3], bh0, bh1);
+          }
+        }
+      }
+    } else if (tid < items) {
+      const float* vs = buf(c);
       const float* pc = ps + (4 * rg) * ldp + c * kAttnKeys;
 #pragma unroll 4
       for (int j = 0; j < kAttnKeys; ++j) {  // keys past M: zero values and zero p
@@ -360,7 +461,20 @@ __global__ void __launch_bounds__(256) attention_tile_kernel(const float* __rest
     }
     __syncthreads();
   }
-  if (tid < items) {
+  if constexpr (MMA) {
+    const int g = lane >> 2, t = lane & 3, rm = 16 * (warp & 1), cn = (dh / 4) * (warp >> 1);
+#pragma unroll
+    for (int nt = 0; nt < 4; ++nt) {
+      if (8 * nt >= dh / 4) break;
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh) {
+        const int r = rm + g + 8 * hh;
+        if (r < nr)
+          *reinterpret_cast<float2*>(o + static_cast<size_t>(q0 + r) * d + hoff + cn + 8 * nt + 2 * t) =
+              make_float2(oacc[nt][2 * hh], oacc[nt][2 * hh + 1]);
+      }
+    }
+  } else if (tid < items) {
 #pragma unroll
     for (int i = 0; i < 4; ++i)
       if (4 * rg + i < nr)
@@ -621,12 +735,18 @@ egt_status forward_core(const egt_model* m, const int32_t* tokens, const int32_t
                                static_cast<int>(attn_smem)));
   // the 64-row staged kernel where its tiles fit (dh <= 128)
   static const bool old_attn = getenv("EGT_ATTN16") != nullptr;
-  const size_t attn2 = attn2_smem(static_cast<int>(M), static_cast<int>(dh));
+  const bool attn_res = attn2_smem(static_cast<int>(M), static_cast<int>(dh), true) <= 200 * 1024;
+  const size_t attn2 = attn2_smem(static_cast<int>(M), static_cast<int>(dh), attn_res);
   const bool tile_attn = !no_fused && !old_attn && dh % 4 == 0 && dh / 4 <= 256 / (kAttnRows2 / 4) &&
                          attn2 <= 200 * 1024;
-  if (tile_attn && attn2 > 48 * 1024)
-    MCUDA(cudaFuncSetAttribute(attention_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  static const bool no_attn_mma = getenv("EGT_ATTN_NO_MMA") != nullptr;  // tuning: CUDA-core phases
+  const bool attn_mma = !no_attn_mma && dh % 32 == 0 && dh <= 128;
+  if (tile_attn && attn2 > 48 * 1024) {
+    MCUDA(cudaFuncSetAttribute(attention_tile_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(attn2)));
+    MCUDA(cudaFuncSetAttribute(attention_tile_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(attn2)));
+  }
   const dim3 tb(16, 16);
   for (uint32_t l = 0; l < c.n_layers && st == EGT_OK; ++l) {
     const egt_dev_packed* const* w = m->layers.data() + 6 * l;
@@ -656,8 +776,12 @@ egt_status forward_core(const egt_model* m, const int32_t* tokens, const int32_t
           static_cast<int>(dh), att_scale);
       ++launch_counter();
     } else if (tile_attn) {
-      attention_tile_kernel<<<dim3((M + kAttnRows2 - 1) / kAttnRows2, H), 256, attn2, s>>>(
-          q, k, v, o, dmask, static_cast<int>(M), static_cast<int>(d), static_cast<int>(dh), att_scale);
+      if (attn_mma)
+        attention_tile_kernel<true><<<dim3((M + kAttnRows2 - 1) / kAttnRows2, H), 256, attn2, s>>>(
+            q, k, v, o, dmask, static_cast<int>(M), static_cast<int>(d), static_cast<int>(dh), att_scale, attn_res);
+      else
+        attention_tile_kernel<false><<<dim3((M + kAttnRows2 - 1) / kAttnRows2, H), 256, attn2, s>>>(
+            q, k, v, o, dmask, static_cast<int>(M), static_cast<int>(d), static_cast<int>(dh), att_scale, attn_res);
       ++launch_counter();
     } else if (fused_attn) {
       fused_attention_kernel<<<dim3((M + kAttnRows - 1) / kAttnRows, H), 256, attn_smem, s>>>(
