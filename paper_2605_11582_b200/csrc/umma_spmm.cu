@@ -864,6 +864,11 @@ UmmaPlan plan_umma(const egt_dev_packed* h, int M, int num_sms, int nseg = 1) {
   static const int s_env = getenv("EGT_UMMA_S") ? atoi(getenv("EGT_UMMA_S")) : 0;  // tuning
   for (int S = 1; S <= std::min(8, KQ); ++S) {  // S CTAs form one cluster (portable size <= 8)
     if (s_env > 0 && S != std::min(s_env, KQ)) continue;
+    // several token tiles: every CTA re-reads its tile's x stages from L2
+    // (T x 512 B per k-quad, ~5x the weights at T = 96), so more CTAs in
+    // flight only add L2 traffic: no split (measured S = 1 113 us vs S = 3
+    // 127 us for 4096 x 11008 at M = 272)
+    if (p.TT > 1 && S > 1 && s_env == 0) continue;
     const int kqc = (KQ + S - 1) / S;
     const int Seff = (KQ + kqc - 1) / kqc;
     const long long ctas = static_cast<long long>(R) * p.TT * Seff;
