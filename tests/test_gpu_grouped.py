@@ -143,3 +143,23 @@ def test_grouped_unpack_bit_exact(port, groups):
     got_v, got_m = d.dequant()
     assert np.array_equal(got_v.cpu().numpy().view(np.uint32), want_v.view(np.uint32))
     assert np.array_equal(got_m, want_m)
+
+
+def test_grouped_decode_loop(port):
+    """The KV-cached decode loop (egt_decoder_*) over g16 layers (fused Q/K/V,
+    rmsnorm / silu / residual on the 16-column-group kernels): the last
+    step's logits against the oracle's full-prefix forward."""
+    import torch
+
+    from paper_2605_11582_b200.model import Decoder
+    from tests.test_gpu_verify import CFG, build_model
+
+    model, oracle_forward = build_model(port, plan=[["int4-2:4"] * 6], group=16)
+    dec = Decoder(model, 40)
+    toks = dec.generate([3, 1, 4, 1, 5], 8)
+    n = len(toks) - 1
+    want = oracle_forward(np.array(toks[:n], np.int32), np.arange(n, dtype=np.int32), np.tril(np.ones((n, n), bool)))
+    logits = torch.empty(CFG["vocab_size"], device="cuda")
+    dec.read(logits)
+    err = np.abs(logits.cpu().numpy() - want[n - 1]) / (1 + np.abs(want[n - 1]))
+    assert err.max() <= 1e-3, err.max()
