@@ -82,6 +82,10 @@ struct UmmaArgs {
   // of 8 row tiles
   CUtensorMap tm[kMaxSeg][4];
   int nseg, RB1;  // segments; 128-row blocks per segment (blockIdx.x = seg * RB1 + block)
+  // 1: row blocks in pairs (cluster x = 2, S = 1) share the token tile's x
+  // stages: each CTA loads one 64-column half of a k-quad slot, multicast to
+  // both (L2 x traffic halved); a slot is refilled once both CTAs consumed it
+  int mcast;
   int NX;  // x ring depth
   int NA;  // A ring depth
   const uint8_t* vals[kMaxSeg];
@@ -181,6 +185,22 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
+// x halves multicast to both CTAs of a row-block pair (cluster x = 2)
+__device__ __forceinline__ void bulk_g2s_mcast(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], %4;\n" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "h"(mask)
+      : "memory");
+}
+// commit arriving on the same barrier offset in every CTA of `mask`
+__device__ __forceinline__ void umma_commit_mcast(uint64_t* bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+                   smem_addr(bar)),
+               "h"(mask)
+               : "memory");
+}
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                    smem_addr(bar))
@@ -356,7 +376,7 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const __grid_con
       // (one sub-stage each) + the x producer's arrive.expect_tx (and its
       // bytes); empty = one MMA commit
       mbar_init(a_full + i, kNumDeq + 1);
-      mbar_init(a_empty + i, 1);
+      mbar_init(a_empty + i, a.mcast ? 2 : 1);  // multicast: both CTAs' commits
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(tm_full + i, 1);
@@ -407,10 +427,15 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const __grid_con
       for (int u = 0; u < KQC; ++u) {  // one k-quad (two contiguous x stages) per slot
         const int s = u % kNA;
         if (u >= kNA) mbar_wait(a_empty + s, ((u / kNA) - 1) & 1);
-        mbar_expect_tx(a_full + s, 2 * x_bytes);
+        mbar_expect_tx(a_full + s, 2 * x_bytes);  // both halves land here (multicast: one from the peer)
         if (tr && u < 72) tr[8 + u] = umma_clock();
         const uint8_t* src = a.xf + (static_cast<size_t>(tile) * a.KS + 2 * (kq0 + u)) * x_bytes;
-        bulk_g2s_plain(x_st + s * 2 * x_bytes, src, 2 * x_bytes, a_full + s);
+        if (a.mcast) {
+          const int half = static_cast<int>(blockIdx.x & 1);
+          bulk_g2s_mcast(x_st + (s * 2 + half) * x_bytes, src + half * x_bytes, x_bytes, a_full + s, 3);
+        } else {
+          bulk_g2s_plain(x_st + s * 2 * x_bytes, src, 2 * x_bytes, a_full + s);
+        }
       }
     }
   } else if (warp == 1) {
@@ -455,7 +480,10 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const __grid_con
           if ((st + 1) % steps_per_scale == 0 || st + 1 == NSTG) umma_commit(tm_full + buf);
         }
         const long long c2 = ck ? clock64() : 0;
-        umma_commit(a_empty + u % kNA);
+        if (a.mcast) umma_commit_mcast(a_empty + u % kNA, 3);  // the peer's x producer reuses the slot too
+        else umma_commit(a_empty + u % kNA);
+        if (a.mcast && u + 1 == KQC)  // both CTAs' last commits landed here before the pair may exit
+          mbar_wait(a_empty + u % kNA, (u / kNA) & 1);
         if (ck) {
           const long long c3 = clock64();
           unsigned long long* o = tr + 900 + 8 * (u - 2);
@@ -707,7 +735,9 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const __grid_con
         for (int z = 0; z < 8; ++z) {
           if (z < a.S) {
             uint32_t remote;
-            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(remote) : "r"(part0 + off), "r"(z));
+            // cluster rank of slice z of this row block (x: the multicast pair)
+            const uint32_t zr = static_cast<uint32_t>(z * (a.mcast ? 2 : 1)) + (a.mcast ? (blockIdx.x & 1) : 0);
+            asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(remote) : "r"(part0 + off), "r"(zr));
             asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];\n"
                          : "=f"(v[b][z].x), "=f"(v[b][z].y), "=f"(v[b][z].z), "=f"(v[b][z].w)
                          : "r"(remote));
@@ -760,7 +790,11 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const __grid_con
     }
   }
   if (tr && tid == kEpiWarp0 * 32) tr[5] = umma_clock();
-  if (a.S == 1) return;
+  if (a.S == 1) {
+    if (a.mcast)  // the peer multicasts into this CTA's shared memory until it is done too
+      asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    return;
+  }
   // every slice's shared memory stays alive until the leader has read it
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
   if (tr && tid == 0) tr[6] = umma_clock();
@@ -864,10 +898,9 @@ UmmaPlan plan_umma(const egt_dev_packed* h, int M, int num_sms, int nseg = 1) {
   static const int s_env = getenv("EGT_UMMA_S") ? atoi(getenv("EGT_UMMA_S")) : 0;  // tuning
   for (int S = 1; S <= std::min(8, KQ); ++S) {  // S CTAs form one cluster (portable size <= 8)
     if (s_env > 0 && S != std::min(s_env, KQ)) continue;
-    // several token tiles: every CTA re-reads its tile's x stages from L2
-    // (T x 512 B per k-quad, ~5x the weights at T = 96), so more CTAs in
-    // flight only add L2 traffic: no split (measured S = 1 113 us vs S = 3
-    // 127 us for 4096 x 11008 at M = 272)
+    // several token tiles already fill the machine: no split (measured
+    // S = 1 113 us vs S = 3 127 us for 4096 x 11008 at M = 272: the second
+    // wave and the cluster reduction cost more than the shorter K range)
     if (p.TT > 1 && S > 1 && s_env == 0) continue;
     const int kqc = (KQ + S - 1) / S;
     const int Seff = (KQ + kqc - 1) / kqc;
@@ -1062,6 +1095,11 @@ cudaError_t launch_umma_multi(const egt_dev_packed* const* hs, int nseg, const f
   a.KS = KS;
   a.KQC = p.KQC;
   a.S = p.S;
+  // x multicast over row-block pairs: measured no faster (A/B at the 7B
+  // shapes, M = 272: within 2 %) -- the L2 x reads are not what bounds the
+  // kernel; kept as an option (EGT_UMMA_MCAST=1)
+  static const bool mcast = getenv("EGT_UMMA_MCAST") != nullptr;
+  a.mcast = mcast && p.S == 1 && p.TT > 1 && (nseg * a.RB1) % 2 == 0 ? 1 : 0;
   a.ldy = ldy;
   a.res = ctx.res;
   a.ldr = ctx.ldr;
@@ -1100,8 +1138,8 @@ cudaError_t launch_umma_multi(const egt_dev_packed* const* hs, int nseg, const f
   cfg.dynamicSmemBytes = smem;
   cfg.stream = ctx.stream;
   cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeClusterDimension;  // the split-K slices of a row block
-  attr[0].val.clusterDim.x = 1;
+  attr[0].id = cudaLaunchAttributeClusterDimension;  // the split-K slices of a row block (or row-block pairs)
+  attr[0].val.clusterDim.x = a.mcast ? 2 : 1;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = p.S;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
