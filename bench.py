@@ -645,23 +645,30 @@ def run_ours(args):
     per_shape = {}
     for s in sorted(set(LAYER_SHAPES)):
         sel = [d for d in layers if (d.rows, d.cols) == s]
-        sub = Sweep(sel, stream)
-        sub.capture()
-        for _ in range(3):
-            sub.replay()
-        reps = max(3, min(50, 20000 // len(sel)))
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        with torch.cuda.stream(stream):
-            e0.record(stream)
-            for _ in range(reps):
-                sub.replay()
-            e1.record(stream)
-        e1.synchronize()
-        us = 1e3 * e0.elapsed_time(e1) / (reps * len(sel))
         b = shape_bytes(host[s])
-        per_shape[f"{s[0]}x{s[1]}"] = {"us_per_call": round(us, 3), "GBps": round(b / us / 1e3, 1),
+        entry = {}
+        # independent launches (the sweep's), then the same calls each waiting
+        # for its predecessor (a decode chain's isolated single-GEMV cost)
+        for indep, key in ((True, "us_per_call"), (False, "dependent_us_per_call")):
+            sub = Sweep(sel, stream, independent=indep)
+            sub.capture()
+            for _ in range(3):
+                sub.replay()
+            reps = max(3, min(50, 20000 // len(sel)))
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                e0.record(stream)
+                for _ in range(reps):
+                    sub.replay()
+                e1.record(stream)
+            e1.synchronize()
+            entry[key] = round(1e3 * e0.elapsed_time(e1) / (reps * len(sel)), 3)
+            del sub
+        us = entry["us_per_call"]
+        per_shape[f"{s[0]}x{s[1]}"] = {"us_per_call": us, "GBps": round(b / us / 1e3, 1),
+                                       "dependent_us_per_call": entry["dependent_us_per_call"],
+                                       "dependent_GBps": round(b / entry["dependent_us_per_call"] / 1e3, 1),
                                        "bytes_per_call": b, "copies": len(sel)}
-        del sub
 
     # the other arms of the path at the 7B shapes -- 1:4, per-row
     # mixed group sizes, dense INT4 (quant_dense_gemv), sparse FP16 2:4 / 1:4 --
