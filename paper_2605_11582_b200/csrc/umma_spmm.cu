@@ -45,6 +45,9 @@
 #include "handle.h"
 #include "xrange.cuh"
 
+#ifndef EGT_UMMA_NR
+#define EGT_UMMA_NR 3
+#endif
 namespace egt_impl {
 using namespace egt_dev;
 using namespace egt_fmt;
@@ -62,7 +65,7 @@ __host__ __device__ constexpr int raw_kq(int fmt) { return fmt == egt_fmt::F16_S
 // a.NX).  The A ring spans the MMA -> commit -> dequantiser -> MMA round
 // trip (~2 us measured with EGT_UMMA_TRACE): 4 slots capped the kernel at
 // ~0.5 us per stage whatever the work.
-constexpr int kNR = 3, kMaxNA = 6;
+constexpr int kNR = EGT_UMMA_NR, kMaxNA = 6;
 // scale hand-off ring (rounds): the dequantisers run up to kMaxNA stages
 // (= rounds at 64-column groups) ahead of the MMA, the epilogue up to two
 // rounds behind it
@@ -249,19 +252,6 @@ __device__ __forceinline__ uint4 lds_v4(uint32_t addr) {
   asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
   return v;
 }
-// Non-suspending probe of an mbarrier phase.  Any mbarrier probe costs
-// ~220 cycles of latency (measured in the MMA loop, clock64): the MMA thread
-// probes the next stage's barriers before issuing this stage's MMAs and
-// commits, and only blocks when a probe said "not yet".
-__device__ __forceinline__ uint32_t mbar_probe(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n.reg .pred p;\nmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok;
-}
 // mbarrier wait that sleeps between probes (the epilogue waits a whole scale
 // step: polling would steal issue slots from the dequantisers)
 __device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
@@ -341,7 +331,6 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const __grid_con
   uint64_t* tm_full = a_empty + kMaxNA;
   uint64_t* tm_empty = tm_full + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tm_empty + 2);
-  __shared__ int s_last;
   __shared__ float s_unsc[kMaxT];
   __shared__ uint32_t s_nonf[kMaxT];
   __shared__ int s_anynf;  // some token of the tile has a non-finite x
