@@ -514,6 +514,40 @@ def measure_decode(torch, egt, plan_name, n_tokens=64, prompt_len=16, max_len=25
         verify[f"{n_nodes}_nodes"] = {"rows": M, "ms_per_pass": round(vms, 3),
                                       "tree_nodes_per_s": round(n_nodes / (vms * 1e-3), 1),
                                       "vs_sequential_decode": round(n_nodes * per_tok / vms, 2)}
+    # trie-constrained beam decode (decode.cpp:423-483) on a
+    # semantic-ID trie (8-way, depth 4: 4096 items; digit d -> token 4 + d),
+    # beam 4, autoregressive, with the KV-cached constrained step vs the
+    # reference's full-prefix recompute; host-driven loop, wall clock
+    beam_decode = None
+    if not os.environ.get("EGT_BENCH_NO_VERIFY"):
+        from paper_2605_11582_b200.model import Trie
+
+        token, parent, payload, frontier = [1], [0], [-1], [0]
+        for _ in range(4):
+            nxt = []
+            for nd in frontier:
+                for dg in range(8):
+                    token.append(4 + dg)
+                    parent.append(nd)
+                    payload.append(-1)
+                    nxt.append(len(token) - 1)
+            frontier = nxt
+        for i, nd in enumerate(frontier):
+            payload[nd] = i
+        trie = Trie(np.array(token, np.uint32), np.array(parent, np.uint32), np.array(payload, np.int64))
+        beam_decode = {"trie": "8-way x depth 4 (4096 items)", "beam": 4, "prompt": prompt_len}
+        for kv in (True, False):
+            model.decode(trie, prompt, beam_size=4, mode="autoregressive", kv_cache=kv)  # warm-up
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            reps = 3
+            for _ in range(reps):
+                out, st = model.decode(trie, prompt, beam_size=4, mode="autoregressive", kv_cache=kv)
+            torch.cuda.synchronize()
+            dms = (time.perf_counter() - t1) * 1e3 / reps
+            beam_decode["kv_cache" if kv else "recompute"] = {"ms_per_decode": round(dms, 3),
+                                                              "steps": st["steps"],
+                                                              "ms_per_step": round(dms / max(1, st["steps"]), 3)}
     res = {"plan": plan_name, "tokens_per_s": round(n_tokens / (ms * 1e-3), 1), "ms_per_token": round(per_tok, 4),
            "weight_bytes_per_token": weight_bytes,
            "weight_GBps": round(weight_bytes / (per_tok * 1e-3) / 1e9, 1),
@@ -523,7 +557,7 @@ def measure_decode(torch, egt, plan_name, n_tokens=64, prompt_len=16, max_len=25
            "e2e_note": f"generate(): H2D prompt, {prompt_len - 1} prefill positions + {n_tokens} generated tokens, "
                        "D2H tokens, host wall clock; tokens/s counts the generated tokens only",
            "finite_tokens": bool(all(0 <= t < cfg["vocab_size"] for t in toks2)), "setup_s": round(setup, 1),
-           "verify_pass": verify}
+           "verify_pass": verify, "constrained_beam_decode": beam_decode}
     del dec, model, layers, head
     torch.cuda.synchronize()
     return res

@@ -661,7 +661,7 @@ egt_status spmv_impl(const egt_dev_packed* h, const float* x, float* y, uint32_t
                             static_cast<int>(ldy), ctx));
     return EGT_OK;
   }
-  if (M > 16 && !pg && input == EGT_INPUT_NONE && !plan_forced() && umma_eligible(h, static_cast<int>(M))) {
+  if (M > 1 && !pg && input == EGT_INPUT_NONE && !plan_forced() && umma_eligible(h, static_cast<int>(M))) {
     // tcgen05 / TMEM many-token kernel (umma_spmm.cu): x stages + per-token
     // range, then split-K partials, in one per-stream workspace
     const int ns = num_sms();
@@ -743,7 +743,7 @@ egt_status egt_spmm_multi(const egt_dev_packed* const* hs, uint32_t n, const flo
            g->tiled.KQ == h->tiled.KQ && g->tiled.SS == h->tiled.SS && g->tiled.pad14 == h->tiled.pad14;
   }
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (n > 1 && same && M > 16 && h->cols > 0 && h->rows > 0 && umma_eligible(h, static_cast<int>(M))) {
+  if (n > 1 && same && M > 1 && h->cols > 0 && h->rows > 0 && umma_eligible(h, static_cast<int>(M))) {
     if (ldx < h->cols || ldy < h->rows) return fail(EGT_EINVAL, "spmm multi: leading dimension too small");
     LaunchCtx ctx;
     ctx.stream = s;

@@ -753,7 +753,7 @@ egt_status forward_core(const egt_model* m, const int32_t* tokens, const int32_t
     rmsnorm(x, a);
     ++launch_counter();
     static const bool no_multi = getenv("EGT_NO_QKV_MULTI") != nullptr;  // tuning: three launches
-    if (M > 16 && !no_multi) {  // one tcgen05 launch over Q, K, V (one x preparation)
+    if (M > 1 && !no_multi) {  // one tcgen05 launch over Q, K, V when the tokens take that path
       const egt_dev_packed* qkv[3] = {w[0], w[1], w[2]};
       float* outs[3] = {q, k, v};
       if (st == EGT_OK) st = egt_spmm_multi(qkv, 3, a, static_cast<uint32_t>(M), w[0]->cols, outs, w[0]->rows, stream);

@@ -941,7 +941,12 @@ unsigned long long* umma_trace_buffer() {
 
 bool umma_eligible(const egt_dev_packed* h, int M) {
   static const bool off = getenv("EGT_NO_UMMA") != nullptr;
-  if (off || M < 17 || h->path != 0) return false;
+  // from 9 tokens (tools/umma_probe.py, UMMA_PROBE_M=2,4,8,16: the tcgen05
+  // kernel is flat in M up to its 96-token tile -- 16 / 39 / 31 us for 4096^2,
+  // 11008 x 4096, 4096 x 11008 -- while the mma.sp token-tiled kernel grows:
+  // 19 / 25 / 28 us at M = 8, 34 / 88 / 91 us at M = 16)
+  static const int min_m = getenv("EGT_UMMA_MIN_M") ? atoi(getenv("EGT_UMMA_MIN_M")) : 9;
+  if (off || M < min_m || h->path != 0) return false;
   const int f = h->format;
   if (f != I4_SP24 && f != I4_DENSE && f != F16_SP24) return false;
   if (has_scales(f) && h->tiled.SS != 4 && h->tiled.SS != 2) return false;

@@ -34,7 +34,7 @@ def _layer(port, rng, fmt, rows, cols, group=128):
 
 
 @pytest.mark.parametrize("fmt", ["int4-2:4", "int4-1:4", "int4-dense", "fp16-2:4"])
-@pytest.mark.parametrize("M", [17, 80, 130, 272])
+@pytest.mark.parametrize("M", [9, 16, 17, 80, 130, 272])
 def test_umma_products(port, fmt, M):
     import torch
 

@@ -21,7 +21,7 @@ for rows, cols in [(4096, 4096), (11008, 4096), (4096, 11008), (32000, 4096)]:
     p = egt.pack(mask, egt.quantize_matrix(w, 128, mask), 2)
     copies = max(2, min(8, (256 << 20) // (rows * cols // 2)))
     mats = [egt.DeviceMatrix.from_packed(p) for _ in range(copies)]
-    for M in (80, 272):
+    for M in [int(v) for v in os.environ.get("UMMA_PROBE_M", "80,272").split(",")]:
         x = torch.from_numpy(rng.uniform(-1, 1, (M, cols)).astype(np.float32)).cuda()
         ys = [torch.empty((M, rows), device="cuda") for _ in mats]
         st = torch.cuda.Stream()
