@@ -545,43 +545,53 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
     }
   }
 #pragma unroll
+  // Several tokens: the n-tile's (up to 4) tokens are loaded together --
+  // every load of a pass in flight at once -- then converted; one token at a
+  // time put one L2 round trip per token on the critical path (M = 4: ~4 us
+  // of staging per dependent call).
+  constexpr int XJ = 4;  // float2 per thread per token per pass
   for (int nt = 0; nt < NT; ++nt) {
     const int mc = (a.dbg == 3 || staged) ? 0 : min(4, Mc - 4 * nt);
-    for (int m = 0; m < mc; ++m) {
-      const float* xr = a.x + static_cast<size_t>(m0 + 4 * nt + m) * a.ldx;
-      const float inv = FUSED && a.xform == EGT_INPUT_RMSNORM ? s_inv[4 * nt + m] : 1.f;
-      const int items = KTc * 16;
-      for (int i0 = 0; i0 < items; i0 += XU * static_cast<int>(blockDim.x)) {
-        float2 v[XU];
+    if (mc == 0) continue;
+    const int items = KTc * 16;
+    float inv[4];
+    uint32_t xbm[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
-        for (int u = 0; u < XU; ++u) {
-          int i = i0 + tid + u * blockDim.x;
-          if (a.dbg == 6 && i < items) i = (i + static_cast<int>(blockIdx.x) * 208) % items;  // tuning: spread L2 lines
-          v[u] = make_float2(0.f, 0.f);
-          if (i < items) {
+    for (int m = 0; m < 4; ++m) inv[m] = FUSED && a.xform == EGT_INPUT_RMSNORM && m < mc ? s_inv[4 * nt + m] : 1.f;
+    for (int i0 = 0; i0 < items; i0 += XJ * static_cast<int>(blockDim.x)) {
+      float2 v[4][XJ];
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const float* xr = a.x + static_cast<size_t>(m0 + 4 * nt + min(m, mc - 1)) * a.ldx;
+#pragma unroll
+        for (int u = 0; u < XJ; ++u) {
+          const int i = i0 + tid + u * static_cast<int>(blockDim.x);
+          v[m][u] = make_float2(0.f, 0.f);
+          if (m < mc && i < items) {
             const int k = (kq0 * 4 + (i >> 4)) * 32 + 2 * ((i >> 2) & 3) + 8 * (i & 3);
-            if (k < a.cols)
-              v[u] = bulk_x ? reinterpret_cast<const float2*>(sB)[(k - kq0 * 128) >> 1]
-                            : make_float2(__ldg(xr + k), __ldg(xr + k + 1));
+            if (k < a.cols) v[m][u] = make_float2(__ldg(xr + k), __ldg(xr + k + 1));
           }
         }
-        if (bulk_x) __syncthreads();  // in place: every raw value read before any fragment is written
+      }
 #pragma unroll
-        for (int u = 0; u < XU; ++u) {
-          int i = i0 + tid + u * blockDim.x;
-          if (a.dbg == 6 && i < items) i = (i + static_cast<int>(blockIdx.x) * 208) % items;
+      for (int m = 0; m < 4; ++m) {
+        if (m >= mc) break;
+#pragma unroll
+        for (int u = 0; u < XJ; ++u) {
+          const int i = i0 + tid + u * static_cast<int>(blockDim.x);
           if (i < items) {
             const int reg = i & 3, t = (i >> 2) & 3, kt = i >> 4;
+            float2 q = v[m][u];
             if (FUSED && a.xform == EGT_INPUT_RMSNORM) {
-              v[u].x *= inv;
-              v[u].y *= inv;
+              q.x *= inv[m];
+              q.y *= inv[m];
             } else if (FUSED && a.xform == EGT_INPUT_SILU) {
-              v[u] = silu2(v[u]);
+              q = silu2(q);
             }
-            xbits = max(xbits, max(__float_as_uint(v[u].x) & 0x7fffffffu, __float_as_uint(v[u].y) & 0x7fffffffu));
-            const __half h0 = __float2half_rn(v[u].x), h1 = __float2half_rn(v[u].y);
-            const __half l0 = __float2half_rn(v[u].x - __half2float(h0));
-            const __half l1 = __float2half_rn(v[u].y - __half2float(h1));
+            xbm[m] = max(xbm[m], max(__float_as_uint(q.x) & 0x7fffffffu, __float_as_uint(q.y) & 0x7fffffffu));
+            const __half h0 = __float2half_rn(q.x), h1 = __float2half_rn(q.y);
+            const __half l0 = __float2half_rn(q.x - __half2float(h0));
+            const __half l1 = __float2half_rn(q.y - __half2float(h1));
             uint32_t* row = sB + static_cast<size_t>(nt * KTc + kt) * LS * 4;
             row[(8 * m + t) * 4 + reg] = static_cast<uint32_t>(__half_as_ushort(h0)) |
                                          (static_cast<uint32_t>(__half_as_ushort(h1)) << 16);
@@ -590,8 +600,13 @@ __global__ void __launch_bounds__(NT == 1 ? 416 : 288, 2) tiled_spmm_kernel(cons
           }
         }
       }
-      note_token(4 * nt + m);
     }
+#pragma unroll
+    for (int m = 0; m < 4; ++m)
+      if (m < mc) {
+        xbits = xbm[m];
+        note_token(4 * nt + m);
+      }
   }
   // the range check at the end-of-staging barrier (see note_token)
   uint32_t restage = 0u;  // token slots to stage again (CTA-uniform)
@@ -1032,6 +1047,11 @@ cudaError_t launch_tiled(const egt_dev_packed* h, const TiledSchedule& sc, const
   static const int dbg = getenv("EGT_DEBUG_MODE") ? atoi(getenv("EGT_DEBUG_MODE")) : 0;
   a.dbg = dbg;
   a.indep = indep ? 1 : 0;  // split-K workspaces alternate for independent launches (capi.cu)
+  static const bool plan_log = getenv("EGT_PLAN_LOG") != nullptr;  // tuning
+  if (plan_log)
+    fprintf(stderr, "tiled plan %ux%u M=%d: RB=%d S=%d NT=%d nw=%d NST=%d CH=%d grid=(%d,%d,%d) smem=%zu indep=%d\n",
+            h->rows, h->cols, M, sc.RB, sc.S, sc.NT, sc.nw, sc.NST, sc.CH, sc.grid_x, sc.grid_y, sc.grid_z, sc.smem,
+            indep ? 1 : 0);
   void* fn = pick_kernel(h->format, h->tiled.SS, M == 1 ? 0 : sc.NT, a.xform != 0 || a.res != nullptr || a.pf_ptr[0] || a.out_silu || a.nseg > 1 || a.npeer > 0);
   cudaError_t err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(sc.smem));
