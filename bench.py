@@ -548,6 +548,20 @@ def measure_decode(torch, egt, plan_name, n_tokens=64, prompt_len=16, max_len=25
             beam_decode["kv_cache" if kv else "recompute"] = {"ms_per_decode": round(dms, 3),
                                                               "steps": st["steps"],
                                                               "ms_per_step": round(dms / max(1, st["steps"]), 3)}
+        # the paper's method: KV-cached steps until the cost model (fitted to
+        # this model's own device timings, decode.cpp:84-120) triggers one
+        # prefix-tree verification pass over the rest of the trie
+        from paper_2605_11582_b200.planning import CostModelEstimator
+
+        cost = CostModelEstimator().measure(model, prompt_len, 4, [64, 256, 1024], reps=2)
+        model.decode(trie, prompt, beam_size=4, mode="ptpv", cost=cost, kv_cache=True)  # warm-up
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        for _ in range(3):
+            out, st = model.decode(trie, prompt, beam_size=4, mode="ptpv", cost=cost, kv_cache=True)
+        torch.cuda.synchronize()
+        beam_decode["ptpv_kv_cache"] = {"ms_per_decode": round((time.perf_counter() - t1) * 1e3 / 3, 3),
+                                        "cost_model_s": [round(v, 7) for v in cost], **st}
     res = {"plan": plan_name, "tokens_per_s": round(n_tokens / (ms * 1e-3), 1), "ms_per_token": round(per_tok, 4),
            "weight_bytes_per_token": weight_bytes,
            "weight_GBps": round(weight_bytes / (per_tok * 1e-3) / 1e9, 1),
