@@ -186,11 +186,13 @@ EGT_API egt_status egt_spmv_fused_multi(const egt_dev_packed* const* hs, uint32_
                                         void* stream);
 
 /* M tokens through n <= 3 matrices of one shape sharing x (the verify pass's
- * Q, K, V, forward_impl model.cpp:156-158): ys[i] (M x rows, row stride ldy)
- * = x * W_i^T.  Many tokens run as ONE tcgen05 launch over the n matrices
- * with one x preparation; otherwise one product per matrix. */
+ * Q, K, V, forward_impl model.cpp:155-158): ys[i] (M x rows, row stride ldy)
+ * = f(x) * W_i^T with f = identity or EGT_INPUT_RMSNORM (per token, eps).
+ * Many tokens run as ONE tcgen05 launch over the n matrices with one x
+ * preparation (the rmsnorm folded into it); otherwise one product per matrix. */
 EGT_API egt_status egt_spmm_multi(const egt_dev_packed* const* hs, uint32_t n, const float* x_dev, uint32_t M,
-                                  uint32_t ldx, float* const* ys_dev, uint32_t ldy, void* stream);
+                                  uint32_t ldx, float* const* ys_dev, uint32_t ldy, uint32_t input, float eps,
+                                  void* stream);
 
 /* Same as egt_spmv with host buffers: H2D of x, the product, D2H of y, and a
  * stream synchronize.  x_len must equal cols (else EGT_EINVAL with the

@@ -661,7 +661,7 @@ egt_status spmv_impl(const egt_dev_packed* h, const float* x, float* y, uint32_t
                             static_cast<int>(ldy), ctx));
     return EGT_OK;
   }
-  if (M > 1 && !pg && input == EGT_INPUT_NONE && !plan_forced() && umma_eligible(h, static_cast<int>(M))) {
+  if (M > 1 && !pg && (input == EGT_INPUT_NONE || input == EGT_INPUT_RMSNORM) && !plan_forced() && umma_eligible(h, static_cast<int>(M))) {
     // tcgen05 / TMEM many-token kernel (umma_spmm.cu): x stages + per-token
     // range, then split-K partials, in one per-stream workspace
     const int ns = num_sms();
@@ -730,7 +730,9 @@ egt_status egt_spmv_ex(const egt_dev_packed* h, const float* x, float* y, uint32
 }
 
 egt_status egt_spmm_multi(const egt_dev_packed* const* hs, uint32_t n, const float* x, uint32_t M, uint32_t ldx,
-                          float* const* ys, uint32_t ldy, void* stream) {
+                          float* const* ys, uint32_t ldy, uint32_t input, float eps, void* stream) {
+  if (input != EGT_INPUT_NONE && input != EGT_INPUT_RMSNORM)
+    return fail(EGT_EINVAL, "spmm multi: input transform must be none or rmsnorm");
   if (!hs || !ys || n == 0 || n > 3) return fail(EGT_EINVAL, "spmm multi: 1 to 3 matrices");
   const egt_dev_packed* h = hs[0];
   if (!h || (!x && M > 0)) return fail(EGT_EINVAL, "spmm multi: null argument");
@@ -748,6 +750,8 @@ egt_status egt_spmm_multi(const egt_dev_packed* const* hs, uint32_t n, const flo
     LaunchCtx ctx;
     ctx.stream = s;
     ctx.pdl = g_pdl;
+    ctx.xform = static_cast<int>(input);
+    ctx.eps = eps;
     const int ns = num_sms();
     const size_t xs = (umma_workspace_bytes(h, static_cast<int>(M)) + 255) / 256 * 256;
     const size_t pf = umma_partial_floats(h, static_cast<int>(M), ns);
@@ -761,7 +765,8 @@ egt_status egt_spmm_multi(const egt_dev_packed* const* hs, uint32_t n, const flo
     return EGT_OK;
   }
   for (uint32_t i = 0; i < n; ++i) {
-    const egt_status st = egt_spmv_ex(hs[i], x, ys[i], M, ldx, ldy, i ? EGT_SPMV_INDEPENDENT : 0u, stream);
+    const egt_status st = egt_spmv_fused(hs[i], x, ys[i], M, ldx, ldy, nullptr, 0, input, eps,
+                                         i ? EGT_SPMV_INDEPENDENT : 0u, nullptr, stream);
     if (st != EGT_OK) return st;
   }
   return EGT_OK;

@@ -750,13 +750,22 @@ egt_status forward_core(const egt_model* m, const int32_t* tokens, const int32_t
   const dim3 tb(16, 16);
   for (uint32_t l = 0; l < c.n_layers && st == EGT_OK; ++l) {
     const egt_dev_packed* const* w = m->layers.data() + 6 * l;
-    rmsnorm(x, a);
-    ++launch_counter();
+    // on the tcgen05 path the rmsnorm of Q/K/V's and ff1's input is folded
+    // into the x preparation (one pass for the row's sum of squares and range)
+    static const bool no_fold = getenv("EGT_NO_RMSNORM_FOLD") != nullptr;  // tuning
     static const bool no_multi = getenv("EGT_NO_QKV_MULTI") != nullptr;  // tuning: three launches
+    const bool fold = !no_fold && !no_multi && M > 1 && egt_impl::umma_eligible(w[0], static_cast<int>(M)) &&
+                      egt_impl::umma_eligible(w[4], static_cast<int>(M));
+    if (!fold) {
+      rmsnorm(x, a);
+      ++launch_counter();
+    }
     if (M > 1 && !no_multi) {  // one tcgen05 launch over Q, K, V when the tokens take that path
       const egt_dev_packed* qkv[3] = {w[0], w[1], w[2]};
       float* outs[3] = {q, k, v};
-      if (st == EGT_OK) st = egt_spmm_multi(qkv, 3, a, static_cast<uint32_t>(M), w[0]->cols, outs, w[0]->rows, stream);
+      if (st == EGT_OK)
+        st = egt_spmm_multi(qkv, 3, fold ? x : a, static_cast<uint32_t>(M), w[0]->cols, outs, w[0]->rows,
+                            fold ? EGT_INPUT_RMSNORM : EGT_INPUT_NONE, kNormEps, stream);
     } else {
       lin(w[0], a, q, 0);
       lin(w[1], a, k, EGT_SPMV_INDEPENDENT);  // K and V read `a`, not the previous product
@@ -799,17 +808,22 @@ egt_status forward_core(const egt_model* m, const int32_t* tokens, const int32_t
     }
     // x += o Wo^T; f = silu(rmsnorm(x) ff1^T); x += f ff2^T -- the residual
     // adds and the silu in the products' epilogues where the path allows
-    auto fused = [&](const egt_dev_packed* h, const float* in, float* outp, const float* res, uint32_t flags) {
+    auto fused = [&](const egt_dev_packed* h, const float* in, float* outp, const float* res, uint32_t flags,
+                     uint32_t input = EGT_INPUT_NONE) {
       if (st == EGT_OK)
         st = egt_spmv_fused(h, in, outp, M, h->cols, h->rows, res, res ? static_cast<uint32_t>(d) : 0,
-                            EGT_INPUT_NONE, kNormEps, flags, nullptr, stream);
+                            input, kNormEps, flags, nullptr, stream);
     };
     const bool glue = w[3]->path == EGT_PATH_TILED && w[4]->path == EGT_PATH_TILED && w[5]->path == EGT_PATH_TILED;
     if (glue) {
       fused(w[3], o, x, x, 0);
-      rmsnorm(x, a);
-      ++launch_counter();
-      fused(w[4], a, f1, nullptr, EGT_SPMV_OUTPUT_SILU);
+      if (fold) {
+        fused(w[4], x, f1, nullptr, EGT_SPMV_OUTPUT_SILU, EGT_INPUT_RMSNORM);
+      } else {
+        rmsnorm(x, a);
+        ++launch_counter();
+        fused(w[4], a, f1, nullptr, EGT_SPMV_OUTPUT_SILU);
+      }
       fused(w[5], f1, x, x, 0);
     } else {
       lin(w[3], o, a, 0);  // a <- o Wo^T

@@ -42,6 +42,7 @@
 #include <cstdlib>
 
 #include "device_common.cuh"
+#include "egt_b200.h"
 #include "handle.h"
 #include "xrange.cuh"
 
@@ -99,6 +100,7 @@ struct UmmaArgs {
   int KQ, RT, rows, SS, E;
   const uint8_t* xf;  // B stages [tile][k-stage][N rows x 64 K fp16, canonical K-major]
   const float* unsc;  // per padded token: 2^-e (xrange.cuh)
+  const float* tinv;  // per padded token: the rmsnorm factor (x' = x * tinv), or null
   const uint32_t* nonfin;
   const float* x;  // the raw activations (non-finite fix-up only)
   int ldx, cols;
@@ -288,9 +290,10 @@ template <int FMT>
 __device__ __noinline__ float umma_nonfinite_terms(const UmmaArgs& a, int sg, int row, int tok, int c0, int c1) {
   const TiledRef m{a.vals[sg], a.meta[sg], a.scales[sg], a.zps[sg], a.KQ, a.rt_begin[sg], a.SS, a.pad14};
   const float* xr = a.x + static_cast<size_t>(tok) * a.ldx;
+  const float inv = a.tinv ? a.tinv[tok] : 1.f;
   float add = 0.f;
   for (int c = c0; c < c1; ++c) {
-    const float xv = xr[c];
+    const float xv = xr[c] * inv;
     if ((__float_as_uint(xv) & 0x7fffffffu) < 0x7f800000u) continue;
     float w;
     if (tiled_value<FMT>(m, row, c, &w)) add += w * xv;
@@ -795,12 +798,17 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const __grid_con
 // land 1024-byte aligned).  One CTA per padded token: its range first
 // (xrange.cuh; every load of a thread in flight together), then one thread
 // per 8-column chunk (two 16-byte stores).
+// xform = EGT_INPUT_RMSNORM: x' = x * inv_tok, inv = 1 / sqrt(mean(x^2) + eps)
+// (model.cpp:57-67) from the same first pass (tinv[tok] for the non-finite
+// fix-up); the range is then the transformed one (max |x'| = max |x| * inv).
 __global__ void __launch_bounds__(256) umma_xprep_kernel(const float* __restrict__ x, int ldx, int M, int cols,
                                                          int T, int KS, uint8_t* __restrict__ xf,
-                                                         float* __restrict__ unsc, uint32_t* __restrict__ nonfin) {
+                                                         float* __restrict__ unsc, uint32_t* __restrict__ nonfin,
+                                                         float* __restrict__ tinv, int xform, float eps) {
   pdl_wait();
   pdl_launch_dependents();
   __shared__ uint32_t s_mx, s_nf;
+  __shared__ float s_ss[8];
   const int tok = blockIdx.x, tid = threadIdx.x;
   if (tid == 0) {
     s_mx = 0u;
@@ -809,6 +817,7 @@ __global__ void __launch_bounds__(256) umma_xprep_kernel(const float* __restrict
   __syncthreads();
   const float* xr = x + static_cast<size_t>(tok) * ldx;
   const bool vec = (ldx & 3) == 0 && (reinterpret_cast<uintptr_t>(x) & 15) == 0;
+  float ss = 0.f;
   if (tok < M) {
     uint32_t mx = 0u, nf = 0u;
     if (vec) {
@@ -822,20 +831,42 @@ __global__ void __launch_bounds__(256) umma_xprep_kernel(const float* __restrict
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
           xr_note(mx, nf, q[u].x); xr_note(mx, nf, q[u].y); xr_note(mx, nf, q[u].z); xr_note(mx, nf, q[u].w);
+          ss = fmaf(q[u].x, q[u].x, fmaf(q[u].y, q[u].y, fmaf(q[u].z, q[u].z, fmaf(q[u].w, q[u].w, ss))));
         }
       }
-      for (int k = 4 * n4 + tid; k < cols; k += blockDim.x) xr_note(mx, nf, __ldg(xr + k));
+      for (int k = 4 * n4 + tid; k < cols; k += blockDim.x) {
+        const float v = __ldg(xr + k);
+        xr_note(mx, nf, v);
+        ss = fmaf(v, v, ss);
+      }
     } else {
-      for (int k = tid; k < cols; k += blockDim.x) xr_note(mx, nf, __ldg(xr + k));
+      for (int k = tid; k < cols; k += blockDim.x) {
+        const float v = __ldg(xr + k);
+        xr_note(mx, nf, v);
+        ss = fmaf(v, v, ss);
+      }
     }
     xr_commit(mx, nf, &s_mx, &s_nf);
   }
+  float inv = 1.f;
+  if (xform == EGT_INPUT_RMSNORM) {
+    ss = warp_sum(ss);
+    if ((tid & 31) == 0) s_ss[tid >> 5] = ss;
+  }
   __syncthreads();
-  const int e = xr_exp(s_mx);
+  if (xform == EGT_INPUT_RMSNORM) {
+    float tot = 0.f;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) tot += s_ss[w];
+    inv = 1.0f / sqrtf(tot / static_cast<float>(cols) + eps);
+  }
+  // range of the transformed row: max |x| * inv (inv > 0), or none when inv = 0
+  const uint32_t tmx = xform == EGT_INPUT_RMSNORM ? (__float_as_uint(__uint_as_float(s_mx) * inv) & 0x7fffffffu) : s_mx;
+  const int e = xr_exp(tmx < 0x7f800000u ? tmx : 0u);
   const float sc = xr_pow2(e);
   if (tid == 0) {
     unsc[tok] = xr_pow2(-e);
     nonfin[tok] = s_nf;
+    tinv[tok] = inv;
   }
   const int N = 2 * T, tl = tok % T, tile = tok / T;
   const uint32_t stage_bytes = static_cast<uint32_t>(N) * kStageK * 2;
@@ -850,6 +881,10 @@ __global__ void __launch_bounds__(256) umma_xprep_kernel(const float* __restrict
     } else {
 #pragma unroll
       for (int u = 0; u < 8; ++u) xv[u] = tok < M && k0 + u < cols ? __ldg(xr + k0 + u) : 0.f;
+    }
+    if (xform == EGT_INPUT_RMSNORM) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) xv[u] *= inv;
     }
     uint32_t h[4], l[4];
 #pragma unroll
@@ -960,7 +995,7 @@ size_t umma_workspace_bytes(const egt_dev_packed* h, int M) {
   const int T = ((M + tiles - 1) / tiles + 15) / 16 * 16;
   const int TT = (M + T - 1) / T;
   const size_t KS = 2 * static_cast<size_t>(h->tiled.KQ);
-  return static_cast<size_t>(TT) * KS * (2 * T) * kStageK * 2 + static_cast<size_t>(TT) * T * 8;
+  return static_cast<size_t>(TT) * KS * (2 * T) * kStageK * 2 + static_cast<size_t>(TT) * T * 12;
 }
 
 // split-K partials stay on chip (cluster DSMEM): no global workspace
@@ -1040,6 +1075,9 @@ cudaError_t launch_umma_multi(const egt_dev_packed* const* hs, int nseg, const f
   uint8_t* xf = ws;
   float* unsc = reinterpret_cast<float*>(ws + static_cast<size_t>(p.TT) * KS * (2 * p.T) * kStageK * 2);
   uint32_t* nonfin = reinterpret_cast<uint32_t*>(unsc + p.TT * p.T);
+  float* tinv = reinterpret_cast<float*>(nonfin + p.TT * p.T);
+  int xform = ctx.xform;
+  float eps = ctx.eps;
   {
     cudaLaunchConfig_t xc = {};
     xc.gridDim = dim3(p.TT * p.T);
@@ -1051,7 +1089,7 @@ cudaError_t launch_umma_multi(const egt_dev_packed* const* hs, int nseg, const f
     xc.attrs = xa;
     xc.numAttrs = ctx.pdl ? 1 : 0;
     int cols = static_cast<int>(h->cols), T = p.T, ks = KS;
-    void* xargs[] = {const_cast<float**>(&x), &ldx, &M, &cols, &T, &ks, &xf, &unsc, &nonfin};
+    void* xargs[] = {const_cast<float**>(&x), &ldx, &M, &cols, &T, &ks, &xf, &unsc, &nonfin, &tinv, &xform, &eps};
     cudaError_t e = cudaLaunchKernelExC(&xc, reinterpret_cast<void*>(&umma_xprep_kernel), xargs);
     if (e != cudaSuccess) return e;
     ++launch_counter();
@@ -1078,6 +1116,7 @@ cudaError_t launch_umma_multi(const egt_dev_packed* const* hs, int nseg, const f
   a.E = h->tiled.E;
   a.xf = xf;
   a.unsc = unsc;
+  a.tinv = xform == EGT_INPUT_RMSNORM ? tinv : nullptr;
   a.nonfin = nonfin;
   a.x = x;
   a.ldx = ldx;

@@ -116,7 +116,7 @@ SIGNATURES = {
     "egt_spmv_fused_multi": (C.c_int, [C.POINTER(C.c_void_p), C.c_uint32, C.c_void_p, C.POINTER(C.c_void_p),
                                        C.c_uint32, C.c_float, C.c_uint32, C.c_void_p]),
     "egt_spmm_multi": (C.c_int, [C.POINTER(C.c_void_p), C.c_uint32, C.c_void_p, C.c_uint32, C.c_uint32,
-                                 C.POINTER(C.c_void_p), C.c_uint32, C.c_void_p]),
+                                 C.POINTER(C.c_void_p), C.c_uint32, C.c_uint32, C.c_float, C.c_void_p]),
     "egt_spmv_host": (C.c_int, [C.c_void_p, f32p, C.c_size_t, f32p, C.c_void_p]),
     "egt_dequant": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "egt_set_pdl": (None, [C.c_int]),

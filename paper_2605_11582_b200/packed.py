@@ -292,15 +292,16 @@ def spmv_fused_multi(mats, x, ys, input: int = 0, eps: float = 1e-6, stream=None
                                      _stream_ptr(stream)))
 
 
-def spmm_multi(mats, x, ys, stream=None):
-    """ys[i] = x @ W_i^T (x: M x cols) for up to three matrices sharing x
-    (egt_spmm_multi; the verify pass's Q, K, V: one tcgen05 launch)."""
+def spmm_multi(mats, x, ys, input: int = 0, eps: float = 1e-6, stream=None):
+    """ys[i] = f(x) @ W_i^T (x: M x cols, f = identity / rmsnorm) for up to
+    three matrices sharing x (egt_spmm_multi; the verify pass's Q, K, V: one
+    tcgen05 launch)."""
     n = len(mats)
     M, ldx = (1, x.shape[0]) if x.dim() == 1 else (x.shape[0], x.stride(0))
     ldy = ys[0].shape[-1] if ys[0].dim() == 1 else ys[0].stride(0)
     hs = (C.c_void_p * n)(*[m.handle.value for m in mats])
     yp = (C.c_void_p * n)(*[y.data_ptr() for y in ys])
-    check(lib().egt_spmm_multi(hs, n, C.c_void_p(x.data_ptr()), M, ldx, yp, ldy, _stream_ptr(stream)))
+    check(lib().egt_spmm_multi(hs, n, C.c_void_p(x.data_ptr()), M, ldx, yp, ldy, input, eps, _stream_ptr(stream)))
 
 
 def spmv(w, x):

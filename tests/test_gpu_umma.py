@@ -116,3 +116,38 @@ def test_umma_multi_segments(port, fmt, M):
         for m in range(0, M, 7):
             ok, err = close(got[m], ref(xs[m]))
             assert ok, (fmt, M, m, err)
+
+
+@pytest.mark.parametrize("M", [12, 80])
+def test_umma_rmsnorm_input(port, M):
+    """rmsnorm (model.cpp:57-67) folded into the tcgen05 x preparation, one
+    matrix (egt_spmv_fused) and Q/K/V (egt_spmm_multi), including a row with
+    an inf (the reference's rmsnorm then gives NaN there and 0 elsewhere)."""
+    import torch
+
+    from paper_2605_11582_b200 import native as N
+    from paper_2605_11582_b200.packed import spmm_multi
+
+    rng = np.random.default_rng(M + 3)
+    rows, cols = 256, 1024
+    mats = [_layer(port, rng, "int4-2:4", rows, cols) for _ in range(3)]
+    xs = rng.uniform(-3, 3, (M, cols)).astype(np.float32)
+    xs[1, 7] = np.inf
+    eps = 1e-6
+    xn = np.empty_like(xs)
+    for m in range(M):
+        inv = np.float32(1.0) / np.sqrt(np.float32(np.mean(xs[m].astype(np.float64) ** 2)) + np.float32(eps))
+        xn[m] = xs[m] * inv
+    x = torch.from_numpy(xs).cuda()
+    y = torch.empty((M, rows), device="cuda")
+    mats[0][0].spmv_fused_into(x, y, input=N.INPUT_RMSNORM, eps=eps)
+    ys = [torch.empty((M, rows), device="cuda") for _ in range(3)]
+    spmm_multi([d for d, _ in mats], x, ys, input=N.INPUT_RMSNORM, eps=eps)
+    for got_all, (d, ref) in [(y, mats[0])] + list(zip(ys, mats)):
+        got = got_all.cpu().numpy()
+        for m in range(M):
+            want = ref(xn[m])
+            assert np.array_equal(np.isnan(got[m]), np.isnan(want)), m
+            fin = np.isfinite(want)
+            ok, err = close(got[m][fin], want[fin])
+            assert ok, (M, m, err)
