@@ -535,16 +535,22 @@ def measure_decode(torch, egt, plan_name, n_tokens=64, prompt_len=16, max_len=25
         for i, nd in enumerate(frontier):
             payload[nd] = i
         trie = Trie(np.array(token, np.uint32), np.array(parent, np.uint32), np.array(payload, np.int64))
-        beam_decode = {"trie": "8-way x depth 4 (4096 items)", "beam": 4, "prompt": prompt_len}
+        beam_decode = {"trie": "8-way x depth 4 (4096 items)", "beam": 4, "prompt": prompt_len,
+                       "timing": "host wall clock per decode (host-driven steps), median of 5 after 2 warm-ups"}
+        def timed_decode(**kw):  # median of 5 host-timed decodes after 2 warm-ups
+            for _ in range(2):
+                model.decode(trie, prompt, beam_size=4, **kw)
+            ts = []
+            for _ in range(5):
+                torch.cuda.synchronize()
+                t1 = time.perf_counter()
+                out, st = model.decode(trie, prompt, beam_size=4, **kw)
+                torch.cuda.synchronize()
+                ts.append((time.perf_counter() - t1) * 1e3)
+            return sorted(ts)[2], st
+
         for kv in (True, False):
-            model.decode(trie, prompt, beam_size=4, mode="autoregressive", kv_cache=kv)  # warm-up
-            torch.cuda.synchronize()
-            t1 = time.perf_counter()
-            reps = 3
-            for _ in range(reps):
-                out, st = model.decode(trie, prompt, beam_size=4, mode="autoregressive", kv_cache=kv)
-            torch.cuda.synchronize()
-            dms = (time.perf_counter() - t1) * 1e3 / reps
+            dms, st = timed_decode(mode="autoregressive", kv_cache=kv)
             beam_decode["kv_cache" if kv else "recompute"] = {"ms_per_decode": round(dms, 3),
                                                               "steps": st["steps"],
                                                               "ms_per_step": round(dms / max(1, st["steps"]), 3)}
@@ -554,14 +560,9 @@ def measure_decode(torch, egt, plan_name, n_tokens=64, prompt_len=16, max_len=25
         from paper_2605_11582_b200.planning import CostModelEstimator
 
         cost = CostModelEstimator().measure(model, prompt_len, 4, [64, 256, 1024], reps=2)
-        model.decode(trie, prompt, beam_size=4, mode="ptpv", cost=cost, kv_cache=True)  # warm-up
-        torch.cuda.synchronize()
-        t1 = time.perf_counter()
-        for _ in range(3):
-            out, st = model.decode(trie, prompt, beam_size=4, mode="ptpv", cost=cost, kv_cache=True)
-        torch.cuda.synchronize()
-        beam_decode["ptpv_kv_cache"] = {"ms_per_decode": round((time.perf_counter() - t1) * 1e3 / 3, 3),
-                                        "cost_model_s": [round(v, 7) for v in cost], **st}
+        dms, st = timed_decode(mode="ptpv", cost=cost, kv_cache=True)
+        beam_decode["ptpv_kv_cache"] = {"ms_per_decode": round(dms, 3), "cost_model_s": [round(v, 7) for v in cost],
+                                        **st}
     res = {"plan": plan_name, "tokens_per_s": round(n_tokens / (ms * 1e-3), 1), "ms_per_token": round(per_tok, 4),
            "weight_bytes_per_token": weight_bytes,
            "weight_GBps": round(weight_bytes / (per_tok * 1e-3) / 1e9, 1),
