@@ -292,6 +292,21 @@ def measure_sharded(world, rank, stream, torch, egt, rng):
             tg = torch.tensor([e0.elapsed_time(e1) * 1e3 / n_g], device="cuda")
             torch.distributed.all_reduce(tg, op=torch.distributed.ReduceOp.MAX)
             res["allgather_us"] = round(float(tg.item()), 3)
+            # end to end per call: the shard's product then the NCCL all-gather
+            # of its y rows (stream order; what a sharded layer costs)
+            yl = torch.empty(plan.max_rows, device="cuda")
+            torch.cuda.synchronize()
+            torch.distributed.barrier()
+            e0.record()
+            for i in range(n_g):
+                sh = shards[i % len(shards)]
+                sh.spmv_into(x, yl[: sh.rows])
+                torch.distributed.all_gather_into_tensor(buf, yl)
+            e1.record()
+            e1.synchronize()
+            te = torch.tensor([e0.elapsed_time(e1) * 1e3 / n_g], device="cuda")
+            torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+            res["gemv_plus_nccl_allgather_us"] = round(float(te.item()), 3)
             yf = fulls[0].spmv(x).cpu().numpy()
             yg = gather_rows(shards[0].spmv(x), plan).cpu().numpy()
             res["gathered_equals_unsharded_max_rel_err"] = float(np.max(np.abs(yg - yf) / (1 + np.abs(yf))))
