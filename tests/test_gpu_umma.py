@@ -92,7 +92,7 @@ def test_umma_sass_is_tcgen05():
     sass = out.stdout
     if out.returncode != 0 or not sass:
         pytest.skip("cuobjdump unavailable")
-    assert "UTCHMMA" in sass and "LDTM" in sass and "UBLKCP" in sass
+    assert "UTCHMMA" in sass and "LDTM" in sass and "UBLKCP" in sass and "UTMALDG" in sass
 
 
 @pytest.mark.parametrize("fmt", ["int4-2:4", "fp16-2:4", "int4-dense"])
