@@ -20,5 +20,6 @@ struct egt_kv_pool {
   float* k = nullptr;
   float* v = nullptr;
   uint32_t capacity = 0, d = 0, layers = 0;
+  size_t floats = 0;  // allocated floats per buffer (>= layers x capacity x d)
 };
 
