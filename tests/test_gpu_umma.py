@@ -151,3 +151,25 @@ def test_umma_rmsnorm_input(port, M):
             fin = np.isfinite(want)
             ok, err = close(got[m][fin], want[fin])
             assert ok, (M, m, err)
+
+
+def test_spmm_multi_errors(port):
+    """egt_spmm_multi's argument contract: 1..3 matrices sharing columns,
+    identity or rmsnorm input, the reference-style EGT_EINVAL messages."""
+    import torch
+
+    import paper_2605_11582_b200 as egt
+    from paper_2605_11582_b200 import native as N
+    from paper_2605_11582_b200.packed import spmm_multi
+
+    rng = np.random.default_rng(4)
+    a, _ = _layer(port, rng, "int4-2:4", 128, 256)
+    b, _ = _layer(port, rng, "int4-2:4", 128, 512)
+    x = torch.zeros((20, 256), device="cuda")
+    ys = [torch.empty((20, 128), device="cuda") for _ in range(4)]
+    with pytest.raises(egt.InvalidArgument, match="1 to 3 matrices"):
+        spmm_multi([a, a, a, a], x, ys)
+    with pytest.raises(egt.InvalidArgument, match="share their columns"):
+        spmm_multi([a, b], x, ys[:2])
+    with pytest.raises(egt.InvalidArgument, match="none or rmsnorm"):
+        spmm_multi([a, a], x, ys[:2], input=N.INPUT_SILU)
