@@ -1,37 +1,42 @@
 // Many-token SparseGemv on the 5th-generation tensor cores (tcgen05 + TMEM):
 // the X * W^T products of the prefix-tree verification pass (forward_impl,
-// model.cpp:156-195; M = committed prefix + tree nodes, 64-272 rows in the
-// BASELINE configs) for INT4 2:4 (and 1:4 stored as 2:4), dense INT4 and
-// FP16 2:4 layers.
+// model.cpp:155-195; M = committed prefix + tree nodes, 64-272 rows in the
+// BASELINE configs) and every product of >= 9 tokens, for INT4 2:4 (and 1:4
+// stored as 2:4), dense INT4 and FP16 2:4 layers with 64- / 128-column groups.
 //
-// One CTA = 128 weight rows x one token tile (T <= 120 tokens) x a K range.
+// One CTA = 128 weight rows x one token tile (T <= 96 tokens) x a K range;
+// with several same-shape matrices (Q, K, V) blockIdx.x = segment x row block.
 // The accumulator lives in TMEM: D[128 rows x 2T] -- x enters as fp16 hi
 // (columns [0, T)) and lo = x - hi (columns [T, 2T)) in one B operand, so a
 // single tcgen05.mma (M = 128, N = 2T) multiplies both and the epilogue sums
-// them in f32 (x keeps ~22 mantissa bits; xrange.cuh scales it).
+// them in f32 (x keeps ~22 mantissa bits; umma_xprep_kernel scales each token
+// by a power of two (xrange.cuh) and folds an input rmsnorm).
 //
-// Warp roles (448 threads, one CTA per SM -- it owns all of TMEM):
-//   warp 0      weight producer: per raw stage three 2-D TMA tensor loads
-//               (values, metadata, zero points of 8 row tiles x 1-2
-//               k-quads), the first ones before the PDL wait -- weights never
+// Warp roles (19 warps, 608 threads, one CTA per SM -- it owns all of TMEM):
+//   warp 0      weight producer: per raw stage (8 row tiles x 1-2 k-quads)
+//               2-D TMA tensor-map loads of values, metadata, zero points,
+//               scales, the first ones before the PDL wait -- weights never
 //               depend on the previous kernel;
-//   warp 18     x producer: the pre-laid-out x stages (64 K each), a deep ring
-//               (TMA round trips from L2 are ~1 us);
-//   warp 1      TMEM allocator + single-thread MMA issuer (4 x K=16 per stage;
-//               tcgen05.commit releases the smem stages / signals the epilogue);
-//   warps 2-9   dequantisers: two groups of four (alternate stages), two
+//   warp 18     x producer: the pre-laid-out x stages, one bulk copy per
+//               k-quad slot (two 64-column sub-stages), counted on the slot's
+//               full barrier with the dequantisers (optionally multicast to
+//               a pair of row blocks, EGT_UMMA_MCAST);
+//   warp 1      TMEM allocator + single-thread MMA issuer: per k-quad slot one
+//               barrier wait, 4 sparse (8 dense) MMAs, one commit -- the
+//               issue chain (~250 cycles per tcgen05.mma whatever N) is what
+//               bounds the kernel (DESIGN 3.1c);
+//   warps 2-9   dequantisers: two groups of four (one sub-stage each), two
 //               row tiles per warp: packed stage -> the A stage in the UMMA
-//               canonical K-major layout (8-row x 16-byte core matrices), the
-//               2:4 pairs expanded in place with zeros (c - z exactly in fp16:
-//               the 0x6400 exponent trick), then fence.proxy.async;
-//   warps 10-17 epilogue: INT4 accumulates one scale step (128 or 64 columns)
-//               per TMEM buffer (two buffers, ping-pong) and folds it into
-//               registers as acc += s_g * (D_hi + D_lo) -- the reference's
-//               (c - z) * s per group, summed in f32; FP16 layers accumulate
-//               the whole K range in TMEM and are read once.
+//               canonical K-major swizzled layout, c - z exact in fp16 (the
+//               0x6400 exponent trick); the 2:4 metadata into TMEM
+//               (tcgen05.st), then fence.proxy.async;
+//   warps 10-17 epilogue: one scale step (128 or 64 columns) per TMEM buffer
+//               (two buffers, ping-pong), acc += s_g * (D_hi + D_lo) -- the
+//               reference's (c - z) * s per group, summed in f32; FP16 layers
+//               accumulate the whole K range in TMEM and are read once.
 // Split-K (S > 1): the S slices of a row block form a thread-block cluster;
-// the leader sums the slices' partials from their shared memory (DSMEM) in
-// slice order (deterministic, no global round trip).
+// each slice sums a 1/S share of the token groups from all slices' shared
+// memory (DSMEM) in slice order (deterministic, no global round trip).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
