@@ -35,8 +35,13 @@
 //               reference's (c - z) * s per group, summed in f32; FP16 layers
 //               accumulate the whole K range in TMEM and are read once.
 // Split-K (S > 1): the S slices of a row block form a thread-block cluster;
-// each slice sums a 1/S share of the token groups from all slices' shared
-// memory (DSMEM) in slice order (deterministic, no global round trip).
+// each slice owns a 1/S share of the token groups: every slice bulk-copies
+// the other slices' shares of its partial tile into their shared memory
+// (cp.async.bulk shared::cta -> shared::cluster, completing on the owner's
+// mbarrier) and the owner sums the S shares in slice order (deterministic,
+// no global round trip).  Loading the shares with DSMEM loads instead ran a
+// ~7 us tail per launch (cold, unrolled straight-line code and remote-load
+// latency; EGT_UMMA_PULL=1 keeps that path for comparison).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -95,6 +100,12 @@ struct UmmaArgs {
   // stages: each CTA loads one 64-column half of a k-quad slot, multicast to
   // both (L2 x traffic halved); a slot is refilled once both CTAs consumed it
   int mcast;
+  // 1: split-K partials are pushed (default; EGT_UMMA_PULL=1 off): each slice's tile is
+  // stored token-group-major (float4 per (4-token group, row)) and every
+  // slice bulk-copies the other slices' shares into their shared memory
+  // (cp.async.bulk shared::cta -> shared::cluster, one mbarrier per CTA);
+  // the owner then sums S local shares with a short rolled loop
+  int push;
   int NX;  // x ring depth
   int NA;  // A ring depth
   const uint8_t* vals[kMaxSeg];
@@ -215,6 +226,29 @@ __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                    smem_addr(bar))
                : "memory");
+}
+// shared::cta -> a cluster peer's shared memory, completing on the peer's mbarrier
+__device__ __forceinline__ void bulk_s2peer(uint32_t dst_cluster, uint32_t src, uint32_t bytes, uint32_t bar_cluster) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   dst_cluster),
+               "r"(src), "r"(bytes), "r"(bar_cluster)
+               : "memory");
+}
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITC_%=:\n"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAITC_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
 }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
@@ -338,7 +372,8 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const __grid_con
   const int kNX = a.NX;
   uint64_t* tm_full = a_empty + kMaxNA;
   uint64_t* tm_empty = tm_full + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tm_empty + 2);
+  uint64_t* recv_bar = tm_empty + 2;  // push: the other slices' shares landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(recv_bar + 1);
   __shared__ float s_unsc[kMaxT];
   __shared__ uint32_t s_nonf[kMaxT];
   __shared__ int s_anynf;  // some token of the tile has a non-finite x
@@ -379,7 +414,13 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const __grid_con
       mbar_init(tm_full + i, 1);
       mbar_init(tm_empty + i, kNumEpi);
     }
+    if (a.push) mbar_init(recv_bar, 1);
     mbar_fence_init();
+    if (a.push && a.S > 1) {  // armed before the cluster barrier the senders wait on
+      const int G4 = T / 4, per = (G4 + a.S - 1) / a.S;
+      const int mine = max(0, min(G4, (static_cast<int>(blockIdx.z) + 1) * per) - static_cast<int>(blockIdx.z) * per);
+      mbar_expect_tx(recv_bar, static_cast<uint32_t>((a.S - 1) * mine * 2048));
+    }
   }
   // TMEM: accumulator buffer(s) at column 0 (T <= 64 columns each), sparse
   // metadata (2 columns per A-stage ring slot) at column 128
@@ -677,13 +718,18 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const __grid_con
     // short -- its instruction fetches are cold (an unrolled per-token tail
     // measured 3.4 us).
     float* part = reinterpret_cast<float*>(x_st);
+    // pull: row-major (tokens contiguous, PT = T + 4); push: float4 per
+    // (4-token group, row), group-major, so a slice's share is contiguous
+    auto pidx = [&](int row, int tl) {
+      return a.push ? ((tl >> 2) * 128 + row) * 4 + (tl & 3) : row * (T + 4) + tl;
+    };
     {
-      float* pr = part + r * (T + 4) + c0;
 #pragma unroll
       for (int k = 0; k < kMaxT / 2; k += 4)
         if (k < th) {
           const float4 u = *reinterpret_cast<const float4*>(s_unsc + c0 + k);
-          *reinterpret_cast<float4*>(pr + k) = make_float4(acc[k] * u.x, acc[k + 1] * u.y, acc[k + 2] * u.z, acc[k + 3] * u.w);
+          *reinterpret_cast<float4*>(part + pidx(r, c0 + k)) =
+              make_float4(acc[k] * u.x, acc[k + 1] * u.y, acc[k + 2] * u.z, acc[k + 3] * u.w);
         }
     }
     if (s_anynf) {  // non-finite x somewhere in the tile: exact fix-up, token by token
@@ -691,9 +737,10 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const __grid_con
       for (int k = 0; k < th; ++k) {
         const int tl = c0 + k, tok = tile * T + tl;
         if (row_ok && tok < a.M && s_nonf[tl])
-          part[r * (T + 4) + tl] += umma_nonfinite_terms<FMT>(a, sg, grow, tok, kc0, kc1);
+          part[pidx(r, tl)] += umma_nonfinite_terms<FMT>(a, sg, grow, tok, kc0, kc1);
       }
     }
+    if (a.push) fence_async_smem();  // the partials are read by the bulk-copy engine
     if (tr && lane == 0) tr[840 + warp - kEpiWarp0] = umma_clock();
   }
 
@@ -711,6 +758,69 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const __grid_con
   if (a.S > 1)
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
   if (tr && tid == 0) tr[4] = umma_clock();
+  if (a.push) {
+    const int G4 = T / 4, per = (G4 + a.S - 1) / a.S, myz = static_cast<int>(blockIdx.z);
+    const uint32_t pbase = smem_addr(x_st), rbase = pbase + static_cast<uint32_t>(T) * 512;
+    if (a.S > 1 && tid == 0) {
+      // slice z's share of this slice's tile -> z's receive area, slot myz
+      for (int z = 0; z < a.S; ++z) {
+        const int n = min(G4, (z + 1) * per) - z * per;
+        if (z == myz || n <= 0) continue;
+        bulk_s2peer(mapa_u32(rbase + static_cast<uint32_t>(myz * per) * 2048, static_cast<uint32_t>(z)),
+                    pbase + static_cast<uint32_t>(z * per) * 2048, static_cast<uint32_t>(n) * 2048,
+                    mapa_u32(smem_addr(recv_bar), static_cast<uint32_t>(z)));
+      }
+    }
+    if (warp >= kEpiWarp0 && warp < kEpiWarp0 + kNumEpi) {
+      const int g0 = myz * per, g1 = min(G4, g0 + per);
+      if (a.S > 1) mbar_wait_cluster(recv_bar, 0);
+      // every copy into this CTA landed (so its sources were read): the exit
+      // barrier may complete while the sums below run
+      if (a.S > 1) asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+      const int nit = max(0, g1 - g0) * 128;
+      for (int it = (warp - kEpiWarp0) * 32 + lane; it < nit; it += kNumEpi * 32) {
+        const int r = it & 127, gq = g0 + (it >> 7), grow = rt0 * 16 + r;
+        float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 1
+        for (int z = 0; z < a.S; ++z) {  // slice order (deterministic)
+          const uint32_t ad = z == myz ? pbase + static_cast<uint32_t>((gq * 128 + r) * 16)
+                                       : rbase + static_cast<uint32_t>(((z * per + gq - g0) * 128 + r) * 16);
+          const uint4 v = lds_v4(ad);
+          sum.x += __uint_as_float(v.x);
+          sum.y += __uint_as_float(v.y);
+          sum.z += __uint_as_float(v.z);
+          sum.w += __uint_as_float(v.w);
+        }
+        if (grow >= a.rows || (rt0 + (r >> 4)) >= a.RT) continue;
+        const float s4[4] = {sum.x, sum.y, sum.z, sum.w};
+        float rr[4] = {0.f, 0.f, 0.f, 0.f};
+        if (a.res) {  // the four residual loads in flight together
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int tok = tile * T + 4 * gq + u;
+            if (tok < a.M) rr[u] = a.res[static_cast<size_t>(tok) * a.ldr + grow];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int tok = tile * T + 4 * gq + u;
+          if (tok < a.M) {
+            float o = s4[u] + rr[u];
+            if (a.out_silu) o = o * (1.0f / (1.0f + expf(-o)));  // model.cpp:80-84
+            a.y[sg][static_cast<size_t>(tok) * a.ldy + grow] = o;
+          }
+        }
+      }
+    } else if (a.S > 1) {
+      asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+    }
+    if (tr && tid == kEpiWarp0 * 32) tr[5] = umma_clock();
+    if (a.S > 1) asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    else if (a.mcast)
+      asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+    if (tr && tid == 0) tr[6] = umma_clock();
+    return;
+  }
   // each slice reduces a 1/S share of the token groups (4 tokens) for all
   // 128 rows: the S partials in slice order (deterministic), float4 DSMEM
   // loads all in flight, then residual / silu and the store (S = 1: this
@@ -1138,6 +1248,11 @@ cudaError_t launch_umma_multi(const egt_dev_packed* const* hs, int nseg, const f
   // kernel; kept as an option (EGT_UMMA_MCAST=1)
   static const bool mcast = getenv("EGT_UMMA_MCAST") != nullptr;
   a.mcast = mcast && p.S == 1 && p.TT > 1 && (nseg * a.RB1) % 2 == 0 ? 1 : 0;
+  // split-K partials pushed by bulk copies (default; EGT_UMMA_PULL=1: the
+  // DSMEM-load reduction): 4096^2 at M = 80 23.2 -> 20.2 us, the verify pass
+  // at 64 nodes 6.22 -> 5.98 ms (tools/umma_probe.py, verify_probe.py)
+  static const bool pull = getenv("EGT_UMMA_PULL") != nullptr;
+  a.push = pull ? 0 : 1;
   a.ldy = ldy;
   a.res = ctx.res;
   a.ldr = ctx.ldr;
@@ -1160,12 +1275,17 @@ cudaError_t launch_umma_multi(const egt_dev_packed* const* hs, int nseg, const f
   const size_t a_bytes = 2 * (sparse_path ? 8192 : 16384), xu_bytes = 2 * x_bytes;
   const size_t fixed = 2048 + kNR * 8 * static_cast<size_t>(a.raw_rt_bytes);
   // split K: the x ring also holds the slice's partials, 128 x (T + 4) f32
-  const int nx_min = p.S > 1 ? static_cast<int>((512 * static_cast<size_t>(p.T + 4) + xu_bytes - 1) / xu_bytes) : 2;
+  // push: the tile (T x 512 B) plus the receive area (S shares of per groups x 2 KB)
+  const size_t g4 = p.T / 4, per = (g4 + p.S - 1) / p.S;
+  const size_t push_bytes = static_cast<size_t>(p.T) * 512 + (p.S > 1 ? p.S * per * 2048 : 0);
+  const size_t pull_bytes = p.S > 1 ? 512 * static_cast<size_t>(p.T + 4) : 0;
   static const int na_env = getenv("EGT_UMMA_NA") ? atoi(getenv("EGT_UMMA_NA")) : 0;
   const long room = static_cast<long>(budget) - static_cast<long>(fixed);
   a.NA = room > 0 ? static_cast<int>(std::min<long>(kMaxNA, room / static_cast<long>(a_bytes + xu_bytes))) : 0;
   if (na_env > 0) a.NA = std::min(a.NA, na_env);
   a.NX = a.NA;  // one ring
+  if (a.push && static_cast<size_t>(a.NX) * xu_bytes < push_bytes) a.push = 0;  // no room: pull
+  const int nx_min = static_cast<int>(((a.push ? push_bytes : pull_bytes) + xu_bytes - 1) / xu_bytes);
   if (a.NA < std::max(2, nx_min)) return cudaErrorInvalidConfiguration;
   const size_t smem = fixed + a.NA * a_bytes + a.NX * xu_bytes;
   err = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
