@@ -49,6 +49,7 @@
 #include <algorithm>
 #include <memory>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 
 #include "device_common.cuh"
@@ -1022,6 +1023,40 @@ struct UmmaPlan {
   size_t smem = 0;
 };
 
+void* pick_umma(int fmt);
+
+// Clusters of S CTAs (one CTA per SM) the GPU runs at once: a cluster's CTAs
+// share a GPC, so S that do not divide a GPC's SM count leave SMs idle (the
+// occupancy API answers for this GPU; cached per S)
+int umma_cluster_capacity(int fmt, int S, int num_sms) {
+  static int cap[3][9] = {};
+  const int f = fmt == I4_SP24 ? 0 : fmt == I4_DENSE ? 1 : 2;
+  if (S < 1 || S > 8) return std::max(1, num_sms / std::max(1, S));
+  if (cap[f][S] == 0) {
+    int n = 0;
+    void* fn = pick_umma(fmt);
+    const int smem = 200 * 1024;
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) == cudaSuccess) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(1, 1, S);
+      cfg.blockDim = dim3(kThreads);
+      cfg.dynamicSmemBytes = smem;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 1;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = S;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      if (cudaOccupancyMaxActiveClusters(&n, fn, &cfg) != cudaSuccess) n = 0;
+    }
+    cudaGetLastError();
+    cap[f][S] = n > 0 ? n : std::max(1, num_sms / S);
+    if (getenv("EGT_PLAN_LOG")) fprintf(stderr, "umma cluster capacity S=%d: %d clusters\n", S, cap[f][S]);
+  }
+  return cap[f][S];
+}
+
 UmmaPlan plan_umma(const egt_dev_packed* h, int M, int num_sms, int nseg = 1) {
   UmmaPlan p;
   const int tiles = (M + kMaxT - 1) / kMaxT;
@@ -1029,23 +1064,24 @@ UmmaPlan plan_umma(const egt_dev_packed* h, int M, int num_sms, int nseg = 1) {
   p.TT = (M + p.T - 1) / p.T;
   const int KQ = h->tiled.KQ;
   const int R = nseg * ((h->tiled.RT + 7) / 8);
-  // cost ~ waves x (k-quads per CTA + a fixed CTA cost in k-quads: ~8 for
-  // the prologue and output tail, ~14 with the cluster's split-K reduction);
-  // fitted to EGT_UMMA_S sweeps of tools/umma_probe.py (7B shapes, M = 80 /
-  // 272: e.g. 4096^2 at M = 272 S = 1 49 us vs S = 3 66 us)
+  // cost ~ waves x (k-quads per CTA + a fixed CTA cost of ~8 k-quads for the
+  // prologue and pipeline fill + ~6 / S for the output tail, which handles a
+  // 1/S share of the tile); fitted to EGT_UMMA_S sweeps of tools/umma_probe.py
+  // with the pushed split-K partials (7B shapes, M = 80 / 130 / 272: e.g.
+  // 11008 x 4096 at M = 80 S = 1 46.3 us vs S = 3 43.8; 4096 x 11008 at M =
+  // 130 S = 1 107 us vs S = 2 66; 4096^2 at M = 272 S = 1 51 us vs S = 2
+  // 55); waves count the clusters the GPU holds at once (S = 3 packs badly:
+  // 4096^2 at M = 272 63 us in three waves).  Clusters of 7-8 slices measured
+  // poorly (4096^2 at M = 80: S = 8 37.7 us vs S = 6 30.7): S <= 6.
   double best = 1e300;
   static const int s_env = getenv("EGT_UMMA_S") ? atoi(getenv("EGT_UMMA_S")) : 0;  // tuning
-  for (int S = 1; S <= std::min(8, KQ); ++S) {  // S CTAs form one cluster (portable size <= 8)
+  for (int S = 1; S <= std::min(s_env > 0 ? 8 : 6, KQ); ++S) {  // S CTAs form one cluster
     if (s_env > 0 && S != std::min(s_env, KQ)) continue;
-    // several token tiles already fill the machine: no split (measured
-    // S = 1 113 us vs S = 3 127 us for 4096 x 11008 at M = 272: the second
-    // wave and the cluster reduction cost more than the shorter K range)
-    if (p.TT > 1 && S > 1 && s_env == 0) continue;
     const int kqc = (KQ + S - 1) / S;
     const int Seff = (KQ + kqc - 1) / kqc;
-    const long long ctas = static_cast<long long>(R) * p.TT * Seff;
-    const double waves = std::ceil(static_cast<double>(ctas) / num_sms);
-    const double cost = waves * (kqc + (Seff > 1 ? 14.0 : 8.0));
+    const long long clusters = static_cast<long long>(R) * p.TT;
+    const double waves = std::ceil(static_cast<double>(clusters) / umma_cluster_capacity(h->format, Seff, num_sms));
+    const double cost = waves * (kqc + 8.0 + 6.0 / Seff);
     if (cost < best - 1e-9) {
       best = cost;
       p.S = Seff;
