@@ -779,13 +779,20 @@ __global__ void __launch_bounds__(kThreads, 1) umma_spmm_kernel(const __grid_con
       // barrier may complete while the sums below run
       if (a.S > 1) asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
       const int nit = max(0, g1 - g0) * 128;
+      // the tile's shared-memory address recomputed here from the window base
+      // (kept from the prologue it was spilled and reloaded from local
+      // memory every item)
+      uint32_t pb;
+      asm volatile("mov.u32 %0, %1;\n" : "=r"(pb) : "r"(((smem_addr(smem_raw) + 1023u) & ~1023u) + 1024u));
+      pb += static_cast<uint32_t>(a.NA) * 2 * kASlot;
+      const uint32_t rb = pb + static_cast<uint32_t>(T) * 512;
       for (int it = (warp - kEpiWarp0) * 32 + lane; it < nit; it += kNumEpi * 32) {
         const int r = it & 127, gq = g0 + (it >> 7), grow = rt0 * 16 + r;
         float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll 1
         for (int z = 0; z < a.S; ++z) {  // slice order (deterministic)
-          const uint32_t ad = z == myz ? pbase + static_cast<uint32_t>((gq * 128 + r) * 16)
-                                       : rbase + static_cast<uint32_t>(((z * per + gq - g0) * 128 + r) * 16);
+          const uint32_t ad = z == myz ? pb + static_cast<uint32_t>((gq * 128 + r) * 16)
+                                       : rb + static_cast<uint32_t>(((z * per + gq - g0) * 128 + r) * 16);
           const uint4 v = lds_v4(ad);
           sum.x += __uint_as_float(v.x);
           sum.y += __uint_as_float(v.y);

@@ -49,6 +49,7 @@ print("epilogue warps: rounds done", [us(v) for v in t[800:808]], "\n  past bar"
       "\n  partials", [us(v) for v in t[840:848]],
       "\n  outputs", [us(v) for v in t[820:828]])
 print("reduce pass starts", us(t[900]), us(t[901]))
+print("tail iterations:", [us(v) for v in t[860:880] if v])
 print("MMA loop cycles per k-quad (waits, MMAs + round commits, slot commits, total):")
 for i in range(8):
     print("  k-quad", 2 + i, [int(v) for v in t[900 + 8 * i:904 + 8 * i]])
