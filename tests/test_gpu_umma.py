@@ -173,3 +173,22 @@ def test_spmm_multi_errors(port):
         spmm_multi([a, b], x, ys[:2])
     with pytest.raises(egt.InvalidArgument, match="none or rmsnorm"):
         spmm_multi([a, a], x, ys[:2], input=N.INPUT_SILU)
+
+
+@pytest.mark.parametrize("M", [130, 272])
+def test_umma_split_k_with_token_tiles(port, M):
+    """Few row blocks, several token tiles: the planner splits K across a
+    cluster per (row block, token tile) and the slices push their partial
+    shares to each other (umma_spmm.cu push path)."""
+    import torch
+
+    rng = np.random.default_rng(M + 11)
+    d, ref = _layer(port, rng, "int4-2:4", 256, 4096)
+    xs = rng.uniform(-1, 1, (M, 4096)).astype(np.float32)
+    res = rng.uniform(-1, 1, (M, 256)).astype(np.float32)
+    y = torch.empty((M, 256), device="cuda")
+    d.spmv_fused_into(torch.from_numpy(xs).cuda(), y, residual=torch.from_numpy(res).cuda())
+    got = y.cpu().numpy()
+    for m in range(M):
+        ok, err = close(got[m], res[m] + ref(xs[m]))
+        assert ok, (M, m, err)
